@@ -1,0 +1,574 @@
+/*
+ * scg_oracle.c -- CPU ORACLE for the SketchyCGAL MaxCut hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_1912_02949_b200/) never imports, links or calls it,
+ * and this file shares no code with the CUDA path; the only common source is
+ * the seeded input stream scg_inputs/include/scg_rng.h (random inputs only).
+ *
+ * Plain, slow, fp64, single-threaded.  Every function follows the paper
+ * (arXiv 1912.02949, /root/reference/PAPER.md, cited as P:<line>) step by step,
+ * in the paper's order and notation, with the readings and the Canonical
+ * Arithmetic Contract (CAC) written down in DESIGN.md section 3.  The CAC
+ * only fixes *how each written operation is rounded* (the paper's Lanczos
+ * method has no reorthogonalization, so any two implementations
+ * that round differently diverge):
+ *   CAC-1  one IEEE fp64 round-to-nearest operation per written +,-,*,/,sqrt;
+ *          fma() only where written (compiled with -ffp-contract=off).
+ *   CAC-2  global sums are EXACT: xsum(p_1..p_N) = RNE(sum_r Q(p_r)), with
+ *          Q(p) = p truncated toward zero to a multiple of 2^-200 (|p| < 2^100).
+ *          dot(a, b) = xsum(fl(a_r * b_r)).
+ *   CAC-3  (D x)_r = d_r x_r + sum_{j in N(r), ascending} m_rj x_j, left to right,
+ *          acc = fl(d_r * x_r); acc = fma(m_rj, x_j, acc).
+ *   CAC-4  Alg. 2 as printed, two-pass, with readings A1-A4.
+ *   CAC-5  tridiagonal min eigenpair by Sturm multisection + inverse iteration.
+ *   CAC-6  scalar schedules evaluated as written in DESIGN.md.
+ *
+ * Parity pins: tests/test_oracle_*.py (closed forms, dense eigensolvers,
+ * math.fsum, loop invariants, brute-force cuts).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "../scg_inputs/include/scg_rng.h"
+
+/* ------------------------------------------------------------------------- */
+/* CAC-2: exact summation.  Big integer in base 2^32, value = sum d[i] 2^(32 i - 200). */
+#define XS_LIMBS 12
+#define XS_LSB_EXP (-200)
+
+typedef struct {
+  int64_t d[XS_LIMBS];
+  int64_t adds;
+  int err; /* 1: |p| >= 2^100 or non-finite summand */
+} xsum_t;
+
+static void xs_init(xsum_t *a) { memset(a, 0, sizeof(*a)); }
+
+static void xs_carry(xsum_t *a) {
+  for (int i = 0; i < XS_LIMBS - 1; ++i) {
+    int64_t c = a->d[i] >> 32; /* floor division by 2^32 */
+    a->d[i] -= c * ((int64_t)1 << 32);
+    a->d[i + 1] += c;
+  }
+}
+
+static void xs_add(xsum_t *a, double p) {
+  if (p == 0.0) return;
+  if (!isfinite(p) || fabs(p) >= 0x1p100) { a->err = 1; return; }
+  union { double f; uint64_t u; } b;
+  b.f = p;
+  int neg = (int)(b.u >> 63);
+  int e = (int)((b.u >> 52) & 0x7ff);
+  uint64_t m = b.u & 0x000fffffffffffffull;
+  if (e == 0) e = 1; else m |= 0x0010000000000000ull;
+  /* p = m * 2^(e - 1075);  shift relative to 2^-200 */
+  int s = e - 1075 - XS_LSB_EXP;
+  if (s < 0) { m = (-s >= 64) ? 0 : (m >> (-s)); s = 0; } /* Q: truncate toward zero */
+  if (m == 0) return;
+  int q = s / 32, r = s % 32;
+  unsigned __int128 x = (unsigned __int128)m << r;
+  int64_t d0 = (int64_t)(uint64_t)(x & 0xffffffffu);
+  int64_t d1 = (int64_t)(uint64_t)((x >> 32) & 0xffffffffu);
+  int64_t d2 = (int64_t)(uint64_t)((x >> 64) & 0xffffffffu);
+  if (neg) { a->d[q] -= d0; a->d[q + 1] -= d1; a->d[q + 2] -= d2; }
+  else { a->d[q] += d0; a->d[q + 1] += d1; a->d[q + 2] += d2; }
+  if (++a->adds >= (1 << 20)) { xs_carry(a); a->adds = 0; }
+}
+
+/* Round the exact sum to the nearest double (ties to even). */
+static double xs_round(xsum_t *a) {
+  xs_carry(a);
+  uint32_t mag[XS_LIMBS];
+  int neg = a->d[XS_LIMBS - 1] < 0;
+  if (neg) { /* magnitude of a negative number: two's complement across digits */
+    int64_t borrow = 0;
+    for (int i = 0; i < XS_LIMBS; ++i) {
+      int64_t v = -a->d[i] - borrow;
+      borrow = 0;
+      while (v < 0) { v += ((int64_t)1 << 32); borrow += 1; }
+      mag[i] = (uint32_t)v;
+    }
+  } else {
+    for (int i = 0; i < XS_LIMBS; ++i) mag[i] = (uint32_t)a->d[i];
+  }
+  int top = -1;
+  for (int i = XS_LIMBS - 1; i >= 0; --i) if (mag[i]) { top = i; break; }
+  if (top < 0) return 0.0;
+  int hb = 31;
+  while (!((mag[top] >> hb) & 1u)) --hb;
+  int B = top * 32 + hb; /* index of the highest set bit */
+  /* gather bits [B-63, B] into M64, sticky = any set bit below B-63 */
+  uint64_t M64 = 0;
+  int sticky = 0;
+  for (int bit = B; bit >= 0; --bit) {
+    int v = (mag[bit / 32] >> (bit % 32)) & 1u;
+    if (B - bit < 64) M64 = (M64 << 1) | (uint64_t)v;
+    else if (v) { sticky = 1; break; }
+  }
+  int nbits = B + 1 < 64 ? B + 1 : 64; /* bits collected */
+  double res;
+  if (nbits <= 53) {
+    res = ldexp((double)M64, XS_LSB_EXP);
+  } else {
+    int drop = nbits - 53;
+    uint64_t keep = M64 >> drop;
+    uint64_t rem = M64 & (((uint64_t)1 << drop) - 1); /* drop <= 11 */
+    uint64_t half = (uint64_t)1 << (drop - 1);
+    int round_up;
+    if (rem > half) round_up = 1;
+    else if (rem < half) round_up = 0;
+    else round_up = sticky ? 1 : (int)(keep & 1u); /* tie: to even */
+    keep += (uint64_t)round_up;
+    /* value = keep * 2^(B - 52 + XS_LSB_EXP) */
+    res = ldexp((double)keep, B - 52 + XS_LSB_EXP);
+  }
+  return neg ? -res : res;
+}
+
+/* CAC-2 dot product. */
+static double o_dot(const double *a, const double *b, int64_t n, int *err) {
+  xsum_t s;
+  xs_init(&s);
+  for (int64_t r = 0; r < n; ++r) xs_add(&s, a[r] * b[r]);
+  if (s.err && err) *err = 1;
+  return xs_round(&s);
+}
+
+double oracle_xsum(const double *p, int64_t n, int *err) {
+  xsum_t s;
+  xs_init(&s);
+  for (int64_t r = 0; r < n; ++r) xs_add(&s, p[r]);
+  if (err) *err = s.err;
+  return xs_round(&s);
+}
+
+double oracle_dot(const double *a, const double *b, int64_t n) { return o_dot(a, b, n, NULL); }
+
+/* ------------------------------------------------------------------------- */
+/* CAC-3: D = offdiag(m) + diag(d), rows ascending.  Primitive 1 + 2 of
+ * eqn:primitives, MaxCut instance P:609-614. */
+typedef struct {
+  int64_t n;
+  const int64_t *rp;   /* off-diagonal CSR */
+  const int32_t *col;
+  const double *m;     /* off-diagonal values of C (or of M) */
+} o_off;
+
+static void o_apply(const o_off *A, const double *d, const double *x, double *y) {
+  for (int64_t r = 0; r < A->n; ++r) {
+    double acc = d[r] * x[r];
+    for (int64_t k = A->rp[r]; k < A->rp[r + 1]; ++k) acc = fma(A->m[k], x[A->col[k]], acc);
+    y[r] = acc;
+  }
+}
+
+void oracle_apply(int64_t n, const int64_t *rp, const int32_t *col, const double *m, const double *d,
+                  const double *x, double *y) {
+  o_off A = {n, rp, col, m};
+  o_apply(&A, d, x, y);
+}
+
+/* ------------------------------------------------------------------------- */
+/* CAC-5: minimum eigenpair of T = tridiag(rho_{1:k-1}, omega_{1:k}, rho_{1:k-1})
+ * (Alg. 2 lines 11-12; "exploit tridiagonal form").  Sturm count =
+ * number of sign changes of the characteristic-polynomial sequence. */
+static int o_sturm(const double *om, const double *rho2, int k, double x) {
+  double pprev = 1.0, p = om[0] - x;
+  int sprev = 1;
+  int s = p > 0.0 ? 1 : (p < 0.0 ? -1 : -sprev);
+  int cnt = (s != sprev);
+  for (int j = 1; j < k; ++j) {
+    double pn = fma(om[j] - x, p, -(rho2[j - 1] * pprev));
+    int sn = pn > 0.0 ? 1 : (pn < 0.0 ? -1 : -s);
+    cnt += (sn != s);
+    pprev = p; p = pn; s = sn;
+    double ap = fabs(p), aq = fabs(pprev);
+    if (ap > 0x1p500) { p *= 0x1p-500; pprev *= 0x1p-500; }
+    else if (ap < 0x1p-500 && aq < 0x1p-500) { p *= 0x1p500; pprev *= 0x1p500; }
+  }
+  return cnt;
+}
+
+static double o_pow2_of(double a) { /* 2^floor(log2 a) for normal a > 0 (exact) */
+  union { double f; uint64_t u; } b;
+  b.f = a;
+  b.u &= 0x7ff0000000000000ull;
+  return b.f;
+}
+
+int oracle_tridiag_mineig(const double *om, const double *rho, int k, double *theta, double *s) {
+  if (k <= 0) return -1;
+  if (k == 1) { *theta = om[0]; s[0] = 1.0; return 0; }
+  double rho2[128];
+  double lo = 0.0, hi = 0.0, NT = 0.0;
+  for (int j = 0; j < k - 1; ++j) rho2[j] = rho[j] * rho[j];
+  for (int j = 0; j < k; ++j) {
+    double rl = j > 0 ? rho[j - 1] : 0.0;
+    double rr = j < k - 1 ? rho[j] : 0.0;
+    double rj = rl + rr;
+    double a = om[j] - rj, b = om[j] + rj;
+    if (j == 0 || a < lo) lo = a;
+    if (j == 0 || b > hi) hi = b;
+  }
+  NT = fabs(lo) > fabs(hi) ? fabs(lo) : fabs(hi);
+  if (NT == 0.0) { *theta = 0.0; for (int j = 0; j < k; ++j) s[j] = j == 0 ? 1.0 : 0.0; return 0; }
+  double pad = NT * 0x1p-20;
+  lo = lo - pad;
+  hi = hi + pad;
+  /* 12 rounds of 32-point multisection: keep count(lo) = 0, count(hi) >= 1 */
+  for (int round = 0; round < 12; ++round) {
+    double h = (hi - lo) / 33.0;
+    double prev = lo;
+    double nlo = lo, nhi = hi;
+    int found = 0;
+    for (int j = 1; j <= 32; ++j) {
+      double x = fma((double)j, h, lo);
+      if (o_sturm(om, rho2, k, x) >= 1) { nlo = prev; nhi = x; found = 1; break; }
+      prev = x;
+    }
+    if (!found) nlo = prev;
+    lo = nlo; hi = nhi;
+  }
+  double th = (lo + hi) * 0.5;
+  *theta = th;
+  /* inverse iteration: Gaussian elimination with partial pivoting of T - theta I
+   * (rows swapped when the sub-diagonal entry is larger), U has three diagonals. */
+  double u0[128], u1[128], u2[128], mul[128], x[128];
+  int swp[128];
+  double tiny = NT * 0x1p-60;
+  double c0 = om[0] - th, c1 = k > 1 ? rho[0] : 0.0, c2 = 0.0;
+  for (int i = 0; i < k - 1; ++i) {
+    double nb = rho[i], na = om[i + 1] - th, nc = (i + 1 < k - 1) ? rho[i + 1] : 0.0;
+    if (fabs(c0) >= fabs(nb)) {
+      double m = c0 != 0.0 ? nb / c0 : 0.0;
+      u0[i] = c0; u1[i] = c1; u2[i] = c2; swp[i] = 0; mul[i] = m;
+      c0 = na - m * c1; c1 = nc - m * c2; c2 = 0.0;
+    } else {
+      double m = c0 / nb;
+      u0[i] = nb; u1[i] = na; u2[i] = nc; swp[i] = 1; mul[i] = m;
+      double t0 = c1 - m * na, t1 = c2 - m * nc;
+      c0 = t0; c1 = t1; c2 = 0.0;
+    }
+  }
+  u0[k - 1] = c0; u1[k - 1] = 0.0; u2[k - 1] = 0.0;
+  for (int i = 0; i < k; ++i)
+    if (fabs(u0[i]) < tiny) u0[i] = u0[i] < 0.0 ? -tiny : tiny;
+  for (int j = 0; j < k; ++j) s[j] = (double)(j % 5 + 1) * 0.25;
+  for (int it = 0; it < 3; ++it) {
+    for (int j = 0; j < k; ++j) x[j] = s[j];
+    for (int i = 0; i < k - 1; ++i) {
+      if (swp[i]) { double t = x[i]; x[i] = x[i + 1]; x[i + 1] = t; }
+      x[i + 1] = fma(-mul[i], x[i], x[i + 1]);
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double t = x[i];
+      if (i + 1 < k) t = fma(-u1[i], x[i + 1], t);
+      if (i + 2 < k) t = fma(-u2[i], x[i + 2], t);
+      x[i] = t / u0[i];
+    }
+    double mx = 0.0;
+    for (int j = 0; j < k; ++j) if (fabs(x[j]) > mx) mx = fabs(x[j]);
+    double sc = 1.0 / o_pow2_of(mx); /* exact power of two */
+    for (int j = 0; j < k; ++j) s[j] = x[j] * sc;
+  }
+  int jm = 0;
+  for (int j = 1; j < k; ++j) if (fabs(s[j]) > fabs(s[jm])) jm = j;
+  if (s[jm] < 0.0) for (int j = 0; j < k; ++j) s[j] = -s[j];
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Alg. 2 ApproxMinEvec, two passes.
+ * g: the randn start vector of line 1; q: the iteration bound (callers pass
+ * min{q_t, n-1}, line 3).  Outputs theta (xi of line 12 = Ritz value), v (line
+ * 13, explicitly normalized: reading A6), k, omega[k], rho[k-1]. */
+typedef struct {
+  double theta;
+  int k;
+  int err;
+  double omega[128];
+  double rho[128];
+  double svec[128];
+} o_lanczos_res;
+
+static void o_lanczos(const o_off *A, const double *d, const double *g, int q, double *v,
+                      double *w1, double *w2, double *w3, double *a, o_lanczos_res *res) {
+  int64_t n = A->n;
+  int err = 0;
+  double *vprev = w1, *vcur = w2, *vnext = w3;
+  /* lines 1-2: v1 = randn / ||randn|| */
+  double nu0 = sqrt(o_dot(g, g, n, &err));
+  for (int64_t r = 0; r < n; ++r) vcur[r] = g[r] / nu0;
+  int k = q;
+  for (int i = 1; i <= q; ++i) {
+    o_apply(A, d, vcur, a);                            /* M v_i */
+    res->omega[i - 1] = o_dot(vcur, a, n, &err);       /* line 5 */
+    if (i == q) { k = q; break; }                       /* reading A2: last step needs no v_{i+1} */
+    double om = res->omega[i - 1];
+    double rp = i >= 2 ? res->rho[i - 2] : 0.0;
+    for (int64_t r = 0; r < n; ++r) {                   /* line 6: three-term recurrence */
+      double w = fma(-om, vcur[r], a[r]);
+      if (i >= 2) w = fma(-rp, vprev[r], w);
+      vnext[r] = w;
+    }
+    double rho = sqrt(o_dot(vnext, vnext, n, &err));    /* line 7 (reading A1) */
+    res->rho[i - 1] = rho;
+    if (rho <= 0x1p-45 * (fabs(om) + rp)) { k = i; break; } /* line 8 (reading A3) */
+    for (int64_t r = 0; r < n; ++r) vnext[r] = vnext[r] / rho; /* line 9 */
+    double *t = vprev; vprev = vcur; vcur = vnext; vnext = t;
+  }
+  res->k = k;
+  /* lines 11-12 */
+  oracle_tridiag_mineig(res->omega, res->rho, k, &res->theta, res->svec);
+  /* line 13, regenerating v_2..v_k (second pass) */
+  vprev = w1; vcur = w2; vnext = w3;
+  for (int64_t r = 0; r < n; ++r) vcur[r] = g[r] / nu0;
+  for (int64_t r = 0; r < n; ++r) v[r] = res->svec[0] * vcur[r];
+  for (int i = 1; i < k; ++i) {
+    o_apply(A, d, vcur, a);
+    double om = res->omega[i - 1];
+    double rp = i >= 2 ? res->rho[i - 2] : 0.0;
+    double rho = res->rho[i - 1];
+    for (int64_t r = 0; r < n; ++r) {
+      double w = fma(-om, vcur[r], a[r]);
+      if (i >= 2) w = fma(-rp, vprev[r], w);
+      vnext[r] = w / rho;
+    }
+    for (int64_t r = 0; r < n; ++r) v[r] = fma(res->svec[i], vnext[r], v[r]);
+    double *t = vprev; vprev = vcur; vcur = vnext; vnext = t;
+  }
+  double nx = sqrt(o_dot(v, v, n, &err));
+  for (int64_t r = 0; r < n; ++r) v[r] = v[r] / nx;
+  res->err = err;
+}
+
+/* Standalone Alg. 2 on a general symmetric matrix (tests): offdiag CSR + diagonal d. */
+int oracle_lanczos(int64_t n, const int64_t *rp, const int32_t *col, const double *m, const double *d,
+                   const double *g, int q, double *v, double *theta, int *k, double *omega, double *rho,
+                   double *svec) {
+  if (q < 1 || q > 127) return -1;
+  o_off A = {n, rp, col, m};
+  double *buf = (double *)malloc(sizeof(double) * (size_t)n * 4);
+  o_lanczos_res res;
+  memset(&res, 0, sizeof(res));
+  o_lanczos(&A, d, g, q, v, buf, buf + n, buf + 2 * n, buf + 3 * n, &res);
+  free(buf);
+  *theta = res.theta;
+  *k = res.k;
+  for (int j = 0; j < res.k; ++j) { omega[j] = res.omega[j]; svec[j] = res.svec[j]; }
+  for (int j = 0; j + 1 < res.k; ++j) rho[j] = res.rho[j];
+  return res.err ? -2 : 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* CAC-6 schedules (Alg. 4 lines 5-6). */
+int oracle_qt(int64_t t, int64_t n) {
+  double lnN = log((double)n);
+  double x = sqrt(sqrt((double)t)) * lnN;
+  int64_t q = (int64_t)ceil(x);
+  if (q < 2) q = 2;
+  if (q > n - 1) q = n - 1;
+  if (q > 127) q = 127;
+  return (int)q;
+}
+
+/* Dual step size, eqn:sketchy-cgal-dual-step, ||A|| = 1 for diag. */
+double oracle_gamma(int64_t t, double alpha, double beta0, double nz) {
+  if (nz == 0.0) return beta0;
+  double sq = sqrt((double)(t + 1));
+  double num = 4.0 * alpha;
+  num = num * alpha;
+  num = num * beta0;
+  double den = ((double)(t + 1) * sq) * nz;
+  double g = num / den;
+  return g < beta0 ? g : beta0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Alg. 4 SketchyCGAL for the MaxCut SDP. */
+typedef struct {
+  int64_t n;
+  int32_t R;
+  double alpha_orig, alpha, beta0, bval, nrmL;
+  int scale;
+  uint64_t seed;
+  int qfix; /* test-only: fixed Lanczos bound (may be n); 0 = schedule */
+  int64_t t; /* iterations done */
+  /* off-diagonal part of C and its diagonal (scaled) */
+  int64_t *rp;
+  int32_t *col;
+  double *m;
+  double *cdiag;
+  double *z, *y, *S, *Omega, *v, *g, *d;
+  double *w1, *w2, *w3, *a, *cv;
+  double p, tau;
+  int err;
+  /* per-iteration log */
+  int64_t logcap;
+  double *log; /* 10 per iteration: t q k theta xi c p znorm gamma tau */
+  double *vhist; /* optional: T x n */
+  int64_t vhist_cap;
+} oracle_t;
+
+void *oracle_create(int64_t n, const int64_t *rp_L, const int32_t *col_L, const double *val_L, int32_t R,
+                    double alpha, double beta0, uint64_t seed, int scale, int qfix, int64_t logcap,
+                    int64_t vhist_cap) {
+  oracle_t *o = (oracle_t *)calloc(1, sizeof(oracle_t));
+  o->n = n; o->R = R; o->beta0 = beta0; o->seed = seed; o->scale = scale; o->qfix = qfix;
+  o->alpha_orig = alpha;
+  /* ||C||_F = ||L||_F over all stored entries (CAC-2), scaling P:1805-1814 (reading A13) */
+  int err = 0;
+  {
+    xsum_t s;
+    xs_init(&s);
+    for (int64_t k = 0; k < rp_L[n]; ++k) xs_add(&s, val_L[k] * val_L[k]);
+    err |= s.err;
+    o->nrmL = sqrt(xs_round(&s));
+  }
+  if (scale) { o->alpha = 1.0; o->bval = 1.0 / (double)n; }
+  else { o->alpha = alpha; o->bval = 1.0; }
+  /* split L into off-diagonal C entries and diagonal: C = -L, scaled C / ||C||_F */
+  int64_t nnz_off = 0;
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t k = rp_L[r]; k < rp_L[r + 1]; ++k) if (col_L[k] != r) nnz_off++;
+  o->rp = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  o->col = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nnz_off ? nnz_off : 1));
+  o->m = (double *)malloc(sizeof(double) * (size_t)(nnz_off ? nnz_off : 1));
+  o->cdiag = (double *)calloc((size_t)n, sizeof(double));
+  int64_t o_k = 0;
+  o->rp[0] = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    for (int64_t k = rp_L[r]; k < rp_L[r + 1]; ++k) {
+      double c = -val_L[k];
+      if (scale) c = c / o->nrmL;
+      if (col_L[k] == r) o->cdiag[r] = c;
+      else { o->col[o_k] = col_L[k]; o->m[o_k] = c; o_k++; }
+    }
+    o->rp[r + 1] = o_k;
+  }
+  o->z = (double *)calloc((size_t)n, sizeof(double));
+  o->y = (double *)calloc((size_t)n, sizeof(double));
+  o->d = (double *)calloc((size_t)n, sizeof(double));
+  o->v = (double *)calloc((size_t)n, sizeof(double));
+  o->g = (double *)calloc((size_t)n, sizeof(double));
+  o->w1 = (double *)calloc((size_t)n, sizeof(double));
+  o->w2 = (double *)calloc((size_t)n, sizeof(double));
+  o->w3 = (double *)calloc((size_t)n, sizeof(double));
+  o->a = (double *)calloc((size_t)n, sizeof(double));
+  o->cv = (double *)calloc((size_t)n, sizeof(double));
+  o->S = (double *)calloc((size_t)n * R, sizeof(double));
+  o->Omega = (double *)malloc(sizeof(double) * (size_t)n * R);
+  /* NystromSketch.Init (Alg. 3 line 2): Omega column-major, reading A8 */
+  for (int32_t kk = 0; kk < R; ++kk)
+    for (int64_t i = 0; i < n; ++i) o->Omega[(int64_t)kk * n + i] = scg_omega(seed, i, kk);
+  o->logcap = logcap;
+  o->log = (double *)calloc((size_t)(logcap > 0 ? logcap : 1) * 10, sizeof(double));
+  o->vhist_cap = vhist_cap;
+  o->vhist = vhist_cap > 0 ? (double *)calloc((size_t)vhist_cap * n, sizeof(double)) : NULL;
+  o->err = err;
+  return o;
+}
+
+void oracle_destroy(void *h) {
+  oracle_t *o = (oracle_t *)h;
+  if (!o) return;
+  free(o->rp); free(o->col); free(o->m); free(o->cdiag);
+  free(o->z); free(o->y); free(o->d); free(o->v); free(o->g);
+  free(o->w1); free(o->w2); free(o->w3); free(o->a); free(o->cv);
+  free(o->S); free(o->Omega); free(o->log); free(o->vhist);
+  free(o);
+}
+
+int oracle_step(void *h, int64_t T) {
+  oracle_t *o = (oracle_t *)h;
+  int64_t n = o->n;
+  o_off A = {n, o->rp, o->col, o->m};
+  int R = o->R;
+  for (int64_t it = 0; it < T; ++it) {
+    int64_t t = o->t + 1;
+    /* line 5: beta = beta0 sqrt(t+1), eta = 2/(t+1) */
+    double sq = sqrt((double)(t + 1));
+    double beta = o->beta0 * sq;
+    double eta = 2.0 / (double)(t + 1);
+    int q = o->qfix > 0 ? o->qfix : oracle_qt(t, n);
+    if (o->qfix <= 0 && q > n - 1) q = (int)(n - 1);
+    /* line 6: D = C + A*(y + beta (z - b)) ; diagonal of D (primitive 2) */
+    for (int64_t r = 0; r < n; ++r) o->d[r] = fma(beta, o->z[r] - o->bval, o->y[r]) + o->cdiag[r];
+    for (int64_t r = 0; r < n; ++r) o->g[r] = scg_lanczos_start(o->seed, t, r);
+    o_lanczos_res res;
+    memset(&res, 0, sizeof(res));
+    o_lanczos(&A, o->d, o->g, q, o->v, o->w1, o->w2, o->w3, o->a, &res);
+    o->err |= res.err;
+    /* monitors: xi = v* D v (eqn 5.1), c = v* C v (p update) */
+    int err = 0;
+    o_apply(&A, o->d, o->v, o->a);
+    double xi = o_dot(o->v, o->a, n, &err);
+    o_apply(&A, o->cdiag, o->v, o->cv);
+    double cval = o_dot(o->v, o->cv, n, &err);
+    double one_m_eta = 1.0 - eta;
+    /* line 7: z <- (1 - eta) z + eta A(alpha v v*)  (primitive 3) */
+    for (int64_t r = 0; r < n; ++r) {
+      double h = o->alpha * (o->v[r] * o->v[r]);
+      o->z[r] = fma(eta, h, one_m_eta * o->z[r]);
+    }
+    /* line 8: gamma from ||z - b||^2, y <- y + gamma (z - b) */
+    for (int64_t r = 0; r < n; ++r) o->a[r] = o->z[r] - o->bval;
+    double nz = o_dot(o->a, o->a, n, &err);
+    double gamma = oracle_gamma(t, o->alpha, o->beta0, nz);
+    for (int64_t r = 0; r < n; ++r) o->y[r] = fma(gamma, o->a[r], o->y[r]);
+    /* line 9: NystromSketch.RankOneUpdate(sqrt(alpha) v, eta): S <- (1-eta) S + eta alpha v (v* Omega) */
+    for (int kk = 0; kk < R; ++kk) {
+      double gk = o_dot(o->v, o->Omega + (int64_t)kk * n, n, &err);
+      double c = (eta * o->alpha) * gk;
+      double *Sk = o->S + (int64_t)kk * n;
+      for (int64_t r = 0; r < n; ++r) Sk[r] = fma(c, o->v[r], one_m_eta * Sk[r]);
+    }
+    /* tau, p */
+    double vv = o_dot(o->v, o->v, n, &err);
+    o->tau = fma(eta * o->alpha, vv, one_m_eta * o->tau);
+    o->p = fma(eta * o->alpha, cval, one_m_eta * o->p);
+    o->err |= err;
+    if (t - 1 < o->logcap) {
+      double *L = o->log + (t - 1) * 10;
+      L[0] = (double)t; L[1] = (double)q; L[2] = (double)res.k; L[3] = res.theta; L[4] = xi;
+      L[5] = cval; L[6] = o->p; L[7] = sqrt(nz); L[8] = gamma; L[9] = o->tau;
+    }
+    if (o->vhist && t - 1 < o->vhist_cap) memcpy(o->vhist + (t - 1) * n, o->v, sizeof(double) * (size_t)n);
+    o->t = t;
+  }
+  return o->err ? -2 : 0;
+}
+
+/* getters */
+int64_t oracle_t_done(void *h) { return ((oracle_t *)h)->t; }
+double oracle_scalar(void *h, int which) {
+  oracle_t *o = (oracle_t *)h;
+  switch (which) {
+    case 0: return o->p;
+    case 1: return o->tau;
+    case 2: return o->nrmL;
+    case 3: return o->alpha;
+    case 4: return o->bval;
+    default: return NAN;
+  }
+}
+void oracle_get(void *h, int which, double *out) {
+  oracle_t *o = (oracle_t *)h;
+  int64_t n = o->n;
+  switch (which) {
+    case 0: memcpy(out, o->z, sizeof(double) * (size_t)n); break;
+    case 1: memcpy(out, o->y, sizeof(double) * (size_t)n); break;
+    case 2: memcpy(out, o->S, sizeof(double) * (size_t)n * o->R); break;
+    case 3: memcpy(out, o->Omega, sizeof(double) * (size_t)n * o->R); break;
+    case 4: memcpy(out, o->v, sizeof(double) * (size_t)n); break;
+    case 5: memcpy(out, o->log, sizeof(double) * (size_t)o->logcap * 10); break;
+    case 6: if (o->vhist) memcpy(out, o->vhist, sizeof(double) * (size_t)o->vhist_cap * n); break;
+    case 7: memcpy(out, o->cdiag, sizeof(double) * (size_t)n); break;
+    case 8: memcpy(out, o->d, sizeof(double) * (size_t)n); break;
+    default: break;
+  }
+}

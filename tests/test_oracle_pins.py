@@ -1,0 +1,432 @@
+"""Pins of the CPU oracle against things other than itself.
+
+Each test names the paper passage (P:<line> of PAPER.md) or SPEC.md worked
+example (S:<line>) it checks, and the independent reference it uses: closed
+forms, numpy/scipy dense eigensolvers, math.fsum / fractions, the dense
+shadow CGAL iteration (Alg. 1), brute-force cut enumeration.
+"""
+import itertools
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+import oracle
+import scg_inputs as si
+
+
+# ------------------------------------------------------------- CAC-2 exact sums
+def test_xsum_equals_fsum_random_and_cancellation():
+    rng = np.random.default_rng(0)
+    for trial in range(50):
+        n = int(rng.integers(1, 3000))
+        scale = 10.0 ** rng.uniform(-30, 20, size=n)
+        p = rng.standard_normal(n) * scale
+        if trial % 3 == 0:  # heavy cancellation
+            p = np.concatenate([p, -p[: n // 2], [1e-3]])
+        assert oracle.xsum(p) == math.fsum(p)
+
+
+def test_xsum_exact_cases():
+    assert oracle.xsum([1e16, 1.0, -1e16]) == 1.0
+    assert oracle.xsum([2.0 ** 53, 1.0, 1.0]) == 2.0 ** 53 + 2.0  # exact then one rounding
+    assert oracle.xsum([2.0 ** 53, 1.0]) == 2.0 ** 53  # tie -> even
+    assert oracle.xsum([2.0 ** 53 + 2.0, 1.0]) == 2.0 ** 53 + 4.0  # tie -> even (up)
+    assert oracle.xsum([]) == 0.0
+    # Q: truncation toward zero at 2^-200
+    assert oracle.xsum([2.0 ** -210]) == 0.0
+    assert oracle.xsum([-(2.0 ** -199 + 2.0 ** -230)]) == -(2.0 ** -199)
+    x = 1.0 + 2.0 ** -52
+    assert oracle.xsum([x * 2.0 ** -148]) == x * 2.0 ** -148  # last mantissa bit exactly 2^-200: kept
+    assert oracle.xsum([x * 2.0 ** -149]) == 2.0 ** -149      # last bit 2^-201: truncated by Q
+    with pytest.raises(OverflowError):
+        oracle.xsum([2.0 ** 101])
+
+
+def test_dot_is_exact_sum_of_rounded_products():
+    rng = np.random.default_rng(1)
+    a, b = rng.standard_normal(1000), rng.standard_normal(1000)
+    assert oracle.dot(a, b) == math.fsum(a * b)
+    exact = sum(Fraction(x) for x in a * b)
+    assert abs(Fraction(oracle.dot(a, b)) - exact) <= Fraction(abs(float(exact))) * Fraction(2) ** -53
+
+
+# ------------------------------------------------------------- CAC-3 row chains
+def test_apply_integer_inputs_exact():
+    # Small integers: every fma is exact, so the chain equals the dense product exactly.
+    rng = np.random.default_rng(2)
+    n = 40
+    M = rng.integers(-5, 6, size=(n, n)).astype(float)
+    M = M + M.T
+    M[rng.random((n, n)) < 0.6] = 0.0
+    M = np.triu(M, 1) + np.triu(M, 1).T + np.diag(np.diag(M))
+    rp, col, m, d = oracle.offdiag_of_dense(M)
+    x = rng.integers(-7, 8, size=n).astype(float)
+    assert np.array_equal(oracle.apply(n, rp, col, m, d, x), M @ x)
+
+
+def test_apply_rounding_bound():
+    rng = np.random.default_rng(3)
+    n = 30
+    M = rng.standard_normal((n, n))
+    M = M + M.T
+    rp, col, m, d = oracle.offdiag_of_dense(M)
+    x = rng.standard_normal(n)
+    y = oracle.apply(n, rp, col, m, d, x)
+    for r in range(n):
+        exact = sum(Fraction(M[r, c]) * Fraction(x[c]) for c in range(n))
+        bound = n * 2.0 ** -53 * float(np.sum(np.abs(M[r] * x))) * 1.01
+        assert abs(float(Fraction(y[r]) - exact)) <= bound
+
+
+# ------------------------------------------------------------- Laplacian
+def test_laplacian_identities():
+    L = si.laplacian("c0")
+    Ld = L.dense()
+    assert np.allclose(Ld @ np.ones(L.n), 0.0)
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal(L.n)
+    assert math.isclose(x @ Ld @ x, oracle.laplacian_quadratic(L, x), rel_tol=1e-12)
+    # single edge and triangle (SPEC S:431-432 examples)
+    L1 = si.laplacian_from_edges(2, [0], [1], [1.0])
+    assert np.array_equal(L1.dense(), np.array([[1.0, -1.0], [-1.0, 1.0]]))
+    L3 = si.laplacian_from_edges(3, [0, 0, 1], [1, 2, 2], [1.0, 1.0, 1.0])
+    assert np.array_equal(L3.dense(), 3 * np.eye(3) - np.ones((3, 3)))
+
+
+# ------------------------------------------------------------- schedules
+def test_qt_schedule_examples():
+    assert oracle.qt(1, 100) == 5
+    assert oracle.qt(16, 100) == 10
+    assert oracle.qt(7, 3) == 2     # S:144 (clip to n - 1)
+    # config[0] / config[3] ranges quoted in SURVEY.md section 8
+    assert oracle.qt(1, 800) == 7 and oracle.qt(1000, 800) == 38
+    assert oracle.qt(1, 1 << 24) == 17 and oracle.qt(1000, 1 << 24) == 94
+
+
+def test_gamma_examples():
+    # eqn:sketchy-cgal-dual-step
+    assert oracle.gamma(1, 1.0, 1.0, 1.0) == 1.0
+    assert oracle.gamma(3, 1.0, 1.0, 2.0) == 0.25
+    assert oracle.gamma(5, 1.0, 1.0, 0.0) == 1.0
+    for t in (1, 10, 100):
+        for nz in (1e-8, 1e-3, 1.0, 1e3):
+            g = oracle.gamma(t, 1.0, 1.0, nz)
+            assert 0.0 <= g <= 1.0
+            assert g * nz <= 4.0 / (t + 1) ** 1.5 * (1 + 1e-15)
+
+
+# ------------------------------------------------------------- tridiagonal (Alg. 2 lines 11-12)
+def test_tridiag_worked_examples():
+    th, s = oracle.tridiag_mineig([2.0], [])
+    assert th == 2.0 and s[0] == 1.0
+    th, s = oracle.tridiag_mineig([0.0, 0.0], [1.0])
+    assert abs(th + 1.0) < 1e-15
+    s = s / np.linalg.norm(s)
+    assert np.allclose(np.abs(s), [2 ** -0.5, 2 ** -0.5], atol=1e-15) and s[0] * s[1] < 0
+    th, s = oracle.tridiag_mineig([1.0, 2.0, 3.0], [0.0, 0.0])  # S:135 decoupled
+    assert abs(th - 1.0) < 1e-15
+    assert np.allclose(s / np.linalg.norm(s), [1.0, 0.0, 0.0], atol=1e-12)
+
+
+def test_tridiag_toeplitz_closed_form():
+    for k in (3, 10, 50, 94):
+        a, b = 0.3, 0.7
+        th, s = oracle.tridiag_mineig(np.full(k, a), np.full(k - 1, b))
+        lam = a - 2 * b * math.cos(math.pi / (k + 1))
+        assert abs(th - lam) <= 1e-14 * (abs(a) + 2 * b)
+        j = np.arange(1, k + 1)
+        ref = np.sin(j * k * math.pi / (k + 1))  # eigenvector of the smallest eigenvalue
+        s = s / np.linalg.norm(s)
+        ref = ref / np.linalg.norm(ref)
+        assert min(np.linalg.norm(s - ref), np.linalg.norm(s + ref)) < 1e-10
+
+
+def test_tridiag_vs_lapack():
+    rng = np.random.default_rng(5)
+    for trial in range(200):
+        k = int(rng.integers(2, 95))
+        om = rng.standard_normal(k) * 10 ** rng.uniform(-3, 3)
+        rho = np.abs(rng.standard_normal(k - 1)) * 10 ** rng.uniform(-3, 3)
+        th, s = oracle.tridiag_mineig(om, rho)
+        w, V = sla.eigh_tridiagonal(om, rho)
+        NT = max(np.abs(om).max() + 2 * rho.max(), 1e-300)
+        assert abs(th - w[0]) <= 1e-12 * NT
+        T = np.diag(om) + np.diag(rho, 1) + np.diag(rho, -1)
+        sn = s / np.linalg.norm(s)
+        assert np.linalg.norm(T @ sn - w[0] * sn) <= 1e-9 * NT
+        jm = int(np.argmax(np.abs(s)))
+        assert s[jm] > 0  # sign convention
+
+
+# ------------------------------------------------------------- Lanczos (Alg. 2)
+def _rand_sym(n, rng):
+    A = rng.standard_normal((n, n))
+    return (A + A.T) / 2
+
+
+def test_lanczos_full_krylov_is_exact():
+    # test-only q = n (reading A4): the Krylov space is everything -> theta = lambda_min
+    rng = np.random.default_rng(6)
+    for n in (3, 5, 8, 12):
+        M = _rand_sym(n, rng)
+        rp, col, m, d = oracle.offdiag_of_dense(M)
+        g = rng.standard_normal(n)
+        r = oracle.lanczos(n, rp, col, m, d, g, n)
+        lam = np.linalg.eigvalsh(M)
+        nrm = np.abs(lam).max()
+        assert abs(r.theta - lam[0]) <= 1e-10 * nrm
+        assert abs(r.v @ M @ r.v - lam[0]) <= 1e-9 * nrm
+        assert abs(np.linalg.norm(r.v) - 1.0) < 1e-14
+
+
+def test_lanczos_spec_examples():
+    # S:125 diag(-2, 1, 5) with the full Krylov space -> (-2, +-e1)
+    M = np.diag([-2.0, 1.0, 5.0])
+    rp, col, m, d = oracle.offdiag_of_dense(M)
+    r = oracle.lanczos(3, rp, col, m, d, np.array([0.3, -1.1, 0.7]), 3)
+    assert abs(r.theta + 2.0) < 1e-12
+    assert abs(abs(r.v[0]) - 1.0) < 1e-10
+    # S:124 M = I: rho_1 = 0 up to rounding -> invariant subspace break (reading A3), xi = 1
+    M = np.eye(3)
+    rp, col, m, d = oracle.offdiag_of_dense(M)
+    r = oracle.lanczos(3, rp, col, m, d, np.array([0.3, -1.1, 0.7]), 3)
+    assert r.k == 1 and abs(r.theta - 1.0) <= 4e-16
+
+
+def test_lanczos_matches_dense_rayleigh_ritz():
+    # Before orthogonality is lost the Ritz value equals lambda_min of V^T M V with V the Krylov basis
+    rng = np.random.default_rng(7)
+    n, q = 300, 6
+    M = _rand_sym(n, rng)
+    rp, col, m, d = oracle.offdiag_of_dense(M)
+    g = rng.standard_normal(n)
+    r = oracle.lanczos(n, rp, col, m, d, g, q)
+    K = np.empty((n, q))
+    K[:, 0] = g
+    for j in range(1, q):
+        K[:, j] = M @ K[:, j - 1]
+    Q, _ = np.linalg.qr(K)
+    H = Q.T @ M @ Q
+    lam = np.linalg.eigvalsh(H)[0]
+    assert abs(r.theta - lam) <= 1e-10 * np.abs(np.linalg.eigvalsh(M)).max()
+    # interlacing: never below lambda_min(M)
+    assert r.theta >= np.linalg.eigvalsh(M)[0] - 1e-12 * np.abs(M).max()
+    # the returned unit vector realises (close to) the Ritz value
+    assert abs(r.v @ M @ r.v - r.theta) < 1e-9
+
+
+def test_lanczos_fact_41_statistical():
+    # Fact 4.1: n=100, eps=1, delta=1/4, q = ceil(1/2 + log(n/delta^2)) = 8
+    rng = np.random.default_rng(8)
+    n, q, trials, ok = 100, 8, 200, 0
+    M = _rand_sym(n, rng)
+    rp, col, m, d = oracle.offdiag_of_dense(M)
+    lam = np.linalg.eigvalsh(M)
+    nrm = np.abs(lam).max()
+    for t in range(trials):
+        r = oracle.lanczos(n, rp, col, m, d, si.normals(99, 1, t, 0, n), q)
+        ok += (r.v @ M @ r.v) <= lam[0] + nrm / 8
+    assert ok / trials >= 0.5
+
+
+# ------------------------------------------------------------- Alg. 4 loop invariants
+def _shadow_cgal(L, o, T, beta0=1.0):
+    """Dense CGAL (Alg. 1) driven by the oracle's v_t; returns per-t shadow states."""
+    n = L.n
+    Lam = L.dense()
+    nrm = np.sqrt((Lam ** 2).sum())
+    C = -Lam / nrm
+    alpha, b = 1.0, 1.0 / n
+    X = np.zeros((n, n))
+    y = np.zeros(n)
+    V = o.vhist
+    out = []
+    for t in range(1, T + 1):
+        beta = beta0 * math.sqrt(t + 1)
+        eta = 2.0 / (t + 1)
+        Dt = C + np.diag(y + beta * (np.diag(X) - b))
+        lam_min = np.linalg.eigvalsh(Dt)[0]
+        v = V[t - 1]
+        X = (1 - eta) * X + eta * alpha * np.outer(v, v)
+        zb = np.diag(X) - b
+        nz = zb @ zb
+        gam = beta0 if nz == 0 else min(beta0, 4 * alpha ** 2 * beta0 / ((t + 1) ** 1.5 * nz))
+        y = y + gam * zb
+        out.append(dict(X=X.copy(), y=y.copy(), lam_min=lam_min, C=C))
+    return out
+
+
+def test_loop_invariants_shadow_cgal():
+    # eqn:loop-invariant: z = A X_t, S = X_t Omega, tau = tr X_t, p = <C, X_t>
+    L = si.laplacian_from_edges(14, *zip(*[(i, j, 1.0) for i in range(14) for j in range(i + 1, 14)
+                                            if (i * 7 + j * 3) % 5 < 2]))
+    n, R, T = L.n, 4, 60
+    o = oracle.Oracle(L, R, seed=11, logcap=T, vhist=T, qfix=n)  # full Krylov space -> exact min eigvec
+    o.step(T)
+    sh = _shadow_cgal(L, o, T)
+    X = sh[-1]["X"]
+    assert np.allclose(o.z, np.diag(X), atol=1e-14, rtol=1e-12)
+    assert np.allclose(o.S, X @ o.Omega, atol=1e-13, rtol=1e-11)
+    assert math.isclose(o.tau, np.trace(X), rel_tol=1e-13)
+    assert math.isclose(o.p, float(np.sum(sh[-1]["C"] * X)), rel_tol=1e-11, abs_tol=1e-15)
+    assert np.allclose(o.y, sh[-1]["y"], rtol=1e-9, atol=1e-13)
+    lg = o.log
+    for t in range(T):
+        # with the full Krylov space the Ritz value is lambda_min(D_t) (D_t assembled densely)
+        assert abs(lg[t, 3] - sh[t]["lam_min"]) <= 1e-9 * (1 + abs(sh[t]["lam_min"]))
+        assert abs(lg[t, 4] - lg[t, 3]) <= 1e-9 * (1 + abs(lg[t, 3]))  # xi = v* D v
+    # tr X_t = alpha for t >= 1 (eta_1 = 1)
+    assert abs(o.z.sum() - 1.0) < 1e-13 and abs(o.tau - 1.0) < 1e-13
+
+
+def test_unscaled_variant_invariants():
+    L = si.laplacian("c0")
+    o = oracle.Oracle(L, 5, seed=0, scale=False, logcap=30)
+    o.step(30)
+    assert math.isclose(o.z.sum(), L.n, rel_tol=1e-12)  # tr X = alpha = n
+    assert o.b == 1.0 and o.alpha == L.n
+
+
+# ------------------------------------------------------------- SDP value closed forms + brute force
+def _edges_graph(n, edges):
+    i, j = zip(*edges)
+    return si.laplacian_from_edges(n, i, j, [1.0] * len(edges))
+
+
+@pytest.mark.parametrize("name,n,edges,sdp", [
+    ("C5", 5, [(k, (k + 1) % 5) for k in range(5)], 10 * (1 + math.cos(math.pi / 5))),  # odd cycle 2n(1+cos(pi/n))
+    ("C8", 8, [(k, (k + 1) % 8) for k in range(8)], 4 * 8),  # bipartite: 4 sum w
+    ("K6", 6, [(i, j) for i in range(6) for j in range(i + 1, 6)], 36.0),  # K_n: n^2
+])
+def test_sdp_value_closed_forms(name, n, edges, sdp):
+    L = _edges_graph(n, edges)
+    o = oracle.Oracle(L, 3, seed=5, logcap=1)
+    o.step(3000)
+    val = o.implicit_objective()
+    assert abs(val - sdp) / sdp < 3e-3, (name, val, sdp)
+
+
+def _brute_maxcut(L):
+    i, j, w = L.edges()
+    best = -1.0
+    for bits in itertools.product([1, -1], repeat=L.n - 1):
+        chi = np.array((1,) + bits)
+        best = max(best, float(np.sum(w * (chi[i] != chi[j]))))
+    return best
+
+
+def test_rounded_cut_vs_brute_force():
+    rng = np.random.default_rng(9)
+    for trial in range(4):
+        n = 12
+        edges = [(a, b) for a in range(n) for b in range(a + 1, n) if rng.random() < 0.4]
+        L = _edges_graph(n, edges)
+        res = oracle.solve(L, R=4, T=400, seed=trial)
+        opt = _brute_maxcut(L)
+        assert res["cut_weight"] <= opt + 1e-9
+        assert res["cut_weight"] >= 0.878 * opt * 0.9   # sign rounding gives a good cut here
+        assert res["implicit_objective"] >= 4 * opt * (1 - 2e-2)  # relaxation dominates
+    # bipartite: the rounded cut is the optimum (all edges)
+    edges = [(a, b) for a in range(6) for b in range(6, 12) if (a + b) % 3]
+    L = _edges_graph(12, edges)
+    res = oracle.solve(L, R=4, T=400, seed=1)
+    assert res["cut_weight"] == len(edges) == _brute_maxcut(L)
+
+
+def test_weak_duality_certificate():
+    # eqn:model-dual-function-supp: alpha lambda_min(C + A* y) - <y, b> <= p* (scaled, minimize)
+    L = si.laplacian("c0")
+    o = oracle.Oracle(L, 4, seed=0, logcap=1)
+    o.step(300)
+    C = -L.dense() / o.nrmL
+    lb = 1.0 * np.linalg.eigvalsh(C + np.diag(o.y))[0] - o.y.sum() / L.n
+    ub_orig = -lb * o.nrmL * L.n  # upper bound on max tr(L X)
+    val = o.implicit_objective()
+    assert ub_orig >= val * (1 - 5e-3)
+    assert (ub_orig - val) / val < 5e-2
+
+
+# ------------------------------------------------------------- Nystrom (Alg. 3 / SM3)
+def test_matlab_eps():
+    assert oracle.matlab_eps(1.0) == 2.0 ** -52
+    assert oracle.matlab_eps(3.0) == 2.0 ** -51
+    assert oracle.matlab_eps(0.75) == 2.0 ** -53
+
+
+def test_nystrom_exact_recovery_low_rank():
+    # rank(X) <= R -> X^ = X with probability one
+    rng = np.random.default_rng(10)
+    n, r, R = 60, 3, 6
+    G = rng.standard_normal((n, r))
+    X = G @ G.T
+    Om = rng.standard_normal((n, R))
+    U, Lam, err = oracle.nystrom_reconstruct(X @ Om, Om, np.trace(X))
+    Xh = U @ np.diag(Lam) @ U.T
+    assert np.linalg.norm(Xh - X) <= 1e-9 * np.linalg.norm(X)
+    assert np.allclose(U.T @ U, np.eye(R), atol=1e-12)
+    assert np.all(np.diff(Lam) <= 1e-12) and np.all(Lam >= 0)
+    assert abs(err[r - 1]) <= 1e-9 * np.trace(X)
+
+
+def test_nystrom_error_identity_and_trace_correction():
+    rng = np.random.default_rng(11)
+    n, R = 40, 8
+    for trial in range(20):
+        G = rng.standard_normal((n, n)) * (0.7 ** np.arange(n))
+        X = G @ G.T
+        Om = rng.standard_normal((n, R))
+        U, Lam, err = oracle.nystrom_reconstruct(X @ Om, Om, np.trace(X))
+        # err_r = ||X - [X^]_r||_* -- X - [X^]_r is psd so the nuclear norm is its trace
+        for rr in (1, 3, R):
+            Xr = U[:, :rr] @ np.diag(Lam[:rr]) @ U[:, :rr].T
+            nuc = np.abs(np.linalg.eigvalsh(X - Xr)).sum()
+            assert abs(err[rr - 1] - nuc) <= 1e-8 * np.trace(X)
+        # err nonincreasing in r and bounds the best rank-r error
+        assert np.all(np.diff(err) <= 1e-9 * np.trace(X))
+        ev = np.sort(np.linalg.eigvalsh(X))[::-1]
+        assert np.all(ev[R:].sum() <= err[-1] + 1e-9 * np.trace(X))
+        # trace correction at most doubles the error
+        Lt = oracle.trace_correct(Lam, np.trace(X))
+        e_hat = np.abs(np.linalg.eigvalsh(X - U @ np.diag(Lam) @ U.T)).sum()
+        e_til = np.abs(np.linalg.eigvalsh(X - U @ np.diag(Lt) @ U.T)).sum()
+        assert e_til <= 2 * e_hat * (1 + 1e-9) + 1e-12
+        assert math.isclose(Lt.sum(), np.trace(X), rel_tol=1e-13)
+
+
+def test_trace_correct_example():
+    assert np.allclose(oracle.trace_correct([0.5, 0.3], 1.0), [0.6, 0.4])
+
+
+def test_fact_51_mean_bound():
+    # Fact 5.1: E ||X - X^||_* <= (1 + r/(R-r-1)) ||X - [X]_r||_*
+    rng = np.random.default_rng(12)
+    n, R, r = 50, 12, 5
+    G = rng.standard_normal((n, n)) * (0.8 ** np.arange(n))
+    X = G @ G.T
+    ev = np.sort(np.linalg.eigvalsh(X))[::-1]
+    tail = ev[r:].sum()
+    errs = []
+    for t in range(300):
+        Om = rng.standard_normal((n, R))
+        U, Lam, _ = oracle.nystrom_reconstruct(X @ Om, Om)
+        errs.append(np.abs(np.linalg.eigvalsh(X - U @ np.diag(Lam) @ U.T)).sum())
+    assert np.mean(errs) <= (1 + r / (R - r - 1)) * tail * 1.1
+
+
+# ------------------------------------------------------------- rounding
+def test_rounding_examples():
+    L3 = si.laplacian_from_edges(3, [0, 0, 1], [1, 2, 2], [1.0, 1.0, 1.0])
+    assert oracle.cut_weight(L3, [1, 1, -1]) == 2.0  # SPEC triangle example
+    chi = np.array([1, 1, -1])
+    assert oracle.cut_weight(L3, chi) == 0.25 * chi @ L3.dense() @ chi
+    P3 = si.laplacian_from_edges(3, [0, 1], [1, 2], [1.0, 1.0])
+    c, w, k = oracle.round_cut(P3, np.array([[1.0], [-1.0], [1.0]]))
+    assert w == 2.0 == _brute_maxcut(P3)
+    c, w, k = oracle.round_cut(P3, np.array([[-0.0], [0.0], [0.0]]))  # sgn(0)=+1
+    assert w == 0.0
+    C5 = _edges_graph(5, [(k, (k + 1) % 5) for k in range(5)])
+    K4 = _edges_graph(4, [(i, j) for i in range(4) for j in range(i + 1, 4)])
+    assert _brute_maxcut(P3) == 2 and _brute_maxcut(C5) == 4 and _brute_maxcut(K4) == 4
