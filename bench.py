@@ -1,0 +1,258 @@
+#!/usr/bin/env python
+"""bench.py -- SketchyCGAL MaxCut iterations/s and Lanczos SpMV HBM GB/s on B200.
+
+Contract (task statement + BASELINE.json): one JSON line on rank 0.
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+A "step" is one SketchyCGAL iteration t (Alg. 4 lines 5-10):
+one randomized Lanczos call (pass 1 + tridiagonal eigensolve + pass 2), the
+monitor matvec, the primal/dual updates and the rank-one sketch update, on the
+synthetic stand-in of BASELINE.json configs[3] (n = 2^24 mutual k-NN random
+geometric graph).  Warm-up runs iterations
+t = 1..W, the timed window is t = W+1..W+K.  The per-iteration working set
+(~1.5 GB) is larger than the 126 MB L2, so no L2 flush is inserted.
+
+--impl reference runs the CPU oracle (oracle/, test infrastructure) on the host
+cores for a bounded sample of the same workload (see cpu_baseline.sample).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SketchyCGAL MaxCut iterations/s and Lanczos SpMV HBM GB/s (fraction of peak), 1/2/4/8 B200"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
+                          and "Not" not in r[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _ncu_traffic(kernel_name: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+    try:
+        with open(path) as f:
+            js = json.load(f)
+        ent = js.get("kernels", {}).get(kernel_name)
+        if ent and js.get("workload") == "c3":
+            return float(ent["dram_bytes"])
+    except Exception:
+        pass
+    return None
+
+
+def cpu_oracle_sample(cfg: str, L, iters: int):
+    """Time the oracle (as it stands, single-threaded C) on `iters` iterations of the workload."""
+    import oracle
+    import scg_inputs as si
+    c = si.CONFIGS[cfg]
+    t0 = time.perf_counter()
+    o = oracle.Oracle(L, c["R"], seed=c["seed"], logcap=iters)
+    t1 = time.perf_counter()
+    o.step(iters)
+    t2 = time.perf_counter()
+    lg = o.log
+    matvecs = float(np.sum(2 * lg[:, 2] - 1 + 1))
+    return dict(value=iters / (t2 - t1), unit="iterations/s", cores=1, kind="oracle",
+                sample=f"oracle (C, 1 thread) on {cfg} iterations t=1..{iters} (q_t={int(lg[0, 1])}..{int(lg[-1, 1])}),"
+                       f" {t2 - t1:.1f} s; setup {t1 - t0:.1f} s excluded",
+                lanczos_matvecs_per_s=matvecs / (t2 - t1), seconds=t2 - t1)
+
+
+def run_reference(args, rank, world):
+    import scg_inputs as si
+    if rank != 0:
+        return
+    L = si.laplacian(args.config)
+    iters = max(1, min(args.steps, args.ref_iters))
+    cb = cpu_oracle_sample(args.config, L, iters)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "iterations/s", "n_gpus": world,
+            "steps": iters, "warmup": 0, "ms_per_step": 1e3 / cb["value"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config_dict(args.config, L, world, 1, iters),
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _config_dict(cfg, L, world, t0, t1):
+    import scg_inputs as si
+    c = si.CONFIGS[cfg]
+    return {"workload": f"{cfg}: {c['desc']}", "n": int(L.n), "m": int(L.m), "R": c["R"], "T_config": c["T"],
+            "t_window": [int(t0), int(t1)], "parallelism": f"rows{world}",
+            "l2": "no flush: per-iteration working set > 126 MB L2 (inputs larger than L2)"}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_1912_02949_b200 as scg
+    import scg_inputs as si
+
+    if world > 1:
+        raise SystemExit("multi-GPU bench: row-sharded path not in this build")
+    torch.cuda.set_device(local_rank)
+    L = si.laplacian(args.config)
+    c = si.CONFIGS[args.config]
+    stream = torch.cuda.Stream()
+    W, K = args.warmup, args.steps
+    with torch.cuda.stream(stream):
+        solver = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], profile=True, device=local_rank,
+                                 stream=ctypes_stream(stream))
+        solver.step(W)
+        solver.synchronize()
+        solver.reset_stats()
+        l0 = solver.launches
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        with ClockSampler(local_rank) as clk:
+            ev0.record(stream)
+            solver.step(K)
+            ev1.record(stream)
+            ev1.synchronize()
+        solver.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        launches = solver.launches - l0
+        stats = solver.kernel_stats()
+        lg = solver.iter_log(W + 1, K)
+    secs = ms / 1e3
+    value = K / secs
+    ks = [s for s in stats if s["launches"] > 0]
+    top = max(ks, key=lambda s: s["total_ms"])
+    peak, peak_kind = _peaks()
+
+    def gbs(s):
+        return s["bytes_per_launch"] * s["launches"] / (s["total_ms"] / 1e3) / 1e9 if s["total_ms"] > 0 else 0.0
+
+    achieved = gbs(top)
+    traffic = _ncu_traffic(top["name"])
+    matvecs = float(np.sum(lg[:, 2] + (lg[:, 2] - 1) + 1))
+    spmv = [s for s in ks if s["name"].startswith("lanczos_a")][0]
+    kernels = {s["name"]: {"launches": s["launches"], "avg_us": 1e3 * s["total_ms"] / s["launches"],
+                           "share": s["total_ms"] / ms, "gbs": round(gbs(s), 1)} for s in ks}
+    # end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(scg, si, L, c, K, W, local_rank)
+    cb = None
+    if rank == 0 and not args.no_cpu:
+        cb = cpu_oracle_sample(args.config, L, args.ref_iters)
+        cb = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    line = {"metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": _config_dict(args.config, L, world, W + 1, W + K),
+            "roofline": {"bound": "hbm", "kernel": top["name"], "achieved": round(achieved, 1), "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": top["bytes_per_launch"]},
+            "lanczos_matvecs_per_s": matvecs / secs, "spmv_gbs": round(gbs(spmv), 1),
+            "spmv_frac": gbs(spmv) / peak, "kernels": kernels,
+            "cpu_baseline": cb, "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(launches)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def ctypes_stream(stream):
+    import ctypes
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def run_e2e(scg, si, L, c, K, W, dev):
+    """Same metric through the C ABI with HOST buffers: init (CSR H2D) + W + K iterations + per-step
+    iteration-record D2H + reconstruct (U, Lambda D2H); value = K / (time of the whole job)."""
+    import torch
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], device=dev)
+    s.step(W + K)
+    lg = s.iter_log()
+    U, lam, _ = s.reconstruct()
+    s.synchronize()
+    t1 = time.perf_counter()
+    s.close()
+    h2d = L.row_ptr.nbytes + L.col.nbytes + L.val.nbytes
+    d2h = lg.nbytes + U.nbytes + lam.nbytes
+    return {"value": (W + K) / (t1 - t0), "unit": "iterations/s", "h2d_bytes_per_step": h2d / (W + K),
+            "d2h_bytes_per_step": d2h / (W + K), "seconds": t1 - t0,
+            "note": "pageable numpy CSR copied inside init; t=1..W+K; includes host CSR split and Omega draw"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-iters", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

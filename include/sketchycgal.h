@@ -1,0 +1,182 @@
+/*
+ * sketchycgal.h -- C ABI of the B200-native SketchyCGAL MaxCut hot path.
+ *
+ * Method: SketchyCGAL (Yurtsever, Tropp, Fercoq, Udell, Cevher, arXiv 1912.02949),
+ * Alg. 4 applied to the MaxCut SDP:
+ *     maximize tr(L X)  s.t.  diag X = 1,  X psd,
+ * posed as the model problem with C = -L, A = diag, b = 1,
+ * alpha = n.  Per iteration t the library runs, on the GPU:
+ *   - one randomized Lanczos min-eigenvector computation of
+ *       D_t = C + A*(y + beta_t (z - b))          (Alg. 2)
+ *     as two passes of fused SpMV + diagonal + three-term-recurrence kernels,
+ *   - the primal update z <- (1-eta) z + eta alpha (v o v)   (Alg. 4 line 8)
+ *   - the dual update    y <- y + gamma (z - b)               (Alg. 4 line 9)
+ *   - the Nystrom sketch S <- (1-eta) S + eta alpha v (v^T Omega)  (Alg. 4 line 10,
+ *     eqn:sketch-update PAPER.md:1162-1169).
+ * The arithmetic follows the Canonical Arithmetic Contract of DESIGN.md section 3
+ * (exact global sums, fixed row-sum order), so iterates are bitwise identical to
+ * the CPU oracle's and independent of grid shape and GPU count.
+ *
+ * Conventions
+ *   - All functions return scg_status (0 = OK, < 0 = error, see below).  No
+ *     exception or C++ type crosses the ABI.  After a CUDA/NCCL error the context
+ *     is sticky-failed and every later call returns SCG_ESTATE.
+ *   - Ownership: every pointer argument is caller-owned HOST memory unless the
+ *     comment says "device".  Inputs are copied before the call returns; outputs
+ *     are written into caller-allocated buffers of the stated size.
+ *   - The context owns all device memory and its CUDA stream.  A context is
+ *     single-writer (not thread-safe); several contexts may coexist.
+ *   - Multi-GPU: one process per GPU; every rank calls every function
+ *     collectively with its own row range.  dist == NULL means one GPU owning
+ *     all rows.
+ *   - Results are reported in ORIGINAL units, even though the
+ *     iteration runs on the scaled problem when SCG_SCALE
+ *     is set.
+ */
+#ifndef SKETCHYCGAL_H
+#define SKETCHYCGAL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct scg_ctx scg_ctx;
+
+typedef enum {
+  SCG_OK = 0,
+  SCG_EINVAL = -1,   /* bad argument: n < 2, R < 1, R > n, alpha <= 0, beta0 <= 0,
+                        malformed CSR (unsorted/out-of-range columns), bad shard bounds */
+  SCG_ENOMEM = -2,   /* device or host allocation failed */
+  SCG_ECUDA = -3,    /* CUDA runtime error (context becomes sticky-failed) */
+  SCG_ENCCL = -4,    /* NCCL error (context becomes sticky-failed) */
+  SCG_ECHOL = -5,    /* Nystrom reconstruction: Cholesky failed after 40 shift doublings */
+  SCG_ESTATE = -6,   /* call on a failed context, or out of order (e.g. objective before reconstruct) */
+  SCG_ERANGE = -7,   /* a summand of an exact sum was non-finite or >= 2^100 (DESIGN.md CAC-2) */
+  SCG_EUNSUPPORTED = -8
+} scg_status;
+
+/* init flags */
+enum {
+  SCG_SCALE = 1u << 0,          /* problem scaling ||C||_F = ||A|| = alpha = 1; default on */
+  SCG_TRACE_CORRECT = 1u << 1,  /* Lambda += (alpha - tr Lambda)/R after reconstruct (Alg. 4 line 13) */
+  SCG_PROFILE = 1u << 8         /* record CUDA events around every kernel launch (bench / kernel stats) */
+};
+
+/* This rank's rows [row_begin, row_end) of the symmetric weighted Laplacian
+ * L = sum_{ij in E} w_ij (e_i - e_j)(e_i - e_j)^T  (eqn:comb-laplacian).
+ * Off-diagonal entries are L_ij = -w_ij (any sign: signed weights are accepted).
+ * Columns must be strictly ascending within a row and global (0..n_global-1). */
+typedef struct {
+  int64_t n_global;
+  int64_t row_begin, row_end;
+  const int64_t *row_ptr;   /* host, (row_end-row_begin)+1 offsets into col_idx / val */
+  const int32_t *col_idx;   /* host, global column ids */
+  const double *val;        /* host, L entries */
+  int32_t has_diagonal;     /* 1: the diagonal entries L_rr are present (used as given);
+                               0: absent, L_rr = -sum_j L_rj is formed */
+} scg_csr;
+
+/* Multi-GPU description (one process per GPU).  The NCCL unique id is created on
+ * rank 0 (sketchycgal_nccl_unique_id) and broadcast by the caller, e.g. through
+ * torch.distributed. */
+typedef struct {
+  int32_t rank, world;
+  const void *nccl_unique_id;   /* host, 128 bytes */
+} scg_dist;
+
+/* One record per iteration t (Alg. 4), original units where noted. */
+typedef struct {
+  int64_t t;          /* iteration index, 1-based */
+  int32_t q;          /* Lanczos bound min(q_t, n-1), q_t = ceil(t^(1/4) ln n) */
+  int32_t k;          /* Lanczos steps taken (< q on invariant-subspace break, Alg. 2 line 8) */
+  double theta;       /* Ritz value: min eigenvalue of the Lanczos tridiagonal (Alg. 2 line 12), scaled units */
+  double xi;          /* Rayleigh quotient v^T D_t v (eqn 5.1), scaled units */
+  double c;           /* v^T C v, scaled units */
+  double p;           /* objective tracker p_{t+1} = <C, X_{t+1}>, scaled units */
+  double znorm;       /* ||z_{t+1} - b||, scaled units */
+  double gamma;       /* dual step gamma_t (eqn:sketchy-cgal-dual-step) */
+  double tau;         /* trace tracker tau */
+} scg_iter_rec;
+
+/* Per-kernel-class timing (SCG_PROFILE), for bench.py's roofline. */
+typedef struct {
+  char name[32];
+  int64_t launches;
+  double total_ms;          /* sum of CUDA-event durations on the context stream */
+  double bytes_per_launch;  /* algorithmic HBM bytes of one launch */
+} scg_kstat;
+
+/* Create a context: copy this rank's CSR to the device, form C = -L (scaled by
+ * 1/||L||_F when SCG_SCALE), draw Omega (n x R standard normal, Alg. 3 line 2,
+ * PAPER.md:1228) from the seeded stream, set z = y = 0, S = 0 (Alg. 4 lines 3-4).
+ *   alpha: trace bound in ORIGINAL units (n for MaxCut); beta0: initial smoothing
+ *   (1 by default); seed: stream seed for Omega and the Lanczos
+ *   start vectors; device: CUDA device ordinal; cuda_stream: optional
+ *   cudaStream_t to run on (NULL: the context creates its own).
+ * Errors: SCG_EINVAL, SCG_ENOMEM, SCG_ECUDA, SCG_ENCCL.  *out is NULL on error. */
+scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, double alpha, double beta0,
+                                   uint64_t seed, uint32_t flags, const scg_dist *dist, int32_t device,
+                                   void *cuda_stream);
+
+/* Advance T iterations (t continues across calls).  Asynchronous on the context
+ * stream; returns after enqueueing and checking launch errors.  Device-side
+ * range errors surface at the next synchronizing call as SCG_ERANGE. */
+scg_status sketchycgal_step(scg_ctx *c, int64_t T);
+
+/* Block until all queued work is done; reports deferred device errors. */
+scg_status sketchycgal_synchronize(scg_ctx *c);
+
+/* NystromSketch.Reconstruct (Alg. 3 lines 11-16; Alg. SM3
+ * PAPER.md:3304-3317) followed by the optional trace correction (Alg. 4 line 13).
+ *   U: host, n_local x R column-major (this rank's rows), orthonormal columns (may be NULL)
+ *   Lambda: host, R, descending, ORIGINAL units (trace-corrected iff SCG_TRACE_CORRECT)
+ *   err: host, R (may be NULL): err_r = tau - sum_{j<=r} Lambda_j, before correction.
+ * The factor stays on the device for objective / feasibility / round. */
+scg_status sketchycgal_reconstruct(scg_ctx *c, double *U, double *Lambda, double *err);
+
+/* out[0] = tr(L X_t) of the implicit iterate from the tracked p;
+ * out[1] = tr(L X^) of the reconstruction (needs reconstruct; NAN before).  Original units. */
+scg_status sketchycgal_objective(scg_ctx *c, double out[2]);
+
+/* out[0] = ||z - b|| / (1 + ||b||) of the implicit iterate;
+ * out[1] = ||diag X^ - 1|| / ||1||;  out[2] = ||diag X^ - 1|| / (1 + ||1||).  Original units. */
+scg_status sketchycgal_feasibility(scg_ctx *c, double out[3]);
+
+/* Rounding: the best of the R sign cuts sgn(U[:,k]) (sgn(0)=+1,
+ * ties -> lowest k), normalized so chi[0] = +1.  chi_local: host int8, n_local. */
+scg_status sketchycgal_round(scg_ctx *c, int8_t *chi_local, double *cut_weight);
+
+/* Copy iteration records t0..t0+count-1 (1-based t) into out. */
+scg_status sketchycgal_iter_log(scg_ctx *c, int64_t t0, int64_t count, scg_iter_rec *out);
+
+/* Test / diagnostics access to the state (this rank's rows).
+ *   which: 0 z, 1 y, 2 S (n_local x R col-major), 3 Omega (same), 4 v (last eigenvector),
+ *          5 d (diagonal of D for the NEXT iteration), 6 C diagonal (scaled). */
+scg_status sketchycgal_get_state(scg_ctx *c, int32_t which, double *out);
+
+/* Apply D_{t+1} = C + diag(d) (primitives 1+2, eqn:primitives PAPER.md:567-590) with
+ * the same row-sum order as the Lanczos kernels: y = D x.  x: host, n_global; y: host, n_local. */
+scg_status sketchycgal_apply_D(scg_ctx *c, const double *x, double *y);
+
+/* Iterations done so far. */
+int64_t sketchycgal_iterations(const scg_ctx *c);
+
+/* Kernel launches issued since init / the last reset (counts only this library's kernels). */
+int64_t sketchycgal_launch_count(const scg_ctx *c);
+
+/* Kernel statistics (needs SCG_PROFILE): fills up to max entries, returns the count (<0 on error). */
+int32_t sketchycgal_kernel_stats(scg_ctx *c, scg_kstat *out, int32_t max);
+void sketchycgal_reset_stats(scg_ctx *c);
+
+/* Write a 128-byte NCCL unique id (call on rank 0, broadcast to all ranks). */
+scg_status sketchycgal_nccl_unique_id(void *out128);
+
+const char *sketchycgal_last_error(const scg_ctx *c);
+void sketchycgal_destroy(scg_ctx *c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKETCHYCGAL_H */

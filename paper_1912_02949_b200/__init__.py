@@ -1,0 +1,261 @@
+"""B200-native SketchyCGAL MaxCut hot path (arXiv 1912.02949) -- Python binding.
+
+Thin ctypes binding of the C ABI in ``include/sketchycgal.h``: argument
+marshalling only.  Every step of the iteration runs in the CUDA kernels of
+``csrc/`` (sm_100a); there is no CPU fallback -- ``load()`` raises if the
+library is missing or no GPU is visible.  PyTorch is used only for device
+selection / streams and ``torch.distributed`` plumbing (multi-GPU bootstrap).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import sys
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(_HERE)
+LIB_DIR = os.path.join(_HERE, "lib")
+LIB_PATH = os.path.join(LIB_DIR, "libsketchycgal.so")
+SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("sketchycgal.cu", "kernels.cuh", "xsum.cuh")]
+HEADERS = [os.path.join(ROOT, "include", "sketchycgal.h"), os.path.join(ROOT, "scg_inputs", "include", "scg_rng.h")]
+
+SCG_SCALE = 1 << 0
+SCG_TRACE_CORRECT = 1 << 1
+SCG_PROFILE = 1 << 8
+
+STATUS = {0: "SCG_OK", -1: "SCG_EINVAL", -2: "SCG_ENOMEM", -3: "SCG_ECUDA", -4: "SCG_ENCCL", -5: "SCG_ECHOL",
+          -6: "SCG_ESTATE", -7: "SCG_ERANGE", -8: "SCG_EUNSUPPORTED"}
+
+
+def _nccl_paths():
+    try:
+        import nvidia.nccl as nn
+        base = os.path.dirname(nn.__file__) if getattr(nn, "__file__", None) else list(nn.__path__)[0]
+    except Exception:
+        base = os.path.join(sys.prefix, "lib", f"python{sys.version_info.major}.{sys.version_info.minor}",
+                            "site-packages", "nvidia", "nccl")
+    inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+    if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.exists(os.path.join(lib, "libnccl.so.2")):
+        return inc, lib
+    return None, None
+
+
+def nvcc_cmd(out: str) -> list[str]:
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
+           "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+           os.path.join(_HERE, "csrc", "sketchycgal.cu"), "-o", out]
+    inc, lib = _nccl_paths()
+    if inc:
+        cmd[1:1] = ["-DSCG_WITH_NCCL", f"-I{inc}"]
+        cmd += [f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}"]
+    return cmd
+
+
+def build(force: bool = False) -> str:
+    """Compile the CUDA library for sm_100a in-tree (nvcc cross-compiles without a GPU)."""
+    os.makedirs(LIB_DIR, exist_ok=True)
+    newest = max(os.path.getmtime(p) for p in SOURCES + HEADERS)
+    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
+        return LIB_PATH
+    tmp = LIB_PATH + f".tmp{os.getpid()}"
+    subprocess.check_call(nvcc_cmd(tmp))
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+class IterRec(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_int64), ("q", ctypes.c_int32), ("k", ctypes.c_int32), ("theta", ctypes.c_double),
+                ("xi", ctypes.c_double), ("c", ctypes.c_double), ("p", ctypes.c_double),
+                ("znorm", ctypes.c_double), ("gamma", ctypes.c_double), ("tau", ctypes.c_double)]
+
+
+class KStat(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_int64), ("total_ms", ctypes.c_double),
+                ("bytes_per_launch", ctypes.c_double)]
+
+
+class Csr(ctypes.Structure):
+    _fields_ = [("n_global", ctypes.c_int64), ("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64),
+                ("row_ptr", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("val", ctypes.c_void_p),
+                ("has_diagonal", ctypes.c_int32)]
+
+
+class Dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p)]
+
+
+EXPORTS = ["sketchycgal_maxcut_init", "sketchycgal_step", "sketchycgal_synchronize", "sketchycgal_reconstruct",
+           "sketchycgal_objective", "sketchycgal_feasibility", "sketchycgal_round", "sketchycgal_iter_log",
+           "sketchycgal_get_state", "sketchycgal_apply_D", "sketchycgal_iterations", "sketchycgal_launch_count",
+           "sketchycgal_kernel_stats", "sketchycgal_reset_stats", "sketchycgal_nccl_unique_id",
+           "sketchycgal_last_error", "sketchycgal_destroy"]
+
+_lib = None
+
+
+def open_library(path: str = LIB_PATH):
+    """dlopen the library and declare the ABI (no GPU needed)."""
+    lib = ctypes.CDLL(path)
+    P, I32, I64, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    lib.sketchycgal_maxcut_init.restype = ctypes.c_int
+    lib.sketchycgal_maxcut_init.argtypes = [ctypes.POINTER(P), ctypes.POINTER(Csr), I32, D, D, ctypes.c_uint64,
+                                            ctypes.c_uint32, ctypes.POINTER(Dist), I32, P]
+    for name, args in [("sketchycgal_step", [P, I64]), ("sketchycgal_synchronize", [P]),
+                       ("sketchycgal_reconstruct", [P, P, P, P]), ("sketchycgal_objective", [P, P]),
+                       ("sketchycgal_feasibility", [P, P]), ("sketchycgal_round", [P, P, P]),
+                       ("sketchycgal_iter_log", [P, I64, I64, P]), ("sketchycgal_get_state", [P, I32, P]),
+                       ("sketchycgal_apply_D", [P, P, P]), ("sketchycgal_nccl_unique_id", [P])]:
+        getattr(lib, name).restype = ctypes.c_int
+        getattr(lib, name).argtypes = args
+    lib.sketchycgal_iterations.restype = I64
+    lib.sketchycgal_iterations.argtypes = [P]
+    lib.sketchycgal_launch_count.restype = I64
+    lib.sketchycgal_launch_count.argtypes = [P]
+    lib.sketchycgal_kernel_stats.restype = I32
+    lib.sketchycgal_kernel_stats.argtypes = [P, P, I32]
+    lib.sketchycgal_reset_stats.restype = None
+    lib.sketchycgal_reset_stats.argtypes = [P]
+    lib.sketchycgal_last_error.restype = ctypes.c_char_p
+    lib.sketchycgal_last_error.argtypes = [P]
+    lib.sketchycgal_destroy.restype = None
+    lib.sketchycgal_destroy.argtypes = [P]
+    return lib
+
+
+def load():
+    """Load the CUDA library.  Fails loudly (no fallback) without the library or a GPU."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"CUDA library {LIB_PATH} is missing: run __graft_entry__.build()")
+        _lib = open_library(LIB_PATH)
+    return _lib
+
+
+class ScgError(RuntimeError):
+    pass
+
+
+def _c64(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+class SketchyCGAL:
+    """One GPU's SketchyCGAL MaxCut solver context (sketchycgal_maxcut_init ... destroy)."""
+
+    def __init__(self, L, R: int, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
+                 scale: bool = True, trace_correct: bool = True, profile: bool = False, device: int = 0,
+                 stream=None, row_begin: int = 0, row_end: int | None = None, dist=None):
+        self.lib = load()
+        self.n = int(L.n)
+        self.R = int(R)
+        self.row_begin = int(row_begin)
+        self.row_end = self.n if row_end is None else int(row_end)
+        self.nl = self.row_end - self.row_begin
+        rp = _c64(L.row_ptr, np.int64)
+        col = _c64(L.col, np.int32)
+        val = _c64(L.val, np.float64)
+        if row_begin != 0 or self.row_end != self.n:  # local rows of a full CSR
+            a, b = int(rp[self.row_begin]), int(rp[self.row_end])
+            col, val = col[a:b], val[a:b]
+            rp = rp[self.row_begin:self.row_end + 1] - a
+        self._keep = (rp, col, val)
+        csr = Csr(self.n, self.row_begin, self.row_end, rp.ctypes.data, col.ctypes.data, val.ctypes.data, 1)
+        flags = (SCG_SCALE if scale else 0) | (SCG_TRACE_CORRECT if trace_correct else 0) | \
+                (SCG_PROFILE if profile else 0)
+        self._h = ctypes.c_void_p()
+        dptr = None
+        if dist is not None:
+            self._dist = dist
+            dptr = ctypes.byref(dist)
+        st = self.lib.sketchycgal_maxcut_init(ctypes.byref(self._h), ctypes.byref(csr), self.R,
+                                              float(self.n if alpha is None else alpha), float(beta0), int(seed),
+                                              flags, dptr, int(device), stream)
+        if st != 0:
+            raise ScgError(f"sketchycgal_maxcut_init: {STATUS.get(st, st)}")
+
+    def _check(self, st, what):
+        if st != 0:
+            msg = self.lib.sketchycgal_last_error(self._h)
+            raise ScgError(f"{what}: {STATUS.get(st, st)} {msg.decode() if msg else ''}")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.sketchycgal_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, T: int):
+        self._check(self.lib.sketchycgal_step(self._h, int(T)), "sketchycgal_step")
+
+    def synchronize(self):
+        self._check(self.lib.sketchycgal_synchronize(self._h), "sketchycgal_synchronize")
+
+    @property
+    def t(self) -> int:
+        return int(self.lib.sketchycgal_iterations(self._h))
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.sketchycgal_launch_count(self._h))
+
+    def iter_log(self, t0: int = 1, count: int | None = None) -> np.ndarray:
+        count = self.t - t0 + 1 if count is None else count
+        buf = (IterRec * count)()
+        self._check(self.lib.sketchycgal_iter_log(self._h, int(t0), int(count), buf), "sketchycgal_iter_log")
+        return np.array([(r.t, r.q, r.k, r.theta, r.xi, r.c, r.p, r.znorm, r.gamma, r.tau) for r in buf],
+                        dtype=np.float64).reshape(count, 10)
+
+    def state(self, which: str) -> np.ndarray:
+        idx = {"z": 0, "y": 1, "S": 2, "Omega": 3, "v": 4, "d": 5, "cdiag": 6}[which]
+        size = self.nl * (self.R if which in ("S", "Omega") else 1)
+        out = np.empty(size, dtype=np.float64)
+        self._check(self.lib.sketchycgal_get_state(self._h, idx, out.ctypes.data), "sketchycgal_get_state")
+        return out.reshape(self.R, self.nl).T if which in ("S", "Omega") else out
+
+    def apply_D(self, x) -> np.ndarray:
+        x = _c64(x, np.float64)
+        y = np.empty(self.nl, dtype=np.float64)
+        self._check(self.lib.sketchycgal_apply_D(self._h, x.ctypes.data, y.ctypes.data), "sketchycgal_apply_D")
+        return y
+
+    def reconstruct(self, want_U: bool = True):
+        U = np.empty((self.R, self.nl), dtype=np.float64) if want_U else None
+        lam = np.empty(self.R, dtype=np.float64)
+        err = np.empty(self.R, dtype=np.float64)
+        self._check(self.lib.sketchycgal_reconstruct(self._h, U.ctypes.data if want_U else None, lam.ctypes.data,
+                                                     err.ctypes.data), "sketchycgal_reconstruct")
+        return (U.T if want_U else None), lam, err
+
+    def objective(self):
+        out = np.empty(2, dtype=np.float64)
+        self._check(self.lib.sketchycgal_objective(self._h, out.ctypes.data), "sketchycgal_objective")
+        return out
+
+    def feasibility(self):
+        out = np.empty(3, dtype=np.float64)
+        self._check(self.lib.sketchycgal_feasibility(self._h, out.ctypes.data), "sketchycgal_feasibility")
+        return out
+
+    def round(self):
+        chi = np.empty(self.nl, dtype=np.int8)
+        w = ctypes.c_double()
+        self._check(self.lib.sketchycgal_round(self._h, chi.ctypes.data, ctypes.byref(w)), "sketchycgal_round")
+        return chi, w.value
+
+    def kernel_stats(self):
+        buf = (KStat * 16)()
+        n = self.lib.sketchycgal_kernel_stats(self._h, buf, 16)
+        return [dict(name=buf[i].name.decode(), launches=buf[i].launches, total_ms=buf[i].total_ms,
+                     bytes_per_launch=buf[i].bytes_per_launch) for i in range(max(n, 0))]
+
+    def reset_stats(self):
+        self.lib.sketchycgal_reset_stats(self._h)

@@ -1,0 +1,669 @@
+// kernels.cuh -- the per-iteration hot path of SketchyCGAL for MaxCut on sm_100a.
+//
+// Every kernel is HBM-bandwidth bound fp64 work (sparse matvec, axpys, rank-one
+// sketch update); none is a dense contraction, so no tensor cores are used
+// (DESIGN.md section 5).  Arithmetic follows the Canonical Arithmetic Contract
+// (DESIGN.md section 3): one IEEE operation per written op, fma only where written
+// (the library is compiled with --fmad=false), exact global sums (xsum.cuh).
+//
+// Data layout, one GPU owning rows [rb, rb + nl):
+//   CSR of the off-diagonal part of C = -L/||L||_F: rp[nl+1] int32, col int32
+//   (global ids, ascending), val fp64; cdiag[nl] = C_rr; d[nl] = diagonal of D_t.
+//   Gathered vectors (Lanczos w_i, g, x) are full length n (global index); own
+//   rows live at [rb, rb + nl).  Local vectors (a, z, y, v) are length nl.
+//   Omega, S: nl x R column-major, leading dimension nl.
+#pragma once
+#include <cstdint>
+
+#include "xsum.cuh"
+#include "../../scg_inputs/include/scg_rng.h"
+
+namespace scg {
+
+constexpr int kMaxQ = 128;   // Lanczos bound cap (max q_t in configs[0..4] is 94)
+constexpr int kMaxR = 64;    // sketch rank cap (BASELINE: R <= 50)
+constexpr int kBlock = 256;
+
+// Device-resident scalars of the current iteration.
+struct DevScalars {
+  double om[kMaxQ];        // omega_i, i = 1..k  (om[i-1])
+  double rho[kMaxQ + 1];   // rho[0] = ||g|| (start-vector norm), rho[i] = rho_i  (Alg. 2 line 7)
+  double s[kMaxQ];         // eigenvector of the tridiagonal (CAC-5)
+  double gk[kMaxR];        // g = v^T Omega
+  double theta, nu_x, xi, c, vv, nz, gamma, p, tau;
+  int k, brk, err, pad;
+};
+
+// Exact-sum slot: up to 3 accumulators + a block ticket counter.
+struct XSlot {
+  long long limbs[3][kLimbs];
+  unsigned int counter;
+  unsigned int pad;
+};
+
+struct Csr {
+  const int *rp;
+  const int *col;
+  const double *val;
+};
+
+// ---------------------------------------------------------------- block reduction
+template <int NS>
+__device__ __forceinline__ bool commit_and_ticket(XAcc (&acc)[NS], XSlot *slot, int err, DevScalars *sc) {
+  __shared__ long long sm[NS][kLimbs][kBlock / 32];
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+#pragma unroll
+    for (int i = 0; i < kLimbs; ++i) {
+      long long v = acc[s].d[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if (lane == 0) sm[s][i][warp] = v;
+    }
+  if (__syncthreads_or(err) && threadIdx.x == 0) atomicOr(&sc->err, 1);
+  if (warp == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int i = 0; i < kLimbs; ++i) {
+        long long v = lane < (int)(blockDim.x >> 5) ? sm[s][i][lane] : 0ll;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0 && v != 0)
+          atomicAdd(reinterpret_cast<unsigned long long *>(&slot->limbs[s][i]), (unsigned long long)v);
+      }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(&slot->counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  return s_last != 0;
+}
+
+// Called by thread 0 of the last block: read + reset slot accumulator s.
+__device__ __forceinline__ double slot_take(XSlot *slot, int s) {
+  long long l[kLimbs];
+  for (int i = 0; i < kLimbs; ++i) {
+    l[i] = (long long)atomicExch(reinterpret_cast<unsigned long long *>(&slot->limbs[s][i]), 0ull);
+  }
+  return xacc_round(l);
+}
+
+// ---------------------------------------------------------------- init kernels
+// ||L||_F^2 over all stored entries: off-diagonal weights (each stored once per
+// direction) and the diagonal (scaling).
+__global__ void k_frob(const double *__restrict__ w, long long nnz, const double *__restrict__ diag, int nl,
+                       XSlot *slot, DevScalars *sc, double *out) {
+  XAcc acc[1];
+  xacc_zero(acc[0]);
+  int err = 0;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
+  for (long long k = tid; k < nnz; k += st) xacc_add(acc[0], w[k] * w[k], err);
+  for (long long r = tid; r < nl; r += st) xacc_add(acc[0], diag[r] * diag[r], err);
+  if (commit_and_ticket<1>(acc, slot, err, sc) && threadIdx.x == 0) {
+    __threadfence();
+    *out = slot_take(slot, 0);
+    slot->counter = 0;
+  }
+}
+
+// C = -L (scaled by 1/nrm when scale): val = fl(w / nrm), cdiag = fl(-L_rr / nrm).
+__global__ void k_scale_c(const double *__restrict__ w, long long nnz, const double *__restrict__ ldiag, int nl,
+                          const double *__restrict__ nrm_ptr, int scale, double *__restrict__ val,
+                          double *__restrict__ cdiag) {
+  const double nrm = *nrm_ptr;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
+  for (long long k = tid; k < nnz; k += st) val[k] = scale ? w[k] / nrm : w[k];
+  for (long long r = tid; r < nl; r += st) cdiag[r] = scale ? (-ldiag[r]) / nrm : -ldiag[r];
+}
+
+// Omega[i, k] ~ N(0,1) from the seeded stream (Alg. 3 line 2).
+__global__ void k_omega(double *__restrict__ Om, int nl, long long rb, int R, uint64_t seed) {
+  const long long tot = (long long)nl * R;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(e / nl);
+    const long long r = e - (long long)k * nl;
+    Om[e] = scg_omega(seed, rb + r, k);
+  }
+}
+
+// d = fl(fma(beta, fl(z - b), y) + C_rr) (primitive 2 with y + beta (z - b)).
+__global__ void k_init_d(const double *__restrict__ z, const double *__restrict__ y, const double *__restrict__ cdiag,
+                         double *__restrict__ d, int nl, double b, double beta) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x)
+    d[r] = fma(beta, z[r] - b, y[r]) + cdiag[r];
+}
+
+// Lanczos start vector g = randn (Alg. 2 line 1) for iteration t and ||g||^2 (exact).
+__global__ void __launch_bounds__(kBlock) k_gen_start(double *__restrict__ g, int nl, long long rb, uint64_t seed,
+                                                      long long t, XSlot *slot, DevScalars *sc, int finalize) {
+  XAcc acc[1];
+  xacc_zero(acc[0]);
+  int err = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double v = scg_lanczos_start(seed, t, rb + r);
+    g[rb + r] = v;
+    xacc_add(acc[0], v * v, err);
+  }
+  if (commit_and_ticket<1>(acc, slot, err, sc) && threadIdx.x == 0 && finalize) {
+    __threadfence();
+    sc->rho[0] = sqrt(slot_take(slot, 0));
+    slot->counter = 0;
+  }
+}
+
+// ---------------------------------------------------------------- Lanczos pass 1
+// Step i, part A (Alg. 2 lines 4-5): a = D v_i with v_i = X_i / rho[i-1] formed on the
+// fly (Alg. 2 line 9 division), omega_i = v_i . a (exact).
+//   (D x)_r = fl(d_r x_r) then fma(C_rj, x_j, acc) over j ascending (CAC-3).
+__global__ void __launch_bounds__(kBlock) k_lanczos_a(Csr C, const double *__restrict__ d,
+                                                      const double *__restrict__ X, int nl, long long rb, int i,
+                                                      double *__restrict__ a, XSlot *slot, DevScalars *sc,
+                                                      int finalize) {
+  if (sc->brk) return;
+  const double den = sc->rho[i - 1];
+  XAcc acc[1];
+  xacc_zero(acc[0]);
+  int err = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double xr = X[rb + r] / den;
+    double s = d[r] * xr;
+    const int e0 = C.rp[r], e1 = C.rp[r + 1];
+    for (int e = e0; e < e1; ++e) s = fma(C.val[e], __ldg(&X[C.col[e]]) / den, s);
+    a[r] = s;
+    xacc_add(acc[0], xr * s, err);
+  }
+  if (commit_and_ticket<1>(acc, slot, err, sc) && threadIdx.x == 0 && finalize) {
+    __threadfence();
+    sc->om[i - 1] = slot_take(slot, 0);
+    slot->counter = 0;
+  }
+}
+
+// finalize helpers (also used after a multi-GPU all-reduce)
+__device__ __forceinline__ void fin_rho(DevScalars *sc, int i, double rho2) {
+  const double rho = sqrt(rho2);
+  sc->rho[i] = rho;
+  const double rp = i >= 2 ? sc->rho[i - 1] : 0.0;
+  if (rho <= 0x1p-45 * (fabs(sc->om[i - 1]) + rp)) {  // Alg. 2 line 8 (reading A3)
+    sc->k = i;
+    sc->brk = 1;
+  }
+}
+
+// Step i, part B (Alg. 2 lines 6-7): w_{i+1} = fma(-rho_{i-1}, v_{i-1}, fma(-omega_i, v_i, a)),
+// rho_i = ||w_{i+1}|| (exact); breakdown test.  Writes the un-normalized w_{i+1}.
+__global__ void __launch_bounds__(kBlock) k_lanczos_b(const double *__restrict__ a, const double *Xi,
+                                                      const double *Xim1, double *Xip1, int nl, long long rb,
+                                                      int i, XSlot *slot, DevScalars *sc, int finalize) {
+  if (sc->brk) return;
+  const double om = sc->om[i - 1];
+  const double den = sc->rho[i - 1];
+  const double denm = i >= 2 ? sc->rho[i - 2] : 1.0;
+  XAcc acc[1];
+  xacc_zero(acc[0]);
+  int err = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double vi = Xi[rb + r] / den;
+    double w = fma(-om, vi, a[r]);
+    if (i >= 2) w = fma(-den, Xim1[rb + r] / denm, w);  // rho_{i-1} = rho[i-1] = den
+    Xip1[rb + r] = w;
+    xacc_add(acc[0], w * w, err);
+  }
+  if (commit_and_ticket<1>(acc, slot, err, sc) && threadIdx.x == 0 && finalize) {
+    __threadfence();
+    fin_rho(sc, i, slot_take(slot, 0));
+    slot->counter = 0;
+  }
+}
+
+// ---------------------------------------------------------------- tridiagonal (CAC-5)
+__device__ int sturm_count(const double *om, const double *rho2, int k, double x) {
+  double pprev = 1.0, p = om[0] - x;
+  int sprev = 1;
+  int s = p > 0.0 ? 1 : (p < 0.0 ? -1 : -sprev);
+  int cnt = (s != sprev);
+  for (int j = 1; j < k; ++j) {
+    const double pn = fma(om[j] - x, p, -(rho2[j - 1] * pprev));
+    const int sn = pn > 0.0 ? 1 : (pn < 0.0 ? -1 : -s);
+    cnt += (sn != s);
+    pprev = p;
+    p = pn;
+    s = sn;
+    const double ap = fabs(p), aq = fabs(pprev);
+    if (ap > 0x1p500) { p *= 0x1p-500; pprev *= 0x1p-500; }
+    else if (ap < 0x1p-500 && aq < 0x1p-500) { p *= 0x1p500; pprev *= 0x1p500; }
+  }
+  return cnt;
+}
+
+// One warp: multisection (32 Sturm counts per round, one per lane) for theta, then
+// inverse iteration (lane 0, partial pivoting) for s (Alg. 2 lines 11-12).
+__global__ void k_tridiag(DevScalars *sc, int q) {
+  __shared__ double om[kMaxQ], rho[kMaxQ], rho2[kMaxQ];
+  const int lane = threadIdx.x;
+  const int k = sc->brk ? sc->k : q;
+  for (int j = lane; j < k; j += 32) om[j] = sc->om[j];
+  for (int j = lane; j < k - 1; j += 32) { rho[j] = sc->rho[j + 1]; rho2[j] = rho[j] * rho[j]; }
+  __syncwarp();
+  if (k == 1) {
+    if (lane == 0) { sc->theta = om[0]; sc->s[0] = 1.0; sc->k = 1; }
+    return;
+  }
+  // Gershgorin interval (sequential on lane 0; min/max are exact anyway)
+  double lo = 0.0, hi = 0.0;
+  if (lane == 0) {
+    for (int j = 0; j < k; ++j) {
+      const double rl = j > 0 ? rho[j - 1] : 0.0;
+      const double rr = j < k - 1 ? rho[j] : 0.0;
+      const double rj = rl + rr;
+      const double a = om[j] - rj, b = om[j] + rj;
+      if (j == 0 || a < lo) lo = a;
+      if (j == 0 || b > hi) hi = b;
+    }
+  }
+  lo = __shfl_sync(0xffffffffu, lo, 0);
+  hi = __shfl_sync(0xffffffffu, hi, 0);
+  const double NT = fabs(lo) > fabs(hi) ? fabs(lo) : fabs(hi);
+  if (NT == 0.0) {
+    if (lane == 0) { sc->theta = 0.0; for (int j = 0; j < k; ++j) sc->s[j] = j == 0 ? 1.0 : 0.0; sc->k = k; }
+    return;
+  }
+  const double pad = NT * 0x1p-20;
+  lo = lo - pad;
+  hi = hi + pad;
+  for (int round = 0; round < 12; ++round) {
+    const double h = (hi - lo) / 33.0;
+    const double x = fma((double)(lane + 1), h, lo);
+    const int c = sturm_count(om, rho2, k, x);
+    const unsigned mask = __ballot_sync(0xffffffffu, c >= 1);
+    const double xm1 = __shfl_up_sync(0xffffffffu, x, 1);
+    if (mask) {
+      const int f = __ffs(mask) - 1;  // first lane (lowest point) with count >= 1
+      const double nhi = __shfl_sync(0xffffffffu, x, f);
+      const double prevx = __shfl_sync(0xffffffffu, xm1, f);
+      const double nlo = f == 0 ? lo : prevx;
+      lo = nlo;
+      hi = nhi;
+    } else {
+      lo = __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+  if (lane != 0) return;
+  const double th = (lo + hi) * 0.5;
+  sc->theta = th;
+  double u0[kMaxQ], u1[kMaxQ], u2[kMaxQ], mul[kMaxQ], xv[kMaxQ], s[kMaxQ];
+  int swp[kMaxQ];
+  const double tiny = NT * 0x1p-60;
+  double c0 = om[0] - th, c1 = rho[0], c2 = 0.0;
+  for (int i = 0; i < k - 1; ++i) {
+    const double nb = rho[i], na = om[i + 1] - th, nc = (i + 1 < k - 1) ? rho[i + 1] : 0.0;
+    if (fabs(c0) >= fabs(nb)) {
+      const double m = c0 != 0.0 ? nb / c0 : 0.0;
+      u0[i] = c0; u1[i] = c1; u2[i] = c2; swp[i] = 0; mul[i] = m;
+      c0 = na - m * c1;
+      c1 = nc - m * c2;
+      c2 = 0.0;
+    } else {
+      const double m = c0 / nb;
+      u0[i] = nb; u1[i] = na; u2[i] = nc; swp[i] = 1; mul[i] = m;
+      const double t0 = c1 - m * na, t1 = c2 - m * nc;
+      c0 = t0;
+      c1 = t1;
+      c2 = 0.0;
+    }
+  }
+  u0[k - 1] = c0; u1[k - 1] = 0.0; u2[k - 1] = 0.0;
+  for (int i = 0; i < k; ++i)
+    if (fabs(u0[i]) < tiny) u0[i] = u0[i] < 0.0 ? -tiny : tiny;
+  for (int j = 0; j < k; ++j) s[j] = (double)(j % 5 + 1) * 0.25;
+  for (int it = 0; it < 3; ++it) {
+    for (int j = 0; j < k; ++j) xv[j] = s[j];
+    for (int i = 0; i < k - 1; ++i) {
+      if (swp[i]) { const double t = xv[i]; xv[i] = xv[i + 1]; xv[i + 1] = t; }
+      xv[i + 1] = fma(-mul[i], xv[i], xv[i + 1]);
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double t = xv[i];
+      if (i + 1 < k) t = fma(-u1[i], xv[i + 1], t);
+      if (i + 2 < k) t = fma(-u2[i], xv[i + 2], t);
+      xv[i] = t / u0[i];
+    }
+    double mx = 0.0;
+    for (int j = 0; j < k; ++j) mx = fabs(xv[j]) > mx ? fabs(xv[j]) : mx;
+    const double p2 = __longlong_as_double(__double_as_longlong(mx) & 0x7ff0000000000000ll);
+    const double sc2 = 1.0 / p2;
+    for (int j = 0; j < k; ++j) s[j] = xv[j] * sc2;
+  }
+  int jm = 0;
+  for (int j = 1; j < k; ++j)
+    if (fabs(s[j]) > fabs(s[jm])) jm = j;
+  const double sg = s[jm] < 0.0 ? -1.0 : 1.0;
+  for (int j = 0; j < k; ++j) sc->s[j] = sg < 0.0 ? -s[j] : s[j];
+  sc->k = k;
+}
+
+// ---------------------------------------------------------------- Lanczos pass 2
+// Step j (Alg. 2 line 13 "regenerate v_2..v_i and form sum"): regenerate w_{j+1}
+// bitwise as in pass 1, v_{j+1} = w_{j+1} / rho_j, x += s_{j+1} v_{j+1}.
+__global__ void __launch_bounds__(kBlock) k_lanczos_c(Csr C, const double *__restrict__ d,
+                                                      const double *__restrict__ Xj, const double *Xjm1,
+                                                      double *Xjp1, double *__restrict__ x, int nl, long long rb,
+                                                      int j, const DevScalars *__restrict__ sc) {
+  if (j >= sc->k) return;  // sc->k holds the effective k after k_tridiag
+  const double den = sc->rho[j - 1];
+  const double denm = j >= 2 ? sc->rho[j - 2] : 1.0;
+  const double om = sc->om[j - 1];
+  const double rhoj = sc->rho[j];
+  const double s1 = sc->s[0], sj1 = sc->s[j];
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double vj = Xj[rb + r] / den;
+    double s = d[r] * vj;
+    const int e0 = C.rp[r], e1 = C.rp[r + 1];
+    for (int e = e0; e < e1; ++e) s = fma(C.val[e], __ldg(&Xj[C.col[e]]) / den, s);
+    double w = fma(-om, vj, s);
+    if (j >= 2) w = fma(-den, Xjm1[rb + r] / denm, w);
+    Xjp1[rb + r] = w;
+    const double vn = w / rhoj;
+    const double xr = j == 1 ? s1 * vj : x[rb + r];
+    x[rb + r] = fma(sj1, vn, xr);
+  }
+}
+
+// ||x||^2 (exact); k == 1 case: x = s_1 v_1.
+__global__ void __launch_bounds__(kBlock) k_norm_x(const double *__restrict__ g, double *__restrict__ x, int nl,
+                                                   long long rb, XSlot *slot, DevScalars *sc, int finalize) {
+  const bool k1 = sc->k == 1;
+  const double s1 = sc->s[0], den = sc->rho[0];
+  XAcc acc[1];
+  xacc_zero(acc[0]);
+  int err = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    double xr;
+    if (k1) { xr = s1 * (g[rb + r] / den); x[rb + r] = xr; }
+    else xr = x[rb + r];
+    xacc_add(acc[0], xr * xr, err);
+  }
+  if (commit_and_ticket<1>(acc, slot, err, sc) && threadIdx.x == 0 && finalize) {
+    __threadfence();
+    sc->nu_x = sqrt(slot_take(slot, 0));
+    slot->counter = 0;
+  }
+}
+
+// Monitor matvec: v = x / ||x|| (written), xi = v.(D v), c = v.(C v), ||v||^2 (exact).
+// (eqn 5.1 PAPER.md:1382; objective tracker PAPER.md:1553; tau PAPER.md:3224.)
+__global__ void __launch_bounds__(kBlock) k_monitor(Csr C, const double *__restrict__ d,
+                                                    const double *__restrict__ cdiag, const double *__restrict__ x,
+                                                    double *__restrict__ v, int nl, long long rb, XSlot *slot,
+                                                    DevScalars *sc, int finalize) {
+  const double nu = sc->nu_x;
+  XAcc acc[3];
+  xacc_zero(acc[0]);
+  xacc_zero(acc[1]);
+  xacc_zero(acc[2]);
+  int err = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double vr = x[rb + r] / nu;
+    v[r] = vr;
+    double s1 = d[r] * vr, s2 = cdiag[r] * vr;
+    const int e0 = C.rp[r], e1 = C.rp[r + 1];
+    for (int e = e0; e < e1; ++e) {
+      const double xc = __ldg(&x[C.col[e]]) / nu;
+      const double m = C.val[e];
+      s1 = fma(m, xc, s1);
+      s2 = fma(m, xc, s2);
+    }
+    xacc_add(acc[0], vr * s1, err);
+    xacc_add(acc[1], vr * s2, err);
+    xacc_add(acc[2], vr * vr, err);
+  }
+  if (commit_and_ticket<3>(acc, slot, err, sc) && threadIdx.x == 0 && finalize) {
+    __threadfence();
+    sc->xi = slot_take(slot, 0);
+    sc->c = slot_take(slot, 1);
+    sc->vv = slot_take(slot, 2);
+    slot->counter = 0;
+  }
+}
+
+// ---------------------------------------------------------------- primal / dual / sketch
+struct IterArgs {
+  long long t;
+  int q;
+  double eta, one_m_eta, alpha, b, beta0, sq, beta_next;
+};
+
+__device__ __forceinline__ double gamma_rule(const IterArgs &A, double nz) {
+  // eqn:sketchy-cgal-dual-step with ||A||^2 = 1 (CAC-6)
+  if (nz == 0.0) return A.beta0;
+  double num = 4.0 * A.alpha;
+  num = num * A.alpha;
+  num = num * A.beta0;
+  const double den = ((double)(A.t + 1) * A.sq) * nz;
+  const double g = num / den;
+  return g < A.beta0 ? g : A.beta0;
+}
+
+// z <- (1-eta) z + eta alpha (v o v) (Alg. 4 line 8, primitive 3), ||z - b||^2 (exact),
+// per-block partials of g = v^T Omega (fp64, fixed tree; off the feedback path).
+__global__ void __launch_bounds__(kBlock) k_primal(const double *__restrict__ v, double *__restrict__ z,
+                                                   const double *__restrict__ Om, int nl, int R, IterArgs A,
+                                                   double *__restrict__ gpart, XSlot *slot, DevScalars *sc,
+                                                   scg_iter_rec *log, int finalize) {
+  __shared__ double red[kBlock / 32][16];
+  XAcc acc[1];
+  xacc_zero(acc[0]);
+  int err = 0;
+  const double ea = A.eta * A.alpha;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double vr = v[r];
+    const double h = A.alpha * (vr * vr);
+    const double zr = fma(A.eta, h, A.one_m_eta * z[r]);
+    z[r] = zr;
+    const double e = zr - A.b;
+    xacc_add(acc[0], e * e, err);
+  }
+  (void)ea;
+  // g partials, 16 columns at a time
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int kc = 0; kc < R; kc += 16) {
+    double gp[16];
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) gp[kk] = 0.0;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+      const double vr = v[r];
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk)
+        if (kc + kk < R) gp[kk] = fma(vr, Om[(long long)(kc + kk) * nl + r], gp[kk]);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double t = gp[kk];
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+      if (lane == 0) red[warp][kk] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < 16 && kc + (int)threadIdx.x < R) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w][threadIdx.x];
+      gpart[(long long)blockIdx.x * R + kc + threadIdx.x] = t;
+    }
+    __syncthreads();
+  }
+  if (commit_and_ticket<1>(acc, slot, err, sc) && finalize) {
+    __shared__ double gsum[kMaxR];
+    // sum block partials in a fixed order: thread k sums column k over blocks
+    if (threadIdx.x < R) {
+      double t = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(&gpart[(long long)b * R + threadIdx.x]);
+      gsum[threadIdx.x] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < R) sc->gk[threadIdx.x] = gsum[threadIdx.x];
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const double nz = slot_take(slot, 0);
+      slot->counter = 0;
+      sc->nz = nz;
+      sc->gamma = gamma_rule(A, nz);
+      const double ea2 = A.eta * A.alpha;
+      sc->tau = fma(ea2, sc->vv, A.one_m_eta * sc->tau);
+      sc->p = fma(ea2, sc->c, A.one_m_eta * sc->p);
+      scg_iter_rec rec;
+      rec.t = A.t;
+      rec.q = A.q;
+      rec.k = sc->k;
+      rec.theta = sc->theta;
+      rec.xi = sc->xi;
+      rec.c = sc->c;
+      rec.p = sc->p;
+      rec.znorm = sqrt(nz);
+      rec.gamma = sc->gamma;
+      rec.tau = sc->tau;
+      log[A.t - 1] = rec;
+    }
+  }
+}
+
+// y <- y + gamma (z - b) (Alg. 4 line 9); d for t+1; S <- (1-eta) S + eta alpha v g^T
+// (Alg. 4 line 10); next start vector g_{t+1} and ||g_{t+1}||^2 (exact).
+__global__ void __launch_bounds__(kBlock) k_dual_sketch(const double *__restrict__ z, double *__restrict__ y,
+                                                        double *__restrict__ d, const double *__restrict__ cdiag,
+                                                        const double *__restrict__ v, double *__restrict__ S,
+                                                        double *__restrict__ g, int nl, long long rb, int R,
+                                                        IterArgs A, uint64_t seed, XSlot *slot, DevScalars *sc,
+                                                        int finalize) {
+  __shared__ double ck[kMaxR];
+  const double gam = sc->gamma;
+  if (threadIdx.x < R) ck[threadIdx.x] = (A.eta * A.alpha) * sc->gk[threadIdx.x];
+  __syncthreads();
+  XAcc acc[1];
+  xacc_zero(acc[0]);
+  int err = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double e = z[r] - A.b;
+    const double yr = fma(gam, e, y[r]);
+    y[r] = yr;
+    d[r] = fma(A.beta_next, e, yr) + cdiag[r];
+    const double vr = v[r];
+    for (int kk = 0; kk < R; ++kk) {
+      double *Sp = S + (long long)kk * nl + r;
+      *Sp = fma(ck[kk], vr, A.one_m_eta * *Sp);
+    }
+    const double gv = scg_lanczos_start(seed, A.t + 1, rb + r);
+    g[rb + r] = gv;
+    xacc_add(acc[0], gv * gv, err);
+  }
+  if (commit_and_ticket<1>(acc, slot, err, sc) && threadIdx.x == 0 && finalize) {
+    __threadfence();
+    sc->rho[0] = sqrt(slot_take(slot, 0));
+    slot->counter = 0;
+    sc->brk = 0;
+    sc->k = 0;
+  }
+}
+
+// ---------------------------------------------------------------- one-shot kernels
+// out = (A + beta B) M   (n x R times R x R), row-wise; M in shared memory.
+__global__ void k_rowmat(double *__restrict__ out, const double *__restrict__ A, const double *__restrict__ B,
+                         double beta, const double *__restrict__ M, int nl, int R) {
+  __shared__ double Ms[kMaxR * kMaxR];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Ms[e] = M[e];
+  __syncthreads();
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    double row[kMaxR];
+    for (int i = 0; i < R; ++i) {
+      double a = A[(long long)i * nl + r];
+      if (B) a = fma(beta, B[(long long)i * nl + r], a);
+      row[i] = a;
+    }
+    for (int j = 0; j < R; ++j) {
+      double s = 0.0;
+      for (int i = 0; i < R; ++i) s = fma(row[i], Ms[i * R + j], s);  // M row-major [i][j]
+      out[(long long)j * nl + r] = s;
+    }
+  }
+}
+
+// partial[pair][block] of column dot products A[:,i]^T B[:,j]  (pair = i*R + j).
+__global__ void k_colpair(const double *__restrict__ A, const double *__restrict__ B, int nl, int R,
+                          double *__restrict__ partial) {
+  __shared__ double red[kBlock / 32];
+  const int pair = blockIdx.y;
+  const int i = pair / R, j = pair % R;
+  const double *a = A + (long long)i * nl, *b = B + (long long)j * nl;
+  double s = 0.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) s = fma(a[r], b[r], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    partial[(long long)pair * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+// Per-column quantities of the reconstruction, partial sums per block:
+//   which 0: u_k^T L u_k  (objective)          partial[k][block]
+//   which 1: cut weight of sgn(U[:,k])          partial[k][block]
+//   which 2: sum_r (diag(X^)_r - 1)^2 with Lam  partial[0][block]
+__global__ void k_colstats(const int *__restrict__ rp, const int *__restrict__ col, const double *__restrict__ w,
+                           const double *__restrict__ ldiag, const double *__restrict__ U, const double *__restrict__ Ufull,
+                           const double *__restrict__ lam, int nl, long long rb, long long nglob, int R, int which,
+                           double *__restrict__ partial) {
+  __shared__ double red[kBlock / 32];
+  const int kcol = blockIdx.y;
+  double s = 0.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    if (which == 0) {
+      const double ur = U[(long long)kcol * nl + r];
+      double lu = ldiag[r] * ur;
+      for (int e = rp[r]; e < rp[r + 1]; ++e) lu = fma(-w[e], Ufull[(long long)kcol * nglob + col[e]], lu);
+      s = fma(ur, lu, s);
+    } else if (which == 1) {
+      const bool sr = U[(long long)kcol * nl + r] >= 0.0;
+      const long long gr = rb + r;
+      for (int e = rp[r]; e < rp[r + 1]; ++e) {
+        const int c = col[e];
+        if (c > gr) {
+          const bool sc_ = Ufull[(long long)kcol * nglob + c] >= 0.0;
+          if (sr != sc_) s += w[e];
+        } else if (c < rb || c >= rb + nl) {
+          // edge to a lower row owned by another rank: counted by that rank
+        }
+      }
+    } else {
+      double dx = 0.0;
+      for (int k = 0; k < R; ++k) {
+        const double u = U[(long long)k * nl + r];
+        dx = fma(lam[k], u * u, dx);
+      }
+      const double e = dx - 1.0;
+      s = fma(e, e, s);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) t += red[ww];
+    partial[(long long)kcol * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+// y = D x for the current d (diagnostics; same chain order as the Lanczos kernels)
+__global__ void k_apply_d(Csr C, const double *__restrict__ d, const double *__restrict__ X, int nl, long long rb,
+                          double *__restrict__ y) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    double s = d[r] * X[rb + r];
+    for (int e = C.rp[r]; e < C.rp[r + 1]; ++e) s = fma(C.val[e], X[C.col[e]], s);
+    y[r] = s;
+  }
+}
+
+}  // namespace scg

@@ -1,0 +1,134 @@
+// xsum.cuh -- exact, order-independent global sums on the GPU (DESIGN.md CAC-2).
+//
+// Definition (CAC-2): for rounded fp64 summands p_r,
+//   xsum(p) = RNE( sum_r Q(p_r) ),  Q(p) = p truncated toward zero to a multiple of 2^-200,
+// with |p_r| < 2^100 (else a sticky range error).  The sum is carried exactly as a
+// signed big integer in base 2^32 ("digits"), 10 int64 limbs per accumulator, so
+// partial sums from any thread, block or GPU combine with plain integer adds
+// (warp shuffles, shared memory, global atomics, NCCL int64 all-reduce) and the
+// result is bitwise independent of the reduction tree and the GPU count.
+//
+// Why exact sums: Alg. 2 runs Lanczos without
+// reorthogonalization, which amplifies any rounding difference (SURVEY.md
+// Appendix A), so the dot products on the feedback path must not depend on the
+// summation order.
+#pragma once
+#include <cstdint>
+
+namespace scg {
+
+constexpr int kLimbs = 10;       // 10 x 32-bit digits (int64 carry-save): LSB 2^-200
+constexpr int kLsbExp = -200;
+
+struct XAcc {
+  long long d[kLimbs];
+};
+
+__device__ __forceinline__ void xacc_zero(XAcc &a) {
+#pragma unroll
+  for (int i = 0; i < kLimbs; ++i) a.d[i] = 0;
+}
+
+// Add the double p exactly (after Q).  err is set for |p| >= 2^100 or non-finite p.
+__device__ __forceinline__ void xacc_add(XAcc &a, double p, int &err) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(p);
+  if ((b << 1) == 0ull) return;  // +-0
+  int e = (int)((b >> 52) & 0x7ffull);
+  if (e >= 1123) { err = 1; return; }  // |p| >= 2^100, inf, nan
+  unsigned long long m = b & 0x000fffffffffffffull;
+  if (e) m |= 0x0010000000000000ull; else e = 1;
+  // p = m 2^(e-1075); position of the mantissa LSB relative to 2^-200
+  int s = e - 1075 - kLsbExp;
+  if (s < 0) {
+    int sh = -s;
+    m = sh >= 64 ? 0ull : (m >> sh);  // Q: truncation toward zero
+    s = 0;
+    if (!m) return;
+  }
+  const int q = s >> 5, r = s & 31;  // q <= 7 because e <= 1122
+  const unsigned int d0 = (unsigned int)(m << r);
+  const unsigned int d1 = r ? (unsigned int)(m >> (32 - r)) : (unsigned int)(m >> 32);
+  const unsigned int d2 = r ? (unsigned int)(m >> (64 - r)) : 0u;
+  long long s0 = (long long)d0, s1 = (long long)d1, s2 = (long long)d2;
+  if (b >> 63) { s0 = -s0; s1 = -s1; s2 = -s2; }
+  switch (q) {  // static register indices (no local-memory array)
+    case 0: a.d[0] += s0; a.d[1] += s1; a.d[2] += s2; break;
+    case 1: a.d[1] += s0; a.d[2] += s1; a.d[3] += s2; break;
+    case 2: a.d[2] += s0; a.d[3] += s1; a.d[4] += s2; break;
+    case 3: a.d[3] += s0; a.d[4] += s1; a.d[5] += s2; break;
+    case 4: a.d[4] += s0; a.d[5] += s1; a.d[6] += s2; break;
+    case 5: a.d[5] += s0; a.d[6] += s1; a.d[7] += s2; break;
+    case 6: a.d[6] += s0; a.d[7] += s1; a.d[8] += s2; break;
+    default: a.d[7] += s0; a.d[8] += s1; a.d[9] += s2; break;
+  }
+}
+
+// bits [lo, lo+cnt) (cnt <= 64) of the magnitude held in 32-bit digits mag[0..nd)
+__device__ __forceinline__ unsigned long long xs_bits(const unsigned int *mag, int nd, int lo, int cnt) {
+  const int di = lo >> 5, off = lo & 31;
+  unsigned int w0 = (di >= 0 && di < nd) ? mag[di] : 0u;
+  unsigned int w1 = (di + 1 >= 0 && di + 1 < nd) ? mag[di + 1] : 0u;
+  unsigned int w2 = (di + 2 >= 0 && di + 2 < nd) ? mag[di + 2] : 0u;
+  unsigned __int128 w = ((unsigned __int128)w2 << 64) | ((unsigned __int128)w1 << 32) | (unsigned __int128)w0;
+  unsigned long long out = (unsigned long long)(w >> off);
+  return cnt >= 64 ? out : (out & ((1ull << cnt) - 1ull));
+}
+
+// true iff any of the bits [0, hi) is set
+__device__ __forceinline__ bool xs_any_below(const unsigned int *mag, int nd, int hi) {
+  const int full = hi >> 5;
+  for (int i = 0; i < full && i < nd; ++i)
+    if (mag[i]) return true;
+  const int rem = hi & 31;
+  if (rem && full < nd && (mag[full] & ((1u << rem) - 1u))) return true;
+  return false;
+}
+
+// Round the exact value held in limbs to the nearest double (ties to even).
+__device__ double xacc_round(const long long *limbs) {
+  long long d[kLimbs];
+  for (int i = 0; i < kLimbs; ++i) d[i] = limbs[i];
+  // carry-normalize digits 0..8 into [0, 2^32)
+  for (int i = 0; i < kLimbs - 1; ++i) {
+    long long c = d[i] >> 32;  // arithmetic shift = floor division
+    d[i] -= c * 4294967296ll;
+    d[i + 1] += c;
+  }
+  bool neg = d[kLimbs - 1] < 0;
+  if (neg) {  // negate every limb and renormalize: value becomes non-negative
+    for (int i = 0; i < kLimbs; ++i) d[i] = -d[i];
+    for (int i = 0; i < kLimbs - 1; ++i) {
+      long long c = d[i] >> 32;
+      d[i] -= c * 4294967296ll;
+      d[i + 1] += c;
+    }
+  }
+  constexpr int ND = kLimbs + 1;
+  unsigned int mag[ND];
+  for (int i = 0; i < kLimbs - 1; ++i) mag[i] = (unsigned int)d[i];
+  mag[kLimbs - 1] = (unsigned int)((unsigned long long)d[kLimbs - 1] & 0xffffffffull);
+  mag[kLimbs] = (unsigned int)((unsigned long long)d[kLimbs - 1] >> 32);
+  int top = -1;
+  for (int i = ND - 1; i >= 0; --i)
+    if (mag[i]) { top = i; break; }
+  if (top < 0) return 0.0;
+  const int B = top * 32 + (31 - __clz(mag[top]));  // highest set bit
+  double res;
+  if (B <= 52) {
+    unsigned long long M = xs_bits(mag, ND, 0, B + 1);
+    res = (double)M * 0x1p-200;  // exact: M < 2^53, result normal
+  } else {
+    const int shift = B - 52;  // bits dropped
+    unsigned long long keep = xs_bits(mag, ND, shift, 53);
+    unsigned long long rbit = xs_bits(mag, ND, shift - 1, 1);
+    const bool sticky = xs_any_below(mag, ND, shift - 1);
+    if (rbit && (sticky || (keep & 1ull))) keep += 1ull;
+    // value = keep * 2^(shift - 200); build the power of two from its exponent bits
+    const int ex = shift + kLsbExp;  // in [-147, 160]
+    const double p2 = __longlong_as_double((long long)(ex + 1023) << 52);
+    res = (double)keep * p2;
+  }
+  return neg ? -res : res;
+}
+
+}  // namespace scg

@@ -1,0 +1,163 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar: the feedback path (theta_t, k_t, z, y, d, v) is
+bitwise identical at every t; off-path quantities (S, xi, c, p) agree to
+rounding; after T the reconstruction-based objective and feasibility agree to
+1e-6 relative (BASELINE.json north_star) and the rounded cut on configs[0] is
+identical.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import scg_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_pair(gpu, L, R, T, seed, scale=True):
+    g = gpu.SketchyCGAL(L, R=R, seed=seed, scale=scale)
+    g.step(T)
+    o = oracle.Oracle(L, R, seed=seed, scale=scale, logcap=T)
+    o.step(T)
+    return g, o
+
+
+def _assert_trajectory(g, o, T):
+    gl, ol = g.iter_log(), o.log
+    assert gl.shape == (T, 10)
+    np.testing.assert_array_equal(gl[:, 0:3], ol[:, 0:3])          # t, q, k
+    np.testing.assert_array_equal(gl[:, 3], ol[:, 3])              # theta (Ritz) bitwise
+    np.testing.assert_array_equal(gl[:, 8], ol[:, 8])              # gamma bitwise
+    np.testing.assert_array_equal(gl[:, 7], ol[:, 7])              # ||z - b|| bitwise
+    np.testing.assert_allclose(gl[:, 4], ol[:, 4], rtol=1e-13, atol=0)  # xi
+    np.testing.assert_allclose(gl[:, 5:7], ol[:, 5:7], rtol=1e-13, atol=0)  # c, p
+    np.testing.assert_array_equal(g.state("z"), o.z)
+    np.testing.assert_array_equal(g.state("y"), o.y)
+    np.testing.assert_array_equal(g.state("v"), o.v)
+    np.testing.assert_array_equal(g.state("Omega"), o.Omega)
+    S_o = o.S
+    np.testing.assert_allclose(g.state("S"), S_o, rtol=0, atol=1e-13 * np.abs(S_o).max())
+
+
+def test_config0_full_trajectory_and_cut(gpu):
+    """configs[0] (ER n=800, R=10, T=1000, seed 0): every iterate, the objective and the cut."""
+    L = si.laplacian("c0")
+    T = 1000
+    g, o = _run_pair(gpu, L, 10, T, seed=0)
+    _assert_trajectory(g, o, T)
+    U, lam, err = g.reconstruct()
+    Uo, lam_o, err_o = oracle.nystrom_reconstruct(o.S, o.Omega, o.tau)
+    unit = L.n / o.alpha
+    lam_tc = oracle.trace_correct(lam_o, o.alpha) * unit
+    np.testing.assert_allclose(lam, lam_tc, rtol=1e-9)
+    np.testing.assert_allclose(err, err_o * unit, rtol=1e-6, atol=1e-9 * L.n)
+    obj = g.objective()
+    obj_o = oracle.objective_hat(L, Uo, lam_tc)
+    assert abs(obj[0] - o.implicit_objective()) <= 1e-12 * abs(obj[0])
+    assert abs(obj[1] - obj_o) <= 1e-6 * abs(obj_o)
+    fz = g.feasibility()
+    f_o = oracle.feasibility_hat(Uo, lam_tc)
+    assert abs(fz[0] - o.implicit_infeasibility()) <= 1e-10 * fz[0]
+    assert abs(fz[1] - f_o[0]) <= 1e-6 * f_o[0] and abs(fz[2] - f_o[1]) <= 1e-6 * f_o[1]
+    chi, w = g.round()
+    chi_o, w_o, _ = oracle.round_cut(L, Uo)
+    np.testing.assert_array_equal(chi, chi_o)
+    assert w == w_o
+
+
+def test_config1_trajectory_signed_weights(gpu):
+    """configs[1] shape (torus, +-1 weights), first 300 iterations bitwise."""
+    L = si.laplacian("c1")
+    g, o = _run_pair(gpu, L, 10, 300, seed=1)
+    _assert_trajectory(g, o, 300)
+
+
+def test_unscaled_variant(gpu):
+    L = si.laplacian("c0")
+    g, o = _run_pair(gpu, L, 5, 60, seed=3, scale=False)
+    _assert_trajectory(g, o, 60)
+
+
+def test_breakdown_complete_graph(gpu):
+    """K_8: D_1 has two eigenvalues -> invariant subspace after 2 steps (Alg. 2 line 8)."""
+    n = 8
+    i, j = np.triu_indices(n, 1)
+    L = si.laplacian_from_edges(n, i, j, np.ones(len(i)))
+    g, o = _run_pair(gpu, L, 3, 25, seed=2)
+    assert o.log[0, 2] == 2 and o.log[0, 1] == 3  # k = 2 < q_1 = ceil(ln 8) = 3
+    _assert_trajectory(g, o, 25)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 33, 257, 1000])
+def test_small_and_ragged_sizes(gpu, n):
+    rng = np.random.default_rng(n)
+    i = np.arange(n - 1)
+    j = i + 1  # a path keeps the graph connected
+    extra = rng.integers(0, n, size=(2 * n, 2))
+    extra = extra[extra[:, 0] != extra[:, 1]]
+    i = np.concatenate([i, extra[:, 0]])
+    j = np.concatenate([j, extra[:, 1]])
+    w = rng.uniform(0.5, 1.5, size=len(i))
+    L = si.laplacian_from_edges(n, i, j, w)
+    R = min(4, n)
+    g, o = _run_pair(gpu, L, R, 40, seed=n)
+    _assert_trajectory(g, o, 40)
+
+
+def test_isolated_vertices_and_heavy_row(gpu):
+    """A star (one row of degree n-50) plus isolated vertices: ragged rows, zero rows."""
+    n = 3000
+    i = np.zeros(n - 50, dtype=np.int64)
+    j = np.arange(1, n - 49)
+    L = si.laplacian_from_edges(n, i, j, np.ones(len(i)))
+    g, o = _run_pair(gpu, L, 5, 30, seed=9)
+    _assert_trajectory(g, o, 30)
+
+
+def test_steps_resume_equals_single_call(gpu):
+    L = si.laplacian("c0")
+    a = gpu.SketchyCGAL(L, R=4, seed=5)
+    a.step(7)
+    a.step(13)
+    b = gpu.SketchyCGAL(L, R=4, seed=5)
+    b.step(20)
+    np.testing.assert_array_equal(a.iter_log(), b.iter_log())
+    np.testing.assert_array_equal(a.state("y"), b.state("y"))
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_full_size_apply_D_bitwise(gpu, cfg):
+    """BASELINE sizes: every row of D x (the SpMV of the Lanczos kernels) equals the oracle's row chain."""
+    L = si.laplacian(cfg)
+    c = si.CONFIGS[cfg]
+    g = gpu.SketchyCGAL(L, R=c["R"], seed=c["seed"])
+    g.step(1)
+    x = si.normals(123, 7, 0, 0, L.n)
+    y = g.apply_D(x)
+    # oracle row chains with the GPU-independent C~ (built by the oracle) and the same d
+    o = oracle.Oracle(L, 1, seed=c["seed"], logcap=0)
+    rows = np.repeat(np.arange(L.n, dtype=np.int64), np.diff(L.row_ptr))
+    off = L.col != rows
+    rp = np.zeros(L.n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows[off], minlength=L.n), out=rp[1:])
+    m = (-L.val[off]) / o.nrmL
+    d = g.state("d")
+    y_o = oracle.apply(L.n, rp, L.col[off], m, d, x)
+    np.testing.assert_array_equal(y, y_o)
+    np.testing.assert_array_equal(g.state("cdiag"), o.cdiag)
+    z = g.state("z")
+    assert abs(z.sum() - 1.0) < 1e-12  # tr X_2 = alpha
+    del o
+
+
+def test_config2_first_iterations_bitwise(gpu):
+    L = si.laplacian("c2")
+    g, o = _run_pair(gpu, L, 10, 3, seed=2)
+    _assert_trajectory(g, o, 3)
+
+
+def test_config3_first_iteration_bitwise(gpu):
+    L = si.laplacian("c3")
+    g, o = _run_pair(gpu, L, 10, 1, seed=3)
+    _assert_trajectory(g, o, 1)
