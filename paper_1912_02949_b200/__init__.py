@@ -18,7 +18,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_HERE)
 LIB_DIR = os.path.join(_HERE, "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libsketchycgal.so")
+LIB_PATH = os.environ.get("SCG_LIB") or os.path.join(LIB_DIR, "libsketchycgal.so")
 SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("sketchycgal.cu", "kernels.cuh", "xsum.cuh")]
 HEADERS = [os.path.join(ROOT, "include", "sketchycgal.h"), os.path.join(ROOT, "scg_inputs", "include", "scg_rng.h")]
 
@@ -43,8 +43,8 @@ def _nccl_paths():
     return None, None
 
 
-def nvcc_cmd(out: str) -> list[str]:
-    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
+def nvcc_cmd(out: str, defines=()) -> list[str]:
+    cmd = ["nvcc", *[f"-D{d}" for d in defines], "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
            "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
            os.path.join(_HERE, "csrc", "sketchycgal.cu"), "-o", out]
     inc, lib = _nccl_paths()

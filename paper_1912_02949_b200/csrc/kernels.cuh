@@ -47,33 +47,185 @@ struct Csr {
   const double *val;
 };
 
-// ---------------------------------------------------------------- block reduction
-template <int NS>
-__device__ __forceinline__ bool commit_and_ticket(XAcc (&acc)[NS], XSlot *slot, int err, DevScalars *sc) {
-  __shared__ long long sm[NS][kLimbs][kBlock / 32];
-  __shared__ int s_last;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// ---------------------------------------------------------------- row engine
+// Rows with at most kLongRow off-diagonal entries are "short": one thread owns a
+// row and runs its sequential CAC-3 chain, loading kChunk entries (col, val, then
+// the gathered x[col]) at a time with all loads of a chunk in flight, and two rows
+// per thread in flight (memory-level parallelism for the HBM-bound SpMV).  Longer
+// rows are "long": a warp loads 32 entries per round (coalesced) and lane 0 runs
+// the chain; long rows are listed at init (longest first) and taken by the first
+// warps of the grid so they start early.
+#ifndef SCG_RPT
+#define SCG_RPT 1
+#endif
+#ifndef SCG_CH
+#define SCG_CH 4
+#endif
+#ifndef SCG_MINB
+#define SCG_MINB 4
+#endif
+constexpr int kLongRow = 32;
+constexpr int kChunk = SCG_CH;   // entries of a row loaded per round
+constexpr int kRpt = SCG_RPT;    // rows per thread in flight
+
+struct Rows {
+  const int *longrows;  // local ids of long rows
+  int nlong;
+};
+
+template <int NC>
+struct RowOut {
+  int r;        // local row
+  double xr;    // x_r (own entry of the gathered vector, divided by den)
+  double s[NC]; // chain results
+};
+
+// Chains of one long row by a warp; result valid in lane 0.
+template <int NC>
+__device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double *__restrict__ X, double den,
+                                               const double *__restrict__ diag0, const double *__restrict__ diag1,
+                                               long long rb, RowOut<NC> &o) {
+  const int lane = threadIdx.x & 31;
+  const int e0 = __ldg(&C.rp[r]), e1 = __ldg(&C.rp[r + 1]);
+  o.r = r;
+  o.xr = X[rb + r] / den;
+  o.s[0] = diag0[r] * o.xr;
+  if (NC > 1) o.s[NC - 1] = diag1[r] * o.xr;
+  int e = e0 + lane;
+  int cn = e < e1 ? __ldg(&C.col[e]) : 0;
+  double mn = e < e1 ? __ldg(&C.val[e]) : 0.0;
+  double xn = e < e1 ? __ldg(&X[cn]) : 0.0;
+  for (int base = e0; base < e1; base += 32) {
+    const int cnt = min(32, e1 - base);
+    const double m = mn, x = xn / den;
+    // prefetch the next round before running this round's chain
+    e = base + 32 + lane;
+    if (e < e1) { cn = __ldg(&C.col[e]); mn = __ldg(&C.val[e]); xn = __ldg(&X[cn]); }
+    for (int j = 0; j < cnt; ++j) {
+      const double mj = __shfl_sync(0xffffffffu, m, j);
+      const double xj = __shfl_sync(0xffffffffu, x, j);
 #pragma unroll
-  for (int s = 0; s < NS; ++s)
-#pragma unroll
-    for (int i = 0; i < kLimbs; ++i) {
-      long long v = acc[s].d[i];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-      if (lane == 0) sm[s][i][warp] = v;
+      for (int c = 0; c < NC; ++c) o.s[c] = fma(mj, xj, o.s[c]);
     }
-  if (__syncthreads_or(err) && threadIdx.x == 0) atomicOr(&sc->err, 1);
-  if (warp == 0) {
+  }
+}
+
+// Visit every row of this rank once: epi(RowOut) is called by the owning thread
+// (short rows) or by lane 0 of the owning warp (long rows).
+template <int NC, class Epi>
+__device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
+                                          const double *__restrict__ diag0, const double *__restrict__ diag1,
+                                          long long rb, int nl, Epi &epi) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int w = gw; w < RL.nlong; w += nw) {
+    RowOut<NC> o;
+    long_row_chain<NC>(C, RL.longrows[w], X, den, diag0, diag1, rb, o);
+    if (lane == 0) epi(o);
+  }
+  const int stride = gridDim.x * blockDim.x;
+  for (int base = blockIdx.x * blockDim.x + threadIdx.x; base < nl; base += kRpt * stride) {
+    int e0[kRpt], e1[kRpt];
+    bool act[kRpt];
+    RowOut<NC> o[kRpt];
 #pragma unroll
-    for (int s = 0; s < NS; ++s)
-#pragma unroll
-      for (int i = 0; i < kLimbs; ++i) {
-        long long v = lane < (int)(blockDim.x >> 5) ? sm[s][i][lane] : 0ll;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        if (lane == 0 && v != 0)
-          atomicAdd(reinterpret_cast<unsigned long long *>(&slot->limbs[s][i]), (unsigned long long)v);
+    for (int u = 0; u < kRpt; ++u) {
+      const int r = base + u * stride;
+      act[u] = false;
+      if (r < nl) {
+        e0[u] = __ldg(&C.rp[r]);
+        e1[u] = __ldg(&C.rp[r + 1]);
+        act[u] = (e1[u] - e0[u]) <= kLongRow;
       }
+      o[u].r = r;
+    }
+    double xo[kRpt], dg0[kRpt], dg1[kRpt];
+#pragma unroll
+    for (int u = 0; u < kRpt; ++u) {
+      if (act[u]) {
+        xo[u] = X[rb + o[u].r];
+        dg0[u] = diag0[o[u].r];
+        if (NC > 1) dg1[u] = diag1[o[u].r];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kRpt; ++u) {
+      if (act[u]) {
+        o[u].xr = xo[u] / den;
+        o[u].s[0] = dg0[u] * o[u].xr;
+        if (NC > 1) o[u].s[NC - 1] = dg1[u] * o[u].xr;
+      }
+    }
+    for (int k = 0;; k += kChunk) {
+      bool more = false;
+#pragma unroll
+      for (int u = 0; u < kRpt; ++u) more |= act[u] && e0[u] + k < e1[u];
+      if (!more) break;
+      int cc[kRpt][kChunk];
+      double vv[kRpt][kChunk], xg[kRpt][kChunk];
+#pragma unroll
+      for (int u = 0; u < kRpt; ++u)
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          const int e = e0[u] + k + j;
+          if (act[u] && e < e1[u]) {
+            cc[u][j] = __ldg(&C.col[e]);
+            vv[u][j] = __ldg(&C.val[e]);
+          }
+        }
+#pragma unroll
+      for (int u = 0; u < kRpt; ++u)
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          const int e = e0[u] + k + j;
+          if (act[u] && e < e1[u]) xg[u][j] = __ldg(&X[cc[u][j]]);
+        }
+#pragma unroll
+      for (int u = 0; u < kRpt; ++u)
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          const int e = e0[u] + k + j;
+          if (act[u] && e < e1[u]) {
+            const double x = xg[u][j] / den;  // v = w / rho (Alg. 2 line 9), formed on the fly
+#pragma unroll
+            for (int c = 0; c < NC; ++c) o[u].s[c] = fma(vv[u][j], x, o[u].s[c]);
+          }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kRpt; ++u)
+      if (act[u]) epi(o[u]);
+  }
+}
+
+// ---------------------------------------------------------------- block reduction
+// Block-level exact accumulators (shared memory) for NS sums.
+template <int NS>
+struct XBlk {
+  long long l[NS][kLimbs];
+};
+
+template <int NS>
+__device__ __forceinline__ void xblk_init(XBlk<NS> &b) {
+  for (int i = threadIdx.x; i < NS * kLimbs; i += blockDim.x) (&b.l[0][0])[i] = 0;
+  __syncthreads();
+}
+
+// Flush every thread's window into the block accumulator, add the block total to
+// the global slot (exact integer atomics), and take a ticket: returns true in the
+// last block to finish (which then finalizes the slot).
+template <int NS>
+__device__ __forceinline__ bool commit_and_ticket(XWin (&acc)[NS], XBlk<NS> &blk, XSlot *slot, int err,
+                                                  DevScalars *sc) {
+  __shared__ int s_last;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) xwin_flush(acc[s], blk.l[s]);
+  if (__syncthreads_or(err) && threadIdx.x == 0) atomicOr(&sc->err, 1);
+  if ((int)threadIdx.x < NS * kLimbs) {
+    const int s = threadIdx.x / kLimbs, i = threadIdx.x % kLimbs;
+    const long long v = blk.l[s][i];
+    if (v != 0) atomicAdd(reinterpret_cast<unsigned long long *>(&slot->limbs[s][i]), (unsigned long long)v);
   }
   __threadfence();
   __syncthreads();
@@ -83,7 +235,7 @@ __device__ __forceinline__ bool commit_and_ticket(XAcc (&acc)[NS], XSlot *slot, 
 }
 
 // Called by thread 0 of the last block: read + reset slot accumulator s.
-__device__ __forceinline__ double slot_take(XSlot *slot, int s) {
+__device__ __noinline__ double slot_take(XSlot *slot, int s) {
   long long l[kLimbs];
   for (int i = 0; i < kLimbs; ++i) {
     l[i] = (long long)atomicExch(reinterpret_cast<unsigned long long *>(&slot->limbs[s][i]), 0ull);
@@ -96,13 +248,15 @@ __device__ __forceinline__ double slot_take(XSlot *slot, int s) {
 // direction) and the diagonal (scaling).
 __global__ void k_frob(const double *__restrict__ w, long long nnz, const double *__restrict__ diag, int nl,
                        XSlot *slot, DevScalars *sc, double *out) {
-  XAcc acc[1];
-  xacc_zero(acc[0]);
+  __shared__ XBlk<1> xb;
+  xblk_init<1>(xb);
+  XWin acc[1];
+  xwin_init(acc[0]);
   int err = 0;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
-  for (long long k = tid; k < nnz; k += st) xacc_add(acc[0], w[k] * w[k], err);
-  for (long long r = tid; r < nl; r += st) xacc_add(acc[0], diag[r] * diag[r], err);
-  if (commit_and_ticket<1>(acc, slot, err, sc) && threadIdx.x == 0) {
+  for (long long k = tid; k < nnz; k += st) xwin_add(acc[0], w[k] * w[k], err, xb.l[0]);
+  for (long long r = tid; r < nl; r += st) xwin_add(acc[0], diag[r] * diag[r], err, xb.l[0]);
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0) {
     __threadfence();
     *out = slot_take(slot, 0);
     slot->counter = 0;
@@ -139,15 +293,17 @@ __global__ void k_init_d(const double *__restrict__ z, const double *__restrict_
 // Lanczos start vector g = randn (Alg. 2 line 1) for iteration t and ||g||^2 (exact).
 __global__ void __launch_bounds__(kBlock) k_gen_start(double *__restrict__ g, int nl, long long rb, uint64_t seed,
                                                       long long t, XSlot *slot, DevScalars *sc, int finalize) {
-  XAcc acc[1];
-  xacc_zero(acc[0]);
+  __shared__ XBlk<1> xb;
+  xblk_init<1>(xb);
+  XWin acc[1];
+  xwin_init(acc[0]);
   int err = 0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
     const double v = scg_lanczos_start(seed, t, rb + r);
     g[rb + r] = v;
-    xacc_add(acc[0], v * v, err);
+    xwin_add(acc[0], v * v, err, xb.l[0]);
   }
-  if (commit_and_ticket<1>(acc, slot, err, sc) && threadIdx.x == 0 && finalize) {
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
     __threadfence();
     sc->rho[0] = sqrt(slot_take(slot, 0));
     slot->counter = 0;
@@ -158,24 +314,34 @@ __global__ void __launch_bounds__(kBlock) k_gen_start(double *__restrict__ g, in
 // Step i, part A (Alg. 2 lines 4-5): a = D v_i with v_i = X_i / rho[i-1] formed on the
 // fly (Alg. 2 line 9 division), omega_i = v_i . a (exact).
 //   (D x)_r = fl(d_r x_r) then fma(C_rj, x_j, acc) over j ascending (CAC-3).
-__global__ void __launch_bounds__(kBlock) k_lanczos_a(Csr C, const double *__restrict__ d,
-                                                      const double *__restrict__ X, int nl, long long rb, int i,
-                                                      double *__restrict__ a, XSlot *slot, DevScalars *sc,
-                                                      int finalize) {
+struct EpiA {
+  double *a;
+  long long *blk;
+  XWin acc[1];
+  int err;
+  __device__ __forceinline__ void operator()(const RowOut<1> &o) {
+    a[o.r] = o.s[0];
+    xwin_add(acc[0], o.xr * o.s[0], err, blk);
+  }
+};
+
+__global__ void __launch_bounds__(kBlock, SCG_MINB) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
+                                                         const double *__restrict__ X, int nl, long long rb, int i,
+                                                         double *__restrict__ a, XSlot *slot, DevScalars *sc,
+                                                         int finalize) {
   if (sc->brk) return;
   const double den = sc->rho[i - 1];
-  XAcc acc[1];
-  xacc_zero(acc[0]);
-  int err = 0;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
-    const double xr = X[rb + r] / den;
-    double s = d[r] * xr;
-    const int e0 = C.rp[r], e1 = C.rp[r + 1];
-    for (int e = e0; e < e1; ++e) s = fma(C.val[e], __ldg(&X[C.col[e]]) / den, s);
-    a[r] = s;
-    xacc_add(acc[0], xr * s, err);
-  }
-  if (commit_and_ticket<1>(acc, slot, err, sc) && threadIdx.x == 0 && finalize) {
+  __shared__ XBlk<1> xb;
+  xblk_init<1>(xb);
+  EpiA epi;
+  epi.a = a;
+  epi.blk = xb.l[0];
+  xwin_init(epi.acc[0]);
+  epi.err = 0;
+  spmv_rows<1>(C, RL, X, den, d, nullptr, rb, nl, epi);
+  int err = epi.err;
+  XWin (&acc)[1] = epi.acc;
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
     __threadfence();
     sc->om[i - 1] = slot_take(slot, 0);
     slot->counter = 0;
@@ -195,24 +361,43 @@ __device__ __forceinline__ void fin_rho(DevScalars *sc, int i, double rho2) {
 
 // Step i, part B (Alg. 2 lines 6-7): w_{i+1} = fma(-rho_{i-1}, v_{i-1}, fma(-omega_i, v_i, a)),
 // rho_i = ||w_{i+1}|| (exact); breakdown test.  Writes the un-normalized w_{i+1}.
-__global__ void __launch_bounds__(kBlock) k_lanczos_b(const double *__restrict__ a, const double *Xi,
+__global__ void __launch_bounds__(kBlock, 4) k_lanczos_b(const double *__restrict__ a, const double *Xi,
                                                       const double *Xim1, double *Xip1, int nl, long long rb,
                                                       int i, XSlot *slot, DevScalars *sc, int finalize) {
   if (sc->brk) return;
   const double om = sc->om[i - 1];
   const double den = sc->rho[i - 1];
   const double denm = i >= 2 ? sc->rho[i - 2] : 1.0;
-  XAcc acc[1];
-  xacc_zero(acc[0]);
+  __shared__ XBlk<1> xb;
+  xblk_init<1>(xb);
+  XWin acc[1];
+  xwin_init(acc[0]);
   int err = 0;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
-    const double vi = Xi[rb + r] / den;
-    double w = fma(-om, vi, a[r]);
-    if (i >= 2) w = fma(-den, Xim1[rb + r] / denm, w);  // rho_{i-1} = rho[i-1] = den
-    Xip1[rb + r] = w;
-    xacc_add(acc[0], w * w, err);
+  const int stride = gridDim.x * blockDim.x;
+  for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < nl; r0 += 4 * stride) {
+    double av[4], xi[4], xm[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = r0 + u * stride;
+      if (r < nl) {
+        av[u] = a[r];
+        xi[u] = Xi[rb + r];
+        xm[u] = i >= 2 ? Xim1[rb + r] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = r0 + u * stride;
+      if (r < nl) {
+        const double vi = xi[u] / den;
+        double w = fma(-om, vi, av[u]);
+        if (i >= 2) w = fma(-den, xm[u] / denm, w);  // rho_{i-1} = rho[i-1] = den
+        Xip1[rb + r] = w;
+        xwin_add(acc[0], w * w, err, xb.l[0]);
+      }
+    }
   }
-  if (commit_and_ticket<1>(acc, slot, err, sc) && threadIdx.x == 0 && finalize) {
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
     __threadfence();
     fin_rho(sc, i, slot_take(slot, 0));
     slot->counter = 0;
@@ -348,28 +533,31 @@ __global__ void k_tridiag(DevScalars *sc, int q) {
 // ---------------------------------------------------------------- Lanczos pass 2
 // Step j (Alg. 2 line 13 "regenerate v_2..v_i and form sum"): regenerate w_{j+1}
 // bitwise as in pass 1, v_{j+1} = w_{j+1} / rho_j, x += s_{j+1} v_{j+1}.
-__global__ void __launch_bounds__(kBlock) k_lanczos_c(Csr C, const double *__restrict__ d,
-                                                      const double *__restrict__ Xj, const double *Xjm1,
-                                                      double *Xjp1, double *__restrict__ x, int nl, long long rb,
-                                                      int j, const DevScalars *__restrict__ sc) {
-  if (j >= sc->k) return;  // sc->k holds the effective k after k_tridiag
-  const double den = sc->rho[j - 1];
-  const double denm = j >= 2 ? sc->rho[j - 2] : 1.0;
-  const double om = sc->om[j - 1];
-  const double rhoj = sc->rho[j];
-  const double s1 = sc->s[0], sj1 = sc->s[j];
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
-    const double vj = Xj[rb + r] / den;
-    double s = d[r] * vj;
-    const int e0 = C.rp[r], e1 = C.rp[r + 1];
-    for (int e = e0; e < e1; ++e) s = fma(C.val[e], __ldg(&Xj[C.col[e]]) / den, s);
-    double w = fma(-om, vj, s);
-    if (j >= 2) w = fma(-den, Xjm1[rb + r] / denm, w);
-    Xjp1[rb + r] = w;
+struct EpiC {
+  const double *Xjm1;
+  double *Xjp1, *x;
+  long long rb;
+  int j;
+  double om, den, denm, rhoj, s1, sj1;
+  __device__ __forceinline__ void operator()(const RowOut<1> &o) {
+    const double vj = o.xr;
+    double w = fma(-om, vj, o.s[0]);
+    if (j >= 2) w = fma(-den, Xjm1[rb + o.r] / denm, w);
+    Xjp1[rb + o.r] = w;
     const double vn = w / rhoj;
-    const double xr = j == 1 ? s1 * vj : x[rb + r];
-    x[rb + r] = fma(sj1, vn, xr);
+    const double xr = j == 1 ? s1 * vj : x[rb + o.r];
+    x[rb + o.r] = fma(sj1, vn, xr);
   }
+};
+
+__global__ void __launch_bounds__(kBlock, SCG_MINB) k_lanczos_c(Csr C, Rows RL, const double *__restrict__ d,
+                                                         const double *__restrict__ Xj, const double *Xjm1,
+                                                         double *Xjp1, double *__restrict__ x, int nl, long long rb,
+                                                         int j, const DevScalars *__restrict__ sc) {
+  if (j >= sc->k) return;  // sc->k holds the effective k after k_tridiag
+  EpiC epi{Xjm1, Xjp1, x, rb, j, sc->om[j - 1], sc->rho[j - 1], j >= 2 ? sc->rho[j - 2] : 1.0, sc->rho[j],
+           sc->s[0], sc->s[j]};
+  spmv_rows<1>(C, RL, Xj, epi.den, d, nullptr, rb, nl, epi);
 }
 
 // ||x||^2 (exact); k == 1 case: x = s_1 v_1.
@@ -377,16 +565,30 @@ __global__ void __launch_bounds__(kBlock) k_norm_x(const double *__restrict__ g,
                                                    long long rb, XSlot *slot, DevScalars *sc, int finalize) {
   const bool k1 = sc->k == 1;
   const double s1 = sc->s[0], den = sc->rho[0];
-  XAcc acc[1];
-  xacc_zero(acc[0]);
+  __shared__ XBlk<1> xb;
+  xblk_init<1>(xb);
+  XWin acc[1];
+  xwin_init(acc[0]);
   int err = 0;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
-    double xr;
-    if (k1) { xr = s1 * (g[rb + r] / den); x[rb + r] = xr; }
-    else xr = x[rb + r];
-    xacc_add(acc[0], xr * xr, err);
+  const int stride = gridDim.x * blockDim.x;
+  for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < nl; r0 += 4 * stride) {
+    double xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = r0 + u * stride;
+      if (r < nl) xv[u] = k1 ? g[rb + r] : x[rb + r];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = r0 + u * stride;
+      if (r < nl) {
+        double xr = xv[u];
+        if (k1) { xr = s1 * (xr / den); x[rb + r] = xr; }
+        xwin_add(acc[0], xr * xr, err, xb.l[0]);
+      }
+    }
   }
-  if (commit_and_ticket<1>(acc, slot, err, sc) && threadIdx.x == 0 && finalize) {
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
     __threadfence();
     sc->nu_x = sqrt(slot_take(slot, 0));
     slot->counter = 0;
@@ -395,32 +597,37 @@ __global__ void __launch_bounds__(kBlock) k_norm_x(const double *__restrict__ g,
 
 // Monitor matvec: v = x / ||x|| (written), xi = v.(D v), c = v.(C v), ||v||^2 (exact).
 // (eqn 5.1 PAPER.md:1382; objective tracker PAPER.md:1553; tau PAPER.md:3224.)
-__global__ void __launch_bounds__(kBlock) k_monitor(Csr C, const double *__restrict__ d,
-                                                    const double *__restrict__ cdiag, const double *__restrict__ x,
-                                                    double *__restrict__ v, int nl, long long rb, XSlot *slot,
-                                                    DevScalars *sc, int finalize) {
-  const double nu = sc->nu_x;
-  XAcc acc[3];
-  xacc_zero(acc[0]);
-  xacc_zero(acc[1]);
-  xacc_zero(acc[2]);
-  int err = 0;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
-    const double vr = x[rb + r] / nu;
-    v[r] = vr;
-    double s1 = d[r] * vr, s2 = cdiag[r] * vr;
-    const int e0 = C.rp[r], e1 = C.rp[r + 1];
-    for (int e = e0; e < e1; ++e) {
-      const double xc = __ldg(&x[C.col[e]]) / nu;
-      const double m = C.val[e];
-      s1 = fma(m, xc, s1);
-      s2 = fma(m, xc, s2);
-    }
-    xacc_add(acc[0], vr * s1, err);
-    xacc_add(acc[1], vr * s2, err);
-    xacc_add(acc[2], vr * vr, err);
+struct EpiM {
+  double *v;
+  long long (*blk)[kLimbs];
+  XWin acc[3];
+  int err;
+  __device__ __forceinline__ void operator()(const RowOut<2> &o) {
+    v[o.r] = o.xr;
+    xwin_add(acc[0], o.xr * o.s[0], err, blk[0]);
+    xwin_add(acc[1], o.xr * o.s[1], err, blk[1]);
+    xwin_add(acc[2], o.xr * o.xr, err, blk[2]);
   }
-  if (commit_and_ticket<3>(acc, slot, err, sc) && threadIdx.x == 0 && finalize) {
+};
+
+__global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const double *__restrict__ d,
+                                                       const double *__restrict__ cdiag, const double *__restrict__ x,
+                                                       double *__restrict__ v, int nl, long long rb, XSlot *slot,
+                                                       DevScalars *sc, int finalize) {
+  const double nu = sc->nu_x;
+  __shared__ XBlk<3> xb;
+  xblk_init<3>(xb);
+  EpiM epi;
+  epi.v = v;
+  epi.blk = xb.l;
+  xwin_init(epi.acc[0]);
+  xwin_init(epi.acc[1]);
+  xwin_init(epi.acc[2]);
+  epi.err = 0;
+  spmv_rows<2>(C, RL, x, nu, d, cdiag, rb, nl, epi);
+  int err = epi.err;
+  XWin (&acc)[3] = epi.acc;
+  if (commit_and_ticket<3>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
     __threadfence();
     sc->xi = slot_take(slot, 0);
     sc->c = slot_take(slot, 1);
@@ -449,51 +656,56 @@ __device__ __forceinline__ double gamma_rule(const IterArgs &A, double nz) {
 
 // z <- (1-eta) z + eta alpha (v o v) (Alg. 4 line 8, primitive 3), ||z - b||^2 (exact),
 // per-block partials of g = v^T Omega (fp64, fixed tree; off the feedback path).
-__global__ void __launch_bounds__(kBlock) k_primal(const double *__restrict__ v, double *__restrict__ z,
+__global__ void __launch_bounds__(kBlock, 4) k_primal(const double *__restrict__ v, double *__restrict__ z,
                                                    const double *__restrict__ Om, int nl, int R, IterArgs A,
                                                    double *__restrict__ gpart, XSlot *slot, DevScalars *sc,
                                                    scg_iter_rec *log, int finalize) {
-  __shared__ double red[kBlock / 32][16];
-  XAcc acc[1];
-  xacc_zero(acc[0]);
+  __shared__ double red[kBlock / 32][kMaxR];
+  __shared__ XBlk<1> xb;
+  xblk_init<1>(xb);
+  XWin acc[1];
+  xwin_init(acc[0]);
   int err = 0;
-  const double ea = A.eta * A.alpha;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
-    const double vr = v[r];
-    const double h = A.alpha * (vr * vr);
-    const double zr = fma(A.eta, h, A.one_m_eta * z[r]);
-    z[r] = zr;
-    const double e = zr - A.b;
-    xacc_add(acc[0], e * e, err);
-  }
-  (void)ea;
-  // g partials, 16 columns at a time
+  // one warp handles 32 consecutive rows per step; lane k accumulates g_k (and g_{k+32})
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int kc = 0; kc < R; kc += 16) {
-    double gp[16];
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) gp[kk] = 0.0;
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
-      const double vr = v[r];
-#pragma unroll
-      for (int kk = 0; kk < 16; ++kk)
-        if (kc + kk < R) gp[kk] = fma(vr, Om[(long long)(kc + kk) * nl + r], gp[kk]);
+  const int nwarp = gridDim.x * (kBlock / 32);
+  double gl0 = 0.0, gl1 = 0.0;
+  for (int base = (blockIdx.x * (kBlock / 32) + warp) * 32; base < nl; base += nwarp * 32) {
+    const int r = base + lane;
+    const bool ok = r < nl;
+    const double vr = ok ? v[r] : 0.0;
+    if (ok) {
+      const double h = A.alpha * (vr * vr);
+      const double zr = fma(A.eta, h, A.one_m_eta * z[r]);
+      z[r] = zr;
+      const double e = zr - A.b;
+      xwin_add(acc[0], e * e, err, xb.l[0]);
     }
+    for (int kc = 0; kc < R; kc += 8) {
+      double p[8];
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      double t = gp[kk];
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
-      if (lane == 0) red[warp][kk] = t;
+      for (int u = 0; u < 8; ++u) p[u] = (ok && kc + u < R) ? vr * __ldg(&Om[(long long)(kc + u) * nl + r]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) p[u] += __shfl_xor_sync(0xffffffffu, p[u], o);
+        const int k = kc + u;
+        if (k < R && lane == (k & 31)) {
+          if (k < 32) gl0 += p[u]; else gl1 += p[u];
+        }
+      }
     }
-    __syncthreads();
-    if (threadIdx.x < 16 && kc + (int)threadIdx.x < R) {
-      double t = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w][threadIdx.x];
-      gpart[(long long)blockIdx.x * R + kc + threadIdx.x] = t;
-    }
-    __syncthreads();
   }
-  if (commit_and_ticket<1>(acc, slot, err, sc) && finalize) {
+  if (lane < R) red[warp][lane] = gl0;
+  if (lane + 32 < R) red[warp][lane + 32] = gl1;
+  __syncthreads();
+  if ((int)threadIdx.x < R) {
+    double t = 0.0;
+    for (int w = 0; w < kBlock / 32; ++w) t += red[w][threadIdx.x];
+    gpart[(long long)blockIdx.x * R + threadIdx.x] = t;
+  }
+  __syncthreads();
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && finalize) {
     __shared__ double gsum[kMaxR];
     // sum block partials in a fixed order: thread k sums column k over blocks
     if (threadIdx.x < R) {
@@ -530,7 +742,7 @@ __global__ void __launch_bounds__(kBlock) k_primal(const double *__restrict__ v,
 
 // y <- y + gamma (z - b) (Alg. 4 line 9); d for t+1; S <- (1-eta) S + eta alpha v g^T
 // (Alg. 4 line 10); next start vector g_{t+1} and ||g_{t+1}||^2 (exact).
-__global__ void __launch_bounds__(kBlock) k_dual_sketch(const double *__restrict__ z, double *__restrict__ y,
+__global__ void __launch_bounds__(kBlock, 3) k_dual_sketch(const double *__restrict__ z, double *__restrict__ y,
                                                         double *__restrict__ d, const double *__restrict__ cdiag,
                                                         const double *__restrict__ v, double *__restrict__ S,
                                                         double *__restrict__ g, int nl, long long rb, int R,
@@ -540,24 +752,57 @@ __global__ void __launch_bounds__(kBlock) k_dual_sketch(const double *__restrict
   const double gam = sc->gamma;
   if (threadIdx.x < R) ck[threadIdx.x] = (A.eta * A.alpha) * sc->gk[threadIdx.x];
   __syncthreads();
-  XAcc acc[1];
-  xacc_zero(acc[0]);
+  __shared__ XBlk<1> xb;
+  xblk_init<1>(xb);
+  XWin acc[1];
+  xwin_init(acc[0]);
   int err = 0;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
-    const double e = z[r] - A.b;
-    const double yr = fma(gam, e, y[r]);
-    y[r] = yr;
-    d[r] = fma(A.beta_next, e, yr) + cdiag[r];
-    const double vr = v[r];
-    for (int kk = 0; kk < R; ++kk) {
-      double *Sp = S + (long long)kk * nl + r;
-      *Sp = fma(ck[kk], vr, A.one_m_eta * *Sp);
+  const int stride = gridDim.x * blockDim.x;
+  for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < nl; r0 += 2 * stride) {
+    double zr[2], yv[2], cd[2], vr[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int r = r0 + u * stride;
+      if (r < nl) { zr[u] = z[r]; yv[u] = y[r]; cd[u] = cdiag[r]; vr[u] = v[r]; }
     }
-    const double gv = scg_lanczos_start(seed, A.t + 1, rb + r);
-    g[rb + r] = gv;
-    xacc_add(acc[0], gv * gv, err);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int r = r0 + u * stride;
+      if (r < nl) {
+        const double e = zr[u] - A.b;
+        const double yr = fma(gam, e, yv[u]);
+        y[r] = yr;
+        d[r] = fma(A.beta_next, e, yr) + cd[u];
+      }
+    }
+    for (int kc = 0; kc < R; kc += 8) {
+      double sv[2][8];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int r = r0 + u * stride;
+          if (r < nl && kc + k < R) sv[u][k] = S[(long long)(kc + k) * nl + r];
+        }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int r = r0 + u * stride;
+          if (r < nl && kc + k < R) S[(long long)(kc + k) * nl + r] = fma(ck[kc + k], vr[u], A.one_m_eta * sv[u][k]);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int r = r0 + u * stride;
+      if (r < nl) {
+        const double gv = scg_lanczos_start(seed, A.t + 1, rb + r);
+        g[rb + r] = gv;
+        xwin_add(acc[0], gv * gv, err, xb.l[0]);
+      }
+    }
   }
-  if (commit_and_ticket<1>(acc, slot, err, sc) && threadIdx.x == 0 && finalize) {
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
     __threadfence();
     sc->rho[0] = sqrt(slot_take(slot, 0));
     slot->counter = 0;
@@ -657,13 +902,16 @@ __global__ void k_colstats(const int *__restrict__ rp, const int *__restrict__ c
 }
 
 // y = D x for the current d (diagnostics; same chain order as the Lanczos kernels)
-__global__ void k_apply_d(Csr C, const double *__restrict__ d, const double *__restrict__ X, int nl, long long rb,
-                          double *__restrict__ y) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
-    double s = d[r] * X[rb + r];
-    for (int e = C.rp[r]; e < C.rp[r + 1]; ++e) s = fma(C.val[e], X[C.col[e]], s);
-    y[r] = s;
-  }
+struct EpiY {
+  double *y;
+  __device__ __forceinline__ void operator()(const RowOut<1> &o) { y[o.r] = o.s[0]; }
+};
+
+__global__ void __launch_bounds__(kBlock) k_apply_d(Csr C, Rows RL, const double *__restrict__ d,
+                                                    const double *__restrict__ X, int nl, long long rb,
+                                                    double *__restrict__ y) {
+  EpiY epi{y};
+  spmv_rows<1>(C, RL, X, 1.0, d, nullptr, rb, nl, epi);
 }
 
 }  // namespace scg

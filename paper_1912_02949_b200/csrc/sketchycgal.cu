@@ -63,7 +63,9 @@ struct scg_ctx {
   XSlot *slots = nullptr;
   scg_iter_rec *dlog = nullptr;
   int64_t log_cap = 0;
-  int grid_rows = 1, grid_primal = 1;
+  int grid_rows = 1, grid_primal = 1, grid_tiles = 1;
+  int *longrows = nullptr;
+  int nlong = 0;
   int64_t t = 0;
   int64_t launches = 0;
   // reconstruction
@@ -301,7 +303,7 @@ void sketchycgal_destroy(scg_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   void *ptrs[] = {c->rp, c->col, c->val, c->wts, c->ldiag, c->cdiag, c->d, c->z, c->y, c->a, c->v, c->g,
                   c->W0, c->W1, c->x, c->S, c->Om, c->gpart, c->U, c->tmp1, c->tmp2, c->dmat, c->partial,
-                  c->dlam, c->dscalar, c->sc, c->slots, c->dlog};
+                  c->dlam, c->dscalar, c->sc, c->slots, c->dlog, c->longrows};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (auto &p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
@@ -384,6 +386,13 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   }
   h_rp[(size_t)nl] = (int)o;
   c->nnz_off = cnt_off;
+  // long rows (kernels.cuh row engine), longest first so they start early
+  std::vector<int> h_long;
+  for (int64_t r = 0; r < nl; ++r)
+    if (h_rp[(size_t)r + 1] - h_rp[(size_t)r] > kLongRow) h_long.push_back((int)r);
+  std::stable_sort(h_long.begin(), h_long.end(), [&](int x, int y) {
+    return h_rp[(size_t)x + 1] - h_rp[(size_t)x] > h_rp[(size_t)y + 1] - h_rp[(size_t)y];
+  });
 
   // ---- device setup
   cudaError_t e0 = cudaSetDevice(device);
@@ -408,11 +417,15 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   if (!ok) return bad(SCG_ENOMEM, "device allocation");
   c->log_cap = 1024;
   if (!alloc((void **)&c->dlog, sizeof(scg_iter_rec) * c->log_cap)) return bad(SCG_ENOMEM, "log");
+  c->nlong = (int)h_long.size();
+  if (!alloc((void **)&c->longrows, sizeof(int) * h_long.size())) return bad(SCG_ENOMEM, "long rows");
 
   // grid sizes from occupancy
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_a, kBlock, 0);
   c->grid_rows = grid_for(nl, std::max(1, occ) * c->nsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_c, kBlock, 0);
+  c->grid_tiles = grid_for(std::max<int64_t>(nl / 2, (int64_t)c->nlong * 32), std::max(1, occ) * c->nsm);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_primal, kBlock, 0);
   c->grid_primal = grid_for(nl, std::max(1, occ) * c->nsm);
   if (!alloc((void **)&c->gpart, sizeof(double) * (size_t)c->grid_primal * R)) return bad(SCG_ENOMEM, "gpart");
@@ -426,6 +439,8 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   CKI(cudaMemcpyAsync(c->col, h_col.data(), sizeof(int) * cnt_off, cudaMemcpyHostToDevice, s));
   CKI(cudaMemcpyAsync(c->wts, h_w.data(), sizeof(double) * cnt_off, cudaMemcpyHostToDevice, s));
   CKI(cudaMemcpyAsync(c->ldiag, h_diag.data(), nlb, cudaMemcpyHostToDevice, s));
+  if (!h_long.empty())
+    CKI(cudaMemcpyAsync(c->longrows, h_long.data(), sizeof(int) * h_long.size(), cudaMemcpyHostToDevice, s));
   CKI(cudaMemsetAsync(c->sc, 0, sizeof(DevScalars), s));
   CKI(cudaMemsetAsync(c->slots, 0, sizeof(XSlot) * SLOT_COUNT, s));
   CKI(cudaMemsetAsync(c->z, 0, nlb, s));
@@ -490,6 +505,8 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
   const int nl = (int)c->nl;
   const long long rb = c->rb;
   Csr C{c->rp, c->col, c->val};
+  Rows TT{c->longrows, c->nlong};
+  const int GT = c->grid_tiles;
   double *Wb[2] = {c->W0, c->W1};
   for (int64_t it = 0; it < T; ++it) {
     const int64_t t = c->t + 1;
@@ -511,7 +528,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     // ---- Lanczos pass 1 (Alg. 2 lines 1-9)
     for (int i = 1; i <= q; ++i) {
       const double *Xi = (i == 1) ? c->g : Wb[i & 1];
-      launch(c, KC_LANCZOS_A, k_lanczos_a, dim3(G), dim3(kBlock), C, (const double *)c->d, Xi, nl, rb, i, c->a,
+      launch(c, KC_LANCZOS_A, k_lanczos_a, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, Xi, nl, rb, i, c->a,
              c->slots + SLOT_OM, c->sc, 1);
       if (i < q) {
         const double *Xim1 = (i == 1) ? nullptr : (i == 2 ? c->g : Wb[(i - 1) & 1]);
@@ -525,13 +542,13 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     for (int j = 1; j < q; ++j) {
       const double *Xj = (j == 1) ? c->g : Wb[j & 1];
       const double *Xjm1 = (j == 1) ? nullptr : (j == 2 ? c->g : Wb[(j - 1) & 1]);
-      launch(c, KC_LANCZOS_C, k_lanczos_c, dim3(G), dim3(kBlock), C, (const double *)c->d, Xj, Xjm1,
+      launch(c, KC_LANCZOS_C, k_lanczos_c, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, Xj, Xjm1,
              Wb[(j + 1) & 1], c->x, nl, rb, j, (const DevScalars *)c->sc);
     }
     launch(c, KC_NORM_X, k_norm_x, dim3(G), dim3(kBlock), (const double *)c->g, c->x, nl, rb,
            c->slots + SLOT_XX, c->sc, 1);
     // ---- monitors, primal, dual, sketch (Alg. 4 lines 8-10)
-    launch(c, KC_MONITOR, k_monitor, dim3(G), dim3(kBlock), C, (const double *)c->d, (const double *)c->cdiag,
+    launch(c, KC_MONITOR, k_monitor, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, (const double *)c->cdiag,
            (const double *)c->x, c->v, nl, rb, c->slots + SLOT_MON, c->sc, 1);
     launch(c, KC_PRIMAL, k_primal, dim3(c->grid_primal), dim3(kBlock), (const double *)c->v, c->z,
            (const double *)c->Om, nl, c->R, A, c->gpart, c->slots + SLOT_NZ, c->sc, c->dlog, 1);
@@ -595,7 +612,8 @@ scg_status sketchycgal_apply_D(scg_ctx *c, const double *xh, double *yh) {
   CK(cudaMalloc(&dy, sizeof(double) * c->nl));
   CK(cudaMemcpy(dx, xh, sizeof(double) * c->n, cudaMemcpyHostToDevice));
   Csr C{c->rp, c->col, c->val};
-  launch(c, KC_OTHER, k_apply_d, dim3(c->grid_rows), dim3(kBlock), C, (const double *)c->d, (const double *)dx,
+  Rows TT{c->longrows, c->nlong};
+  launch(c, KC_OTHER, k_apply_d, dim3(c->grid_tiles), dim3(kBlock), C, TT, (const double *)c->d, (const double *)dx,
          (int)c->nl, (long long)c->rb, dy);
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaMemcpy(yh, dy, sizeof(double) * c->nl, cudaMemcpyDeviceToHost));

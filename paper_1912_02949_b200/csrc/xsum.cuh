@@ -63,6 +63,88 @@ __device__ __forceinline__ void xacc_add(XAcc &a, double p, int &err) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-light per-thread accumulator: a 4-digit window [qa, qa+3] of the full
+// 10-digit number, anchored at the digit class of the thread's first summand.
+// A summand whose 3 digits fall in the window is added in registers; any other
+// summand is added exactly, digit by digit, to the block's shared-memory
+// accumulator (rare slow path).  Exactness does not depend on the anchor.
+struct XWin {
+  long long w0, w1, w2, w3, w4;
+  int qa;  // window digits [qa, qa+4]; -1: no summand yet
+};
+
+__device__ __forceinline__ void xwin_init(XWin &a) {
+  a.w0 = a.w1 = a.w2 = a.w3 = a.w4 = 0;
+  a.qa = -1;
+}
+
+// Split p (after Q) into its digit class q and three signed 32-bit digits.
+// Returns false for +-0 or a summand truncated to 0; sets err on range error.
+__device__ __forceinline__ bool xs_split(double p, int &q, long long &s0, long long &s1, long long &s2, int &err) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(p);
+  if ((b << 1) == 0ull) return false;
+  int e = (int)((b >> 52) & 0x7ffull);
+  if (e >= 1123) { err = 1; return false; }
+  unsigned long long m = b & 0x000fffffffffffffull;
+  if (e) m |= 0x0010000000000000ull; else e = 1;
+  int s = e - 1075 - kLsbExp;
+  if (s < 0) {
+    const int sh = -s;
+    m = sh >= 64 ? 0ull : (m >> sh);
+    s = 0;
+    if (!m) return false;
+  }
+  q = s >> 5;
+  const int r = s & 31;
+  s0 = (long long)(unsigned int)(m << r);
+  s1 = (long long)(r ? (unsigned int)(m >> (32 - r)) : (unsigned int)(m >> 32));
+  s2 = (long long)(r ? (unsigned int)(m >> (64 - r)) : 0u);
+  if (b >> 63) { s0 = -s0; s1 = -s1; s2 = -s2; }
+  return true;
+}
+
+// The window covers the digit classes qa, qa+1, qa+2, centred on the class of
+// the thread's first summand (magnitudes straddling a class boundary stay fast).
+__device__ __forceinline__ void xwin_add(XWin &a, double p, int &err, long long *blk) {
+  int q;
+  long long s0, s1, s2;
+  if (!xs_split(p, q, s0, s1, s2, err)) return;
+  if (a.qa < 0) a.qa = q < 1 ? 0 : (q > 6 ? 5 : q - 1);
+  const int d = q - a.qa;
+  if (d == 0) { a.w0 += s0; a.w1 += s1; a.w2 += s2; }
+  else if (d == 1) { a.w1 += s0; a.w2 += s1; a.w3 += s2; }
+  else if (d == 2) { a.w2 += s0; a.w3 += s1; a.w4 += s2; }
+  else {
+    atomicAdd(reinterpret_cast<unsigned long long *>(&blk[q]), (unsigned long long)s0);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&blk[q + 1]), (unsigned long long)s1);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&blk[q + 2]), (unsigned long long)s2);
+  }
+}
+
+// Flush a thread's window into the block accumulator (all 32 lanes of the warp call this).
+__device__ __forceinline__ void xwin_flush(const XWin &a, long long *blk) {
+  const int qa0 = __shfl_sync(0xffffffffu, a.qa, 0);
+  const bool same = __all_sync(0xffffffffu, a.qa == qa0 || a.qa < 0) && qa0 >= 0;
+  const bool mine = (threadIdx.x & 31) == 0;
+  long long w[5] = {a.w0, a.w1, a.w2, a.w3, a.w4};
+  if (same) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) w[j] += __shfl_down_sync(0xffffffffu, w[j], o);
+    }
+    if (mine)
+#pragma unroll
+      for (int j = 0; j < 5; ++j)
+        if (w[j]) atomicAdd(reinterpret_cast<unsigned long long *>(&blk[qa0 + j]), (unsigned long long)w[j]);
+  } else if (a.qa >= 0) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j)
+      if (w[j]) atomicAdd(reinterpret_cast<unsigned long long *>(&blk[a.qa + j]), (unsigned long long)w[j]);
+  }
+}
+
 // bits [lo, lo+cnt) (cnt <= 64) of the magnitude held in 32-bit digits mag[0..nd)
 __device__ __forceinline__ unsigned long long xs_bits(const unsigned int *mag, int nd, int lo, int cnt) {
   const int di = lo >> 5, off = lo & 31;
@@ -85,7 +167,7 @@ __device__ __forceinline__ bool xs_any_below(const unsigned int *mag, int nd, in
 }
 
 // Round the exact value held in limbs to the nearest double (ties to even).
-__device__ double xacc_round(const long long *limbs) {
+__device__ __noinline__ double xacc_round(const long long *limbs) {
   long long d[kLimbs];
   for (int i = 0; i < kLimbs; ++i) d[i] = limbs[i];
   // carry-normalize digits 0..8 into [0, 2^32)

@@ -1,0 +1,21 @@
+#!/usr/bin/env python3
+"""Summarize an ncu report: per kernel time, dram bytes, key throughput and stall metrics."""
+import csv, io, subprocess, sys, json
+rep = sys.argv[1]
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr, units = rows[0], rows[1]
+keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum", "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
+        "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem"]
+stall = [h for h in hdr if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio")]
+for r in rows[2:]:
+    d = dict(zip(hdr, r))
+    print("====", d["Kernel Name"].split("(")[0], d.get("ID", ""))
+    for k in keys:
+        if k in d:
+            print(f"  {k:60s} {d[k]} {units[hdr.index(k)]}")
+    st = sorted(((float(d[h] or 0), h) for h in stall), reverse=True)[:7]
+    print("  top stalls:", ", ".join(f"{h.replace('smsp__average_warps_issue_stalled_','').replace('_per_issue_active.ratio','')}={v:.2f}" for v, h in st))
