@@ -61,6 +61,10 @@ typedef enum {
 enum {
   SCG_SCALE = 1u << 0,          /* problem scaling ||C||_F = ||A|| = alpha = 1; default on */
   SCG_TRACE_CORRECT = 1u << 1,  /* Lambda += (alpha - tr Lambda)/R after reconstruct (Alg. 4 line 13) */
+  SCG_REGENERATE = 1u << 2,     /* storage-optimal two-pass Lanczos (regenerate v_2..v_k, Alg. 2 line 13 comment);
+                                   default: keep the Lanczos vectors in HBM and combine them in one pass
+                                   (Remark "Time-storage tradeoff") -- bitwise identical
+                                   results, O(q n) device memory (falls back to two-pass if it does not fit) */
   SCG_PROFILE = 1u << 8         /* record CUDA events around every kernel launch (bench / kernel stats) */
 };
 

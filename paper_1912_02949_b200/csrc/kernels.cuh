@@ -560,6 +560,43 @@ __global__ void __launch_bounds__(kBlock, SCG_MINB) k_lanczos_c(Csr C, Rows RL, 
   spmv_rows<1>(C, RL, Xj, epi.den, d, nullptr, rb, nl, epi);
 }
 
+// Stored-vector mode (Remark "Time-storage tradeoff"): the
+// Lanczos vectors w_j kept by pass 1 (slot j-1 of Wst, leading dimension ldw)
+// replace the pass-2 regeneration: x = s_1 v_1 + sum_j fma(s_j, v_j, .), v_j = w_j / rho_{j-1},
+// bitwise equal to the two-pass result; then ||x||^2 (exact).
+__global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict__ Wst, long long ldw,
+                                                       double *__restrict__ x, int nl, long long rb, XSlot *slot,
+                                                       DevScalars *sc, int finalize) {
+  __shared__ double s_s[kMaxQ], s_r[kMaxQ];
+  const int k = sc->k;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) { s_s[j] = sc->s[j]; s_r[j] = sc->rho[j]; }
+  __shared__ XBlk<1> xb;
+  xblk_init<1>(xb);
+  XWin acc[1];
+  xwin_init(acc[0]);
+  int err = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double *w = Wst + rb + r;
+    double xr = s_s[0] * (__ldg(w) / s_r[0]);
+    int j = 1;
+    for (; j + 4 <= k; j += 4) {
+      double wv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) wv[u] = __ldg(w + (long long)(j + u) * ldw);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xr = fma(s_s[j + u], wv[u] / s_r[j + u], xr);
+    }
+    for (; j < k; ++j) xr = fma(s_s[j], __ldg(w + (long long)j * ldw) / s_r[j], xr);
+    x[rb + r] = xr;
+    xwin_add(acc[0], xr * xr, err, xb.l[0]);
+  }
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
+    __threadfence();
+    sc->nu_x = sqrt(slot_take(slot, 0));
+    slot->counter = 0;
+  }
+}
+
 // ||x||^2 (exact); k == 1 case: x = s_1 v_1.
 __global__ void __launch_bounds__(kBlock) k_norm_x(const double *__restrict__ g, double *__restrict__ x, int nl,
                                                    long long rb, XSlot *slot, DevScalars *sc, int finalize) {

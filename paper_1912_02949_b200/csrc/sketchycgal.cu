@@ -25,12 +25,12 @@ using namespace scg;
 namespace {
 
 enum KClass {
-  KC_LANCZOS_A = 0, KC_LANCZOS_B, KC_TRIDIAG, KC_LANCZOS_C, KC_NORM_X, KC_MONITOR, KC_PRIMAL, KC_DUAL_SKETCH,
-  KC_OTHER, KC_COUNT
+  KC_LANCZOS_A = 0, KC_LANCZOS_B, KC_TRIDIAG, KC_LANCZOS_C, KC_NORM_X, KC_COMBINE, KC_MONITOR, KC_PRIMAL,
+  KC_DUAL_SKETCH, KC_OTHER, KC_COUNT
 };
 const char *kKClassName[KC_COUNT] = {"lanczos_a_spmv_dot", "lanczos_b_axpy_norm", "tridiag_mineig",
-                                     "lanczos_c_spmv_regen", "norm_x", "monitor_spmv", "primal_z_gpart",
-                                     "dual_sketch_next_g", "other"};
+                                     "lanczos_c_spmv_regen", "norm_x", "combine_stored", "monitor_spmv",
+                                     "primal_z_gpart", "dual_sketch_next_g", "other"};
 
 struct EvPair {
   cudaEvent_t a, b;
@@ -76,7 +76,13 @@ struct scg_ctx {
   std::vector<cudaEvent_t> evpool;
   int64_t kl[KC_COUNT] = {0};
   double kms[KC_COUNT] = {0};
-  double kbytes[KC_COUNT] = {0};
+  double kbytes[KC_COUNT] = {0};     // algorithmic bytes of one launch (fixed-size classes)
+  double kbytes_sum[KC_COUNT] = {0}; // accumulated algorithmic bytes
+  // Lanczos vector storage: slot 0 = start vector g; store mode: slot j-1 = w_j (j <= q);
+  // regenerate mode: slots 1, 2 = ring of w_i
+  double *Wst = nullptr;
+  int wcap = 0;
+  bool store = true;
   // errors
   int failed = 0;
   std::string err_msg;
@@ -148,6 +154,7 @@ void launch(scg_ctx *c, int cls, Kern kern, dim3 grid, dim3 block, Args... args)
     c->pending.push_back(p);
   }
   c->kl[cls]++;
+  c->kbytes_sum[cls] += c->kbytes[cls];
   c->launches++;
 }
 
@@ -301,8 +308,8 @@ void sketchycgal_destroy(scg_ctx *c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  void *ptrs[] = {c->rp, c->col, c->val, c->wts, c->ldiag, c->cdiag, c->d, c->z, c->y, c->a, c->v, c->g,
-                  c->W0, c->W1, c->x, c->S, c->Om, c->gpart, c->U, c->tmp1, c->tmp2, c->dmat, c->partial,
+  void *ptrs[] = {c->rp, c->col, c->val, c->wts, c->ldiag, c->cdiag, c->d, c->z, c->y, c->a, c->v, c->Wst,
+                  c->x, c->S, c->Om, c->gpart, c->U, c->tmp1, c->tmp2, c->dmat, c->partial,
                   c->dlam, c->dscalar, c->sc, c->slots, c->dlog, c->longrows};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -409,8 +416,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
             alloc((void **)&c->val, sizeof(double) * cnt_off) && alloc((void **)&c->wts, sizeof(double) * cnt_off) &&
             alloc((void **)&c->ldiag, nlb) && alloc((void **)&c->cdiag, nlb) && alloc((void **)&c->d, nlb) &&
             alloc((void **)&c->z, nlb) && alloc((void **)&c->y, nlb) && alloc((void **)&c->a, nlb) &&
-            alloc((void **)&c->v, nlb) && alloc((void **)&c->g, nb) && alloc((void **)&c->W0, nb) &&
-            alloc((void **)&c->W1, nb) && alloc((void **)&c->x, nb) &&
+            alloc((void **)&c->v, nlb) && alloc((void **)&c->Wst, nb * 3) && alloc((void **)&c->x, nb) &&
             alloc((void **)&c->S, nlb * R) && alloc((void **)&c->Om, nlb * R) &&
             alloc((void **)&c->sc, sizeof(DevScalars)) && alloc((void **)&c->slots, sizeof(XSlot) * SLOT_COUNT) &&
             alloc((void **)&c->dscalar, sizeof(double) * 8);
@@ -428,6 +434,9 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   c->grid_tiles = grid_for(std::max<int64_t>(nl / 2, (int64_t)c->nlong * 32), std::max(1, occ) * c->nsm);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_primal, kBlock, 0);
   c->grid_primal = grid_for(nl, std::max(1, occ) * c->nsm);
+  c->wcap = 3;
+  c->g = c->Wst;
+  c->store = (flags & SCG_REGENERATE) == 0;
   if (!alloc((void **)&c->gpart, sizeof(double) * (size_t)c->grid_primal * R)) return bad(SCG_ENOMEM, "gpart");
 
   cudaStream_t s = c->stream;
@@ -447,9 +456,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   CKI(cudaMemsetAsync(c->y, 0, nlb, s));
   CKI(cudaMemsetAsync(c->S, 0, nlb * R, s));
   CKI(cudaMemsetAsync(c->x, 0, nb, s));
-  CKI(cudaMemsetAsync(c->W0, 0, nb, s));
-  CKI(cudaMemsetAsync(c->W1, 0, nb, s));
-  CKI(cudaMemsetAsync(c->g, 0, nb, s));
+  CKI(cudaMemsetAsync(c->Wst, 0, nb * 3, s));
   // ||L||_F (exact sum over all stored entries) and C = -L / ||L||_F
   const int gnnz = (int)std::min<long long>(std::max<long long>(1, (cnt_off + kBlock - 1) / kBlock), 8 * c->nsm);
   launch(c, KC_OTHER, k_frob, dim3(gnnz), dim3(kBlock), (const double *)c->wts, (long long)cnt_off,
@@ -477,10 +484,11 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   c->kbytes[KC_TRIDIAG] = 0.0;
   c->kbytes[KC_LANCZOS_C] = 4.0 * (NL + 1) + 12.0 * NNZ + 8.0 * NL + 8.0 * N + 8.0 * NL + 8.0 * NL + 16.0 * NL;
   c->kbytes[KC_NORM_X] = 8.0 * NL;
+  c->kbytes[KC_COMBINE] = 0.0;  // 8 nl k + 8 nl per launch, accumulated in step()
   c->kbytes[KC_MONITOR] = 4.0 * (NL + 1) + 12.0 * NNZ + 16.0 * NL + 8.0 * N + 8.0 * NL;
   c->kbytes[KC_PRIMAL] = 24.0 * NL + 8.0 * NL * R;
   c->kbytes[KC_DUAL_SKETCH] = 56.0 * NL + 16.0 * NL * R;
-  for (int k = 0; k < KC_COUNT; ++k) { c->kl[k] = 0; c->kms[k] = 0; }
+  for (int k = 0; k < KC_COUNT; ++k) { c->kl[k] = 0; c->kms[k] = 0; c->kbytes_sum[k] = 0; }
   c->launches = 0;
   *out = c;
   return SCG_OK;
@@ -507,7 +515,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
   Csr C{c->rp, c->col, c->val};
   Rows TT{c->longrows, c->nlong};
   const int GT = c->grid_tiles;
-  double *Wb[2] = {c->W0, c->W1};
+  const long long ldw = (long long)c->n;
   for (int64_t it = 0; it < T; ++it) {
     const int64_t t = c->t + 1;
     // Alg. 4 line 5 and the q_t schedule (CAC-6), evaluated on the host
@@ -525,28 +533,54 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     if (q > c->n - 1) q = c->n - 1;
     if (q > kMaxQ - 1) q = kMaxQ - 1;
     A.q = (int)q;
+    if (c->store && c->wcap < q) {  // grow the Lanczos-vector store (slot 0 = g is kept)
+      const int cap = (int)std::min<int64_t>(q + 16, kMaxQ);
+      double *nw = nullptr;
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      const size_t need = sizeof(double) * (size_t)c->n * cap;
+      if (need + (size_t)(1ull << 30) < fr && cudaMalloc(&nw, need) == cudaSuccess) {
+        CK(cudaMemcpyAsync(nw, c->Wst, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        cudaFree(c->Wst);
+        c->Wst = nw;
+        c->g = nw;
+        c->wcap = cap;
+      } else {
+        c->store = false;  // does not fit: storage-optimal two-pass mode
+      }
+    }
+    auto slot = [&](int j) -> double * {  // buffer holding w_j (j >= 1; w_1 = g)
+      if (c->store) return c->Wst + (long long)(j - 1) * ldw;
+      return j == 1 ? c->Wst : c->Wst + (long long)(1 + (j & 1)) * ldw;
+    };
     // ---- Lanczos pass 1 (Alg. 2 lines 1-9)
     for (int i = 1; i <= q; ++i) {
-      const double *Xi = (i == 1) ? c->g : Wb[i & 1];
+      const double *Xi = slot(i);
       launch(c, KC_LANCZOS_A, k_lanczos_a, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, Xi, nl, rb, i, c->a,
              c->slots + SLOT_OM, c->sc, 1);
       if (i < q) {
-        const double *Xim1 = (i == 1) ? nullptr : (i == 2 ? c->g : Wb[(i - 1) & 1]);
-        launch(c, KC_LANCZOS_B, k_lanczos_b, dim3(G), dim3(kBlock), (const double *)c->a, Xi, Xim1,
-               Wb[(i + 1) & 1], nl, rb, i, c->slots + SLOT_RHO, c->sc, 1);
+        const double *Xim1 = (i == 1) ? nullptr : slot(i - 1);
+        launch(c, KC_LANCZOS_B, k_lanczos_b, dim3(G), dim3(kBlock), (const double *)c->a, Xi, Xim1, slot(i + 1),
+               nl, rb, i, c->slots + SLOT_RHO, c->sc, 1);
       }
     }
     // ---- tridiagonal eigenpair (lines 11-12)
     launch(c, KC_TRIDIAG, k_tridiag, dim3(1), dim3(32), c->sc, (int)q);
-    // ---- pass 2 (line 13)
-    for (int j = 1; j < q; ++j) {
-      const double *Xj = (j == 1) ? c->g : Wb[j & 1];
-      const double *Xjm1 = (j == 1) ? nullptr : (j == 2 ? c->g : Wb[(j - 1) & 1]);
-      launch(c, KC_LANCZOS_C, k_lanczos_c, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, Xj, Xjm1,
-             Wb[(j + 1) & 1], c->x, nl, rb, j, (const DevScalars *)c->sc);
+    if (c->store) {  // ---- line 13 from the stored vectors (Remark)
+      c->kbytes[KC_COMBINE] = 8.0 * (double)c->nl * (double)q + 8.0 * (double)c->nl;
+      launch(c, KC_COMBINE, k_combine, dim3(c->grid_rows), dim3(kBlock), (const double *)c->Wst, ldw, c->x, nl, rb,
+             c->slots + SLOT_XX, c->sc, 1);
+    } else {  // ---- pass 2 (line 13): regenerate v_2..v_k
+      for (int j = 1; j < q; ++j) {
+        const double *Xj = slot(j);
+        const double *Xjm1 = (j == 1) ? nullptr : slot(j - 1);
+        launch(c, KC_LANCZOS_C, k_lanczos_c, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, Xj, Xjm1,
+               slot(j + 1), c->x, nl, rb, j, (const DevScalars *)c->sc);
+      }
+      launch(c, KC_NORM_X, k_norm_x, dim3(G), dim3(kBlock), (const double *)c->g, c->x, nl, rb,
+             c->slots + SLOT_XX, c->sc, 1);
     }
-    launch(c, KC_NORM_X, k_norm_x, dim3(G), dim3(kBlock), (const double *)c->g, c->x, nl, rb,
-           c->slots + SLOT_XX, c->sc, 1);
     // ---- monitors, primal, dual, sketch (Alg. 4 lines 8-10)
     launch(c, KC_MONITOR, k_monitor, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, (const double *)c->cdiag,
            (const double *)c->x, c->v, nl, rb, c->slots + SLOT_MON, c->sc, 1);
@@ -825,7 +859,7 @@ int32_t sketchycgal_kernel_stats(scg_ctx *c, scg_kstat *out, int32_t max) {
     std::snprintf(out[cnt].name, sizeof(out[cnt].name), "%s", kKClassName[k]);
     out[cnt].launches = c->kl[k];
     out[cnt].total_ms = c->kms[k];
-    out[cnt].bytes_per_launch = c->kbytes[k];
+    out[cnt].bytes_per_launch = c->kl[k] ? c->kbytes_sum[k] / (double)c->kl[k] : c->kbytes[k];
     ++cnt;
   }
   return cnt;
@@ -834,7 +868,7 @@ int32_t sketchycgal_kernel_stats(scg_ctx *c, scg_kstat *out, int32_t max) {
 void sketchycgal_reset_stats(scg_ctx *c) {
   if (!c) return;
   ev_flush(c);
-  for (int k = 0; k < KC_COUNT; ++k) { c->kl[k] = 0; c->kms[k] = 0; }
+  for (int k = 0; k < KC_COUNT; ++k) { c->kl[k] = 0; c->kms[k] = 0; c->kbytes_sum[k] = 0; }
   c->launches = 0;
 }
 

@@ -15,8 +15,8 @@ import scg_inputs as si
 pytestmark = pytest.mark.gpu
 
 
-def _run_pair(gpu, L, R, T, seed, scale=True):
-    g = gpu.SketchyCGAL(L, R=R, seed=seed, scale=scale)
+def _run_pair(gpu, L, R, T, seed, scale=True, regenerate=False):
+    g = gpu.SketchyCGAL(L, R=R, seed=seed, scale=scale, regenerate=regenerate)
     g.step(T)
     o = oracle.Oracle(L, R, seed=seed, scale=scale, logcap=T)
     o.step(T)
@@ -66,11 +66,19 @@ def test_config0_full_trajectory_and_cut(gpu):
     assert w == w_o
 
 
-def test_config1_trajectory_signed_weights(gpu):
-    """configs[1] shape (torus, +-1 weights), first 300 iterations bitwise."""
+@pytest.mark.parametrize("regenerate", [False, True])
+def test_config1_trajectory_signed_weights(gpu, regenerate):
+    """configs[1] shape (torus, +-1 weights), first 300 iterations bitwise, both Lanczos modes."""
     L = si.laplacian("c1")
-    g, o = _run_pair(gpu, L, 10, 300, seed=1)
+    g, o = _run_pair(gpu, L, 10, 300, seed=1, regenerate=regenerate)
     _assert_trajectory(g, o, 300)
+
+
+def test_config0_regenerate_mode(gpu):
+    """Storage-optimal two-pass Lanczos (Alg. 2 as printed) on configs[0], 400 iterations."""
+    L = si.laplacian("c0")
+    g, o = _run_pair(gpu, L, 10, 400, seed=0, regenerate=True)
+    _assert_trajectory(g, o, 400)
 
 
 def test_unscaled_variant(gpu):
@@ -79,12 +87,13 @@ def test_unscaled_variant(gpu):
     _assert_trajectory(g, o, 60)
 
 
-def test_breakdown_complete_graph(gpu):
+@pytest.mark.parametrize("regenerate", [False, True])
+def test_breakdown_complete_graph(gpu, regenerate):
     """K_8: D_1 has two eigenvalues -> invariant subspace after 2 steps (Alg. 2 line 8)."""
     n = 8
     i, j = np.triu_indices(n, 1)
     L = si.laplacian_from_edges(n, i, j, np.ones(len(i)))
-    g, o = _run_pair(gpu, L, 3, 25, seed=2)
+    g, o = _run_pair(gpu, L, 3, 25, seed=2, regenerate=regenerate)
     assert o.log[0, 2] == 2 and o.log[0, 1] == 3  # k = 2 < q_1 = ceil(ln 8) = 3
     _assert_trajectory(g, o, 25)
 
@@ -151,9 +160,10 @@ def test_full_size_apply_D_bitwise(gpu, cfg):
     del o
 
 
-def test_config2_first_iterations_bitwise(gpu):
+@pytest.mark.parametrize("regenerate", [False, True])
+def test_config2_first_iterations_bitwise(gpu, regenerate):
     L = si.laplacian("c2")
-    g, o = _run_pair(gpu, L, 10, 3, seed=2)
+    g, o = _run_pair(gpu, L, 10, 3, seed=2, regenerate=regenerate)
     _assert_trajectory(g, o, 3)
 
 
