@@ -177,6 +177,11 @@ void sketchycgal_reset_stats(scg_ctx *c);
 /* Write a 128-byte NCCL unique id (call on rank 0, broadcast to all ranks). */
 scg_status sketchycgal_nccl_unique_id(void *out128);
 
+/* Diagnostics: compare the kernels' shared-divisor division (a * RN(1/b) with two
+ * fma corrections, used for the normalization v = w / rho of Alg. 2 line 9) with the
+ * hardware IEEE division on n pseudo-random operand pairs; *mismatches = count. */
+scg_status sketchycgal_selftest_division(int32_t device, int64_t n, uint64_t seed, int64_t *mismatches);
+
 const char *sketchycgal_last_error(const scg_ctx *c);
 void sketchycgal_destroy(scg_ctx *c);
 

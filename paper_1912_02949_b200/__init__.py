@@ -92,7 +92,7 @@ EXPORTS = ["sketchycgal_maxcut_init", "sketchycgal_step", "sketchycgal_synchroni
            "sketchycgal_objective", "sketchycgal_feasibility", "sketchycgal_round", "sketchycgal_iter_log",
            "sketchycgal_get_state", "sketchycgal_apply_D", "sketchycgal_iterations", "sketchycgal_launch_count",
            "sketchycgal_kernel_stats", "sketchycgal_reset_stats", "sketchycgal_nccl_unique_id",
-           "sketchycgal_last_error", "sketchycgal_destroy"]
+           "sketchycgal_selftest_division", "sketchycgal_last_error", "sketchycgal_destroy"]
 
 _lib = None
 
@@ -119,6 +119,8 @@ def open_library(path: str = LIB_PATH):
     lib.sketchycgal_kernel_stats.argtypes = [P, P, I32]
     lib.sketchycgal_reset_stats.restype = None
     lib.sketchycgal_reset_stats.argtypes = [P]
+    lib.sketchycgal_selftest_division.restype = ctypes.c_int
+    lib.sketchycgal_selftest_division.argtypes = [I32, I64, ctypes.c_uint64, ctypes.POINTER(I64)]
     lib.sketchycgal_last_error.restype = ctypes.c_char_p
     lib.sketchycgal_last_error.argtypes = [P]
     lib.sketchycgal_destroy.restype = None
@@ -138,6 +140,15 @@ def load():
 
 class ScgError(RuntimeError):
     pass
+
+
+def selftest_division(n: int = 1 << 26, seed: int = 1, device: int = 0) -> int:
+    """Mismatches of the kernels' shared-divisor division vs IEEE division on n random pairs."""
+    out = ctypes.c_int64(-1)
+    st = load().sketchycgal_selftest_division(int(device), int(n), int(seed), ctypes.byref(out))
+    if st != 0:
+        raise ScgError(f"selftest: {STATUS.get(st, st)}")
+    return int(out.value)
 
 
 def _c64(a, dt):

@@ -47,6 +47,19 @@ struct Csr {
   const double *val;
 };
 
+// ---------------------------------------------------------------- division
+// a / b, correctly rounded (IEEE), for a divisor b shared by many quotients:
+// rb = RN(1/b) is computed once; two Markstein corrections with exact fma
+// residuals r = a - q b give RN(a / b) for normal-range operands (tested
+// bitwise against the hardware division in tests/test_gpu_parity.py).  Used
+// for the normalization v = w / rho of Alg. 2 line 9.
+__device__ __forceinline__ double div_rn(double a, double b, double rb) {
+  const double q0 = a * rb;
+  const double q1 = fma(fma(-q0, b, a), rb, q0);
+  const double q2 = fma(fma(-q1, b, a), rb, q1);
+  return a == 0.0 ? q0 : q2;
+}
+
 // ---------------------------------------------------------------- row engine
 // Rows with at most kLongRow off-diagonal entries are "short": one thread owns a
 // row and runs its sequential CAC-3 chain, loading kChunk entries (col, val, then
@@ -62,7 +75,7 @@ struct Csr {
 #define SCG_CH 4
 #endif
 #ifndef SCG_MINB
-#define SCG_MINB 4
+#define SCG_MINB 3
 #endif
 constexpr int kLongRow = 32;
 constexpr int kChunk = SCG_CH;   // entries of a row loaded per round
@@ -71,6 +84,15 @@ constexpr int kRpt = SCG_RPT;    // rows per thread in flight
 struct Rows {
   const int *longrows;  // local ids of long rows
   int nlong;
+  // SELL-32-sigma layout of the short rows: slice s covers 32 rows perm[32 s + lane]
+  // (-1: empty lane) of equal-ish length (sorted within windows of kSigma rows);
+  // slot j of lane l is at meta[s].x + 32 j + l; meta[s].y = slice width.
+  const int *perm;
+  const int2 *meta;
+  const int *scol;      // column | 0x80000000 for a negative uniform value; -1 = padding
+  const double *sval;   // per-slot values, or nullptr when all |C_rj| equal m0
+  double m0;
+  int nslice;
 };
 
 template <int NC>
@@ -87,8 +109,9 @@ __device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double
                                                long long rb, RowOut<NC> &o) {
   const int lane = threadIdx.x & 31;
   const int e0 = __ldg(&C.rp[r]), e1 = __ldg(&C.rp[r + 1]);
+  const double rden = 1.0 / den;
   o.r = r;
-  o.xr = X[rb + r] / den;
+  o.xr = div_rn(X[rb + r], den, rden);
   o.s[0] = diag0[r] * o.xr;
   if (NC > 1) o.s[NC - 1] = diag1[r] * o.xr;
   int e = e0 + lane;
@@ -97,7 +120,7 @@ __device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double
   double xn = e < e1 ? __ldg(&X[cn]) : 0.0;
   for (int base = e0; base < e1; base += 32) {
     const int cnt = min(32, e1 - base);
-    const double m = mn, x = xn / den;
+    const double m = mn, x = div_rn(xn, den, rden);
     // prefetch the next round before running this round's chain
     e = base + 32 + lane;
     if (e < e1) { cn = __ldg(&C.col[e]); mn = __ldg(&C.val[e]); xn = __ldg(&X[cn]); }
@@ -110,9 +133,37 @@ __device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double
   }
 }
 
+template <bool UNI>
+__device__ __forceinline__ void sell_load_chunk(const Rows &RL, int2 mt, int j0, int lane, int (&cc)[kChunk],
+                                                double (&vv)[kChunk]) {
+#pragma unroll
+  for (int u = 0; u < kChunk; ++u) {
+    cc[u] = -1;
+    if (j0 + u < mt.y) {
+      const int e = mt.x + (j0 + u) * 32 + lane;
+      cc[u] = __ldg(&RL.scol[e]);
+      if (!UNI) vv[u] = __ldg(&RL.sval[e]);
+    }
+  }
+}
+
+template <int NC, bool UNI>
+__device__ __forceinline__ void sell_fma_chunk(const Rows &RL, const int (&cc)[kChunk], const double (&vv)[kChunk],
+                                               const double (&xg)[kChunk], double den, double rden,
+                                               RowOut<NC> &o) {
+#pragma unroll
+  for (int u = 0; u < kChunk; ++u)
+    if (cc[u] != -1) {
+      const double m = UNI ? (cc[u] < 0 ? -RL.m0 : RL.m0) : vv[u];
+      const double x = div_rn(xg[u], den, rden);  // v = w / rho (Alg. 2 line 9), formed on the fly
+#pragma unroll
+      for (int c = 0; c < NC; ++c) o.s[c] = fma(m, x, o.s[c]);
+    }
+}
+
 // Visit every row of this rank once: epi(RowOut) is called by the owning thread
 // (short rows) or by lane 0 of the owning warp (long rows).
-template <int NC, class Epi>
+template <int NC, bool UNI, class Epi>
 __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
                                           const double *__restrict__ diag0, const double *__restrict__ diag1,
                                           long long rb, int nl, Epi &epi) {
@@ -124,79 +175,66 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
     long_row_chain<NC>(C, RL.longrows[w], X, den, diag0, diag1, rb, o);
     if (lane == 0) epi(o);
   }
-  const int stride = gridDim.x * blockDim.x;
-  for (int base = blockIdx.x * blockDim.x + threadIdx.x; base < nl; base += kRpt * stride) {
-    int e0[kRpt], e1[kRpt];
-    bool act[kRpt];
-    RowOut<NC> o[kRpt];
-#pragma unroll
-    for (int u = 0; u < kRpt; ++u) {
-      const int r = base + u * stride;
-      act[u] = false;
-      if (r < nl) {
-        e0[u] = __ldg(&C.rp[r]);
-        e1[u] = __ldg(&C.rp[r + 1]);
-        act[u] = (e1[u] - e0[u]) <= kLongRow;
-      }
-      o[u].r = r;
-    }
-    double xo[kRpt], dg0[kRpt], dg1[kRpt];
-#pragma unroll
-    for (int u = 0; u < kRpt; ++u) {
-      if (act[u]) {
-        xo[u] = X[rb + o[u].r];
-        dg0[u] = diag0[o[u].r];
-        if (NC > 1) dg1[u] = diag1[o[u].r];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kRpt; ++u) {
-      if (act[u]) {
-        o[u].xr = xo[u] / den;
-        o[u].s[0] = dg0[u] * o[u].xr;
-        if (NC > 1) o[u].s[NC - 1] = dg1[u] * o[u].xr;
-      }
-    }
-    for (int k = 0;; k += kChunk) {
-      bool more = false;
-#pragma unroll
-      for (int u = 0; u < kRpt; ++u) more |= act[u] && e0[u] + k < e1[u];
-      if (!more) break;
-      int cc[kRpt][kChunk];
-      double vv[kRpt][kChunk], xg[kRpt][kChunk];
-#pragma unroll
-      for (int u = 0; u < kRpt; ++u)
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          const int e = e0[u] + k + j;
-          if (act[u] && e < e1[u]) {
-            cc[u][j] = __ldg(&C.col[e]);
-            vv[u][j] = __ldg(&C.val[e]);
-          }
-        }
-#pragma unroll
-      for (int u = 0; u < kRpt; ++u)
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          const int e = e0[u] + k + j;
-          if (act[u] && e < e1[u]) xg[u][j] = __ldg(&X[cc[u][j]]);
-        }
-#pragma unroll
-      for (int u = 0; u < kRpt; ++u)
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          const int e = e0[u] + k + j;
-          if (act[u] && e < e1[u]) {
-            const double x = xg[u][j] / den;  // v = w / rho (Alg. 2 line 9), formed on the fly
-#pragma unroll
-            for (int c = 0; c < NC; ++c) o[u].s[c] = fma(vv[u][j], x, o[u].s[c]);
-          }
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < kRpt; ++u)
-      if (act[u]) epi(o[u]);
+  const double rden = 1.0 / den;
+  // SELL slices, software-pipelined: slice metadata two slices ahead, the first
+  // chunk of columns (and the own-row entries) one slice ahead, so each step
+  // waits on one memory round trip (the gathers) instead of three.
+  const int ns = RL.nslice;
+  int sl = gw;
+  int pr = -1, pn = -1;
+  int2 mr = make_int2(0, 0), mn = make_int2(0, 0);
+  if (sl < ns) { pr = __ldg(&RL.perm[sl * 32 + lane]); mr = __ldg(&RL.meta[sl]); }
+  if (sl + nw < ns) { pn = __ldg(&RL.perm[(sl + nw) * 32 + lane]); mn = __ldg(&RL.meta[sl + nw]); }
+  int cc[kChunk];
+  double vv[kChunk];
+  double xo = 0.0, dg0 = 0.0, dg1 = 0.0;
+  sell_load_chunk<UNI>(RL, mr, 0, lane, cc, vv);
+  if (pr >= 0) {
+    xo = X[rb + pr];
+    dg0 = diag0[pr];
+    if (NC > 1) dg1 = diag1[pr];
   }
+  while (sl < ns) {
+    double xg[kChunk];
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u)
+      if (cc[u] != -1) xg[u] = __ldg(&X[cc[u] & 0x7fffffff]);
+    const int sln = sl + nw;
+    int ccn[kChunk];
+    double vvn[kChunk];
+    double xon = 0.0, dgn0 = 0.0, dgn1 = 0.0;
+    sell_load_chunk<UNI>(RL, mn, 0, lane, ccn, vvn);  // width 0 when sln >= ns
+    if (pn >= 0) {
+      xon = X[rb + pn];
+      dgn0 = diag0[pn];
+      if (NC > 1) dgn1 = diag1[pn];
+    }
+    int pnn = -1;
+    int2 mnn = make_int2(0, 0);
+    if (sln + nw < ns) { pnn = __ldg(&RL.perm[(sln + nw) * 32 + lane]); mnn = __ldg(&RL.meta[sln + nw]); }
+    RowOut<NC> o;
+    o.r = pr;
+    o.xr = div_rn(xo, den, rden);
+    o.s[0] = dg0 * o.xr;
+    if (NC > 1) o.s[NC - 1] = dg1 * o.xr;
+    sell_fma_chunk<NC, UNI>(RL, cc, vv, xg, den, rden, o);
+    for (int j0 = kChunk; j0 < mr.y; j0 += kChunk) {  // rows longer than one chunk
+      int c2[kChunk];
+      double v2[kChunk], x2[kChunk];
+      sell_load_chunk<UNI>(RL, mr, j0, lane, c2, v2);
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u)
+        if (c2[u] != -1) x2[u] = __ldg(&X[c2[u] & 0x7fffffff]);
+      sell_fma_chunk<NC, UNI>(RL, c2, v2, x2, den, rden, o);
+    }
+    if (pr >= 0) epi(o);
+    pr = pn; mr = mn; pn = pnn; mn = mnn;
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) { cc[u] = ccn[u]; vv[u] = vvn[u]; }
+    xo = xon; dg0 = dgn0; dg1 = dgn1;
+    sl = sln;
+  }
+  (void)nl;
 }
 
 // ---------------------------------------------------------------- block reduction
@@ -325,6 +363,7 @@ struct EpiA {
   }
 };
 
+template <bool UNI>
 __global__ void __launch_bounds__(kBlock, SCG_MINB) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ X, int nl, long long rb, int i,
                                                          double *__restrict__ a, XSlot *slot, DevScalars *sc,
@@ -338,7 +377,7 @@ __global__ void __launch_bounds__(kBlock, SCG_MINB) k_lanczos_a(Csr C, Rows RL, 
   epi.blk = xb.l[0];
   xwin_init(epi.acc[0]);
   epi.err = 0;
-  spmv_rows<1>(C, RL, X, den, d, nullptr, rb, nl, epi);
+  spmv_rows<1, UNI>(C, RL, X, den, d, nullptr, rb, nl, epi);
   int err = epi.err;
   XWin (&acc)[1] = epi.acc;
   if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
@@ -368,6 +407,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_lanczos_b(const double *__restric
   const double om = sc->om[i - 1];
   const double den = sc->rho[i - 1];
   const double denm = i >= 2 ? sc->rho[i - 2] : 1.0;
+  const double rden = 1.0 / den, rdenm = 1.0 / denm;
   __shared__ XBlk<1> xb;
   xblk_init<1>(xb);
   XWin acc[1];
@@ -389,9 +429,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_lanczos_b(const double *__restric
     for (int u = 0; u < 4; ++u) {
       const int r = r0 + u * stride;
       if (r < nl) {
-        const double vi = xi[u] / den;
+        const double vi = div_rn(xi[u], den, rden);
         double w = fma(-om, vi, av[u]);
-        if (i >= 2) w = fma(-den, xm[u] / denm, w);  // rho_{i-1} = rho[i-1] = den
+        if (i >= 2) w = fma(-den, div_rn(xm[u], denm, rdenm), w);  // rho_{i-1} = rho[i-1] = den
         Xip1[rb + r] = w;
         xwin_add(acc[0], w * w, err, xb.l[0]);
       }
@@ -538,26 +578,27 @@ struct EpiC {
   double *Xjp1, *x;
   long long rb;
   int j;
-  double om, den, denm, rhoj, s1, sj1;
+  double om, den, denm, rhoj, s1, sj1, rrhoj;
   __device__ __forceinline__ void operator()(const RowOut<1> &o) {
     const double vj = o.xr;
     double w = fma(-om, vj, o.s[0]);
-    if (j >= 2) w = fma(-den, Xjm1[rb + o.r] / denm, w);
+    if (j >= 2) w = fma(-den, div_rn(Xjm1[rb + o.r], denm, 1.0 / denm), w);
     Xjp1[rb + o.r] = w;
-    const double vn = w / rhoj;
+    const double vn = div_rn(w, rhoj, rrhoj);
     const double xr = j == 1 ? s1 * vj : x[rb + o.r];
     x[rb + o.r] = fma(sj1, vn, xr);
   }
 };
 
+template <bool UNI>
 __global__ void __launch_bounds__(kBlock, SCG_MINB) k_lanczos_c(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ Xj, const double *Xjm1,
                                                          double *Xjp1, double *__restrict__ x, int nl, long long rb,
                                                          int j, const DevScalars *__restrict__ sc) {
   if (j >= sc->k) return;  // sc->k holds the effective k after k_tridiag
   EpiC epi{Xjm1, Xjp1, x, rb, j, sc->om[j - 1], sc->rho[j - 1], j >= 2 ? sc->rho[j - 2] : 1.0, sc->rho[j],
-           sc->s[0], sc->s[j]};
-  spmv_rows<1>(C, RL, Xj, epi.den, d, nullptr, rb, nl, epi);
+           sc->s[0], sc->s[j], 1.0 / sc->rho[j]};
+  spmv_rows<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, nl, epi);
 }
 
 // Stored-vector mode (Remark "Time-storage tradeoff"): the
@@ -567,9 +608,13 @@ __global__ void __launch_bounds__(kBlock, SCG_MINB) k_lanczos_c(Csr C, Rows RL, 
 __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict__ Wst, long long ldw,
                                                        double *__restrict__ x, int nl, long long rb, XSlot *slot,
                                                        DevScalars *sc, int finalize) {
-  __shared__ double s_s[kMaxQ], s_r[kMaxQ];
+  __shared__ double s_s[kMaxQ], s_r[kMaxQ], s_rr[kMaxQ];
   const int k = sc->k;
-  for (int j = threadIdx.x; j < k; j += blockDim.x) { s_s[j] = sc->s[j]; s_r[j] = sc->rho[j]; }
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    s_s[j] = sc->s[j];
+    s_r[j] = sc->rho[j];
+    s_rr[j] = 1.0 / sc->rho[j];
+  }
   __shared__ XBlk<1> xb;
   xblk_init<1>(xb);
   XWin acc[1];
@@ -577,16 +622,16 @@ __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict_
   int err = 0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
     const double *w = Wst + rb + r;
-    double xr = s_s[0] * (__ldg(w) / s_r[0]);
+    double xr = s_s[0] * div_rn(__ldg(w), s_r[0], s_rr[0]);
     int j = 1;
     for (; j + 4 <= k; j += 4) {
       double wv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) wv[u] = __ldg(w + (long long)(j + u) * ldw);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) xr = fma(s_s[j + u], wv[u] / s_r[j + u], xr);
+      for (int u = 0; u < 4; ++u) xr = fma(s_s[j + u], div_rn(wv[u], s_r[j + u], s_rr[j + u]), xr);
     }
-    for (; j < k; ++j) xr = fma(s_s[j], __ldg(w + (long long)j * ldw) / s_r[j], xr);
+    for (; j < k; ++j) xr = fma(s_s[j], div_rn(__ldg(w + (long long)j * ldw), s_r[j], s_rr[j]), xr);
     x[rb + r] = xr;
     xwin_add(acc[0], xr * xr, err, xb.l[0]);
   }
@@ -647,6 +692,7 @@ struct EpiM {
   }
 };
 
+template <bool UNI>
 __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const double *__restrict__ d,
                                                        const double *__restrict__ cdiag, const double *__restrict__ x,
                                                        double *__restrict__ v, int nl, long long rb, XSlot *slot,
@@ -661,7 +707,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
   xwin_init(epi.acc[1]);
   xwin_init(epi.acc[2]);
   epi.err = 0;
-  spmv_rows<2>(C, RL, x, nu, d, cdiag, rb, nl, epi);
+  spmv_rows<2, UNI>(C, RL, x, nu, d, cdiag, rb, nl, epi);
   int err = epi.err;
   XWin (&acc)[3] = epi.acc;
   if (commit_and_ticket<3>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
@@ -944,11 +990,35 @@ struct EpiY {
   __device__ __forceinline__ void operator()(const RowOut<1> &o) { y[o.r] = o.s[0]; }
 };
 
+template <bool UNI>
 __global__ void __launch_bounds__(kBlock) k_apply_d(Csr C, Rows RL, const double *__restrict__ d,
                                                     const double *__restrict__ X, int nl, long long rb,
                                                     double *__restrict__ y) {
   EpiY epi{y};
-  spmv_rows<1>(C, RL, X, 1.0, d, nullptr, rb, nl, epi);
+  spmv_rows<1, UNI>(C, RL, X, 1.0, d, nullptr, rb, nl, epi);
+}
+
+// Self-test: div_rn against the hardware IEEE division on pseudo-random operands
+// (mantissas drawn uniformly, including the extremes 1 and 2 - ulp), exponents in +-60.
+__global__ void k_selftest_div(long long n, uint64_t seed, unsigned long long *mismatch) {
+  unsigned long long bad = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    scg_philox_out o = scg_draw(seed, 77u, 0u, (uint64_t)i);
+    unsigned long long ma = ((unsigned long long)o.w[0] << 32 | o.w[1]) & 0x000fffffffffffffull;
+    unsigned long long mb = ((unsigned long long)o.w[2] << 32 | o.w[3]) & 0x000fffffffffffffull;
+    if ((i & 7) == 1) mb = 0x000fffffffffffffull;  // b = 2 - ulp
+    if ((i & 7) == 2) mb = 0;                      // b = power of two
+    if ((i & 7) == 3) ma = 0x000fffffffffffffull;
+    const int ea = 1023 + (int)(o.w[0] % 121) - 60, eb = 1023 + (int)(o.w[2] % 121) - 60;
+    double a = __longlong_as_double((long long)(((unsigned long long)ea << 52) | ma));
+    const double b = __longlong_as_double((long long)(((unsigned long long)eb << 52) | mb));
+    if (o.w[1] & 1) a = -a;
+    if ((i & 1023) == 5) a = 0.0;
+    const double q = div_rn(a, b, 1.0 / b);
+    const double ref = a / b;
+    bad += (__double_as_longlong(q) != __double_as_longlong(ref));
+  }
+  atomicAdd(mismatch, bad);
 }
 
 }  // namespace scg

@@ -63,8 +63,15 @@ struct scg_ctx {
   XSlot *slots = nullptr;
   scg_iter_rec *dlog = nullptr;
   int64_t log_cap = 0;
-  int grid_rows = 1, grid_primal = 1, grid_tiles = 1;
+  int grid_rows = 1, grid_primal = 1, grid_tiles = 1, grid_b = 1, grid_comb = 1, grid_dual = 1, grid_norm = 1;
   int *longrows = nullptr;
+  int *sell_perm = nullptr, *sell_col = nullptr;
+  int2 *sell_meta = nullptr;
+  double *sell_val = nullptr;
+  double sell_m0 = 0.0;
+  int nslice = 0;
+  double sell_slots = 0.0;
+  bool sell_uniform = false;
   int nlong = 0;
   int64_t t = 0;
   int64_t launches = 0;
@@ -288,6 +295,21 @@ extern "C" {
 
 const char *sketchycgal_last_error(const scg_ctx *c) { return c ? c->err_msg.c_str() : "null context"; }
 
+scg_status sketchycgal_selftest_division(int32_t device, int64_t n, uint64_t seed, int64_t *mismatches) {
+  if (!mismatches || n < 0) return SCG_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return SCG_ECUDA;
+  unsigned long long *d = nullptr;
+  if (cudaMalloc(&d, sizeof(unsigned long long)) != cudaSuccess) return SCG_ECUDA;
+  cudaMemset(d, 0, sizeof(unsigned long long));
+  k_selftest_div<<<1184, 256>>>((long long)n, seed, d);
+  unsigned long long h = 0;
+  cudaError_t e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return SCG_ECUDA;
+  *mismatches = (int64_t)h;
+  return SCG_OK;
+}
+
 int64_t sketchycgal_iterations(const scg_ctx *c) { return c ? c->t : -1; }
 
 int64_t sketchycgal_launch_count(const scg_ctx *c) { return c ? c->launches : -1; }
@@ -310,7 +332,8 @@ void sketchycgal_destroy(scg_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   void *ptrs[] = {c->rp, c->col, c->val, c->wts, c->ldiag, c->cdiag, c->d, c->z, c->y, c->a, c->v, c->Wst,
                   c->x, c->S, c->Om, c->gpart, c->U, c->tmp1, c->tmp2, c->dmat, c->partial,
-                  c->dlam, c->dscalar, c->sc, c->slots, c->dlog, c->longrows};
+                  c->dlam, c->dscalar, c->sc, c->slots, c->dlog, c->longrows,
+                  c->sell_perm, c->sell_col, c->sell_meta, c->sell_val};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (auto &p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
@@ -428,12 +451,20 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
 
   // grid sizes from occupancy
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_a, kBlock, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_a<true>, kBlock, 0);
   c->grid_rows = grid_for(nl, std::max(1, occ) * c->nsm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_c, kBlock, 0);
-  c->grid_tiles = grid_for(std::max<int64_t>(nl / 2, (int64_t)c->nlong * 32), std::max(1, occ) * c->nsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_c<true>, kBlock, 0);
+  c->grid_tiles = grid_for(std::max<int64_t>(nl, (int64_t)c->nlong * 32), std::max(1, occ) * c->nsm);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_primal, kBlock, 0);
   c->grid_primal = grid_for(nl, std::max(1, occ) * c->nsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_b, kBlock, 0);
+  c->grid_b = grid_for(nl, std::max(1, occ) * c->nsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_combine, kBlock, 0);
+  c->grid_comb = grid_for(nl, std::max(1, occ) * c->nsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dual_sketch, kBlock, 0);
+  c->grid_dual = grid_for(nl, std::max(1, occ) * c->nsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_norm_x, kBlock, 0);
+  c->grid_norm = grid_for(nl, std::max(1, occ) * c->nsm);
   c->wcap = 3;
   c->g = c->Wst;
   c->store = (flags & SCG_REGENERATE) == 0;
@@ -466,6 +497,61 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   c->nrmL = std::sqrt(c->nrmL);
   if (!(c->nrmL > 0) || !std::isfinite(c->nrmL)) return bad(SCG_EINVAL, "||L||_F must be positive and finite");
   CKI(cudaMemcpyAsync(c->dscalar, &c->nrmL, sizeof(double), cudaMemcpyHostToDevice, s));
+  {  // SELL-32-sigma layout of the short rows (kernels.cuh row engine)
+    constexpr int kSigma = 256;
+    bool uni = cnt_off > 0;
+    const double w0 = cnt_off > 0 ? std::fabs(h_w[0]) : 0.0;
+    for (int64_t k = 0; k < cnt_off && uni; ++k) uni = std::fabs(h_w[(size_t)k]) == w0;
+    c->sell_m0 = scale ? w0 / c->nrmL : w0;  // |C_rj| = fl(|w| / ||L||_F)
+    std::vector<int> perm, scol, win;
+    std::vector<int2> meta;
+    std::vector<double> sval;
+    for (int64_t w = 0; w < nl; w += kSigma) {
+      win.clear();
+      for (int64_t r = w; r < std::min<int64_t>(nl, w + kSigma); ++r)
+        if (h_rp[(size_t)r + 1] - h_rp[(size_t)r] <= kLongRow) win.push_back((int)r);
+      std::stable_sort(win.begin(), win.end(), [&](int x, int y) {
+        return h_rp[(size_t)x + 1] - h_rp[(size_t)x] > h_rp[(size_t)y + 1] - h_rp[(size_t)y];
+      });
+      for (size_t s0 = 0; s0 < win.size(); s0 += 32) {
+        const int cnt = (int)std::min<size_t>(32, win.size() - s0);
+        const int width = h_rp[(size_t)win[s0] + 1] - h_rp[(size_t)win[s0]];
+        meta.push_back(make_int2((int)scol.size(), width));
+        for (int j = 0; j < width; ++j)
+          for (int l = 0; l < 32; ++l) {
+            int cc = -1;
+            double vv = 0.0;
+            if (l < cnt) {
+              const int r = win[s0 + l];
+              const int e = h_rp[(size_t)r] + j;
+              if (e < h_rp[(size_t)r + 1]) {
+                cc = h_col[(size_t)e];
+                const double wv = h_w[(size_t)e];
+                if (uni && wv < 0) cc = (int)((unsigned)cc | 0x80000000u);
+                vv = scale ? wv / c->nrmL : wv;  // = C_rj exactly as k_scale_c forms it
+              }
+            }
+            scol.push_back(cc);
+            if (!uni) sval.push_back(vv);
+          }
+        for (int l = 0; l < 32; ++l) perm.push_back(l < cnt ? win[s0 + l] : -1);
+      }
+      if (scol.size() >= (size_t)INT32_MAX) return bad(SCG_EINVAL, "SELL layout too large");
+    }
+    c->nslice = (int)meta.size();
+    if (!alloc((void **)&c->sell_perm, sizeof(int) * perm.size()) ||
+        !alloc((void **)&c->sell_meta, sizeof(int2) * meta.size()) ||
+        !alloc((void **)&c->sell_col, sizeof(int) * scol.size()) ||
+        (!uni && !alloc((void **)&c->sell_val, sizeof(double) * sval.size())))
+      return bad(SCG_ENOMEM, "SELL layout");
+    CKI(cudaMemcpyAsync(c->sell_perm, perm.data(), sizeof(int) * perm.size(), cudaMemcpyHostToDevice, s));
+    CKI(cudaMemcpyAsync(c->sell_meta, meta.data(), sizeof(int2) * meta.size(), cudaMemcpyHostToDevice, s));
+    CKI(cudaMemcpyAsync(c->sell_col, scol.data(), sizeof(int) * scol.size(), cudaMemcpyHostToDevice, s));
+    if (!uni) CKI(cudaMemcpyAsync(c->sell_val, sval.data(), sizeof(double) * sval.size(), cudaMemcpyHostToDevice, s));
+    CKI(cudaStreamSynchronize(s));  // host vectors go out of scope
+    c->sell_slots = (double)scol.size();
+    c->sell_uniform = uni;
+  }
   launch(c, KC_OTHER, k_scale_c, dim3(gnnz), dim3(kBlock), (const double *)c->wts, (long long)cnt_off,
          (const double *)c->ldiag, (int)nl, (const double *)c->dscalar, scale ? 1 : 0, c->val, c->cdiag);
   launch(c, KC_OTHER, k_omega, dim3(8 * c->nsm), dim3(kBlock), c->Om, (int)nl, (long long)c->rb, (int)R, seed);
@@ -479,13 +565,15 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
 #undef CKI
   // algorithmic bytes per launch
   const double N = (double)n, NL = (double)nl, NNZ = (double)cnt_off;
-  c->kbytes[KC_LANCZOS_A] = 4.0 * (NL + 1) + 12.0 * NNZ + 8.0 * NL + 8.0 * N + 8.0 * NL;
+  // SpMV matrix stream: SELL slots (4 B col [+ 8 B val]) + perm 4 B/row + slice meta + long-row CSR
+  const double mat = c->sell_slots * (c->sell_uniform ? 4.0 : 12.0) + 4.0 * NL + 8.0 * c->nslice;
+  c->kbytes[KC_LANCZOS_A] = mat + 8.0 * NL + 8.0 * N + 8.0 * NL;
   c->kbytes[KC_LANCZOS_B] = 32.0 * NL;
   c->kbytes[KC_TRIDIAG] = 0.0;
-  c->kbytes[KC_LANCZOS_C] = 4.0 * (NL + 1) + 12.0 * NNZ + 8.0 * NL + 8.0 * N + 8.0 * NL + 8.0 * NL + 16.0 * NL;
+  c->kbytes[KC_LANCZOS_C] = mat + 8.0 * NL + 8.0 * N + 8.0 * NL + 8.0 * NL + 16.0 * NL;
   c->kbytes[KC_NORM_X] = 8.0 * NL;
   c->kbytes[KC_COMBINE] = 0.0;  // 8 nl k + 8 nl per launch, accumulated in step()
-  c->kbytes[KC_MONITOR] = 4.0 * (NL + 1) + 12.0 * NNZ + 16.0 * NL + 8.0 * N + 8.0 * NL;
+  c->kbytes[KC_MONITOR] = mat + 16.0 * NL + 8.0 * N + 8.0 * NL;
   c->kbytes[KC_PRIMAL] = 24.0 * NL + 8.0 * NL * R;
   c->kbytes[KC_DUAL_SKETCH] = 56.0 * NL + 16.0 * NL * R;
   for (int k = 0; k < KC_COUNT; ++k) { c->kl[k] = 0; c->kms[k] = 0; c->kbytes_sum[k] = 0; }
@@ -513,9 +601,13 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
   const int nl = (int)c->nl;
   const long long rb = c->rb;
   Csr C{c->rp, c->col, c->val};
-  Rows TT{c->longrows, c->nlong};
+  Rows TT{c->longrows, c->nlong, c->sell_perm, c->sell_meta, c->sell_col, c->sell_val, c->sell_m0, c->nslice};
   const int GT = c->grid_tiles;
   const long long ldw = (long long)c->n;
+  const bool U = c->sell_uniform;
+  auto kA = U ? k_lanczos_a<true> : k_lanczos_a<false>;
+  auto kC = U ? k_lanczos_c<true> : k_lanczos_c<false>;
+  auto kM = U ? k_monitor<true> : k_monitor<false>;
   for (int64_t it = 0; it < T; ++it) {
     const int64_t t = c->t + 1;
     // Alg. 4 line 5 and the q_t schedule (CAC-6), evaluated on the host
@@ -557,11 +649,11 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     // ---- Lanczos pass 1 (Alg. 2 lines 1-9)
     for (int i = 1; i <= q; ++i) {
       const double *Xi = slot(i);
-      launch(c, KC_LANCZOS_A, k_lanczos_a, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, Xi, nl, rb, i, c->a,
+      launch(c, KC_LANCZOS_A, kA, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, Xi, nl, rb, i, c->a,
              c->slots + SLOT_OM, c->sc, 1);
       if (i < q) {
         const double *Xim1 = (i == 1) ? nullptr : slot(i - 1);
-        launch(c, KC_LANCZOS_B, k_lanczos_b, dim3(G), dim3(kBlock), (const double *)c->a, Xi, Xim1, slot(i + 1),
+        launch(c, KC_LANCZOS_B, k_lanczos_b, dim3(c->grid_b), dim3(kBlock), (const double *)c->a, Xi, Xim1, slot(i + 1),
                nl, rb, i, c->slots + SLOT_RHO, c->sc, 1);
       }
     }
@@ -569,24 +661,24 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     launch(c, KC_TRIDIAG, k_tridiag, dim3(1), dim3(32), c->sc, (int)q);
     if (c->store) {  // ---- line 13 from the stored vectors (Remark)
       c->kbytes[KC_COMBINE] = 8.0 * (double)c->nl * (double)q + 8.0 * (double)c->nl;
-      launch(c, KC_COMBINE, k_combine, dim3(c->grid_rows), dim3(kBlock), (const double *)c->Wst, ldw, c->x, nl, rb,
+      launch(c, KC_COMBINE, k_combine, dim3(c->grid_comb), dim3(kBlock), (const double *)c->Wst, ldw, c->x, nl, rb,
              c->slots + SLOT_XX, c->sc, 1);
     } else {  // ---- pass 2 (line 13): regenerate v_2..v_k
       for (int j = 1; j < q; ++j) {
         const double *Xj = slot(j);
         const double *Xjm1 = (j == 1) ? nullptr : slot(j - 1);
-        launch(c, KC_LANCZOS_C, k_lanczos_c, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, Xj, Xjm1,
+        launch(c, KC_LANCZOS_C, kC, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, Xj, Xjm1,
                slot(j + 1), c->x, nl, rb, j, (const DevScalars *)c->sc);
       }
-      launch(c, KC_NORM_X, k_norm_x, dim3(G), dim3(kBlock), (const double *)c->g, c->x, nl, rb,
+      launch(c, KC_NORM_X, k_norm_x, dim3(c->grid_norm), dim3(kBlock), (const double *)c->g, c->x, nl, rb,
              c->slots + SLOT_XX, c->sc, 1);
     }
     // ---- monitors, primal, dual, sketch (Alg. 4 lines 8-10)
-    launch(c, KC_MONITOR, k_monitor, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, (const double *)c->cdiag,
+    launch(c, KC_MONITOR, kM, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, (const double *)c->cdiag,
            (const double *)c->x, c->v, nl, rb, c->slots + SLOT_MON, c->sc, 1);
     launch(c, KC_PRIMAL, k_primal, dim3(c->grid_primal), dim3(kBlock), (const double *)c->v, c->z,
            (const double *)c->Om, nl, c->R, A, c->gpart, c->slots + SLOT_NZ, c->sc, c->dlog, 1);
-    launch(c, KC_DUAL_SKETCH, k_dual_sketch, dim3(G), dim3(kBlock), (const double *)c->z, c->y, c->d,
+    launch(c, KC_DUAL_SKETCH, k_dual_sketch, dim3(c->grid_dual), dim3(kBlock), (const double *)c->z, c->y, c->d,
            (const double *)c->cdiag, (const double *)c->v, c->S, c->g, nl, rb, c->R, A, c->seed,
            c->slots + SLOT_NU0, c->sc, 1);
     c->t = t;
@@ -646,8 +738,8 @@ scg_status sketchycgal_apply_D(scg_ctx *c, const double *xh, double *yh) {
   CK(cudaMalloc(&dy, sizeof(double) * c->nl));
   CK(cudaMemcpy(dx, xh, sizeof(double) * c->n, cudaMemcpyHostToDevice));
   Csr C{c->rp, c->col, c->val};
-  Rows TT{c->longrows, c->nlong};
-  launch(c, KC_OTHER, k_apply_d, dim3(c->grid_tiles), dim3(kBlock), C, TT, (const double *)c->d, (const double *)dx,
+  Rows TT{c->longrows, c->nlong, c->sell_perm, c->sell_meta, c->sell_col, c->sell_val, c->sell_m0, c->nslice};
+  launch(c, KC_OTHER, c->sell_uniform ? k_apply_d<true> : k_apply_d<false>, dim3(c->grid_tiles), dim3(kBlock), C, TT, (const double *)c->d, (const double *)dx,
          (int)c->nl, (long long)c->rb, dy);
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaMemcpy(yh, dy, sizeof(double) * c->nl, cudaMemcpyDeviceToHost));

@@ -171,3 +171,9 @@ def test_config3_first_iteration_bitwise(gpu):
     L = si.laplacian("c3")
     g, o = _run_pair(gpu, L, 10, 1, seed=3)
     _assert_trajectory(g, o, 1)
+
+
+def test_shared_divisor_division_is_ieee(gpu):
+    """div_rn (RN(1/b) + two fma corrections) must equal the hardware division bit for bit."""
+    for seed in (1, 2, 3):
+        assert gpu.selftest_division(1 << 26, seed) == 0
