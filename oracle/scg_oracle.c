@@ -21,7 +21,8 @@
  *          dot(a, b) = xsum(fl(a_r * b_r)).
  *   CAC-3  (D x)_r = d_r x_r + sum_{j in N(r), ascending} m_rj x_j, left to right,
  *          acc = fl(d_r * x_r); acc = fma(m_rj, x_j, acc).
- *   CAC-4  Alg. 2 as printed, two-pass, with readings A1-A4.
+ *   CAC-4  Alg. 2 as printed, two-pass, with readings R1-R5; a
+ *          normalization v / rho is evaluated as v * fl(1/rho) (reading R26).
  *   CAC-5  tridiagonal min eigenpair by Sturm multisection + inverse iteration.
  *   CAC-6  scalar schedules evaluated as written in DESIGN.md.
  *
@@ -302,7 +303,8 @@ static void o_lanczos(const o_off *A, const double *d, const double *g, int q, d
   double *vprev = w1, *vcur = w2, *vnext = w3;
   /* lines 1-2: v1 = randn / ||randn|| */
   double nu0 = sqrt(o_dot(g, g, n, &err));
-  for (int64_t r = 0; r < n; ++r) vcur[r] = g[r] / nu0;
+  double rnu0 = 1.0 / nu0; /* v / rho is evaluated as v * fl(1/rho) (reading R26) */
+  for (int64_t r = 0; r < n; ++r) vcur[r] = g[r] * rnu0;
   int k = q;
   for (int i = 1; i <= q; ++i) {
     o_apply(A, d, vcur, a);                            /* M v_i */
@@ -318,7 +320,8 @@ static void o_lanczos(const o_off *A, const double *d, const double *g, int q, d
     double rho = sqrt(o_dot(vnext, vnext, n, &err));    /* line 7 (reading A1) */
     res->rho[i - 1] = rho;
     if (rho <= 0x1p-45 * (fabs(om) + rp)) { k = i; break; } /* line 8 (reading A3) */
-    for (int64_t r = 0; r < n; ++r) vnext[r] = vnext[r] / rho; /* line 9 */
+    double rrho = 1.0 / rho;
+    for (int64_t r = 0; r < n; ++r) vnext[r] = vnext[r] * rrho; /* line 9 */
     double *t = vprev; vprev = vcur; vcur = vnext; vnext = t;
   }
   res->k = k;
@@ -326,23 +329,23 @@ static void o_lanczos(const o_off *A, const double *d, const double *g, int q, d
   oracle_tridiag_mineig(res->omega, res->rho, k, &res->theta, res->svec);
   /* line 13, regenerating v_2..v_k (second pass) */
   vprev = w1; vcur = w2; vnext = w3;
-  for (int64_t r = 0; r < n; ++r) vcur[r] = g[r] / nu0;
+  for (int64_t r = 0; r < n; ++r) vcur[r] = g[r] * rnu0;
   for (int64_t r = 0; r < n; ++r) v[r] = res->svec[0] * vcur[r];
   for (int i = 1; i < k; ++i) {
     o_apply(A, d, vcur, a);
     double om = res->omega[i - 1];
     double rp = i >= 2 ? res->rho[i - 2] : 0.0;
-    double rho = res->rho[i - 1];
+    double rrho = 1.0 / res->rho[i - 1];
     for (int64_t r = 0; r < n; ++r) {
       double w = fma(-om, vcur[r], a[r]);
       if (i >= 2) w = fma(-rp, vprev[r], w);
-      vnext[r] = w / rho;
+      vnext[r] = w * rrho;
     }
     for (int64_t r = 0; r < n; ++r) v[r] = fma(res->svec[i], vnext[r], v[r]);
     double *t = vprev; vprev = vcur; vcur = vnext; vnext = t;
   }
-  double nx = sqrt(o_dot(v, v, n, &err));
-  for (int64_t r = 0; r < n; ++r) v[r] = v[r] / nx;
+  double rnx = 1.0 / sqrt(o_dot(v, v, n, &err));
+  for (int64_t r = 0; r < n; ++r) v[r] = v[r] * rnx;
   res->err = err;
 }
 

@@ -48,6 +48,7 @@ struct Csr {
 };
 
 // ---------------------------------------------------------------- division
+// (Diagnostics only since the contract evaluates v / rho as v * fl(1/rho), R26.)
 // a / b, correctly rounded (IEEE), for a divisor b shared by many quotients:
 // rb = RN(1/b) is computed once; two Markstein corrections with exact fma
 // residuals r = a - q b give RN(a / b) for normal-range operands (tested
@@ -74,8 +75,14 @@ __device__ __forceinline__ double div_rn(double a, double b, double rb) {
 #ifndef SCG_CH
 #define SCG_CH 4
 #endif
+#ifndef SCG_TMA
+#define SCG_TMA 0  // TMA-staged SELL engine (experimental: slower than the register pipeline on c3)
+#endif
+#ifndef SCG_PIPE
+#define SCG_PIPE 1
+#endif
 #ifndef SCG_MINB
-#define SCG_MINB 3
+#define SCG_MINB 2
 #endif
 constexpr int kLongRow = 32;
 constexpr int kChunk = SCG_CH;   // entries of a row loaded per round
@@ -93,7 +100,13 @@ struct Rows {
   const double *sval;   // per-slot values, or nullptr when all |C_rj| equal m0
   double m0;
   int nslice;
+  // windows of kWin consecutive rows (the SELL sorting windows): window w holds
+  // slices [wstart[w], wstart[w+1])
+  const int *wstart;
+  int nwin;
 };
+
+constexpr int kWin = 1024;  // rows per window (= SELL sorting window sigma)
 
 template <int NC>
 struct RowOut {
@@ -111,7 +124,7 @@ __device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double
   const int e0 = __ldg(&C.rp[r]), e1 = __ldg(&C.rp[r + 1]);
   const double rden = 1.0 / den;
   o.r = r;
-  o.xr = div_rn(X[rb + r], den, rden);
+  o.xr = (X[rb + r]) * rden;
   o.s[0] = diag0[r] * o.xr;
   if (NC > 1) o.s[NC - 1] = diag1[r] * o.xr;
   int e = e0 + lane;
@@ -120,7 +133,7 @@ __device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double
   double xn = e < e1 ? __ldg(&X[cn]) : 0.0;
   for (int base = e0; base < e1; base += 32) {
     const int cnt = min(32, e1 - base);
-    const double m = mn, x = div_rn(xn, den, rden);
+    const double m = mn, x = (xn) * rden;
     // prefetch the next round before running this round's chain
     e = base + 32 + lane;
     if (e < e1) { cn = __ldg(&C.col[e]); mn = __ldg(&C.val[e]); xn = __ldg(&X[cn]); }
@@ -155,10 +168,216 @@ __device__ __forceinline__ void sell_fma_chunk(const Rows &RL, const int (&cc)[k
   for (int u = 0; u < kChunk; ++u)
     if (cc[u] != -1) {
       const double m = UNI ? (cc[u] < 0 ? -RL.m0 : RL.m0) : vv[u];
-      const double x = div_rn(xg[u], den, rden);  // v = w / rho (Alg. 2 line 9), formed on the fly
+      const double x = (xg[u]) * rden;  // v = w / rho (Alg. 2 line 9), formed on the fly
 #pragma unroll
       for (int c = 0; c < NC; ++c) o.s[c] = fma(m, x, o.s[c]);
     }
+}
+
+// ---------------------------------------------------------------- TMA-staged SELL engine
+// A block walks windows of kWin consecutive rows.  For each window one thread
+// issues bulk asynchronous copies (cp.async.bulk, completion on an mbarrier) of
+// the window's SELL columns (+ values), slice-to-row map, diagonal(s) and own
+// entries of the gathered vector into a shared-memory stage; two stages, so the
+// next window streams in while this one is computed.  Threads then read their
+// row's slots from shared memory and issue only the random gathers x[col] to
+// global memory (two slices per warp, all gathers of a chunk in flight).
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, unsigned long long *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int NC, bool UNI>
+struct TmaStage {
+  static constexpr int kCap = UNI ? 4096 : 2048;  // SELL slots per window
+  int cols[kCap];
+  double vals[UNI ? 2 : kCap];
+  int perm[kWin];
+  double d0[kWin];
+  double d1[NC > 1 ? kWin : 2];
+  double xo[kWin];
+};
+
+template <int NC, bool UNI>
+struct TmaSmem {
+  TmaStage<NC, UNI> st[2];
+  unsigned long long bar[2];
+};
+
+// Issue the copies of window `win` into `st` (thread 0 only).
+template <int NC, bool UNI>
+__device__ __forceinline__ void tma_issue(const Rows &RL, const double *X, const double *diag0,
+                                          const double *diag1, long long rb, int win, TmaStage<NC, UNI> &st,
+                                          unsigned long long *bar) {
+  const int s0 = __ldg(&RL.wstart[win]), s1 = __ldg(&RL.wstart[win + 1]);
+  const int nsl = s1 - s0;
+  int slots = 0, slot0 = 0;
+  if (nsl > 0) {
+    slot0 = __ldg(&RL.meta[s0].x);
+    const int2 ml = __ldg(&RL.meta[s1 - 1]);
+    slots = ml.x + 32 * ml.y - slot0;
+  }
+  if (nsl == 0 || slots > TmaStage<NC, UNI>::kCap) {  // empty or oversized: consumers read global memory
+    mbar_arrive(bar);
+    return;
+  }
+  const uint32_t rowb = (uint32_t)(kWin * sizeof(double));
+  uint32_t bytes = (uint32_t)slots * 4u + (uint32_t)nsl * 128u + 2u * rowb;
+  if (!UNI) bytes += (uint32_t)slots * 8u;
+  if (NC > 1) bytes += rowb;
+  mbar_arrive_tx(bar, bytes);
+  if (slots > 0) bulk_g2s(st.cols, RL.scol + slot0, (uint32_t)slots * 4u, bar);
+  if (!UNI && slots > 0) bulk_g2s(st.vals, RL.sval + slot0, (uint32_t)slots * 8u, bar);
+  bulk_g2s(st.perm, RL.perm + (long long)s0 * 32, (uint32_t)nsl * 128u, bar);
+  const long long r0 = (long long)win * kWin;
+  bulk_g2s(st.d0, diag0 + r0, rowb, bar);
+  if (NC > 1) bulk_g2s(st.d1, diag1 + r0, rowb, bar);
+  bulk_g2s(st.xo, X + rb + r0, rowb, bar);
+}
+
+// Up to kQ slices (sl0 + 8 q) of one warp, all gathers in flight together; the
+// pointers select shared (staged) or global data.
+template <int NC>
+struct QOf {
+  static constexpr int v = NC == 1 ? 4 : 2;
+};
+template <int NC, bool UNI, class Epi>
+__device__ __forceinline__ void tma_quad(const Rows &RL, const int *colp, const double *valp, int slot0,
+                                         const int *permp, int s0, const double *d0p, const double *d1p,
+                                         const double *xop, int r0, const double *__restrict__ X, double rden,
+                                         int sl0, int s1, int lane, Epi &epi) {
+  constexpr int kQ = QOf<NC>::v;
+  int rq[kQ];
+  int2 mq[kQ];
+  RowOut<NC> o[kQ];
+  int wmax = 0;
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) {
+    const int sl = sl0 + 8 * q;
+    rq[q] = -1;
+    mq[q] = make_int2(0, 0);
+    if (sl < s1) {
+      rq[q] = permp[(sl - s0) * 32 + lane];
+      mq[q] = __ldg(&RL.meta[sl]);
+    }
+    wmax = mq[q].y > wmax ? mq[q].y : wmax;
+    o[q].r = rq[q];
+    const int rl = rq[q] - r0;
+    const double xv = rq[q] >= 0 ? xop[rl] : 0.0;
+    o[q].xr = xv * rden;
+    o[q].s[0] = (rq[q] >= 0 ? d0p[rl] : 0.0) * o[q].xr;
+    if (NC > 1) o[q].s[NC - 1] = (rq[q] >= 0 ? d1p[rl] : 0.0) * o[q].xr;
+  }
+  for (int j0 = 0; j0 < wmax; j0 += kChunk) {
+    // phase 1: all gathers of this chunk for the kQ slices (columns read from shared memory)
+    double gq[kQ][kChunk];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q)
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u)
+        if (j0 + u < mq[q].y) {
+          const int c = colp[mq[q].x - slot0 + (j0 + u) * 32 + lane];
+          if (c != -1) gq[q][u] = __ldg(&X[c & 0x7fffffff]);
+        }
+    // phase 2: the CAC-3 chains (columns re-read from shared memory)
+#pragma unroll
+    for (int q = 0; q < kQ; ++q)
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u)
+        if (j0 + u < mq[q].y) {
+          const int e = mq[q].x - slot0 + (j0 + u) * 32 + lane;
+          const int c = colp[e];
+          if (c != -1) {
+            const double m = UNI ? (c < 0 ? -RL.m0 : RL.m0) : valp[e];
+            const double x = gq[q][u] * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
+#pragma unroll
+            for (int cc = 0; cc < NC; ++cc) o[q].s[cc] = fma(m, x, o[q].s[cc]);
+          }
+        }
+  }
+#pragma unroll
+  for (int q = 0; q < kQ; ++q)
+    if (rq[q] >= 0) epi(o[q]);
+}
+
+template <int NC, bool UNI, class Epi>
+__device__ __forceinline__ void spmv_tma(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
+                                         const double *__restrict__ diag0, const double *__restrict__ diag1,
+                                         long long rb, Epi &epi, TmaSmem<NC, UNI> &sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if ((int)blockIdx.x < RL.nwin) tma_issue<NC, UNI>(RL, X, diag0, diag1, rb, blockIdx.x, sm.st[0], &sm.bar[0]);
+    if ((int)(blockIdx.x + gridDim.x) < RL.nwin)
+      tma_issue<NC, UNI>(RL, X, diag0, diag1, rb, blockIdx.x + gridDim.x, sm.st[1], &sm.bar[1]);
+  }
+  // long rows first (warp per row), overlapping the first copies
+  {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwg = (gridDim.x * blockDim.x) >> 5;
+    for (int w = gw; w < RL.nlong; w += nwg) {
+      RowOut<NC> o;
+      long_row_chain<NC>(C, RL.longrows[w], X, den, diag0, diag1, rb, o);
+      if (lane == 0) epi(o);
+    }
+  }
+  const double rden = 1.0 / den;
+  int it = 0;
+  for (int win = blockIdx.x; win < RL.nwin; win += gridDim.x, ++it) {
+    const int stg = it & 1;
+    mbar_wait(&sm.bar[stg], (uint32_t)((it >> 1) & 1));
+    TmaStage<NC, UNI> &st = sm.st[stg];
+    const int s0 = __ldg(&RL.wstart[win]), s1 = __ldg(&RL.wstart[win + 1]);
+    const int nsl = s1 - s0;
+    if (nsl > 0) {
+      const int slot0 = __ldg(&RL.meta[s0].x);
+      const int2 ml = __ldg(&RL.meta[s1 - 1]);
+      const bool big = ml.x + 32 * ml.y - slot0 > TmaStage<NC, UNI>::kCap;
+      const int r0 = win * kWin;
+      for (int b = warp; b < nsl; b += 8 * QOf<NC>::v) {
+        if (!big)
+          tma_quad<NC, UNI>(RL, st.cols, st.vals, slot0, st.perm, s0, st.d0, st.d1, st.xo, r0, X, rden, s0 + b, s1,
+                            lane, epi);
+        else
+          tma_quad<NC, UNI>(RL, RL.scol + slot0, RL.sval ? RL.sval + slot0 : nullptr, slot0,
+                            RL.perm + (long long)s0 * 32, s0, diag0 + r0, diag1 ? diag1 + r0 : nullptr,
+                            X + rb + r0, r0, X, rden, s0 + b, s1, lane, epi);
+      }
+    }
+    __syncthreads();  // stage fully consumed
+    if (threadIdx.x == 0 && win + 2 * (int)gridDim.x < RL.nwin)
+      tma_issue<NC, UNI>(RL, X, diag0, diag1, rb, win + 2 * gridDim.x, st, &sm.bar[stg]);
+  }
 }
 
 // Visit every row of this rank once: epi(RowOut) is called by the owning thread
@@ -176,64 +395,115 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
     if (lane == 0) epi(o);
   }
   const double rden = 1.0 / den;
-  // SELL slices, software-pipelined: slice metadata two slices ahead, the first
-  // chunk of columns (and the own-row entries) one slice ahead, so each step
-  // waits on one memory round trip (the gathers) instead of three.
-  const int ns = RL.nslice;
-  int sl = gw;
-  int pr = -1, pn = -1;
-  int2 mr = make_int2(0, 0), mn = make_int2(0, 0);
-  if (sl < ns) { pr = __ldg(&RL.perm[sl * 32 + lane]); mr = __ldg(&RL.meta[sl]); }
-  if (sl + nw < ns) { pn = __ldg(&RL.perm[(sl + nw) * 32 + lane]); mn = __ldg(&RL.meta[sl + nw]); }
-  int cc[kChunk];
-  double vv[kChunk];
-  double xo = 0.0, dg0 = 0.0, dg1 = 0.0;
-  sell_load_chunk<UNI>(RL, mr, 0, lane, cc, vv);
-  if (pr >= 0) {
-    xo = X[rb + pr];
-    dg0 = diag0[pr];
-    if (NC > 1) dg1 = diag1[pr];
-  }
-  while (sl < ns) {
-    double xg[kChunk];
-#pragma unroll
-    for (int u = 0; u < kChunk; ++u)
-      if (cc[u] != -1) xg[u] = __ldg(&X[cc[u] & 0x7fffffff]);
-    const int sln = sl + nw;
-    int ccn[kChunk];
-    double vvn[kChunk];
-    double xon = 0.0, dgn0 = 0.0, dgn1 = 0.0;
-    sell_load_chunk<UNI>(RL, mn, 0, lane, ccn, vvn);  // width 0 when sln >= ns
-    if (pn >= 0) {
-      xon = X[rb + pn];
-      dgn0 = diag0[pn];
-      if (NC > 1) dgn1 = diag1[pn];
-    }
-    int pnn = -1;
-    int2 mnn = make_int2(0, 0);
-    if (sln + nw < ns) { pnn = __ldg(&RL.perm[(sln + nw) * 32 + lane]); mnn = __ldg(&RL.meta[sln + nw]); }
+#if SCG_PIPE == 0
+  // SELL slices, one per warp step; latency hidden by occupancy (few registers)
+  for (int sl = gw; sl < RL.nslice; sl += nw) {
+    const int p0 = __ldg(&RL.perm[sl * 32 + lane]);
+    const int2 m0 = __ldg(&RL.meta[sl]);
     RowOut<NC> o;
-    o.r = pr;
-    o.xr = div_rn(xo, den, rden);
-    o.s[0] = dg0 * o.xr;
-    if (NC > 1) o.s[NC - 1] = dg1 * o.xr;
-    sell_fma_chunk<NC, UNI>(RL, cc, vv, xg, den, rden, o);
-    for (int j0 = kChunk; j0 < mr.y; j0 += kChunk) {  // rows longer than one chunk
-      int c2[kChunk];
-      double v2[kChunk], x2[kChunk];
-      sell_load_chunk<UNI>(RL, mr, j0, lane, c2, v2);
+    o.r = p0;
+    double xo = 0.0, d0 = 0.0, d1 = 0.0;
+    if (p0 >= 0) { xo = X[rb + p0]; d0 = diag0[p0]; if (NC > 1) d1 = diag1[p0]; }
+    for (int j0 = 0; j0 < m0.y; j0 += kChunk) {
+      int cx[kChunk];
+      double vx[kChunk], xx[kChunk];
+      sell_load_chunk<UNI>(RL, m0, j0, lane, cx, vx);
 #pragma unroll
       for (int u = 0; u < kChunk; ++u)
-        if (c2[u] != -1) x2[u] = __ldg(&X[c2[u] & 0x7fffffff]);
-      sell_fma_chunk<NC, UNI>(RL, c2, v2, x2, den, rden, o);
+        if (cx[u] != -1) xx[u] = __ldg(&X[cx[u] & 0x7fffffff]);
+      if (j0 == 0) {
+        o.xr = (xo) * rden;
+        o.s[0] = d0 * o.xr;
+        if (NC > 1) o.s[NC - 1] = d1 * o.xr;
+      }
+      sell_fma_chunk<NC, UNI>(RL, cx, vx, xx, den, rden, o);
     }
-    if (pr >= 0) epi(o);
-    pr = pn; mr = mn; pn = pnn; mn = mnn;
-#pragma unroll
-    for (int u = 0; u < kChunk; ++u) { cc[u] = ccn[u]; vv[u] = vvn[u]; }
-    xo = xon; dg0 = dgn0; dg1 = dgn1;
-    sl = sln;
+    if (m0.y == 0) {
+      o.xr = (xo) * rden;
+      o.s[0] = d0 * o.xr;
+      if (NC > 1) o.s[NC - 1] = d1 * o.xr;
+    }
+    if (p0 >= 0) epi(o);
   }
+#else
+  // SELL slices, software-pipelined three deep: in the step that computes slice i
+  // the gathers and own-row loads of slice i+1, the column loads of slice i+2 and
+  // the (perm, meta) loads of slice i+3 are issued, so a step never waits on a
+  // load issued in the same step.
+  const int *__restrict__ perm = RL.perm;
+  const int2 *__restrict__ meta = RL.meta;
+  // each block owns a contiguous range of slices (neighbouring rows share their
+  // gathered entries in the SM's L1); its warps interleave within the range
+  const int per = (RL.nslice + gridDim.x - 1) / gridDim.x;
+  const int ns = min(RL.nslice, (int)(blockIdx.x + 1) * per);
+  const int wstep = blockDim.x >> 5;
+  int sl = blockIdx.x * per + (threadIdx.x >> 5);
+  // stage 3 (perm/meta), stage 2 (+cols), stage 1 (+gathers, own), stage 0 (compute)
+  int p0 = -1, p1 = -1, p2 = -1, p3 = -1;
+  int2 m0 = make_int2(0, 0), m1 = m0, m2 = m0, m3 = m0;
+  if (sl < ns) { p0 = __ldg(&perm[sl * 32 + lane]); m0 = __ldg(&meta[sl]); }
+  if (sl + wstep < ns) { p1 = __ldg(&perm[(sl + wstep) * 32 + lane]); m1 = __ldg(&meta[sl + wstep]); }
+  if (sl + 2 * wstep < ns) { p2 = __ldg(&perm[(sl + 2 * wstep) * 32 + lane]); m2 = __ldg(&meta[sl + 2 * wstep]); }
+  if (sl + 3 * wstep < ns) { p3 = __ldg(&perm[(sl + 3 * wstep) * 32 + lane]); m3 = __ldg(&meta[sl + 3 * wstep]); }
+  int c0[kChunk], c1[kChunk], c2[kChunk];
+  double v0[kChunk], v1[kChunk], v2[kChunk];
+  sell_load_chunk<UNI>(RL, m0, 0, lane, c0, v0);
+  sell_load_chunk<UNI>(RL, m1, 0, lane, c1, v1);
+  sell_load_chunk<UNI>(RL, m2, 0, lane, c2, v2);
+  double g0[kChunk], g1[kChunk];
+#pragma unroll
+  for (int u = 0; u < kChunk; ++u)
+    if (c0[u] != -1) g0[u] = __ldg(&X[c0[u] & 0x7fffffff]);
+  double xo0 = 0.0, d00 = 0.0, d10 = 0.0, xo1 = 0.0, d01 = 0.0, d11 = 0.0;
+  if (p0 >= 0) { xo0 = X[rb + p0]; d00 = diag0[p0]; if (NC > 1) d10 = diag1[p0]; }
+  while (sl < ns) {
+    // stage 1: gathers and own-row loads of slice i+1
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u)
+#ifdef SCG_EXP_NOGATHER
+      if (c1[u] != -1) g1[u] = __ldg(&X[rb + (sl + wstep) * 32 + lane]);
+#else
+      if (c1[u] != -1) g1[u] = __ldg(&X[c1[u] & 0x7fffffff]);
+#endif
+    if (p1 >= 0) { xo1 = X[rb + p1]; d01 = diag0[p1]; if (NC > 1) d11 = diag1[p1]; }
+    // stage 2: columns of slice i+3 (meta known), stage 3: perm/meta of slice i+4
+    int c3[kChunk];
+    double v3[kChunk];
+    sell_load_chunk<UNI>(RL, m3, 0, lane, c3, v3);
+    int p4 = -1;
+    int2 m4 = make_int2(0, 0);
+    const int sl4 = sl + 4 * wstep;
+    if (sl4 < ns) { p4 = __ldg(&perm[sl4 * 32 + lane]); m4 = __ldg(&meta[sl4]); }
+    // stage 0: compute slice i
+    RowOut<NC> o;
+    o.r = p0;
+    o.xr = (xo0) * rden;
+    o.s[0] = d00 * o.xr;
+    if (NC > 1) o.s[NC - 1] = d10 * o.xr;
+    sell_fma_chunk<NC, UNI>(RL, c0, v0, g0, den, rden, o);
+    for (int j0 = kChunk; j0 < m0.y; j0 += kChunk) {  // rows longer than one chunk
+      int cx[kChunk];
+      double vx[kChunk], xx[kChunk];
+      sell_load_chunk<UNI>(RL, m0, j0, lane, cx, vx);
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u)
+        if (cx[u] != -1) xx[u] = __ldg(&X[cx[u] & 0x7fffffff]);
+      sell_fma_chunk<NC, UNI>(RL, cx, vx, xx, den, rden, o);
+    }
+    if (p0 >= 0) epi(o);
+    // rotate the pipeline
+    p0 = p1; p1 = p2; p2 = p3; p3 = p4;
+    m0 = m1; m1 = m2; m2 = m3; m3 = m4;
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) {
+      c0[u] = c1[u]; c1[u] = c2[u]; c2[u] = c3[u];
+      v0[u] = v1[u]; v1[u] = v2[u]; v2[u] = v3[u];
+      g0[u] = g1[u];
+    }
+    xo0 = xo1; d00 = d01; d10 = d11;
+    sl += wstep;
+  }
+#endif
   (void)nl;
 }
 
@@ -359,12 +629,14 @@ struct EpiA {
   int err;
   __device__ __forceinline__ void operator()(const RowOut<1> &o) {
     a[o.r] = o.s[0];
+#ifndef SCG_EXP_NODOT
     xwin_add(acc[0], o.xr * o.s[0], err, blk);
+#endif
   }
 };
 
 template <bool UNI>
-__global__ void __launch_bounds__(kBlock, SCG_MINB) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
+__global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ X, int nl, long long rb, int i,
                                                          double *__restrict__ a, XSlot *slot, DevScalars *sc,
                                                          int finalize) {
@@ -377,7 +649,12 @@ __global__ void __launch_bounds__(kBlock, SCG_MINB) k_lanczos_a(Csr C, Rows RL, 
   epi.blk = xb.l[0];
   xwin_init(epi.acc[0]);
   epi.err = 0;
+#if SCG_TMA
+  extern __shared__ __align__(128) unsigned char smraw[];
+  spmv_tma<1, UNI>(C, RL, X, den, d, nullptr, rb, epi, *reinterpret_cast<TmaSmem<1, UNI> *>(smraw));
+#else
   spmv_rows<1, UNI>(C, RL, X, den, d, nullptr, rb, nl, epi);
+#endif
   int err = epi.err;
   XWin (&acc)[1] = epi.acc;
   if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
@@ -429,9 +706,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_lanczos_b(const double *__restric
     for (int u = 0; u < 4; ++u) {
       const int r = r0 + u * stride;
       if (r < nl) {
-        const double vi = div_rn(xi[u], den, rden);
+        const double vi = (xi[u]) * rden;
         double w = fma(-om, vi, av[u]);
-        if (i >= 2) w = fma(-den, div_rn(xm[u], denm, rdenm), w);  // rho_{i-1} = rho[i-1] = den
+        if (i >= 2) w = fma(-den, (xm[u]) * rdenm, w);  // rho_{i-1} = rho[i-1] = den
         Xip1[rb + r] = w;
         xwin_add(acc[0], w * w, err, xb.l[0]);
       }
@@ -578,27 +855,32 @@ struct EpiC {
   double *Xjp1, *x;
   long long rb;
   int j;
-  double om, den, denm, rhoj, s1, sj1, rrhoj;
+  double om, den, denm, rhoj, s1, sj1, rrhoj, rdenm;
   __device__ __forceinline__ void operator()(const RowOut<1> &o) {
     const double vj = o.xr;
     double w = fma(-om, vj, o.s[0]);
-    if (j >= 2) w = fma(-den, div_rn(Xjm1[rb + o.r], denm, 1.0 / denm), w);
+    if (j >= 2) w = fma(-den, Xjm1[rb + o.r] * rdenm, w);
     Xjp1[rb + o.r] = w;
-    const double vn = div_rn(w, rhoj, rrhoj);
+    const double vn = (w) * rrhoj;
     const double xr = j == 1 ? s1 * vj : x[rb + o.r];
     x[rb + o.r] = fma(sj1, vn, xr);
   }
 };
 
 template <bool UNI>
-__global__ void __launch_bounds__(kBlock, SCG_MINB) k_lanczos_c(Csr C, Rows RL, const double *__restrict__ d,
+__global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_c(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ Xj, const double *Xjm1,
                                                          double *Xjp1, double *__restrict__ x, int nl, long long rb,
                                                          int j, const DevScalars *__restrict__ sc) {
   if (j >= sc->k) return;  // sc->k holds the effective k after k_tridiag
   EpiC epi{Xjm1, Xjp1, x, rb, j, sc->om[j - 1], sc->rho[j - 1], j >= 2 ? sc->rho[j - 2] : 1.0, sc->rho[j],
-           sc->s[0], sc->s[j], 1.0 / sc->rho[j]};
+           sc->s[0], sc->s[j], 1.0 / sc->rho[j], 1.0 / (j >= 2 ? sc->rho[j - 2] : 1.0)};
+#if SCG_TMA
+  extern __shared__ __align__(128) unsigned char smraw[];
+  spmv_tma<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, epi, *reinterpret_cast<TmaSmem<1, UNI> *>(smraw));
+#else
   spmv_rows<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, nl, epi);
+#endif
 }
 
 // Stored-vector mode (Remark "Time-storage tradeoff"): the
@@ -622,16 +904,16 @@ __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict_
   int err = 0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
     const double *w = Wst + rb + r;
-    double xr = s_s[0] * div_rn(__ldg(w), s_r[0], s_rr[0]);
+    double xr = s_s[0] * (__ldg(w) * s_rr[0]);
     int j = 1;
     for (; j + 4 <= k; j += 4) {
       double wv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) wv[u] = __ldg(w + (long long)(j + u) * ldw);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) xr = fma(s_s[j + u], div_rn(wv[u], s_r[j + u], s_rr[j + u]), xr);
+      for (int u = 0; u < 4; ++u) xr = fma(s_s[j + u], (wv[u]) * s_rr[j + u], xr);
     }
-    for (; j < k; ++j) xr = fma(s_s[j], div_rn(__ldg(w + (long long)j * ldw), s_r[j], s_rr[j]), xr);
+    for (; j < k; ++j) xr = fma(s_s[j], __ldg(w + (long long)j * ldw) * s_rr[j], xr);
     x[rb + r] = xr;
     xwin_add(acc[0], xr * xr, err, xb.l[0]);
   }
@@ -646,7 +928,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict_
 __global__ void __launch_bounds__(kBlock) k_norm_x(const double *__restrict__ g, double *__restrict__ x, int nl,
                                                    long long rb, XSlot *slot, DevScalars *sc, int finalize) {
   const bool k1 = sc->k == 1;
-  const double s1 = sc->s[0], den = sc->rho[0];
+  const double s1 = sc->s[0], rden = 1.0 / sc->rho[0];
   __shared__ XBlk<1> xb;
   xblk_init<1>(xb);
   XWin acc[1];
@@ -665,7 +947,7 @@ __global__ void __launch_bounds__(kBlock) k_norm_x(const double *__restrict__ g,
       const int r = r0 + u * stride;
       if (r < nl) {
         double xr = xv[u];
-        if (k1) { xr = s1 * (xr / den); x[rb + r] = xr; }
+        if (k1) { xr = s1 * (xr * rden); x[rb + r] = xr; }
         xwin_add(acc[0], xr * xr, err, xb.l[0]);
       }
     }
@@ -707,7 +989,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
   xwin_init(epi.acc[1]);
   xwin_init(epi.acc[2]);
   epi.err = 0;
+#if SCG_TMA
+  extern __shared__ __align__(128) unsigned char smraw[];
+  spmv_tma<2, UNI>(C, RL, x, nu, d, cdiag, rb, epi, *reinterpret_cast<TmaSmem<2, UNI> *>(smraw));
+#else
   spmv_rows<2, UNI>(C, RL, x, nu, d, cdiag, rb, nl, epi);
+#endif
   int err = epi.err;
   XWin (&acc)[3] = epi.acc;
   if (commit_and_ticket<3>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
@@ -995,7 +1282,12 @@ __global__ void __launch_bounds__(kBlock) k_apply_d(Csr C, Rows RL, const double
                                                     const double *__restrict__ X, int nl, long long rb,
                                                     double *__restrict__ y) {
   EpiY epi{y};
+#if SCG_TMA
+  extern __shared__ __align__(128) unsigned char smraw[];
+  spmv_tma<1, UNI>(C, RL, X, 1.0, d, nullptr, rb, epi, *reinterpret_cast<TmaSmem<1, UNI> *>(smraw));
+#else
   spmv_rows<1, UNI>(C, RL, X, 1.0, d, nullptr, rb, nl, epi);
+#endif
 }
 
 // Self-test: div_rn against the hardware IEEE division on pseudo-random operands

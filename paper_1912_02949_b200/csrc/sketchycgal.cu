@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -44,7 +45,7 @@ struct scg_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int nsm = 148;
-  int64_t n = 0, nl = 0, rb = 0;
+  int64_t n = 0, nl = 0, rb = 0, npad = 0;
   long long nnz_off = 0;
   int R = 0;
   uint32_t flags = 0;
@@ -70,6 +71,10 @@ struct scg_ctx {
   double *sell_val = nullptr;
   double sell_m0 = 0.0;
   int nslice = 0;
+  int *sell_wstart = nullptr;
+  int nwin = 0;
+  size_t smem1 = 0, smem2 = 0;
+  int grid_mon = 1;
   double sell_slots = 0.0;
   bool sell_uniform = false;
   int nlong = 0;
@@ -145,7 +150,15 @@ cudaEvent_t ev_get(scg_ctx *c) {
 }
 
 template <typename Kern, typename... Args>
+void launch_smem(scg_ctx *c, int cls, Kern kern, dim3 grid, dim3 block, size_t smem, Args... args);
+
+template <typename Kern, typename... Args>
 void launch(scg_ctx *c, int cls, Kern kern, dim3 grid, dim3 block, Args... args) {
+  launch_smem(c, cls, kern, grid, block, 0, args...);
+}
+
+template <typename Kern, typename... Args>
+void launch_smem(scg_ctx *c, int cls, Kern kern, dim3 grid, dim3 block, size_t smem, Args... args) {
   const bool prof = (c->flags & SCG_PROFILE) != 0;
   EvPair p{};
   if (prof) {
@@ -155,7 +168,7 @@ void launch(scg_ctx *c, int cls, Kern kern, dim3 grid, dim3 block, Args... args)
     p.cls = cls;
     cudaEventRecord(p.a, c->stream);
   }
-  kern<<<grid, block, 0, c->stream>>>(args...);
+  kern<<<grid, block, smem, c->stream>>>(args...);
   if (prof) {
     cudaEventRecord(p.b, c->stream);
     c->pending.push_back(p);
@@ -333,7 +346,8 @@ void sketchycgal_destroy(scg_ctx *c) {
   void *ptrs[] = {c->rp, c->col, c->val, c->wts, c->ldiag, c->cdiag, c->d, c->z, c->y, c->a, c->v, c->Wst,
                   c->x, c->S, c->Om, c->gpart, c->U, c->tmp1, c->tmp2, c->dmat, c->partial,
                   c->dlam, c->dscalar, c->sc, c->slots, c->dlog, c->longrows,
-                  c->sell_perm, c->sell_col, c->sell_meta, c->sell_val};
+                  c->sell_perm, c->sell_col, c->sell_meta, c->sell_val,
+                  c->sell_wstart};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (auto &p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
@@ -434,7 +448,10 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
     c->own_stream = true;
   }
   auto alloc = [&](void **p, size_t bytes) -> bool { return cudaMalloc(p, bytes ? bytes : 8) == cudaSuccess; };
-  const size_t nb = sizeof(double) * (size_t)n, nlb = sizeof(double) * (size_t)nl;
+  // vectors are padded to whole kWin-row windows (the TMA engine copies whole windows)
+  c->npad = (n + kWin - 1) / kWin * kWin;
+  const int64_t nlpad = (nl + kWin - 1) / kWin * kWin;
+  const size_t nb = sizeof(double) * (size_t)c->npad, nlb = sizeof(double) * (size_t)nlpad;
   bool ok = alloc((void **)&c->rp, sizeof(int) * (nl + 1)) && alloc((void **)&c->col, sizeof(int) * cnt_off) &&
             alloc((void **)&c->val, sizeof(double) * cnt_off) && alloc((void **)&c->wts, sizeof(double) * cnt_off) &&
             alloc((void **)&c->ldiag, nlb) && alloc((void **)&c->cdiag, nlb) && alloc((void **)&c->d, nlb) &&
@@ -498,7 +515,8 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   if (!(c->nrmL > 0) || !std::isfinite(c->nrmL)) return bad(SCG_EINVAL, "||L||_F must be positive and finite");
   CKI(cudaMemcpyAsync(c->dscalar, &c->nrmL, sizeof(double), cudaMemcpyHostToDevice, s));
   {  // SELL-32-sigma layout of the short rows (kernels.cuh row engine)
-    constexpr int kSigma = 256;
+    const int kSigma = SCG_TMA ? kWin : 256;  // sorting window of SELL-32-sigma (= TMA staging window)
+    std::vector<int> wstart;
     bool uni = cnt_off > 0;
     const double w0 = cnt_off > 0 ? std::fabs(h_w[0]) : 0.0;
     for (int64_t k = 0; k < cnt_off && uni; ++k) uni = std::fabs(h_w[(size_t)k]) == w0;
@@ -507,6 +525,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
     std::vector<int2> meta;
     std::vector<double> sval;
     for (int64_t w = 0; w < nl; w += kSigma) {
+      wstart.push_back((int)meta.size());
       win.clear();
       for (int64_t r = w; r < std::min<int64_t>(nl, w + kSigma); ++r)
         if (h_rp[(size_t)r + 1] - h_rp[(size_t)r] <= kLongRow) win.push_back((int)r);
@@ -539,6 +558,10 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
       if (scol.size() >= (size_t)INT32_MAX) return bad(SCG_EINVAL, "SELL layout too large");
     }
     c->nslice = (int)meta.size();
+    wstart.push_back((int)meta.size());
+    c->nwin = (int)wstart.size() - 1;
+    if (!alloc((void **)&c->sell_wstart, sizeof(int) * wstart.size())) return bad(SCG_ENOMEM, "SELL windows");
+    CKI(cudaMemcpyAsync(c->sell_wstart, wstart.data(), sizeof(int) * wstart.size(), cudaMemcpyHostToDevice, s));
     if (!alloc((void **)&c->sell_perm, sizeof(int) * perm.size()) ||
         !alloc((void **)&c->sell_meta, sizeof(int2) * meta.size()) ||
         !alloc((void **)&c->sell_col, sizeof(int) * scol.size()) ||
@@ -551,6 +574,35 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
     CKI(cudaStreamSynchronize(s));  // host vectors go out of scope
     c->sell_slots = (double)scol.size();
     c->sell_uniform = uni;
+  }
+  {  // dynamic shared memory and grids of the TMA-staged SpMV kernels
+    const bool U = c->sell_uniform;
+    c->smem1 = !SCG_TMA ? 0 : (U ? sizeof(TmaSmem<1, true>) : sizeof(TmaSmem<1, false>));
+    c->smem2 = !SCG_TMA ? 0 : (U ? sizeof(TmaSmem<2, true>) : sizeof(TmaSmem<2, false>));
+    auto setsm = [&](const void *k, size_t b) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b); };
+    if (U) {
+      setsm((const void *)k_lanczos_a<true>, c->smem1);
+      setsm((const void *)k_lanczos_c<true>, c->smem1);
+      setsm((const void *)k_apply_d<true>, c->smem1);
+      setsm((const void *)k_monitor<true>, c->smem2);
+    } else {
+      setsm((const void *)k_lanczos_a<false>, c->smem1);
+      setsm((const void *)k_lanczos_c<false>, c->smem1);
+      setsm((const void *)k_apply_d<false>, c->smem1);
+      setsm((const void *)k_monitor<false>, c->smem2);
+    }
+    int oa = 1, om = 1;
+    if (U) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<true>, kBlock, c->smem1);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<true>, kBlock, c->smem2);
+    } else {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<false>, kBlock, c->smem1);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<false>, kBlock, c->smem2);
+    }
+    const int need = SCG_TMA ? std::max(c->nwin, (c->nlong + 7) / 8)
+                             : (int)std::max<int64_t>((c->nslice + 7) / 8, (c->nlong + 7) / 8);
+    c->grid_tiles = std::max(1, std::min(need, std::max(1, oa) * c->nsm));
+    c->grid_mon = std::max(1, std::min(need, std::max(1, om) * c->nsm));
   }
   launch(c, KC_OTHER, k_scale_c, dim3(gnnz), dim3(kBlock), (const double *)c->wts, (long long)cnt_off,
          (const double *)c->ldiag, (int)nl, (const double *)c->dscalar, scale ? 1 : 0, c->val, c->cdiag);
@@ -597,13 +649,14 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     c->dlog = nl;
     c->log_cap = cap;
   }
-  const int G = c->grid_rows;
+
   const int nl = (int)c->nl;
   const long long rb = c->rb;
   Csr C{c->rp, c->col, c->val};
-  Rows TT{c->longrows, c->nlong, c->sell_perm, c->sell_meta, c->sell_col, c->sell_val, c->sell_m0, c->nslice};
+  Rows TT{c->longrows, c->nlong, c->sell_perm, c->sell_meta, c->sell_col, c->sell_val, c->sell_m0, c->nslice,
+          c->sell_wstart, c->nwin};
   const int GT = c->grid_tiles;
-  const long long ldw = (long long)c->n;
+  const long long ldw = (long long)c->npad;
   const bool U = c->sell_uniform;
   auto kA = U ? k_lanczos_a<true> : k_lanczos_a<false>;
   auto kC = U ? k_lanczos_c<true> : k_lanczos_c<false>;
@@ -630,9 +683,9 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       double *nw = nullptr;
       size_t fr = 0, tot = 0;
       cudaMemGetInfo(&fr, &tot);
-      const size_t need = sizeof(double) * (size_t)c->n * cap;
+      const size_t need = sizeof(double) * (size_t)c->npad * cap;
       if (need + (size_t)(1ull << 30) < fr && cudaMalloc(&nw, need) == cudaSuccess) {
-        CK(cudaMemcpyAsync(nw, c->Wst, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpyAsync(nw, c->Wst, sizeof(double) * c->npad, cudaMemcpyDeviceToDevice, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         cudaFree(c->Wst);
         c->Wst = nw;
@@ -649,7 +702,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     // ---- Lanczos pass 1 (Alg. 2 lines 1-9)
     for (int i = 1; i <= q; ++i) {
       const double *Xi = slot(i);
-      launch(c, KC_LANCZOS_A, kA, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, Xi, nl, rb, i, c->a,
+      launch_smem(c, KC_LANCZOS_A, kA, dim3(GT), dim3(kBlock), c->smem1, C, TT, (const double *)c->d, Xi, nl, rb, i, c->a,
              c->slots + SLOT_OM, c->sc, 1);
       if (i < q) {
         const double *Xim1 = (i == 1) ? nullptr : slot(i - 1);
@@ -667,14 +720,14 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       for (int j = 1; j < q; ++j) {
         const double *Xj = slot(j);
         const double *Xjm1 = (j == 1) ? nullptr : slot(j - 1);
-        launch(c, KC_LANCZOS_C, kC, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, Xj, Xjm1,
+        launch_smem(c, KC_LANCZOS_C, kC, dim3(GT), dim3(kBlock), c->smem1, C, TT, (const double *)c->d, Xj, Xjm1,
                slot(j + 1), c->x, nl, rb, j, (const DevScalars *)c->sc);
       }
       launch(c, KC_NORM_X, k_norm_x, dim3(c->grid_norm), dim3(kBlock), (const double *)c->g, c->x, nl, rb,
              c->slots + SLOT_XX, c->sc, 1);
     }
     // ---- monitors, primal, dual, sketch (Alg. 4 lines 8-10)
-    launch(c, KC_MONITOR, kM, dim3(GT), dim3(kBlock), C, TT, (const double *)c->d, (const double *)c->cdiag,
+    launch_smem(c, KC_MONITOR, kM, dim3(c->grid_mon), dim3(kBlock), c->smem2, C, TT, (const double *)c->d, (const double *)c->cdiag,
            (const double *)c->x, c->v, nl, rb, c->slots + SLOT_MON, c->sc, 1);
     launch(c, KC_PRIMAL, k_primal, dim3(c->grid_primal), dim3(kBlock), (const double *)c->v, c->z,
            (const double *)c->Om, nl, c->R, A, c->gpart, c->slots + SLOT_NZ, c->sc, c->dlog, 1);
@@ -734,12 +787,14 @@ scg_status sketchycgal_apply_D(scg_ctx *c, const double *xh, double *yh) {
   if (st) return st;
   // use tmp buffers: x into c->x is not allowed (state); allocate scratch
   double *dx = nullptr, *dy = nullptr;
-  CK(cudaMalloc(&dx, sizeof(double) * c->n));
+  CK(cudaMalloc(&dx, sizeof(double) * c->npad));
   CK(cudaMalloc(&dy, sizeof(double) * c->nl));
   CK(cudaMemcpy(dx, xh, sizeof(double) * c->n, cudaMemcpyHostToDevice));
   Csr C{c->rp, c->col, c->val};
-  Rows TT{c->longrows, c->nlong, c->sell_perm, c->sell_meta, c->sell_col, c->sell_val, c->sell_m0, c->nslice};
-  launch(c, KC_OTHER, c->sell_uniform ? k_apply_d<true> : k_apply_d<false>, dim3(c->grid_tiles), dim3(kBlock), C, TT, (const double *)c->d, (const double *)dx,
+  Rows TT{c->longrows, c->nlong, c->sell_perm, c->sell_meta, c->sell_col, c->sell_val, c->sell_m0, c->nslice,
+          c->sell_wstart, c->nwin};
+  launch_smem(c, KC_OTHER, c->sell_uniform ? k_apply_d<true> : k_apply_d<false>, dim3(c->grid_tiles), dim3(kBlock),
+              c->smem1, C, TT, (const double *)c->d, (const double *)dx,
          (int)c->nl, (long long)c->rb, dy);
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaMemcpy(yh, dy, sizeof(double) * c->nl, cudaMemcpyDeviceToHost));

@@ -1,6 +1,6 @@
 #!/bin/bash
 # print kernel: registers spill-bytes
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 --fmad=false -std=c++17 -Xptxas -v -c -o /tmp/x.o csrc/sketchycgal.cu 2>&1 | python3 -c "
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 --fmad=false -std=c++17 -Xptxas -v -c -o /tmp/x.o paper_1912_02949_b200/csrc/sketchycgal.cu 2>&1 | python3 -c "
 import sys,re
 name=None
 for line in sys.stdin:
