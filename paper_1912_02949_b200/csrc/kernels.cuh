@@ -1026,7 +1026,7 @@ __device__ __forceinline__ double gamma_rule(const IterArgs &A, double nz) {
 
 // z <- (1-eta) z + eta alpha (v o v) (Alg. 4 line 8, primitive 3), ||z - b||^2 (exact),
 // per-block partials of g = v^T Omega (fp64, fixed tree; off the feedback path).
-__global__ void __launch_bounds__(kBlock, 4) k_primal(const double *__restrict__ v, double *__restrict__ z,
+__global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__ v, double *__restrict__ z,
                                                    const double *__restrict__ Om, int nl, int R, IterArgs A,
                                                    double *__restrict__ gpart, XSlot *slot, DevScalars *sc,
                                                    scg_iter_rec *log, int finalize) {
@@ -1036,38 +1036,48 @@ __global__ void __launch_bounds__(kBlock, 4) k_primal(const double *__restrict__
   XWin acc[1];
   xwin_init(acc[0]);
   int err = 0;
-  // one warp handles 32 consecutive rows per step; lane k accumulates g_k (and g_{k+32})
+  // thread-per-row; per-thread partial g_k for 16 columns at a time
+  constexpr int kPR = 1;
+  const int stride = gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwarp = gridDim.x * (kBlock / 32);
-  double gl0 = 0.0, gl1 = 0.0;
-  for (int base = (blockIdx.x * (kBlock / 32) + warp) * 32; base < nl; base += nwarp * 32) {
-    const int r = base + lane;
-    const bool ok = r < nl;
-    const double vr = ok ? v[r] : 0.0;
-    if (ok) {
-      const double h = A.alpha * (vr * vr);
-      const double zr = fma(A.eta, h, A.one_m_eta * z[r]);
-      z[r] = zr;
-      const double e = zr - A.b;
-      xwin_add(acc[0], e * e, err, xb.l[0]);
-    }
-    for (int kc = 0; kc < R; kc += 8) {
-      double p[8];
+  for (int kc = 0; kc < R; kc += 16) {
+    double gp[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) p[u] = (ok && kc + u < R) ? vr * __ldg(&Om[(long long)(kc + u) * nl + r]) : 0.0;
+    for (int u = 0; u < 16; ++u) gp[u] = 0.0;
+    for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < nl; r0 += kPR * stride) {
+      double vr[kPR], zv[kPR], om[kPR][16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int h = 0; h < kPR; ++h) {
+        const int r = r0 + h * stride;
+        vr[h] = r < nl ? v[r] : 0.0;
+        zv[h] = (kc == 0 && r < nl) ? z[r] : 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) p[u] += __shfl_xor_sync(0xffffffffu, p[u], o);
-        const int k = kc + u;
-        if (k < R && lane == (k & 31)) {
-          if (k < 32) gl0 += p[u]; else gl1 += p[u];
+        for (int u = 0; u < 16; ++u) om[h][u] = (r < nl && kc + u < R) ? __ldg(&Om[(long long)(kc + u) * nl + r]) : 0.0;
+      }
+#pragma unroll
+      for (int h = 0; h < kPR; ++h) {
+        const int r = r0 + h * stride;
+        if (r < nl) {
+          if (kc == 0) {
+            const double hv = A.alpha * (vr[h] * vr[h]);
+            const double zr = fma(A.eta, hv, A.one_m_eta * zv[h]);
+            z[r] = zr;
+            const double e = zr - A.b;
+            xwin_add(acc[0], e * e, err, xb.l[0]);
+          }
+#pragma unroll
+          for (int u = 0; u < 16; ++u) gp[u] = fma(vr[h], om[h][u], gp[u]);
         }
       }
     }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      double t = gp[u];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+      if (lane == 0 && kc + u < R) red[warp][kc + u] = t;
+    }
   }
-  if (lane < R) red[warp][lane] = gl0;
-  if (lane + 32 < R) red[warp][lane + 32] = gl1;
   __syncthreads();
   if ((int)threadIdx.x < R) {
     double t = 0.0;
