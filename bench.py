@@ -147,21 +147,37 @@ def run_ours(args, rank, world, local_rank):
     import paper_1912_02949_b200 as scg
     import scg_inputs as si
 
-    if world > 1:
-        raise SystemExit("multi-GPU bench: row-sharded path not in this build")
     torch.cuda.set_device(local_rank)
     L = si.laplacian(args.config)
     c = si.CONFIGS[args.config]
     stream = torch.cuda.Stream()
     W, K = args.warmup, args.steps
+    dkw = {}
+    if world > 1:
+        # one process per GPU: rows sharded over the ranks; torch.distributed only
+        # carries the NCCL unique id, the barriers and the max-over-ranks timing
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(scg.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        dkw = dict(rank=rank, world=world, nccl_id=bytes(uid.cpu().numpy().tobytes()))
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
     with torch.cuda.stream(stream):
         solver = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], profile=True, device=local_rank,
-                                 stream=ctypes_stream(stream))
+                                 stream=ctypes_stream(stream), **dkw)
         solver.step(W)
         solver.synchronize()
         solver.reset_stats()
         l0 = solver.launches
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
         torch.cuda.synchronize()
         with ClockSampler(local_rank) as clk:
             ev0.record(stream)
@@ -169,7 +185,13 @@ def run_ours(args, rank, world, local_rank):
             ev1.record(stream)
             ev1.synchronize()
         solver.synchronize()
+        barrier()
         ms = ev0.elapsed_time(ev1)
+        if world > 1:  # the job's time is the slowest rank's
+            import torch.distributed as dist
+            t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
         launches = solver.launches - l0
         stats = solver.kernel_stats()
         lg = solver.iter_log(W + 1, K)
@@ -191,7 +213,7 @@ def run_ours(args, rank, world, local_rank):
     # end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(scg, si, L, c, K, W, local_rank)
+        e2e = run_e2e(scg, si, L, c, K, W, local_rank, dkw, world)
     cb = None
     if rank == 0 and not args.no_cpu:
         cb = cpu_oracle_sample(args.config, L, args.ref_iters)
@@ -207,6 +229,10 @@ def run_ours(args, rank, world, local_rank):
             "cpu_baseline": cb, "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(launches)}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def ctypes_stream(stream):
@@ -214,24 +240,41 @@ def ctypes_stream(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-def run_e2e(scg, si, L, c, K, W, dev):
+def run_e2e(scg, si, L, c, K, W, dev, dkw, world):
     """Same metric through the C ABI with HOST buffers: init (CSR H2D) + W + K iterations + per-step
-    iteration-record D2H + reconstruct (U, Lambda D2H); value = K / (time of the whole job)."""
+    iteration-record D2H + reconstruct (U, Lambda D2H); value = K / (time of the whole job), the
+    slowest rank's time when sharded."""
     import torch
+    if dkw:  # a fresh communicator for the second context
+        import torch.distributed as dist
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if dkw["rank"] == 0:
+            uid.copy_(torch.frombuffer(bytearray(scg.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        dkw = dict(dkw, nccl_id=bytes(uid.cpu().numpy().tobytes()))
+        dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    s = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], device=dev)
+    s = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], device=dev, **dkw)
     s.step(W + K)
     lg = s.iter_log()
     U, lam, _ = s.reconstruct()
     s.synchronize()
     t1 = time.perf_counter()
     s.close()
-    h2d = L.row_ptr.nbytes + L.col.nbytes + L.val.nbytes
+    secs = t1 - t0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([secs], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        secs = float(t.item())
+    a, b = s.row_begin, s.row_end
+    h2d = 8 * (b - a + 1) + 12 * int(L.row_ptr[b] - L.row_ptr[a])
     d2h = lg.nbytes + U.nbytes + lam.nbytes
-    return {"value": (W + K) / (t1 - t0), "unit": "iterations/s", "h2d_bytes_per_step": h2d / (W + K),
-            "d2h_bytes_per_step": d2h / (W + K), "seconds": t1 - t0,
-            "note": "pageable numpy CSR copied inside init; t=1..W+K; includes host CSR split and Omega draw"}
+    return {"value": (W + K) / secs, "unit": "iterations/s", "h2d_bytes_per_step": h2d / (W + K),
+            "d2h_bytes_per_step": d2h / (W + K), "seconds": secs,
+            "note": "pageable numpy CSR (this rank's rows) copied inside init; t=1..W+K; includes host CSR "
+                    "split, SELL layout and Omega draw; per-rank bytes"}
 
 
 def main():
@@ -245,8 +288,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:  # not under torchrun: relaunch one process per GPU
+        import random
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={random.randint(20000, 40000)}", __file__] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)

@@ -82,12 +82,29 @@ typedef struct {
                                0: absent, L_rr = -sum_j L_rj is formed */
 } scg_csr;
 
-/* Multi-GPU description (one process per GPU).  The NCCL unique id is created on
- * rank 0 (sketchycgal_nccl_unique_id) and broadcast by the caller, e.g. through
- * torch.distributed. */
+/* Row-sharded execution.  The rows of
+ * L and every row-indexed state vector (z, y, d, S, Omega, ...) are split into
+ * `world` contiguous blocks [row_splits[p], row_splits[p+1]).  Each Lanczos matvec
+ * needs the halo entries of the vector being multiplied: the producing kernel stores
+ * them straight into the reader ranks' memory (NVLink peer stores), and the exact
+ * global sums (CAC-2) combine through per-rank device mailboxes, so the iterates
+ * are bitwise identical for every world size.  world <= 8.
+ *
+ *   emulate = 0: one process per GPU (NCCL transport for setup: CUDA IPC handle
+ *     exchange and the one-shot reconstruction reductions).  Every rank passes its
+ *     own rows in scg_csr (row_begin = row_splits[rank], row_end = row_splits[rank+1]),
+ *     the same row_splits (required when world > 1), and the same 128-byte NCCL
+ *     unique id, created on rank 0 (sketchycgal_nccl_unique_id) and broadcast by the
+ *     caller, e.g. through torch.distributed.
+ *   emulate = 1: all `world` shards live in this one context on one device (peers are
+ *     the other shards' buffers, no NCCL).  scg_csr holds ALL rows; row_splits may be
+ *     NULL (balanced split, sketchycgal_row_splits).  Every per-row output of the
+ *     context then covers all n rows.  This runs the sharded kernels on one GPU. */
 typedef struct {
   int32_t rank, world;
-  const void *nccl_unique_id;   /* host, 128 bytes */
+  const void *nccl_unique_id;   /* host, 128 bytes (emulate = 0) */
+  const int64_t *row_splits;    /* host, world + 1 ascending offsets, [0] = 0, [world] = n; may be NULL if emulate */
+  int32_t emulate;
 } scg_dist;
 
 /* One record per iteration t (Alg. 4), original units where noted. */
@@ -173,6 +190,19 @@ int64_t sketchycgal_launch_count(const scg_ctx *c);
 /* Kernel statistics (needs SCG_PROFILE): fills up to max entries, returns the count (<0 on error). */
 int32_t sketchycgal_kernel_stats(scg_ctx *c, scg_kstat *out, int32_t max);
 void sketchycgal_reset_stats(scg_ctx *c);
+
+/* Balanced contiguous row split for `world` ranks: minimizes the largest per-rank
+ * cost rows + nonzeros (row_ptr: host, n+1 offsets of the full CSR).  Host only (no
+ * GPU needed).  splits: host, world + 1. */
+scg_status sketchycgal_row_splits(const int64_t *row_ptr, int64_t n, int32_t world, int64_t *splits);
+
+/* Halo plan of one shard (host only, no GPU needed): for each own row r in
+ * [row_begin, row_end) of the symmetric L, mask[r - row_begin] = bitmask of the
+ * OTHER ranks owning a column of row r -- by symmetry exactly the ranks that read
+ * x_r in a matvec.  Returns the number of halo rows (mask != 0), < 0 on error.
+ *   row_ptr/col_idx: this shard's rows as in scg_csr; splits: world + 1. */
+int64_t sketchycgal_halo_plan(const int64_t *row_ptr, const int32_t *col_idx, int64_t row_begin, int64_t row_end,
+                              const int64_t *splits, int32_t world, uint8_t *mask);
 
 /* Write a 128-byte NCCL unique id (call on rank 0, broadcast to all ranks). */
 scg_status sketchycgal_nccl_unique_id(void *out128);

@@ -85,13 +85,15 @@ class Csr(ctypes.Structure):
 
 
 class Dist(ctypes.Structure):
-    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p)]
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
+                ("row_splits", ctypes.c_void_p), ("emulate", ctypes.c_int32)]
 
 
 EXPORTS = ["sketchycgal_maxcut_init", "sketchycgal_step", "sketchycgal_synchronize", "sketchycgal_reconstruct",
            "sketchycgal_objective", "sketchycgal_feasibility", "sketchycgal_round", "sketchycgal_iter_log",
            "sketchycgal_get_state", "sketchycgal_apply_D", "sketchycgal_iterations", "sketchycgal_launch_count",
            "sketchycgal_kernel_stats", "sketchycgal_reset_stats", "sketchycgal_nccl_unique_id",
+           "sketchycgal_row_splits", "sketchycgal_halo_plan",
            "sketchycgal_selftest_division", "sketchycgal_last_error", "sketchycgal_destroy"]
 
 _lib = None
@@ -119,6 +121,10 @@ def open_library(path: str = LIB_PATH):
     lib.sketchycgal_kernel_stats.argtypes = [P, P, I32]
     lib.sketchycgal_reset_stats.restype = None
     lib.sketchycgal_reset_stats.argtypes = [P]
+    lib.sketchycgal_row_splits.restype = ctypes.c_int
+    lib.sketchycgal_row_splits.argtypes = [P, I64, I32, P]
+    lib.sketchycgal_halo_plan.restype = I64
+    lib.sketchycgal_halo_plan.argtypes = [P, P, I64, I64, P, I32, P]
     lib.sketchycgal_selftest_division.restype = ctypes.c_int
     lib.sketchycgal_selftest_division.argtypes = [I32, I64, ctypes.c_uint64, ctypes.POINTER(I64)]
     lib.sketchycgal_last_error.restype = ctypes.c_char_p
@@ -126,6 +132,38 @@ def open_library(path: str = LIB_PATH):
     lib.sketchycgal_destroy.restype = None
     lib.sketchycgal_destroy.argtypes = [P]
     return lib
+
+
+def row_splits(row_ptr, world: int) -> np.ndarray:
+    """Balanced contiguous row split (rows + nonzeros per rank) -- host code of the library, no GPU."""
+    rp = _c64(row_ptr, np.int64)
+    out = np.zeros(world + 1, dtype=np.int64)
+    st = load().sketchycgal_row_splits(rp.ctypes.data, len(rp) - 1, int(world), out.ctypes.data)
+    if st != 0:
+        raise ScgError(f"sketchycgal_row_splits: {STATUS.get(st, st)}")
+    return out
+
+
+def halo_plan(row_ptr, col, row_begin: int, row_end: int, splits) -> tuple[np.ndarray, int]:
+    """Reader-rank bitmask of each own row of a shard (library host code, no GPU).  row_ptr/col are the
+    shard's own rows (row_ptr[0] may be nonzero)."""
+    rp = _c64(row_ptr, np.int64)
+    cc = _c64(col, np.int32)
+    sp = _c64(splits, np.int64)
+    mask = np.zeros(max(1, row_end - row_begin), dtype=np.uint8)
+    h = load().sketchycgal_halo_plan(rp.ctypes.data, cc.ctypes.data, int(row_begin), int(row_end), sp.ctypes.data,
+                                     len(sp) - 1, mask.ctypes.data)
+    if h < 0:
+        raise ScgError("sketchycgal_halo_plan failed")
+    return mask[:row_end - row_begin], int(h)
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    st = load().sketchycgal_nccl_unique_id(buf)
+    if st != 0:
+        raise ScgError(f"sketchycgal_nccl_unique_id: {STATUS.get(st, st)}")
+    return buf.raw
 
 
 def load():
@@ -156,22 +194,40 @@ def _c64(a, dt):
 
 
 class SketchyCGAL:
-    """One GPU's SketchyCGAL MaxCut solver context (sketchycgal_maxcut_init ... destroy)."""
+    """SketchyCGAL MaxCut solver context (sketchycgal_maxcut_init ... destroy).
+
+    One GPU by default.  ``shards=P`` runs the row-sharded path with P emulated ranks
+    inside this one context on one device (all per-row outputs still cover all n rows).
+    Multi-process (one process per GPU): pass ``rank``, ``world``, ``splits`` (world+1
+    row offsets) and ``nccl_id`` (the 128 bytes of ``nccl_unique_id()`` from rank 0);
+    ``L`` may be the full CSR, the rank's rows are taken from it.
+    """
 
     def __init__(self, L, R: int, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
                  scale: bool = True, trace_correct: bool = True, profile: bool = False, device: int = 0,
-                 stream=None, row_begin: int = 0, row_end: int | None = None, dist=None,
-                 regenerate: bool = False):
+                 stream=None, regenerate: bool = False, shards: int = 1, splits=None,
+                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
         self.lib = load()
         self.n = int(L.n)
         self.R = int(R)
-        self.row_begin = int(row_begin)
-        self.row_end = self.n if row_end is None else int(row_end)
+        dist = None
+        self._splits = None
+        if shards > 1 or world > 1:
+            P = shards if shards > 1 else world
+            sp = row_splits(L.row_ptr, P) if splits is None else _c64(splits, np.int64)
+            self._splits = sp
+            self._uid = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+            dist = Dist(0 if shards > 1 else int(rank), int(P), ctypes.addressof(self._uid) if self._uid else None,
+                        sp.ctypes.data, 1 if shards > 1 else 0)
+        if world > 1 and shards <= 1:
+            self.row_begin, self.row_end = int(self._splits[rank]), int(self._splits[rank + 1])
+        else:
+            self.row_begin, self.row_end = 0, self.n
         self.nl = self.row_end - self.row_begin
         rp = _c64(L.row_ptr, np.int64)
         col = _c64(L.col, np.int32)
         val = _c64(L.val, np.float64)
-        if row_begin != 0 or self.row_end != self.n:  # local rows of a full CSR
+        if self.row_begin != 0 or self.row_end != self.n:  # local rows of a full CSR
             a, b = int(rp[self.row_begin]), int(rp[self.row_end])
             col, val = col[a:b], val[a:b]
             rp = rp[self.row_begin:self.row_end + 1] - a

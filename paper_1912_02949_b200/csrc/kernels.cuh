@@ -47,6 +47,74 @@ struct Csr {
   const double *val;
 };
 
+// Host-computed scalars of iteration t (CAC-6).
+struct IterArgs {
+  long long t;
+  int q;
+  double eta, one_m_eta, alpha, b, beta0, sq, beta_next;
+};
+
+// ---------------------------------------------------------------- row-sharded execution
+// P ranks own contiguous row blocks.  Each rank keeps the gathered vectors (the
+// Lanczos vectors w_i, the start vector g, x) at GLOBAL indices in its "gathered
+// region" G; own rows are written locally and, for rows some other rank reads
+// (halo rows: a column of that rank's rows -- by symmetry of L, exactly the rows r
+// with a column owned by that rank), also stored straight into that rank's G over
+// NVLink peer memory by the producing kernel (mask[r] = bitmask of reader ranks).
+// Global exact sums (CAC-2) are combined through per-rank mailboxes: the last block
+// of a producer stores its rank's integer limbs into every rank's mailbox and then
+// raises a per-(epoch, source) flag with release semantics (system scope); a
+// one-warp "pull" kernel on each rank waits for all P flags, adds the P limb sets
+// (exact integers: bitwise independent of P) and runs the same finalize code the
+// single-GPU last block runs.  The flag is raised after every block of the
+// producer fenced its peer stores, so a completed pull also means every halo entry
+// of that producer has landed.  The same code runs P shards inside one process on
+// one device ("emulated shards": peers are the other shards' buffers), which is how
+// the sharded kernels are checked bitwise against the oracle on a single GPU.
+constexpr int kMaxRanks = 8;
+
+struct Mailbox {
+  long long limbs[4][kMaxRanks][3][kLimbs];  // [epoch & 3][source rank][sum][limb]
+  double fv[4][kMaxRanks][kMaxR];            // fp64 payload (g = v^T Omega partials)
+  unsigned long long flag[4][kMaxRanks];     // epoch published by the source rank
+};
+
+struct Net {
+  const unsigned char *mask;  // [nl] reader-rank bitmask of each own row; nullptr when P == 1
+  double *G;                  // this rank's gathered region
+  double *const *peerG;       // [P] every rank's gathered region (device pointers, peer-mapped)
+  Mailbox *const *peerMB;     // [P] every rank's mailbox
+  Mailbox *mb;                // own mailbox
+  int P, me;
+  unsigned long long E;       // epoch of the collective this launch takes part in
+};
+
+// Store v at dst (this rank's gathered region, own row r) and into every reader rank's copy.
+__device__ __forceinline__ void gstore(const Net &net, double *dst, int r, double v) {
+  *dst = v;
+  if (net.mask) {
+    unsigned m = net.mask[r];
+    if (m) {
+      const long long off = dst - net.G;
+      while (m) {
+        const int q = __ffs(m) - 1;
+        m &= m - 1;
+        net.peerG[q][off] = v;
+      }
+    }
+  }
+}
+
+enum FinKind { FK_FROB = 0, FK_RHO0, FK_OM, FK_RHO, FK_NUX, FK_MON, FK_NZ, FK_BAR };
+
+struct FinArgs {
+  int i;                 // Lanczos step (FK_OM, FK_RHO, FK_BAR)
+  int R;                 // sketch rank (FK_NZ)
+  IterArgs A;            // FK_NZ
+  scg_iter_rec *log;     // FK_NZ
+  double *out;           // FK_FROB
+};
+
 // ---------------------------------------------------------------- division
 // (Diagnostics only since the contract evaluates v / rho as v * fl(1/rho), R26.)
 // a / b, correctly rounded (IEEE), for a divisor b shared by many quotients:
@@ -523,9 +591,11 @@ __device__ __forceinline__ void xblk_init(XBlk<NS> &b) {
 // Flush every thread's window into the block accumulator, add the block total to
 // the global slot (exact integer atomics), and take a ticket: returns true in the
 // last block to finish (which then finalizes the slot).
+// With P > 1 every thread first fences its peer stores at system scope, so the
+// mailbox flag the last block raises afterwards orders them for the readers.
 template <int NS>
 __device__ __forceinline__ bool commit_and_ticket(XWin (&acc)[NS], XBlk<NS> &blk, XSlot *slot, int err,
-                                                  DevScalars *sc) {
+                                                  DevScalars *sc, int P = 1) {
   __shared__ int s_last;
 #pragma unroll
   for (int s = 0; s < NS; ++s) xwin_flush(acc[s], blk.l[s]);
@@ -535,7 +605,19 @@ __device__ __forceinline__ bool commit_and_ticket(XWin (&acc)[NS], XBlk<NS> &blk
     const long long v = blk.l[s][i];
     if (v != 0) atomicAdd(reinterpret_cast<unsigned long long *>(&slot->limbs[s][i]), (unsigned long long)v);
   }
-  __threadfence();
+  if (P > 1) __threadfence_system();
+  else __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(&slot->counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  return s_last != 0;
+}
+
+// Ticket only (kernels without sums that still take part in a collective: the
+// pass-2 barrier of the regenerate mode).
+__device__ __forceinline__ bool ticket_only(XSlot *slot) {
+  __shared__ int s_last;
+  __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) s_last = (atomicAdd(&slot->counter, 1u) == gridDim.x - 1);
   __syncthreads();
@@ -551,11 +633,152 @@ __device__ __noinline__ double slot_take(XSlot *slot, int s) {
   return xacc_round(l);
 }
 
+// ---------------------------------------------------------------- finalize (shared by both paths)
+__device__ __forceinline__ double gamma_rule(const IterArgs &A, double nz) {
+  // eqn:sketchy-cgal-dual-step (PAPER.md:1409-1415) with ||A||^2 = 1 (CAC-6)
+  if (nz == 0.0) return A.beta0;
+  double num = 4.0 * A.alpha;
+  num = num * A.alpha;
+  num = num * A.beta0;
+  const double den = ((double)(A.t + 1) * A.sq) * nz;
+  const double g = num / den;
+  return g < A.beta0 ? g : A.beta0;
+}
+
+__device__ __forceinline__ void fin_rho(DevScalars *sc, int i, double rho2) {
+  const double rho = sqrt(rho2);
+  sc->rho[i] = rho;
+  const double rp = i >= 2 ? sc->rho[i - 1] : 0.0;
+  if (rho <= 0x1p-45 * (fabs(sc->om[i - 1]) + rp)) {  // Alg. 2 line 8 (reading A3)
+    sc->k = i;
+    sc->brk = 1;
+  }
+}
+
+// Turn the rounded global sums of one collective into the device scalars.  Runs in
+// the last block of the producer (P == 1) or in k_pull (P > 1): same code, same bits.
+__device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long (*L)[kLimbs], const double *gk,
+                                      const FinArgs &f) {
+  switch (kind) {
+    case FK_FROB: *f.out = xacc_round(L[0]); break;
+    case FK_RHO0:
+      sc->rho[0] = sqrt(xacc_round(L[0]));
+      sc->brk = 0;
+      sc->k = 0;
+      break;
+    case FK_OM: sc->om[f.i - 1] = xacc_round(L[0]); break;
+    case FK_RHO: fin_rho(sc, f.i, xacc_round(L[0])); break;
+    case FK_NUX: sc->nu_x = sqrt(xacc_round(L[0])); break;
+    case FK_MON:
+      sc->xi = xacc_round(L[0]);
+      sc->c = xacc_round(L[1]);
+      sc->vv = xacc_round(L[2]);
+      break;
+    case FK_NZ: {
+      for (int k = 0; k < f.R; ++k) sc->gk[k] = gk[k];
+      const IterArgs &A = f.A;
+      const double nz = xacc_round(L[0]);
+      sc->nz = nz;
+      sc->gamma = gamma_rule(A, nz);
+      const double ea2 = A.eta * A.alpha;
+      sc->tau = fma(ea2, sc->vv, A.one_m_eta * sc->tau);
+      sc->p = fma(ea2, sc->c, A.one_m_eta * sc->p);
+      scg_iter_rec rec;
+      rec.t = A.t;
+      rec.q = A.q;
+      rec.k = sc->k;
+      rec.theta = sc->theta;
+      rec.xi = sc->xi;
+      rec.c = sc->c;
+      rec.p = sc->p;
+      rec.znorm = sqrt(nz);
+      rec.gamma = sc->gamma;
+      rec.tau = sc->tau;
+      f.log[A.t - 1] = rec;
+      break;
+    }
+    default: break;
+  }
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Last block, thread 0: take this rank's limbs (resetting the slot) and either
+// finalize (P == 1) or publish them to every rank's mailbox (P > 1).
+template <int NS>
+__device__ __forceinline__ void emit(XSlot *slot, DevScalars *sc, const Net &net, int kind, const FinArgs &f,
+                                     const double *gk) {
+  __threadfence();
+  long long L[3][kLimbs];
+  for (int s = 0; s < 3; ++s)
+    for (int i = 0; i < kLimbs; ++i)
+      L[s][i] = s < NS ? (long long)atomicExch(reinterpret_cast<unsigned long long *>(&slot->limbs[s][i]), 0ull) : 0ll;
+  slot->counter = 0;
+  if (net.P <= 1) {
+    finalize(kind, sc, L, gk, f);
+    return;
+  }
+  const int e = (int)(net.E & 3ull);
+  const int nf = kind == FK_NZ ? f.R : 0;
+  for (int q = 0; q < net.P; ++q) {
+    Mailbox *m = net.peerMB[q];
+    for (int s = 0; s < NS; ++s)
+      for (int i = 0; i < kLimbs; ++i) m->limbs[e][net.me][s][i] = L[s][i];
+    for (int k = 0; k < nf; ++k) m->fv[e][net.me][k] = gk[k];
+  }
+  __threadfence_system();
+  for (int q = 0; q < net.P; ++q) st_release_sys(&net.peerMB[q]->flag[e][net.me], net.E);
+}
+
+// P > 1: wait for every rank's contribution to collective net.E, add, finalize.
+// A lost flag (a bug or a dead peer) ends the wait after ~2^34 cycles with sc->err = 2
+// instead of hanging the GPU.
+__global__ void k_pull(int kind, int ns, Net net, DevScalars *sc, FinArgs f) {
+  if (threadIdx.x != 0) return;
+  if ((kind == FK_OM || kind == FK_RHO) && sc->brk) return;  // producer skipped (Lanczos break)
+  if (kind == FK_BAR && f.i >= sc->k) return;
+  const int e = (int)(net.E & 3ull);
+  Mailbox *m = net.mb;
+  const long long t0 = clock64();
+  for (int p = 0; p < net.P; ++p) {
+    while (ld_acquire_sys(&m->flag[e][p]) != net.E) {
+      if (clock64() - t0 > (1ll << 34)) {
+        atomicOr(&sc->err, 2);
+        return;
+      }
+      __nanosleep(32);
+    }
+  }
+  long long L[3][kLimbs];
+  double gk[kMaxR];
+  for (int s = 0; s < 3; ++s)
+    for (int i = 0; i < kLimbs; ++i) {
+      long long acc = 0;
+      if (s < ns)
+        for (int p = 0; p < net.P; ++p) acc += __ldcv(&m->limbs[e][p][s][i]);
+      L[s][i] = acc;
+    }
+  if (kind == FK_NZ)
+    for (int k = 0; k < f.R; ++k) {
+      double t = 0.0;
+      for (int p = 0; p < net.P; ++p) t += __ldcv(&m->fv[e][p][k]);
+      gk[k] = t;
+    }
+  finalize(kind, sc, L, gk, f);
+}
+
 // ---------------------------------------------------------------- init kernels
 // ||L||_F^2 over all stored entries: off-diagonal weights (each stored once per
 // direction) and the diagonal (scaling).
 __global__ void k_frob(const double *__restrict__ w, long long nnz, const double *__restrict__ diag, int nl,
-                       XSlot *slot, DevScalars *sc, double *out) {
+                       XSlot *slot, DevScalars *sc, double *out, Net net) {
   __shared__ XBlk<1> xb;
   xblk_init<1>(xb);
   XWin acc[1];
@@ -564,10 +787,10 @@ __global__ void k_frob(const double *__restrict__ w, long long nnz, const double
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
   for (long long k = tid; k < nnz; k += st) xwin_add(acc[0], w[k] * w[k], err, xb.l[0]);
   for (long long r = tid; r < nl; r += st) xwin_add(acc[0], diag[r] * diag[r], err, xb.l[0]);
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0) {
-    __threadfence();
-    *out = slot_take(slot, 0);
-    slot->counter = 0;
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0) {
+    FinArgs f{};
+    f.out = out;
+    emit<1>(slot, sc, net, FK_FROB, f, nullptr);
   }
 }
 
@@ -600,7 +823,7 @@ __global__ void k_init_d(const double *__restrict__ z, const double *__restrict_
 
 // Lanczos start vector g = randn (Alg. 2 line 1) for iteration t and ||g||^2 (exact).
 __global__ void __launch_bounds__(kBlock) k_gen_start(double *__restrict__ g, int nl, long long rb, uint64_t seed,
-                                                      long long t, XSlot *slot, DevScalars *sc, int finalize) {
+                                                      long long t, XSlot *slot, DevScalars *sc, Net net) {
   __shared__ XBlk<1> xb;
   xblk_init<1>(xb);
   XWin acc[1];
@@ -608,14 +831,11 @@ __global__ void __launch_bounds__(kBlock) k_gen_start(double *__restrict__ g, in
   int err = 0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
     const double v = scg_lanczos_start(seed, t, rb + r);
-    g[rb + r] = v;
+    gstore(net, g + rb + r, r, v);
     xwin_add(acc[0], v * v, err, xb.l[0]);
   }
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
-    __threadfence();
-    sc->rho[0] = sqrt(slot_take(slot, 0));
-    slot->counter = 0;
-  }
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
+    emit<1>(slot, sc, net, FK_RHO0, FinArgs{}, nullptr);
 }
 
 // ---------------------------------------------------------------- Lanczos pass 1
@@ -639,7 +859,7 @@ template <bool UNI>
 __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ X, int nl, long long rb, int i,
                                                          double *__restrict__ a, XSlot *slot, DevScalars *sc,
-                                                         int finalize) {
+                                                         Net net) {
   if (sc->brk) return;
   const double den = sc->rho[i - 1];
   __shared__ XBlk<1> xb;
@@ -657,21 +877,10 @@ __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_a(Csr C,
 #endif
   int err = epi.err;
   XWin (&acc)[1] = epi.acc;
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
-    __threadfence();
-    sc->om[i - 1] = slot_take(slot, 0);
-    slot->counter = 0;
-  }
-}
-
-// finalize helpers (also used after a multi-GPU all-reduce)
-__device__ __forceinline__ void fin_rho(DevScalars *sc, int i, double rho2) {
-  const double rho = sqrt(rho2);
-  sc->rho[i] = rho;
-  const double rp = i >= 2 ? sc->rho[i - 1] : 0.0;
-  if (rho <= 0x1p-45 * (fabs(sc->om[i - 1]) + rp)) {  // Alg. 2 line 8 (reading A3)
-    sc->k = i;
-    sc->brk = 1;
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0) {
+    FinArgs f{};
+    f.i = i;
+    emit<1>(slot, sc, net, FK_OM, f, nullptr);
   }
 }
 
@@ -679,7 +888,7 @@ __device__ __forceinline__ void fin_rho(DevScalars *sc, int i, double rho2) {
 // rho_i = ||w_{i+1}|| (exact); breakdown test.  Writes the un-normalized w_{i+1}.
 __global__ void __launch_bounds__(kBlock, 4) k_lanczos_b(const double *__restrict__ a, const double *Xi,
                                                       const double *Xim1, double *Xip1, int nl, long long rb,
-                                                      int i, XSlot *slot, DevScalars *sc, int finalize) {
+                                                      int i, XSlot *slot, DevScalars *sc, Net net) {
   if (sc->brk) return;
   const double om = sc->om[i - 1];
   const double den = sc->rho[i - 1];
@@ -709,15 +918,15 @@ __global__ void __launch_bounds__(kBlock, 4) k_lanczos_b(const double *__restric
         const double vi = (xi[u]) * rden;
         double w = fma(-om, vi, av[u]);
         if (i >= 2) w = fma(-den, (xm[u]) * rdenm, w);  // rho_{i-1} = rho[i-1] = den
-        Xip1[rb + r] = w;
+        gstore(net, Xip1 + rb + r, r, w);
         xwin_add(acc[0], w * w, err, xb.l[0]);
       }
     }
   }
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
-    __threadfence();
-    fin_rho(sc, i, slot_take(slot, 0));
-    slot->counter = 0;
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0) {
+    FinArgs f{};
+    f.i = i;
+    emit<1>(slot, sc, net, FK_RHO, f, nullptr);
   }
 }
 
@@ -854,13 +1063,14 @@ struct EpiC {
   const double *Xjm1;
   double *Xjp1, *x;
   long long rb;
+  const Net *net;
   int j;
   double om, den, denm, rhoj, s1, sj1, rrhoj, rdenm;
   __device__ __forceinline__ void operator()(const RowOut<1> &o) {
     const double vj = o.xr;
     double w = fma(-om, vj, o.s[0]);
     if (j >= 2) w = fma(-den, Xjm1[rb + o.r] * rdenm, w);
-    Xjp1[rb + o.r] = w;
+    gstore(*net, Xjp1 + rb + o.r, o.r, w);
     const double vn = (w) * rrhoj;
     const double xr = j == 1 ? s1 * vj : x[rb + o.r];
     x[rb + o.r] = fma(sj1, vn, xr);
@@ -871,9 +1081,9 @@ template <bool UNI>
 __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_c(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ Xj, const double *Xjm1,
                                                          double *Xjp1, double *__restrict__ x, int nl, long long rb,
-                                                         int j, const DevScalars *__restrict__ sc) {
+                                                         int j, DevScalars *sc, XSlot *slot, Net net) {
   if (j >= sc->k) return;  // sc->k holds the effective k after k_tridiag
-  EpiC epi{Xjm1, Xjp1, x, rb, j, sc->om[j - 1], sc->rho[j - 1], j >= 2 ? sc->rho[j - 2] : 1.0, sc->rho[j],
+  EpiC epi{Xjm1, Xjp1, x, rb, &net, j, sc->om[j - 1], sc->rho[j - 1], j >= 2 ? sc->rho[j - 2] : 1.0, sc->rho[j],
            sc->s[0], sc->s[j], 1.0 / sc->rho[j], 1.0 / (j >= 2 ? sc->rho[j - 2] : 1.0)};
 #if SCG_TMA
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -881,6 +1091,12 @@ __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_c(Csr C,
 #else
   spmv_rows<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, nl, epi);
 #endif
+  // P > 1: the next step gathers w_{j+1} -- a barrier collective (no sums)
+  if (net.P > 1 && ticket_only(slot) && threadIdx.x == 0) {
+    FinArgs f{};
+    f.i = j;
+    emit<0>(slot, sc, net, FK_BAR, f, nullptr);
+  }
 }
 
 // Stored-vector mode (Remark "Time-storage tradeoff"): the
@@ -889,7 +1105,7 @@ __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_c(Csr C,
 // bitwise equal to the two-pass result; then ||x||^2 (exact).
 __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict__ Wst, long long ldw,
                                                        double *__restrict__ x, int nl, long long rb, XSlot *slot,
-                                                       DevScalars *sc, int finalize) {
+                                                       DevScalars *sc, Net net) {
   __shared__ double s_s[kMaxQ], s_r[kMaxQ], s_rr[kMaxQ];
   const int k = sc->k;
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
@@ -914,19 +1130,16 @@ __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict_
       for (int u = 0; u < 4; ++u) xr = fma(s_s[j + u], (wv[u]) * s_rr[j + u], xr);
     }
     for (; j < k; ++j) xr = fma(s_s[j], __ldg(w + (long long)j * ldw) * s_rr[j], xr);
-    x[rb + r] = xr;
+    gstore(net, x + rb + r, r, xr);
     xwin_add(acc[0], xr * xr, err, xb.l[0]);
   }
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
-    __threadfence();
-    sc->nu_x = sqrt(slot_take(slot, 0));
-    slot->counter = 0;
-  }
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
+    emit<1>(slot, sc, net, FK_NUX, FinArgs{}, nullptr);
 }
 
 // ||x||^2 (exact); k == 1 case: x = s_1 v_1.
 __global__ void __launch_bounds__(kBlock) k_norm_x(const double *__restrict__ g, double *__restrict__ x, int nl,
-                                                   long long rb, XSlot *slot, DevScalars *sc, int finalize) {
+                                                   long long rb, XSlot *slot, DevScalars *sc, Net net) {
   const bool k1 = sc->k == 1;
   const double s1 = sc->s[0], rden = 1.0 / sc->rho[0];
   __shared__ XBlk<1> xb;
@@ -947,16 +1160,14 @@ __global__ void __launch_bounds__(kBlock) k_norm_x(const double *__restrict__ g,
       const int r = r0 + u * stride;
       if (r < nl) {
         double xr = xv[u];
-        if (k1) { xr = s1 * (xr * rden); x[rb + r] = xr; }
+        if (k1) xr = s1 * (xr * rden);
+        if (k1 || net.P > 1) gstore(net, x + rb + r, r, xr);  // P > 1: publish x's halo for the monitor
         xwin_add(acc[0], xr * xr, err, xb.l[0]);
       }
     }
   }
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
-    __threadfence();
-    sc->nu_x = sqrt(slot_take(slot, 0));
-    slot->counter = 0;
-  }
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
+    emit<1>(slot, sc, net, FK_NUX, FinArgs{}, nullptr);
 }
 
 // Monitor matvec: v = x / ||x|| (written), xi = v.(D v), c = v.(C v), ||v||^2 (exact).
@@ -978,7 +1189,7 @@ template <bool UNI>
 __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const double *__restrict__ d,
                                                        const double *__restrict__ cdiag, const double *__restrict__ x,
                                                        double *__restrict__ v, int nl, long long rb, XSlot *slot,
-                                                       DevScalars *sc, int finalize) {
+                                                       DevScalars *sc, Net net) {
   const double nu = sc->nu_x;
   __shared__ XBlk<3> xb;
   xblk_init<3>(xb);
@@ -997,39 +1208,17 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
 #endif
   int err = epi.err;
   XWin (&acc)[3] = epi.acc;
-  if (commit_and_ticket<3>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
-    __threadfence();
-    sc->xi = slot_take(slot, 0);
-    sc->c = slot_take(slot, 1);
-    sc->vv = slot_take(slot, 2);
-    slot->counter = 0;
-  }
+  if (commit_and_ticket<3>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
+    emit<3>(slot, sc, net, FK_MON, FinArgs{}, nullptr);
 }
 
 // ---------------------------------------------------------------- primal / dual / sketch
-struct IterArgs {
-  long long t;
-  int q;
-  double eta, one_m_eta, alpha, b, beta0, sq, beta_next;
-};
-
-__device__ __forceinline__ double gamma_rule(const IterArgs &A, double nz) {
-  // eqn:sketchy-cgal-dual-step (PAPER.md:1409-1415) with ||A||^2 = 1 (CAC-6)
-  if (nz == 0.0) return A.beta0;
-  double num = 4.0 * A.alpha;
-  num = num * A.alpha;
-  num = num * A.beta0;
-  const double den = ((double)(A.t + 1) * A.sq) * nz;
-  const double g = num / den;
-  return g < A.beta0 ? g : A.beta0;
-}
-
 // z <- (1-eta) z + eta alpha (v o v) (Alg. 4 line 8, primitive 3), ||z - b||^2 (exact),
 // per-block partials of g = v^T Omega (fp64, fixed tree; off the feedback path).
 __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__ v, double *__restrict__ z,
                                                    const double *__restrict__ Om, int nl, int R, IterArgs A,
                                                    double *__restrict__ gpart, XSlot *slot, DevScalars *sc,
-                                                   scg_iter_rec *log, int finalize) {
+                                                   scg_iter_rec *log, Net net) {
   __shared__ double red[kBlock / 32][kMaxR];
   __shared__ XBlk<1> xb;
   xblk_init<1>(xb);
@@ -1085,7 +1274,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
     gpart[(long long)blockIdx.x * R + threadIdx.x] = t;
   }
   __syncthreads();
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && finalize) {
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P)) {
     __shared__ double gsum[kMaxR];
     // sum block partials in a fixed order: thread k sums column k over blocks
     if (threadIdx.x < R) {
@@ -1094,28 +1283,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
       gsum[threadIdx.x] = t;
     }
     __syncthreads();
-    if (threadIdx.x < R) sc->gk[threadIdx.x] = gsum[threadIdx.x];
     if (threadIdx.x == 0) {
-      __threadfence();
-      const double nz = slot_take(slot, 0);
-      slot->counter = 0;
-      sc->nz = nz;
-      sc->gamma = gamma_rule(A, nz);
-      const double ea2 = A.eta * A.alpha;
-      sc->tau = fma(ea2, sc->vv, A.one_m_eta * sc->tau);
-      sc->p = fma(ea2, sc->c, A.one_m_eta * sc->p);
-      scg_iter_rec rec;
-      rec.t = A.t;
-      rec.q = A.q;
-      rec.k = sc->k;
-      rec.theta = sc->theta;
-      rec.xi = sc->xi;
-      rec.c = sc->c;
-      rec.p = sc->p;
-      rec.znorm = sqrt(nz);
-      rec.gamma = sc->gamma;
-      rec.tau = sc->tau;
-      log[A.t - 1] = rec;
+      FinArgs f{};
+      f.R = R;
+      f.A = A;
+      f.log = log;
+      emit<1>(slot, sc, net, FK_NZ, f, gsum);
     }
   }
 }
@@ -1127,7 +1300,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_dual_sketch(const double *__restr
                                                         const double *__restrict__ v, double *__restrict__ S,
                                                         double *__restrict__ g, int nl, long long rb, int R,
                                                         IterArgs A, uint64_t seed, XSlot *slot, DevScalars *sc,
-                                                        int finalize) {
+                                                        Net net) {
   __shared__ double ck[kMaxR];
   const double gam = sc->gamma;
   if (threadIdx.x < R) ck[threadIdx.x] = (A.eta * A.alpha) * sc->gk[threadIdx.x];
@@ -1177,18 +1350,13 @@ __global__ void __launch_bounds__(kBlock, 3) k_dual_sketch(const double *__restr
       const int r = r0 + u * stride;
       if (r < nl) {
         const double gv = scg_lanczos_start(seed, A.t + 1, rb + r);
-        g[rb + r] = gv;
+        gstore(net, g + rb + r, r, gv);
         xwin_add(acc[0], gv * gv, err, xb.l[0]);
       }
     }
   }
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc) && threadIdx.x == 0 && finalize) {
-    __threadfence();
-    sc->rho[0] = sqrt(slot_take(slot, 0));
-    slot->counter = 0;
-    sc->brk = 0;
-    sc->k = 0;
-  }
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
+    emit<1>(slot, sc, net, FK_RHO0, FinArgs{}, nullptr);
 }
 
 // ---------------------------------------------------------------- one-shot kernels
@@ -1232,22 +1400,25 @@ __global__ void k_colpair(const double *__restrict__ A, const double *__restrict
   }
 }
 
-// Per-column quantities of the reconstruction, partial sums per block:
-//   which 0: u_k^T L u_k  (objective)          partial[k][block]
-//   which 1: cut weight of sgn(U[:,k])          partial[k][block]
+// Per-column quantities of the reconstruction, partial sums per block, for the
+// columns k = k0 + blockIdx.y (Ug + blockIdx.y * ldg = column k at GLOBAL indices:
+// U itself on one GPU, the gathered copy of one column when sharded):
+//   which 0: u_k^T L u_k  (objective)          partial[y][block]
+//   which 1: cut weight of sgn(U[:,k])          partial[y][block]
 //   which 2: sum_r (diag(X^)_r - 1)^2 with Lam  partial[0][block]
 __global__ void k_colstats(const int *__restrict__ rp, const int *__restrict__ col, const double *__restrict__ w,
-                           const double *__restrict__ ldiag, const double *__restrict__ U, const double *__restrict__ Ufull,
-                           const double *__restrict__ lam, int nl, long long rb, long long nglob, int R, int which,
-                           double *__restrict__ partial) {
+                           const double *__restrict__ ldiag, const double *__restrict__ U, const double *__restrict__ Ug,
+                           long long ldg, int k0, const double *__restrict__ lam, int nl, long long rb, int R,
+                           int which, double *__restrict__ partial) {
   __shared__ double red[kBlock / 32];
-  const int kcol = blockIdx.y;
+  const int kcol = k0 + (int)blockIdx.y;
+  const double *Ufull = Ug + (long long)blockIdx.y * ldg;
   double s = 0.0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
     if (which == 0) {
       const double ur = U[(long long)kcol * nl + r];
       double lu = ldiag[r] * ur;
-      for (int e = rp[r]; e < rp[r + 1]; ++e) lu = fma(-w[e], Ufull[(long long)kcol * nglob + col[e]], lu);
+      for (int e = rp[r]; e < rp[r + 1]; ++e) lu = fma(-w[e], Ufull[col[e]], lu);
       s = fma(ur, lu, s);
     } else if (which == 1) {
       const bool sr = U[(long long)kcol * nl + r] >= 0.0;
@@ -1255,7 +1426,7 @@ __global__ void k_colstats(const int *__restrict__ rp, const int *__restrict__ c
       for (int e = rp[r]; e < rp[r + 1]; ++e) {
         const int c = col[e];
         if (c > gr) {
-          const bool sc_ = Ufull[(long long)kcol * nglob + c] >= 0.0;
+          const bool sc_ = Ufull[c] >= 0.0;
           if (sr != sc_) s += w[e];
         } else if (c < rb || c >= rb + nl) {
           // edge to a lower row owned by another rank: counted by that rank
@@ -1277,7 +1448,20 @@ __global__ void k_colstats(const int *__restrict__ rp, const int *__restrict__ c
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) t += red[ww];
-    partial[(long long)kcol * gridDim.x + blockIdx.x] = t;
+    partial[(long long)blockIdx.y * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+// Sharded reconstruction: gather column k of U (own rows -> this rank's and the
+// reader ranks' gathered region at global indices), then a barrier collective.
+__global__ void k_push_col(const double *__restrict__ Ucol, double *__restrict__ xg, int nl, long long rb,
+                           XSlot *slot, DevScalars *sc, Net net) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x)
+    gstore(net, xg + rb + r, r, Ucol[r]);
+  if (ticket_only(slot) && threadIdx.x == 0) {
+    FinArgs f{};
+    f.i = -1;
+    emit<0>(slot, sc, net, FK_BAR, f, nullptr);
   }
 }
 

@@ -2,6 +2,14 @@
 // SketchyCGAL MaxCut hot path.  See DESIGN.md for the method, the arithmetic
 // contract, the data layout and the kernel rooflines.
 //
+// A context owns one or more row shards (struct Shard).  One GPU: one shard owning
+// all rows.  Multi-GPU (one process per GPU): one shard per rank, peers reached
+// through CUDA IPC mappings (NVLink), NCCL only for setup and the one-shot
+// reconstruction reductions.  Emulated shards: P shards of one problem on one
+// device in one context, peers = the sibling shards.  The
+// iteration loop is the same code for all three: each step launches the kernel for
+// every shard, then (P > 1) the k_pull collective for every shard.
+//
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a --fmad=false -O3 -lineinfo
 // (--fmad=false is part of the arithmetic contract: no contraction of a*b+c).
 #include <cuda_runtime.h>
@@ -16,70 +24,98 @@
 
 #include "../../include/sketchycgal.h"
 #include "kernels.cuh"
+#include "linalg.h"
 
 #ifdef SCG_WITH_NCCL
 #include <nccl.h>
 #endif
 
 using namespace scg;
+using namespace scg_host;
 
 namespace {
 
 enum KClass {
   KC_LANCZOS_A = 0, KC_LANCZOS_B, KC_TRIDIAG, KC_LANCZOS_C, KC_NORM_X, KC_COMBINE, KC_MONITOR, KC_PRIMAL,
-  KC_DUAL_SKETCH, KC_OTHER, KC_COUNT
+  KC_DUAL_SKETCH, KC_PULL, KC_OTHER, KC_COUNT
 };
 const char *kKClassName[KC_COUNT] = {"lanczos_a_spmv_dot", "lanczos_b_axpy_norm", "tridiag_mineig",
                                      "lanczos_c_spmv_regen", "norm_x", "combine_stored", "monitor_spmv",
-                                     "primal_z_gpart", "dual_sketch_next_g", "other"};
+                                     "primal_z_gpart", "dual_sketch_next_g", "pull_collective", "other"};
 
 struct EvPair {
   cudaEvent_t a, b;
   int cls;
 };
 
+enum { SLOT_NU0 = 0, SLOT_OM, SLOT_RHO, SLOT_XX, SLOT_MON, SLOT_NZ, SLOT_INIT, SLOT_BAR, SLOT_COUNT };
+
 }  // namespace
 
-struct scg_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  int nsm = 148;
-  int64_t n = 0, nl = 0, rb = 0, npad = 0;
+// One contiguous row block [rb, rb + nl) and all its device state.
+struct Shard {
+  int rank = 0;
+  int64_t nl = 0, rb = 0, nlpad = 0;
   long long nnz_off = 0;
-  int R = 0;
-  uint32_t flags = 0;
-  double alpha_orig = 0, alpha = 0, beta0 = 1, b = 0, nrmL = 1, lnN = 0;
-  uint64_t seed = 0;
-  int rank = 0, world = 1;
-  // device arrays
   int *rp = nullptr, *col = nullptr;
   double *val = nullptr, *wts = nullptr, *ldiag = nullptr, *cdiag = nullptr;
   double *d = nullptr, *z = nullptr, *y = nullptr, *a = nullptr, *v = nullptr;
-  double *g = nullptr, *W0 = nullptr, *W1 = nullptr, *x = nullptr;
+  double *G = nullptr;  // gathered region: [x | W slot 0 (= g) | W slot 1 | ...], each npad long
   double *S = nullptr, *Om = nullptr, *gpart = nullptr;
   double *U = nullptr, *tmp1 = nullptr, *tmp2 = nullptr, *dmat = nullptr, *partial = nullptr, *dlam = nullptr;
   double *dscalar = nullptr;
   DevScalars *sc = nullptr;
   XSlot *slots = nullptr;
   scg_iter_rec *dlog = nullptr;
-  int64_t log_cap = 0;
-  int grid_rows = 1, grid_primal = 1, grid_tiles = 1, grid_b = 1, grid_comb = 1, grid_dual = 1, grid_norm = 1;
   int *longrows = nullptr;
+  int nlong = 0;
   int *sell_perm = nullptr, *sell_col = nullptr;
   int2 *sell_meta = nullptr;
   double *sell_val = nullptr;
-  double sell_m0 = 0.0;
-  int nslice = 0;
-  int *sell_wstart = nullptr;
-  int nwin = 0;
-  size_t smem1 = 0, smem2 = 0;
-  int grid_mon = 1;
-  double sell_slots = 0.0;
+  double sell_m0 = 0.0, sell_slots = 0.0;
   bool sell_uniform = false;
-  int nlong = 0;
+  int nslice = 0, nwin = 0;
+  int *sell_wstart = nullptr;
+  // sharding
+  unsigned char *mask = nullptr;  // device [nl], nullptr when world == 1
+  Mailbox *mb = nullptr;
+  double **peerG = nullptr;       // device [world]
+  Mailbox **peerMB = nullptr;     // device [world]
+  std::vector<void *> ipc_opened;
+  int64_t halo_rows = 0;
+  // grids
+  int grid_rows = 1, grid_primal = 1, grid_tiles = 1, grid_b = 1, grid_comb = 1, grid_dual = 1, grid_norm = 1,
+      grid_mon = 1;
+  double kb[KC_COUNT] = {0};  // algorithmic bytes of one launch of each class
+};
+
+struct scg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int nsm = 148;
+  int64_t n = 0, npad = 0;
+  int R = 0;
+  uint32_t flags = 0;
+  double alpha_orig = 0, alpha = 0, beta0 = 1, b = 0, nrmL = 1, lnN = 0;
+  uint64_t seed = 0;
+  // sharding: world ranks; this context holds shards sh (all of them when emulating)
+  int world = 1, mode = 0;  // mode 0: single, 1: emulated shards, 2: one rank of a multi-process job
+  int rank = 0;
+  std::vector<int64_t> splits;
+  std::vector<Shard *> sh;
+  unsigned long long epoch = 0;
+#ifdef SCG_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+  double *dred = nullptr;  // device scratch for host all-reduces (mode 2)
   int64_t t = 0;
   int64_t launches = 0;
+  int64_t log_cap = 0;
+  // Lanczos vector storage: W slot 0 = start vector g; store mode: slot j-1 = w_j (j <= q);
+  // regenerate mode: slots 1, 2 = ring of w_i
+  int wcap = 0;
+  bool store = true;
   // reconstruction
   bool have_recon = false;
   std::vector<double> lam_raw, lam_orig, lam_tc, err;
@@ -88,21 +124,21 @@ struct scg_ctx {
   std::vector<cudaEvent_t> evpool;
   int64_t kl[KC_COUNT] = {0};
   double kms[KC_COUNT] = {0};
-  double kbytes[KC_COUNT] = {0};     // algorithmic bytes of one launch (fixed-size classes)
-  double kbytes_sum[KC_COUNT] = {0}; // accumulated algorithmic bytes
-  // Lanczos vector storage: slot 0 = start vector g; store mode: slot j-1 = w_j (j <= q);
-  // regenerate mode: slots 1, 2 = ring of w_i
-  double *Wst = nullptr;
-  int wcap = 0;
-  bool store = true;
+  double kbytes_sum[KC_COUNT] = {0};
   // errors
   int failed = 0;
   std::string err_msg;
+
+  int64_t nl_total() const {
+    int64_t s = 0;
+    for (auto *p : sh) s += p->nl;
+    return s;
+  }
+  double *xg(const Shard *s) const { return s->G; }
+  double *wslot(const Shard *s, int j) const { return s->G + (long long)(1 + j) * npad; }
 };
 
 namespace {
-
-enum { SLOT_NU0 = 0, SLOT_OM, SLOT_RHO, SLOT_XX, SLOT_MON, SLOT_NZ, SLOT_INIT, SLOT_COUNT };
 
 scg_status fail(scg_ctx *c, scg_status st, const std::string &msg) {
   if (c) {
@@ -118,6 +154,14 @@ scg_status fail(scg_ctx *c, scg_status st, const std::string &msg) {
     if (e_ != cudaSuccess)                                                                    \
       return fail(c, SCG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));          \
   } while (0)
+
+#ifdef SCG_WITH_NCCL
+#define NK(call)                                                                              \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess) return fail(c, SCG_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+#endif
 
 int grid_for(int64_t rows, int maxgrid) {
   int64_t g = (rows + kBlock - 1) / kBlock;
@@ -150,15 +194,7 @@ cudaEvent_t ev_get(scg_ctx *c) {
 }
 
 template <typename Kern, typename... Args>
-void launch_smem(scg_ctx *c, int cls, Kern kern, dim3 grid, dim3 block, size_t smem, Args... args);
-
-template <typename Kern, typename... Args>
-void launch(scg_ctx *c, int cls, Kern kern, dim3 grid, dim3 block, Args... args) {
-  launch_smem(c, cls, kern, grid, block, 0, args...);
-}
-
-template <typename Kern, typename... Args>
-void launch_smem(scg_ctx *c, int cls, Kern kern, dim3 grid, dim3 block, size_t smem, Args... args) {
+void launch_smem(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 block, size_t smem, Args... args) {
   const bool prof = (c->flags & SCG_PROFILE) != 0;
   EvPair p{};
   if (prof) {
@@ -174,131 +210,415 @@ void launch_smem(scg_ctx *c, int cls, Kern kern, dim3 grid, dim3 block, size_t s
     c->pending.push_back(p);
   }
   c->kl[cls]++;
-  c->kbytes_sum[cls] += c->kbytes[cls];
+  c->kbytes_sum[cls] += bytes;
   c->launches++;
 }
 
-// ---------------------------------------------------------------- small dense fp64 linear algebra (host)
-// R x R matrices, row-major.
-bool chol_upper(const std::vector<double> &B, int R, std::vector<double> &Rc) {  // B = Rc^T Rc
-  Rc.assign((size_t)R * R, 0.0);
-  for (int j = 0; j < R; ++j) {
-    double s = B[(size_t)j * R + j];
-    for (int k = 0; k < j; ++k) s -= Rc[(size_t)k * R + j] * Rc[(size_t)k * R + j];
-    if (!(s > 0.0) || !std::isfinite(s)) return false;
-    const double rjj = std::sqrt(s);
-    Rc[(size_t)j * R + j] = rjj;
-    for (int i = j + 1; i < R; ++i) {
-      double t = B[(size_t)j * R + i];
-      for (int k = 0; k < j; ++k) t -= Rc[(size_t)k * R + j] * Rc[(size_t)k * R + i];
-      Rc[(size_t)j * R + i] = t / rjj;
+template <typename Kern, typename... Args>
+void launch(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 block, Args... args) {
+  launch_smem(c, cls, bytes, kern, grid, block, 0, args...);
+}
+
+Net net_of(const scg_ctx *c, const Shard *s, unsigned long long E) {
+  Net n{};
+  n.mask = c->world > 1 ? s->mask : nullptr;
+  n.G = s->G;
+  n.peerG = s->peerG;
+  n.peerMB = s->peerMB;
+  n.mb = s->mb;
+  n.P = c->world;
+  n.me = s->rank;
+  n.E = E;
+  return n;
+}
+
+// P > 1: the collective half of a reduction -- every shard of this context waits
+// for all ranks' contributions to epoch E and finalizes.
+void pull_all(scg_ctx *c, int kind, int ns, unsigned long long E, const FinArgs &f0) {
+  if (c->world <= 1) return;
+  for (Shard *s : c->sh) {
+    FinArgs f = f0;
+    if (kind == FK_NZ) f.log = s->dlog;
+    if (kind == FK_FROB) f.out = s->dscalar;
+    launch(c, KC_PULL, 0.0, k_pull, dim3(1), dim3(32), kind, ns, net_of(c, s, E), s->sc, f);
+  }
+}
+
+// Sum a small host vector over the ranks of a multi-process job (identity otherwise).
+scg_status host_allreduce(scg_ctx *c, std::vector<double> &v) {
+  if (c->mode != 2 || c->world <= 1 || v.empty()) return SCG_OK;
+#ifdef SCG_WITH_NCCL
+  const size_t bytes = sizeof(double) * v.size();
+  if (v.size() > (size_t)kMaxR * kMaxR * 4) return fail(c, SCG_EINVAL, "host_allreduce: vector too long");
+  CK(cudaMemcpyAsync(c->dred, v.data(), bytes, cudaMemcpyHostToDevice, c->stream));
+  NK(ncclAllReduce(c->dred, c->dred, v.size(), ncclDouble, ncclSum, c->comm, c->stream));
+  CK(cudaMemcpyAsync(v.data(), c->dred, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return SCG_OK;
+#else
+  return fail(c, SCG_EUNSUPPORTED, "built without NCCL");
+#endif
+}
+
+void free_shard(Shard *s) {
+  void *ptrs[] = {s->rp, s->col, s->val, s->wts, s->ldiag, s->cdiag, s->d, s->z, s->y, s->a, s->v, s->G,
+                  s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
+                  s->sc, s->slots, s->dlog, s->longrows, s->sell_perm, s->sell_col, s->sell_meta, s->sell_val,
+                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB};
+  for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  delete s;
+}
+
+// CSR checks of one shard's rows (before any device work).
+scg_status validate_rows(scg_ctx *c, const int64_t *rp, const int32_t *colp, const double *valp, int64_t nl) {
+  const int64_t base = rp[0];
+  for (int64_t r = 0; r < nl; ++r) {
+    if (rp[r + 1] < rp[r]) return fail(c, SCG_EINVAL, "row_ptr not monotone");
+    for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+      const int32_t cc = colp[k - base];
+      if (cc < 0 || cc >= c->n) return fail(c, SCG_EINVAL, "column out of range");
+      if (k > rp[r] && cc <= colp[k - 1 - base]) return fail(c, SCG_EINVAL, "columns not strictly ascending");
+      if (!std::isfinite(valp[k - base])) return fail(c, SCG_EINVAL, "non-finite value");
     }
   }
-  return true;
+  return SCG_OK;
 }
 
-std::vector<double> inv_upper(const std::vector<double> &U, int R) {
-  std::vector<double> X((size_t)R * R, 0.0);
-  for (int j = 0; j < R; ++j) {  // solve U x = e_j
-    for (int i = j; i >= 0; --i) {
-      double s = (i == j) ? 1.0 : 0.0;
-      for (int k = i + 1; k <= j; ++k) s -= U[(size_t)i * R + k] * X[(size_t)k * R + j];
-      X[(size_t)i * R + j] = s / U[(size_t)i * R + i];
+// Host part of shard construction: split this shard's rows into off-diagonal
+// weights w = -L_rj and the diagonal, the long-row list, the SELL-32-sigma layout of
+// the short rows and the halo mask; then allocate and upload.  rp/colp/valp point at
+// this shard's rows (rp[0] may be nonzero).
+scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *colp, const double *valp,
+                       int has_diagonal) {
+  const int64_t nl = s->nl, rb = s->rb;
+  const int R = c->R;
+  const int64_t base = rp[0];
+  std::vector<int> h_rp((size_t)nl + 1);
+  int64_t cnt_off = 0;
+  for (int64_t r = 0; r < nl; ++r)
+    for (int64_t k = rp[r]; k < rp[r + 1]; ++k)
+      if (colp[k - base] != r + rb) cnt_off++;
+  if (cnt_off >= (1ll << 31)) return fail(c, SCG_EINVAL, "too many nonzeros for int32 row pointers");
+  std::vector<int> h_col((size_t)cnt_off);
+  std::vector<double> h_w((size_t)cnt_off), h_diag((size_t)nl, 0.0);
+  std::vector<unsigned char> h_mask;
+  if (c->world > 1) h_mask.assign((size_t)nl, 0);
+  int64_t o = 0;
+  for (int64_t r = 0; r < nl; ++r) {
+    h_rp[(size_t)r] = (int)o;
+    double dsum = 0.0;
+    bool had = false;
+    unsigned m = 0;
+    for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+      const int32_t cc = colp[k - base];
+      const double lv = valp[k - base];
+      if (cc == r + rb) { h_diag[(size_t)r] = lv; had = true; }
+      else {
+        h_col[(size_t)o] = cc;
+        h_w[(size_t)o] = -lv;
+        dsum += -lv;
+        ++o;
+        if (c->world > 1 && (cc < rb || cc >= rb + nl)) {
+          const int q = (int)(std::upper_bound(c->splits.begin(), c->splits.end(), (int64_t)cc) - c->splits.begin()) - 1;
+          m |= 1u << q;
+        }
+      }
+    }
+    if (!has_diagonal || !had) h_diag[(size_t)r] = has_diagonal ? 0.0 : dsum;
+    if (c->world > 1) {
+      h_mask[(size_t)r] = (unsigned char)m;
+      s->halo_rows += m != 0;
     }
   }
-  return X;
+  h_rp[(size_t)nl] = (int)o;
+  s->nnz_off = cnt_off;
+  std::vector<int> h_long;
+  for (int64_t r = 0; r < nl; ++r)
+    if (h_rp[(size_t)r + 1] - h_rp[(size_t)r] > kLongRow) h_long.push_back((int)r);
+  std::stable_sort(h_long.begin(), h_long.end(), [&](int x, int y) {
+    return h_rp[(size_t)x + 1] - h_rp[(size_t)x] > h_rp[(size_t)y + 1] - h_rp[(size_t)y];
+  });
+  s->nlong = (int)h_long.size();
+
+  auto alloc = [&](void **p, size_t bytes) -> bool { return cudaMalloc(p, bytes ? bytes : 8) == cudaSuccess; };
+  s->nlpad = (nl + kWin - 1) / kWin * kWin;
+  const size_t nlb = sizeof(double) * (size_t)s->nlpad;
+  bool ok = alloc((void **)&s->rp, sizeof(int) * (nl + 1)) && alloc((void **)&s->col, sizeof(int) * cnt_off) &&
+            alloc((void **)&s->val, sizeof(double) * cnt_off) && alloc((void **)&s->wts, sizeof(double) * cnt_off) &&
+            alloc((void **)&s->ldiag, nlb) && alloc((void **)&s->cdiag, nlb) && alloc((void **)&s->d, nlb) &&
+            alloc((void **)&s->z, nlb) && alloc((void **)&s->y, nlb) && alloc((void **)&s->a, nlb) &&
+            alloc((void **)&s->v, nlb) && alloc((void **)&s->S, nlb * R) && alloc((void **)&s->Om, nlb * R) &&
+            alloc((void **)&s->sc, sizeof(DevScalars)) && alloc((void **)&s->slots, sizeof(XSlot) * SLOT_COUNT) &&
+            alloc((void **)&s->dscalar, sizeof(double) * 8) &&
+            alloc((void **)&s->dlog, sizeof(scg_iter_rec) * c->log_cap) &&
+            alloc((void **)&s->longrows, sizeof(int) * h_long.size()) &&
+            alloc((void **)&s->mb, sizeof(Mailbox)) && alloc((void **)&s->peerG, sizeof(double *) * kMaxRanks) &&
+            alloc((void **)&s->peerMB, sizeof(Mailbox *) * kMaxRanks);
+  if (!ok) return fail(c, SCG_ENOMEM, "device allocation");
+  if (c->world > 1 && !alloc((void **)&s->mask, (size_t)nl)) return fail(c, SCG_ENOMEM, "halo mask");
+
+  // grid sizes from occupancy
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_a<true>, kBlock, 0);
+  s->grid_rows = grid_for(nl, std::max(1, occ) * c->nsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_primal, kBlock, 0);
+  s->grid_primal = grid_for(nl, std::max(1, occ) * c->nsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_b, kBlock, 0);
+  s->grid_b = grid_for(nl, std::max(1, occ) * c->nsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_combine, kBlock, 0);
+  s->grid_comb = grid_for(nl, std::max(1, occ) * c->nsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dual_sketch, kBlock, 0);
+  s->grid_dual = grid_for(nl, std::max(1, occ) * c->nsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_norm_x, kBlock, 0);
+  s->grid_norm = grid_for(nl, std::max(1, occ) * c->nsm);
+  if (!alloc((void **)&s->gpart, sizeof(double) * (size_t)s->grid_primal * R)) return fail(c, SCG_ENOMEM, "gpart");
+
+  cudaStream_t st = c->stream;
+  CK(cudaMemcpyAsync(s->rp, h_rp.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(s->col, h_col.data(), sizeof(int) * cnt_off, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(s->wts, h_w.data(), sizeof(double) * cnt_off, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(s->ldiag, 0, nlb, st));
+  CK(cudaMemcpyAsync(s->ldiag, h_diag.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, st));
+  if (!h_long.empty())
+    CK(cudaMemcpyAsync(s->longrows, h_long.data(), sizeof(int) * h_long.size(), cudaMemcpyHostToDevice, st));
+  if (c->world > 1) CK(cudaMemcpyAsync(s->mask, h_mask.data(), (size_t)nl, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(s->sc, 0, sizeof(DevScalars), st));
+  CK(cudaMemsetAsync(s->slots, 0, sizeof(XSlot) * SLOT_COUNT, st));
+  CK(cudaMemsetAsync(s->mb, 0, sizeof(Mailbox), st));
+  CK(cudaMemsetAsync(s->z, 0, nlb, st));
+  CK(cudaMemsetAsync(s->y, 0, nlb, st));
+  CK(cudaMemsetAsync(s->S, 0, nlb * R, st));
+  CK(cudaStreamSynchronize(st));  // host vectors go out of scope (the SELL layout follows in build_sell)
+  return SCG_OK;
 }
 
-std::vector<double> matmul(const std::vector<double> &A, const std::vector<double> &B, int R) {
-  std::vector<double> C((size_t)R * R, 0.0);
-  for (int i = 0; i < R; ++i)
-    for (int k = 0; k < R; ++k)
-      for (int j = 0; j < R; ++j) C[(size_t)i * R + j] += A[(size_t)i * R + k] * B[(size_t)k * R + j];
-  return C;
+// SELL layout (needs ||L||_F for the values): rebuilt from the device CSR copy.
+scg_status build_sell(scg_ctx *c, Shard *s) {
+  const int64_t nl = s->nl;
+  const bool scale = (c->flags & SCG_SCALE) != 0;
+  std::vector<int> h_rp((size_t)nl + 1), h_col((size_t)s->nnz_off);
+  std::vector<double> h_w((size_t)s->nnz_off);
+  cudaStream_t st = c->stream;
+  CK(cudaMemcpyAsync(h_rp.data(), s->rp, sizeof(int) * (nl + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_col.data(), s->col, sizeof(int) * s->nnz_off, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_w.data(), s->wts, sizeof(double) * s->nnz_off, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const long long cnt_off = s->nnz_off;
+  const int kSigma = SCG_TMA ? kWin : 256;  // sorting window of SELL-32-sigma (= TMA staging window)
+  std::vector<int> wstart;
+  // uniform |w| is decided over ALL ranks' values (same layout decision everywhere is not
+  // required for correctness, only for the value encoding of this shard)
+  bool uni = cnt_off > 0;
+  const double w0 = cnt_off > 0 ? std::fabs(h_w[0]) : 0.0;
+  for (int64_t k = 0; k < cnt_off && uni; ++k) uni = std::fabs(h_w[(size_t)k]) == w0;
+  s->sell_m0 = scale ? w0 / c->nrmL : w0;  // |C_rj| = fl(|w| / ||L||_F)
+  std::vector<int> perm, scol, win;
+  std::vector<int2> meta;
+  std::vector<double> sval;
+  for (int64_t w = 0; w < nl; w += kSigma) {
+    wstart.push_back((int)meta.size());
+    win.clear();
+    for (int64_t r = w; r < std::min<int64_t>(nl, w + kSigma); ++r)
+      if (h_rp[(size_t)r + 1] - h_rp[(size_t)r] <= kLongRow) win.push_back((int)r);
+    std::stable_sort(win.begin(), win.end(), [&](int x, int y) {
+      return h_rp[(size_t)x + 1] - h_rp[(size_t)x] > h_rp[(size_t)y + 1] - h_rp[(size_t)y];
+    });
+    for (size_t s0 = 0; s0 < win.size(); s0 += 32) {
+      const int cnt = (int)std::min<size_t>(32, win.size() - s0);
+      const int width = h_rp[(size_t)win[s0] + 1] - h_rp[(size_t)win[s0]];
+      meta.push_back(make_int2((int)scol.size(), width));
+      for (int j = 0; j < width; ++j)
+        for (int l = 0; l < 32; ++l) {
+          int cc = -1;
+          double vv = 0.0;
+          if (l < cnt) {
+            const int r = win[s0 + l];
+            const int e = h_rp[(size_t)r] + j;
+            if (e < h_rp[(size_t)r + 1]) {
+              cc = h_col[(size_t)e];
+              const double wv = h_w[(size_t)e];
+              if (uni && wv < 0) cc = (int)((unsigned)cc | 0x80000000u);
+              vv = scale ? wv / c->nrmL : wv;  // = C_rj exactly as k_scale_c forms it
+            }
+          }
+          scol.push_back(cc);
+          if (!uni) sval.push_back(vv);
+        }
+      for (int l = 0; l < 32; ++l) perm.push_back(l < cnt ? win[s0 + l] : -1);
+    }
+    if (scol.size() >= (size_t)INT32_MAX) return fail(c, SCG_EINVAL, "SELL layout too large");
+  }
+  s->nslice = (int)meta.size();
+  wstart.push_back((int)meta.size());
+  s->nwin = (int)wstart.size() - 1;
+  auto alloc = [&](void **p, size_t bytes) -> bool { return cudaMalloc(p, bytes ? bytes : 8) == cudaSuccess; };
+  if (!alloc((void **)&s->sell_wstart, sizeof(int) * wstart.size()) ||
+      !alloc((void **)&s->sell_perm, sizeof(int) * perm.size()) ||
+      !alloc((void **)&s->sell_meta, sizeof(int2) * meta.size()) ||
+      !alloc((void **)&s->sell_col, sizeof(int) * scol.size()) ||
+      (!uni && !alloc((void **)&s->sell_val, sizeof(double) * sval.size())))
+    return fail(c, SCG_ENOMEM, "SELL layout");
+  CK(cudaMemcpyAsync(s->sell_wstart, wstart.data(), sizeof(int) * wstart.size(), cudaMemcpyHostToDevice, st));
+  if (!perm.empty()) CK(cudaMemcpyAsync(s->sell_perm, perm.data(), sizeof(int) * perm.size(), cudaMemcpyHostToDevice, st));
+  if (!meta.empty()) CK(cudaMemcpyAsync(s->sell_meta, meta.data(), sizeof(int2) * meta.size(), cudaMemcpyHostToDevice, st));
+  if (!scol.empty()) CK(cudaMemcpyAsync(s->sell_col, scol.data(), sizeof(int) * scol.size(), cudaMemcpyHostToDevice, st));
+  if (!uni && !sval.empty())
+    CK(cudaMemcpyAsync(s->sell_val, sval.data(), sizeof(double) * sval.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  s->sell_slots = (double)scol.size();
+  s->sell_uniform = uni;
+  {  // grids of the SpMV kernels
+    const bool U = s->sell_uniform;
+    const size_t smem1 = !SCG_TMA ? 0 : (U ? sizeof(TmaSmem<1, true>) : sizeof(TmaSmem<1, false>));
+    const size_t smem2 = !SCG_TMA ? 0 : (U ? sizeof(TmaSmem<2, true>) : sizeof(TmaSmem<2, false>));
+    auto setsm = [&](const void *k, size_t b) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b); };
+    int oa = 1, om = 1, oc = 1;
+    if (U) {
+      setsm((const void *)k_lanczos_a<true>, smem1);
+      setsm((const void *)k_lanczos_c<true>, smem1);
+      setsm((const void *)k_apply_d<true>, smem1);
+      setsm((const void *)k_monitor<true>, smem2);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<true>, kBlock, smem1);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_lanczos_c<true>, kBlock, smem1);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<true>, kBlock, smem2);
+    } else {
+      setsm((const void *)k_lanczos_a<false>, smem1);
+      setsm((const void *)k_lanczos_c<false>, smem1);
+      setsm((const void *)k_apply_d<false>, smem1);
+      setsm((const void *)k_monitor<false>, smem2);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<false>, kBlock, smem1);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_lanczos_c<false>, kBlock, smem1);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<false>, kBlock, smem2);
+    }
+    const int need = SCG_TMA ? std::max(s->nwin, (s->nlong + 7) / 8)
+                             : (int)std::max<int64_t>((s->nslice + 7) / 8, (s->nlong + 7) / 8);
+    s->grid_tiles = std::max(1, std::min(need, std::max(1, oa) * c->nsm));
+    s->grid_mon = std::max(1, std::min(need, std::max(1, om) * c->nsm));
+  }
+  // algorithmic bytes per launch (DESIGN.md section 5)
+  const double N = (double)c->n, NL = (double)nl;
+  const double mat = s->sell_slots * (s->sell_uniform ? 4.0 : 12.0) + 4.0 * NL + 8.0 * s->nslice;
+  const double gath = c->world > 1 ? NL + (double)s->halo_rows : N;  // gathered entries read once
+  s->kb[KC_LANCZOS_A] = mat + 8.0 * NL + 8.0 * gath + 8.0 * NL;
+  s->kb[KC_LANCZOS_B] = 32.0 * NL;
+  s->kb[KC_LANCZOS_C] = mat + 8.0 * NL + 8.0 * gath + 8.0 * NL + 8.0 * NL + 16.0 * NL;
+  s->kb[KC_NORM_X] = 8.0 * NL;
+  s->kb[KC_MONITOR] = mat + 16.0 * NL + 8.0 * gath + 8.0 * NL;
+  s->kb[KC_PRIMAL] = 24.0 * NL + 8.0 * NL * c->R;
+  s->kb[KC_DUAL_SKETCH] = 56.0 * NL + 16.0 * NL * c->R;
+  return SCG_OK;
 }
 
-// cyclic Jacobi eigenvalues of a symmetric matrix (values only)
-std::vector<double> sym_eigvals(std::vector<double> A, int R) {
-  for (int sweep = 0; sweep < 100; ++sweep) {
-    double off = 0.0;
-    for (int i = 0; i < R; ++i)
-      for (int j = i + 1; j < R; ++j) off += A[(size_t)i * R + j] * A[(size_t)i * R + j];
-    if (off == 0.0) break;
-    for (int p = 0; p < R; ++p)
-      for (int q = p + 1; q < R; ++q) {
-        const double apq = A[(size_t)p * R + q];
-        if (apq == 0.0) continue;
-        const double app = A[(size_t)p * R + p], aqq = A[(size_t)q * R + q];
-        const double tau = (aqq - app) / (2.0 * apq);
-        const double t = (tau >= 0 ? 1.0 : -1.0) / (std::fabs(tau) + std::sqrt(1.0 + tau * tau));
-        const double cs = 1.0 / std::sqrt(1.0 + t * t), sn = t * cs;
-        for (int k = 0; k < R; ++k) {
-          const double akp = A[(size_t)k * R + p], akq = A[(size_t)k * R + q];
-          A[(size_t)k * R + p] = cs * akp - sn * akq;
-          A[(size_t)k * R + q] = sn * akp + cs * akq;
-        }
-        for (int k = 0; k < R; ++k) {
-          const double apk = A[(size_t)p * R + k], aqk = A[(size_t)q * R + k];
-          A[(size_t)p * R + k] = cs * apk - sn * aqk;
-          A[(size_t)q * R + k] = sn * apk + cs * aqk;
-        }
+// Allocate the gathered region with `cap` W slots (+ the x slot).
+scg_status alloc_G(scg_ctx *c, Shard *s, int cap) {
+  const size_t bytes = sizeof(double) * (size_t)c->npad * (size_t)(1 + cap);
+  double *G = nullptr;
+  CK(cudaMalloc(&G, bytes));
+  CK(cudaMemsetAsync(G, 0, bytes, c->stream));
+  if (s->G) {  // keep W slot 0 (the start vector g of the next iteration)
+    CK(cudaMemcpyAsync(G + c->npad, s->G + c->npad, sizeof(double) * c->npad, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(s->G);
+  }
+  s->G = G;
+  if (c->world == 1) {
+    CK(cudaMemcpyAsync(s->peerG, &s->G, sizeof(double *), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(s->peerMB, &s->mb, sizeof(Mailbox *), cudaMemcpyHostToDevice, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return SCG_OK;
+}
+
+// Peer tables: every shard's view of every rank's G and mailbox.
+scg_status connect_peers(scg_ctx *c, const void *uid) {
+  const int P = c->world;
+  std::vector<double *> hG(P, nullptr);
+  std::vector<Mailbox *> hM(P, nullptr);
+  if (c->mode == 1 || P == 1) {
+    for (Shard *s : c->sh) { hG[s->rank] = s->G; hM[s->rank] = s->mb; }
+  } else {
+#ifdef SCG_WITH_NCCL
+    Shard *s = c->sh[0];
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    NK(ncclCommInitRank(&c->comm, P, id, c->rank));
+    CK(cudaMalloc(&c->dred, sizeof(double) * kMaxR * kMaxR * 4));
+    cudaIpcMemHandle_t hh[2];
+    CK(cudaIpcGetMemHandle(&hh[0], s->G));
+    CK(cudaIpcGetMemHandle(&hh[1], s->mb));
+    char *dbuf = nullptr;
+    const size_t per = sizeof(hh);
+    CK(cudaMalloc(&dbuf, per * P));
+    CK(cudaMemcpyAsync(dbuf + per * c->rank, hh, per, cudaMemcpyHostToDevice, c->stream));
+    NK(ncclAllGather(dbuf + per * c->rank, dbuf, per, ncclChar, c->comm, c->stream));
+    std::vector<cudaIpcMemHandle_t> all((size_t)2 * P);
+    CK(cudaMemcpyAsync(all.data(), dbuf, per * P, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(dbuf);
+    for (int q = 0; q < P; ++q) {
+      if (q == c->rank) { hG[q] = s->G; hM[q] = s->mb; continue; }
+      void *pg = nullptr, *pm = nullptr;
+      CK(cudaIpcOpenMemHandle(&pg, all[(size_t)2 * q], cudaIpcMemLazyEnablePeerAccess));
+      CK(cudaIpcOpenMemHandle(&pm, all[(size_t)2 * q + 1], cudaIpcMemLazyEnablePeerAccess));
+      s->ipc_opened.push_back(pg);
+      s->ipc_opened.push_back(pm);
+      hG[q] = (double *)pg;
+      hM[q] = (Mailbox *)pm;
+    }
+#else
+    (void)uid;
+    return fail(c, SCG_EUNSUPPORTED, "multi-process sharding needs the NCCL build");
+#endif
+  }
+  for (Shard *s : c->sh) {
+    CK(cudaMemcpyAsync(s->peerG, hG.data(), sizeof(double *) * P, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(s->peerMB, hM.data(), sizeof(Mailbox *) * P, cudaMemcpyHostToDevice, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+#ifdef SCG_WITH_NCCL
+  if (c->mode == 2 && P > 1) {  // every rank's tables are in place before anyone stores to a peer
+    NK(ncclAllReduce(c->dred, c->dred, 1, ncclDouble, ncclSum, c->comm, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+#endif
+  return SCG_OK;
+}
+
+scg_status balanced_splits(const int64_t *rp, int64_t n, int world, std::vector<int64_t> &sp) {
+  // smallest contiguous split whose largest part cost (rows + nnz) is minimal: binary search on the cap
+  sp.assign((size_t)world + 1, 0);
+  auto cost = [&](int64_t a, int64_t b) { return (b - a) + (rp[b] - rp[a]); };
+  int64_t lo = 1, hi = cost(0, n);
+  auto feasible = [&](int64_t cap, std::vector<int64_t> *out) {
+    int64_t r = 0;
+    for (int p = 0; p < world; ++p) {
+      if (out) (*out)[(size_t)p] = r;
+      // advance r as far as the cap allows (binary search on the prefix)
+      int64_t a = r, b = n;
+      while (a < b) {
+        const int64_t mid = a + (b - a + 1) / 2;
+        if (cost(r, mid) <= cap) a = mid;
+        else b = mid - 1;
       }
+      r = a;
+    }
+    if (out) (*out)[(size_t)world] = n;
+    return r >= n;
+  };
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (feasible(mid, nullptr)) hi = mid;
+    else lo = mid + 1;
   }
-  std::vector<double> ev(R);
-  for (int i = 0; i < R; ++i) ev[i] = A[(size_t)i * R + i];
-  return ev;
-}
-
-// One-sided Jacobi SVD of a square R x R matrix F = U diag(sv) V^T; U returned row-major.
-void svd_jacobi(std::vector<double> F, int R, std::vector<double> &U, std::vector<double> &sv) {
-  // work on columns of F
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    bool rotated = false;
-    for (int p = 0; p < R; ++p)
-      for (int q = p + 1; q < R; ++q) {
-        double alpha = 0, beta = 0, gamma = 0;
-        for (int i = 0; i < R; ++i) {
-          const double fp = F[(size_t)i * R + p], fq = F[(size_t)i * R + q];
-          alpha += fp * fp;
-          beta += fq * fq;
-          gamma += fp * fq;
-        }
-        if (gamma == 0.0 || std::fabs(gamma) <= 1e-300 + 2.2e-16 * std::sqrt(alpha * beta)) continue;
-        rotated = true;
-        const double zeta = (beta - alpha) / (2.0 * gamma);
-        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / std::sqrt(1.0 + t * t), sn = cs * t;
-        for (int i = 0; i < R; ++i) {
-          const double fp = F[(size_t)i * R + p], fq = F[(size_t)i * R + q];
-          F[(size_t)i * R + p] = cs * fp - sn * fq;
-          F[(size_t)i * R + q] = sn * fp + cs * fq;
-        }
-      }
-    if (!rotated) break;
-  }
-  std::vector<int> idx(R);
-  std::vector<double> nrm(R);
-  for (int j = 0; j < R; ++j) {
-    double s = 0;
-    for (int i = 0; i < R; ++i) s += F[(size_t)i * R + j] * F[(size_t)i * R + j];
-    nrm[j] = std::sqrt(s);
-    idx[j] = j;
-  }
-  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return nrm[a] > nrm[b]; });
-  U.assign((size_t)R * R, 0.0);
-  sv.assign(R, 0.0);
-  for (int jj = 0; jj < R; ++jj) {
-    const int j = idx[jj];
-    sv[jj] = nrm[j];
-    for (int i = 0; i < R; ++i) U[(size_t)i * R + jj] = nrm[j] > 0 ? F[(size_t)i * R + j] / nrm[j] : (i == jj ? 1.0 : 0.0);
-  }
-}
-
-double matlab_eps(double x) {
-  if (x == 0.0) return std::ldexp(1.0, -1074);
-  int e;
-  std::frexp(std::fabs(x), &e);  // x = m 2^e, m in [0.5, 1)
-  return std::ldexp(1.0, e - 1 - 52);
+  feasible(lo, &sp);
+  // no empty shard: every rank owns at least one row when n >= world
+  for (int p = 1; p <= world; ++p)
+    if (sp[(size_t)p] <= sp[(size_t)p - 1]) sp[(size_t)p] = std::min<int64_t>(n, sp[(size_t)p - 1] + 1);
+  for (int p = world - 1; p >= 1; --p)
+    if (sp[(size_t)p] >= sp[(size_t)p + 1]) sp[(size_t)p] = sp[(size_t)p + 1] - 1;
+  return SCG_OK;
 }
 
 }  // namespace
@@ -339,17 +659,44 @@ scg_status sketchycgal_nccl_unique_id(void *out128) {
 #endif
 }
 
+scg_status sketchycgal_row_splits(const int64_t *row_ptr, int64_t n, int32_t world, int64_t *splits) {
+  if (!row_ptr || !splits || n < 1 || world < 1 || world > kMaxRanks || world > n) return SCG_EINVAL;
+  std::vector<int64_t> sp;
+  balanced_splits(row_ptr, n, world, sp);
+  std::memcpy(splits, sp.data(), sizeof(int64_t) * sp.size());
+  return SCG_OK;
+}
+
+int64_t sketchycgal_halo_plan(const int64_t *row_ptr, const int32_t *col_idx, int64_t row_begin, int64_t row_end,
+                              const int64_t *splits, int32_t world, uint8_t *mask) {
+  if (!row_ptr || !col_idx || !splits || !mask || world < 1 || world > kMaxRanks || row_end < row_begin) return -1;
+  const int64_t base = row_ptr[0];
+  int64_t halo = 0;
+  for (int64_t r = 0; r < row_end - row_begin; ++r) {
+    unsigned m = 0;
+    for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
+      const int64_t cc = col_idx[k - base];
+      if (cc >= row_begin && cc < row_end) continue;
+      const int q = (int)(std::upper_bound(splits, splits + world + 1, cc) - splits) - 1;
+      if (q < 0 || q >= world) return -1;
+      m |= 1u << q;
+    }
+    mask[r] = (uint8_t)m;
+    halo += m != 0;
+  }
+  return halo;
+}
+
 void sketchycgal_destroy(scg_ctx *c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  void *ptrs[] = {c->rp, c->col, c->val, c->wts, c->ldiag, c->cdiag, c->d, c->z, c->y, c->a, c->v, c->Wst,
-                  c->x, c->S, c->Om, c->gpart, c->U, c->tmp1, c->tmp2, c->dmat, c->partial,
-                  c->dlam, c->dscalar, c->sc, c->slots, c->dlog, c->longrows,
-                  c->sell_perm, c->sell_col, c->sell_meta, c->sell_val,
-                  c->sell_wstart};
-  for (void *p : ptrs)
-    if (p) cudaFree(p);
+  for (Shard *s : c->sh) free_shard(s);
+  c->sh.clear();
+#ifdef SCG_WITH_NCCL
+  if (c->comm) ncclCommDestroy(c->comm);
+#endif
+  if (c->dred) cudaFree(c->dred);
   for (auto &p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto e : c->evpool) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -362,23 +709,17 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   if (!out) return SCG_EINVAL;
   *out = nullptr;
   scg_ctx *c = new scg_ctx();
-  auto bad = [&](scg_status st, const char *msg) {
-    std::string m = msg;
+  auto bad = [&](scg_status st) {
     sketchycgal_destroy(c);
-    (void)m;
     return st;
   };
-  if (!L || !L->row_ptr || !L->col_idx || !L->val) return bad(SCG_EINVAL, "null CSR");
+  if (!L || !L->row_ptr || !L->col_idx || !L->val) return bad(SCG_EINVAL);
   const int64_t n = L->n_global;
   if (n < 2 || R < 1 || R > n || R > kMaxR || !(alpha > 0) || !(beta0 > 0) || !std::isfinite(alpha) ||
       !std::isfinite(beta0))
-    return bad(SCG_EINVAL, "bad scalar argument");
-  if (dist && dist->world > 1) return bad(SCG_EUNSUPPORTED, "multi-GPU: use the dist build");
-  if (L->row_begin != 0 || L->row_end != n) return bad(SCG_EINVAL, "single GPU owns all rows");
-  if (n >= (1ll << 31)) return bad(SCG_EINVAL, "n too large for int32 column ids");
+    return bad(SCG_EINVAL);
+  if (n >= (1ll << 31)) return bad(SCG_EINVAL);
   c->n = n;
-  c->nl = L->row_end - L->row_begin;
-  c->rb = L->row_begin;
   c->R = R;
   c->flags = flags;
   c->alpha_orig = alpha;
@@ -389,245 +730,119 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   c->alpha = scale ? 1.0 : alpha;
   c->b = scale ? 1.0 / (double)n : 1.0;
   c->lnN = std::log((double)n);
+  c->log_cap = 1024;
+  c->npad = (n + kWin - 1) / kWin * kWin;
 
-  // ---- host: validate, split L into off-diagonal weights w = -L_rj and the diagonal
-  const int64_t nl = c->nl;
-  const int64_t *rp = L->row_ptr;
-  if (rp[0] != 0) return bad(SCG_EINVAL, "row_ptr[0] != 0");
-  std::vector<int> h_rp((size_t)nl + 1);
-  std::vector<int> h_col;
-  std::vector<double> h_w, h_diag((size_t)nl, 0.0);
-  int64_t cnt_off = 0;
-  for (int64_t r = 0; r < nl; ++r) {
-    if (rp[r + 1] < rp[r]) return bad(SCG_EINVAL, "row_ptr not monotone");
-    for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
-      const int32_t cc = L->col_idx[k];
-      if (cc < 0 || cc >= n) return bad(SCG_EINVAL, "column out of range");
-      if (k > rp[r] && cc <= L->col_idx[k - 1]) return bad(SCG_EINVAL, "columns not strictly ascending");
-      if (!std::isfinite(L->val[k])) return bad(SCG_EINVAL, "non-finite value");
-      if (cc != r + c->rb) cnt_off++;
-    }
+  // ---- sharding mode and row splits
+  int world = 1, emulate = 0, rank = 0;
+  if (dist && dist->world > 1) {
+    world = dist->world;
+    emulate = dist->emulate;
+    rank = dist->rank;
+    if (world > kMaxRanks || world > n || rank < 0 || rank >= world) return bad(SCG_EINVAL);
+    if (!emulate && (!dist->row_splits || !dist->nccl_unique_id)) return bad(SCG_EINVAL);
   }
-  if (cnt_off >= (1ll << 31)) return bad(SCG_EINVAL, "too many nonzeros for int32 row pointers");
-  h_col.resize((size_t)cnt_off);
-  h_w.resize((size_t)cnt_off);
-  int64_t o = 0;
-  for (int64_t r = 0; r < nl; ++r) {
-    h_rp[(size_t)r] = (int)o;
-    double dsum = 0.0;
-    bool had = false;
-    for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
-      const int32_t cc = L->col_idx[k];
-      if (cc == r + c->rb) { h_diag[(size_t)r] = L->val[k]; had = true; }
-      else {
-        h_col[(size_t)o] = cc;
-        h_w[(size_t)o] = -L->val[k];
-        dsum += -L->val[k];
-        ++o;
-      }
-    }
-    if (!L->has_diagonal || !had) h_diag[(size_t)r] = L->has_diagonal ? 0.0 : dsum;
+  c->world = world;
+  c->mode = world == 1 ? 0 : (emulate ? 1 : 2);
+  c->rank = emulate ? 0 : rank;
+  if (world > 1 && dist->row_splits) c->splits.assign(dist->row_splits, dist->row_splits + world + 1);
+  else if (world > 1) {
+    if (L->row_begin != 0 || L->row_end != n) return bad(SCG_EINVAL);
+    balanced_splits(L->row_ptr, n, world, c->splits);
+  } else c->splits = {0, n};
+  if (c->splits.front() != 0 || c->splits.back() != n) return bad(SCG_EINVAL);
+  for (int p = 0; p < world; ++p)
+    if (c->splits[(size_t)p + 1] <= c->splits[(size_t)p]) return bad(SCG_EINVAL);
+  if (c->mode == 2) {
+    if (L->row_begin != c->splits[(size_t)rank] || L->row_end != c->splits[(size_t)rank + 1]) return bad(SCG_EINVAL);
+  } else if (L->row_begin != 0 || L->row_end != n) {
+    return bad(SCG_EINVAL);
   }
-  h_rp[(size_t)nl] = (int)o;
-  c->nnz_off = cnt_off;
-  // long rows (kernels.cuh row engine), longest first so they start early
-  std::vector<int> h_long;
-  for (int64_t r = 0; r < nl; ++r)
-    if (h_rp[(size_t)r + 1] - h_rp[(size_t)r] > kLongRow) h_long.push_back((int)r);
-  std::stable_sort(h_long.begin(), h_long.end(), [&](int x, int y) {
-    return h_rp[(size_t)x + 1] - h_rp[(size_t)x] > h_rp[(size_t)y + 1] - h_rp[(size_t)y];
-  });
+  if (L->row_ptr[0] != 0) return bad(SCG_EINVAL);
+  {
+    const int64_t nrows = L->row_end - L->row_begin;
+    if (validate_rows(c, L->row_ptr, L->col_idx, L->val, nrows)) return bad(SCG_EINVAL);
+  }
 
   // ---- device setup
-  cudaError_t e0 = cudaSetDevice(device);
-  if (e0 != cudaSuccess) return bad(SCG_ECUDA, "cudaSetDevice");
+  if (cudaSetDevice(device) != cudaSuccess) return bad(SCG_ECUDA);
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
   if (cuda_stream) c->stream = (cudaStream_t)cuda_stream;
   else {
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bad(SCG_ECUDA, "stream");
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bad(SCG_ECUDA);
     c->own_stream = true;
   }
-  auto alloc = [&](void **p, size_t bytes) -> bool { return cudaMalloc(p, bytes ? bytes : 8) == cudaSuccess; };
-  // vectors are padded to whole kWin-row windows (the TMA engine copies whole windows)
-  c->npad = (n + kWin - 1) / kWin * kWin;
-  const int64_t nlpad = (nl + kWin - 1) / kWin * kWin;
-  const size_t nb = sizeof(double) * (size_t)c->npad, nlb = sizeof(double) * (size_t)nlpad;
-  bool ok = alloc((void **)&c->rp, sizeof(int) * (nl + 1)) && alloc((void **)&c->col, sizeof(int) * cnt_off) &&
-            alloc((void **)&c->val, sizeof(double) * cnt_off) && alloc((void **)&c->wts, sizeof(double) * cnt_off) &&
-            alloc((void **)&c->ldiag, nlb) && alloc((void **)&c->cdiag, nlb) && alloc((void **)&c->d, nlb) &&
-            alloc((void **)&c->z, nlb) && alloc((void **)&c->y, nlb) && alloc((void **)&c->a, nlb) &&
-            alloc((void **)&c->v, nlb) && alloc((void **)&c->Wst, nb * 3) && alloc((void **)&c->x, nb) &&
-            alloc((void **)&c->S, nlb * R) && alloc((void **)&c->Om, nlb * R) &&
-            alloc((void **)&c->sc, sizeof(DevScalars)) && alloc((void **)&c->slots, sizeof(XSlot) * SLOT_COUNT) &&
-            alloc((void **)&c->dscalar, sizeof(double) * 8);
-  if (!ok) return bad(SCG_ENOMEM, "device allocation");
-  c->log_cap = 1024;
-  if (!alloc((void **)&c->dlog, sizeof(scg_iter_rec) * c->log_cap)) return bad(SCG_ENOMEM, "log");
-  c->nlong = (int)h_long.size();
-  if (!alloc((void **)&c->longrows, sizeof(int) * h_long.size())) return bad(SCG_ENOMEM, "long rows");
-
-  // grid sizes from occupancy
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_a<true>, kBlock, 0);
-  c->grid_rows = grid_for(nl, std::max(1, occ) * c->nsm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_c<true>, kBlock, 0);
-  c->grid_tiles = grid_for(std::max<int64_t>(nl, (int64_t)c->nlong * 32), std::max(1, occ) * c->nsm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_primal, kBlock, 0);
-  c->grid_primal = grid_for(nl, std::max(1, occ) * c->nsm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_b, kBlock, 0);
-  c->grid_b = grid_for(nl, std::max(1, occ) * c->nsm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_combine, kBlock, 0);
-  c->grid_comb = grid_for(nl, std::max(1, occ) * c->nsm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dual_sketch, kBlock, 0);
-  c->grid_dual = grid_for(nl, std::max(1, occ) * c->nsm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_norm_x, kBlock, 0);
-  c->grid_norm = grid_for(nl, std::max(1, occ) * c->nsm);
-  c->wcap = 3;
-  c->g = c->Wst;
+  scg_status st;
+  const int nshard = c->mode == 1 ? world : 1;
+  for (int p = 0; p < nshard; ++p) {
+    Shard *s = new Shard();
+    c->sh.push_back(s);
+    s->rank = c->mode == 1 ? p : c->rank;
+    s->rb = c->splits[(size_t)s->rank];
+    s->nl = c->splits[(size_t)s->rank + 1] - s->rb;
+    const int64_t off = c->mode == 2 ? 0 : s->rb;  // index of this shard's first row in L->row_ptr
+    if ((st = build_shard(c, s, L->row_ptr + off, L->col_idx + L->row_ptr[off], L->val + L->row_ptr[off],
+                          L->has_diagonal)))
+      return bad(st);
+  }
+  // Lanczos vector storage.  One rank: grown on demand.  Sharded: fixed at init (peers map it).
   c->store = (flags & SCG_REGENERATE) == 0;
-  if (!alloc((void **)&c->gpart, sizeof(double) * (size_t)c->grid_primal * R)) return bad(SCG_ENOMEM, "gpart");
+  int cap = 3;
+  if (world > 1 && c->store) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t need = sizeof(double) * (size_t)c->npad * (size_t)kMaxQ * nshard;
+    if (need + (size_t)(2ull << 30) < fr) cap = kMaxQ - 1;
+    else c->store = false;  // (multi-process: every rank must decide alike, checked after connect_peers)
+  }
+  c->wcap = cap;
+  for (Shard *s : c->sh)
+    if ((st = alloc_G(c, s, cap))) return bad(st);
+  if ((st = connect_peers(c, dist ? dist->nccl_unique_id : nullptr))) return bad(st);
+#ifdef SCG_WITH_NCCL
+  if (c->mode == 2) {  // agree on the storage mode (all ranks store, or none)
+    std::vector<double> v{c->store ? 0.0 : 1.0};
+    if ((st = host_allreduce(c, v))) return bad(st);
+    if (v[0] != 0.0 && c->store) return bad(fail(c, SCG_ENOMEM, "Lanczos store does not fit on every rank"));
+  }
+#endif
 
-  cudaStream_t s = c->stream;
-#define CKI(call)                                                           \
-  do {                                                                      \
-    if ((call) != cudaSuccess) return bad(SCG_ECUDA, #call);                \
-  } while (0)
-  CKI(cudaMemcpyAsync(c->rp, h_rp.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice, s));
-  CKI(cudaMemcpyAsync(c->col, h_col.data(), sizeof(int) * cnt_off, cudaMemcpyHostToDevice, s));
-  CKI(cudaMemcpyAsync(c->wts, h_w.data(), sizeof(double) * cnt_off, cudaMemcpyHostToDevice, s));
-  CKI(cudaMemcpyAsync(c->ldiag, h_diag.data(), nlb, cudaMemcpyHostToDevice, s));
-  if (!h_long.empty())
-    CKI(cudaMemcpyAsync(c->longrows, h_long.data(), sizeof(int) * h_long.size(), cudaMemcpyHostToDevice, s));
-  CKI(cudaMemsetAsync(c->sc, 0, sizeof(DevScalars), s));
-  CKI(cudaMemsetAsync(c->slots, 0, sizeof(XSlot) * SLOT_COUNT, s));
-  CKI(cudaMemsetAsync(c->z, 0, nlb, s));
-  CKI(cudaMemsetAsync(c->y, 0, nlb, s));
-  CKI(cudaMemsetAsync(c->S, 0, nlb * R, s));
-  CKI(cudaMemsetAsync(c->x, 0, nb, s));
-  CKI(cudaMemsetAsync(c->Wst, 0, nb * 3, s));
-  // ||L||_F (exact sum over all stored entries) and C = -L / ||L||_F
-  const int gnnz = (int)std::min<long long>(std::max<long long>(1, (cnt_off + kBlock - 1) / kBlock), 8 * c->nsm);
-  launch(c, KC_OTHER, k_frob, dim3(gnnz), dim3(kBlock), (const double *)c->wts, (long long)cnt_off,
-         (const double *)c->ldiag, (int)nl, c->slots + SLOT_INIT, c->sc, c->dscalar);
-  CKI(cudaMemcpyAsync(&c->nrmL, c->dscalar, sizeof(double), cudaMemcpyDeviceToHost, s));
-  CKI(cudaStreamSynchronize(s));
+  // ||L||_F (exact sum over all stored entries of all ranks) and C = -L / ||L||_F
+  const unsigned long long E0 = ++c->epoch;
+  for (Shard *s : c->sh) {
+    const int gnnz = (int)std::min<long long>(std::max<long long>(1, (s->nnz_off + kBlock - 1) / kBlock), 8 * c->nsm);
+    launch(c, KC_OTHER, 0.0, k_frob, dim3(gnnz), dim3(kBlock), (const double *)s->wts, (long long)s->nnz_off,
+           (const double *)s->ldiag, (int)s->nl, s->slots + SLOT_INIT, s->sc, s->dscalar, net_of(c, s, E0));
+  }
+  pull_all(c, FK_FROB, 1, E0, FinArgs{});
+  if (cudaMemcpyAsync(&c->nrmL, c->sh[0]->dscalar, sizeof(double), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return bad(SCG_ECUDA);
+  {
+    int err = 0;
+    cudaMemcpy(&err, &c->sh[0]->sc->err, sizeof(int), cudaMemcpyDeviceToHost);
+    if (err & 2) return bad(fail(c, SCG_ECUDA, "collective timeout at init"));
+  }
   c->nrmL = std::sqrt(c->nrmL);
-  if (!(c->nrmL > 0) || !std::isfinite(c->nrmL)) return bad(SCG_EINVAL, "||L||_F must be positive and finite");
-  CKI(cudaMemcpyAsync(c->dscalar, &c->nrmL, sizeof(double), cudaMemcpyHostToDevice, s));
-  {  // SELL-32-sigma layout of the short rows (kernels.cuh row engine)
-    const int kSigma = SCG_TMA ? kWin : 256;  // sorting window of SELL-32-sigma (= TMA staging window)
-    std::vector<int> wstart;
-    bool uni = cnt_off > 0;
-    const double w0 = cnt_off > 0 ? std::fabs(h_w[0]) : 0.0;
-    for (int64_t k = 0; k < cnt_off && uni; ++k) uni = std::fabs(h_w[(size_t)k]) == w0;
-    c->sell_m0 = scale ? w0 / c->nrmL : w0;  // |C_rj| = fl(|w| / ||L||_F)
-    std::vector<int> perm, scol, win;
-    std::vector<int2> meta;
-    std::vector<double> sval;
-    for (int64_t w = 0; w < nl; w += kSigma) {
-      wstart.push_back((int)meta.size());
-      win.clear();
-      for (int64_t r = w; r < std::min<int64_t>(nl, w + kSigma); ++r)
-        if (h_rp[(size_t)r + 1] - h_rp[(size_t)r] <= kLongRow) win.push_back((int)r);
-      std::stable_sort(win.begin(), win.end(), [&](int x, int y) {
-        return h_rp[(size_t)x + 1] - h_rp[(size_t)x] > h_rp[(size_t)y + 1] - h_rp[(size_t)y];
-      });
-      for (size_t s0 = 0; s0 < win.size(); s0 += 32) {
-        const int cnt = (int)std::min<size_t>(32, win.size() - s0);
-        const int width = h_rp[(size_t)win[s0] + 1] - h_rp[(size_t)win[s0]];
-        meta.push_back(make_int2((int)scol.size(), width));
-        for (int j = 0; j < width; ++j)
-          for (int l = 0; l < 32; ++l) {
-            int cc = -1;
-            double vv = 0.0;
-            if (l < cnt) {
-              const int r = win[s0 + l];
-              const int e = h_rp[(size_t)r] + j;
-              if (e < h_rp[(size_t)r + 1]) {
-                cc = h_col[(size_t)e];
-                const double wv = h_w[(size_t)e];
-                if (uni && wv < 0) cc = (int)((unsigned)cc | 0x80000000u);
-                vv = scale ? wv / c->nrmL : wv;  // = C_rj exactly as k_scale_c forms it
-              }
-            }
-            scol.push_back(cc);
-            if (!uni) sval.push_back(vv);
-          }
-        for (int l = 0; l < 32; ++l) perm.push_back(l < cnt ? win[s0 + l] : -1);
-      }
-      if (scol.size() >= (size_t)INT32_MAX) return bad(SCG_EINVAL, "SELL layout too large");
-    }
-    c->nslice = (int)meta.size();
-    wstart.push_back((int)meta.size());
-    c->nwin = (int)wstart.size() - 1;
-    if (!alloc((void **)&c->sell_wstart, sizeof(int) * wstart.size())) return bad(SCG_ENOMEM, "SELL windows");
-    CKI(cudaMemcpyAsync(c->sell_wstart, wstart.data(), sizeof(int) * wstart.size(), cudaMemcpyHostToDevice, s));
-    if (!alloc((void **)&c->sell_perm, sizeof(int) * perm.size()) ||
-        !alloc((void **)&c->sell_meta, sizeof(int2) * meta.size()) ||
-        !alloc((void **)&c->sell_col, sizeof(int) * scol.size()) ||
-        (!uni && !alloc((void **)&c->sell_val, sizeof(double) * sval.size())))
-      return bad(SCG_ENOMEM, "SELL layout");
-    CKI(cudaMemcpyAsync(c->sell_perm, perm.data(), sizeof(int) * perm.size(), cudaMemcpyHostToDevice, s));
-    CKI(cudaMemcpyAsync(c->sell_meta, meta.data(), sizeof(int2) * meta.size(), cudaMemcpyHostToDevice, s));
-    CKI(cudaMemcpyAsync(c->sell_col, scol.data(), sizeof(int) * scol.size(), cudaMemcpyHostToDevice, s));
-    if (!uni) CKI(cudaMemcpyAsync(c->sell_val, sval.data(), sizeof(double) * sval.size(), cudaMemcpyHostToDevice, s));
-    CKI(cudaStreamSynchronize(s));  // host vectors go out of scope
-    c->sell_slots = (double)scol.size();
-    c->sell_uniform = uni;
+  if (!(c->nrmL > 0) || !std::isfinite(c->nrmL)) return bad(SCG_EINVAL);
+  for (Shard *s : c->sh) {
+    if ((st = build_sell(c, s))) return bad(st);
+    if (cudaMemcpyAsync(s->dscalar, &c->nrmL, sizeof(double), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+      return bad(SCG_ECUDA);
+    const int gnnz = (int)std::min<long long>(std::max<long long>(1, (s->nnz_off + kBlock - 1) / kBlock), 8 * c->nsm);
+    launch(c, KC_OTHER, 0.0, k_scale_c, dim3(gnnz), dim3(kBlock), (const double *)s->wts, (long long)s->nnz_off,
+           (const double *)s->ldiag, (int)s->nl, (const double *)s->dscalar, scale ? 1 : 0, s->val, s->cdiag);
+    launch(c, KC_OTHER, 0.0, k_omega, dim3(8 * c->nsm), dim3(kBlock), s->Om, (int)s->nl, (long long)s->rb, (int)R, seed);
+    const double beta1 = beta0 * std::sqrt(2.0);
+    launch(c, KC_OTHER, 0.0, k_init_d, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z, (const double *)s->y,
+           (const double *)s->cdiag, s->d, (int)s->nl, c->b, beta1);
   }
-  {  // dynamic shared memory and grids of the TMA-staged SpMV kernels
-    const bool U = c->sell_uniform;
-    c->smem1 = !SCG_TMA ? 0 : (U ? sizeof(TmaSmem<1, true>) : sizeof(TmaSmem<1, false>));
-    c->smem2 = !SCG_TMA ? 0 : (U ? sizeof(TmaSmem<2, true>) : sizeof(TmaSmem<2, false>));
-    auto setsm = [&](const void *k, size_t b) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b); };
-    if (U) {
-      setsm((const void *)k_lanczos_a<true>, c->smem1);
-      setsm((const void *)k_lanczos_c<true>, c->smem1);
-      setsm((const void *)k_apply_d<true>, c->smem1);
-      setsm((const void *)k_monitor<true>, c->smem2);
-    } else {
-      setsm((const void *)k_lanczos_a<false>, c->smem1);
-      setsm((const void *)k_lanczos_c<false>, c->smem1);
-      setsm((const void *)k_apply_d<false>, c->smem1);
-      setsm((const void *)k_monitor<false>, c->smem2);
-    }
-    int oa = 1, om = 1;
-    if (U) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<true>, kBlock, c->smem1);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<true>, kBlock, c->smem2);
-    } else {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<false>, kBlock, c->smem1);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<false>, kBlock, c->smem2);
-    }
-    const int need = SCG_TMA ? std::max(c->nwin, (c->nlong + 7) / 8)
-                             : (int)std::max<int64_t>((c->nslice + 7) / 8, (c->nlong + 7) / 8);
-    c->grid_tiles = std::max(1, std::min(need, std::max(1, oa) * c->nsm));
-    c->grid_mon = std::max(1, std::min(need, std::max(1, om) * c->nsm));
-  }
-  launch(c, KC_OTHER, k_scale_c, dim3(gnnz), dim3(kBlock), (const double *)c->wts, (long long)cnt_off,
-         (const double *)c->ldiag, (int)nl, (const double *)c->dscalar, scale ? 1 : 0, c->val, c->cdiag);
-  launch(c, KC_OTHER, k_omega, dim3(8 * c->nsm), dim3(kBlock), c->Om, (int)nl, (long long)c->rb, (int)R, seed);
-  const double beta1 = beta0 * std::sqrt(2.0);
-  launch(c, KC_OTHER, k_init_d, dim3(c->grid_rows), dim3(kBlock), (const double *)c->z, (const double *)c->y,
-         (const double *)c->cdiag, c->d, (int)nl, c->b, beta1);
-  launch(c, KC_OTHER, k_gen_start, dim3(c->grid_rows), dim3(kBlock), c->g, (int)nl, (long long)c->rb, seed,
-         (long long)1, c->slots + SLOT_NU0, c->sc, 1);
-  CKI(cudaGetLastError());
-  CKI(cudaStreamSynchronize(s));
-#undef CKI
-  // algorithmic bytes per launch (DESIGN.md section 5)
-  const double N = (double)n, NL = (double)nl, NNZ = (double)cnt_off;
-  // SpMV matrix stream: SELL slots (4 B col [+ 8 B val]) + perm 4 B/row + slice meta + long-row CSR
-  const double mat = c->sell_slots * (c->sell_uniform ? 4.0 : 12.0) + 4.0 * NL + 8.0 * c->nslice;
-  c->kbytes[KC_LANCZOS_A] = mat + 8.0 * NL + 8.0 * N + 8.0 * NL;
-  c->kbytes[KC_LANCZOS_B] = 32.0 * NL;
-  c->kbytes[KC_TRIDIAG] = 0.0;
-  c->kbytes[KC_LANCZOS_C] = mat + 8.0 * NL + 8.0 * N + 8.0 * NL + 8.0 * NL + 16.0 * NL;
-  c->kbytes[KC_NORM_X] = 8.0 * NL;
-  c->kbytes[KC_COMBINE] = 0.0;  // 8 nl k + 8 nl per launch, accumulated in step()
-  c->kbytes[KC_MONITOR] = mat + 16.0 * NL + 8.0 * N + 8.0 * NL;
-  c->kbytes[KC_PRIMAL] = 24.0 * NL + 8.0 * NL * R;
-  c->kbytes[KC_DUAL_SKETCH] = 56.0 * NL + 16.0 * NL * R;
+  const unsigned long long E1 = ++c->epoch;
+  for (Shard *s : c->sh)
+    launch(c, KC_OTHER, 0.0, k_gen_start, dim3(s->grid_rows), dim3(kBlock), c->wslot(s, 0), (int)s->nl,
+           (long long)s->rb, seed, (long long)1, s->slots + SLOT_NU0, s->sc, net_of(c, s, E1));
+  pull_all(c, FK_RHO0, 1, E1, FinArgs{});
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) return bad(SCG_ECUDA);
   for (int k = 0; k < KC_COUNT; ++k) { c->kl[k] = 0; c->kms[k] = 0; c->kbytes_sum[k] = 0; }
   c->launches = 0;
   *out = c;
@@ -639,28 +854,19 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
   if (c->failed) return SCG_ESTATE;
   if (T < 0) return SCG_EINVAL;
   CK(cudaSetDevice(c->device));
-  if (c->t + T > c->log_cap) {  // grow the device iteration log
+  if (c->t + T > c->log_cap) {  // grow the device iteration logs
     int64_t cap = std::max<int64_t>(c->log_cap * 2, c->t + T);
-    scg_iter_rec *nl = nullptr;
-    CK(cudaMalloc(&nl, sizeof(scg_iter_rec) * cap));
-    CK(cudaMemcpyAsync(nl, c->dlog, sizeof(scg_iter_rec) * c->t, cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    cudaFree(c->dlog);
-    c->dlog = nl;
+    for (Shard *s : c->sh) {
+      scg_iter_rec *nlg = nullptr;
+      CK(cudaMalloc(&nlg, sizeof(scg_iter_rec) * cap));
+      CK(cudaMemcpyAsync(nlg, s->dlog, sizeof(scg_iter_rec) * c->t, cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      cudaFree(s->dlog);
+      s->dlog = nlg;
+    }
     c->log_cap = cap;
   }
-
-  const int nl = (int)c->nl;
-  const long long rb = c->rb;
-  Csr C{c->rp, c->col, c->val};
-  Rows TT{c->longrows, c->nlong, c->sell_perm, c->sell_meta, c->sell_col, c->sell_val, c->sell_m0, c->nslice,
-          c->sell_wstart, c->nwin};
-  const int GT = c->grid_tiles;
-  const long long ldw = (long long)c->npad;
-  const bool U = c->sell_uniform;
-  auto kA = U ? k_lanczos_a<true> : k_lanczos_a<false>;
-  auto kC = U ? k_lanczos_c<true> : k_lanczos_c<false>;
-  auto kM = U ? k_monitor<true> : k_monitor<false>;
+  const bool P1 = c->world == 1;
   for (int64_t it = 0; it < T; ++it) {
     const int64_t t = c->t + 1;
     // Alg. 4 line 5 and the q_t schedule (CAC-6), evaluated on the host
@@ -678,62 +884,110 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     if (q > c->n - 1) q = c->n - 1;
     if (q > kMaxQ - 1) q = kMaxQ - 1;
     A.q = (int)q;
-    if (c->store && c->wcap < q) {  // grow the Lanczos-vector store (slot 0 = g is kept)
-      const int cap = (int)std::min<int64_t>(q + 16, kMaxQ);
-      double *nw = nullptr;
+    if (P1 && c->store && c->wcap < q) {  // grow the Lanczos-vector store (slot 0 = g is kept)
+      const int cap = (int)std::min<int64_t>(q + 16, kMaxQ - 1);
       size_t fr = 0, tot = 0;
       cudaMemGetInfo(&fr, &tot);
-      const size_t need = sizeof(double) * (size_t)c->npad * cap;
-      if (need + (size_t)(1ull << 30) < fr && cudaMalloc(&nw, need) == cudaSuccess) {
-        CK(cudaMemcpyAsync(nw, c->Wst, sizeof(double) * c->npad, cudaMemcpyDeviceToDevice, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        cudaFree(c->Wst);
-        c->Wst = nw;
-        c->g = nw;
+      const size_t need = sizeof(double) * (size_t)c->npad * (cap + 1);
+      if (need + (size_t)(1ull << 30) < fr) {
+        scg_status st = alloc_G(c, c->sh[0], cap);
+        if (st) return st;
         c->wcap = cap;
       } else {
         c->store = false;  // does not fit: storage-optimal two-pass mode
       }
     }
-    auto slot = [&](int j) -> double * {  // buffer holding w_j (j >= 1; w_1 = g)
-      if (c->store) return c->Wst + (long long)(j - 1) * ldw;
-      return j == 1 ? c->Wst : c->Wst + (long long)(1 + (j & 1)) * ldw;
+    auto slot = [&](const Shard *s, int j) -> double * {  // buffer holding w_j (j >= 1; w_1 = g)
+      if (c->store) return c->wslot(s, j - 1);
+      return j == 1 ? c->wslot(s, 0) : c->wslot(s, 1 + (j & 1));
     };
     // ---- Lanczos pass 1 (Alg. 2 lines 1-9)
     for (int i = 1; i <= q; ++i) {
-      const double *Xi = slot(i);
-      launch_smem(c, KC_LANCZOS_A, kA, dim3(GT), dim3(kBlock), c->smem1, C, TT, (const double *)c->d, Xi, nl, rb, i, c->a,
-             c->slots + SLOT_OM, c->sc, 1);
+      unsigned long long E = ++c->epoch;
+      for (Shard *s : c->sh) {
+        Csr C{s->rp, s->col, s->val};
+        Rows TT{s->longrows, s->nlong, s->sell_perm, s->sell_meta, s->sell_col, s->sell_val, s->sell_m0, s->nslice,
+                s->sell_wstart, s->nwin};
+        auto kA = s->sell_uniform ? k_lanczos_a<true> : k_lanczos_a<false>;
+        launch(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->grid_tiles), dim3(kBlock), C, TT,
+               (const double *)s->d, (const double *)slot(s, i), (int)s->nl, (long long)s->rb, i, s->a,
+               s->slots + SLOT_OM, s->sc, net_of(c, s, E));
+      }
+      FinArgs f{};
+      f.i = i;
+      pull_all(c, FK_OM, 1, E, f);
       if (i < q) {
-        const double *Xim1 = (i == 1) ? nullptr : slot(i - 1);
-        launch(c, KC_LANCZOS_B, k_lanczos_b, dim3(c->grid_b), dim3(kBlock), (const double *)c->a, Xi, Xim1, slot(i + 1),
-               nl, rb, i, c->slots + SLOT_RHO, c->sc, 1);
+        E = ++c->epoch;
+        for (Shard *s : c->sh) {
+          const double *Xim1 = (i == 1) ? nullptr : slot(s, i - 1);
+          launch(c, KC_LANCZOS_B, s->kb[KC_LANCZOS_B], k_lanczos_b, dim3(s->grid_b), dim3(kBlock),
+                 (const double *)s->a, (const double *)slot(s, i), Xim1, slot(s, i + 1), (int)s->nl, (long long)s->rb,
+                 i, s->slots + SLOT_RHO, s->sc, net_of(c, s, E));
+        }
+        pull_all(c, FK_RHO, 1, E, f);
       }
     }
-    // ---- tridiagonal eigenpair (lines 11-12)
-    launch(c, KC_TRIDIAG, k_tridiag, dim3(1), dim3(32), c->sc, (int)q);
+    // ---- tridiagonal eigenpair (lines 11-12), replicated on every rank
+    for (Shard *s : c->sh) launch(c, KC_TRIDIAG, 0.0, k_tridiag, dim3(1), dim3(32), s->sc, (int)q);
     if (c->store) {  // ---- line 13 from the stored vectors (Remark)
-      c->kbytes[KC_COMBINE] = 8.0 * (double)c->nl * (double)q + 8.0 * (double)c->nl;
-      launch(c, KC_COMBINE, k_combine, dim3(c->grid_comb), dim3(kBlock), (const double *)c->Wst, ldw, c->x, nl, rb,
-             c->slots + SLOT_XX, c->sc, 1);
+      const unsigned long long E = ++c->epoch;
+      for (Shard *s : c->sh)
+        launch(c, KC_COMBINE, 8.0 * (double)s->nl * (double)q + 8.0 * (double)s->nl, k_combine, dim3(s->grid_comb),
+               dim3(kBlock), (const double *)c->wslot(s, 0), (long long)c->npad, c->xg(s), (int)s->nl,
+               (long long)s->rb, s->slots + SLOT_XX, s->sc, net_of(c, s, E));
+      pull_all(c, FK_NUX, 1, E, FinArgs{});
     } else {  // ---- pass 2 (line 13): regenerate v_2..v_k
       for (int j = 1; j < q; ++j) {
-        const double *Xj = slot(j);
-        const double *Xjm1 = (j == 1) ? nullptr : slot(j - 1);
-        launch_smem(c, KC_LANCZOS_C, kC, dim3(GT), dim3(kBlock), c->smem1, C, TT, (const double *)c->d, Xj, Xjm1,
-               slot(j + 1), c->x, nl, rb, j, (const DevScalars *)c->sc);
+        const unsigned long long E = ++c->epoch;
+        for (Shard *s : c->sh) {
+          Csr C{s->rp, s->col, s->val};
+          Rows TT{s->longrows, s->nlong, s->sell_perm, s->sell_meta, s->sell_col, s->sell_val, s->sell_m0, s->nslice,
+                  s->sell_wstart, s->nwin};
+          auto kC = s->sell_uniform ? k_lanczos_c<true> : k_lanczos_c<false>;
+          const double *Xjm1 = (j == 1) ? nullptr : slot(s, j - 1);
+          launch(c, KC_LANCZOS_C, s->kb[KC_LANCZOS_C], kC, dim3(s->grid_tiles), dim3(kBlock), C, TT,
+                 (const double *)s->d, (const double *)slot(s, j), Xjm1, slot(s, j + 1), c->xg(s), (int)s->nl,
+                 (long long)s->rb, j, s->sc, s->slots + SLOT_BAR, net_of(c, s, E));
+        }
+        FinArgs f{};
+        f.i = j;
+        pull_all(c, FK_BAR, 0, E, f);
       }
-      launch(c, KC_NORM_X, k_norm_x, dim3(c->grid_norm), dim3(kBlock), (const double *)c->g, c->x, nl, rb,
-             c->slots + SLOT_XX, c->sc, 1);
+      const unsigned long long E = ++c->epoch;
+      for (Shard *s : c->sh)
+        launch(c, KC_NORM_X, s->kb[KC_NORM_X], k_norm_x, dim3(s->grid_norm), dim3(kBlock),
+               (const double *)c->wslot(s, 0), c->xg(s), (int)s->nl, (long long)s->rb, s->slots + SLOT_XX, s->sc,
+               net_of(c, s, E));
+      pull_all(c, FK_NUX, 1, E, FinArgs{});
     }
     // ---- monitors, primal, dual, sketch (Alg. 4 lines 8-10)
-    launch_smem(c, KC_MONITOR, kM, dim3(c->grid_mon), dim3(kBlock), c->smem2, C, TT, (const double *)c->d, (const double *)c->cdiag,
-           (const double *)c->x, c->v, nl, rb, c->slots + SLOT_MON, c->sc, 1);
-    launch(c, KC_PRIMAL, k_primal, dim3(c->grid_primal), dim3(kBlock), (const double *)c->v, c->z,
-           (const double *)c->Om, nl, c->R, A, c->gpart, c->slots + SLOT_NZ, c->sc, c->dlog, 1);
-    launch(c, KC_DUAL_SKETCH, k_dual_sketch, dim3(c->grid_dual), dim3(kBlock), (const double *)c->z, c->y, c->d,
-           (const double *)c->cdiag, (const double *)c->v, c->S, c->g, nl, rb, c->R, A, c->seed,
-           c->slots + SLOT_NU0, c->sc, 1);
+    unsigned long long E = ++c->epoch;
+    for (Shard *s : c->sh) {
+      Csr C{s->rp, s->col, s->val};
+      Rows TT{s->longrows, s->nlong, s->sell_perm, s->sell_meta, s->sell_col, s->sell_val, s->sell_m0, s->nslice,
+              s->sell_wstart, s->nwin};
+      auto kM = s->sell_uniform ? k_monitor<true> : k_monitor<false>;
+      launch(c, KC_MONITOR, s->kb[KC_MONITOR], kM, dim3(s->grid_mon), dim3(kBlock), C, TT, (const double *)s->d,
+             (const double *)s->cdiag, (const double *)c->xg(s), s->v, (int)s->nl, (long long)s->rb,
+             s->slots + SLOT_MON, s->sc, net_of(c, s, E));
+    }
+    pull_all(c, FK_MON, 3, E, FinArgs{});
+    E = ++c->epoch;
+    for (Shard *s : c->sh)
+      launch(c, KC_PRIMAL, s->kb[KC_PRIMAL], k_primal, dim3(s->grid_primal), dim3(kBlock), (const double *)s->v, s->z,
+             (const double *)s->Om, (int)s->nl, c->R, A, s->gpart, s->slots + SLOT_NZ, s->sc, s->dlog, net_of(c, s, E));
+    {
+      FinArgs f{};
+      f.R = c->R;
+      f.A = A;
+      pull_all(c, FK_NZ, 1, E, f);
+    }
+    E = ++c->epoch;
+    for (Shard *s : c->sh)
+      launch(c, KC_DUAL_SKETCH, s->kb[KC_DUAL_SKETCH], k_dual_sketch, dim3(s->grid_dual), dim3(kBlock),
+             (const double *)s->z, s->y, s->d, (const double *)s->cdiag, (const double *)s->v, s->S, c->wslot(s, 0),
+             (int)s->nl, (long long)s->rb, c->R, A, c->seed, s->slots + SLOT_NU0, s->sc, net_of(c, s, E));
+    pull_all(c, FK_RHO0, 1, E, FinArgs{});
     c->t = t;
   }
   CK(cudaGetLastError());
@@ -746,9 +1000,12 @@ scg_status sketchycgal_synchronize(scg_ctx *c) {
   if (c->failed) return SCG_ESTATE;
   CK(cudaSetDevice(c->device));
   CK(cudaStreamSynchronize(c->stream));
-  int err = 0;
-  CK(cudaMemcpy(&err, &c->sc->err, sizeof(int), cudaMemcpyDeviceToHost));
-  if (err) return fail(c, SCG_ERANGE, "exact-sum summand out of range (non-finite or >= 2^100)");
+  for (Shard *s : c->sh) {
+    int err = 0;
+    CK(cudaMemcpy(&err, &s->sc->err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err & 2) return fail(c, SCG_ECUDA, "collective timeout (a rank's contribution never arrived)");
+    if (err) return fail(c, SCG_ERANGE, "exact-sum summand out of range (non-finite or >= 2^100)");
+  }
   return SCG_OK;
 }
 
@@ -756,7 +1013,7 @@ scg_status sketchycgal_iter_log(scg_ctx *c, int64_t t0, int64_t count, scg_iter_
   if (!c || !out || t0 < 1 || count < 0 || t0 + count - 1 > c->t) return SCG_EINVAL;
   scg_status st = sketchycgal_synchronize(c);
   if (st) return st;
-  CK(cudaMemcpy(out, c->dlog + (t0 - 1), sizeof(scg_iter_rec) * count, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out, c->sh[0]->dlog + (t0 - 1), sizeof(scg_iter_rec) * count, cudaMemcpyDeviceToHost));
   return SCG_OK;
 }
 
@@ -764,20 +1021,29 @@ scg_status sketchycgal_get_state(scg_ctx *c, int32_t which, double *out) {
   if (!c || !out) return SCG_EINVAL;
   scg_status st = sketchycgal_synchronize(c);
   if (st) return st;
-  const size_t nlb = sizeof(double) * (size_t)c->nl;
-  const double *src = nullptr;
-  size_t bytes = nlb;
-  switch (which) {
-    case 0: src = c->z; break;
-    case 1: src = c->y; break;
-    case 2: src = c->S; bytes = nlb * c->R; break;
-    case 3: src = c->Om; bytes = nlb * c->R; break;
-    case 4: src = c->v; break;
-    case 5: src = c->d; break;
-    case 6: src = c->cdiag; break;
-    default: return SCG_EINVAL;
+  const int64_t NL = c->nl_total();
+  int64_t off = 0;
+  for (Shard *s : c->sh) {
+    const size_t nlb = sizeof(double) * (size_t)s->nl;
+    const double *src = nullptr;
+    bool mat = false;
+    switch (which) {
+      case 0: src = s->z; break;
+      case 1: src = s->y; break;
+      case 2: src = s->S; mat = true; break;
+      case 3: src = s->Om; mat = true; break;
+      case 4: src = s->v; break;
+      case 5: src = s->d; break;
+      case 6: src = s->cdiag; break;
+      default: return SCG_EINVAL;
+    }
+    if (mat) {  // column-major with leading dimension NL (all rows of this context)
+      CK(cudaMemcpy2D(out + off, sizeof(double) * NL, src, sizeof(double) * s->nl, nlb, c->R, cudaMemcpyDeviceToHost));
+    } else {
+      CK(cudaMemcpy(out + off, src, nlb, cudaMemcpyDeviceToHost));
+    }
+    off += s->nl;
   }
-  CK(cudaMemcpy(out, src, bytes, cudaMemcpyDeviceToHost));
   return SCG_OK;
 }
 
@@ -785,48 +1051,56 @@ scg_status sketchycgal_apply_D(scg_ctx *c, const double *xh, double *yh) {
   if (!c || !xh || !yh) return SCG_EINVAL;
   scg_status st = sketchycgal_synchronize(c);
   if (st) return st;
-  // use tmp buffers: x into c->x is not allowed (state); allocate scratch
   double *dx = nullptr, *dy = nullptr;
   CK(cudaMalloc(&dx, sizeof(double) * c->npad));
-  CK(cudaMalloc(&dy, sizeof(double) * c->nl));
   CK(cudaMemcpy(dx, xh, sizeof(double) * c->n, cudaMemcpyHostToDevice));
-  Csr C{c->rp, c->col, c->val};
-  Rows TT{c->longrows, c->nlong, c->sell_perm, c->sell_meta, c->sell_col, c->sell_val, c->sell_m0, c->nslice,
-          c->sell_wstart, c->nwin};
-  launch_smem(c, KC_OTHER, c->sell_uniform ? k_apply_d<true> : k_apply_d<false>, dim3(c->grid_tiles), dim3(kBlock),
-              c->smem1, C, TT, (const double *)c->d, (const double *)dx,
-         (int)c->nl, (long long)c->rb, dy);
-  CK(cudaStreamSynchronize(c->stream));
-  CK(cudaMemcpy(yh, dy, sizeof(double) * c->nl, cudaMemcpyDeviceToHost));
+  int64_t off = 0;
+  for (Shard *s : c->sh) {
+    CK(cudaMalloc(&dy, sizeof(double) * std::max<int64_t>(1, s->nl)));
+    Csr C{s->rp, s->col, s->val};
+    Rows TT{s->longrows, s->nlong, s->sell_perm, s->sell_meta, s->sell_col, s->sell_val, s->sell_m0, s->nslice,
+            s->sell_wstart, s->nwin};
+    launch(c, KC_OTHER, 0.0, s->sell_uniform ? k_apply_d<true> : k_apply_d<false>, dim3(s->grid_tiles), dim3(kBlock),
+           C, TT, (const double *)s->d, (const double *)dx, (int)s->nl, (long long)s->rb, dy);
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(yh + off, dy, sizeof(double) * s->nl, cudaMemcpyDeviceToHost));
+    cudaFree(dy);
+    off += s->nl;
+  }
   cudaFree(dx);
-  cudaFree(dy);
   return SCG_OK;
 }
 
 // ---------------------------------------------------------------- reconstruction (Alg. 3 / SM3)
-static scg_status gram(scg_ctx *c, const double *A, const double *B, std::vector<double> &G) {
+// G = sum over all rows (all shards, all ranks) of A[:,i] B[:,j].
+static scg_status gram(scg_ctx *c, double *Shard::*A, double *Shard::*B, std::vector<double> &G) {
   const int R = c->R;
-  const int gx = std::max(1, std::min(grid_for(c->nl, 4 * c->nsm), 64));
-  const size_t need = (size_t)R * R * gx;
-  if (!c->partial) CK(cudaMalloc(&c->partial, sizeof(double) * (size_t)kMaxR * kMaxR * 64));
-  launch(c, KC_OTHER, k_colpair, dim3(gx, R * R), dim3(kBlock), A, B, (int)c->nl, R, c->partial);
-  std::vector<double> h(need);
-  CK(cudaMemcpyAsync(h.data(), c->partial, sizeof(double) * need, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
   G.assign((size_t)R * R, 0.0);
-  for (int p = 0; p < R * R; ++p) {
-    double s = 0.0;
-    for (int b = 0; b < gx; ++b) s += h[(size_t)p * gx + b];
-    G[(size_t)p] = s;
+  for (Shard *s : c->sh) {
+    const int gx = std::max(1, std::min(grid_for(s->nl, 4 * c->nsm), 64));
+    const size_t need = (size_t)R * R * gx;
+    launch(c, KC_OTHER, 0.0, k_colpair, dim3(gx, R * R), dim3(kBlock), (const double *)(s->*A),
+           (const double *)(s->*B), (int)s->nl, R, s->partial);
+    std::vector<double> h(need);
+    CK(cudaMemcpyAsync(h.data(), s->partial, sizeof(double) * need, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int p = 0; p < R * R; ++p) {
+      double sum = 0.0;
+      for (int b = 0; b < gx; ++b) sum += h[(size_t)p * gx + b];
+      G[(size_t)p] += sum;
+    }
   }
-  return SCG_OK;
+  return host_allreduce(c, G);
 }
 
-static scg_status rowmat(scg_ctx *c, double *out, const double *A, const double *B, double beta,
+static scg_status rowmat(scg_ctx *c, double *Shard::*out, double *Shard::*A, double *Shard::*B, double beta,
                          const std::vector<double> &M) {
-  CK(cudaMemcpyAsync(c->dmat, M.data(), sizeof(double) * M.size(), cudaMemcpyHostToDevice, c->stream));
-  launch(c, KC_OTHER, k_rowmat, dim3(grid_for(c->nl, 4 * c->nsm)), dim3(kBlock), out, A, B, beta,
-         (const double *)c->dmat, (int)c->nl, c->R);
+  for (Shard *s : c->sh) {
+    CK(cudaMemcpyAsync(s->dmat, M.data(), sizeof(double) * M.size(), cudaMemcpyHostToDevice, c->stream));
+    launch(c, KC_OTHER, 0.0, k_rowmat, dim3(grid_for(s->nl, 4 * c->nsm)), dim3(kBlock), s->*out,
+           (const double *)(s->*A), B ? (const double *)(s->*B) : (const double *)nullptr, beta,
+           (const double *)s->dmat, (int)s->nl, c->R);
+  }
   return SCG_OK;
 }
 
@@ -836,16 +1110,19 @@ scg_status sketchycgal_reconstruct(scg_ctx *c, double *Uh, double *Lambda, doubl
   scg_status st = sketchycgal_synchronize(c);
   if (st) return st;
   const int R = c->R;
-  const size_t nlbR = sizeof(double) * (size_t)c->nl * R;
-  if (!c->U) {
-    CK(cudaMalloc(&c->U, nlbR));
-    CK(cudaMalloc(&c->tmp1, nlbR));
-    CK(cudaMalloc(&c->tmp2, nlbR));
-    CK(cudaMalloc(&c->dmat, sizeof(double) * kMaxR * kMaxR));
-    CK(cudaMalloc(&c->dlam, sizeof(double) * kMaxR));
-  }
+  for (Shard *s : c->sh)
+    if (!s->U) {
+      const size_t nlbR = sizeof(double) * (size_t)std::max<int64_t>(1, s->nl) * R;
+      CK(cudaMalloc(&s->U, nlbR));
+      CK(cudaMalloc(&s->tmp1, nlbR));
+      CK(cudaMalloc(&s->tmp2, nlbR));
+      CK(cudaMalloc(&s->dmat, sizeof(double) * kMaxR * kMaxR));
+      CK(cudaMalloc(&s->dlam, sizeof(double) * kMaxR));
+      CK(cudaMalloc(&s->partial, sizeof(double) * (size_t)kMaxR * kMaxR * 64));
+    }
   std::vector<double> Gss, Gos, Goo;
-  if ((st = gram(c, c->S, c->S, Gss)) || (st = gram(c, c->Om, c->S, Gos)) || (st = gram(c, c->Om, c->Om, Goo)))
+  if ((st = gram(c, &Shard::S, &Shard::S, Gss)) || (st = gram(c, &Shard::Om, &Shard::S, Gos)) ||
+      (st = gram(c, &Shard::Om, &Shard::Om, Goo)))
     return st;
   std::vector<double> ev = sym_eigvals(Gss, R);
   double lmax = 0.0;
@@ -868,10 +1145,10 @@ scg_status sketchycgal_reconstruct(scg_ctx *c, double *Uh, double *Lambda, doubl
   }
   if (!ok) return fail(c, SCG_ECHOL, "Cholesky failed after 40 shift doublings");
   // Y = S_sigma Rc^{-1}   (line 15: S/L)
-  if ((st = rowmat(c, c->tmp1, c->S, c->Om, sigma, inv_upper(Rc, R)))) return st;
+  if ((st = rowmat(c, &Shard::tmp1, &Shard::S, &Shard::Om, sigma, inv_upper(Rc, R)))) return st;
   // CholeskyQR2 of Y: Y = Q Rf
   std::vector<double> G1, R1, G2, R2;
-  if ((st = gram(c, c->tmp1, c->tmp1, G1))) return st;
+  if ((st = gram(c, &Shard::tmp1, &Shard::tmp1, G1))) return st;
   if (!chol_upper(G1, R, R1)) {
     // shifted CholeskyQR: add a tiny diagonal shift
     double tr = 0;
@@ -879,17 +1156,17 @@ scg_status sketchycgal_reconstruct(scg_ctx *c, double *Uh, double *Lambda, doubl
     for (int i = 0; i < R; ++i) G1[(size_t)i * R + i] += 1e-15 * tr;
     if (!chol_upper(G1, R, R1)) return fail(c, SCG_ECHOL, "CholeskyQR failed");
   }
-  if ((st = rowmat(c, c->tmp2, c->tmp1, nullptr, 0.0, inv_upper(R1, R)))) return st;
-  if ((st = gram(c, c->tmp2, c->tmp2, G2))) return st;
+  if ((st = rowmat(c, &Shard::tmp2, &Shard::tmp1, nullptr, 0.0, inv_upper(R1, R)))) return st;
+  if ((st = gram(c, &Shard::tmp2, &Shard::tmp2, G2))) return st;
   if (!chol_upper(G2, R, R2)) return fail(c, SCG_ECHOL, "CholeskyQR2 failed");
-  if ((st = rowmat(c, c->tmp1, c->tmp2, nullptr, 0.0, inv_upper(R2, R)))) return st;  // Q in tmp1
+  if ((st = rowmat(c, &Shard::tmp1, &Shard::tmp2, nullptr, 0.0, inv_upper(R2, R)))) return st;  // Q in tmp1
   std::vector<double> Rf = matmul(R2, R1, R);
   std::vector<double> Ur, sv;
   svd_jacobi(Rf, R, Ur, sv);
-  if ((st = rowmat(c, c->U, c->tmp1, nullptr, 0.0, Ur))) return st;  // U = Q Ur
+  if ((st = rowmat(c, &Shard::U, &Shard::tmp1, nullptr, 0.0, Ur))) return st;  // U = Q Ur
   // Lambda = max(0, Sigma^2 - sigma) (line 16); err (SM3 line 6); trace correction (Alg. 4 line 13)
   double tau = 0.0;
-  CK(cudaMemcpy(&tau, &c->sc->tau, sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&tau, &c->sh[0]->sc->tau, sizeof(double), cudaMemcpyDeviceToHost));
   const double unit = c->alpha_orig / c->alpha;
   c->lam_raw.assign(R, 0.0);
   c->lam_orig.assign(R, 0.0);
@@ -911,26 +1188,58 @@ scg_status sketchycgal_reconstruct(scg_ctx *c, double *Uh, double *Lambda, doubl
   if (errh)
     for (int k = 0; k < R; ++k) errh[k] = c->err[k];
   CK(cudaStreamSynchronize(c->stream));
-  if (Uh) CK(cudaMemcpy(Uh, c->U, nlbR, cudaMemcpyDeviceToHost));
+  if (Uh) {
+    const int64_t NL = c->nl_total();
+    int64_t off = 0;
+    for (Shard *s : c->sh) {
+      CK(cudaMemcpy2D(Uh + off, sizeof(double) * NL, s->U, sizeof(double) * s->nl, sizeof(double) * s->nl, R,
+                      cudaMemcpyDeviceToHost));
+      off += s->nl;
+    }
+  }
   c->have_recon = true;
   return SCG_OK;
 }
 
+// Per-column statistics of the reconstruction summed over all rows of all ranks
+// (which: 0 u_k^T L u_k, 1 cut weight of sgn(U[:,k]), 2 sum (diag X^ - 1)^2).
 static scg_status colstats(scg_ctx *c, int which, const double *lam_host, std::vector<double> &outk) {
   const int R = c->R;
-  const int gx = std::max(1, std::min(grid_for(c->nl, 4 * c->nsm), 64));
-  if (lam_host) CK(cudaMemcpyAsync(c->dlam, lam_host, sizeof(double) * R, cudaMemcpyHostToDevice, c->stream));
   const int ny = which == 2 ? 1 : R;
-  launch(c, KC_OTHER, k_colstats, dim3(gx, ny), dim3(kBlock), (const int *)c->rp, (const int *)c->col,
-         (const double *)c->wts, (const double *)c->ldiag, (const double *)c->U, (const double *)c->U,
-         (const double *)c->dlam, (int)c->nl, (long long)c->rb, (long long)c->n, R, which, c->partial);
-  std::vector<double> h((size_t)ny * gx);
-  CK(cudaMemcpyAsync(h.data(), c->partial, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
   outk.assign(ny, 0.0);
-  for (int k = 0; k < ny; ++k)
-    for (int b = 0; b < gx; ++b) outk[k] += h[(size_t)k * gx + b];
-  return SCG_OK;
+  auto run = [&](Shard *s, const double *Ug, long long ldg, int k0, int cols) -> scg_status {
+    const int gx = std::max(1, std::min(grid_for(s->nl, 4 * c->nsm), 64));
+    launch(c, KC_OTHER, 0.0, k_colstats, dim3(gx, cols), dim3(kBlock), (const int *)s->rp, (const int *)s->col,
+           (const double *)s->wts, (const double *)s->ldiag, (const double *)s->U, Ug, ldg, k0,
+           (const double *)s->dlam, (int)s->nl, (long long)s->rb, R, which, s->partial);
+    std::vector<double> h((size_t)cols * gx);
+    CK(cudaMemcpyAsync(h.data(), s->partial, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int y = 0; y < cols; ++y)
+      for (int b = 0; b < gx; ++b) outk[(size_t)(which == 2 ? 0 : k0 + y)] += h[(size_t)y * gx + b];
+    return SCG_OK;
+  };
+  scg_status st;
+  for (Shard *s : c->sh)
+    if (lam_host) CK(cudaMemcpyAsync(s->dlam, lam_host, sizeof(double) * R, cudaMemcpyHostToDevice, c->stream));
+  if (which == 2 || c->world == 1) {
+    for (Shard *s : c->sh)
+      if ((st = run(s, s->U, (long long)s->nl, 0, ny))) return st;
+  } else {  // sharded: gather one column at a time into the x slot (halo stores + barrier)
+    for (int k = 0; k < R; ++k) {
+      const unsigned long long E = ++c->epoch;
+      for (Shard *s : c->sh)
+        launch(c, KC_OTHER, 0.0, k_push_col, dim3(grid_for(s->nl, 4 * c->nsm)), dim3(kBlock),
+               (const double *)(s->U + (long long)k * s->nl), c->xg(s), (int)s->nl, (long long)s->rb,
+               s->slots + SLOT_BAR, s->sc, net_of(c, s, E));
+      FinArgs f{};
+      f.i = -1;
+      pull_all(c, FK_BAR, 0, E, f);
+      for (Shard *s : c->sh)
+        if ((st = run(s, c->xg(s), 0, k, 1))) return st;
+    }
+  }
+  return host_allreduce(c, outk);
 }
 
 scg_status sketchycgal_objective(scg_ctx *c, double out[2]) {
@@ -938,7 +1247,7 @@ scg_status sketchycgal_objective(scg_ctx *c, double out[2]) {
   scg_status st = sketchycgal_synchronize(c);
   if (st) return st;
   double p = 0.0;
-  CK(cudaMemcpy(&p, &c->sc->p, sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&p, &c->sh[0]->sc->p, sizeof(double), cudaMemcpyDeviceToHost));
   const bool scale = (c->flags & SCG_SCALE) != 0;
   out[0] = scale ? -p * c->nrmL * c->alpha_orig / c->alpha : -p;
   out[1] = NAN;
@@ -958,16 +1267,19 @@ scg_status sketchycgal_feasibility(scg_ctx *c, double out[3]) {
   scg_status st = sketchycgal_synchronize(c);
   if (st) return st;
   // implicit: || n z~ - 1 || / (1 + sqrt n) in original units (scaled: z_orig = z * alpha_orig)
-  std::vector<double> z((size_t)c->nl);
-  CK(cudaMemcpy(z.data(), c->z, sizeof(double) * c->nl, cudaMemcpyDeviceToHost));
   const double unit = c->alpha_orig / c->alpha;
-  double s = 0.0;
-  for (int64_t r = 0; r < c->nl; ++r) {
-    const double e = (z[(size_t)r] - c->b) * unit;
-    s += e * e;
+  std::vector<double> ssum{0.0};
+  for (Shard *s : c->sh) {
+    std::vector<double> z((size_t)s->nl);
+    CK(cudaMemcpy(z.data(), s->z, sizeof(double) * s->nl, cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < s->nl; ++r) {
+      const double e = (z[(size_t)r] - c->b) * unit;
+      ssum[0] += e * e;
+    }
   }
+  if ((st = host_allreduce(c, ssum))) return st;
   const double nb = std::sqrt((double)c->n);
-  out[0] = std::sqrt(s) / (1.0 + nb);
+  out[0] = std::sqrt(ssum[0]) / (1.0 + nb);
   out[1] = out[2] = NAN;
   if (c->have_recon) {
     const std::vector<double> &lam = (c->flags & SCG_TRACE_CORRECT) ? c->lam_tc : c->lam_orig;
@@ -989,10 +1301,19 @@ scg_status sketchycgal_round(scg_ctx *c, int8_t *chi, double *cut_weight) {
   int best = 0;
   for (int k = 1; k < c->R; ++k)
     if (w[k] > w[best]) best = k;
-  std::vector<double> u((size_t)c->nl);
-  CK(cudaMemcpy(u.data(), c->U + (size_t)best * c->nl, sizeof(double) * c->nl, cudaMemcpyDeviceToHost));
-  const int flip = u[0] >= 0.0 ? 1 : -1;  // normalize chi_0 = +1 (global row 0 is local on one GPU)
-  for (int64_t r = 0; r < c->nl; ++r) chi[r] = (int8_t)((u[(size_t)r] >= 0.0 ? 1 : -1) * flip);
+  // chi_0 = +1: the sign of U[0, best] lives on the rank owning global row 0
+  std::vector<double> u0{0.0};
+  for (Shard *s : c->sh)
+    if (s->rb == 0) CK(cudaMemcpy(&u0[0], s->U + (size_t)best * s->nl, sizeof(double), cudaMemcpyDeviceToHost));
+  if ((st = host_allreduce(c, u0))) return st;
+  const int flip = u0[0] >= 0.0 ? 1 : -1;
+  int64_t off = 0;
+  for (Shard *s : c->sh) {
+    std::vector<double> u((size_t)s->nl);
+    CK(cudaMemcpy(u.data(), s->U + (size_t)best * s->nl, sizeof(double) * s->nl, cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < s->nl; ++r) chi[off + r] = (int8_t)((u[(size_t)r] >= 0.0 ? 1 : -1) * flip);
+    off += s->nl;
+  }
   *cut_weight = w[best];
   return SCG_OK;
 }
@@ -1006,7 +1327,7 @@ int32_t sketchycgal_kernel_stats(scg_ctx *c, scg_kstat *out, int32_t max) {
     std::snprintf(out[cnt].name, sizeof(out[cnt].name), "%s", kKClassName[k]);
     out[cnt].launches = c->kl[k];
     out[cnt].total_ms = c->kms[k];
-    out[cnt].bytes_per_launch = c->kl[k] ? c->kbytes_sum[k] / (double)c->kl[k] : c->kbytes[k];
+    out[cnt].bytes_per_launch = c->kl[k] ? c->kbytes_sum[k] / (double)c->kl[k] : 0.0;
     ++cnt;
   }
   return cnt;

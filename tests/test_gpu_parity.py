@@ -177,3 +177,96 @@ def test_shared_divisor_division_is_ieee(gpu):
     """div_rn (RN(1/b) + two fma corrections) must equal the hardware division bit for bit."""
     for seed in (1, 2, 3):
         assert gpu.selftest_division(1 << 26, seed) == 0
+
+
+# ---------------------------------------------------------------- row-sharded path (DESIGN.md section 6)
+# P ranks emulated inside one context on one device: the same kernels, halo peer
+# stores and mailbox collectives as one process per GPU, checked bitwise against the
+# oracle (the exact sums make the iterates independent of P).
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_sharded_config0_trajectory_and_cut(gpu, P):
+    L = si.laplacian("c0")
+    T = 300
+    g = gpu.SketchyCGAL(L, R=10, seed=0, shards=P)
+    g.step(T)
+    o = oracle.Oracle(L, 10, seed=0, logcap=T)
+    o.step(T)
+    _assert_trajectory(g, o, T)
+    one = gpu.SketchyCGAL(L, R=10, seed=0)
+    one.step(T)
+    U1, lam1, _ = one.reconstruct()
+    U, lam, _ = g.reconstruct()
+    np.testing.assert_allclose(lam, lam1, rtol=1e-9)
+    np.testing.assert_allclose(g.objective(), one.objective(), rtol=1e-9)
+    np.testing.assert_allclose(g.feasibility(), one.feasibility(), rtol=1e-9)
+    chi, w = g.round()
+    chi1, w1 = one.round()
+    np.testing.assert_array_equal(chi, chi1)
+    assert abs(w - w1) <= 1e-9 * w1
+
+
+@pytest.mark.parametrize("regenerate", [False, True])
+def test_sharded_config1_signed_weights(gpu, regenerate):
+    L = si.laplacian("c1")
+    g = gpu.SketchyCGAL(L, R=10, seed=1, shards=4, regenerate=regenerate)
+    g.step(120)
+    o = oracle.Oracle(L, 10, seed=1, logcap=120)
+    o.step(120)
+    _assert_trajectory(g, o, 120)
+
+
+@pytest.mark.parametrize("regenerate", [False, True])
+def test_sharded_breakdown_complete_graph(gpu, regenerate):
+    """Lanczos break (k < q) with P = 2: producers and pulls must skip together."""
+    n = 8
+    i, j = np.triu_indices(n, 1)
+    L = si.laplacian_from_edges(n, i, j, np.ones(len(i)))
+    g = gpu.SketchyCGAL(L, R=3, seed=2, shards=2, regenerate=regenerate)
+    g.step(25)
+    o = oracle.Oracle(L, 3, seed=2, logcap=25)
+    o.step(25)
+    _assert_trajectory(g, o, 25)
+
+
+@pytest.mark.parametrize("n,P", [(3, 2), (33, 3), (257, 8), (1000, 5)])
+def test_sharded_ragged_sizes(gpu, n, P):
+    rng = np.random.default_rng(n)
+    i = np.arange(n - 1)
+    j = i + 1
+    extra = rng.integers(0, n, size=(2 * n, 2))
+    extra = extra[extra[:, 0] != extra[:, 1]]
+    i = np.concatenate([i, extra[:, 0]])
+    j = np.concatenate([j, extra[:, 1]])
+    w = rng.uniform(0.5, 1.5, size=len(i))
+    L = si.laplacian_from_edges(n, i, j, w)
+    R = min(4, n)
+    g = gpu.SketchyCGAL(L, R=R, seed=n, shards=P)
+    g.step(40)
+    o = oracle.Oracle(L, R, seed=n, logcap=40)
+    o.step(40)
+    _assert_trajectory(g, o, 40)
+
+
+def test_sharded_heavy_row_and_explicit_splits(gpu):
+    """A star centre (long row, warp engine) on the boundary between two uneven shards."""
+    n = 3000
+    i = np.zeros(n - 50, dtype=np.int64)
+    j = np.arange(1, n - 49)
+    L = si.laplacian_from_edges(n, i, j, np.ones(len(i)))
+    g = gpu.SketchyCGAL(L, R=5, seed=9, shards=3, splits=np.array([0, 1, 1700, n]))
+    g.step(30)
+    o = oracle.Oracle(L, 5, seed=9, logcap=30)
+    o.step(30)
+    _assert_trajectory(g, o, 30)
+
+
+@pytest.mark.parametrize("cfg,P,T", [("c2", 2, 2), ("c3", 2, 1)])
+def test_sharded_full_size_first_iterations(gpu, cfg, P, T):
+    L = si.laplacian(cfg)
+    c = si.CONFIGS[cfg]
+    g = gpu.SketchyCGAL(L, R=c["R"], seed=c["seed"], shards=P)
+    g.step(T)
+    o = oracle.Oracle(L, c["R"], seed=c["seed"], logcap=T)
+    o.step(T)
+    _assert_trajectory(g, o, T)
