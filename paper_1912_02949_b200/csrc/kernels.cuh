@@ -143,8 +143,8 @@ __device__ __forceinline__ double div_rn(double a, double b, double rb) {
 #ifndef SCG_CH
 #define SCG_CH 4
 #endif
-#ifndef SCG_TMA
-#define SCG_TMA 0  // TMA-staged SELL engine (experimental: slower than the register pipeline on c3)
+#ifndef SCG_ENGINE
+#define SCG_ENGINE 1  // short-row SpMV engine: 0 = SELL-32-sigma register pipeline, 1 = tile-staged CSR
 #endif
 #ifndef SCG_PIPE
 #define SCG_PIPE 1
@@ -172,6 +172,14 @@ struct Rows {
   // slices [wstart[w], wstart[w+1])
   const int *wstart;
   int nwin;
+  // tile-staged CSR layout of the short rows (SCG_ENGINE 1): trp[r] = offset of row r's
+  // entries in tcol/tval, bit 31 of trp[r+1] set iff row r is long (no entries here);
+  // tile k covers rows [tinfo[k].x, tinfo[k+1].x) and entries [tinfo[k].y, tinfo[k+1].y)
+  const unsigned *trp;
+  const int *tcol;      // column | 0x80000000 for a negative uniform value
+  const double *tval;   // values, or nullptr when all |C_rj| equal m0
+  const int2 *tinfo;
+  int ntiles;
 };
 
 constexpr int kWin = 1024;  // rows per window (= SELL sorting window sigma)
@@ -242,14 +250,7 @@ __device__ __forceinline__ void sell_fma_chunk(const Rows &RL, const int (&cc)[k
     }
 }
 
-// ---------------------------------------------------------------- TMA-staged SELL engine
-// A block walks windows of kWin consecutive rows.  For each window one thread
-// issues bulk asynchronous copies (cp.async.bulk, completion on an mbarrier) of
-// the window's SELL columns (+ values), slice-to-row map, diagonal(s) and own
-// entries of the gathered vector into a shared-memory stage; two stages, so the
-// next window streams in while this one is computed.  Threads then read their
-// row's slots from shared memory and issue only the random gathers x[col] to
-// global memory (two slices per warp, all gathers of a chunk in flight).
+// ---------------------------------------------------------------- TMA / mbarrier / cp.async helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -278,174 +279,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
-}
-
-template <int NC, bool UNI>
-struct TmaStage {
-  static constexpr int kCap = UNI ? 4096 : 2048;  // SELL slots per window
-  int cols[kCap];
-  double vals[UNI ? 2 : kCap];
-  int perm[kWin];
-  double d0[kWin];
-  double d1[NC > 1 ? kWin : 2];
-  double xo[kWin];
-};
-
-template <int NC, bool UNI>
-struct TmaSmem {
-  TmaStage<NC, UNI> st[2];
-  unsigned long long bar[2];
-};
-
-// Issue the copies of window `win` into `st` (thread 0 only).
-template <int NC, bool UNI>
-__device__ __forceinline__ void tma_issue(const Rows &RL, const double *X, const double *diag0,
-                                          const double *diag1, long long rb, int win, TmaStage<NC, UNI> &st,
-                                          unsigned long long *bar) {
-  const int s0 = __ldg(&RL.wstart[win]), s1 = __ldg(&RL.wstart[win + 1]);
-  const int nsl = s1 - s0;
-  int slots = 0, slot0 = 0;
-  if (nsl > 0) {
-    slot0 = __ldg(&RL.meta[s0].x);
-    const int2 ml = __ldg(&RL.meta[s1 - 1]);
-    slots = ml.x + 32 * ml.y - slot0;
-  }
-  if (nsl == 0 || slots > TmaStage<NC, UNI>::kCap) {  // empty or oversized: consumers read global memory
-    mbar_arrive(bar);
-    return;
-  }
-  const uint32_t rowb = (uint32_t)(kWin * sizeof(double));
-  uint32_t bytes = (uint32_t)slots * 4u + (uint32_t)nsl * 128u + 2u * rowb;
-  if (!UNI) bytes += (uint32_t)slots * 8u;
-  if (NC > 1) bytes += rowb;
-  mbar_arrive_tx(bar, bytes);
-  if (slots > 0) bulk_g2s(st.cols, RL.scol + slot0, (uint32_t)slots * 4u, bar);
-  if (!UNI && slots > 0) bulk_g2s(st.vals, RL.sval + slot0, (uint32_t)slots * 8u, bar);
-  bulk_g2s(st.perm, RL.perm + (long long)s0 * 32, (uint32_t)nsl * 128u, bar);
-  const long long r0 = (long long)win * kWin;
-  bulk_g2s(st.d0, diag0 + r0, rowb, bar);
-  if (NC > 1) bulk_g2s(st.d1, diag1 + r0, rowb, bar);
-  bulk_g2s(st.xo, X + rb + r0, rowb, bar);
-}
-
-// Up to kQ slices (sl0 + 8 q) of one warp, all gathers in flight together; the
-// pointers select shared (staged) or global data.
-template <int NC>
-struct QOf {
-  static constexpr int v = NC == 1 ? 4 : 2;
-};
-template <int NC, bool UNI, class Epi>
-__device__ __forceinline__ void tma_quad(const Rows &RL, const int *colp, const double *valp, int slot0,
-                                         const int *permp, int s0, const double *d0p, const double *d1p,
-                                         const double *xop, int r0, const double *__restrict__ X, double rden,
-                                         int sl0, int s1, int lane, Epi &epi) {
-  constexpr int kQ = QOf<NC>::v;
-  int rq[kQ];
-  int2 mq[kQ];
-  RowOut<NC> o[kQ];
-  int wmax = 0;
-#pragma unroll
-  for (int q = 0; q < kQ; ++q) {
-    const int sl = sl0 + 8 * q;
-    rq[q] = -1;
-    mq[q] = make_int2(0, 0);
-    if (sl < s1) {
-      rq[q] = permp[(sl - s0) * 32 + lane];
-      mq[q] = __ldg(&RL.meta[sl]);
-    }
-    wmax = mq[q].y > wmax ? mq[q].y : wmax;
-    o[q].r = rq[q];
-    const int rl = rq[q] - r0;
-    const double xv = rq[q] >= 0 ? xop[rl] : 0.0;
-    o[q].xr = xv * rden;
-    o[q].s[0] = (rq[q] >= 0 ? d0p[rl] : 0.0) * o[q].xr;
-    if (NC > 1) o[q].s[NC - 1] = (rq[q] >= 0 ? d1p[rl] : 0.0) * o[q].xr;
-  }
-  for (int j0 = 0; j0 < wmax; j0 += kChunk) {
-    // phase 1: all gathers of this chunk for the kQ slices (columns read from shared memory)
-    double gq[kQ][kChunk];
-#pragma unroll
-    for (int q = 0; q < kQ; ++q)
-#pragma unroll
-      for (int u = 0; u < kChunk; ++u)
-        if (j0 + u < mq[q].y) {
-          const int c = colp[mq[q].x - slot0 + (j0 + u) * 32 + lane];
-          if (c != -1) gq[q][u] = __ldg(&X[c & 0x7fffffff]);
-        }
-    // phase 2: the CAC-3 chains (columns re-read from shared memory)
-#pragma unroll
-    for (int q = 0; q < kQ; ++q)
-#pragma unroll
-      for (int u = 0; u < kChunk; ++u)
-        if (j0 + u < mq[q].y) {
-          const int e = mq[q].x - slot0 + (j0 + u) * 32 + lane;
-          const int c = colp[e];
-          if (c != -1) {
-            const double m = UNI ? (c < 0 ? -RL.m0 : RL.m0) : valp[e];
-            const double x = gq[q][u] * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
-#pragma unroll
-            for (int cc = 0; cc < NC; ++cc) o[q].s[cc] = fma(m, x, o[q].s[cc]);
-          }
-        }
-  }
-#pragma unroll
-  for (int q = 0; q < kQ; ++q)
-    if (rq[q] >= 0) epi(o[q]);
-}
-
-template <int NC, bool UNI, class Epi>
-__device__ __forceinline__ void spmv_tma(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
-                                         const double *__restrict__ diag0, const double *__restrict__ diag1,
-                                         long long rb, Epi &epi, TmaSmem<NC, UNI> &sm) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    mbar_init(&sm.bar[0], 1);
-    mbar_init(&sm.bar[1], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if ((int)blockIdx.x < RL.nwin) tma_issue<NC, UNI>(RL, X, diag0, diag1, rb, blockIdx.x, sm.st[0], &sm.bar[0]);
-    if ((int)(blockIdx.x + gridDim.x) < RL.nwin)
-      tma_issue<NC, UNI>(RL, X, diag0, diag1, rb, blockIdx.x + gridDim.x, sm.st[1], &sm.bar[1]);
-  }
-  // long rows first (warp per row), overlapping the first copies
-  {
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwg = (gridDim.x * blockDim.x) >> 5;
-    for (int w = gw; w < RL.nlong; w += nwg) {
-      RowOut<NC> o;
-      long_row_chain<NC>(C, RL.longrows[w], X, den, diag0, diag1, rb, o);
-      if (lane == 0) epi(o);
-    }
-  }
-  const double rden = 1.0 / den;
-  int it = 0;
-  for (int win = blockIdx.x; win < RL.nwin; win += gridDim.x, ++it) {
-    const int stg = it & 1;
-    mbar_wait(&sm.bar[stg], (uint32_t)((it >> 1) & 1));
-    TmaStage<NC, UNI> &st = sm.st[stg];
-    const int s0 = __ldg(&RL.wstart[win]), s1 = __ldg(&RL.wstart[win + 1]);
-    const int nsl = s1 - s0;
-    if (nsl > 0) {
-      const int slot0 = __ldg(&RL.meta[s0].x);
-      const int2 ml = __ldg(&RL.meta[s1 - 1]);
-      const bool big = ml.x + 32 * ml.y - slot0 > TmaStage<NC, UNI>::kCap;
-      const int r0 = win * kWin;
-      for (int b = warp; b < nsl; b += 8 * QOf<NC>::v) {
-        if (!big)
-          tma_quad<NC, UNI>(RL, st.cols, st.vals, slot0, st.perm, s0, st.d0, st.d1, st.xo, r0, X, rden, s0 + b, s1,
-                            lane, epi);
-        else
-          tma_quad<NC, UNI>(RL, RL.scol + slot0, RL.sval ? RL.sval + slot0 : nullptr, slot0,
-                            RL.perm + (long long)s0 * 32, s0, diag0 + r0, diag1 ? diag1 + r0 : nullptr,
-                            X + rb + r0, r0, X, rden, s0 + b, s1, lane, epi);
-      }
-    }
-    __syncthreads();  // stage fully consumed
-    if (threadIdx.x == 0 && win + 2 * (int)gridDim.x < RL.nwin)
-      tma_issue<NC, UNI>(RL, X, diag0, diag1, rb, win + 2 * gridDim.x, st, &sm.bar[stg]);
-  }
 }
 
 // Visit every row of this rank once: epi(RowOut) is called by the owning thread
@@ -573,6 +406,166 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
   }
 #endif
   (void)nl;
+}
+
+
+// ---------------------------------------------------------------- tile-staged CSR engine (SCG_ENGINE 1)
+// The short rows are cut into tiles of <= kTR consecutive rows and <= TileCap entries
+// (host-built).  A block walks its tiles (k = blockIdx.x + j gridDim.x) through a
+// three-stage pipeline held entirely in shared memory, so in-flight loads cost no
+// registers:
+//   stage S (tile j+2): one thread issues TMA bulk copies (cp.async.bulk, mbarrier
+//     completion) of the tile's contiguous structure: row offsets, columns (+ values),
+//     the own entries of the gathered vector and the diagonal(s);
+//   stage G (tile j+1): every thread issues cp.async (LDGSTS) gathers X[col] of a
+//     strided share of the tile's entries into shared memory;
+//   stage C (tile j): thread-per-row CAC-3 chains from shared memory, then the epilogue.
+// Long rows (> kLongRow entries) are done first by warps of the grid (warp per row).
+constexpr int kTR = 256;  // rows per tile = threads per block of the tile engine
+template <bool UNI>
+struct TileCap {
+  static constexpr int v = UNI ? 2048 : 1024;
+};
+
+template <int NC, bool UNI>
+struct __align__(16) TileBuf {
+  unsigned rp[kTR + 8];
+  int col[TileCap<UNI>::v + 8];
+  double val[UNI ? 2 : TileCap<UNI>::v + 4];
+  double xo[kTR + 4];
+  double d0[kTR + 4];
+  double d1[NC > 1 ? kTR + 4 : 2];
+};
+
+template <int NC, bool UNI>
+struct __align__(16) TileSmem {
+  TileBuf<NC, UNI> sb[3];
+  double gx[2][TileCap<UNI>::v];
+  unsigned long long bar[3];
+};
+
+__device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Elements [i0, i1) of a global array (element size es) are copied as the 16-byte
+// aligned byte range around them; sdst then holds the array from the aligned element
+// at or below i0 (seg_shift elements before i0).  Arrays carry >= 16 bytes of slack.
+__device__ __forceinline__ uint32_t seg_bytes(int es, long long i0, long long i1) {
+  if (i1 <= i0) return 0u;
+  return (uint32_t)((((i1 * es) + 15) & ~15ll) - ((i0 * es) & ~15ll));
+}
+__device__ __forceinline__ void bulk_seg(void *sdst, const void *gbase, int es, long long i0, long long i1,
+                                         unsigned long long *bar) {
+  if (i1 <= i0) return;
+  bulk_g2s(sdst, (const char *)gbase + ((i0 * es) & ~15ll), seg_bytes(es, i0, i1), bar);
+}
+__device__ __forceinline__ int seg_shift(long long i0, int es) { return (int)(((i0 * es) & 15ll) / es); }
+
+template <int NC, bool UNI>
+__device__ __forceinline__ void tile_issue(const Rows &RL, const double *X, const double *diag0, const double *diag1,
+                                           long long rb, int k, TileBuf<NC, UNI> &b, unsigned long long *bar) {
+  const int2 t0 = __ldg(&RL.tinfo[k]), t1 = __ldg(&RL.tinfo[k + 1]);
+  uint32_t bytes = seg_bytes(4, t0.x, t1.x + 1) + seg_bytes(4, t0.y, t1.y) + seg_bytes(8, rb + t0.x, rb + t1.x) +
+                   seg_bytes(8, t0.x, t1.x);
+  if (!UNI) bytes += seg_bytes(8, t0.y, t1.y);
+  if (NC > 1) bytes += seg_bytes(8, t0.x, t1.x);
+  mbar_arrive_tx(bar, bytes);
+  bulk_seg(b.rp, RL.trp, 4, t0.x, t1.x + 1, bar);
+  bulk_seg(b.col, RL.tcol, 4, t0.y, t1.y, bar);
+  if (!UNI) bulk_seg(b.val, RL.tval, 8, t0.y, t1.y, bar);
+  bulk_seg(b.xo, X, 8, rb + t0.x, rb + t1.x, bar);
+  bulk_seg(b.d0, diag0, 8, t0.x, t1.x, bar);
+  if (NC > 1) bulk_seg(b.d1, diag1, 8, t0.x, t1.x, bar);
+}
+
+template <int NC, bool UNI>
+__device__ __forceinline__ void tile_gather(const Rows &RL, const double *__restrict__ X, int k,
+                                            const TileBuf<NC, UNI> &b, double *gx) {
+  const int2 t0 = __ldg(&RL.tinfo[k]), t1 = __ldg(&RL.tinfo[k + 1]);
+  const int ne = t1.y - t0.y, sh = seg_shift(t0.y, 4);
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+    const int c = b.col[sh + e] & 0x7fffffff;
+    cp_async8(gx + e, X + c);
+  }
+}
+
+template <int NC, bool UNI, class Epi>
+__device__ __forceinline__ void tile_compute(const Rows &RL, int k, const TileBuf<NC, UNI> &b, const double *gx,
+                                             double rden, long long rb, Epi &epi) {
+  const int2 t0 = __ldg(&RL.tinfo[k]), t1 = __ldg(&RL.tinfo[k + 1]);
+  const int i = threadIdx.x;
+  if (i >= t1.x - t0.x) return;
+  const int shr = seg_shift(t0.x, 4), shc = seg_shift(t0.y, 4), shv = seg_shift(t0.y, 8);
+  const int shx = seg_shift(rb + t0.x, 8), shd = seg_shift(t0.x, 8);
+  const unsigned ra = b.rp[shr + i], rn = b.rp[shr + i + 1];
+  if (rn >> 31) return;  // long row: done by the warp engine
+  const int e0 = (int)(ra & 0x7fffffffu) - t0.y, e1 = (int)(rn & 0x7fffffffu) - t0.y;
+  RowOut<NC> o;
+  o.r = t0.x + i;
+  o.xr = b.xo[shx + i] * rden;
+  o.s[0] = b.d0[shd + i] * o.xr;
+  if (NC > 1) o.s[NC - 1] = b.d1[shd + i] * o.xr;
+  for (int e = e0; e < e1; ++e) {
+    const int c = b.col[shc + e];
+    const double m = UNI ? (c < 0 ? -RL.m0 : RL.m0) : b.val[shv + e];
+    const double x = gx[e] * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) o.s[cc] = fma(m, x, o.s[cc]);
+  }
+  epi(o);
+}
+
+template <int NC, bool UNI, class Epi>
+__device__ __forceinline__ void spmv_tiles(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
+                                           const double *__restrict__ diag0, const double *__restrict__ diag1,
+                                           long long rb, Epi &epi, TileSmem<NC, UNI> &sm) {
+  const int lane = threadIdx.x & 31;
+  const int J = RL.ntiles > (int)blockIdx.x ? (RL.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  auto tile = [&](int j) { return (int)blockIdx.x + j * (int)gridDim.x; };
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 3; ++q) mbar_init(&sm.bar[q], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (J > 0) tile_issue<NC, UNI>(RL, X, diag0, diag1, rb, tile(0), sm.sb[0], &sm.bar[0]);
+    if (J > 1) tile_issue<NC, UNI>(RL, X, diag0, diag1, rb, tile(1), sm.sb[1], &sm.bar[1]);
+  }
+  {  // long rows (warp per row) while the first tiles stream in
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwg = (gridDim.x * blockDim.x) >> 5;
+    for (int w = gw; w < RL.nlong; w += nwg) {
+      RowOut<NC> o;
+      long_row_chain<NC>(C, RL.longrows[w], X, den, diag0, diag1, rb, o);
+      if (lane == 0) epi(o);
+    }
+  }
+  const double rden = 1.0 / den;
+  if (J > 0) {
+    mbar_wait(&sm.bar[0], 0u);
+    tile_gather<NC, UNI>(RL, X, tile(0), sm.sb[0], sm.gx[0]);
+  }
+  cp_async_commit();
+  for (int j = 0; j < J; ++j) {
+    const int b = j % 3;
+    if (j + 1 < J) {  // stage G of tile j+1
+      const int b1 = (j + 1) % 3;
+      mbar_wait(&sm.bar[b1], (uint32_t)(((j + 1) / 3) & 1));
+      tile_gather<NC, UNI>(RL, X, tile(j + 1), sm.sb[b1], sm.gx[(j + 1) & 1]);
+    }
+    cp_async_commit();
+    if (threadIdx.x == 0 && j + 2 < J)  // stage S of tile j+2 (its buffer held tile j-1, released below)
+      tile_issue<NC, UNI>(RL, X, diag0, diag1, rb, tile(j + 2), sm.sb[(j + 2) % 3], &sm.bar[(j + 2) % 3]);
+    cp_async_wait<1>();  // this thread's gathers of tile j
+    __syncthreads();     // everyone's
+    tile_compute<NC, UNI>(RL, tile(j), sm.sb[b], sm.gx[j & 1], rden, rb, epi);
+    __syncthreads();  // buffers of tile j free
+  }
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------- block reduction
@@ -869,9 +862,9 @@ __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_a(Csr C,
   epi.blk = xb.l[0];
   xwin_init(epi.acc[0]);
   epi.err = 0;
-#if SCG_TMA
+#if SCG_ENGINE == 1
   extern __shared__ __align__(128) unsigned char smraw[];
-  spmv_tma<1, UNI>(C, RL, X, den, d, nullptr, rb, epi, *reinterpret_cast<TmaSmem<1, UNI> *>(smraw));
+  spmv_tiles<1, UNI>(C, RL, X, den, d, nullptr, rb, epi, *reinterpret_cast<TileSmem<1, UNI> *>(smraw));
 #else
   spmv_rows<1, UNI>(C, RL, X, den, d, nullptr, rb, nl, epi);
 #endif
@@ -1085,9 +1078,9 @@ __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_c(Csr C,
   if (j >= sc->k) return;  // sc->k holds the effective k after k_tridiag
   EpiC epi{Xjm1, Xjp1, x, rb, &net, j, sc->om[j - 1], sc->rho[j - 1], j >= 2 ? sc->rho[j - 2] : 1.0, sc->rho[j],
            sc->s[0], sc->s[j], 1.0 / sc->rho[j], 1.0 / (j >= 2 ? sc->rho[j - 2] : 1.0)};
-#if SCG_TMA
+#if SCG_ENGINE == 1
   extern __shared__ __align__(128) unsigned char smraw[];
-  spmv_tma<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, epi, *reinterpret_cast<TmaSmem<1, UNI> *>(smraw));
+  spmv_tiles<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, epi, *reinterpret_cast<TileSmem<1, UNI> *>(smraw));
 #else
   spmv_rows<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, nl, epi);
 #endif
@@ -1200,9 +1193,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
   xwin_init(epi.acc[1]);
   xwin_init(epi.acc[2]);
   epi.err = 0;
-#if SCG_TMA
+#if SCG_ENGINE == 1
   extern __shared__ __align__(128) unsigned char smraw[];
-  spmv_tma<2, UNI>(C, RL, x, nu, d, cdiag, rb, epi, *reinterpret_cast<TmaSmem<2, UNI> *>(smraw));
+  spmv_tiles<2, UNI>(C, RL, x, nu, d, cdiag, rb, epi, *reinterpret_cast<TileSmem<2, UNI> *>(smraw));
 #else
   spmv_rows<2, UNI>(C, RL, x, nu, d, cdiag, rb, nl, epi);
 #endif
@@ -1476,9 +1469,9 @@ __global__ void __launch_bounds__(kBlock) k_apply_d(Csr C, Rows RL, const double
                                                     const double *__restrict__ X, int nl, long long rb,
                                                     double *__restrict__ y) {
   EpiY epi{y};
-#if SCG_TMA
+#if SCG_ENGINE == 1
   extern __shared__ __align__(128) unsigned char smraw[];
-  spmv_tma<1, UNI>(C, RL, X, 1.0, d, nullptr, rb, epi, *reinterpret_cast<TmaSmem<1, UNI> *>(smraw));
+  spmv_tiles<1, UNI>(C, RL, X, 1.0, d, nullptr, rb, epi, *reinterpret_cast<TileSmem<1, UNI> *>(smraw));
 #else
   spmv_rows<1, UNI>(C, RL, X, 1.0, d, nullptr, rb, nl, epi);
 #endif

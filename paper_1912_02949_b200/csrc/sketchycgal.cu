@@ -76,6 +76,12 @@ struct Shard {
   bool sell_uniform = false;
   int nslice = 0, nwin = 0;
   int *sell_wstart = nullptr;
+  unsigned *trp = nullptr;  // tile-staged CSR (SCG_ENGINE 1)
+  int *tcol = nullptr;
+  double *tval = nullptr;
+  int2 *tinfo = nullptr;
+  int ntiles = 0;
+  size_t smem1 = 0, smem2 = 0;
   // sharding
   unsigned char *mask = nullptr;  // device [nl], nullptr when world == 1
   Mailbox *mb = nullptr;
@@ -219,6 +225,26 @@ void launch(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 block,
   launch_smem(c, cls, bytes, kern, grid, block, 0, args...);
 }
 
+Rows rows_of(const Shard *s) {
+  Rows r{};
+  r.longrows = s->longrows;
+  r.nlong = s->nlong;
+  r.perm = s->sell_perm;
+  r.meta = s->sell_meta;
+  r.scol = s->sell_col;
+  r.sval = s->sell_val;
+  r.m0 = s->sell_m0;
+  r.nslice = s->nslice;
+  r.wstart = s->sell_wstart;
+  r.nwin = s->nwin;
+  r.trp = s->trp;
+  r.tcol = s->tcol;
+  r.tval = s->tval;
+  r.tinfo = s->tinfo;
+  r.ntiles = s->ntiles;
+  return r;
+}
+
 Net net_of(const scg_ctx *c, const Shard *s, unsigned long long E) {
   Net n{};
   n.mask = c->world > 1 ? s->mask : nullptr;
@@ -264,7 +290,7 @@ void free_shard(Shard *s) {
   void *ptrs[] = {s->rp, s->col, s->val, s->wts, s->ldiag, s->cdiag, s->d, s->z, s->y, s->a, s->v, s->G,
                   s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
                   s->sc, s->slots, s->dlog, s->longrows, s->sell_perm, s->sell_col, s->sell_meta, s->sell_val,
-                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB};
+                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tinfo};
   for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -343,7 +369,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   s->nlong = (int)h_long.size();
 
   auto alloc = [&](void **p, size_t bytes) -> bool { return cudaMalloc(p, bytes ? bytes : 8) == cudaSuccess; };
-  s->nlpad = (nl + kWin - 1) / kWin * kWin;
+  s->nlpad = (nl + 4 + kWin - 1) / kWin * kWin;  // >= 16 bytes of slack for the bulk copies
   const size_t nlb = sizeof(double) * (size_t)s->nlpad;
   bool ok = alloc((void **)&s->rp, sizeof(int) * (nl + 1)) && alloc((void **)&s->col, sizeof(int) * cnt_off) &&
             alloc((void **)&s->val, sizeof(double) * cnt_off) && alloc((void **)&s->wts, sizeof(double) * cnt_off) &&
@@ -394,8 +420,10 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   return SCG_OK;
 }
 
-// SELL layout (needs ||L||_F for the values): rebuilt from the device CSR copy.
-scg_status build_sell(scg_ctx *c, Shard *s) {
+// Short-row layout of the SpMV engine (needs ||L||_F for the values), built on the host
+// from the device CSR copy: the tile-staged CSR (SCG_ENGINE 1) or SELL-32-sigma (0).
+// Values are scaled exactly as k_scale_c forms them (one IEEE division each).
+scg_status build_layout(scg_ctx *c, Shard *s) {
   const int64_t nl = s->nl;
   const bool scale = (c->flags & SCG_SCALE) != 0;
   std::vector<int> h_rp((size_t)nl + 1), h_col((size_t)s->nnz_off);
@@ -406,100 +434,149 @@ scg_status build_sell(scg_ctx *c, Shard *s) {
   CK(cudaMemcpyAsync(h_w.data(), s->wts, sizeof(double) * s->nnz_off, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const long long cnt_off = s->nnz_off;
-  const int kSigma = SCG_TMA ? kWin : 256;  // sorting window of SELL-32-sigma (= TMA staging window)
-  std::vector<int> wstart;
-  // uniform |w| is decided over ALL ranks' values (same layout decision everywhere is not
-  // required for correctness, only for the value encoding of this shard)
-  bool uni = cnt_off > 0;
+  bool uni = cnt_off > 0;  // all |w| equal: values are encoded in the column's sign bit
   const double w0 = cnt_off > 0 ? std::fabs(h_w[0]) : 0.0;
   for (int64_t k = 0; k < cnt_off && uni; ++k) uni = std::fabs(h_w[(size_t)k]) == w0;
   s->sell_m0 = scale ? w0 / c->nrmL : w0;  // |C_rj| = fl(|w| / ||L||_F)
-  std::vector<int> perm, scol, win;
-  std::vector<int2> meta;
-  std::vector<double> sval;
-  for (int64_t w = 0; w < nl; w += kSigma) {
-    wstart.push_back((int)meta.size());
-    win.clear();
-    for (int64_t r = w; r < std::min<int64_t>(nl, w + kSigma); ++r)
-      if (h_rp[(size_t)r + 1] - h_rp[(size_t)r] <= kLongRow) win.push_back((int)r);
-    std::stable_sort(win.begin(), win.end(), [&](int x, int y) {
-      return h_rp[(size_t)x + 1] - h_rp[(size_t)x] > h_rp[(size_t)y + 1] - h_rp[(size_t)y];
-    });
-    for (size_t s0 = 0; s0 < win.size(); s0 += 32) {
-      const int cnt = (int)std::min<size_t>(32, win.size() - s0);
-      const int width = h_rp[(size_t)win[s0] + 1] - h_rp[(size_t)win[s0]];
-      meta.push_back(make_int2((int)scol.size(), width));
-      for (int j = 0; j < width; ++j)
-        for (int l = 0; l < 32; ++l) {
-          int cc = -1;
-          double vv = 0.0;
-          if (l < cnt) {
-            const int r = win[s0 + l];
-            const int e = h_rp[(size_t)r] + j;
-            if (e < h_rp[(size_t)r + 1]) {
-              cc = h_col[(size_t)e];
-              const double wv = h_w[(size_t)e];
-              if (uni && wv < 0) cc = (int)((unsigned)cc | 0x80000000u);
-              vv = scale ? wv / c->nrmL : wv;  // = C_rj exactly as k_scale_c forms it
-            }
-          }
-          scol.push_back(cc);
-          if (!uni) sval.push_back(vv);
-        }
-      for (int l = 0; l < 32; ++l) perm.push_back(l < cnt ? win[s0 + l] : -1);
-    }
-    if (scol.size() >= (size_t)INT32_MAX) return fail(c, SCG_EINVAL, "SELL layout too large");
-  }
-  s->nslice = (int)meta.size();
-  wstart.push_back((int)meta.size());
-  s->nwin = (int)wstart.size() - 1;
-  auto alloc = [&](void **p, size_t bytes) -> bool { return cudaMalloc(p, bytes ? bytes : 8) == cudaSuccess; };
-  if (!alloc((void **)&s->sell_wstart, sizeof(int) * wstart.size()) ||
-      !alloc((void **)&s->sell_perm, sizeof(int) * perm.size()) ||
-      !alloc((void **)&s->sell_meta, sizeof(int2) * meta.size()) ||
-      !alloc((void **)&s->sell_col, sizeof(int) * scol.size()) ||
-      (!uni && !alloc((void **)&s->sell_val, sizeof(double) * sval.size())))
-    return fail(c, SCG_ENOMEM, "SELL layout");
-  CK(cudaMemcpyAsync(s->sell_wstart, wstart.data(), sizeof(int) * wstart.size(), cudaMemcpyHostToDevice, st));
-  if (!perm.empty()) CK(cudaMemcpyAsync(s->sell_perm, perm.data(), sizeof(int) * perm.size(), cudaMemcpyHostToDevice, st));
-  if (!meta.empty()) CK(cudaMemcpyAsync(s->sell_meta, meta.data(), sizeof(int2) * meta.size(), cudaMemcpyHostToDevice, st));
-  if (!scol.empty()) CK(cudaMemcpyAsync(s->sell_col, scol.data(), sizeof(int) * scol.size(), cudaMemcpyHostToDevice, st));
-  if (!uni && !sval.empty())
-    CK(cudaMemcpyAsync(s->sell_val, sval.data(), sizeof(double) * sval.size(), cudaMemcpyHostToDevice, st));
-  CK(cudaStreamSynchronize(st));
-  s->sell_slots = (double)scol.size();
   s->sell_uniform = uni;
+  auto alloc = [&](void **p, size_t bytes) -> bool { return cudaMalloc(p, bytes ? bytes : 8) == cudaSuccess; };
+  auto enc = [&](int64_t e) {
+    int cc = h_col[(size_t)e];
+    if (uni && h_w[(size_t)e] < 0) cc = (int)((unsigned)cc | 0x80000000u);
+    return cc;
+  };
+  auto valof = [&](int64_t e) { return scale ? h_w[(size_t)e] / c->nrmL : h_w[(size_t)e]; };
+  double matbytes = 0.0;
+#if SCG_ENGINE == 1
+  {
+    const int cap = uni ? TileCap<true>::v : TileCap<false>::v;
+    std::vector<unsigned> trp((size_t)nl + 1 + 4, 0u);
+    std::vector<int> tcol;
+    std::vector<double> tval;
+    std::vector<int2> tinfo;
+    int rows_in = 0, nnz_in = 0;
+    for (int64_t r = 0; r < nl; ++r) {
+      const int len = h_rp[(size_t)r + 1] - h_rp[(size_t)r];
+      const bool lng = len > kLongRow;
+      const int add = lng ? 0 : len;
+      if (r == 0 || rows_in == kTR || nnz_in + add > cap) {
+        tinfo.push_back(make_int2((int)r, (int)tcol.size()));
+        rows_in = 0;
+        nnz_in = 0;
+      }
+      trp[(size_t)r] |= (unsigned)tcol.size();
+      if (!lng)
+        for (int e = h_rp[(size_t)r]; e < h_rp[(size_t)r + 1]; ++e) {
+          tcol.push_back(enc(e));
+          if (!uni) tval.push_back(valof(e));
+        }
+      trp[(size_t)r + 1] = (unsigned)tcol.size() | (lng ? 0x80000000u : 0u);
+      ++rows_in;
+      nnz_in += add;
+    }
+    if (tcol.size() >= (size_t)INT32_MAX) return fail(c, SCG_EINVAL, "tile layout too large");
+    tinfo.push_back(make_int2((int)nl, (int)tcol.size()));
+    s->ntiles = (int)tinfo.size() - 1;
+    const size_t nnz_s = tcol.size();
+    tcol.resize(nnz_s + 4, 0);
+    if (!uni) tval.resize(nnz_s + 2, 0.0);
+    if (!alloc((void **)&s->trp, sizeof(unsigned) * trp.size()) || !alloc((void **)&s->tcol, sizeof(int) * tcol.size()) ||
+        !alloc((void **)&s->tinfo, sizeof(int2) * tinfo.size()) ||
+        (!uni && !alloc((void **)&s->tval, sizeof(double) * tval.size())))
+      return fail(c, SCG_ENOMEM, "tile layout");
+    CK(cudaMemcpyAsync(s->trp, trp.data(), sizeof(unsigned) * trp.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->tcol, tcol.data(), sizeof(int) * tcol.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->tinfo, tinfo.data(), sizeof(int2) * tinfo.size(), cudaMemcpyHostToDevice, st));
+    if (!uni) CK(cudaMemcpyAsync(s->tval, tval.data(), sizeof(double) * tval.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    long long nnz_long = (long long)cnt_off - (long long)nnz_s;
+    matbytes = 4.0 * (double)(nl + 1) + (double)nnz_s * (uni ? 4.0 : 12.0) + 8.0 * s->ntiles +
+               12.0 * (double)nnz_long + 8.0 * s->nlong;
+    s->smem1 = uni ? sizeof(TileSmem<1, true>) : sizeof(TileSmem<1, false>);
+    s->smem2 = uni ? sizeof(TileSmem<2, true>) : sizeof(TileSmem<2, false>);
+  }
+#else
+  {
+    const int kSigma = 256;  // sorting window of SELL-32-sigma
+    std::vector<int> wstart, perm, scol, win;
+    std::vector<int2> meta;
+    std::vector<double> sval;
+    for (int64_t w = 0; w < nl; w += kSigma) {
+      wstart.push_back((int)meta.size());
+      win.clear();
+      for (int64_t r = w; r < std::min<int64_t>(nl, w + kSigma); ++r)
+        if (h_rp[(size_t)r + 1] - h_rp[(size_t)r] <= kLongRow) win.push_back((int)r);
+      std::stable_sort(win.begin(), win.end(), [&](int x, int y) {
+        return h_rp[(size_t)x + 1] - h_rp[(size_t)x] > h_rp[(size_t)y + 1] - h_rp[(size_t)y];
+      });
+      for (size_t s0 = 0; s0 < win.size(); s0 += 32) {
+        const int cnt = (int)std::min<size_t>(32, win.size() - s0);
+        const int width = h_rp[(size_t)win[s0] + 1] - h_rp[(size_t)win[s0]];
+        meta.push_back(make_int2((int)scol.size(), width));
+        for (int j = 0; j < width; ++j)
+          for (int l = 0; l < 32; ++l) {
+            int cc = -1;
+            double vv = 0.0;
+            if (l < cnt) {
+              const int r = win[s0 + l];
+              const int e = h_rp[(size_t)r] + j;
+              if (e < h_rp[(size_t)r + 1]) { cc = enc(e); vv = valof(e); }
+            }
+            scol.push_back(cc);
+            if (!uni) sval.push_back(vv);
+          }
+        for (int l = 0; l < 32; ++l) perm.push_back(l < cnt ? win[s0 + l] : -1);
+      }
+      if (scol.size() >= (size_t)INT32_MAX) return fail(c, SCG_EINVAL, "SELL layout too large");
+    }
+    s->nslice = (int)meta.size();
+    wstart.push_back((int)meta.size());
+    s->nwin = (int)wstart.size() - 1;
+    if (!alloc((void **)&s->sell_wstart, sizeof(int) * wstart.size()) ||
+        !alloc((void **)&s->sell_perm, sizeof(int) * perm.size()) ||
+        !alloc((void **)&s->sell_meta, sizeof(int2) * meta.size()) ||
+        !alloc((void **)&s->sell_col, sizeof(int) * scol.size()) ||
+        (!uni && !alloc((void **)&s->sell_val, sizeof(double) * sval.size())))
+      return fail(c, SCG_ENOMEM, "SELL layout");
+    CK(cudaMemcpyAsync(s->sell_wstart, wstart.data(), sizeof(int) * wstart.size(), cudaMemcpyHostToDevice, st));
+    if (!perm.empty()) CK(cudaMemcpyAsync(s->sell_perm, perm.data(), sizeof(int) * perm.size(), cudaMemcpyHostToDevice, st));
+    if (!meta.empty()) CK(cudaMemcpyAsync(s->sell_meta, meta.data(), sizeof(int2) * meta.size(), cudaMemcpyHostToDevice, st));
+    if (!scol.empty()) CK(cudaMemcpyAsync(s->sell_col, scol.data(), sizeof(int) * scol.size(), cudaMemcpyHostToDevice, st));
+    if (!uni && !sval.empty())
+      CK(cudaMemcpyAsync(s->sell_val, sval.data(), sizeof(double) * sval.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    s->sell_slots = (double)scol.size();
+    matbytes = s->sell_slots * (uni ? 4.0 : 12.0) + 4.0 * (double)nl + 8.0 * s->nslice;
+    s->smem1 = s->smem2 = 0;
+  }
+#endif
   {  // grids of the SpMV kernels
     const bool U = s->sell_uniform;
-    const size_t smem1 = !SCG_TMA ? 0 : (U ? sizeof(TmaSmem<1, true>) : sizeof(TmaSmem<1, false>));
-    const size_t smem2 = !SCG_TMA ? 0 : (U ? sizeof(TmaSmem<2, true>) : sizeof(TmaSmem<2, false>));
     auto setsm = [&](const void *k, size_t b) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b); };
-    int oa = 1, om = 1, oc = 1;
+    int oa = 1, om = 1;
     if (U) {
-      setsm((const void *)k_lanczos_a<true>, smem1);
-      setsm((const void *)k_lanczos_c<true>, smem1);
-      setsm((const void *)k_apply_d<true>, smem1);
-      setsm((const void *)k_monitor<true>, smem2);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<true>, kBlock, smem1);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_lanczos_c<true>, kBlock, smem1);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<true>, kBlock, smem2);
+      setsm((const void *)k_lanczos_a<true>, s->smem1);
+      setsm((const void *)k_lanczos_c<true>, s->smem1);
+      setsm((const void *)k_apply_d<true>, s->smem1);
+      setsm((const void *)k_monitor<true>, s->smem2);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<true>, kBlock, s->smem1);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<true>, kBlock, s->smem2);
     } else {
-      setsm((const void *)k_lanczos_a<false>, smem1);
-      setsm((const void *)k_lanczos_c<false>, smem1);
-      setsm((const void *)k_apply_d<false>, smem1);
-      setsm((const void *)k_monitor<false>, smem2);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<false>, kBlock, smem1);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_lanczos_c<false>, kBlock, smem1);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<false>, kBlock, smem2);
+      setsm((const void *)k_lanczos_a<false>, s->smem1);
+      setsm((const void *)k_lanczos_c<false>, s->smem1);
+      setsm((const void *)k_apply_d<false>, s->smem1);
+      setsm((const void *)k_monitor<false>, s->smem2);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<false>, kBlock, s->smem1);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<false>, kBlock, s->smem2);
     }
-    const int need = SCG_TMA ? std::max(s->nwin, (s->nlong + 7) / 8)
-                             : (int)std::max<int64_t>((s->nslice + 7) / 8, (s->nlong + 7) / 8);
+    const int need = SCG_ENGINE == 1 ? std::max(s->ntiles, (s->nlong + 7) / 8)
+                                     : (int)std::max<int64_t>((s->nslice + 7) / 8, (s->nlong + 7) / 8);
     s->grid_tiles = std::max(1, std::min(need, std::max(1, oa) * c->nsm));
     s->grid_mon = std::max(1, std::min(need, std::max(1, om) * c->nsm));
   }
   // algorithmic bytes per launch
   const double N = (double)c->n, NL = (double)nl;
-  const double mat = s->sell_slots * (s->sell_uniform ? 4.0 : 12.0) + 4.0 * NL + 8.0 * s->nslice;
+  const double mat = matbytes;
   const double gath = c->world > 1 ? NL + (double)s->halo_rows : N;  // gathered entries read once
   s->kb[KC_LANCZOS_A] = mat + 8.0 * NL + 8.0 * gath + 8.0 * NL;
   s->kb[KC_LANCZOS_B] = 32.0 * NL;
@@ -731,7 +808,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   c->b = scale ? 1.0 / (double)n : 1.0;
   c->lnN = std::log((double)n);
   c->log_cap = 1024;
-  c->npad = (n + kWin - 1) / kWin * kWin;
+  c->npad = (n + 4 + kWin - 1) / kWin * kWin;  // >= 16 bytes of slack for the bulk copies
 
   // ---- sharding mode and row splits
   int world = 1, emulate = 0, rank = 0;
@@ -826,7 +903,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   c->nrmL = std::sqrt(c->nrmL);
   if (!(c->nrmL > 0) || !std::isfinite(c->nrmL)) return bad(SCG_EINVAL);
   for (Shard *s : c->sh) {
-    if ((st = build_sell(c, s))) return bad(st);
+    if ((st = build_layout(c, s))) return bad(st);
     if (cudaMemcpyAsync(s->dscalar, &c->nrmL, sizeof(double), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
       return bad(SCG_ECUDA);
     const int gnnz = (int)std::min<long long>(std::max<long long>(1, (s->nnz_off + kBlock - 1) / kBlock), 8 * c->nsm);
@@ -906,10 +983,9 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       unsigned long long E = ++c->epoch;
       for (Shard *s : c->sh) {
         Csr C{s->rp, s->col, s->val};
-        Rows TT{s->longrows, s->nlong, s->sell_perm, s->sell_meta, s->sell_col, s->sell_val, s->sell_m0, s->nslice,
-                s->sell_wstart, s->nwin};
+        Rows TT = rows_of(s);
         auto kA = s->sell_uniform ? k_lanczos_a<true> : k_lanczos_a<false>;
-        launch(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->grid_tiles), dim3(kBlock), C, TT,
+        launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->grid_tiles), dim3(kBlock), s->smem1, C, TT,
                (const double *)s->d, (const double *)slot(s, i), (int)s->nl, (long long)s->rb, i, s->a,
                s->slots + SLOT_OM, s->sc, net_of(c, s, E));
       }
@@ -941,11 +1017,10 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
         const unsigned long long E = ++c->epoch;
         for (Shard *s : c->sh) {
           Csr C{s->rp, s->col, s->val};
-          Rows TT{s->longrows, s->nlong, s->sell_perm, s->sell_meta, s->sell_col, s->sell_val, s->sell_m0, s->nslice,
-                  s->sell_wstart, s->nwin};
+          Rows TT = rows_of(s);
           auto kC = s->sell_uniform ? k_lanczos_c<true> : k_lanczos_c<false>;
           const double *Xjm1 = (j == 1) ? nullptr : slot(s, j - 1);
-          launch(c, KC_LANCZOS_C, s->kb[KC_LANCZOS_C], kC, dim3(s->grid_tiles), dim3(kBlock), C, TT,
+          launch_smem(c, KC_LANCZOS_C, s->kb[KC_LANCZOS_C], kC, dim3(s->grid_tiles), dim3(kBlock), s->smem1, C, TT,
                  (const double *)s->d, (const double *)slot(s, j), Xjm1, slot(s, j + 1), c->xg(s), (int)s->nl,
                  (long long)s->rb, j, s->sc, s->slots + SLOT_BAR, net_of(c, s, E));
         }
@@ -964,10 +1039,9 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     unsigned long long E = ++c->epoch;
     for (Shard *s : c->sh) {
       Csr C{s->rp, s->col, s->val};
-      Rows TT{s->longrows, s->nlong, s->sell_perm, s->sell_meta, s->sell_col, s->sell_val, s->sell_m0, s->nslice,
-              s->sell_wstart, s->nwin};
+      Rows TT = rows_of(s);
       auto kM = s->sell_uniform ? k_monitor<true> : k_monitor<false>;
-      launch(c, KC_MONITOR, s->kb[KC_MONITOR], kM, dim3(s->grid_mon), dim3(kBlock), C, TT, (const double *)s->d,
+      launch_smem(c, KC_MONITOR, s->kb[KC_MONITOR], kM, dim3(s->grid_mon), dim3(kBlock), s->smem2, C, TT, (const double *)s->d,
              (const double *)s->cdiag, (const double *)c->xg(s), s->v, (int)s->nl, (long long)s->rb,
              s->slots + SLOT_MON, s->sc, net_of(c, s, E));
     }
@@ -1058,9 +1132,8 @@ scg_status sketchycgal_apply_D(scg_ctx *c, const double *xh, double *yh) {
   for (Shard *s : c->sh) {
     CK(cudaMalloc(&dy, sizeof(double) * std::max<int64_t>(1, s->nl)));
     Csr C{s->rp, s->col, s->val};
-    Rows TT{s->longrows, s->nlong, s->sell_perm, s->sell_meta, s->sell_col, s->sell_val, s->sell_m0, s->nslice,
-            s->sell_wstart, s->nwin};
-    launch(c, KC_OTHER, 0.0, s->sell_uniform ? k_apply_d<true> : k_apply_d<false>, dim3(s->grid_tiles), dim3(kBlock),
+    Rows TT = rows_of(s);
+    launch_smem(c, KC_OTHER, 0.0, s->sell_uniform ? k_apply_d<true> : k_apply_d<false>, dim3(s->grid_tiles), dim3(kBlock), s->smem1,
            C, TT, (const double *)s->d, (const double *)dx, (int)s->nl, (long long)s->rb, dy);
     CK(cudaStreamSynchronize(c->stream));
     CK(cudaMemcpy(yh + off, dy, sizeof(double) * s->nl, cudaMemcpyDeviceToHost));
