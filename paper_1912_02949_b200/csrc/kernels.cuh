@@ -173,12 +173,12 @@ struct Rows {
   const int *wstart;
   int nwin;
   // tile-staged CSR layout of the short rows (SCG_ENGINE 1): trp[r] = offset of row r's
-  // entries in tcol/tval, bit 31 of trp[r+1] set iff row r is long (no entries here);
-  // tile k covers rows [tinfo[k].x, tinfo[k+1].x) and entries [tinfo[k].y, tinfo[k+1].y)
+  // entries in tcol/tval, bit 31 of trp[r+1] set iff row r is long (no entries here)
   const unsigned *trp;
-  const int *tcol;      // column | 0x80000000 for a negative uniform value
+  const int *tcol;      // entry code (see the tile engine below)
   const double *tval;   // values, or nullptr when all |C_rj| equal m0
-  const int2 *tinfo;
+  const int *tout;      // out-of-window columns of every tile
+  const struct TileDesc *tdesc;
   int ntiles;
 };
 
@@ -410,21 +410,40 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
 
 
 // ---------------------------------------------------------------- tile-staged CSR engine (SCG_ENGINE 1)
-// The short rows are cut into tiles of <= kTR consecutive rows and <= TileCap entries
-// (host-built).  A block walks its tiles (k = blockIdx.x + j gridDim.x) through a
-// three-stage pipeline held entirely in shared memory, so in-flight loads cost no
-// registers:
-//   stage S (tile j+2): one thread issues TMA bulk copies (cp.async.bulk, mbarrier
-//     completion) of the tile's contiguous structure: row offsets, columns (+ values),
-//     the own entries of the gathered vector and the diagonal(s);
-//   stage G (tile j+1): every thread issues cp.async (LDGSTS) gathers X[col] of a
-//     strided share of the tile's entries into shared memory;
+// The short rows are cut (on the host) into tiles of <= kTR consecutive rows.  Each
+// tile has an index WINDOW [wlo, whi) of the gathered vector that contains its own
+// rows and, for graphs with locality (Morton-ordered geometric graphs, tori, rings),
+// most of its columns.  Entry encoding (tcol): bit 31 = sign of a uniform value;
+// bit 30 clear: bits 0..29 = column - wlo (read from the staged window); bit 30 set:
+// bits 0..29 = index into the tile's out-of-window list (tout, absolute columns).
+// A block walks its tiles (k = blockIdx.x + j gridDim.x) through a kNS-stage
+// shared-memory pipeline, so in-flight loads cost no registers:
+//   stage S (tile j+kNS-1): one thread issues TMA bulk copies (cp.async.bulk,
+//     mbarrier completion) of the tile's row offsets, entries (+ values), out list,
+//     window of the gathered vector and diagonal(s) -- all contiguous;
+//   stage G (tile j+kNS-2): cp.async (LDGSTS) gathers of the out-of-window entries;
 //   stage C (tile j): thread-per-row CAC-3 chains from shared memory, then the epilogue.
 // Long rows (> kLongRow entries) are done first by warps of the grid (warp per row).
 constexpr int kTR = 256;  // rows per tile = threads per block of the tile engine
+#ifndef SCG_NS
+#define SCG_NS 3
+#endif
+constexpr int kNS = SCG_NS;  // >= 2: structure leads by kNS-1 tiles, gathers by kNS-2
+static_assert(kNS >= 2, "tile pipeline needs two stages");
+#ifndef SCG_HALO
+#define SCG_HALO 256
+#endif
+constexpr int kH = SCG_HALO;                    // window reach beyond the tile's rows (host side)
+constexpr int kWinCap = kTR + 2 * kH;           // window elements
+constexpr int kOutCap = 512;                    // out-of-window entries per tile
 template <bool UNI>
 struct TileCap {
-  static constexpr int v = UNI ? 2048 : 1024;
+  static constexpr int v = UNI ? 1024 : 768;
+};
+
+struct TileDesc {  // host-built, one per tile
+  int r0, r1, e0, e1;   // rows [r0, r1) (local), entries [e0, e1)
+  int o0, o1, wlo, whi; // out list [o0, o1); window [wlo, whi) of GLOBAL indices
 };
 
 template <int NC, bool UNI>
@@ -432,16 +451,20 @@ struct __align__(16) TileBuf {
   unsigned rp[kTR + 8];
   int col[TileCap<UNI>::v + 8];
   double val[UNI ? 2 : TileCap<UNI>::v + 4];
-  double xo[kTR + 4];
+  int out[kOutCap + 8];
+  double win[kWinCap + 4];
   double d0[kTR + 4];
   double d1[NC > 1 ? kTR + 4 : 2];
+  double gx[kOutCap];
 };
+
+constexpr int kTLCap = 96;  // tile descriptors of one block held in shared memory
 
 template <int NC, bool UNI>
 struct __align__(16) TileSmem {
-  TileBuf<NC, UNI> sb[3];
-  double gx[2][TileCap<UNI>::v];
-  unsigned long long bar[3];
+  TileBuf<NC, UNI> sb[kNS];
+  TileDesc tl[kTLCap];
+  unsigned long long bar[kNS];
 };
 
 __device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
@@ -451,68 +474,71 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Elements [i0, i1) of a global array (element size es) are copied as the 16-byte
+// Elements [i0, i1) of a global array (element size ES) are copied as the 16-byte
 // aligned byte range around them; sdst then holds the array from the aligned element
 // at or below i0 (seg_shift elements before i0).  Arrays carry >= 16 bytes of slack.
-__device__ __forceinline__ uint32_t seg_bytes(int es, long long i0, long long i1) {
+template <int ES>
+__device__ __forceinline__ uint32_t seg_bytes(long long i0, long long i1) {
   if (i1 <= i0) return 0u;
-  return (uint32_t)((((i1 * es) + 15) & ~15ll) - ((i0 * es) & ~15ll));
+  return (uint32_t)((((i1 * ES) + 15) & ~15ll) - ((i0 * ES) & ~15ll));
 }
-__device__ __forceinline__ void bulk_seg(void *sdst, const void *gbase, int es, long long i0, long long i1,
+template <int ES>
+__device__ __forceinline__ void bulk_seg(void *sdst, const void *gbase, long long i0, long long i1,
                                          unsigned long long *bar) {
   if (i1 <= i0) return;
-  bulk_g2s(sdst, (const char *)gbase + ((i0 * es) & ~15ll), seg_bytes(es, i0, i1), bar);
+  bulk_g2s(sdst, (const char *)gbase + ((i0 * ES) & ~15ll), seg_bytes<ES>(i0, i1), bar);
 }
-__device__ __forceinline__ int seg_shift(long long i0, int es) { return (int)(((i0 * es) & 15ll) / es); }
+template <int ES>
+__device__ __forceinline__ int seg_shift(long long i0) { return (int)(((i0 * ES) & 15ll) / ES); }
 
 template <int NC, bool UNI>
 __device__ __forceinline__ void tile_issue(const Rows &RL, const double *X, const double *diag0, const double *diag1,
-                                           long long rb, int k, TileBuf<NC, UNI> &b, unsigned long long *bar) {
-  const int2 t0 = __ldg(&RL.tinfo[k]), t1 = __ldg(&RL.tinfo[k + 1]);
-  uint32_t bytes = seg_bytes(4, t0.x, t1.x + 1) + seg_bytes(4, t0.y, t1.y) + seg_bytes(8, rb + t0.x, rb + t1.x) +
-                   seg_bytes(8, t0.x, t1.x);
-  if (!UNI) bytes += seg_bytes(8, t0.y, t1.y);
-  if (NC > 1) bytes += seg_bytes(8, t0.x, t1.x);
+                                           const TileDesc &T, TileBuf<NC, UNI> &b, unsigned long long *bar) {
+  uint32_t bytes = seg_bytes<4>(T.r0, T.r1 + 1) + seg_bytes<4>(T.e0, T.e1) + seg_bytes<4>(T.o0, T.o1) +
+                   seg_bytes<8>(T.wlo, T.whi) + seg_bytes<8>(T.r0, T.r1);
+  if (!UNI) bytes += seg_bytes<8>(T.e0, T.e1);
+  if (NC > 1) bytes += seg_bytes<8>(T.r0, T.r1);
   mbar_arrive_tx(bar, bytes);
-  bulk_seg(b.rp, RL.trp, 4, t0.x, t1.x + 1, bar);
-  bulk_seg(b.col, RL.tcol, 4, t0.y, t1.y, bar);
-  if (!UNI) bulk_seg(b.val, RL.tval, 8, t0.y, t1.y, bar);
-  bulk_seg(b.xo, X, 8, rb + t0.x, rb + t1.x, bar);
-  bulk_seg(b.d0, diag0, 8, t0.x, t1.x, bar);
-  if (NC > 1) bulk_seg(b.d1, diag1, 8, t0.x, t1.x, bar);
+  bulk_seg<4>(b.rp, RL.trp, T.r0, T.r1 + 1, bar);
+  bulk_seg<4>(b.col, RL.tcol, T.e0, T.e1, bar);
+  if (!UNI) bulk_seg<8>(b.val, RL.tval, T.e0, T.e1, bar);
+  bulk_seg<4>(b.out, RL.tout, T.o0, T.o1, bar);
+  bulk_seg<8>(b.win, X, T.wlo, T.whi, bar);
+  bulk_seg<8>(b.d0, diag0, T.r0, T.r1, bar);
+  if (NC > 1) bulk_seg<8>(b.d1, diag1, T.r0, T.r1, bar);
 }
 
 template <int NC, bool UNI>
-__device__ __forceinline__ void tile_gather(const Rows &RL, const double *__restrict__ X, int k,
-                                            const TileBuf<NC, UNI> &b, double *gx) {
-  const int2 t0 = __ldg(&RL.tinfo[k]), t1 = __ldg(&RL.tinfo[k + 1]);
-  const int ne = t1.y - t0.y, sh = seg_shift(t0.y, 4);
-  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
-    const int c = b.col[sh + e] & 0x7fffffff;
-    cp_async8(gx + e, X + c);
-  }
+__device__ __forceinline__ void tile_gather(const double *__restrict__ X, const TileDesc &T, TileBuf<NC, UNI> &b) {
+  const int no = T.o1 - T.o0;
+  const int *op = b.out + seg_shift<4>(T.o0);
+  for (int k = threadIdx.x; k < no; k += kTR) cp_async8(b.gx + k, X + op[k]);
 }
 
 template <int NC, bool UNI, class Epi>
-__device__ __forceinline__ void tile_compute(const Rows &RL, int k, const TileBuf<NC, UNI> &b, const double *gx,
+__device__ __forceinline__ void tile_compute(const Rows &RL, const TileDesc &T, const TileBuf<NC, UNI> &b,
                                              double rden, long long rb, Epi &epi) {
-  const int2 t0 = __ldg(&RL.tinfo[k]), t1 = __ldg(&RL.tinfo[k + 1]);
   const int i = threadIdx.x;
-  if (i >= t1.x - t0.x) return;
-  const int shr = seg_shift(t0.x, 4), shc = seg_shift(t0.y, 4), shv = seg_shift(t0.y, 8);
-  const int shx = seg_shift(rb + t0.x, 8), shd = seg_shift(t0.x, 8);
+  if (i >= T.r1 - T.r0) return;
+  const int shr = seg_shift<4>(T.r0);
   const unsigned ra = b.rp[shr + i], rn = b.rp[shr + i + 1];
   if (rn >> 31) return;  // long row: done by the warp engine
-  const int e0 = (int)(ra & 0x7fffffffu) - t0.y, e1 = (int)(rn & 0x7fffffffu) - t0.y;
+  const int e0 = (int)(ra & 0x7fffffffu) - T.e0, e1 = (int)(rn & 0x7fffffffu) - T.e0;
+  const int *colp = b.col + seg_shift<4>(T.e0);
+  const double *valp = b.val + seg_shift<8>(T.e0);
+  const double *wp = b.win + seg_shift<8>(T.wlo);
   RowOut<NC> o;
-  o.r = t0.x + i;
-  o.xr = b.xo[shx + i] * rden;
+  o.r = T.r0 + i;
+  o.xr = wp[(int)(rb + T.r0 + i - T.wlo)] * rden;
+  const int shd = seg_shift<8>(T.r0);
   o.s[0] = b.d0[shd + i] * o.xr;
   if (NC > 1) o.s[NC - 1] = b.d1[shd + i] * o.xr;
   for (int e = e0; e < e1; ++e) {
-    const int c = b.col[shc + e];
-    const double m = UNI ? (c < 0 ? -RL.m0 : RL.m0) : b.val[shv + e];
-    const double x = gx[e] * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
+    const int c = colp[e];
+    const int idx = c & 0x3fffffff;
+    const double g = (c & 0x40000000) ? b.gx[idx] : wp[idx];
+    const double m = UNI ? (c < 0 ? -RL.m0 : RL.m0) : valp[e];
+    const double x = g * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc) o.s[cc] = fma(m, x, o.s[cc]);
   }
@@ -525,16 +551,19 @@ __device__ __forceinline__ void spmv_tiles(const Csr &C, const Rows &RL, const d
                                            long long rb, Epi &epi, TileSmem<NC, UNI> &sm) {
   const int lane = threadIdx.x & 31;
   const int J = RL.ntiles > (int)blockIdx.x ? (RL.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  auto tile = [&](int j) { return (int)blockIdx.x + j * (int)gridDim.x; };
+  // this block's tile descriptors (tiles blockIdx.x + j gridDim.x) into shared memory
+  for (int j = threadIdx.x; j < J && j < kTLCap; j += blockDim.x)
+    sm.tl[j] = RL.tdesc[(int)blockIdx.x + j * (int)gridDim.x];
+  auto desc = [&](int j) -> const TileDesc & {
+    return j < kTLCap ? sm.tl[j] : RL.tdesc[(int)blockIdx.x + j * (int)gridDim.x];
+  };
   if (threadIdx.x == 0) {
-    for (int q = 0; q < 3; ++q) mbar_init(&sm.bar[q], 1);
+    for (int q = 0; q < kNS; ++q) mbar_init(&sm.bar[q], 1);
     mbar_fence_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (J > 0) tile_issue<NC, UNI>(RL, X, diag0, diag1, rb, tile(0), sm.sb[0], &sm.bar[0]);
-    if (J > 1) tile_issue<NC, UNI>(RL, X, diag0, diag1, rb, tile(1), sm.sb[1], &sm.bar[1]);
-  }
+  if (threadIdx.x == 0)
+    for (int q = 0; q < kNS - 1 && q < J; ++q) tile_issue<NC, UNI>(RL, X, diag0, diag1, desc(q), sm.sb[q], &sm.bar[q]);
   {  // long rows (warp per row) while the first tiles stream in
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwg = (gridDim.x * blockDim.x) >> 5;
@@ -545,25 +574,28 @@ __device__ __forceinline__ void spmv_tiles(const Csr &C, const Rows &RL, const d
     }
   }
   const double rden = 1.0 / den;
-  if (J > 0) {
-    mbar_wait(&sm.bar[0], 0u);
-    tile_gather<NC, UNI>(RL, X, tile(0), sm.sb[0], sm.gx[0]);
-  }
-  cp_async_commit();
-  for (int j = 0; j < J; ++j) {
-    const int b = j % 3;
-    if (j + 1 < J) {  // stage G of tile j+1
-      const int b1 = (j + 1) % 3;
-      mbar_wait(&sm.bar[b1], (uint32_t)(((j + 1) / 3) & 1));
-      tile_gather<NC, UNI>(RL, X, tile(j + 1), sm.sb[b1], sm.gx[(j + 1) & 1]);
+  for (int q = 0; q < kNS - 2; ++q) {
+    if (q < J) {
+      mbar_wait(&sm.bar[q], 0u);
+      tile_gather<NC, UNI>(X, desc(q), sm.sb[q]);
     }
     cp_async_commit();
-    if (threadIdx.x == 0 && j + 2 < J)  // stage S of tile j+2 (its buffer held tile j-1, released below)
-      tile_issue<NC, UNI>(RL, X, diag0, diag1, rb, tile(j + 2), sm.sb[(j + 2) % 3], &sm.bar[(j + 2) % 3]);
-    cp_async_wait<1>();  // this thread's gathers of tile j
-    __syncthreads();     // everyone's
-    tile_compute<NC, UNI>(RL, tile(j), sm.sb[b], sm.gx[j & 1], rden, rb, epi);
-    __syncthreads();  // buffers of tile j free
+  }
+  for (int j = 0; j < J; ++j) {
+    if (threadIdx.x == 0 && j + kNS - 1 < J) {  // structure of tile j+kNS-1 (its slot held tile j-1)
+      const int q = (j + kNS - 1) % kNS;
+      tile_issue<NC, UNI>(RL, X, diag0, diag1, desc(j + kNS - 1), sm.sb[q], &sm.bar[q]);
+    }
+    if (j + kNS - 2 < J) {  // out-of-window gathers of tile j+kNS-2
+      const int q = (j + kNS - 2) % kNS;
+      mbar_wait(&sm.bar[q], (uint32_t)(((j + kNS - 2) / kNS) & 1));
+      tile_gather<NC, UNI>(X, desc(j + kNS - 2), sm.sb[q]);
+    }
+    cp_async_commit();
+    cp_async_wait<kNS - 2>();  // this thread's gathers of tile j
+    __syncthreads();           // everyone's
+    tile_compute<NC, UNI>(RL, desc(j), sm.sb[j % kNS], rden, rb, epi);
+    __syncthreads();  // slot of tile j free
   }
   cp_async_wait<0>();
 }

@@ -79,8 +79,10 @@ struct Shard {
   unsigned *trp = nullptr;  // tile-staged CSR (SCG_ENGINE 1)
   int *tcol = nullptr;
   double *tval = nullptr;
-  int2 *tinfo = nullptr;
-  int ntiles = 0;
+  int *tout = nullptr;
+  TileDesc *tdesc = nullptr;
+  int ntiles = 0, tile_h = 0;
+  long long tile_out = 0;
   size_t smem1 = 0, smem2 = 0;
   // sharding
   unsigned char *mask = nullptr;  // device [nl], nullptr when world == 1
@@ -240,7 +242,8 @@ Rows rows_of(const Shard *s) {
   r.trp = s->trp;
   r.tcol = s->tcol;
   r.tval = s->tval;
-  r.tinfo = s->tinfo;
+  r.tout = s->tout;
+  r.tdesc = s->tdesc;
   r.ntiles = s->ntiles;
   return r;
 }
@@ -290,7 +293,7 @@ void free_shard(Shard *s) {
   void *ptrs[] = {s->rp, s->col, s->val, s->wts, s->ldiag, s->cdiag, s->d, s->z, s->y, s->a, s->v, s->G,
                   s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
                   s->sc, s->slots, s->dlog, s->longrows, s->sell_perm, s->sell_col, s->sell_meta, s->sell_val,
-                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tinfo};
+                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tout, s->tdesc};
   for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -450,48 +453,90 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
 #if SCG_ENGINE == 1
   {
     const int cap = uni ? TileCap<true>::v : TileCap<false>::v;
+    const int64_t n = c->n, rb = s->rb;
+    // window reach: kH when it captures most columns (graphs with locality), else own rows only
+    auto in_win = [&](int64_t g0, int64_t h, int64_t col) { return col >= g0 - h && col < g0 + kTR + h; };
+    int64_t H = kH;
+    {
+      long long inw = 0, tot = 0;
+      for (int64_t r0 = 0; r0 < nl; r0 += kTR)
+        for (int64_t r = r0; r < std::min<int64_t>(nl, r0 + kTR); ++r)
+          for (int e = h_rp[(size_t)r]; e < h_rp[(size_t)r + 1]; ++e) { inw += in_win(rb + r0, kH, h_col[(size_t)e]); ++tot; }
+      if (tot > 0 && 4 * inw < tot) H = 0;
+    }
     std::vector<unsigned> trp((size_t)nl + 1 + 4, 0u);
-    std::vector<int> tcol;
+    std::vector<int> tcol, tout;
     std::vector<double> tval;
-    std::vector<int2> tinfo;
-    int rows_in = 0, nnz_in = 0;
+    std::vector<TileDesc> tdesc;
+    TileDesc cur{};
+    int rows_in = 0, nnz_in = 0, out_in = 0;
+    auto close_tile = [&](int64_t r_end) {
+      cur.r1 = (int)r_end;
+      cur.e1 = (int)tcol.size();
+      cur.o1 = (int)tout.size();
+      tdesc.push_back(cur);
+    };
     for (int64_t r = 0; r < nl; ++r) {
       const int len = h_rp[(size_t)r + 1] - h_rp[(size_t)r];
       const bool lng = len > kLongRow;
       const int add = lng ? 0 : len;
-      if (r == 0 || rows_in == kTR || nnz_in + add > cap) {
-        tinfo.push_back(make_int2((int)r, (int)tcol.size()));
-        rows_in = 0;
-        nnz_in = 0;
+      int add_out = 0;
+      if (!lng && rows_in > 0)
+        for (int e = h_rp[(size_t)r]; e < h_rp[(size_t)r + 1]; ++e) add_out += !in_win(rb + cur.r0, H, h_col[(size_t)e]);
+      if (r == 0 || rows_in == kTR || nnz_in + add > cap || out_in + add_out > kOutCap) {
+        if (r > 0) close_tile(r);
+        cur = TileDesc{};
+        cur.r0 = (int)r;
+        cur.e0 = (int)tcol.size();
+        cur.o0 = (int)tout.size();
+        const int64_t g0 = rb + r;
+        cur.wlo = (int)std::max<int64_t>(0, g0 - H);
+        cur.whi = (int)std::min<int64_t>(n, g0 + kTR + H);
+        rows_in = nnz_in = out_in = 0;
       }
       trp[(size_t)r] |= (unsigned)tcol.size();
       if (!lng)
         for (int e = h_rp[(size_t)r]; e < h_rp[(size_t)r + 1]; ++e) {
-          tcol.push_back(enc(e));
+          const int64_t cc = h_col[(size_t)e];
+          int code;
+          if (in_win(rb + cur.r0, H, cc)) code = (int)(cc - cur.wlo);
+          else {
+            code = 0x40000000 | (int)(tout.size() - (size_t)cur.o0);
+            tout.push_back((int)cc);
+            ++out_in;
+          }
+          if (uni && h_w[(size_t)e] < 0) code = (int)((unsigned)code | 0x80000000u);
+          tcol.push_back(code);
           if (!uni) tval.push_back(valof(e));
         }
       trp[(size_t)r + 1] = (unsigned)tcol.size() | (lng ? 0x80000000u : 0u);
       ++rows_in;
       nnz_in += add;
     }
-    if (tcol.size() >= (size_t)INT32_MAX) return fail(c, SCG_EINVAL, "tile layout too large");
-    tinfo.push_back(make_int2((int)nl, (int)tcol.size()));
-    s->ntiles = (int)tinfo.size() - 1;
-    const size_t nnz_s = tcol.size();
+    close_tile(nl);
+    if (tcol.size() >= (size_t)INT32_MAX || tout.size() >= (size_t)INT32_MAX) return fail(c, SCG_EINVAL, "tile layout too large");
+    s->ntiles = (int)tdesc.size();
+    const size_t nnz_s = tcol.size(), nout = tout.size();
     tcol.resize(nnz_s + 4, 0);
+    tout.resize(nout + 4, 0);
     if (!uni) tval.resize(nnz_s + 2, 0.0);
     if (!alloc((void **)&s->trp, sizeof(unsigned) * trp.size()) || !alloc((void **)&s->tcol, sizeof(int) * tcol.size()) ||
-        !alloc((void **)&s->tinfo, sizeof(int2) * tinfo.size()) ||
+        !alloc((void **)&s->tout, sizeof(int) * tout.size()) ||
+        !alloc((void **)&s->tdesc, sizeof(TileDesc) * tdesc.size()) ||
         (!uni && !alloc((void **)&s->tval, sizeof(double) * tval.size())))
       return fail(c, SCG_ENOMEM, "tile layout");
     CK(cudaMemcpyAsync(s->trp, trp.data(), sizeof(unsigned) * trp.size(), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(s->tcol, tcol.data(), sizeof(int) * tcol.size(), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(s->tinfo, tinfo.data(), sizeof(int2) * tinfo.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->tout, tout.data(), sizeof(int) * tout.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->tdesc, tdesc.data(), sizeof(TileDesc) * tdesc.size(), cudaMemcpyHostToDevice, st));
     if (!uni) CK(cudaMemcpyAsync(s->tval, tval.data(), sizeof(double) * tval.size(), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
-    long long nnz_long = (long long)cnt_off - (long long)nnz_s;
-    matbytes = 4.0 * (double)(nl + 1) + (double)nnz_s * (uni ? 4.0 : 12.0) + 8.0 * s->ntiles +
-               12.0 * (double)nnz_long + 8.0 * s->nlong;
+    const long long nnz_long = (long long)cnt_off - (long long)nnz_s;
+    // algorithmic matrix bytes: row offsets, entry codes (+ values), out list, long rows
+    matbytes = 4.0 * (double)(nl + 1) + (double)nnz_s * (uni ? 4.0 : 12.0) + 4.0 * (double)nout +
+               32.0 * s->ntiles + 12.0 * (double)nnz_long + 8.0 * s->nlong;
+    s->tile_h = (int)H;
+    s->tile_out = (long long)nout;
     s->smem1 = uni ? sizeof(TileSmem<1, true>) : sizeof(TileSmem<1, false>);
     s->smem2 = uni ? sizeof(TileSmem<2, true>) : sizeof(TileSmem<2, false>);
   }
@@ -552,7 +597,10 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
 #endif
   {  // grids of the SpMV kernels
     const bool U = s->sell_uniform;
-    auto setsm = [&](const void *k, size_t b) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b); };
+    auto setsm = [&](const void *k, size_t b) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+      if (b > 0) cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    };
     int oa = 1, om = 1;
     if (U) {
       setsm((const void *)k_lanczos_a<true>, s->smem1);
@@ -573,6 +621,10 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
                                      : (int)std::max<int64_t>((s->nslice + 7) / 8, (s->nlong + 7) / 8);
     s->grid_tiles = std::max(1, std::min(need, std::max(1, oa) * c->nsm));
     s->grid_mon = std::max(1, std::min(need, std::max(1, om) * c->nsm));
+    if (std::getenv("SCG_DEBUG"))
+      std::fprintf(stderr, "[scg] shard %d: nl=%lld tiles=%d long=%d uni=%d H=%d out=%lld/%lld smem1=%zu occ_a=%d occ_m=%d grid=%d\n",
+                   s->rank, (long long)nl, s->ntiles, s->nlong, (int)U, s->tile_h, s->tile_out, (long long)s->nnz_off,
+                   s->smem1, oa, om, s->grid_tiles);
   }
   // algorithmic bytes per launch
   const double N = (double)c->n, NL = (double)nl;

@@ -215,13 +215,15 @@ static scg_graph *gen_powerlaw(int64_t n, uint64_t seed) {
 }
 
 /* ---- family 3: mutual k-NN random geometric graph in Morton order ---- */
+/* 21-bit coordinate -> its bits at the even positions 0, 2, ..., 40 (2-D Z-order;
+ * code = spread21(qx) | spread21(qy) << 1 < 2^42, sorted in full by the 48-bit radix sort) */
 static uint64_t spread21(uint64_t x) {
   x &= 0x1fffffull;
-  x = (x | (x << 32)) & 0x1f00000000ffffull;
-  x = (x | (x << 16)) & 0x1f0000ff0000ffull;
-  x = (x | (x << 8)) & 0x100f00f00f00f00full;
-  x = (x | (x << 4)) & 0x10c30c30c30c30c3ull;
-  x = (x | (x << 2)) & 0x1249249249249249ull;
+  x = (x | (x << 16)) & 0x0000ffff0000ffffull;
+  x = (x | (x << 8)) & 0x00ff00ff00ff00ffull;
+  x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0full;
+  x = (x | (x << 2)) & 0x3333333333333333ull;
+  x = (x | (x << 1)) & 0x5555555555555555ull;
   return x;
 }
 
