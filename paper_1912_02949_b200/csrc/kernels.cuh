@@ -144,7 +144,7 @@ __device__ __forceinline__ double div_rn(double a, double b, double rb) {
 #define SCG_CH 4
 #endif
 #ifndef SCG_ENGINE
-#define SCG_ENGINE 1  // short-row SpMV engine: 0 = SELL-32-sigma register pipeline, 1 = tile-staged CSR
+#define SCG_ENGINE 0  // short-row SpMV engine: 0 = SELL-32-sigma register pipeline, 1 = window/tile-staged CSR (TMA)
 #endif
 #ifndef SCG_PIPE
 #define SCG_PIPE 1
