@@ -159,10 +159,11 @@ constexpr int kRpt = SCG_RPT;    // rows per thread in flight
 struct Rows {
   const int *longrows;  // local ids of long rows
   int nlong;
-  // SELL-32-sigma layout of the short rows: slice s covers 32 rows perm[32 s + lane]
-  // (-1: empty lane) of equal-ish length (sorted within windows of kSigma rows);
-  // slot j of lane l is at meta[s].x + 32 j + l; meta[s].y = slice width.
-  const int *perm;
+  // SELL-32-sigma layout of the short rows.  Rows are relabeled at init so that each
+  // window of kSigma rows is sorted by length (long rows first): slice s covers the 32
+  // consecutive rows 32 s .. 32 s + 31; slot j of lane l is at meta[s].x + 32 j + l;
+  // meta[s].y = width | (number of leading long-row lanes, skipped) << 8.
+  const int *perm;      // unused (identity after relabeling)
   const int2 *meta;
   const int *scol;      // column | 0x80000000 for a negative uniform value; -1 = padding
   const double *sval;   // per-slot values, or nullptr when all |C_rj| equal m0
@@ -299,39 +300,34 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
 #if SCG_PIPE == 0
   // SELL slices, one per warp step; latency hidden by occupancy (few registers)
   for (int sl = gw; sl < RL.nslice; sl += nw) {
-    const int p0 = __ldg(&RL.perm[sl * 32 + lane]);
     const int2 m0 = __ldg(&RL.meta[sl]);
+    const int p0 = sl * 32 + lane;
+    const bool ok = p0 < nl && lane >= (m0.y >> 8);
+    const int2 mw = make_int2(m0.x, m0.y & 0xff);
     RowOut<NC> o;
     o.r = p0;
     double xo = 0.0, d0 = 0.0, d1 = 0.0;
-    if (p0 >= 0) { xo = X[rb + p0]; d0 = diag0[p0]; if (NC > 1) d1 = diag1[p0]; }
-    for (int j0 = 0; j0 < m0.y; j0 += kChunk) {
+    if (ok) { xo = X[rb + p0]; d0 = diag0[p0]; if (NC > 1) d1 = diag1[p0]; }
+    o.xr = (xo) * rden;
+    o.s[0] = d0 * o.xr;
+    if (NC > 1) o.s[NC - 1] = d1 * o.xr;
+    for (int j0 = 0; j0 < mw.y; j0 += kChunk) {
       int cx[kChunk];
       double vx[kChunk], xx[kChunk];
-      sell_load_chunk<UNI>(RL, m0, j0, lane, cx, vx);
+      sell_load_chunk<UNI>(RL, mw, j0, lane, cx, vx);
 #pragma unroll
       for (int u = 0; u < kChunk; ++u)
         if (cx[u] != -1) xx[u] = __ldg(&X[cx[u] & 0x7fffffff]);
-      if (j0 == 0) {
-        o.xr = (xo) * rden;
-        o.s[0] = d0 * o.xr;
-        if (NC > 1) o.s[NC - 1] = d1 * o.xr;
-      }
       sell_fma_chunk<NC, UNI>(RL, cx, vx, xx, den, rden, o);
     }
-    if (m0.y == 0) {
-      o.xr = (xo) * rden;
-      o.s[0] = d0 * o.xr;
-      if (NC > 1) o.s[NC - 1] = d1 * o.xr;
-    }
-    if (p0 >= 0) epi(o);
+    if (ok) epi(o);
   }
 #else
   // SELL slices, software-pipelined three deep: in the step that computes slice i
   // the gathers and own-row loads of slice i+1, the column loads of slice i+2 and
-  // the (perm, meta) loads of slice i+3 are issued, so a step never waits on a
-  // load issued in the same step.
-  const int *__restrict__ perm = RL.perm;
+  // the meta load of slice i+3 are issued, so a step never waits on a load issued
+  // in the same step.  Slice sl covers rows 32 sl + lane (consecutive: coalesced
+  // own-entry, diagonal and output accesses).
   const int2 *__restrict__ meta = RL.meta;
   // each block owns a contiguous range of slices (neighbouring rows share their
   // gathered entries in the SM's L1); its warps interleave within the range
@@ -339,61 +335,57 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
   const int ns = min(RL.nslice, (int)(blockIdx.x + 1) * per);
   const int wstep = blockDim.x >> 5;
   int sl = blockIdx.x * per + (threadIdx.x >> 5);
-  // stage 3 (perm/meta), stage 2 (+cols), stage 1 (+gathers, own), stage 0 (compute)
-  int p0 = -1, p1 = -1, p2 = -1, p3 = -1;
-  int2 m0 = make_int2(0, 0), m1 = m0, m2 = m0, m3 = m0;
-  if (sl < ns) { p0 = __ldg(&perm[sl * 32 + lane]); m0 = __ldg(&meta[sl]); }
-  if (sl + wstep < ns) { p1 = __ldg(&perm[(sl + wstep) * 32 + lane]); m1 = __ldg(&meta[sl + wstep]); }
-  if (sl + 2 * wstep < ns) { p2 = __ldg(&perm[(sl + 2 * wstep) * 32 + lane]); m2 = __ldg(&meta[sl + 2 * wstep]); }
-  if (sl + 3 * wstep < ns) { p3 = __ldg(&perm[(sl + 3 * wstep) * 32 + lane]); m3 = __ldg(&meta[sl + 3 * wstep]); }
+  auto mload = [&](int q) -> int2 { return q < ns ? __ldg(&meta[q]) : make_int2(0, 0); };
+  auto width = [](int2 m) { return make_int2(m.x, m.y & 0xff); };
+  int2 m0 = mload(sl), m1 = mload(sl + wstep), m2 = mload(sl + 2 * wstep), m3 = mload(sl + 3 * wstep);
   int c0[kChunk], c1[kChunk], c2[kChunk];
   double v0[kChunk], v1[kChunk], v2[kChunk];
-  sell_load_chunk<UNI>(RL, m0, 0, lane, c0, v0);
-  sell_load_chunk<UNI>(RL, m1, 0, lane, c1, v1);
-  sell_load_chunk<UNI>(RL, m2, 0, lane, c2, v2);
+  sell_load_chunk<UNI>(RL, width(m0), 0, lane, c0, v0);
+  sell_load_chunk<UNI>(RL, width(m1), 0, lane, c1, v1);
+  sell_load_chunk<UNI>(RL, width(m2), 0, lane, c2, v2);
   double g0[kChunk], g1[kChunk];
 #pragma unroll
   for (int u = 0; u < kChunk; ++u)
     if (c0[u] != -1) g0[u] = __ldg(&X[c0[u] & 0x7fffffff]);
+  auto own = [&](int q, int2 m, double &xo, double &dd0, double &dd1) {
+    const int p = q * 32 + lane;
+    if (q < ns && p < nl && lane >= (m.y >> 8)) { xo = X[rb + p]; dd0 = diag0[p]; if (NC > 1) dd1 = diag1[p]; }
+  };
   double xo0 = 0.0, d00 = 0.0, d10 = 0.0, xo1 = 0.0, d01 = 0.0, d11 = 0.0;
-  if (p0 >= 0) { xo0 = X[rb + p0]; d00 = diag0[p0]; if (NC > 1) d10 = diag1[p0]; }
+  own(sl, m0, xo0, d00, d10);
   while (sl < ns) {
     // stage 1: gathers and own-row loads of slice i+1
 #pragma unroll
     for (int u = 0; u < kChunk; ++u)
-#ifdef SCG_EXP_NOGATHER
-      if (c1[u] != -1) g1[u] = __ldg(&X[rb + (sl + wstep) * 32 + lane]);
-#else
       if (c1[u] != -1) g1[u] = __ldg(&X[c1[u] & 0x7fffffff]);
-#endif
-    if (p1 >= 0) { xo1 = X[rb + p1]; d01 = diag0[p1]; if (NC > 1) d11 = diag1[p1]; }
-    // stage 2: columns of slice i+3 (meta known), stage 3: perm/meta of slice i+4
+    xo1 = 0.0; d01 = 0.0; d11 = 0.0;
+    own(sl + wstep, m1, xo1, d01, d11);
+    // stage 2: columns of slice i+3 (meta known), stage 3: meta of slice i+4
     int c3[kChunk];
     double v3[kChunk];
-    sell_load_chunk<UNI>(RL, m3, 0, lane, c3, v3);
-    int p4 = -1;
-    int2 m4 = make_int2(0, 0);
-    const int sl4 = sl + 4 * wstep;
-    if (sl4 < ns) { p4 = __ldg(&perm[sl4 * 32 + lane]); m4 = __ldg(&meta[sl4]); }
+    sell_load_chunk<UNI>(RL, width(m3), 0, lane, c3, v3);
+    const int2 m4 = mload(sl + 4 * wstep);
     // stage 0: compute slice i
+    const int p0 = sl * 32 + lane;
+    const bool ok = p0 < nl && lane >= (m0.y >> 8);
     RowOut<NC> o;
     o.r = p0;
     o.xr = (xo0) * rden;
     o.s[0] = d00 * o.xr;
     if (NC > 1) o.s[NC - 1] = d10 * o.xr;
     sell_fma_chunk<NC, UNI>(RL, c0, v0, g0, den, rden, o);
-    for (int j0 = kChunk; j0 < m0.y; j0 += kChunk) {  // rows longer than one chunk
+    const int2 mw = width(m0);
+    for (int j0 = kChunk; j0 < mw.y; j0 += kChunk) {  // rows longer than one chunk
       int cx[kChunk];
       double vx[kChunk], xx[kChunk];
-      sell_load_chunk<UNI>(RL, m0, j0, lane, cx, vx);
+      sell_load_chunk<UNI>(RL, mw, j0, lane, cx, vx);
 #pragma unroll
       for (int u = 0; u < kChunk; ++u)
         if (cx[u] != -1) xx[u] = __ldg(&X[cx[u] & 0x7fffffff]);
       sell_fma_chunk<NC, UNI>(RL, cx, vx, xx, den, rden, o);
     }
-    if (p0 >= 0) epi(o);
+    if (ok) epi(o);
     // rotate the pipeline
-    p0 = p1; p1 = p2; p2 = p3; p3 = p4;
     m0 = m1; m1 = m2; m2 = m3; m3 = m4;
 #pragma unroll
     for (int u = 0; u < kChunk; ++u) {
@@ -830,12 +822,15 @@ __global__ void k_scale_c(const double *__restrict__ w, long long nnz, const dou
 }
 
 // Omega[i, k] ~ N(0,1) from the seeded stream (Alg. 3 line 2).
-__global__ void k_omega(double *__restrict__ Om, int nl, long long rb, int R, uint64_t seed) {
+// orig[r]: original (input) index of local row r minus rb -- rows are relabeled at init
+// (DESIGN.md section 5); the seeded streams are indexed by the ORIGINAL vertex id.
+__global__ void k_omega(double *__restrict__ Om, int nl, long long rb, int R, uint64_t seed,
+                        const int *__restrict__ orig) {
   const long long tot = (long long)nl * R;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
     const int k = (int)(e / nl);
     const long long r = e - (long long)k * nl;
-    Om[e] = scg_omega(seed, rb + r, k);
+    Om[e] = scg_omega(seed, rb + orig[r], k);
   }
 }
 
@@ -848,14 +843,15 @@ __global__ void k_init_d(const double *__restrict__ z, const double *__restrict_
 
 // Lanczos start vector g = randn (Alg. 2 line 1) for iteration t and ||g||^2 (exact).
 __global__ void __launch_bounds__(kBlock) k_gen_start(double *__restrict__ g, int nl, long long rb, uint64_t seed,
-                                                      long long t, XSlot *slot, DevScalars *sc, Net net) {
+                                                      long long t, XSlot *slot, DevScalars *sc, Net net,
+                                                      const int *__restrict__ orig) {
   __shared__ XBlk<1> xb;
   xblk_init<1>(xb);
   XWin acc[1];
   xwin_init(acc[0]);
   int err = 0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
-    const double v = scg_lanczos_start(seed, t, rb + r);
+    const double v = scg_lanczos_start(seed, t, rb + orig[r]);
     gstore(net, g + rb + r, r, v);
     xwin_add(acc[0], v * v, err, xb.l[0]);
   }
@@ -1325,7 +1321,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_dual_sketch(const double *__restr
                                                         const double *__restrict__ v, double *__restrict__ S,
                                                         double *__restrict__ g, int nl, long long rb, int R,
                                                         IterArgs A, uint64_t seed, XSlot *slot, DevScalars *sc,
-                                                        Net net) {
+                                                        Net net, const int *__restrict__ orig) {
   __shared__ double ck[kMaxR];
   const double gam = sc->gamma;
   if (threadIdx.x < R) ck[threadIdx.x] = (A.eta * A.alpha) * sc->gk[threadIdx.x];
@@ -1374,7 +1370,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_dual_sketch(const double *__restr
     for (int u = 0; u < 2; ++u) {
       const int r = r0 + u * stride;
       if (r < nl) {
-        const double gv = scg_lanczos_start(seed, A.t + 1, rb + r);
+        const double gv = scg_lanczos_start(seed, A.t + 1, rb + orig[r]);
         gstore(net, g + rb + r, r, gv);
         xwin_add(acc[0], gv * gv, err, xb.l[0]);
       }

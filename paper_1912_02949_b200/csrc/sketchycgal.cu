@@ -84,6 +84,9 @@ struct Shard {
   int ntiles = 0, tile_h = 0;
   long long tile_out = 0;
   size_t smem1 = 0, smem2 = 0;
+  // row relabeling (SELL engine): local row nu holds input row rb + origloc[nu]
+  std::vector<int> origloc;
+  int *orig = nullptr;            // device copy of origloc
   // sharding
   unsigned char *mask = nullptr;  // device [nl], nullptr when world == 1
   Mailbox *mb = nullptr;
@@ -112,6 +115,7 @@ struct scg_ctx {
   int rank = 0;
   std::vector<int64_t> splits;
   std::vector<Shard *> sh;
+  std::vector<int> gmap;  // input vertex id -> device row label (identity without relabeling)
   unsigned long long epoch = 0;
 #ifdef SCG_WITH_NCCL
   ncclComm_t comm = nullptr;
@@ -293,11 +297,63 @@ void free_shard(Shard *s) {
   void *ptrs[] = {s->rp, s->col, s->val, s->wts, s->ldiag, s->cdiag, s->d, s->z, s->y, s->a, s->v, s->G,
                   s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
                   s->sc, s->slots, s->dlog, s->longrows, s->sell_perm, s->sell_col, s->sell_meta, s->sell_val,
-                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tout, s->tdesc};
+                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tout, s->tdesc, s->orig};
   for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete s;
+}
+
+// Row relabeling of one shard (SELL engine): within windows of kSortWin consecutive rows,
+// rows sorted by length, longest first (long rows lead), ties by input order.  A
+// symmetric permutation of L: the SpMV slices become contiguous rows.  The CAC-3 chain
+// order (ascending INPUT column) and every exact sum are unchanged, so results are
+// bitwise those of the input labeling; the seeded streams and all outputs use input ids.
+constexpr int64_t kSortWin = 256;
+void relabel_perm(const int64_t *rp, int64_t nl, std::vector<int> &origloc) {
+  origloc.resize((size_t)nl);
+  for (int64_t r = 0; r < nl; ++r) origloc[(size_t)r] = (int)r;
+#if SCG_ENGINE == 0
+  for (int64_t w = 0; w < nl; w += kSortWin) {
+    const int64_t e = std::min<int64_t>(nl, w + kSortWin);
+    std::stable_sort(origloc.begin() + w, origloc.begin() + e,
+                     [&](int x, int y) { return rp[x + 1] - rp[x] > rp[y + 1] - rp[y]; });
+  }
+#endif
+}
+
+// gmap[input id] = device label, for every vertex (all ranks' permutations).
+scg_status build_gmap(scg_ctx *c) {
+  c->gmap.assign((size_t)c->n, 0);
+  if (c->mode != 2) {
+    for (Shard *s : c->sh)
+      for (int64_t nu = 0; nu < s->nl; ++nu) c->gmap[(size_t)(s->rb + s->origloc[(size_t)nu])] = (int)(s->rb + nu);
+    return SCG_OK;
+  }
+#ifdef SCG_WITH_NCCL
+  // every rank's origloc, broadcast by its owner (variable sizes: grouped broadcasts)
+  int *buf = nullptr;
+  CK(cudaMalloc(&buf, sizeof(int) * (size_t)c->n));
+  Shard *me = c->sh[0];
+  CK(cudaMemcpyAsync(buf + me->rb, me->origloc.data(), sizeof(int) * me->nl, cudaMemcpyHostToDevice, c->stream));
+  NK(ncclGroupStart());
+  for (int q = 0; q < c->world; ++q) {
+    const int64_t a = c->splits[(size_t)q], b = c->splits[(size_t)q + 1];
+    NK(ncclBroadcast(buf + a, buf + a, (size_t)(b - a), ncclInt32, q, c->comm, c->stream));
+  }
+  NK(ncclGroupEnd());
+  std::vector<int> all((size_t)c->n);
+  CK(cudaMemcpyAsync(all.data(), buf, sizeof(int) * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(buf);
+  for (int q = 0; q < c->world; ++q) {
+    const int64_t a = c->splits[(size_t)q], b = c->splits[(size_t)q + 1];
+    for (int64_t nu = 0; nu < b - a; ++nu) c->gmap[(size_t)(a + all[(size_t)(a + nu)])] = (int)(a + nu);
+  }
+  return SCG_OK;
+#else
+  return fail(c, SCG_EUNSUPPORTED, "multi-process sharding needs the NCCL build");
+#endif
 }
 
 // CSR checks of one shard's rows (before any device work).
@@ -335,16 +391,20 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   std::vector<unsigned char> h_mask;
   if (c->world > 1) h_mask.assign((size_t)nl, 0);
   int64_t o = 0;
-  for (int64_t r = 0; r < nl; ++r) {
-    h_rp[(size_t)r] = (int)o;
+  // device row nu is input row r = origloc[nu]; its entries stay in the input (ascending
+  // input column) order -- the CAC-3 chain order -- with columns relabeled by gmap
+  for (int64_t nu = 0; nu < nl; ++nu) {
+    const int64_t r = s->origloc[(size_t)nu];
+    h_rp[(size_t)nu] = (int)o;
     double dsum = 0.0;
     bool had = false;
     unsigned m = 0;
     for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
-      const int32_t cc = colp[k - base];
+      const int32_t c_in = colp[k - base];
       const double lv = valp[k - base];
-      if (cc == r + rb) { h_diag[(size_t)r] = lv; had = true; }
+      if (c_in == r + rb) { h_diag[(size_t)nu] = lv; had = true; }
       else {
+        const int32_t cc = c->gmap[(size_t)c_in];
         h_col[(size_t)o] = cc;
         h_w[(size_t)o] = -lv;
         dsum += -lv;
@@ -355,9 +415,9 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
         }
       }
     }
-    if (!has_diagonal || !had) h_diag[(size_t)r] = has_diagonal ? 0.0 : dsum;
+    if (!has_diagonal || !had) h_diag[(size_t)nu] = has_diagonal ? 0.0 : dsum;
     if (c->world > 1) {
-      h_mask[(size_t)r] = (unsigned char)m;
+      h_mask[(size_t)nu] = (unsigned char)m;
       s->halo_rows += m != 0;
     }
   }
@@ -384,6 +444,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
             alloc((void **)&s->dlog, sizeof(scg_iter_rec) * c->log_cap) &&
             alloc((void **)&s->longrows, sizeof(int) * h_long.size()) &&
             alloc((void **)&s->mb, sizeof(Mailbox)) && alloc((void **)&s->peerG, sizeof(double *) * kMaxRanks) &&
+            alloc((void **)&s->orig, sizeof(int) * (size_t)nl) &&
             alloc((void **)&s->peerMB, sizeof(Mailbox *) * kMaxRanks);
   if (!ok) return fail(c, SCG_ENOMEM, "device allocation");
   if (c->world > 1 && !alloc((void **)&s->mask, (size_t)nl)) return fail(c, SCG_ENOMEM, "halo mask");
@@ -413,6 +474,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   if (!h_long.empty())
     CK(cudaMemcpyAsync(s->longrows, h_long.data(), sizeof(int) * h_long.size(), cudaMemcpyHostToDevice, st));
   if (c->world > 1) CK(cudaMemcpyAsync(s->mask, h_mask.data(), (size_t)nl, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(s->orig, s->origloc.data(), sizeof(int) * (size_t)nl, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(s->sc, 0, sizeof(DevScalars), st));
   CK(cudaMemsetAsync(s->slots, 0, sizeof(XSlot) * SLOT_COUNT, st));
   CK(cudaMemsetAsync(s->mb, 0, sizeof(Mailbox), st));
@@ -542,56 +604,51 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
   }
 #else
   {
-    const int kSigma = 256;  // sorting window of SELL-32-sigma
-    std::vector<int> wstart, perm, scol, win;
+    // rows are already sorted by length within windows of kSigma rows (relabel_perm), so a
+    // slice is 32 consecutive rows; leading long rows (warp engine) are skipped lanes
+    const int64_t nsl = (nl + 31) / 32;
+    std::vector<int> scol;
     std::vector<int2> meta;
     std::vector<double> sval;
-    for (int64_t w = 0; w < nl; w += kSigma) {
-      wstart.push_back((int)meta.size());
-      win.clear();
-      for (int64_t r = w; r < std::min<int64_t>(nl, w + kSigma); ++r)
-        if (h_rp[(size_t)r + 1] - h_rp[(size_t)r] <= kLongRow) win.push_back((int)r);
-      std::stable_sort(win.begin(), win.end(), [&](int x, int y) {
-        return h_rp[(size_t)x + 1] - h_rp[(size_t)x] > h_rp[(size_t)y + 1] - h_rp[(size_t)y];
-      });
-      for (size_t s0 = 0; s0 < win.size(); s0 += 32) {
-        const int cnt = (int)std::min<size_t>(32, win.size() - s0);
-        const int width = h_rp[(size_t)win[s0] + 1] - h_rp[(size_t)win[s0]];
-        meta.push_back(make_int2((int)scol.size(), width));
-        for (int j = 0; j < width; ++j)
-          for (int l = 0; l < 32; ++l) {
-            int cc = -1;
-            double vv = 0.0;
-            if (l < cnt) {
-              const int r = win[s0 + l];
-              const int e = h_rp[(size_t)r] + j;
-              if (e < h_rp[(size_t)r + 1]) { cc = enc(e); vv = valof(e); }
-            }
-            scol.push_back(cc);
-            if (!uni) sval.push_back(vv);
-          }
-        for (int l = 0; l < 32; ++l) perm.push_back(l < cnt ? win[s0 + l] : -1);
+    for (int64_t q = 0; q < nsl; ++q) {
+      int nskip = 0, width = 0;
+      for (int l = 0; l < 32; ++l) {
+        const int64_t r = q * 32 + l;
+        if (r >= nl) break;
+        const int len = h_rp[(size_t)r + 1] - h_rp[(size_t)r];
+        if (len > kLongRow) {
+          if (nskip != l) return fail(c, SCG_EINVAL, "SELL: long rows must lead their slice");
+          nskip = l + 1;
+        } else width = std::max(width, len);
       }
+      meta.push_back(make_int2((int)scol.size(), width | (nskip << 8)));
+      for (int j = 0; j < width; ++j)
+        for (int l = 0; l < 32; ++l) {
+          const int64_t r = q * 32 + l;
+          int cc = -1;
+          double vv = 0.0;
+          if (l >= nskip && r < nl) {
+            const int e = h_rp[(size_t)r] + j;
+            if (e < h_rp[(size_t)r + 1]) { cc = enc(e); vv = valof(e); }
+          }
+          scol.push_back(cc);
+          if (!uni) sval.push_back(vv);
+        }
       if (scol.size() >= (size_t)INT32_MAX) return fail(c, SCG_EINVAL, "SELL layout too large");
     }
     s->nslice = (int)meta.size();
-    wstart.push_back((int)meta.size());
-    s->nwin = (int)wstart.size() - 1;
-    if (!alloc((void **)&s->sell_wstart, sizeof(int) * wstart.size()) ||
-        !alloc((void **)&s->sell_perm, sizeof(int) * perm.size()) ||
-        !alloc((void **)&s->sell_meta, sizeof(int2) * meta.size()) ||
+    s->nwin = 0;
+    if (!alloc((void **)&s->sell_meta, sizeof(int2) * meta.size()) ||
         !alloc((void **)&s->sell_col, sizeof(int) * scol.size()) ||
         (!uni && !alloc((void **)&s->sell_val, sizeof(double) * sval.size())))
       return fail(c, SCG_ENOMEM, "SELL layout");
-    CK(cudaMemcpyAsync(s->sell_wstart, wstart.data(), sizeof(int) * wstart.size(), cudaMemcpyHostToDevice, st));
-    if (!perm.empty()) CK(cudaMemcpyAsync(s->sell_perm, perm.data(), sizeof(int) * perm.size(), cudaMemcpyHostToDevice, st));
     if (!meta.empty()) CK(cudaMemcpyAsync(s->sell_meta, meta.data(), sizeof(int2) * meta.size(), cudaMemcpyHostToDevice, st));
     if (!scol.empty()) CK(cudaMemcpyAsync(s->sell_col, scol.data(), sizeof(int) * scol.size(), cudaMemcpyHostToDevice, st));
     if (!uni && !sval.empty())
       CK(cudaMemcpyAsync(s->sell_val, sval.data(), sizeof(double) * sval.size(), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
     s->sell_slots = (double)scol.size();
-    matbytes = s->sell_slots * (uni ? 4.0 : 12.0) + 4.0 * (double)nl + 8.0 * s->nslice;
+    matbytes = s->sell_slots * (uni ? 4.0 : 12.0) + 8.0 * s->nslice;
     s->smem1 = s->smem2 = 0;
   }
 #endif
@@ -670,10 +727,7 @@ scg_status connect_peers(scg_ctx *c, const void *uid) {
   } else {
 #ifdef SCG_WITH_NCCL
     Shard *s = c->sh[0];
-    ncclUniqueId id;
-    std::memcpy(&id, uid, sizeof(id));
-    NK(ncclCommInitRank(&c->comm, P, id, c->rank));
-    CK(cudaMalloc(&c->dred, sizeof(double) * kMaxR * kMaxR * 4));
+    (void)uid;  // the communicator was created at the start of init
     cudaIpcMemHandle_t hh[2];
     CK(cudaIpcGetMemHandle(&hh[0], s->G));
     CK(cudaIpcGetMemHandle(&hh[1], s->mb));
@@ -903,6 +957,17 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   }
   scg_status st;
   const int nshard = c->mode == 1 ? world : 1;
+#ifdef SCG_WITH_NCCL
+  if (c->mode == 2) {
+    ncclUniqueId id;
+    std::memcpy(&id, dist->nccl_unique_id, sizeof(id));
+    if (ncclCommInitRank(&c->comm, world, id, c->rank) != ncclSuccess) return bad(SCG_ENCCL);
+    if (cudaMalloc(&c->dred, sizeof(double) * kMaxR * kMaxR * 4) != cudaSuccess) return bad(SCG_ENOMEM);
+  }
+#else
+  if (c->mode == 2) return bad(SCG_EUNSUPPORTED);
+#endif
+  // row relabeling within sorting windows (SELL engine), then the global id map
   for (int p = 0; p < nshard; ++p) {
     Shard *s = new Shard();
     c->sh.push_back(s);
@@ -910,6 +975,11 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
     s->rb = c->splits[(size_t)s->rank];
     s->nl = c->splits[(size_t)s->rank + 1] - s->rb;
     const int64_t off = c->mode == 2 ? 0 : s->rb;  // index of this shard's first row in L->row_ptr
+    relabel_perm(L->row_ptr + off, s->nl, s->origloc);
+  }
+  if ((st = build_gmap(c))) return bad(st);
+  for (Shard *s : c->sh) {
+    const int64_t off = c->mode == 2 ? 0 : s->rb;
     if ((st = build_shard(c, s, L->row_ptr + off, L->col_idx + L->row_ptr[off], L->val + L->row_ptr[off],
                           L->has_diagonal)))
       return bad(st);
@@ -961,7 +1031,8 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
     const int gnnz = (int)std::min<long long>(std::max<long long>(1, (s->nnz_off + kBlock - 1) / kBlock), 8 * c->nsm);
     launch(c, KC_OTHER, 0.0, k_scale_c, dim3(gnnz), dim3(kBlock), (const double *)s->wts, (long long)s->nnz_off,
            (const double *)s->ldiag, (int)s->nl, (const double *)s->dscalar, scale ? 1 : 0, s->val, s->cdiag);
-    launch(c, KC_OTHER, 0.0, k_omega, dim3(8 * c->nsm), dim3(kBlock), s->Om, (int)s->nl, (long long)s->rb, (int)R, seed);
+    launch(c, KC_OTHER, 0.0, k_omega, dim3(8 * c->nsm), dim3(kBlock), s->Om, (int)s->nl, (long long)s->rb, (int)R, seed,
+           (const int *)s->orig);
     const double beta1 = beta0 * std::sqrt(2.0);
     launch(c, KC_OTHER, 0.0, k_init_d, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z, (const double *)s->y,
            (const double *)s->cdiag, s->d, (int)s->nl, c->b, beta1);
@@ -969,7 +1040,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   const unsigned long long E1 = ++c->epoch;
   for (Shard *s : c->sh)
     launch(c, KC_OTHER, 0.0, k_gen_start, dim3(s->grid_rows), dim3(kBlock), c->wslot(s, 0), (int)s->nl,
-           (long long)s->rb, seed, (long long)1, s->slots + SLOT_NU0, s->sc, net_of(c, s, E1));
+           (long long)s->rb, seed, (long long)1, s->slots + SLOT_NU0, s->sc, net_of(c, s, E1), (const int *)s->orig);
   pull_all(c, FK_RHO0, 1, E1, FinArgs{});
   if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) return bad(SCG_ECUDA);
   for (int k = 0; k < KC_COUNT; ++k) { c->kl[k] = 0; c->kms[k] = 0; c->kbytes_sum[k] = 0; }
@@ -1112,7 +1183,8 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     for (Shard *s : c->sh)
       launch(c, KC_DUAL_SKETCH, s->kb[KC_DUAL_SKETCH], k_dual_sketch, dim3(s->grid_dual), dim3(kBlock),
              (const double *)s->z, s->y, s->d, (const double *)s->cdiag, (const double *)s->v, s->S, c->wslot(s, 0),
-             (int)s->nl, (long long)s->rb, c->R, A, c->seed, s->slots + SLOT_NU0, s->sc, net_of(c, s, E));
+             (int)s->nl, (long long)s->rb, c->R, A, c->seed, s->slots + SLOT_NU0, s->sc, net_of(c, s, E),
+             (const int *)s->orig);
     pull_all(c, FK_RHO0, 1, E, FinArgs{});
     c->t = t;
   }
@@ -1143,6 +1215,14 @@ scg_status sketchycgal_iter_log(scg_ctx *c, int64_t t0, int64_t count, scg_iter_
   return SCG_OK;
 }
 
+// Copy a device row vector (device labels) of shard s into out[off + input row] (host).
+static scg_status fetch_rows(scg_ctx *c, const Shard *s, const double *dsrc, double *out, int64_t off) {
+  std::vector<double> h((size_t)s->nl);
+  CK(cudaMemcpy(h.data(), dsrc, sizeof(double) * (size_t)s->nl, cudaMemcpyDeviceToHost));
+  for (int64_t nu = 0; nu < s->nl; ++nu) out[off + s->origloc[(size_t)nu]] = h[(size_t)nu];
+  return SCG_OK;
+}
+
 scg_status sketchycgal_get_state(scg_ctx *c, int32_t which, double *out) {
   if (!c || !out) return SCG_EINVAL;
   scg_status st = sketchycgal_synchronize(c);
@@ -1150,7 +1230,6 @@ scg_status sketchycgal_get_state(scg_ctx *c, int32_t which, double *out) {
   const int64_t NL = c->nl_total();
   int64_t off = 0;
   for (Shard *s : c->sh) {
-    const size_t nlb = sizeof(double) * (size_t)s->nl;
     const double *src = nullptr;
     bool mat = false;
     switch (which) {
@@ -1163,11 +1242,9 @@ scg_status sketchycgal_get_state(scg_ctx *c, int32_t which, double *out) {
       case 6: src = s->cdiag; break;
       default: return SCG_EINVAL;
     }
-    if (mat) {  // column-major with leading dimension NL (all rows of this context)
-      CK(cudaMemcpy2D(out + off, sizeof(double) * NL, src, sizeof(double) * s->nl, nlb, c->R, cudaMemcpyDeviceToHost));
-    } else {
-      CK(cudaMemcpy(out + off, src, nlb, cudaMemcpyDeviceToHost));
-    }
+    // column-major with leading dimension NL (all rows of this context), input row order
+    for (int k = 0; k < (mat ? c->R : 1); ++k)
+      if ((st = fetch_rows(c, s, src + (size_t)k * s->nl, out + (size_t)k * NL, off))) return st;
     off += s->nl;
   }
   return SCG_OK;
@@ -1179,7 +1256,11 @@ scg_status sketchycgal_apply_D(scg_ctx *c, const double *xh, double *yh) {
   if (st) return st;
   double *dx = nullptr, *dy = nullptr;
   CK(cudaMalloc(&dx, sizeof(double) * c->npad));
-  CK(cudaMemcpy(dx, xh, sizeof(double) * c->n, cudaMemcpyHostToDevice));
+  {  // x in input order -> device labels
+    std::vector<double> xr((size_t)c->n);
+    for (int64_t g = 0; g < c->n; ++g) xr[(size_t)c->gmap[(size_t)g]] = xh[g];
+    CK(cudaMemcpy(dx, xr.data(), sizeof(double) * c->n, cudaMemcpyHostToDevice));
+  }
   int64_t off = 0;
   for (Shard *s : c->sh) {
     CK(cudaMalloc(&dy, sizeof(double) * std::max<int64_t>(1, s->nl)));
@@ -1188,7 +1269,7 @@ scg_status sketchycgal_apply_D(scg_ctx *c, const double *xh, double *yh) {
     launch_smem(c, KC_OTHER, 0.0, s->sell_uniform ? k_apply_d<true> : k_apply_d<false>, dim3(s->grid_tiles), dim3(kBlock), s->smem1,
            C, TT, (const double *)s->d, (const double *)dx, (int)s->nl, (long long)s->rb, dy);
     CK(cudaStreamSynchronize(c->stream));
-    CK(cudaMemcpy(yh + off, dy, sizeof(double) * s->nl, cudaMemcpyDeviceToHost));
+    if ((st = fetch_rows(c, s, dy, yh, off))) return st;
     cudaFree(dy);
     off += s->nl;
   }
@@ -1317,8 +1398,8 @@ scg_status sketchycgal_reconstruct(scg_ctx *c, double *Uh, double *Lambda, doubl
     const int64_t NL = c->nl_total();
     int64_t off = 0;
     for (Shard *s : c->sh) {
-      CK(cudaMemcpy2D(Uh + off, sizeof(double) * NL, s->U, sizeof(double) * s->nl, sizeof(double) * s->nl, R,
-                      cudaMemcpyDeviceToHost));
+      for (int k = 0; k < R; ++k)
+        if ((st = fetch_rows(c, s, s->U + (size_t)k * s->nl, Uh + (size_t)k * NL, off))) return st;
       off += s->nl;
     }
   }
@@ -1429,14 +1510,16 @@ scg_status sketchycgal_round(scg_ctx *c, int8_t *chi, double *cut_weight) {
   // chi_0 = +1: the sign of U[0, best] lives on the rank owning global row 0
   std::vector<double> u0{0.0};
   for (Shard *s : c->sh)
-    if (s->rb == 0) CK(cudaMemcpy(&u0[0], s->U + (size_t)best * s->nl, sizeof(double), cudaMemcpyDeviceToHost));
+    if (s->rb == 0)
+      CK(cudaMemcpy(&u0[0], s->U + (size_t)best * s->nl + c->gmap[0], sizeof(double), cudaMemcpyDeviceToHost));
   if ((st = host_allreduce(c, u0))) return st;
   const int flip = u0[0] >= 0.0 ? 1 : -1;
   int64_t off = 0;
   for (Shard *s : c->sh) {
     std::vector<double> u((size_t)s->nl);
     CK(cudaMemcpy(u.data(), s->U + (size_t)best * s->nl, sizeof(double) * s->nl, cudaMemcpyDeviceToHost));
-    for (int64_t r = 0; r < s->nl; ++r) chi[off + r] = (int8_t)((u[(size_t)r] >= 0.0 ? 1 : -1) * flip);
+    for (int64_t nu = 0; nu < s->nl; ++nu)
+      chi[off + s->origloc[(size_t)nu]] = (int8_t)((u[(size_t)nu] >= 0.0 ? 1 : -1) * flip);
     off += s->nl;
   }
   *cut_weight = w[best];
