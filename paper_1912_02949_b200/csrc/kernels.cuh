@@ -178,9 +178,11 @@ struct Rows {
   const unsigned *trp;
   const int *tcol;      // entry code (see the tile engine below)
   const double *tval;   // values, or nullptr when all |C_rj| equal m0
-  const int *tout;      // out-of-window columns of every tile
+  const int *tout;      // out-of-window columns of every tile (engine 1) / chunk (engine 2)
   const struct TileDesc *tdesc;
   int ntiles;
+  const int *cout;      // engine 2: out list offsets per chunk
+  long long nglob;
 };
 
 constexpr int kWin = 1024;  // rows per window (= SELL sorting window sigma)
@@ -401,6 +403,30 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
 }
 
 
+__device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Elements [i0, i1) of a global array (element size ES) are copied as the 16-byte
+// aligned byte range around them; sdst then holds the array from the aligned element
+// at or below i0 (seg_shift elements before i0).  Arrays carry >= 16 bytes of slack.
+template <int ES>
+__device__ __forceinline__ uint32_t seg_bytes(long long i0, long long i1) {
+  if (i1 <= i0) return 0u;
+  return (uint32_t)((((i1 * ES) + 15) & ~15ll) - ((i0 * ES) & ~15ll));
+}
+template <int ES>
+__device__ __forceinline__ void bulk_seg(void *sdst, const void *gbase, long long i0, long long i1,
+                                         unsigned long long *bar) {
+  if (i1 <= i0) return;
+  bulk_g2s(sdst, (const char *)gbase + ((i0 * ES) & ~15ll), seg_bytes<ES>(i0, i1), bar);
+}
+template <int ES>
+__device__ __forceinline__ int seg_shift(long long i0) { return (int)(((i0 * ES) & 15ll) / ES); }
+
 // ---------------------------------------------------------------- tile-staged CSR engine (SCG_ENGINE 1)
 // The short rows are cut (on the host) into tiles of <= kTR consecutive rows.  Each
 // tile has an index WINDOW [wlo, whi) of the gathered vector that contains its own
@@ -458,30 +484,6 @@ struct __align__(16) TileSmem {
   TileDesc tl[kTLCap];
   unsigned long long bar[kNS];
 };
-
-__device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// Elements [i0, i1) of a global array (element size ES) are copied as the 16-byte
-// aligned byte range around them; sdst then holds the array from the aligned element
-// at or below i0 (seg_shift elements before i0).  Arrays carry >= 16 bytes of slack.
-template <int ES>
-__device__ __forceinline__ uint32_t seg_bytes(long long i0, long long i1) {
-  if (i1 <= i0) return 0u;
-  return (uint32_t)((((i1 * ES) + 15) & ~15ll) - ((i0 * ES) & ~15ll));
-}
-template <int ES>
-__device__ __forceinline__ void bulk_seg(void *sdst, const void *gbase, long long i0, long long i1,
-                                         unsigned long long *bar) {
-  if (i1 <= i0) return;
-  bulk_g2s(sdst, (const char *)gbase + ((i0 * ES) & ~15ll), seg_bytes<ES>(i0, i1), bar);
-}
-template <int ES>
-__device__ __forceinline__ int seg_shift(long long i0) { return (int)(((i0 * ES) & 15ll) / ES); }
 
 template <int NC, bool UNI>
 __device__ __forceinline__ void tile_issue(const Rows &RL, const double *X, const double *diag0, const double *diag1,
@@ -590,6 +592,172 @@ __device__ __forceinline__ void spmv_tiles(const Csr &C, const Rows &RL, const d
     __syncthreads();  // slot of tile j free
   }
   cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------- SELL-W engine (SCG_ENGINE 2)
+// SELL slices (32 consecutive relabeled rows, column-major slots: coalesced column
+// loads) processed in chunks of kCW rows.  Per chunk one thread issues TMA bulk copies
+// of the chunk's WINDOW of the gathered vector X[wlo, whi) (global ids, wlo = chunk
+// start - kHW), its diagonal(s) and slice metadata, and the chunk's list of
+// out-of-window columns; once those land, the block issues cp.async gathers of the
+// out-of-window entries.  Entry codes (scol): bit 31 sign of a uniform value; bit 30
+// clear: bits 0..29 = column - wlo (window); bit 30 set, bit 29 clear: index into the
+// chunk's out list; bits 30 and 29 set: bits 0..28 = absolute column (list overflow,
+// plain global gather).  Two chunk stages, so the next chunk streams in while this
+// one is computed; only the column stream and the output remain in the compute phase.
+constexpr int kCW = 1024;   // rows per chunk (32 slices)
+#ifndef SCG_HW
+#define SCG_HW 256
+#endif
+constexpr int kHW = SCG_HW;  // window reach beyond the chunk
+constexpr int kExtCap = 1024;
+constexpr int kCS = 2;       // chunk stages
+
+template <int NC>
+struct __align__(16) SellWBuf {
+  double win[kCW + 2 * kHW + 4];
+  double d0[kCW + 4];
+  double d1[NC > 1 ? kCW + 4 : 2];
+  int2 meta[kCW / 32 + 2];
+  int ol[kExtCap + 4];
+  double ext[kExtCap];
+};
+template <int NC>
+struct __align__(16) SellWSmem {
+  SellWBuf<NC> b[kCS];
+  unsigned long long bar[kCS];
+};
+
+struct ChunkGeo {
+  long long wlo, whi;  // window (global ids)
+  int r0, r1;          // rows (local)
+  int s0, s1;          // slices
+  int o0, o1;          // out list
+};
+__device__ __forceinline__ ChunkGeo chunk_geo(const Rows &RL, int k, int nl, long long rb, long long n) {
+  ChunkGeo g;
+  g.r0 = k * kCW;
+  g.r1 = min(nl, g.r0 + kCW);
+  g.s0 = k * (kCW / 32);
+  g.s1 = min(RL.nslice, g.s0 + kCW / 32);
+  g.wlo = rb + g.r0 - kHW;
+  if (g.wlo < 0) g.wlo = 0;
+  g.whi = rb + g.r0 + kCW + kHW;
+  if (g.whi > n) g.whi = n;
+  g.o0 = __ldg(&RL.cout[k]);
+  g.o1 = __ldg(&RL.cout[k + 1]);
+  return g;
+}
+
+template <int NC>
+__device__ __forceinline__ void chunk_issue(const Rows &RL, const double *X, const double *diag0,
+                                            const double *diag1, const ChunkGeo &g, SellWBuf<NC> &b,
+                                            unsigned long long *bar) {
+  uint32_t bytes = seg_bytes<8>(g.wlo, g.whi) + seg_bytes<8>(g.r0, g.r1) + seg_bytes<8>(g.s0, g.s1) +
+                   seg_bytes<4>(g.o0, g.o1);
+  if (NC > 1) bytes += seg_bytes<8>(g.r0, g.r1);
+  mbar_arrive_tx(bar, bytes);
+  bulk_seg<8>(b.win, X, g.wlo, g.whi, bar);
+  bulk_seg<8>(b.d0, diag0, g.r0, g.r1, bar);
+  if (NC > 1) bulk_seg<8>(b.d1, diag1, g.r0, g.r1, bar);
+  bulk_seg<8>(b.meta, RL.meta, g.s0, g.s1, bar);
+  bulk_seg<4>(b.ol, RL.tout, g.o0, g.o1, bar);
+}
+
+template <int NC, bool UNI, class Epi>
+__device__ __forceinline__ void spmv_sellw(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
+                                           const double *__restrict__ diag0, const double *__restrict__ diag1,
+                                           long long rb, int nl, Epi &epi, SellWSmem<NC> &sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const long long n = RL.nglob;
+  const int nch = (nl + kCW - 1) / kCW;
+  const int per = (nch + gridDim.x - 1) / gridDim.x;
+  const int k0 = blockIdx.x * per, k1 = min(nch, k0 + per);
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kCS; ++q) mbar_init(&sm.bar[q], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = 0; q < kCS && k0 + q < k1; ++q)
+      chunk_issue<NC>(RL, X, diag0, diag1, chunk_geo(RL, k0 + q, nl, rb, n), sm.b[q], &sm.bar[q]);
+  {  // long rows (warp per row) while the first chunks stream in
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwg = (gridDim.x * blockDim.x) >> 5;
+    for (int w = gw; w < RL.nlong; w += nwg) {
+      RowOut<NC> o;
+      long_row_chain<NC>(C, RL.longrows[w], X, den, diag0, diag1, rb, o);
+      if (lane == 0) epi(o);
+    }
+  }
+  const double rden = 1.0 / den;
+  for (int k = k0; k < k1; ++k) {
+    const int q = (k - k0) % kCS;
+    SellWBuf<NC> &b = sm.b[q];
+    const ChunkGeo g = chunk_geo(RL, k, nl, rb, n);
+    mbar_wait(&sm.bar[q], (uint32_t)(((k - k0) / kCS) & 1));
+    {  // out-of-window gathers of this chunk
+      const int no = g.o1 - g.o0;
+      const int *op = b.ol + seg_shift<4>(g.o0);
+      for (int t = threadIdx.x; t < no; t += blockDim.x) cp_async8(b.ext + t, X + op[t]);
+      cp_async_commit();
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double *wp = b.win + seg_shift<8>(g.wlo);
+    const double *dp0 = b.d0 + seg_shift<8>(g.r0);
+    const double *dp1 = b.d1 + seg_shift<8>(g.r0);
+    const int2 *mp = b.meta + seg_shift<8>(g.s0);
+    // slices of this chunk: warp w takes s0 + w, s0 + w + nwarp, ...; the columns of the
+    // warp's next slice are loaded while the current one is computed
+    int sl = g.s0 + warp;
+    int cn[kChunk];
+    int2 mn = sl < g.s1 ? mp[sl - g.s0] : make_int2(0, 0);
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) cn[u] = (u < (mn.y & 0xff)) ? __ldg(&RL.scol[mn.x + u * 32 + lane]) : 0;
+    for (; sl < g.s1; sl += nwarp) {
+      const int2 m = mn;
+      int cc[kChunk];
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u) cc[u] = cn[u];
+      const int sn = sl + nwarp;
+      mn = sn < g.s1 ? mp[sn - g.s0] : make_int2(0, 0);
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u) cn[u] = (u < (mn.y & 0xff)) ? __ldg(&RL.scol[mn.x + u * 32 + lane]) : 0;
+      const int width = m.y & 0xff;
+      const int p = sl * 32 + lane;
+      if (p >= nl || lane < (m.y >> 8)) continue;
+      RowOut<NC> o;
+      o.r = p;
+      o.xr = wp[(int)(rb + p - g.wlo)] * rden;
+      o.s[0] = dp0[p - g.r0] * o.xr;
+      if (NC > 1) o.s[NC - 1] = dp1[p - g.r0] * o.xr;
+      for (int j = 0; j < width; ++j) {
+        int c;
+        if (j < kChunk) {
+#pragma unroll
+          for (int u = 0; u < kChunk; ++u)
+            if (u == j) c = cc[u];
+        } else {
+          c = __ldg(&RL.scol[m.x + j * 32 + lane]);
+        }
+        if (c == -1) break;  // padding (rows end at their length)
+        const int v = c & 0x3fffffff;
+        double gv;
+        if (!(c & 0x40000000)) gv = wp[v];
+        else if (!(c & 0x20000000)) gv = b.ext[v];
+        else gv = __ldg(&X[v & 0x1fffffff]);
+        const double mm = UNI ? (c < 0 ? -RL.m0 : RL.m0) : __ldg(&RL.sval[m.x + j * 32 + lane]);
+        const double x = gv * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
+#pragma unroll
+        for (int t = 0; t < NC; ++t) o.s[t] = fma(mm, x, o.s[t]);
+      }
+      epi(o);
+    }
+    __syncthreads();  // chunk buffer free
+    if (threadIdx.x == 0 && k + kCS < k1)
+      chunk_issue<NC>(RL, X, diag0, diag1, chunk_geo(RL, k + kCS, nl, rb, n), sm.b[q], &sm.bar[q]);
+  }
 }
 
 // ---------------------------------------------------------------- block reduction
@@ -893,6 +1061,9 @@ __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_a(Csr C,
 #if SCG_ENGINE == 1
   extern __shared__ __align__(128) unsigned char smraw[];
   spmv_tiles<1, UNI>(C, RL, X, den, d, nullptr, rb, epi, *reinterpret_cast<TileSmem<1, UNI> *>(smraw));
+#elif SCG_ENGINE == 2
+  extern __shared__ __align__(128) unsigned char smraw[];
+  spmv_sellw<1, UNI>(C, RL, X, den, d, nullptr, rb, nl, epi, *reinterpret_cast<SellWSmem<1> *>(smraw));
 #else
   spmv_rows<1, UNI>(C, RL, X, den, d, nullptr, rb, nl, epi);
 #endif
@@ -921,26 +1092,59 @@ __global__ void __launch_bounds__(kBlock, 4) k_lanczos_b(const double *__restric
   xwin_init(acc[0]);
   int err = 0;
   const int stride = gridDim.x * blockDim.x;
-  for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < nl; r0 += 4 * stride) {
-    double av[4], xi[4], xm[4];
+  auto row = [&](int r, double av, double xi, double xm) {
+    const double vi = (xi) * rden;
+    double w = fma(-om, vi, av);
+    if (i >= 2) w = fma(-den, (xm) * rdenm, w);  // rho_{i-1} = rho[i-1] = den
+    gstore(net, Xip1 + rb + r, r, w);
+    xwin_add(acc[0], w * w, err, xb.l[0]);
+  };
+  if ((rb & 1) == 0) {
+    // 16-byte vectors: thread handles row pairs (2p, 2p+1), two pairs in flight
+    const int np = nl >> 1;
+    const double2 *a2 = reinterpret_cast<const double2 *>(a);
+    const double2 *xi2 = reinterpret_cast<const double2 *>(Xi + rb);
+    const double2 *xm2 = reinterpret_cast<const double2 *>(Xim1 ? Xim1 + rb : Xi + rb);
+    for (int p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += 2 * stride) {
+      double2 av[2], xi[2], xm[2];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int r = r0 + u * stride;
-      if (r < nl) {
-        av[u] = a[r];
-        xi[u] = Xi[rb + r];
-        xm[u] = i >= 2 ? Xim1[rb + r] : 0.0;
+      for (int u = 0; u < 2; ++u) {
+        const int p = p0 + u * stride;
+        if (p < np) {
+          av[u] = __ldcs(&a2[p]);  // a is dead after this step: evict first
+          xi[u] = xi2[p];
+          xm[u] = i >= 2 ? xm2[p] : make_double2(0.0, 0.0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int p = p0 + u * stride;
+        if (p < np) {
+          row(2 * p, av[u].x, xi[u].x, xm[u].x);
+          row(2 * p + 1, av[u].y, xi[u].y, xm[u].y);
+        }
       }
     }
+    if ((nl & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      const int r = nl - 1;
+      row(r, a[r], Xi[rb + r], i >= 2 ? Xim1[rb + r] : 0.0);
+    }
+  } else {
+    for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < nl; r0 += 4 * stride) {
+      double av[4], xi[4], xm[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int r = r0 + u * stride;
-      if (r < nl) {
-        const double vi = (xi[u]) * rden;
-        double w = fma(-om, vi, av[u]);
-        if (i >= 2) w = fma(-den, (xm[u]) * rdenm, w);  // rho_{i-1} = rho[i-1] = den
-        gstore(net, Xip1 + rb + r, r, w);
-        xwin_add(acc[0], w * w, err, xb.l[0]);
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + u * stride;
+        if (r < nl) {
+          av[u] = a[r];
+          xi[u] = Xi[rb + r];
+          xm[u] = i >= 2 ? Xim1[rb + r] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + u * stride;
+        if (r < nl) row(r, av[u], xi[u], xm[u]);
       }
     }
   }
@@ -1109,6 +1313,9 @@ __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_c(Csr C,
 #if SCG_ENGINE == 1
   extern __shared__ __align__(128) unsigned char smraw[];
   spmv_tiles<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, epi, *reinterpret_cast<TileSmem<1, UNI> *>(smraw));
+#elif SCG_ENGINE == 2
+  extern __shared__ __align__(128) unsigned char smraw[];
+  spmv_sellw<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, nl, epi, *reinterpret_cast<SellWSmem<1> *>(smraw));
 #else
   spmv_rows<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, nl, epi);
 #endif
@@ -1224,6 +1431,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
 #if SCG_ENGINE == 1
   extern __shared__ __align__(128) unsigned char smraw[];
   spmv_tiles<2, UNI>(C, RL, x, nu, d, cdiag, rb, epi, *reinterpret_cast<TileSmem<2, UNI> *>(smraw));
+#elif SCG_ENGINE == 2
+  extern __shared__ __align__(128) unsigned char smraw[];
+  spmv_sellw<2, UNI>(C, RL, x, nu, d, cdiag, rb, nl, epi, *reinterpret_cast<SellWSmem<2> *>(smraw));
 #else
   spmv_rows<2, UNI>(C, RL, x, nu, d, cdiag, rb, nl, epi);
 #endif
@@ -1500,6 +1710,9 @@ __global__ void __launch_bounds__(kBlock) k_apply_d(Csr C, Rows RL, const double
 #if SCG_ENGINE == 1
   extern __shared__ __align__(128) unsigned char smraw[];
   spmv_tiles<1, UNI>(C, RL, X, 1.0, d, nullptr, rb, epi, *reinterpret_cast<TileSmem<1, UNI> *>(smraw));
+#elif SCG_ENGINE == 2
+  extern __shared__ __align__(128) unsigned char smraw[];
+  spmv_sellw<1, UNI>(C, RL, X, 1.0, d, nullptr, rb, nl, epi, *reinterpret_cast<SellWSmem<1> *>(smraw));
 #else
   spmv_rows<1, UNI>(C, RL, X, 1.0, d, nullptr, rb, nl, epi);
 #endif

@@ -79,7 +79,7 @@ struct Shard {
   unsigned *trp = nullptr;  // tile-staged CSR (SCG_ENGINE 1)
   int *tcol = nullptr;
   double *tval = nullptr;
-  int *tout = nullptr;
+  int *tout = nullptr, *cout = nullptr;
   TileDesc *tdesc = nullptr;
   int ntiles = 0, tile_h = 0;
   long long tile_out = 0;
@@ -231,8 +231,9 @@ void launch(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 block,
   launch_smem(c, cls, bytes, kern, grid, block, 0, args...);
 }
 
-Rows rows_of(const Shard *s) {
+Rows rows_of(const Shard *s, int64_t n) {
   Rows r{};
+  r.nglob = n;
   r.longrows = s->longrows;
   r.nlong = s->nlong;
   r.perm = s->sell_perm;
@@ -248,6 +249,7 @@ Rows rows_of(const Shard *s) {
   r.tval = s->tval;
   r.tout = s->tout;
   r.tdesc = s->tdesc;
+  r.cout = s->cout;
   r.ntiles = s->ntiles;
   return r;
 }
@@ -297,7 +299,7 @@ void free_shard(Shard *s) {
   void *ptrs[] = {s->rp, s->col, s->val, s->wts, s->ldiag, s->cdiag, s->d, s->z, s->y, s->a, s->v, s->G,
                   s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
                   s->sc, s->slots, s->dlog, s->longrows, s->sell_perm, s->sell_col, s->sell_meta, s->sell_val,
-                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tout, s->tdesc, s->orig};
+                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tout, s->tdesc, s->orig, s->cout};
   for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -313,7 +315,7 @@ constexpr int64_t kSortWin = 256;
 void relabel_perm(const int64_t *rp, int64_t nl, std::vector<int> &origloc) {
   origloc.resize((size_t)nl);
   for (int64_t r = 0; r < nl; ++r) origloc[(size_t)r] = (int)r;
-#if SCG_ENGINE == 0
+#if SCG_ENGINE != 1
   for (int64_t w = 0; w < nl; w += kSortWin) {
     const int64_t e = std::min<int64_t>(nl, w + kSortWin);
     std::stable_sort(origloc.begin() + w, origloc.begin() + e,
@@ -610,7 +612,30 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
     std::vector<int> scol;
     std::vector<int2> meta;
     std::vector<double> sval;
+    // engine 2 (SELL-W): entries coded relative to their chunk's window / out list
+    std::vector<int> tout, cout;
+    const int64_t n = c->n, rb = s->rb;
+    int64_t wlo = 0, whi = 0;
+    int ocount = 0;
+    auto code_of = [&](int64_t e) -> int {
+      if (SCG_ENGINE != 2) return enc(e);
+      const int64_t cc = h_col[(size_t)e];
+      int code;
+      if (cc >= wlo && cc < whi) code = (int)(cc - wlo);
+      else if (ocount < kExtCap) { code = 0x40000000 | ocount++; tout.push_back((int)cc); }
+      else code = 0x60000000 | (int)cc;
+      if (uni && h_w[(size_t)e] < 0) code = (int)((unsigned)code | 0x80000000u);
+      return code;
+    };
+    if (SCG_ENGINE == 2 && n >= (1ll << 29)) return fail(c, SCG_EINVAL, "SELL-W: n must be < 2^29");
     for (int64_t q = 0; q < nsl; ++q) {
+      if (SCG_ENGINE == 2 && q % (kCW / 32) == 0) {  // new chunk
+        const int64_t r0 = q * 32;
+        wlo = std::max<int64_t>(0, rb + r0 - kHW);
+        whi = std::min<int64_t>(n, rb + r0 + kCW + kHW);
+        cout.push_back((int)tout.size());
+        ocount = 0;
+      }
       int nskip = 0, width = 0;
       for (int l = 0; l < 32; ++l) {
         const int64_t r = q * 32 + l;
@@ -629,7 +654,7 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
           double vv = 0.0;
           if (l >= nskip && r < nl) {
             const int e = h_rp[(size_t)r] + j;
-            if (e < h_rp[(size_t)r + 1]) { cc = enc(e); vv = valof(e); }
+            if (e < h_rp[(size_t)r + 1]) { cc = code_of(e); vv = valof(e); }
           }
           scol.push_back(cc);
           if (!uni) sval.push_back(vv);
@@ -638,6 +663,16 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
     }
     s->nslice = (int)meta.size();
     s->nwin = 0;
+    if (SCG_ENGINE == 2) {
+      cout.push_back((int)tout.size());
+      s->tile_out = (long long)tout.size();
+      tout.resize(tout.size() + 4, 0);
+      meta.resize(meta.size() + 2, make_int2(0, 0));  // bulk-copy slack
+      if (!alloc((void **)&s->tout, sizeof(int) * tout.size()) || !alloc((void **)&s->cout, sizeof(int) * cout.size()))
+        return fail(c, SCG_ENOMEM, "SELL-W layout");
+      CK(cudaMemcpyAsync(s->tout, tout.data(), sizeof(int) * tout.size(), cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(s->cout, cout.data(), sizeof(int) * cout.size(), cudaMemcpyHostToDevice, st));
+    }
     if (!alloc((void **)&s->sell_meta, sizeof(int2) * meta.size()) ||
         !alloc((void **)&s->sell_col, sizeof(int) * scol.size()) ||
         (!uni && !alloc((void **)&s->sell_val, sizeof(double) * sval.size())))
@@ -649,7 +684,13 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
     CK(cudaStreamSynchronize(st));
     s->sell_slots = (double)scol.size();
     matbytes = s->sell_slots * (uni ? 4.0 : 12.0) + 8.0 * s->nslice;
+#if SCG_ENGINE == 2
+    matbytes += 4.0 * (double)s->tile_out + 4.0 * (double)((nl + kCW - 1) / kCW);
+    s->smem1 = sizeof(SellWSmem<1>);
+    s->smem2 = sizeof(SellWSmem<2>);
+#else
     s->smem1 = s->smem2 = 0;
+#endif
   }
 #endif
   {  // grids of the SpMV kernels
@@ -674,8 +715,9 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<false>, kBlock, s->smem1);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<false>, kBlock, s->smem2);
     }
-    const int need = SCG_ENGINE == 1 ? std::max(s->ntiles, (s->nlong + 7) / 8)
-                                     : (int)std::max<int64_t>((s->nslice + 7) / 8, (s->nlong + 7) / 8);
+    const int need = SCG_ENGINE == 1   ? std::max(s->ntiles, (s->nlong + 7) / 8)
+                     : SCG_ENGINE == 2 ? (int)std::max<int64_t>((nl + kCW - 1) / kCW, (s->nlong + 7) / 8)
+                                       : (int)std::max<int64_t>((s->nslice + 7) / 8, (s->nlong + 7) / 8);
     s->grid_tiles = std::max(1, std::min(need, std::max(1, oa) * c->nsm));
     s->grid_mon = std::max(1, std::min(need, std::max(1, om) * c->nsm));
     if (std::getenv("SCG_DEBUG"))
@@ -1106,7 +1148,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       unsigned long long E = ++c->epoch;
       for (Shard *s : c->sh) {
         Csr C{s->rp, s->col, s->val};
-        Rows TT = rows_of(s);
+        Rows TT = rows_of(s, c->n);
         auto kA = s->sell_uniform ? k_lanczos_a<true> : k_lanczos_a<false>;
         launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->grid_tiles), dim3(kBlock), s->smem1, C, TT,
                (const double *)s->d, (const double *)slot(s, i), (int)s->nl, (long long)s->rb, i, s->a,
@@ -1140,7 +1182,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
         const unsigned long long E = ++c->epoch;
         for (Shard *s : c->sh) {
           Csr C{s->rp, s->col, s->val};
-          Rows TT = rows_of(s);
+          Rows TT = rows_of(s, c->n);
           auto kC = s->sell_uniform ? k_lanczos_c<true> : k_lanczos_c<false>;
           const double *Xjm1 = (j == 1) ? nullptr : slot(s, j - 1);
           launch_smem(c, KC_LANCZOS_C, s->kb[KC_LANCZOS_C], kC, dim3(s->grid_tiles), dim3(kBlock), s->smem1, C, TT,
@@ -1162,7 +1204,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     unsigned long long E = ++c->epoch;
     for (Shard *s : c->sh) {
       Csr C{s->rp, s->col, s->val};
-      Rows TT = rows_of(s);
+      Rows TT = rows_of(s, c->n);
       auto kM = s->sell_uniform ? k_monitor<true> : k_monitor<false>;
       launch_smem(c, KC_MONITOR, s->kb[KC_MONITOR], kM, dim3(s->grid_mon), dim3(kBlock), s->smem2, C, TT, (const double *)s->d,
              (const double *)s->cdiag, (const double *)c->xg(s), s->v, (int)s->nl, (long long)s->rb,
@@ -1265,7 +1307,7 @@ scg_status sketchycgal_apply_D(scg_ctx *c, const double *xh, double *yh) {
   for (Shard *s : c->sh) {
     CK(cudaMalloc(&dy, sizeof(double) * std::max<int64_t>(1, s->nl)));
     Csr C{s->rp, s->col, s->val};
-    Rows TT = rows_of(s);
+    Rows TT = rows_of(s, c->n);
     launch_smem(c, KC_OTHER, 0.0, s->sell_uniform ? k_apply_d<true> : k_apply_d<false>, dim3(s->grid_tiles), dim3(kBlock), s->smem1,
            C, TT, (const double *)s->d, (const double *)dx, (int)s->nl, (long long)s->rb, dy);
     CK(cudaStreamSynchronize(c->stream));
