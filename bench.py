@@ -256,7 +256,11 @@ def run_e2e(scg, si, L, c, K, W, dev, dkw, world):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     s = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], device=dev, **dkw)
+    s.synchronize()
+    ti = time.perf_counter()
     s.step(W + K)
+    s.synchronize()
+    ts = time.perf_counter()
     lg = s.iter_log()
     U, lam, _ = s.reconstruct()
     s.synchronize()
@@ -273,6 +277,7 @@ def run_e2e(scg, si, L, c, K, W, dev, dkw, world):
     d2h = lg.nbytes + U.nbytes + lam.nbytes
     return {"value": (W + K) / secs, "unit": "iterations/s", "h2d_bytes_per_step": h2d / (W + K),
             "d2h_bytes_per_step": d2h / (W + K), "seconds": secs,
+            "breakdown_s": {"init": round(ti - t0, 3), "steps": round(ts - ti, 3), "outputs": round(t1 - ts, 3)},
             "note": "pageable numpy CSR (this rank's rows) copied inside init; t=1..W+K; includes host CSR "
                     "split, SELL layout and Omega draw; per-rank bytes"}
 

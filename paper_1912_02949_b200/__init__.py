@@ -46,7 +46,7 @@ def _nccl_paths():
 
 def nvcc_cmd(out: str, defines=()) -> list[str]:
     cmd = ["nvcc", *[f"-D{d}" for d in defines], "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
-           "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+           "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp", "-shared", "-cudart", "static", "-lgomp",
            os.path.join(_HERE, "csrc", "sketchycgal.cu"), "-o", out]
     inc, lib = _nccl_paths()
     if inc:

@@ -1524,18 +1524,18 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
   }
 }
 
-// y <- y + gamma (z - b) (Alg. 4 line 9); d for t+1; S <- (1-eta) S + eta alpha v g^T
-// (Alg. 4 line 10); next start vector g_{t+1} and ||g_{t+1}||^2 (exact).
+// y <- y + gamma (z - b) (Alg. 4 line 9); d for t+1; next start vector g_{t+1} and
+// ||g_{t+1}||^2 (exact).  The sketch update of Alg. 4 line 10 is deferred (k_sketch_flush):
+// this kernel records its coefficients ck = fl(eta alpha) g_k in the ring slot js.
 __global__ void __launch_bounds__(kBlock, 3) k_dual_sketch(const double *__restrict__ z, double *__restrict__ y,
                                                         double *__restrict__ d, const double *__restrict__ cdiag,
-                                                        const double *__restrict__ v, double *__restrict__ S,
+                                                        double *__restrict__ ckr, int js,
                                                         double *__restrict__ g, int nl, long long rb, int R,
                                                         IterArgs A, uint64_t seed, XSlot *slot, DevScalars *sc,
                                                         Net net, const int *__restrict__ orig) {
-  __shared__ double ck[kMaxR];
   const double gam = sc->gamma;
-  if (threadIdx.x < R) ck[threadIdx.x] = (A.eta * A.alpha) * sc->gk[threadIdx.x];
-  __syncthreads();
+  if (blockIdx.x == 0 && (int)threadIdx.x < R)
+    ckr[js * kMaxR + threadIdx.x] = (A.eta * A.alpha) * sc->gk[threadIdx.x];
   __shared__ XBlk<1> xb;
   xblk_init<1>(xb);
   XWin acc[1];
@@ -1543,11 +1543,12 @@ __global__ void __launch_bounds__(kBlock, 3) k_dual_sketch(const double *__restr
   int err = 0;
   const int stride = gridDim.x * blockDim.x;
   for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < nl; r0 += 2 * stride) {
-    double zr[2], yv[2], cd[2], vr[2];
+    double zr[2], yv[2], cd[2];
+    int og[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int r = r0 + u * stride;
-      if (r < nl) { zr[u] = z[r]; yv[u] = y[r]; cd[u] = cdiag[r]; vr[u] = v[r]; }
+      if (r < nl) { zr[u] = z[r]; yv[u] = y[r]; cd[u] = cdiag[r]; og[u] = orig[r]; }
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -1557,30 +1558,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_dual_sketch(const double *__restr
         const double yr = fma(gam, e, yv[u]);
         y[r] = yr;
         d[r] = fma(A.beta_next, e, yr) + cd[u];
-      }
-    }
-    for (int kc = 0; kc < R; kc += 8) {
-      double sv[2][8];
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int r = r0 + u * stride;
-          if (r < nl && kc + k < R) sv[u][k] = S[(long long)(kc + k) * nl + r];
-        }
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int r = r0 + u * stride;
-          if (r < nl && kc + k < R) S[(long long)(kc + k) * nl + r] = fma(ck[kc + k], vr[u], A.one_m_eta * sv[u][k]);
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int r = r0 + u * stride;
-      if (r < nl) {
-        const double gv = scg_lanczos_start(seed, A.t + 1, rb + orig[r]);
+        const double gv = scg_lanczos_start(seed, A.t + 1, rb + og[u]);
         gstore(net, g + rb + r, r, gv);
         xwin_add(acc[0], gv * gv, err, xb.l[0]);
       }
@@ -1588,6 +1566,46 @@ __global__ void __launch_bounds__(kBlock, 3) k_dual_sketch(const double *__restr
   }
   if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
     emit<1>(slot, sc, net, FK_RHO0, FinArgs{}, nullptr);
+}
+
+// Deferred sketch updates (Alg. 4 line 10, eqn:sketch-update PAPER.md:1162-1169): S is
+// write-only between reconstructions, so the last nb rank-one updates
+//   S <- (1 - eta_j) S + (eta_j alpha) v_j g_j^T,   j = 0 .. nb-1 in iteration order,
+// are applied in one pass over S, element by element in registers with exactly the
+// per-iteration operations fma(ck_j[k], v_j[r], fl((1 - eta_j) S[r, k])): bitwise the
+// S of one update per iteration, with one read and one write of S per nb iterations.
+constexpr int kSketchB = 16;
+struct FlushArgs {
+  int nb;
+  double ome[kSketchB];  // 1 - eta_j
+};
+__global__ void __launch_bounds__(kBlock) k_sketch_flush(double *__restrict__ S, const double *__restrict__ V,
+                                                         long long ldv, const double *__restrict__ ckr, FlushArgs F,
+                                                         int nl, int R) {
+  __shared__ double ck[kSketchB][kMaxR];
+  for (int e = threadIdx.x; e < F.nb * kMaxR; e += blockDim.x) ck[e / kMaxR][e % kMaxR] = ckr[e];
+  __syncthreads();
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    double vj[kSketchB];
+#pragma unroll
+    for (int j = 0; j < kSketchB; ++j) vj[j] = j < F.nb ? __ldcs(&V[(long long)j * ldv + r]) : 0.0;
+    for (int k0 = 0; k0 < R; k0 += 4) {
+      double sv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k0 + k < R) sv[k] = S[(long long)(k0 + k) * nl + r];
+#pragma unroll
+      for (int j = 0; j < kSketchB; ++j)
+        if (j < F.nb) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k0 + k < R) sv[k] = fma(ck[j][k0 + k], vj[j], F.ome[j] * sv[k]);
+        }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k0 + k < R) S[(long long)(k0 + k) * nl + r] = sv[k];
+    }
+  }
 }
 
 // ---------------------------------------------------------------- one-shot kernels

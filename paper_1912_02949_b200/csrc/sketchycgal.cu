@@ -13,8 +13,10 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a --fmad=false -O3 -lineinfo
 // (--fmad=false is part of the arithmetic contract: no contraction of a*b+c).
 #include <cuda_runtime.h>
+#include <omp.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -37,11 +39,11 @@ namespace {
 
 enum KClass {
   KC_LANCZOS_A = 0, KC_LANCZOS_B, KC_TRIDIAG, KC_LANCZOS_C, KC_NORM_X, KC_COMBINE, KC_MONITOR, KC_PRIMAL,
-  KC_DUAL_SKETCH, KC_PULL, KC_OTHER, KC_COUNT
+  KC_DUAL_SKETCH, KC_SKETCH, KC_PULL, KC_OTHER, KC_COUNT
 };
 const char *kKClassName[KC_COUNT] = {"lanczos_a_spmv_dot", "lanczos_b_axpy_norm", "tridiag_mineig",
                                      "lanczos_c_spmv_regen", "norm_x", "combine_stored", "monitor_spmv",
-                                     "primal_z_gpart", "dual_sketch_next_g", "pull_collective", "other"};
+                                     "primal_z_gpart", "dual_next_g", "sketch_flush", "pull_collective", "other"};
 
 struct EvPair {
   cudaEvent_t a, b;
@@ -60,6 +62,7 @@ struct Shard {
   int *rp = nullptr, *col = nullptr;
   double *val = nullptr, *wts = nullptr, *ldiag = nullptr, *cdiag = nullptr;
   double *d = nullptr, *z = nullptr, *y = nullptr, *a = nullptr, *v = nullptr;
+  double *V = nullptr, *ckr = nullptr;  // deferred sketch updates: ring of kSketchB eigenvectors + coefficients
   double *G = nullptr;  // gathered region: [x | W slot 0 (= g) | W slot 1 | ...], each npad long
   double *S = nullptr, *Om = nullptr, *gpart = nullptr;
   double *U = nullptr, *tmp1 = nullptr, *tmp2 = nullptr, *dmat = nullptr, *partial = nullptr, *dlam = nullptr;
@@ -87,6 +90,8 @@ struct Shard {
   // row relabeling (SELL engine): local row nu holds input row rb + origloc[nu]
   std::vector<int> origloc;
   int *orig = nullptr;            // device copy of origloc
+  std::vector<int> h_rp, h_col;   // host CSR (device labels) kept from build_shard to build_layout
+  std::vector<double> h_w;
   // sharding
   unsigned char *mask = nullptr;  // device [nl], nullptr when world == 1
   Mailbox *mb = nullptr;
@@ -128,6 +133,10 @@ struct scg_ctx {
   // regenerate mode: slots 1, 2 = ring of w_i
   int wcap = 0;
   bool store = true;
+  // deferred sketch updates (k_sketch_flush): iterations pending, their 1 - eta, last v slot
+  int spend = 0, vlast = 0;
+  double ome[kSketchB] = {0};
+  double *vslot(const Shard *s, int j) const { return s->V + (long long)j * s->nlpad; }
   // reconstruction
   bool have_recon = false;
   std::vector<double> lam_raw, lam_orig, lam_tc, err;
@@ -299,7 +308,7 @@ void free_shard(Shard *s) {
   void *ptrs[] = {s->rp, s->col, s->val, s->wts, s->ldiag, s->cdiag, s->d, s->z, s->y, s->a, s->v, s->G,
                   s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
                   s->sc, s->slots, s->dlog, s->longrows, s->sell_perm, s->sell_col, s->sell_meta, s->sell_val,
-                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tout, s->tdesc, s->orig, s->cout};
+                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tout, s->tdesc, s->orig, s->cout, s->V, s->ckr};
   for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -316,6 +325,7 @@ void relabel_perm(const int64_t *rp, int64_t nl, std::vector<int> &origloc) {
   origloc.resize((size_t)nl);
   for (int64_t r = 0; r < nl; ++r) origloc[(size_t)r] = (int)r;
 #if SCG_ENGINE != 1
+#pragma omp parallel for schedule(static, 64)
   for (int64_t w = 0; w < nl; w += kSortWin) {
     const int64_t e = std::min<int64_t>(nl, w + kSortWin);
     std::stable_sort(origloc.begin() + w, origloc.begin() + e,
@@ -329,6 +339,7 @@ scg_status build_gmap(scg_ctx *c) {
   c->gmap.assign((size_t)c->n, 0);
   if (c->mode != 2) {
     for (Shard *s : c->sh)
+#pragma omp parallel for schedule(static, 65536)
       for (int64_t nu = 0; nu < s->nl; ++nu) c->gmap[(size_t)(s->rb + s->origloc[(size_t)nu])] = (int)(s->rb + nu);
     return SCG_OK;
   }
@@ -361,15 +372,21 @@ scg_status build_gmap(scg_ctx *c) {
 // CSR checks of one shard's rows (before any device work).
 scg_status validate_rows(scg_ctx *c, const int64_t *rp, const int32_t *colp, const double *valp, int64_t nl) {
   const int64_t base = rp[0];
+  int bad = 0;  // 1 monotone, 2 range, 4 order, 8 finite
+#pragma omp parallel for schedule(static, 4096) reduction(| : bad)
   for (int64_t r = 0; r < nl; ++r) {
-    if (rp[r + 1] < rp[r]) return fail(c, SCG_EINVAL, "row_ptr not monotone");
+    if (rp[r + 1] < rp[r]) { bad |= 1; continue; }
     for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
       const int32_t cc = colp[k - base];
-      if (cc < 0 || cc >= c->n) return fail(c, SCG_EINVAL, "column out of range");
-      if (k > rp[r] && cc <= colp[k - 1 - base]) return fail(c, SCG_EINVAL, "columns not strictly ascending");
-      if (!std::isfinite(valp[k - base])) return fail(c, SCG_EINVAL, "non-finite value");
+      if (cc < 0 || cc >= c->n) bad |= 2;
+      if (k > rp[r] && cc <= colp[k - 1 - base]) bad |= 4;
+      if (!std::isfinite(valp[k - base])) bad |= 8;
     }
   }
+  if (bad & 1) return fail(c, SCG_EINVAL, "row_ptr not monotone");
+  if (bad & 2) return fail(c, SCG_EINVAL, "column out of range");
+  if (bad & 4) return fail(c, SCG_EINVAL, "columns not strictly ascending");
+  if (bad & 8) return fail(c, SCG_EINVAL, "non-finite value");
   return SCG_OK;
 }
 
@@ -382,22 +399,36 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   const int64_t nl = s->nl, rb = s->rb;
   const int R = c->R;
   const int64_t base = rp[0];
-  std::vector<int> h_rp((size_t)nl + 1);
-  int64_t cnt_off = 0;
-  for (int64_t r = 0; r < nl; ++r)
-    for (int64_t k = rp[r]; k < rp[r + 1]; ++k)
-      if (colp[k - base] != r + rb) cnt_off++;
-  if (cnt_off >= (1ll << 31)) return fail(c, SCG_EINVAL, "too many nonzeros for int32 row pointers");
-  std::vector<int> h_col((size_t)cnt_off);
-  std::vector<double> h_w((size_t)cnt_off), h_diag((size_t)nl, 0.0);
-  std::vector<unsigned char> h_mask;
-  if (c->world > 1) h_mask.assign((size_t)nl, 0);
-  int64_t o = 0;
   // device row nu is input row r = origloc[nu]; its entries stay in the input (ascending
-  // input column) order -- the CAC-3 chain order -- with columns relabeled by gmap
+  // input column) order -- the CAC-3 chain order -- with columns relabeled by gmap.
+  // Two parallel passes: count off-diagonal entries per row, then fill.
+  std::vector<int> &h_rp = s->h_rp;
+  h_rp.assign((size_t)nl + 1, 0);
+#pragma omp parallel for schedule(static, 4096)
   for (int64_t nu = 0; nu < nl; ++nu) {
     const int64_t r = s->origloc[(size_t)nu];
-    h_rp[(size_t)nu] = (int)o;
+    int cnt = 0;
+    for (int64_t k = rp[r]; k < rp[r + 1]; ++k) cnt += colp[k - base] != r + rb;
+    h_rp[(size_t)nu + 1] = cnt;
+  }
+  int64_t cnt_off = 0;
+  for (int64_t nu = 0; nu < nl; ++nu) {
+    cnt_off += h_rp[(size_t)nu + 1];
+    if (cnt_off >= (1ll << 31)) return fail(c, SCG_EINVAL, "too many nonzeros for int32 row pointers");
+    h_rp[(size_t)nu + 1] = (int)cnt_off;
+  }
+  std::vector<int> &h_col = s->h_col;
+  std::vector<double> &h_w = s->h_w;
+  h_col.resize((size_t)cnt_off);
+  h_w.resize((size_t)cnt_off);
+  std::vector<double> h_diag((size_t)nl, 0.0);
+  std::vector<unsigned char> h_mask;
+  if (c->world > 1) h_mask.assign((size_t)nl, 0);
+  long long halo = 0;
+#pragma omp parallel for schedule(static, 4096) reduction(+ : halo)
+  for (int64_t nu = 0; nu < nl; ++nu) {
+    const int64_t r = s->origloc[(size_t)nu];
+    int64_t o = h_rp[(size_t)nu];
     double dsum = 0.0;
     bool had = false;
     unsigned m = 0;
@@ -420,10 +451,10 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
     if (!has_diagonal || !had) h_diag[(size_t)nu] = has_diagonal ? 0.0 : dsum;
     if (c->world > 1) {
       h_mask[(size_t)nu] = (unsigned char)m;
-      s->halo_rows += m != 0;
+      halo += m != 0;
     }
   }
-  h_rp[(size_t)nl] = (int)o;
+  s->halo_rows = halo;
   s->nnz_off = cnt_off;
   std::vector<int> h_long;
   for (int64_t r = 0; r < nl; ++r)
@@ -440,7 +471,8 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
             alloc((void **)&s->val, sizeof(double) * cnt_off) && alloc((void **)&s->wts, sizeof(double) * cnt_off) &&
             alloc((void **)&s->ldiag, nlb) && alloc((void **)&s->cdiag, nlb) && alloc((void **)&s->d, nlb) &&
             alloc((void **)&s->z, nlb) && alloc((void **)&s->y, nlb) && alloc((void **)&s->a, nlb) &&
-            alloc((void **)&s->v, nlb) && alloc((void **)&s->S, nlb * R) && alloc((void **)&s->Om, nlb * R) &&
+            alloc((void **)&s->V, nlb * kSketchB) && alloc((void **)&s->ckr, sizeof(double) * kSketchB * kMaxR) &&
+            alloc((void **)&s->S, nlb * R) && alloc((void **)&s->Om, nlb * R) &&
             alloc((void **)&s->sc, sizeof(DevScalars)) && alloc((void **)&s->slots, sizeof(XSlot) * SLOT_COUNT) &&
             alloc((void **)&s->dscalar, sizeof(double) * 8) &&
             alloc((void **)&s->dlog, sizeof(scg_iter_rec) * c->log_cap) &&
@@ -493,17 +525,15 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
 scg_status build_layout(scg_ctx *c, Shard *s) {
   const int64_t nl = s->nl;
   const bool scale = (c->flags & SCG_SCALE) != 0;
-  std::vector<int> h_rp((size_t)nl + 1), h_col((size_t)s->nnz_off);
-  std::vector<double> h_w((size_t)s->nnz_off);
+  const std::vector<int> &h_rp = s->h_rp, &h_col = s->h_col;
+  const std::vector<double> &h_w = s->h_w;
   cudaStream_t st = c->stream;
-  CK(cudaMemcpyAsync(h_rp.data(), s->rp, sizeof(int) * (nl + 1), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(h_col.data(), s->col, sizeof(int) * s->nnz_off, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(h_w.data(), s->wts, sizeof(double) * s->nnz_off, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
   const long long cnt_off = s->nnz_off;
-  bool uni = cnt_off > 0;  // all |w| equal: values are encoded in the column's sign bit
   const double w0 = cnt_off > 0 ? std::fabs(h_w[0]) : 0.0;
-  for (int64_t k = 0; k < cnt_off && uni; ++k) uni = std::fabs(h_w[(size_t)k]) == w0;
+  int nonuni = 0;
+#pragma omp parallel for schedule(static, 65536) reduction(| : nonuni)
+  for (int64_t k = 0; k < cnt_off; ++k) nonuni |= std::fabs(h_w[(size_t)k]) != w0;
+  const bool uni = cnt_off > 0 && !nonuni;  // all |w| equal: values are encoded in the column's sign bit
   s->sell_m0 = scale ? w0 / c->nrmL : w0;  // |C_rj| = fl(|w| / ||L||_F)
   s->sell_uniform = uni;
   auto alloc = [&](void **p, size_t bytes) -> bool { return cudaMalloc(p, bytes ? bytes : 8) == cudaSuccess; };
@@ -628,38 +658,63 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
       return code;
     };
     if (SCG_ENGINE == 2 && n >= (1ll << 29)) return fail(c, SCG_EINVAL, "SELL-W: n must be < 2^29");
+    // pass 1 (parallel): slice widths and leading long lanes; slot bases by prefix sum
+    std::vector<int> swid((size_t)nsl), sskip((size_t)nsl);
+    int badlong = 0;
+#pragma omp parallel for schedule(static, 1024) reduction(| : badlong)
     for (int64_t q = 0; q < nsl; ++q) {
-      if (SCG_ENGINE == 2 && q % (kCW / 32) == 0) {  // new chunk
-        const int64_t r0 = q * 32;
-        wlo = std::max<int64_t>(0, rb + r0 - kHW);
-        whi = std::min<int64_t>(n, rb + r0 + kCW + kHW);
-        cout.push_back((int)tout.size());
-        ocount = 0;
-      }
       int nskip = 0, width = 0;
       for (int l = 0; l < 32; ++l) {
         const int64_t r = q * 32 + l;
         if (r >= nl) break;
         const int len = h_rp[(size_t)r + 1] - h_rp[(size_t)r];
         if (len > kLongRow) {
-          if (nskip != l) return fail(c, SCG_EINVAL, "SELL: long rows must lead their slice");
+          if (nskip != l) badlong = 1;
           nskip = l + 1;
         } else width = std::max(width, len);
       }
-      meta.push_back(make_int2((int)scol.size(), width | (nskip << 8)));
+      swid[(size_t)q] = width;
+      sskip[(size_t)q] = nskip;
+    }
+    if (badlong) return fail(c, SCG_EINVAL, "SELL: long rows must lead their slice");
+    meta.resize((size_t)nsl);
+    size_t slots = 0;
+    for (int64_t q = 0; q < nsl; ++q) {
+      meta[(size_t)q] = make_int2((int)slots, swid[(size_t)q] | (sskip[(size_t)q] << 8));
+      slots += (size_t)swid[(size_t)q] * 32;
+      if (slots >= (size_t)INT32_MAX) return fail(c, SCG_EINVAL, "SELL layout too large");
+    }
+    scol.assign(slots, -1);
+    if (!uni) sval.assign(slots, 0.0);
+    // pass 2: fill the slots (parallel; serial for engine 2, whose out lists grow per chunk)
+    auto fill = [&](int64_t q) {
+      const int width = swid[(size_t)q], nskip = sskip[(size_t)q];
+      const size_t b0 = (size_t)meta[(size_t)q].x;
       for (int j = 0; j < width; ++j)
-        for (int l = 0; l < 32; ++l) {
+        for (int l = nskip; l < 32; ++l) {
           const int64_t r = q * 32 + l;
-          int cc = -1;
-          double vv = 0.0;
-          if (l >= nskip && r < nl) {
-            const int e = h_rp[(size_t)r] + j;
-            if (e < h_rp[(size_t)r + 1]) { cc = code_of(e); vv = valof(e); }
+          if (r >= nl) break;
+          const int e = h_rp[(size_t)r] + j;
+          if (e < h_rp[(size_t)r + 1]) {
+            scol[b0 + (size_t)j * 32 + l] = code_of(e);
+            if (!uni) sval[b0 + (size_t)j * 32 + l] = valof(e);
           }
-          scol.push_back(cc);
-          if (!uni) sval.push_back(vv);
         }
-      if (scol.size() >= (size_t)INT32_MAX) return fail(c, SCG_EINVAL, "SELL layout too large");
+    };
+    if (SCG_ENGINE == 2) {
+      for (int64_t q = 0; q < nsl; ++q) {
+        if (q % (kCW / 32) == 0) {  // new chunk
+          const int64_t r0 = q * 32;
+          wlo = std::max<int64_t>(0, rb + r0 - kHW);
+          whi = std::min<int64_t>(n, rb + r0 + kCW + kHW);
+          cout.push_back((int)tout.size());
+          ocount = 0;
+        }
+        fill(q);
+      }
+    } else {
+#pragma omp parallel for schedule(static, 1024)
+      for (int64_t q = 0; q < nsl; ++q) fill(q);
     }
     s->nslice = (int)meta.size();
     s->nwin = 0;
@@ -735,7 +790,9 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
   s->kb[KC_NORM_X] = 8.0 * NL;
   s->kb[KC_MONITOR] = mat + 16.0 * NL + 8.0 * gath + 8.0 * NL;
   s->kb[KC_PRIMAL] = 24.0 * NL + 8.0 * NL * c->R;
-  s->kb[KC_DUAL_SKETCH] = 56.0 * NL + 16.0 * NL * c->R;
+  s->kb[KC_DUAL_SKETCH] = 60.0 * NL;  // z, y, cdiag, orig read; y, d, g written
+  std::vector<int>().swap(s->h_col);  // host copies no longer needed
+  std::vector<double>().swap(s->h_w);
   return SCG_OK;
 }
 
@@ -846,6 +903,19 @@ scg_status balanced_splits(const int64_t *rp, int64_t n, int world, std::vector<
   return SCG_OK;
 }
 
+// Apply the pending rank-one sketch updates (k_sketch_flush) on every shard.
+void sketch_flush(scg_ctx *c) {
+  if (c->spend == 0) return;
+  FlushArgs F{};
+  F.nb = c->spend;
+  for (int j = 0; j < c->spend; ++j) F.ome[j] = c->ome[j];
+  for (Shard *s : c->sh)
+    launch(c, KC_SKETCH, 8.0 * F.nb * (double)s->nl + 16.0 * c->R * (double)s->nl, k_sketch_flush,
+           dim3(s->grid_dual), dim3(kBlock), s->S, (const double *)s->V, (long long)s->nlpad,
+           (const double *)s->ckr, F, (int)s->nl, c->R);
+  c->spend = 0;
+}
+
 }  // namespace
 
 // ================================================================ C ABI
@@ -939,6 +1009,14 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
     return st;
   };
   if (!L || !L->row_ptr || !L->col_idx || !L->val) return bad(SCG_EINVAL);
+  const bool dbg = std::getenv("SCG_DEBUG") != nullptr;
+  auto t_0 = std::chrono::steady_clock::now();
+  auto tick = [&](const char *what) {
+    if (!dbg) return;
+    const auto t_1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[scg] init %-14s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t_1 - t_0).count());
+    t_0 = t_1;
+  };
   const int64_t n = L->n_global;
   if (n < 2 || R < 1 || R > n || R > kMaxR || !(alpha > 0) || !(beta0 > 0) || !std::isfinite(alpha) ||
       !std::isfinite(beta0))
@@ -1019,13 +1097,16 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
     const int64_t off = c->mode == 2 ? 0 : s->rb;  // index of this shard's first row in L->row_ptr
     relabel_perm(L->row_ptr + off, s->nl, s->origloc);
   }
+  tick("device+relabel");
   if ((st = build_gmap(c))) return bad(st);
+  tick("gmap");
   for (Shard *s : c->sh) {
     const int64_t off = c->mode == 2 ? 0 : s->rb;
     if ((st = build_shard(c, s, L->row_ptr + off, L->col_idx + L->row_ptr[off], L->val + L->row_ptr[off],
                           L->has_diagonal)))
       return bad(st);
   }
+  tick("shards");
   // Lanczos vector storage.  One rank: grown on demand.  Sharded: fixed at init (peers map it).
   c->store = (flags & SCG_REGENERATE) == 0;
   int cap = 3;
@@ -1066,6 +1147,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   }
   c->nrmL = std::sqrt(c->nrmL);
   if (!(c->nrmL > 0) || !std::isfinite(c->nrmL)) return bad(SCG_EINVAL);
+  tick("G+peers+frob");
   for (Shard *s : c->sh) {
     if ((st = build_layout(c, s))) return bad(st);
     if (cudaMemcpyAsync(s->dscalar, &c->nrmL, sizeof(double), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
@@ -1085,6 +1167,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
            (long long)s->rb, seed, (long long)1, s->slots + SLOT_NU0, s->sc, net_of(c, s, E1), (const int *)s->orig);
   pull_all(c, FK_RHO0, 1, E1, FinArgs{});
   if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) return bad(SCG_ECUDA);
+  tick("layout+omega");
   for (int k = 0; k < KC_COUNT; ++k) { c->kl[k] = 0; c->kms[k] = 0; c->kbytes_sum[k] = 0; }
   c->launches = 0;
   *out = c;
@@ -1201,19 +1284,20 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       pull_all(c, FK_NUX, 1, E, FinArgs{});
     }
     // ---- monitors, primal, dual, sketch (Alg. 4 lines 8-10)
+    const int js = c->spend;  // ring slot of this iteration's v
     unsigned long long E = ++c->epoch;
     for (Shard *s : c->sh) {
       Csr C{s->rp, s->col, s->val};
       Rows TT = rows_of(s, c->n);
       auto kM = s->sell_uniform ? k_monitor<true> : k_monitor<false>;
       launch_smem(c, KC_MONITOR, s->kb[KC_MONITOR], kM, dim3(s->grid_mon), dim3(kBlock), s->smem2, C, TT, (const double *)s->d,
-             (const double *)s->cdiag, (const double *)c->xg(s), s->v, (int)s->nl, (long long)s->rb,
+             (const double *)s->cdiag, (const double *)c->xg(s), c->vslot(s, js), (int)s->nl, (long long)s->rb,
              s->slots + SLOT_MON, s->sc, net_of(c, s, E));
     }
     pull_all(c, FK_MON, 3, E, FinArgs{});
     E = ++c->epoch;
     for (Shard *s : c->sh)
-      launch(c, KC_PRIMAL, s->kb[KC_PRIMAL], k_primal, dim3(s->grid_primal), dim3(kBlock), (const double *)s->v, s->z,
+      launch(c, KC_PRIMAL, s->kb[KC_PRIMAL], k_primal, dim3(s->grid_primal), dim3(kBlock), (const double *)c->vslot(s, js), s->z,
              (const double *)s->Om, (int)s->nl, c->R, A, s->gpart, s->slots + SLOT_NZ, s->sc, s->dlog, net_of(c, s, E));
     {
       FinArgs f{};
@@ -1224,10 +1308,13 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     E = ++c->epoch;
     for (Shard *s : c->sh)
       launch(c, KC_DUAL_SKETCH, s->kb[KC_DUAL_SKETCH], k_dual_sketch, dim3(s->grid_dual), dim3(kBlock),
-             (const double *)s->z, s->y, s->d, (const double *)s->cdiag, (const double *)s->v, s->S, c->wslot(s, 0),
+             (const double *)s->z, s->y, s->d, (const double *)s->cdiag, s->ckr, js, c->wslot(s, 0),
              (int)s->nl, (long long)s->rb, c->R, A, c->seed, s->slots + SLOT_NU0, s->sc, net_of(c, s, E),
              (const int *)s->orig);
     pull_all(c, FK_RHO0, 1, E, FinArgs{});
+    c->ome[js] = A.one_m_eta;
+    c->vlast = js;
+    if (++c->spend == kSketchB) sketch_flush(c);
     c->t = t;
   }
   CK(cudaGetLastError());
@@ -1267,6 +1354,8 @@ static scg_status fetch_rows(scg_ctx *c, const Shard *s, const double *dsrc, dou
 
 scg_status sketchycgal_get_state(scg_ctx *c, int32_t which, double *out) {
   if (!c || !out) return SCG_EINVAL;
+  if (c->failed) return SCG_ESTATE;
+  if (which == 2) sketch_flush(c);
   scg_status st = sketchycgal_synchronize(c);
   if (st) return st;
   const int64_t NL = c->nl_total();
@@ -1279,7 +1368,7 @@ scg_status sketchycgal_get_state(scg_ctx *c, int32_t which, double *out) {
       case 1: src = s->y; break;
       case 2: src = s->S; mat = true; break;
       case 3: src = s->Om; mat = true; break;
-      case 4: src = s->v; break;
+      case 4: src = c->vslot(s, c->vlast); break;
       case 5: src = s->d; break;
       case 6: src = s->cdiag; break;
       default: return SCG_EINVAL;
@@ -1355,6 +1444,8 @@ static scg_status rowmat(scg_ctx *c, double *Shard::*out, double *Shard::*A, dou
 scg_status sketchycgal_reconstruct(scg_ctx *c, double *Uh, double *Lambda, double *errh) {
   if (!c || !Lambda) return SCG_EINVAL;
   if (c->t < 1) return fail(c, SCG_ESTATE, "reconstruct before any iteration");
+  if (c->failed) return SCG_ESTATE;
+  sketch_flush(c);
   scg_status st = sketchycgal_synchronize(c);
   if (st) return st;
   const int R = c->R;
