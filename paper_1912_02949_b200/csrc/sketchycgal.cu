@@ -796,12 +796,13 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
   return SCG_OK;
 }
 
-// Allocate the gathered region with `cap` W slots (+ the x slot).
+// Allocate the gathered region with `cap` W slots (+ the x slot).  Slots are always
+// written before they are read; only the x slot and W slot 0 are zeroed.
 scg_status alloc_G(scg_ctx *c, Shard *s, int cap) {
   const size_t bytes = sizeof(double) * (size_t)c->npad * (size_t)(1 + cap);
   double *G = nullptr;
   CK(cudaMalloc(&G, bytes));
-  CK(cudaMemsetAsync(G, 0, bytes, c->stream));
+  CK(cudaMemsetAsync(G, 0, sizeof(double) * (size_t)c->npad * 2, c->stream));
   if (s->G) {  // keep W slot 0 (the start vector g of the next iteration)
     CK(cudaMemcpyAsync(G + c->npad, s->G + c->npad, sizeof(double) * c->npad, cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1110,6 +1111,14 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   // Lanczos vector storage.  One rank: grown on demand.  Sharded: fixed at init (peers map it).
   c->store = (flags & SCG_REGENERATE) == 0;
   int cap = 3;
+  if (world == 1 && c->store) {  // pre-size the store for q_t up to t = 1000 when it fits comfortably
+    int64_t q1000 = (int64_t)std::ceil(std::sqrt(std::sqrt(1000.0)) * c->lnN);
+    q1000 = std::min<int64_t>(std::min<int64_t>(q1000, n - 1), kMaxQ - 1);
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t need = sizeof(double) * (size_t)c->npad * (size_t)(q1000 + 2);
+    if (2 * need < fr) cap = (int)std::max<int64_t>(3, q1000 + 1);
+  }
   if (world > 1 && c->store) {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
@@ -1348,6 +1357,7 @@ scg_status sketchycgal_iter_log(scg_ctx *c, int64_t t0, int64_t count, scg_iter_
 static scg_status fetch_rows(scg_ctx *c, const Shard *s, const double *dsrc, double *out, int64_t off) {
   std::vector<double> h((size_t)s->nl);
   CK(cudaMemcpy(h.data(), dsrc, sizeof(double) * (size_t)s->nl, cudaMemcpyDeviceToHost));
+#pragma omp parallel for schedule(static, 65536)
   for (int64_t nu = 0; nu < s->nl; ++nu) out[off + s->origloc[(size_t)nu]] = h[(size_t)nu];
   return SCG_OK;
 }
