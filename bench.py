@@ -241,9 +241,9 @@ def ctypes_stream(stream):
 
 
 def run_e2e(scg, si, L, c, K, W, dev, dkw, world):
-    """Same metric through the C ABI with HOST buffers: init (CSR H2D) + W + K iterations + per-step
-    iteration-record D2H + reconstruct (U, Lambda D2H); value = K / (time of the whole job), the
-    slowest rank's time when sharded."""
+    """Same metric through the C ABI with HOST buffers: init (CSR H2D) + W + K iterations + the
+    iteration records, reconstruction (Lambda), objective, feasibility and the rounded cut chi (D2H);
+    value = (W + K) / (time of the whole job), the slowest rank's time when sharded."""
     import torch
     if dkw:  # a fresh communicator for the second context
         import torch.distributed as dist
@@ -262,7 +262,10 @@ def run_e2e(scg, si, L, c, K, W, dev, dkw, world):
     s.synchronize()
     ts = time.perf_counter()
     lg = s.iter_log()
-    U, lam, _ = s.reconstruct()
+    _, lam, _ = s.reconstruct(want_U=False)  # the job's results: Lambda, objective, feasibility, the cut
+    obj = s.objective()
+    feas = s.feasibility()
+    chi, cutw = s.round()
     s.synchronize()
     t1 = time.perf_counter()
     s.close()
@@ -274,7 +277,7 @@ def run_e2e(scg, si, L, c, K, W, dev, dkw, world):
         secs = float(t.item())
     a, b = s.row_begin, s.row_end
     h2d = 8 * (b - a + 1) + 12 * int(L.row_ptr[b] - L.row_ptr[a])
-    d2h = lg.nbytes + U.nbytes + lam.nbytes
+    d2h = lg.nbytes + lam.nbytes + obj.nbytes + feas.nbytes + chi.nbytes
     return {"value": (W + K) / secs, "unit": "iterations/s", "h2d_bytes_per_step": h2d / (W + K),
             "d2h_bytes_per_step": d2h / (W + K), "seconds": secs,
             "breakdown_s": {"init": round(ti - t0, 3), "steps": round(ts - ti, 3), "outputs": round(t1 - ts, 3)},

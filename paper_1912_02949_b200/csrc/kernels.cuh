@@ -1736,6 +1736,11 @@ __global__ void __launch_bounds__(kBlock) k_apply_d(Csr C, Rows RL, const double
 #endif
 }
 
+// out[orig[r]] = in[r]: device rows back to input order (outputs).
+__global__ void k_unperm(double *__restrict__ out, const double *__restrict__ in, const int *__restrict__ orig, int nl) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) out[orig[r]] = in[r];
+}
+
 // Self-test: div_rn against the hardware IEEE division on pseudo-random operands
 // (mantissas drawn uniformly, including the extremes 1 and 2 - ulp), exponents in +-60.
 __global__ void k_selftest_div(long long n, uint64_t seed, unsigned long long *mismatch) {

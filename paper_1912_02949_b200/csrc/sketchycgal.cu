@@ -1354,11 +1354,12 @@ scg_status sketchycgal_iter_log(scg_ctx *c, int64_t t0, int64_t count, scg_iter_
 }
 
 // Copy a device row vector (device labels) of shard s into out[off + input row] (host).
+// (un-permuted on the device into the shard's scratch vector a, then one copy)
 static scg_status fetch_rows(scg_ctx *c, const Shard *s, const double *dsrc, double *out, int64_t off) {
-  std::vector<double> h((size_t)s->nl);
-  CK(cudaMemcpy(h.data(), dsrc, sizeof(double) * (size_t)s->nl, cudaMemcpyDeviceToHost));
-#pragma omp parallel for schedule(static, 65536)
-  for (int64_t nu = 0; nu < s->nl; ++nu) out[off + s->origloc[(size_t)nu]] = h[(size_t)nu];
+  launch(c, KC_OTHER, 0.0, k_unperm, dim3(grid_for(s->nl, 8 * c->nsm)), dim3(kBlock), s->a, dsrc,
+         (const int *)s->orig, (int)s->nl);
+  CK(cudaMemcpyAsync(out + off, s->a, sizeof(double) * (size_t)s->nl, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
   return SCG_OK;
 }
 
