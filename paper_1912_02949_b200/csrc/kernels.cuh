@@ -147,10 +147,11 @@ __device__ __forceinline__ double div_rn(double a, double b, double rb) {
 #define SCG_ENGINE 0  // short-row SpMV engine: 0 = SELL-32-sigma register pipeline, 1 = window/tile-staged CSR (TMA)
 #endif
 #ifndef SCG_PIPE
-#define SCG_PIPE 1
+#define SCG_PIPE 3  // 3: width-specialized 3-stage pipeline (default), 2: width-specialized 2-stage,
+                    // 1: predicated 3-stage, 0: unpipelined
 #endif
 #ifndef SCG_MINB
-#define SCG_MINB 2
+#define SCG_MINB 3  // min blocks per SM of the uniform-weight SpMV kernels (register cap 80)
 #endif
 constexpr int kLongRow = 32;
 constexpr int kChunk = SCG_CH;   // entries of a row loaded per round
@@ -299,6 +300,205 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
     if (lane == 0) epi(o);
   }
   const double rden = 1.0 / den;
+#if SCG_PIPE == 3
+  if (NC == 1) {
+  // Width-specialized three-stage pipeline: while slice i is computed, the gathers and
+  // own entries of slice i+1, the columns of slice i+2 and the meta of slice i+3 are in
+  // flight; every stage runs only the slots of its slice's width (warp-uniform switch).
+  const int per = (RL.nslice + gridDim.x - 1) / gridDim.x;
+  const int ns = min(RL.nslice, (int)(blockIdx.x + 1) * per);
+  const int wstep = blockDim.x >> 5;
+  int sl = blockIdx.x * per + (threadIdx.x >> 5);
+  auto mload = [&](int q) -> int2 { return q < ns ? __ldg(&RL.meta[q]) : make_int2(0, 0); };
+  auto cload = [&](int2 m, int (&cv)[4]) {
+    const int w = m.y & 0xff;
+    const int *cp = RL.scol + m.x + lane;
+    cv[0] = w > 0 ? __ldg(cp) : -1;
+    cv[1] = w > 1 ? __ldg(cp + 32) : -1;
+    cv[2] = w > 2 ? __ldg(cp + 64) : -1;
+    cv[3] = w > 3 ? __ldg(cp + 96) : -1;
+  };
+  auto gload = [&](int2 m, const int (&cv)[4], double (&gv)[4]) {
+    switch (m.y & 0xff) {
+      case 0: break;
+      case 1: gv[0] = cv[0] != -1 ? __ldg(&X[cv[0] & 0x7fffffff]) : 0.0; break;
+      case 2:
+        gv[0] = cv[0] != -1 ? __ldg(&X[cv[0] & 0x7fffffff]) : 0.0;
+        gv[1] = cv[1] != -1 ? __ldg(&X[cv[1] & 0x7fffffff]) : 0.0;
+        break;
+      case 3:
+        gv[0] = cv[0] != -1 ? __ldg(&X[cv[0] & 0x7fffffff]) : 0.0;
+        gv[1] = cv[1] != -1 ? __ldg(&X[cv[1] & 0x7fffffff]) : 0.0;
+        gv[2] = cv[2] != -1 ? __ldg(&X[cv[2] & 0x7fffffff]) : 0.0;
+        break;
+      default:
+        gv[0] = cv[0] != -1 ? __ldg(&X[cv[0] & 0x7fffffff]) : 0.0;
+        gv[1] = cv[1] != -1 ? __ldg(&X[cv[1] & 0x7fffffff]) : 0.0;
+        gv[2] = cv[2] != -1 ? __ldg(&X[cv[2] & 0x7fffffff]) : 0.0;
+        gv[3] = cv[3] != -1 ? __ldg(&X[cv[3] & 0x7fffffff]) : 0.0;
+        break;
+    }
+  };
+  auto oload = [&](int q, int2 m, double &xo, double &dd) {
+    const int p = q * 32 + lane;
+    xo = 0.0;
+    dd = 0.0;
+    if (q < ns && p < nl && lane >= (m.y >> 8)) { xo = X[rb + p]; dd = diag0[p]; }
+  };
+  int2 m0 = mload(sl), m1 = mload(sl + wstep), m2 = mload(sl + 2 * wstep);
+  int c0[4], c1[4];
+  cload(m0, c0);
+  cload(m1, c1);
+  double g0[4] = {0.0, 0.0, 0.0, 0.0};
+  double xo0, d00;
+  gload(m0, c0, g0);
+  oload(sl, m0, xo0, d00);
+  for (; sl < ns; sl += wstep) {
+    const int2 m3 = mload(sl + 3 * wstep);
+    int c2[4];
+    cload(m2, c2);
+    double g1[4] = {0.0, 0.0, 0.0, 0.0};
+    double xo1, d01;
+    gload(m1, c1, g1);
+    oload(sl + wstep, m1, xo1, d01);
+    // compute slice i
+    const int p = sl * 32 + lane;
+    const bool ok = p < nl && lane >= (m0.y >> 8);
+    RowOut<NC> o;
+    o.r = p;
+    o.xr = xo0 * rden;
+    o.s[0] = d00 * o.xr;
+    auto step = [&](int c, double g) {
+      if (c != -1) {
+        const double mm = UNI ? (c < 0 ? -RL.m0 : RL.m0) : 0.0;
+        o.s[0] = fma(mm, g * rden, o.s[0]);  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
+      }
+    };
+    auto stepv = [&](int c, double g, int j) {
+      if (c != -1) o.s[0] = fma(__ldg(&RL.sval[m0.x + j * 32 + lane]), g * rden, o.s[0]);
+    };
+    const int w = m0.y & 0xff;
+    if (UNI) {
+      switch (w) {
+        case 0: break;
+        case 1: step(c0[0], g0[0]); break;
+        case 2: step(c0[0], g0[0]); step(c0[1], g0[1]); break;
+        case 3: step(c0[0], g0[0]); step(c0[1], g0[1]); step(c0[2], g0[2]); break;
+        default: step(c0[0], g0[0]); step(c0[1], g0[1]); step(c0[2], g0[2]); step(c0[3], g0[3]); break;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (u < w) stepv(c0[u], g0[u], u);
+    }
+    for (int j0 = 4; j0 < w; j0 += 4) {  // rows longer than four slots
+      int cx[4];
+      double gx[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cx[u] = j0 + u < w ? __ldg(&RL.scol[m0.x + (j0 + u) * 32 + lane]) : -1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) gx[u] = cx[u] != -1 ? __ldg(&X[cx[u] & 0x7fffffff]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (UNI) step(cx[u], gx[u]);
+        else stepv(cx[u], gx[u], j0 + u);
+      }
+    }
+    if (ok) epi(o);
+    // rotate
+    m0 = m1; m1 = m2; m2 = m3;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { c0[u] = c1[u]; c1[u] = c2[u]; g0[u] = g1[u]; }
+    xo0 = xo1; d00 = d01;
+  }
+  return;
+  }
+#endif
+#if SCG_PIPE == 2
+  if (NC == 1) {
+  // Width-specialized slices: each warp walks a contiguous range of slices; the meta and
+  // the first four column slots of the next slice are loaded while the current slice is
+  // computed; a warp-uniform switch on the slice width runs straight-line code (no
+  // predicated padding slots) for widths 0..4, a chunked loop above.
+  const int per = (RL.nslice + gridDim.x - 1) / gridDim.x;
+  const int ns = min(RL.nslice, (int)(blockIdx.x + 1) * per);
+  const int wstep = blockDim.x >> 5;
+  int sl = blockIdx.x * per + (threadIdx.x >> 5);
+  int2 mn = sl < ns ? __ldg(&RL.meta[sl]) : make_int2(0, 0);
+  int2 mn2 = sl + wstep < ns ? __ldg(&RL.meta[sl + wstep]) : make_int2(0, 0);  // meta two slices ahead
+  int cn0 = -1, cn1 = -1, cn2 = -1, cn3 = -1;
+  auto prefetch = [&](int2 m) {
+    const int w = m.y & 0xff;
+    const int *cp = RL.scol + m.x + lane;
+    cn0 = w > 0 ? __ldg(cp) : -1;
+    cn1 = w > 1 ? __ldg(cp + 32) : -1;
+    cn2 = w > 2 ? __ldg(cp + 64) : -1;
+    cn3 = w > 3 ? __ldg(cp + 96) : -1;
+  };
+  prefetch(mn);
+  for (; sl < ns; sl += wstep) {
+    const int2 m = mn;
+    const int c0 = cn0, c1 = cn1, c2 = cn2, c3 = cn3;
+    mn = mn2;
+    const int sn2 = sl + 2 * wstep;
+    mn2 = sn2 < ns ? __ldg(&RL.meta[sn2]) : make_int2(0, 0);
+    prefetch(mn);
+    const int w = m.y & 0xff;
+    const int p = sl * 32 + lane;
+    const bool ok = p < nl && lane >= (m.y >> 8);
+    double xo = 0.0, dd0 = 0.0, dd1 = 0.0;
+    if (ok) { xo = X[rb + p]; dd0 = diag0[p]; if (NC > 1) dd1 = diag1[p]; }
+    auto gat = [&](int c) -> double { return c != -1 ? __ldg(&X[c & 0x7fffffff]) : 0.0; };
+    auto val = [&](int c, int j) -> double {
+      return UNI ? (c < 0 ? -RL.m0 : RL.m0) : __ldg(&RL.sval[m.x + j * 32 + lane]);
+    };
+    RowOut<NC> o;
+    o.r = p;
+    auto step = [&](int c, double g, int j) {
+      if (c != -1) {
+        const double mm = val(c, j);
+        const double x = g * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
+#pragma unroll
+        for (int t = 0; t < NC; ++t) o.s[t] = fma(mm, x, o.s[t]);
+      }
+    };
+    auto init = [&]() {
+      o.xr = xo * rden;
+      o.s[0] = dd0 * o.xr;
+      if (NC > 1) o.s[NC - 1] = dd1 * o.xr;
+    };
+    switch (w) {
+      case 0: init(); break;
+      case 1: { const double g0 = gat(c0); init(); step(c0, g0, 0); } break;
+      case 2: { const double g0 = gat(c0), g1 = gat(c1); init(); step(c0, g0, 0); step(c1, g1, 1); } break;
+      case 3: {
+        const double g0 = gat(c0), g1 = gat(c1), g2 = gat(c2);
+        init(); step(c0, g0, 0); step(c1, g1, 1); step(c2, g2, 2);
+      } break;
+      case 4: {
+        const double g0 = gat(c0), g1 = gat(c1), g2 = gat(c2), g3 = gat(c3);
+        init(); step(c0, g0, 0); step(c1, g1, 1); step(c2, g2, 2); step(c3, g3, 3);
+      } break;
+      default: {
+        const double g0 = gat(c0), g1 = gat(c1), g2 = gat(c2), g3 = gat(c3);
+        init(); step(c0, g0, 0); step(c1, g1, 1); step(c2, g2, 2); step(c3, g3, 3);
+        for (int j0 = 4; j0 < w; j0 += 4) {
+          int cx[4];
+          double gx[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) cx[u] = j0 + u < w ? __ldg(&RL.scol[m.x + (j0 + u) * 32 + lane]) : -1;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) gx[u] = gat(cx[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) step(cx[u], gx[u], j0 + u);
+        }
+      } break;
+    }
+    if (ok) epi(o);
+  }
+  return;
+  }
+#endif
 #if SCG_PIPE == 0
   // SELL slices, one per warp step; latency hidden by occupancy (few registers)
   for (int sl = gw; sl < RL.nslice; sl += nw) {
