@@ -310,13 +310,18 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
   const int wstep = blockDim.x >> 5;
   int sl = blockIdx.x * per + (threadIdx.x >> 5);
   auto mload = [&](int q) -> int2 { return q < ns ? __ldg(&RL.meta[q]) : make_int2(0, 0); };
-  auto cload = [&](int2 m, int (&cv)[4]) {
+  auto cload = [&](int2 m, int (&cv)[4], double (&vv)[4]) {
     const int w = m.y & 0xff;
     const int *cp = RL.scol + m.x + lane;
     cv[0] = w > 0 ? __ldg(cp) : -1;
     cv[1] = w > 1 ? __ldg(cp + 32) : -1;
     cv[2] = w > 2 ? __ldg(cp + 64) : -1;
     cv[3] = w > 3 ? __ldg(cp + 96) : -1;
+    if (!UNI) {  // values travel with their columns
+      const double *vp = RL.sval + m.x + lane;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) vv[u] = w > u ? __ldg(vp + 32 * u) : 0.0;
+    }
   };
   auto gload = [&](int2 m, const int (&cv)[4], double (&gv)[4]) {
     switch (m.y & 0xff) {
@@ -347,8 +352,9 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
   };
   int2 m0 = mload(sl), m1 = mload(sl + wstep), m2 = mload(sl + 2 * wstep);
   int c0[4], c1[4];
-  cload(m0, c0);
-  cload(m1, c1);
+  double v0[4], v1[4];
+  cload(m0, c0, v0);
+  cload(m1, c1, v1);
   double g0[4] = {0.0, 0.0, 0.0, 0.0};
   double xo0, d00;
   gload(m0, c0, g0);
@@ -356,7 +362,8 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
   for (; sl < ns; sl += wstep) {
     const int2 m3 = mload(sl + 3 * wstep);
     int c2[4];
-    cload(m2, c2);
+    double v2[4];
+    cload(m2, c2, v2);
     double g1[4] = {0.0, 0.0, 0.0, 0.0};
     double xo1, d01;
     gload(m1, c1, g1);
@@ -374,8 +381,8 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
         o.s[0] = fma(mm, g * rden, o.s[0]);  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
       }
     };
-    auto stepv = [&](int c, double g, int j) {
-      if (c != -1) o.s[0] = fma(__ldg(&RL.sval[m0.x + j * 32 + lane]), g * rden, o.s[0]);
+    auto stepv = [&](int c, double g, double vv) {
+      if (c != -1) o.s[0] = fma(vv, g * rden, o.s[0]);
     };
     const int w = m0.y & 0xff;
     if (UNI) {
@@ -389,7 +396,7 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
     } else {
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (u < w) stepv(c0[u], g0[u], u);
+        if (u < w) stepv(c0[u], g0[u], v0[u]);
     }
     for (int j0 = 4; j0 < w; j0 += 4) {  // rows longer than four slots
       int cx[4];
@@ -401,14 +408,17 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (UNI) step(cx[u], gx[u]);
-        else stepv(cx[u], gx[u], j0 + u);
+        else stepv(cx[u], gx[u], cx[u] != -1 ? __ldg(&RL.sval[m0.x + (j0 + u) * 32 + lane]) : 0.0);
       }
     }
     if (ok) epi(o);
     // rotate
     m0 = m1; m1 = m2; m2 = m3;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { c0[u] = c1[u]; c1[u] = c2[u]; g0[u] = g1[u]; }
+    for (int u = 0; u < 4; ++u) {
+      c0[u] = c1[u]; c1[u] = c2[u]; g0[u] = g1[u];
+      if (!UNI) { v0[u] = v1[u]; v1[u] = v2[u]; }
+    }
     xo0 = xo1; d00 = d01;
   }
   return;
