@@ -195,12 +195,17 @@ struct RowOut {
   double s[NC]; // chain results
 };
 
-// Chains of one long row by a warp; result valid in lane 0.
+// Chains of one long row by a warp; result valid in lane 0.  Each round the warp loads
+// 32 entries (coalesced columns and values, gathered x) and stages the (value, x) pairs
+// in a per-warp shared buffer; lane 0 then runs the sequential CAC-3 chain from shared
+// memory with the loads unrolled ahead, so only the fma dependency is on the critical
+// path, while the next round's loads are already in flight.
 template <int NC>
 __device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double *__restrict__ X, double den,
                                                const double *__restrict__ diag0, const double *__restrict__ diag1,
                                                long long rb, RowOut<NC> &o) {
-  const int lane = threadIdx.x & 31;
+  __shared__ double2 lbuf[kBlock / 32][32];
+  const int lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) & (kBlock / 32 - 1);
   const int e0 = __ldg(&C.rp[r]), e1 = __ldg(&C.rp[r + 1]);
   const double rden = 1.0 / den;
   o.r = r;
@@ -213,17 +218,30 @@ __device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double
   double xn = e < e1 ? __ldg(&X[cn]) : 0.0;
   for (int base = e0; base < e1; base += 32) {
     const int cnt = min(32, e1 - base);
-    const double m = mn, x = (xn) * rden;
+    __syncwarp();
+    lbuf[wid][lane] = make_double2(mn, (xn) * rden);  // v = w * fl(1/rho) (reading R26)
+    __syncwarp();
     // prefetch the next round before running this round's chain
     e = base + 32 + lane;
     if (e < e1) { cn = __ldg(&C.col[e]); mn = __ldg(&C.val[e]); xn = __ldg(&X[cn]); }
-    for (int j = 0; j < cnt; ++j) {
-      const double mj = __shfl_sync(0xffffffffu, m, j);
-      const double xj = __shfl_sync(0xffffffffu, x, j);
+    if (lane == 0) {
+      if (cnt == 32) {
 #pragma unroll
-      for (int c = 0; c < NC; ++c) o.s[c] = fma(mj, xj, o.s[c]);
+        for (int j = 0; j < 32; ++j) {
+          const double2 p = lbuf[wid][j];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) o.s[c] = fma(p.x, p.y, o.s[c]);
+        }
+      } else {
+        for (int j = 0; j < cnt; ++j) {
+          const double2 p = lbuf[wid][j];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) o.s[c] = fma(p.x, p.y, o.s[c]);
+        }
+      }
     }
   }
+  __syncwarp();
 }
 
 template <bool UNI>
