@@ -212,18 +212,29 @@ __device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double
   o.xr = (X[rb + r]) * rden;
   o.s[0] = diag0[r] * o.xr;
   if (NC > 1) o.s[NC - 1] = diag1[r] * o.xr;
-  int e = e0 + lane;
-  int cn = e < e1 ? __ldg(&C.col[e]) : 0;
-  double mn = e < e1 ? __ldg(&C.val[e]) : 0.0;
-  double xn = e < e1 ? __ldg(&X[cn]) : 0.0;
+  // rounds k+1 .. k+kLR-1 are in flight while round k is chained
+  constexpr int kLR = 4;
+  double mq[kLR], xq[kLR];
+#pragma unroll
+  for (int u = 0; u < kLR; ++u) {
+    const int e = e0 + 32 * u + lane;
+    mq[u] = 0.0;
+    xq[u] = 0.0;
+    if (e < e1) { mq[u] = __ldg(&C.val[e]); xq[u] = __ldg(&X[__ldg(&C.col[e])]); }
+  }
   for (int base = e0; base < e1; base += 32) {
     const int cnt = min(32, e1 - base);
     __syncwarp();
-    lbuf[wid][lane] = make_double2(mn, (xn) * rden);  // v = w * fl(1/rho) (reading R26)
+    lbuf[wid][lane] = make_double2(mq[0], (xq[0]) * rden);  // v = w * fl(1/rho) (reading R26)
     __syncwarp();
-    // prefetch the next round before running this round's chain
-    e = base + 32 + lane;
-    if (e < e1) { cn = __ldg(&C.col[e]); mn = __ldg(&C.val[e]); xn = __ldg(&X[cn]); }
+#pragma unroll
+    for (int u = 0; u + 1 < kLR; ++u) { mq[u] = mq[u + 1]; xq[u] = xq[u + 1]; }
+    {
+      const int e = base + 32 * kLR + lane;
+      mq[kLR - 1] = 0.0;
+      xq[kLR - 1] = 0.0;
+      if (e < e1) { mq[kLR - 1] = __ldg(&C.val[e]); xq[kLR - 1] = __ldg(&X[__ldg(&C.col[e])]); }
+    }
     if (lane == 0) {
       if (cnt == 32) {
 #pragma unroll
