@@ -20,7 +20,8 @@
  *          Q(p) = p truncated toward zero to a multiple of 2^-200 (|p| < 2^100).
  *          dot(a, b) = xsum(fl(a_r * b_r)).
  *   CAC-3  (D x)_r = d_r x_r + sum_{j in N(r), ascending} m_rj x_j, left to right,
- *          acc = fl(d_r * x_r); acc = fma(m_rj, x_j, acc).
+ *          acc = fl(d_r * x_r); acc = fma(m_rj, x_j, acc); rows of more than 32
+ *          entries: 32 strided partial chains combined by halving (reading R27).
  *   CAC-4  Alg. 2 as printed, two-pass, with readings R1-R5; a
  *          normalization v / rho is evaluated as v * fl(1/rho) (reading R26).
  *   CAC-5  tridiagonal min eigenpair by Sturm multisection + inverse iteration.
@@ -159,11 +160,30 @@ typedef struct {
   const double *m;     /* off-diagonal values of C (or of M) */
 } o_off;
 
+/* CAC-3 row of D x.  Rows with at most 32 off-diagonal entries: one chain from fl(d_r x_r).
+ * Longer rows (reading R27, SURVEY.md section 8(c) CAC-2 with W = 32): partial chain l
+ * (l = 0..31) runs over the entries k = l, l+32, l+64, ... of the row (ascending column
+ * order) by fma from 0; the 32 partials combine by halving, L[l] = L[l] + L[l+off] for
+ * off = 16, 8, 4, 2, 1 and l < off; the row is fl(fl(d_r x_r) + L[0]). */
+#define O_LONG_ROW 32
 static void o_apply(const o_off *A, const double *d, const double *x, double *y) {
   for (int64_t r = 0; r < A->n; ++r) {
-    double acc = d[r] * x[r];
-    for (int64_t k = A->rp[r]; k < A->rp[r + 1]; ++k) acc = fma(A->m[k], x[A->col[k]], acc);
-    y[r] = acc;
+    const int64_t a = A->rp[r], b = A->rp[r + 1];
+    if (b - a <= O_LONG_ROW) {
+      double acc = d[r] * x[r];
+      for (int64_t k = a; k < b; ++k) acc = fma(A->m[k], x[A->col[k]], acc);
+      y[r] = acc;
+    } else {
+      double L[O_LONG_ROW];
+      for (int l = 0; l < O_LONG_ROW; ++l) L[l] = 0.0;
+      for (int64_t k = a; k < b; ++k) {
+        const int l = (int)((k - a) % O_LONG_ROW);
+        L[l] = fma(A->m[k], x[A->col[k]], L[l]);
+      }
+      for (int off = O_LONG_ROW / 2; off >= 1; off /= 2)
+        for (int l = 0; l < off; ++l) L[l] = L[l] + L[l + off];
+      y[r] = d[r] * x[r] + L[0];
+    }
   }
 }
 

@@ -195,24 +195,18 @@ struct RowOut {
   double s[NC]; // chain results
 };
 
-// Chains of one long row by a warp; result valid in lane 0.  Each round the warp loads
-// 32 entries (coalesced columns and values, gathered x) and stages the (value, x) pairs
-// in a per-warp shared buffer; lane 0 then runs the sequential CAC-3 chain from shared
-// memory with the loads unrolled ahead, so only the fma dependency is on the critical
-// path, while the next round's loads are already in flight.
+// One long row (> kLongRow entries) by a warp; result valid in lane 0.  CAC-3 for long
+// rows (reading R27): lane l runs the partial chain over the row's entries l, l+32, ...
+// (ascending column order) by fma from 0 -- exactly the coalesced round structure --;
+// the partials combine by halving (L[l] += L[l+off], off = 16..1) and the row is
+// fl(fl(d_r x_r) + L[0]).  Rounds k+1 .. k+kLR-1 are loaded while round k is chained.
 template <int NC>
 __device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double *__restrict__ X, double den,
                                                const double *__restrict__ diag0, const double *__restrict__ diag1,
                                                long long rb, RowOut<NC> &o) {
-  __shared__ double2 lbuf[kBlock / 32][32];
-  const int lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) & (kBlock / 32 - 1);
+  const int lane = threadIdx.x & 31;
   const int e0 = __ldg(&C.rp[r]), e1 = __ldg(&C.rp[r + 1]);
   const double rden = 1.0 / den;
-  o.r = r;
-  o.xr = (X[rb + r]) * rden;
-  o.s[0] = diag0[r] * o.xr;
-  if (NC > 1) o.s[NC - 1] = diag1[r] * o.xr;
-  // rounds k+1 .. k+kLR-1 are in flight while round k is chained
   constexpr int kLR = 4;
   double mq[kLR], xq[kLR];
 #pragma unroll
@@ -222,11 +216,12 @@ __device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double
     xq[u] = 0.0;
     if (e < e1) { mq[u] = __ldg(&C.val[e]); xq[u] = __ldg(&X[__ldg(&C.col[e])]); }
   }
+  double part[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) part[c] = 0.0;
   for (int base = e0; base < e1; base += 32) {
-    const int cnt = min(32, e1 - base);
-    __syncwarp();
-    lbuf[wid][lane] = make_double2(mq[0], (xq[0]) * rden);  // v = w * fl(1/rho) (reading R26)
-    __syncwarp();
+    const bool have = base + lane < e1;
+    const double m = mq[0], x = (xq[0]) * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
 #pragma unroll
     for (int u = 0; u + 1 < kLR; ++u) { mq[u] = mq[u + 1]; xq[u] = xq[u + 1]; }
     {
@@ -235,24 +230,21 @@ __device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double
       xq[kLR - 1] = 0.0;
       if (e < e1) { mq[kLR - 1] = __ldg(&C.val[e]); xq[kLR - 1] = __ldg(&X[__ldg(&C.col[e])]); }
     }
-    if (lane == 0) {
-      if (cnt == 32) {
+    if (have)
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const double2 p = lbuf[wid][j];
-#pragma unroll
-          for (int c = 0; c < NC; ++c) o.s[c] = fma(p.x, p.y, o.s[c]);
-        }
-      } else {
-        for (int j = 0; j < cnt; ++j) {
-          const double2 p = lbuf[wid][j];
-#pragma unroll
-          for (int c = 0; c < NC; ++c) o.s[c] = fma(p.x, p.y, o.s[c]);
-        }
-      }
-    }
+      for (int c = 0; c < NC; ++c) part[c] = fma(m, x, part[c]);
   }
-  __syncwarp();
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double t = __shfl_down_sync(0xffffffffu, part[c], off);
+      if (lane < off) part[c] = part[c] + t;
+    }
+  o.r = r;
+  o.xr = (X[rb + r]) * rden;
+  o.s[0] = diag0[r] * o.xr + part[0];
+  if (NC > 1) o.s[NC - 1] = diag1[r] * o.xr + part[NC - 1];
 }
 
 template <bool UNI>

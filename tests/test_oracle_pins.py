@@ -81,6 +81,53 @@ def test_apply_rounding_bound():
         assert abs(float(Fraction(y[r]) - exact)) <= bound
 
 
+def test_apply_long_rows_integer_exact_and_bounded():
+    # Rows of > 32 entries take the strided partial chains (reading R27): still exact on
+    # small integers, and within the summation rounding bound on real data.
+    rng = np.random.default_rng(5)
+    n = 300
+    M = rng.integers(-5, 6, size=(n, n)).astype(float)
+    M = np.triu(M, 1)
+    M = M + M.T + np.diag(rng.integers(-9, 10, size=n).astype(float))
+    rp, col, m, d = oracle.offdiag_of_dense(M)
+    assert np.max(np.diff(rp)) > 200
+    x = rng.integers(-7, 8, size=n).astype(float)
+    assert np.array_equal(oracle.apply(n, rp, col, m, d, x), M @ x)
+    Mr = rng.standard_normal((n, n))
+    Mr = Mr + Mr.T
+    rp, col, m, d = oracle.offdiag_of_dense(Mr)
+    xr = rng.standard_normal(n)
+    y = oracle.apply(n, rp, col, m, d, xr)
+    for r in range(0, n, 37):
+        exact = sum(Fraction(Mr[r, c]) * Fraction(xr[c]) for c in range(n))
+        bound = n * 2.0 ** -53 * float(np.sum(np.abs(Mr[r] * xr))) * 1.01
+        assert abs(float(Fraction(y[r]) - exact)) <= bound
+
+
+def _fma(a, b, c):  # correctly rounded fma via exact rationals (float(Fraction) rounds to nearest)
+    return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+def test_apply_long_row_order_differs_from_single_chain():
+    # The partial-chain order (R27) rounds differently from one left-to-right chain: on data
+    # built to cancel the two orders give different bits, so the GPU parity tests pin the
+    # order, not just the value.
+    rng = np.random.default_rng(0)
+    rng.standard_normal(69), rng.uniform(-20, 20, 69), rng.standard_normal(70)  # skip the first draw
+    n = 70
+    M = np.zeros((n, n))
+    v = rng.standard_normal(n - 1) * np.exp(rng.uniform(-20, 20, n - 1))  # wide dynamic range
+    M[0, 1:] = v
+    M[1:, 0] = v
+    x = rng.standard_normal(n)
+    rp, col, m, d = oracle.offdiag_of_dense(M)
+    y = oracle.apply(n, rp, col, m, d, x)
+    acc = d[0] * x[0]
+    for k in range(rp[0], rp[1]):
+        acc = _fma(m[k], x[col[k]], acc)
+    assert y[0] != acc
+
+
 # ------------------------------------------------------------- Laplacian
 def test_laplacian_identities():
     L = si.laplacian("c0")
