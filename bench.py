@@ -4,7 +4,9 @@
 Contract (task statement + BASELINE.json): one JSON line on rank 0.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
 
-A "step" is one SketchyCGAL iteration t (Alg. 4 lines 5-10):
+By default W = 3 and K = 997, so the timed window t = 4..1000 is the whole T = 1000 run
+of configs[3] (q_t grows from 17 to 94 over the run; an early short window would overstate
+the rate).  A "step" is one SketchyCGAL iteration t (Alg. 4 lines 5-10):
 one randomized Lanczos call (pass 1 + tridiagonal eigensolve + pass 2), the
 monitor matvec, the primal/dual updates and the rank-one sketch update, on the
 synthetic stand-in of BASELINE.json configs[3] (n = 2^24 mutual k-NN random
@@ -137,8 +139,10 @@ def run_reference(args, rank, world):
 def _config_dict(cfg, L, world, t0, t1):
     import scg_inputs as si
     c = si.CONFIGS[cfg]
+    lnN = float(np.log(float(L.n)))
+    q = [min(L.n - 1, max(2, int(np.ceil(np.sqrt(np.sqrt(float(t))) * lnN)))) for t in (t0, t1)]
     return {"workload": f"{cfg}: {c['desc']}", "n": int(L.n), "m": int(L.m), "R": c["R"], "T_config": c["T"],
-            "t_window": [int(t0), int(t1)], "parallelism": f"rows{world}",
+            "t_window": [int(t0), int(t1)], "q_t_window": q, "parallelism": f"rows{world}",
             "l2": "no flush: per-iteration working set > 126 MB L2 (inputs larger than L2)"}
 
 
@@ -288,7 +292,7 @@ def run_e2e(scg, si, L, c, K, W, dev, dkw, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=997)  # t = 4..1000: the whole configs[3] run (T = 1000)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
