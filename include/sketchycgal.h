@@ -119,6 +119,11 @@ typedef struct {
   double znorm;       /* ||z_{t+1} - b||, scaled units */
   double gamma;       /* dual step gamma_t (eqn:sketchy-cgal-dual-step) */
   double tau;         /* trace tracker tau */
+  double gap;         /* surrogate duality gap g_t(X_t) with lambda_min(D_t) ~ xi_t (eqn:cgal-gap,
+                         PAPER.md:1550-1555), scaled units, state before the update of iteration t */
+  double bound;       /* posterior suboptimality bound of X_t, = the stopping numerator
+                         p_t + <y_t, b> + beta_t/2 <z_t - b, z_t + b> - alpha xi_t
+                         (PAPER.md:1557-1562, 4044-4048), scaled units */
 } scg_iter_rec;
 
 /* Per-kernel-class timing (SCG_PROFILE), for bench.py's roofline. */
@@ -145,6 +150,17 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
  * stream; returns after enqueueing and checking launch errors.  Device-side
  * range errors surface at the next synchronizing call as SCG_ERANGE. */
 scg_status sketchycgal_step(scg_ctx *c, int64_t T);
+
+/* Run up to T_max more iterations and stop at the first iteration t that meets the
+ * stopping rule of PAPER.md:4044-4048 (scaled problem):
+ *   bound_t / (1 + |p_t|) <= eps   and   ||z_t - b|| / (1 + ||b||) <= eps,
+ * with bound_t the posterior suboptimality bound of the record (lambda_min(D_t) ~ xi_t,
+ * as the paper's own implementation does) and p_t, z_t the state before
+ * iteration t's update.  The rule is checked on the iteration records every
+ * check_every iterations, so up to check_every - 1 iterations past t may have run
+ * (sketchycgal_iterations tells).  *t_stop = t, or -1 if T_max iterations ran without
+ * meeting the rule.  Errors: SCG_EINVAL (T_max < 0, eps <= 0, check_every < 1). */
+scg_status sketchycgal_run(scg_ctx *c, int64_t T_max, double eps, int64_t check_every, int64_t *t_stop);
 
 /* Block until all queued work is done; reports deferred device errors. */
 scg_status sketchycgal_synchronize(scg_ctx *c);

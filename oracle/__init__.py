@@ -247,7 +247,7 @@ class Oracle:
 
     @property
     def log(self) -> np.ndarray:
-        return self._get(5, self.logcap * 10).reshape(self.logcap, 10)
+        return self._get(5, self.logcap * 12).reshape(self.logcap, 12)
 
     @property
     def vhist(self) -> np.ndarray:

@@ -413,6 +413,7 @@ double oracle_gamma(int64_t t, double alpha, double beta0, double nz) {
 
 /* ------------------------------------------------------------------------- */
 /* Alg. 4 SketchyCGAL for the MaxCut SDP. */
+#define O_LOGW 12 /* t, q, k, theta, xi, c, p, ||z-b||, gamma, tau, gap, bound */
 typedef struct {
   int64_t n;
   int32_t R;
@@ -427,6 +428,7 @@ typedef struct {
   double *m;
   double *cdiag;
   double *z, *y, *S, *Omega, *v, *g, *d;
+  double *ones; /* all-ones vector: xsum(y) = dot(y, 1) exactly */
   double *w1, *w2, *w3, *a, *cv;
   double p, tau;
   int err;
@@ -474,6 +476,8 @@ void *oracle_create(int64_t n, const int64_t *rp_L, const int32_t *col_L, const 
     o->rp[r + 1] = o_k;
   }
   o->z = (double *)calloc((size_t)n, sizeof(double));
+  o->ones = (double *)malloc(sizeof(double) * (size_t)n);
+  for (int64_t i = 0; i < n; ++i) o->ones[i] = 1.0;
   o->y = (double *)calloc((size_t)n, sizeof(double));
   o->d = (double *)calloc((size_t)n, sizeof(double));
   o->v = (double *)calloc((size_t)n, sizeof(double));
@@ -489,7 +493,7 @@ void *oracle_create(int64_t n, const int64_t *rp_L, const int32_t *col_L, const 
   for (int32_t kk = 0; kk < R; ++kk)
     for (int64_t i = 0; i < n; ++i) o->Omega[(int64_t)kk * n + i] = scg_omega(seed, i, kk);
   o->logcap = logcap;
-  o->log = (double *)calloc((size_t)(logcap > 0 ? logcap : 1) * 10, sizeof(double));
+  o->log = (double *)calloc((size_t)(logcap > 0 ? logcap : 1) * O_LOGW, sizeof(double));
   o->vhist_cap = vhist_cap;
   o->vhist = vhist_cap > 0 ? (double *)calloc((size_t)vhist_cap * n, sizeof(double)) : NULL;
   o->err = err;
@@ -502,7 +506,7 @@ void oracle_destroy(void *h) {
   free(o->rp); free(o->col); free(o->m); free(o->cdiag);
   free(o->z); free(o->y); free(o->d); free(o->v); free(o->g);
   free(o->w1); free(o->w2); free(o->w3); free(o->a); free(o->cv);
-  free(o->S); free(o->Omega); free(o->log); free(o->vhist);
+  free(o->S); free(o->Omega); free(o->log); free(o->vhist); free(o->ones);
   free(o);
 }
 
@@ -519,6 +523,21 @@ int oracle_step(void *h, int64_t T) {
     double eta = 2.0 / (double)(t + 1);
     int q = o->qfix > 0 ? o->qfix : oracle_qt(t, n);
     if (o->qfix <= 0 && q > n - 1) q = (int)(n - 1);
+    /* Surrogate duality gap g_t(X_t) (eqn:cgal-gap, as P:1550-1554) and the
+     * posterior suboptimality bound (eqn:scgal-posterior-error-bd), which is
+     * also the numerator of the stopping rule:
+     *   gap   = p_t + <y_t, z_t> + beta_t <z_t - b, z_t> - alpha lambda_min(D_t)
+     *   bound = p_t + <y_t, b> + beta_t/2 <z_t - b, z_t + b> - alpha lambda_min(D_t)
+     * with lambda_min(D_t) ~ xi_t (reading A22 puts alpha in front), the inner
+     * products from exact sums of the state before this iteration's update, evaluated in
+     * the order written in DESIGN.md CAC-6.  xi_t is known after the monitor below. */
+    int gerr = 0;
+    const double S_y = o_dot(o->y, o->ones, n, &gerr);
+    const double S_yz = o_dot(o->y, o->z, n, &gerr);
+    const double S_zz = o_dot(o->z, o->z, n, &gerr);
+    const double S_z = o_dot(o->z, o->ones, n, &gerr);
+    const double p_t = o->p;
+    o->err |= gerr;
     /* line 6: D = C + A*(y + beta (z - b)) ; diagonal of D (primitive 2) */
     for (int64_t r = 0; r < n; ++r) o->d[r] = fma(beta, o->z[r] - o->bval, o->y[r]) + o->cdiag[r];
     for (int64_t r = 0; r < n; ++r) o->g[r] = scg_lanczos_start(o->seed, t, r);
@@ -556,9 +575,13 @@ int oracle_step(void *h, int64_t T) {
     o->p = fma(eta * o->alpha, cval, one_m_eta * o->p);
     o->err |= err;
     if (t - 1 < o->logcap) {
-      double *L = o->log + (t - 1) * 10;
+      double *L = o->log + (t - 1) * O_LOGW;
       L[0] = (double)t; L[1] = (double)q; L[2] = (double)res.k; L[3] = res.theta; L[4] = xi;
       L[5] = cval; L[6] = o->p; L[7] = sqrt(nz); L[8] = gamma; L[9] = o->tau;
+      const double ax = o->alpha * xi;
+      L[10] = ((p_t + S_yz) + beta * (S_zz - o->bval * S_z)) - ax;
+      const double nbb = ((double)n * o->bval) * o->bval;
+      L[11] = ((p_t + o->bval * S_y) + (0.5 * beta) * (S_zz - nbb)) - ax;
     }
     if (o->vhist && t - 1 < o->vhist_cap) memcpy(o->vhist + (t - 1) * n, o->v, sizeof(double) * (size_t)n);
     o->t = t;
@@ -588,7 +611,7 @@ void oracle_get(void *h, int which, double *out) {
     case 2: memcpy(out, o->S, sizeof(double) * (size_t)n * o->R); break;
     case 3: memcpy(out, o->Omega, sizeof(double) * (size_t)n * o->R); break;
     case 4: memcpy(out, o->v, sizeof(double) * (size_t)n); break;
-    case 5: memcpy(out, o->log, sizeof(double) * (size_t)o->logcap * 10); break;
+    case 5: memcpy(out, o->log, sizeof(double) * (size_t)o->logcap * O_LOGW); break;
     case 6: if (o->vhist) memcpy(out, o->vhist, sizeof(double) * (size_t)o->vhist_cap * n); break;
     case 7: memcpy(out, o->cdiag, sizeof(double) * (size_t)n); break;
     case 8: memcpy(out, o->d, sizeof(double) * (size_t)n); break;

@@ -70,7 +70,8 @@ def build(force: bool = False) -> str:
 class IterRec(ctypes.Structure):
     _fields_ = [("t", ctypes.c_int64), ("q", ctypes.c_int32), ("k", ctypes.c_int32), ("theta", ctypes.c_double),
                 ("xi", ctypes.c_double), ("c", ctypes.c_double), ("p", ctypes.c_double),
-                ("znorm", ctypes.c_double), ("gamma", ctypes.c_double), ("tau", ctypes.c_double)]
+                ("znorm", ctypes.c_double), ("gamma", ctypes.c_double), ("tau", ctypes.c_double),
+                ("gap", ctypes.c_double), ("bound", ctypes.c_double)]
 
 
 class KStat(ctypes.Structure):
@@ -93,7 +94,7 @@ EXPORTS = ["sketchycgal_maxcut_init", "sketchycgal_step", "sketchycgal_synchroni
            "sketchycgal_objective", "sketchycgal_feasibility", "sketchycgal_round", "sketchycgal_iter_log",
            "sketchycgal_get_state", "sketchycgal_apply_D", "sketchycgal_iterations", "sketchycgal_launch_count",
            "sketchycgal_kernel_stats", "sketchycgal_reset_stats", "sketchycgal_nccl_unique_id",
-           "sketchycgal_row_splits", "sketchycgal_halo_plan",
+           "sketchycgal_row_splits", "sketchycgal_halo_plan", "sketchycgal_run",
            "sketchycgal_selftest_division", "sketchycgal_last_error", "sketchycgal_destroy"]
 
 _lib = None
@@ -121,6 +122,8 @@ def open_library(path: str = LIB_PATH):
     lib.sketchycgal_kernel_stats.argtypes = [P, P, I32]
     lib.sketchycgal_reset_stats.restype = None
     lib.sketchycgal_reset_stats.argtypes = [P]
+    lib.sketchycgal_run.restype = ctypes.c_int
+    lib.sketchycgal_run.argtypes = [P, I64, D, I64, ctypes.POINTER(I64)]
     lib.sketchycgal_row_splits.restype = ctypes.c_int
     lib.sketchycgal_row_splits.argtypes = [P, I64, I32, P]
     lib.sketchycgal_halo_plan.restype = I64
@@ -265,6 +268,14 @@ class SketchyCGAL:
     def step(self, T: int):
         self._check(self.lib.sketchycgal_step(self._h, int(T)), "sketchycgal_step")
 
+    def run(self, T_max: int, eps: float = 0.1, check_every: int = 64):
+        """Iterate until the stopping rule (PAPER.md:4044-4048) holds or T_max more iterations ran;
+        returns the first iteration t meeting it, or None."""
+        out = ctypes.c_int64(-1)
+        self._check(self.lib.sketchycgal_run(self._h, int(T_max), float(eps), int(check_every), ctypes.byref(out)),
+                    "sketchycgal_run")
+        return None if out.value < 0 else int(out.value)
+
     def synchronize(self):
         self._check(self.lib.sketchycgal_synchronize(self._h), "sketchycgal_synchronize")
 
@@ -280,8 +291,8 @@ class SketchyCGAL:
         count = self.t - t0 + 1 if count is None else count
         buf = (IterRec * count)()
         self._check(self.lib.sketchycgal_iter_log(self._h, int(t0), int(count), buf), "sketchycgal_iter_log")
-        return np.array([(r.t, r.q, r.k, r.theta, r.xi, r.c, r.p, r.znorm, r.gamma, r.tau) for r in buf],
-                        dtype=np.float64).reshape(count, 10)
+        return np.array([(r.t, r.q, r.k, r.theta, r.xi, r.c, r.p, r.znorm, r.gamma, r.tau, r.gap, r.bound)
+                         for r in buf], dtype=np.float64).reshape(count, 12)
 
     def state(self, which: str) -> np.ndarray:
         idx = {"z": 0, "y": 1, "S": 2, "Omega": 3, "v": 4, "d": 5, "cdiag": 6}[which]

@@ -31,12 +31,14 @@ struct DevScalars {
   double s[kMaxQ];         // eigenvector of the tridiagonal (CAC-5)
   double gk[kMaxR];        // g = v^T Omega
   double theta, nu_x, xi, c, vv, nz, gamma, p, tau;
+  double my[4];            // sums over the state (y_t, z_t) of the NEXT iteration: y, y.z, z.z, z (k_dual_sketch)
   int k, brk, err, pad;
 };
 
 // Exact-sum slot: up to 3 accumulators + a block ticket counter.
+constexpr int kMaxSums = 5;  // exact sums one kernel can produce
 struct XSlot {
-  long long limbs[3][kLimbs];
+  long long limbs[kMaxSums][kLimbs];
   unsigned int counter;
   unsigned int pad;
 };
@@ -51,7 +53,7 @@ struct Csr {
 struct IterArgs {
   long long t;
   int q;
-  double eta, one_m_eta, alpha, b, beta0, sq, beta_next;
+  double eta, one_m_eta, alpha, b, beta0, sq, beta_next, nbb;  // nbb = fl(fl(n b) b) = ||b||^2
 };
 
 // ---------------------------------------------------------------- row-sharded execution
@@ -74,7 +76,7 @@ struct IterArgs {
 constexpr int kMaxRanks = 8;
 
 struct Mailbox {
-  long long limbs[4][kMaxRanks][3][kLimbs];  // [epoch & 3][source rank][sum][limb]
+  long long limbs[4][kMaxRanks][kMaxSums][kLimbs];  // [epoch & 3][source rank][sum][limb]
   double fv[4][kMaxRanks][kMaxR];            // fp64 payload (g = v^T Omega partials)
   unsigned long long flag[4][kMaxRanks];     // epoch published by the source rank
 };
@@ -105,7 +107,7 @@ __device__ __forceinline__ void gstore(const Net &net, double *dst, int r, doubl
   }
 }
 
-enum FinKind { FK_FROB = 0, FK_RHO0, FK_OM, FK_RHO, FK_NUX, FK_MON, FK_NZ, FK_BAR };
+enum FinKind { FK_FROB = 0, FK_RHO0, FK_OM, FK_RHO, FK_NUX, FK_MON, FK_NZ, FK_BAR, FK_RHO0M };
 
 struct FinArgs {
   int i;                 // Lanczos step (FK_OM, FK_RHO, FK_BAR)
@@ -1078,9 +1080,12 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
   switch (kind) {
     case FK_FROB: *f.out = xacc_round(L[0]); break;
     case FK_RHO0:
+    case FK_RHO0M:
       sc->rho[0] = sqrt(xacc_round(L[0]));
       sc->brk = 0;
       sc->k = 0;
+      if (kind == FK_RHO0M)
+        for (int j = 0; j < 4; ++j) sc->my[j] = xacc_round(L[1 + j]);
       break;
     case FK_OM: sc->om[f.i - 1] = xacc_round(L[0]); break;
     case FK_RHO: fin_rho(sc, f.i, xacc_round(L[0])); break;
@@ -1094,6 +1099,23 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
       for (int k = 0; k < f.R; ++k) sc->gk[k] = gk[k];
       const IterArgs &A = f.A;
       const double nz = xacc_round(L[0]);
+      // surrogate duality gap (eqn:cgal-gap) and posterior suboptimality
+      // bound (eqn:scgal-posterior-error-bd; = the stopping numerator
+      // P:4044-4048) of the implicit iterate X_t, with lambda_min(D_t) ~ xi_t and
+      // the sums my = (sum y_t, y_t.z_t, z_t.z_t, sum z_t) -- DESIGN.md CAC-6
+      double gapv, boundv;
+      {
+        const double beta = A.beta0 * A.sq;
+        const double pt = sc->p, ax = A.alpha * sc->xi;
+        const double zmb_z = sc->my[2] - A.b * sc->my[3];
+        double g = pt + sc->my[1];
+        g = g + beta * zmb_z;
+        gapv = g - ax;
+        const double zpb = sc->my[2] - A.nbb;
+        double u = pt + A.b * sc->my[0];
+        u = u + (0.5 * beta) * zpb;
+        boundv = u - ax;
+      }
       sc->nz = nz;
       sc->gamma = gamma_rule(A, nz);
       const double ea2 = A.eta * A.alpha;
@@ -1110,6 +1132,8 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
       rec.znorm = sqrt(nz);
       rec.gamma = sc->gamma;
       rec.tau = sc->tau;
+      rec.gap = gapv;
+      rec.bound = boundv;
       f.log[A.t - 1] = rec;
       break;
     }
@@ -1132,8 +1156,8 @@ template <int NS>
 __device__ __forceinline__ void emit(XSlot *slot, DevScalars *sc, const Net &net, int kind, const FinArgs &f,
                                      const double *gk) {
   __threadfence();
-  long long L[3][kLimbs];
-  for (int s = 0; s < 3; ++s)
+  long long L[kMaxSums][kLimbs];
+  for (int s = 0; s < kMaxSums; ++s)
     for (int i = 0; i < kLimbs; ++i)
       L[s][i] = s < NS ? (long long)atomicExch(reinterpret_cast<unsigned long long *>(&slot->limbs[s][i]), 0ull) : 0ll;
   slot->counter = 0;
@@ -1172,9 +1196,9 @@ __global__ void k_pull(int kind, int ns, Net net, DevScalars *sc, FinArgs f) {
       __nanosleep(32);
     }
   }
-  long long L[3][kLimbs];
+  long long L[kMaxSums][kLimbs];
   double gk[kMaxR];
-  for (int s = 0; s < 3; ++s)
+  for (int s = 0; s < kMaxSums; ++s)
     for (int i = 0; i < kLimbs; ++i) {
       long long acc = 0;
       if (s < ns)
@@ -1758,7 +1782,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
 // y <- y + gamma (z - b) (Alg. 4 line 9); d for t+1; next start vector g_{t+1} and
 // ||g_{t+1}||^2 (exact).  The sketch update of Alg. 4 line 10 is deferred (k_sketch_flush):
 // this kernel records its coefficients ck = fl(eta alpha) g_k in the ring slot js.
-__global__ void __launch_bounds__(kBlock, 3) k_dual_sketch(const double *__restrict__ z, double *__restrict__ y,
+__global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restrict__ z, double *__restrict__ y,
                                                         double *__restrict__ d, const double *__restrict__ cdiag,
                                                         double *__restrict__ ckr, int js,
                                                         double *__restrict__ g, int nl, long long rb, int R,
@@ -1767,10 +1791,13 @@ __global__ void __launch_bounds__(kBlock, 3) k_dual_sketch(const double *__restr
   const double gam = sc->gamma;
   if (blockIdx.x == 0 && (int)threadIdx.x < R)
     ckr[js * kMaxR + threadIdx.x] = (A.eta * A.alpha) * sc->gk[threadIdx.x];
-  __shared__ XBlk<1> xb;
-  xblk_init<1>(xb);
-  XWin acc[1];
-  xwin_init(acc[0]);
+  // exact sums: ||g_{t+1}||^2, and over the next iteration's state (y_{t+1}, z_{t+1}):
+  // sum y, y.z, z.z, sum z (surrogate gap / stopping rule, finalize FK_NZ)
+  __shared__ XBlk<5> xb;
+  xblk_init<5>(xb);
+  XWin acc[5];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) xwin_init(acc[q]);
   int err = 0;
   const int stride = gridDim.x * blockDim.x;
   for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < nl; r0 += 2 * stride) {
@@ -1792,11 +1819,15 @@ __global__ void __launch_bounds__(kBlock, 3) k_dual_sketch(const double *__restr
         const double gv = scg_lanczos_start(seed, A.t + 1, rb + og[u]);
         gstore(net, g + rb + r, r, gv);
         xwin_add(acc[0], gv * gv, err, xb.l[0]);
+        xwin_add(acc[1], yr, err, xb.l[1]);
+        xwin_add(acc[2], yr * zr[u], err, xb.l[2]);
+        xwin_add(acc[3], zr[u] * zr[u], err, xb.l[3]);
+        xwin_add(acc[4], zr[u], err, xb.l[4]);
       }
     }
   }
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
-    emit<1>(slot, sc, net, FK_RHO0, FinArgs{}, nullptr);
+  if (commit_and_ticket<5>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
+    emit<5>(slot, sc, net, FK_RHO0M, FinArgs{}, nullptr);
 }
 
 // Deferred sketch updates (Alg. 4 line 10, eqn:sketch-update PAPER.md:1162-1169): S is

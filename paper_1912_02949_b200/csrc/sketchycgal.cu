@@ -1213,6 +1213,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     A.b = c->b;
     A.beta0 = c->beta0;
     A.beta_next = c->beta0 * std::sqrt((double)(t + 2));
+    A.nbb = ((double)c->n * c->b) * c->b;
     int64_t q = (int64_t)std::ceil(std::sqrt(std::sqrt((double)t)) * c->lnN);
     if (q < 2) q = 2;
     if (q > c->n - 1) q = c->n - 1;
@@ -1320,7 +1321,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
              (const double *)s->z, s->y, s->d, (const double *)s->cdiag, s->ckr, js, c->wslot(s, 0),
              (int)s->nl, (long long)s->rb, c->R, A, c->seed, s->slots + SLOT_NU0, s->sc, net_of(c, s, E),
              (const int *)s->orig);
-    pull_all(c, FK_RHO0, 1, E, FinArgs{});
+    pull_all(c, FK_RHO0M, 5, E, FinArgs{});
     c->ome[js] = A.one_m_eta;
     c->vlast = js;
     if (++c->spend == kSketchB) sketch_flush(c);
@@ -1328,6 +1329,48 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
   }
   CK(cudaGetLastError());
   c->have_recon = false;
+  return SCG_OK;
+}
+
+// Stopping rule on the iteration records: iteration t meets it when
+//   bound_t / (1 + |p_t|) <= eps  and  ||z_t - b|| / (1 + ||b||) <= eps,
+// p_t and z_t being the state BEFORE iteration t's update (record t-1; p_1 = 0, z_1 = 0).
+static bool meets_stop(const scg_ctx *c, const scg_iter_rec &r, const scg_iter_rec *prev, double eps) {
+  const double pt = prev ? prev->p : 0.0;
+  const double nb = c->b * std::sqrt((double)c->n);
+  const double zres = prev ? prev->znorm : nb;
+  return r.bound / (1.0 + std::fabs(pt)) <= eps && zres / (1.0 + nb) <= eps;
+}
+
+scg_status sketchycgal_run(scg_ctx *c, int64_t T_max, double eps, int64_t check_every, int64_t *t_stop) {
+  if (!c || !t_stop || T_max < 0 || !(eps > 0) || check_every < 1) return SCG_EINVAL;
+  *t_stop = -1;
+  scg_iter_rec prev{};
+  bool have_prev = false;
+  if (c->t > 0) {
+    scg_status st = sketchycgal_iter_log(c, c->t, 1, &prev);
+    if (st) return st;
+    have_prev = true;
+  }
+  std::vector<scg_iter_rec> rec;
+  int64_t done = 0;
+  while (done < T_max) {
+    const int64_t k = std::min(check_every, T_max - done);
+    const int64_t t0 = c->t + 1;
+    scg_status st = sketchycgal_step(c, k);
+    if (st) return st;
+    rec.resize((size_t)k);
+    if ((st = sketchycgal_iter_log(c, t0, k, rec.data()))) return st;
+    for (int64_t j = 0; j < k; ++j) {
+      if (meets_stop(c, rec[(size_t)j], have_prev ? &prev : nullptr, eps)) {
+        *t_stop = rec[(size_t)j].t;
+        return SCG_OK;
+      }
+      prev = rec[(size_t)j];
+      have_prev = true;
+    }
+    done += k;
+  }
   return SCG_OK;
 }
 

@@ -25,7 +25,8 @@ def _run_pair(gpu, L, R, T, seed, scale=True, regenerate=False):
 
 def _assert_trajectory(g, o, T):
     gl, ol = g.iter_log(), o.log
-    assert gl.shape == (T, 10)
+    assert gl.shape == (T, 12)
+    np.testing.assert_array_equal(gl[:, 10:12], ol[:, 10:12])     # surrogate gap, posterior bound bitwise
     np.testing.assert_array_equal(gl[:, 0:3], ol[:, 0:3])          # t, q, k
     np.testing.assert_array_equal(gl[:, 3], ol[:, 3])              # theta (Ritz) bitwise
     np.testing.assert_array_equal(gl[:, 8], ol[:, 8])              # gamma bitwise
@@ -270,3 +271,30 @@ def test_sharded_full_size_first_iterations(gpu, cfg, P, T):
     o = oracle.Oracle(L, c["R"], seed=c["seed"], logcap=T)
     o.step(T)
     _assert_trajectory(g, o, T)
+
+
+def _first_stop(log, n, eps):
+    """First t of a 12-column iteration log meeting the stopping rule, scaled units."""
+    b = 1.0 / n
+    nb = b * np.sqrt(n)
+    for i in range(log.shape[0]):
+        p_t = log[i - 1, 6] if i > 0 else 0.0
+        zres = log[i - 1, 7] if i > 0 else nb
+        if log[i, 11] / (1.0 + abs(p_t)) <= eps and zres / (1.0 + nb) <= eps:
+            return int(log[i, 0])
+    return None
+
+
+@pytest.mark.parametrize("shards", [1, 2])
+def test_stopping_rule_run(gpu, shards):
+    """sketchycgal_run stops at the first iteration meeting the paper's stopping rule (f2)."""
+    L = si.laplacian("c0")
+    o = oracle.Oracle(L, 10, seed=0, logcap=1000)
+    o.step(1000)
+    eps = 0.1
+    t_o = _first_stop(o.log, L.n, eps)
+    assert t_o is not None and t_o > 1
+    g = gpu.SketchyCGAL(L, R=10, seed=0, shards=shards)
+    t = g.run(1000, eps=eps, check_every=37)
+    assert t == t_o
+    assert t_o <= g.t < t_o + 37

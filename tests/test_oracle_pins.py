@@ -477,3 +477,37 @@ def test_rounding_examples():
     C5 = _edges_graph(5, [(k, (k + 1) % 5) for k in range(5)])
     K4 = _edges_graph(4, [(i, j) for i in range(4) for j in range(i + 1, 4)])
     assert _brute_maxcut(P3) == 2 and _brute_maxcut(C5) == 4 and _brute_maxcut(K4) == 4
+
+
+# ------------------------------------------------------------- f2: gap and posterior bound
+def test_posterior_bound_dominates_suboptimality():
+    """eqn:scgal-posterior-error-bd: with the exact lambda_min(D_t), the bound
+    p_t + <y_t, b> + beta_t/2 <z_t - b, z_t + b> - alpha lambda_min(D_t) is >= p_t - p_star,
+    p_star from the closed-form SDP value of an odd cycle (2n(1+cos(pi/n))).  The logged bound
+    uses xi_t >= lambda_min, so it is <= the exact one; gap - bound equals
+    <y_t, z_t - b> + beta_t/2 ||z_t - b||^2 (P:1557 derivation)."""
+    n = 5
+    L = _edges_graph(n, [(k, (k + 1) % n) for k in range(n)])
+    sdp = 2 * n * (1 + math.cos(math.pi / n))
+    T = 600
+    o = oracle.Oracle(L, 3, seed=11, logcap=T + 1)
+    Ld = L.dense()
+    prev_bound = None
+    for t in (5, 50, 600):
+        o.step(t - o.t)
+        y, z, p, b, alpha = o.y.copy(), o.z.copy(), o.p, o.b, o.alpha
+        p_star = -sdp / (n * o.nrmL)
+        beta = 1.0 * math.sqrt(t + 2)  # beta of iteration t+1 (state before its update)
+        D = -Ld / o.nrmL + np.diag(y + beta * (z - b))
+        lam = float(np.linalg.eigvalsh(D)[0])
+        bound_exact = p + b * y.sum() + 0.5 * beta * float(np.dot(z - b, z + b)) - alpha * lam
+        assert p - p_star <= bound_exact + 1e-12, (t, p - p_star, bound_exact)
+        if prev_bound is not None:
+            assert bound_exact < prev_bound
+        prev_bound = bound_exact
+        # the record of iteration t+1 (same state) once that iteration has run
+        o.step(1)
+        rec = o.log[t]
+        assert rec[11] <= bound_exact + 1e-12
+        ident = float(np.dot(y, z - b)) + 0.5 * beta * float(np.dot(z - b, z - b))
+        assert abs((rec[10] - rec[11]) - ident) <= 1e-12 * max(1.0, abs(rec[10]))
