@@ -152,7 +152,8 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
 scg_status sketchycgal_step(scg_ctx *c, int64_t T);
 
 /* Run up to T_max more iterations and stop at the first iteration t that meets the
- * stopping rule of PAPER.md:4044-4048 (scaled problem):
+ * stopping rule of PAPER.md:4044-4048, in ORIGINAL units (p, bound times ||L||_F n,
+ * z times n when SCG_SCALE; b = 1):
  *   bound_t / (1 + |p_t|) <= eps   and   ||z_t - b|| / (1 + ||b||) <= eps,
  * with bound_t the posterior suboptimality bound of the record (lambda_min(D_t) ~ xi_t,
  * as the paper's own implementation does) and p_t, z_t the state before

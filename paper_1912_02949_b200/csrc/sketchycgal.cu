@@ -1335,11 +1335,15 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
 // Stopping rule on the iteration records: iteration t meets it when
 //   bound_t / (1 + |p_t|) <= eps  and  ||z_t - b|| / (1 + ||b||) <= eps,
 // p_t and z_t being the state BEFORE iteration t's update (record t-1; p_1 = 0, z_1 = 0).
+// Evaluated in ORIGINAL units (reading R28): objective values scale by
+// ||L||_F alpha/alpha~ and z by alpha/alpha~ when SCG_SCALE is set; b = 1, ||b|| = sqrt(n).
 static bool meets_stop(const scg_ctx *c, const scg_iter_rec &r, const scg_iter_rec *prev, double eps) {
-  const double pt = prev ? prev->p : 0.0;
-  const double nb = c->b * std::sqrt((double)c->n);
-  const double zres = prev ? prev->znorm : nb;
-  return r.bound / (1.0 + std::fabs(pt)) <= eps && zres / (1.0 + nb) <= eps;
+  const bool scale = (c->flags & SCG_SCALE) != 0;
+  const double uz = c->alpha_orig / c->alpha, uo = scale ? c->nrmL * uz : 1.0;
+  const double pt = prev ? prev->p * uo : 0.0;
+  const double nb = std::sqrt((double)c->n);
+  const double zres = prev ? prev->znorm * uz : nb;
+  return (r.bound * uo) / (1.0 + std::fabs(pt)) <= eps && zres / (1.0 + nb) <= eps;
 }
 
 scg_status sketchycgal_run(scg_ctx *c, int64_t T_max, double eps, int64_t check_every, int64_t *t_stop) {

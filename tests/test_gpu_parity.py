@@ -273,14 +273,15 @@ def test_sharded_full_size_first_iterations(gpu, cfg, P, T):
     _assert_trajectory(g, o, T)
 
 
-def _first_stop(log, n, eps):
-    """First t of a 12-column iteration log meeting the stopping rule, scaled units."""
-    b = 1.0 / n
-    nb = b * np.sqrt(n)
+def _first_stop(log, n, nrmL, eps):
+    """First t of a 12-column (scaled-units) iteration log meeting the stopping rule of
+    PAPER.md:4044-4048 in original units (reading R28): objective x n ||L||_F, z x n, b = 1."""
+    uz, uo = float(n), float(n) * nrmL
+    nb = np.sqrt(n)
     for i in range(log.shape[0]):
-        p_t = log[i - 1, 6] if i > 0 else 0.0
-        zres = log[i - 1, 7] if i > 0 else nb
-        if log[i, 11] / (1.0 + abs(p_t)) <= eps and zres / (1.0 + nb) <= eps:
+        p_t = log[i - 1, 6] * uo if i > 0 else 0.0
+        zres = log[i - 1, 7] * uz if i > 0 else nb
+        if log[i, 11] * uo / (1.0 + abs(p_t)) <= eps and zres / (1.0 + nb) <= eps:
             return int(log[i, 0])
     return None
 
@@ -292,7 +293,7 @@ def test_stopping_rule_run(gpu, shards):
     o = oracle.Oracle(L, 10, seed=0, logcap=1000)
     o.step(1000)
     eps = 0.1
-    t_o = _first_stop(o.log, L.n, eps)
+    t_o = _first_stop(o.log, L.n, o.nrmL, eps)
     assert t_o is not None and t_o > 1
     g = gpu.SketchyCGAL(L, R=10, seed=0, shards=shards)
     t = g.run(1000, eps=eps, check_every=37)
