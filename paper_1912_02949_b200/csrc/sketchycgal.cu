@@ -101,7 +101,7 @@ struct Shard {
   int64_t halo_rows = 0;
   // grids
   int grid_rows = 1, grid_primal = 1, grid_tiles = 1, grid_b = 1, grid_comb = 1, grid_dual = 1, grid_norm = 1,
-      grid_mon = 1;
+      grid_mon = 1, grid_flush = 1;
   double kb[KC_COUNT] = {0};  // algorithmic bytes of one launch of each class
 };
 
@@ -497,6 +497,8 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   s->grid_dual = grid_for(nl, std::max(1, occ) * c->nsm);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_norm_x, kBlock, 0);
   s->grid_norm = grid_for(nl, std::max(1, occ) * c->nsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sketch_flush, kBlock, 0);
+  s->grid_flush = grid_for(nl, std::max(1, occ) * c->nsm);
   if (!alloc((void **)&s->gpart, sizeof(double) * (size_t)s->grid_primal * R)) return fail(c, SCG_ENOMEM, "gpart");
 
   cudaStream_t st = c->stream;
@@ -912,7 +914,7 @@ void sketch_flush(scg_ctx *c) {
   for (int j = 0; j < c->spend; ++j) F.ome[j] = c->ome[j];
   for (Shard *s : c->sh)
     launch(c, KC_SKETCH, 8.0 * F.nb * (double)s->nl + 16.0 * c->R * (double)s->nl, k_sketch_flush,
-           dim3(s->grid_dual), dim3(kBlock), s->S, (const double *)s->V, (long long)s->nlpad,
+           dim3(s->grid_flush), dim3(kBlock), s->S, (const double *)s->V, (long long)s->nlpad,
            (const double *)s->ckr, F, (int)s->nl, c->R);
   c->spend = 0;
 }
