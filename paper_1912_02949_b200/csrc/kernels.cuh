@@ -1182,6 +1182,7 @@ __device__ __forceinline__ void emit(XSlot *slot, DevScalars *sc, const Net &net
 // instead of hanging the GPU.
 __global__ void k_pull(int kind, int ns, Net net, DevScalars *sc, FinArgs f) {
   if (threadIdx.x != 0) return;
+  if (sc->err & 2) return;  // an earlier collective timed out: fail fast (reported by synchronize)
   if ((kind == FK_OM || kind == FK_RHO) && sc->brk) return;  // producer skipped (Lanczos break)
   if (kind == FK_BAR && f.i >= sc->k) return;
   const int e = (int)(net.E & 3ull);
