@@ -65,6 +65,10 @@ enum {
                                    default: keep the Lanczos vectors in HBM and combine them in one pass
                                    (Remark "Time-storage tradeoff") -- bitwise identical
                                    results, O(q n) device memory (falls back to two-pass if it does not fit) */
+  SCG_TRACE_LE = 1u << 3,       /* trace-bounded set tr X <= alpha instead of tr X = alpha:
+                                   the LMO is H = alpha v v^T if xi_t < 0, else 0; e.g. the
+                                   DIMACS-style MaxCut setup alpha = 1.05 n.  Trace correction then
+                                   uses the tracked trace tau instead of alpha (reading R29) */
   SCG_PROFILE = 1u << 8         /* record CUDA events around every kernel launch (bench / kernel stats) */
 };
 

@@ -70,7 +70,7 @@ def _load():
         lib.oracle_gamma.argtypes = [I64, D, D, D]
         lib.oracle_create.restype = P
         lib.oracle_create.argtypes = [I64, P, P, P, ctypes.c_int32, D, D, ctypes.c_uint64, ctypes.c_int,
-                                      ctypes.c_int, I64, I64]
+                                      ctypes.c_int, I64, I64, ctypes.c_int]
         lib.oracle_destroy.argtypes = [P]
         lib.oracle_step.restype = ctypes.c_int
         lib.oracle_step.argtypes = [P, I64]
@@ -189,7 +189,7 @@ class Oracle:
     """Alg. 4 SketchyCGAL for MaxCut (C = -L, A = diag, b = 1, alpha = n)."""
 
     def __init__(self, L, R: int, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
-                 scale: bool = True, qfix: int = 0, logcap: int = 0, vhist: int = 0):
+                 scale: bool = True, qfix: int = 0, logcap: int = 0, vhist: int = 0, trace_le: bool = False):
         self.L = L
         self.n = L.n
         self.R = int(R)
@@ -202,7 +202,8 @@ class Oracle:
         self._val = _f64(L.val)
         self._h = _load().oracle_create(self.n, self._rp.ctypes.data, self._col.ctypes.data, self._val.ctypes.data,
                                         self.R, self.alpha_orig, float(beta0), int(seed), 1 if scale else 0,
-                                        int(qfix), self.logcap, self.vhist_cap)
+                                        int(qfix), self.logcap, self.vhist_cap, 1 if trace_le else 0)
+        self.trace_le = bool(trace_le)
         self.beta0 = float(beta0)
 
     def __del__(self):

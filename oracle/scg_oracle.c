@@ -419,6 +419,7 @@ typedef struct {
   int32_t R;
   double alpha_orig, alpha, beta0, bval, nrmL;
   int scale;
+  int trace_le; /* tr X <= alpha: H = alpha v v* if xi < 0, else 0 */
   uint64_t seed;
   int qfix; /* test-only: fixed Lanczos bound (may be n); 0 = schedule */
   int64_t t; /* iterations done */
@@ -441,9 +442,10 @@ typedef struct {
 
 void *oracle_create(int64_t n, const int64_t *rp_L, const int32_t *col_L, const double *val_L, int32_t R,
                     double alpha, double beta0, uint64_t seed, int scale, int qfix, int64_t logcap,
-                    int64_t vhist_cap) {
+                    int64_t vhist_cap, int trace_le) {
   oracle_t *o = (oracle_t *)calloc(1, sizeof(oracle_t));
   o->n = n; o->R = R; o->beta0 = beta0; o->seed = seed; o->scale = scale; o->qfix = qfix;
+  o->trace_le = trace_le;
   o->alpha_orig = alpha;
   /* ||C||_F = ||L||_F over all stored entries (CAC-2), scaling P:1805-1814 (reading A13) */
   int err = 0;
@@ -454,7 +456,7 @@ void *oracle_create(int64_t n, const int64_t *rp_L, const int32_t *col_L, const 
     err |= s.err;
     o->nrmL = sqrt(xs_round(&s));
   }
-  if (scale) { o->alpha = 1.0; o->bval = 1.0 / (double)n; }
+  if (scale) { o->alpha = alpha / (double)n; o->bval = 1.0 / (double)n; } /* X~ = X / n (A13) */
   else { o->alpha = alpha; o->bval = 1.0; }
   /* split L into off-diagonal C entries and diagonal: C = -L, scaled C / ||C||_F */
   int64_t nnz_off = 0;
@@ -552,10 +554,13 @@ int oracle_step(void *h, int64_t T) {
     o_apply(&A, o->cdiag, o->v, o->cv);
     double cval = o_dot(o->v, o->cv, n, &err);
     double one_m_eta = 1.0 - eta;
-    /* line 7: z <- (1 - eta) z + eta A(alpha v v*)  (primitive 3) */
+    /* LMO: H = alpha v v*; for the trace-bounded set tr X <= alpha, H = 0 when xi >= 0
+     * (xi is the Rayleigh quotient approximating lambda_min) */
+    const int hoff = o->trace_le && !(xi < 0.0);
+    /* line 7: z <- (1 - eta) z + eta A(H)  (primitive 3) */
     for (int64_t r = 0; r < n; ++r) {
       double h = o->alpha * (o->v[r] * o->v[r]);
-      o->z[r] = fma(eta, h, one_m_eta * o->z[r]);
+      o->z[r] = hoff ? one_m_eta * o->z[r] : fma(eta, h, one_m_eta * o->z[r]);
     }
     /* line 8: gamma from ||z - b||^2, y <- y + gamma (z - b) */
     for (int64_t r = 0; r < n; ++r) o->a[r] = o->z[r] - o->bval;
@@ -565,20 +570,26 @@ int oracle_step(void *h, int64_t T) {
     /* line 9: NystromSketch.RankOneUpdate(sqrt(alpha) v, eta): S <- (1-eta) S + eta alpha v (v* Omega) */
     for (int kk = 0; kk < R; ++kk) {
       double gk = o_dot(o->v, o->Omega + (int64_t)kk * n, n, &err);
-      double c = (eta * o->alpha) * gk;
+      double c = hoff ? 0.0 : (eta * o->alpha) * gk;
       double *Sk = o->S + (int64_t)kk * n;
       for (int64_t r = 0; r < n; ++r) Sk[r] = fma(c, o->v[r], one_m_eta * Sk[r]);
     }
     /* tau, p */
     double vv = o_dot(o->v, o->v, n, &err);
-    o->tau = fma(eta * o->alpha, vv, one_m_eta * o->tau);
-    o->p = fma(eta * o->alpha, cval, one_m_eta * o->p);
+    if (hoff) {
+      o->tau = one_m_eta * o->tau;
+      o->p = one_m_eta * o->p;
+    } else {
+      o->tau = fma(eta * o->alpha, vv, one_m_eta * o->tau);
+      o->p = fma(eta * o->alpha, cval, one_m_eta * o->p);
+    }
     o->err |= err;
     if (t - 1 < o->logcap) {
       double *L = o->log + (t - 1) * O_LOGW;
       L[0] = (double)t; L[1] = (double)q; L[2] = (double)res.k; L[3] = res.theta; L[4] = xi;
       L[5] = cval; L[6] = o->p; L[7] = sqrt(nz); L[8] = gamma; L[9] = o->tau;
-      const double ax = o->alpha * xi;
+      /* min over the set of <D, H>: alpha xi (tr X = alpha) or alpha min(xi, 0) (tr X <= alpha) */
+      const double ax = o->alpha * ((o->trace_le && xi > 0.0) ? 0.0 : xi);
       L[10] = ((p_t + S_yz) + beta * (S_zz - o->bval * S_z)) - ax;
       const double nbb = ((double)n * o->bval) * o->bval;
       L[11] = ((p_t + o->bval * S_y) + (0.5 * beta) * (S_zz - nbb)) - ax;

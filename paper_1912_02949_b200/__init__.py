@@ -25,6 +25,7 @@ HEADERS = [os.path.join(ROOT, "include", "sketchycgal.h"), os.path.join(ROOT, "s
 SCG_SCALE = 1 << 0
 SCG_TRACE_CORRECT = 1 << 1
 SCG_REGENERATE = 1 << 2
+SCG_TRACE_LE = 1 << 3
 SCG_PROFILE = 1 << 8
 
 STATUS = {0: "SCG_OK", -1: "SCG_EINVAL", -2: "SCG_ENOMEM", -3: "SCG_ECUDA", -4: "SCG_ENCCL", -5: "SCG_ECHOL",
@@ -208,7 +209,7 @@ class SketchyCGAL:
 
     def __init__(self, L, R: int, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
                  scale: bool = True, trace_correct: bool = True, profile: bool = False, device: int = 0,
-                 stream=None, regenerate: bool = False, shards: int = 1, splits=None,
+                 stream=None, regenerate: bool = False, trace_le: bool = False, shards: int = 1, splits=None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
         self.lib = load()
         self.n = int(L.n)
@@ -237,7 +238,8 @@ class SketchyCGAL:
         self._keep = (rp, col, val)
         csr = Csr(self.n, self.row_begin, self.row_end, rp.ctypes.data, col.ctypes.data, val.ctypes.data, 1)
         flags = (SCG_SCALE if scale else 0) | (SCG_TRACE_CORRECT if trace_correct else 0) | \
-                (SCG_PROFILE if profile else 0) | (SCG_REGENERATE if regenerate else 0)
+                (SCG_PROFILE if profile else 0) | (SCG_REGENERATE if regenerate else 0) | \
+                (SCG_TRACE_LE if trace_le else 0)
         self._h = ctypes.c_void_p()
         dptr = None
         if dist is not None:

@@ -53,6 +53,7 @@ struct Csr {
 struct IterArgs {
   long long t;
   int q;
+  int trace_le;  // SCG_TRACE_LE: H = 0 when xi_t >= 0
   double eta, one_m_eta, alpha, b, beta0, sq, beta_next, nbb;  // nbb = fl(fl(n b) b) = ||b||^2
 };
 
@@ -91,9 +92,16 @@ struct Net {
   unsigned long long E;       // epoch of the collective this launch takes part in
 };
 
+#ifndef SCG_STCS
+#define SCG_STCS 0  // 1: evict-first (st.global.cs) stores of the Lanczos outputs
+#endif
 // Store v at dst (this rank's gathered region, own row r) and into every reader rank's copy.
 __device__ __forceinline__ void gstore(const Net &net, double *dst, int r, double v) {
+#if SCG_STCS
+  __stcs(dst, v);
+#else
   *dst = v;
+#endif
   if (net.mask) {
     unsigned m = net.mask[r];
     if (m) {
@@ -1106,7 +1114,8 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
       double gapv, boundv;
       {
         const double beta = A.beta0 * A.sq;
-        const double pt = sc->p, ax = A.alpha * sc->xi;
+        // min over the constraint set of <D_t, H>: alpha xi_t (tr X = alpha), alpha min(xi_t, 0) (tr X <= alpha)
+        const double pt = sc->p, ax = A.alpha * ((A.trace_le && sc->xi > 0.0) ? 0.0 : sc->xi);
         const double zmb_z = sc->my[2] - A.b * sc->my[3];
         double g = pt + sc->my[1];
         g = g + beta * zmb_z;
@@ -1119,8 +1128,13 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
       sc->nz = nz;
       sc->gamma = gamma_rule(A, nz);
       const double ea2 = A.eta * A.alpha;
-      sc->tau = fma(ea2, sc->vv, A.one_m_eta * sc->tau);
-      sc->p = fma(ea2, sc->c, A.one_m_eta * sc->p);
+      if (A.trace_le && !(sc->xi < 0.0)) {  // H = 0: X <- (1 - eta) X
+        sc->tau = A.one_m_eta * sc->tau;
+        sc->p = A.one_m_eta * sc->p;
+      } else {
+        sc->tau = fma(ea2, sc->vv, A.one_m_eta * sc->tau);
+        sc->p = fma(ea2, sc->c, A.one_m_eta * sc->p);
+      }
       scg_iter_rec rec;
       rec.t = A.t;
       rec.q = A.q;
@@ -1293,7 +1307,11 @@ struct EpiA {
   XWin acc[1];
   int err;
   __device__ __forceinline__ void operator()(const RowOut<1> &o) {
+#if SCG_STCS
+    __stcs(&a[o.r], o.s[0]);
+#else
     a[o.r] = o.s[0];
+#endif
 #ifndef SCG_EXP_NODOT
     xwin_add(acc[0], o.xr * o.s[0], err, blk);
 #endif
@@ -1361,10 +1379,13 @@ __global__ void __launch_bounds__(kBlock, 4) k_lanczos_b(const double *__restric
     const double2 *a2 = reinterpret_cast<const double2 *>(a);
     const double2 *xi2 = reinterpret_cast<const double2 *>(Xi + rb);
     const double2 *xm2 = reinterpret_cast<const double2 *>(Xim1 ? Xim1 + rb : Xi + rb);
-    for (int p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += 2 * stride) {
-      double2 av[2], xi[2], xm[2];
+#ifndef SCG_BU
+#define SCG_BU 2
+#endif
+    for (int p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += SCG_BU * stride) {
+      double2 av[SCG_BU], xi[SCG_BU], xm[SCG_BU];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < SCG_BU; ++u) {
         const int p = p0 + u * stride;
         if (p < np) {
           av[u] = __ldcs(&a2[p]);  // a is dead after this step: evict first
@@ -1373,7 +1394,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_lanczos_b(const double *__restric
         }
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < SCG_BU; ++u) {
         const int p = p0 + u * stride;
         if (p < np) {
           row(2 * p, av[u].x, xi[u].x, xm[u].x);
@@ -1706,6 +1727,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
                                                    const double *__restrict__ Om, int nl, int R, IterArgs A,
                                                    double *__restrict__ gpart, XSlot *slot, DevScalars *sc,
                                                    scg_iter_rec *log, Net net) {
+  const bool hoff = A.trace_le && !(sc->xi < 0.0);
   __shared__ double red[kBlock / 32][kMaxR];
   __shared__ XBlk<1> xb;
   xblk_init<1>(xb);
@@ -1736,7 +1758,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
         if (r < nl) {
           if (kc == 0) {
             const double hv = A.alpha * (vr[h] * vr[h]);
-            const double zr = fma(A.eta, hv, A.one_m_eta * zv[h]);
+            // trace-bounded LMO with xi_t >= 0: H = 0
+            const double zr = hoff ? A.one_m_eta * zv[h] : fma(A.eta, hv, A.one_m_eta * zv[h]);
             z[r] = zr;
             const double e = zr - A.b;
             xwin_add(acc[0], e * e, err, xb.l[0]);
@@ -1790,8 +1813,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
                                                         IterArgs A, uint64_t seed, XSlot *slot, DevScalars *sc,
                                                         Net net, const int *__restrict__ orig) {
   const double gam = sc->gamma;
-  if (blockIdx.x == 0 && (int)threadIdx.x < R)
-    ckr[js * kMaxR + threadIdx.x] = (A.eta * A.alpha) * sc->gk[threadIdx.x];
+  if (blockIdx.x == 0 && (int)threadIdx.x < R)  // H = 0 (trace-bounded, xi_t >= 0): no rank-one term
+    ckr[js * kMaxR + threadIdx.x] = (A.trace_le && !(sc->xi < 0.0)) ? 0.0 : (A.eta * A.alpha) * sc->gk[threadIdx.x];
   // exact sums: ||g_{t+1}||^2, and over the next iteration's state (y_{t+1}, z_{t+1}):
   // sum y, y.z, z.z, sum z (surrogate gap / stopping rule, finalize FK_NZ)
   __shared__ XBlk<5> xb;

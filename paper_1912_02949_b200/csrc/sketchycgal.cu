@@ -1033,7 +1033,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   c->seed = seed;
   c->device = device;
   const bool scale = (flags & SCG_SCALE) != 0;
-  c->alpha = scale ? 1.0 : alpha;
+  c->alpha = scale ? alpha / (double)n : alpha;  // X~ = X / n (= 1 for the MaxCut trace n)
   c->b = scale ? 1.0 / (double)n : 1.0;
   c->lnN = std::log((double)n);
   c->log_cap = 1024;
@@ -1216,6 +1216,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     A.beta0 = c->beta0;
     A.beta_next = c->beta0 * std::sqrt((double)(t + 2));
     A.nbb = ((double)c->n * c->b) * c->b;
+    A.trace_le = (c->flags & SCG_TRACE_LE) ? 1 : 0;
     int64_t q = (int64_t)std::ceil(std::sqrt(std::sqrt((double)t)) * c->lnN);
     if (q < 2) q = 2;
     if (q > c->n - 1) q = c->n - 1;
@@ -1580,7 +1581,9 @@ scg_status sketchycgal_reconstruct(scg_ctx *c, double *Uh, double *Lambda, doubl
     cum += c->lam_raw[k];
     c->err[k] = (tau - cum) * unit;
     c->lam_orig[k] = c->lam_raw[k] * unit;
-    c->lam_tc[k] = (c->lam_raw[k] + (c->alpha - tot) / R) * unit;
+    // trace correction (Alg. 4 line 13) to the known trace: alpha, or tau when tr X <= alpha (R29)
+    const double trace = (c->flags & SCG_TRACE_LE) ? tau : c->alpha;
+    c->lam_tc[k] = (c->lam_raw[k] + (trace - tot) / R) * unit;
   }
   const std::vector<double> &lam_out = (c->flags & SCG_TRACE_CORRECT) ? c->lam_tc : c->lam_orig;
   for (int k = 0; k < R; ++k) Lambda[k] = lam_out[k];

@@ -299,3 +299,23 @@ def test_stopping_rule_run(gpu, shards):
     t = g.run(1000, eps=eps, check_every=37)
     assert t == t_o
     assert t_o <= g.t < t_o + 37
+
+
+@pytest.mark.parametrize("shards", [1, 2])
+def test_trace_bounded_lmo(gpu, shards):
+    """f3: tr X <= 1.05 n (SCG_TRACE_LE), H = 0 when xi_t >= 0: trajectory bitwise, the H = 0
+    branch exercised, reconstruction trace-corrected to the tracked trace tau (R29)."""
+    L = si.laplacian("c0")
+    T = 400 if shards == 1 else 150
+    alpha = 1.05 * L.n
+    g = gpu.SketchyCGAL(L, R=10, seed=0, alpha=alpha, trace_le=True, shards=shards)
+    g.step(T)
+    o = oracle.Oracle(L, 10, seed=0, alpha=alpha, trace_le=True, logcap=T)
+    o.step(T)
+    assert np.any(o.log[:, 4] >= 0.0)
+    _assert_trajectory(g, o, T)
+    U, lam, _ = g.reconstruct()
+    Uo, lam_o, _ = oracle.nystrom_reconstruct(o.S, o.Omega, o.tau)
+    lam_tc = oracle.trace_correct(lam_o, o.tau) * L.n
+    np.testing.assert_allclose(lam, lam_tc, rtol=1e-9)
+    assert abs(lam.sum() - o.tau * L.n) <= 1e-9 * abs(o.tau * L.n)

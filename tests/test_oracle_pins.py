@@ -511,3 +511,22 @@ def test_posterior_bound_dominates_suboptimality():
         assert rec[11] <= bound_exact + 1e-12
         ident = float(np.dot(y, z - b)) + 0.5 * beta * float(np.dot(z - b, z - b))
         assert abs((rec[10] - rec[11]) - ident) <= 1e-12 * max(1.0, abs(rec[10]))
+
+
+# ------------------------------------------------------------- f3: trace-bounded LMO
+def test_trace_bounded_sdp_value_and_trace():
+    """tr X <= 1.05 n with H = 0 when xi_t >= 0: diag X = 1 still forces
+    tr X = n at the optimum, so the closed-form SDP value of C5 is recovered; the tracked trace
+    tau_t = tr X_t never exceeds alpha; the H = 0 branch does fire."""
+    n = 5
+    L = _edges_graph(n, [(k, (k + 1) % n) for k in range(n)])
+    sdp = 2 * n * (1 + math.cos(math.pi / n))
+    o = oracle.Oracle(L, 3, seed=5, logcap=3000, alpha=1.05 * n, trace_le=True)
+    o.step(3000)
+    assert abs(o.implicit_objective() - sdp) / sdp < 3e-3
+    assert np.all(o.log[:, 9] <= o.alpha * (1 + 1e-14))
+    assert np.any(o.log[:, 4] >= 0.0)  # some iterations took H = 0
+    # equality run for comparison: same limit
+    oe = oracle.Oracle(L, 3, seed=5, logcap=1)
+    oe.step(3000)
+    assert abs(o.implicit_objective() - oe.implicit_objective()) / sdp < 3e-3
