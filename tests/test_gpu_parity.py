@@ -301,18 +301,29 @@ def test_stopping_rule_run(gpu, shards):
     assert t_o <= g.t < t_o + 37
 
 
-@pytest.mark.parametrize("shards", [1, 2])
-def test_trace_bounded_lmo(gpu, shards):
-    """f3: tr X <= 1.05 n (SCG_TRACE_LE), H = 0 when xi_t >= 0: trajectory bitwise, the H = 0
-    branch exercised, reconstruction trace-corrected to the tracked trace tau (R29)."""
-    L = si.laplacian("c0")
-    T = 400 if shards == 1 else 150
+def _psd_cost_graph():
+    """All-negative weights: C = -L is psd, so xi_t >= 0 (H = 0) happens early."""
+    rng = np.random.default_rng(1)
+    n = 60
+    i, j = np.triu_indices(n, 1)
+    keep = rng.random(len(i)) < 0.1
+    return si.laplacian_from_edges(n, i[keep], j[keep], -np.ones(int(keep.sum())))
+
+
+@pytest.mark.parametrize("graph,shards", [("psd", 1), ("psd", 3), ("c0", 1), ("c0", 2)])
+def test_trace_bounded_lmo(gpu, graph, shards):
+    """f3: tr X <= 1.05 n (SCG_TRACE_LE), H = 0 when xi_t >= 0: trajectory bitwise (the H = 0
+    branch fires on the psd-cost graph), reconstruction trace-corrected to the tracked trace (R29)."""
+    L = _psd_cost_graph() if graph == "psd" else si.laplacian("c0")
+    T = 300
+    R = 4 if graph == "psd" else 10
     alpha = 1.05 * L.n
-    g = gpu.SketchyCGAL(L, R=10, seed=0, alpha=alpha, trace_le=True, shards=shards)
+    g = gpu.SketchyCGAL(L, R=R, seed=3, alpha=alpha, trace_le=True, shards=shards)
     g.step(T)
-    o = oracle.Oracle(L, 10, seed=0, alpha=alpha, trace_le=True, logcap=T)
+    o = oracle.Oracle(L, R, seed=3, alpha=alpha, trace_le=True, logcap=T)
     o.step(T)
-    assert np.any(o.log[:, 4] >= 0.0)
+    if graph == "psd":
+        assert np.any(o.log[:, 4] >= 0.0)
     _assert_trajectory(g, o, T)
     U, lam, _ = g.reconstruct()
     Uo, lam_o, _ = oracle.nystrom_reconstruct(o.S, o.Omega, o.tau)
