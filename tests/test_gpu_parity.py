@@ -174,6 +174,14 @@ def test_config3_first_iteration_bitwise(gpu):
     _assert_trajectory(g, o, 1)
 
 
+def test_config4_first_iteration_bitwise(gpu):
+    """configs[4] at full size (n = 2^25, non-uniform weights, random matching edges): one whole
+    iteration bitwise (R = 2 keeps the oracle's Omega work small; R does not enter the matvecs)."""
+    L = si.laplacian("c4")
+    g, o = _run_pair(gpu, L, 2, 1, seed=4)
+    _assert_trajectory(g, o, 1)
+
+
 def test_shared_divisor_division_is_ieee(gpu):
     """div_rn (RN(1/b) + two fma corrections) must equal the hardware division bit for bit."""
     for seed in (1, 2, 3):
