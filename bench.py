@@ -174,7 +174,7 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
 
     with torch.cuda.stream(stream):
-        solver = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], profile=True, device=local_rank,
+        solver = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], profile=not args.no_profile, device=local_rank,
                                  stream=ctypes_stream(stream), **dkw)
         solver.step(W)
         solver.synchronize()
@@ -299,6 +299,7 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-profile", action="store_true", help="no per-kernel events (no roofline line)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:  # not under torchrun: relaunch one process per GPU
         import random

@@ -134,7 +134,8 @@ typedef struct {
 typedef struct {
   char name[32];
   int64_t launches;
-  double total_ms;          /* sum of CUDA-event durations on the context stream */
+  double total_ms;          /* CUDA-event time on the context stream: every 16th launch of the class is
+                               timed (env SCG_PROF_EVERY), the sum extrapolated to all launches */
   double bytes_per_launch;  /* algorithmic HBM bytes of one launch */
 } scg_kstat;
 

@@ -49,6 +49,16 @@ struct Csr {
   const double *val;
 };
 
+// Programmatic dependent launch: every kernel is launched with programmatic stream
+// serialization, waits at entry until the previous grid has completed and flushed
+// (griddepcontrol.wait), then lets the next grid be scheduled while it runs.  Launch
+// latency and block scheduling overlap the previous kernel's tail; all data dependences
+// are honored by the wait.  (No-ops when launched without the attribute.)
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Host-computed scalars of iteration t (CAC-6).
 struct IterArgs {
   long long t;
@@ -1195,6 +1205,7 @@ __device__ __forceinline__ void emit(XSlot *slot, DevScalars *sc, const Net &net
 // A lost flag (a bug or a dead peer) ends the wait after ~2^34 cycles with sc->err = 2
 // instead of hanging the GPU.
 __global__ void k_pull(int kind, int ns, Net net, DevScalars *sc, FinArgs f) {
+  pdl_entry();
   if (threadIdx.x != 0) return;
   if (sc->err & 2) return;  // an earlier collective timed out: fail fast (reported by synchronize)
   if ((kind == FK_OM || kind == FK_RHO) && sc->brk) return;  // producer skipped (Lanczos break)
@@ -1234,6 +1245,7 @@ __global__ void k_pull(int kind, int ns, Net net, DevScalars *sc, FinArgs f) {
 // direction) and the diagonal (scaling).
 __global__ void k_frob(const double *__restrict__ w, long long nnz, const double *__restrict__ diag, int nl,
                        XSlot *slot, DevScalars *sc, double *out, Net net) {
+  pdl_entry();
   __shared__ XBlk<1> xb;
   xblk_init<1>(xb);
   XWin acc[1];
@@ -1253,6 +1265,7 @@ __global__ void k_frob(const double *__restrict__ w, long long nnz, const double
 __global__ void k_scale_c(const double *__restrict__ w, long long nnz, const double *__restrict__ ldiag, int nl,
                           const double *__restrict__ nrm_ptr, int scale, double *__restrict__ val,
                           double *__restrict__ cdiag) {
+  pdl_entry();
   const double nrm = *nrm_ptr;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
   for (long long k = tid; k < nnz; k += st) val[k] = scale ? w[k] / nrm : w[k];
@@ -1264,6 +1277,7 @@ __global__ void k_scale_c(const double *__restrict__ w, long long nnz, const dou
 // (DESIGN.md section 5); the seeded streams are indexed by the ORIGINAL vertex id.
 __global__ void k_omega(double *__restrict__ Om, int nl, long long rb, int R, uint64_t seed,
                         const int *__restrict__ orig) {
+  pdl_entry();
   const long long tot = (long long)nl * R;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
     const int k = (int)(e / nl);
@@ -1275,6 +1289,7 @@ __global__ void k_omega(double *__restrict__ Om, int nl, long long rb, int R, ui
 // d = fl(fma(beta, fl(z - b), y) + C_rr) (primitive 2 with y + beta (z - b)).
 __global__ void k_init_d(const double *__restrict__ z, const double *__restrict__ y, const double *__restrict__ cdiag,
                          double *__restrict__ d, int nl, double b, double beta) {
+  pdl_entry();
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x)
     d[r] = fma(beta, z[r] - b, y[r]) + cdiag[r];
 }
@@ -1283,6 +1298,7 @@ __global__ void k_init_d(const double *__restrict__ z, const double *__restrict_
 __global__ void __launch_bounds__(kBlock) k_gen_start(double *__restrict__ g, int nl, long long rb, uint64_t seed,
                                                       long long t, XSlot *slot, DevScalars *sc, Net net,
                                                       const int *__restrict__ orig) {
+  pdl_entry();
   __shared__ XBlk<1> xb;
   xblk_init<1>(xb);
   XWin acc[1];
@@ -1323,6 +1339,7 @@ __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_a(Csr C,
                                                          const double *__restrict__ X, int nl, long long rb, int i,
                                                          double *__restrict__ a, XSlot *slot, DevScalars *sc,
                                                          Net net) {
+  pdl_entry();
   if (sc->brk) return;
   const double den = sc->rho[i - 1];
   __shared__ XBlk<1> xb;
@@ -1355,6 +1372,7 @@ __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_a(Csr C,
 __global__ void __launch_bounds__(kBlock, 4) k_lanczos_b(const double *__restrict__ a, const double *Xi,
                                                       const double *Xim1, double *Xip1, int nl, long long rb,
                                                       int i, XSlot *slot, DevScalars *sc, Net net) {
+  pdl_entry();
   if (sc->brk) return;
   const double om = sc->om[i - 1];
   const double den = sc->rho[i - 1];
@@ -1455,6 +1473,7 @@ __device__ int sturm_count(const double *om, const double *rho2, int k, double x
 // One warp: multisection (32 Sturm counts per round, one per lane) for theta, then
 // inverse iteration (lane 0, partial pivoting) for s (Alg. 2 lines 11-12).
 __global__ void k_tridiag(DevScalars *sc, int q) {
+  pdl_entry();
   __shared__ double om[kMaxQ], rho[kMaxQ], rho2[kMaxQ];
   const int lane = threadIdx.x;
   const int k = sc->brk ? sc->k : q;
@@ -1584,6 +1603,7 @@ __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_c(Csr C,
                                                          const double *__restrict__ Xj, const double *Xjm1,
                                                          double *Xjp1, double *__restrict__ x, int nl, long long rb,
                                                          int j, DevScalars *sc, XSlot *slot, Net net) {
+  pdl_entry();
   if (j >= sc->k) return;  // sc->k holds the effective k after k_tridiag
   EpiC epi{Xjm1, Xjp1, x, rb, &net, j, sc->om[j - 1], sc->rho[j - 1], j >= 2 ? sc->rho[j - 2] : 1.0, sc->rho[j],
            sc->s[0], sc->s[j], 1.0 / sc->rho[j], 1.0 / (j >= 2 ? sc->rho[j - 2] : 1.0)};
@@ -1611,6 +1631,7 @@ __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_c(Csr C,
 __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict__ Wst, long long ldw,
                                                        double *__restrict__ x, int nl, long long rb, XSlot *slot,
                                                        DevScalars *sc, Net net) {
+  pdl_entry();
   __shared__ double s_s[kMaxQ], s_r[kMaxQ], s_rr[kMaxQ];
   const int k = sc->k;
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
@@ -1645,6 +1666,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict_
 // ||x||^2 (exact); k == 1 case: x = s_1 v_1.
 __global__ void __launch_bounds__(kBlock) k_norm_x(const double *__restrict__ g, double *__restrict__ x, int nl,
                                                    long long rb, XSlot *slot, DevScalars *sc, Net net) {
+  pdl_entry();
   const bool k1 = sc->k == 1;
   const double s1 = sc->s[0], rden = 1.0 / sc->rho[0];
   __shared__ XBlk<1> xb;
@@ -1695,6 +1717,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
                                                        const double *__restrict__ cdiag, const double *__restrict__ x,
                                                        double *__restrict__ v, int nl, long long rb, XSlot *slot,
                                                        DevScalars *sc, Net net) {
+  pdl_entry();
   const double nu = sc->nu_x;
   __shared__ XBlk<3> xb;
   xblk_init<3>(xb);
@@ -1727,6 +1750,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
                                                    const double *__restrict__ Om, int nl, int R, IterArgs A,
                                                    double *__restrict__ gpart, XSlot *slot, DevScalars *sc,
                                                    scg_iter_rec *log, Net net) {
+  pdl_entry();
   const bool hoff = A.trace_le && !(sc->xi < 0.0);
   __shared__ double red[kBlock / 32][kMaxR];
   __shared__ XBlk<1> xb;
@@ -1812,6 +1836,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
                                                         double *__restrict__ g, int nl, long long rb, int R,
                                                         IterArgs A, uint64_t seed, XSlot *slot, DevScalars *sc,
                                                         Net net, const int *__restrict__ orig) {
+  pdl_entry();
   const double gam = sc->gamma;
   if (blockIdx.x == 0 && (int)threadIdx.x < R)  // H = 0 (trace-bounded, xi_t >= 0): no rank-one term
     ckr[js * kMaxR + threadIdx.x] = (A.trace_le && !(sc->xi < 0.0)) ? 0.0 : (A.eta * A.alpha) * sc->gk[threadIdx.x];
@@ -1868,6 +1893,7 @@ struct FlushArgs {
 __global__ void __launch_bounds__(kBlock) k_sketch_flush(double *__restrict__ S, const double *__restrict__ V,
                                                          long long ldv, const double *__restrict__ ckr, FlushArgs F,
                                                          int nl, int R) {
+  pdl_entry();
   __shared__ double ck[kSketchB][kMaxR];
   for (int e = threadIdx.x; e < F.nb * kMaxR; e += blockDim.x) ck[e / kMaxR][e % kMaxR] = ckr[e];
   __syncthreads();
@@ -1898,6 +1924,7 @@ __global__ void __launch_bounds__(kBlock) k_sketch_flush(double *__restrict__ S,
 // out = (A + beta B) M   (n x R times R x R), row-wise; M in shared memory.
 __global__ void k_rowmat(double *__restrict__ out, const double *__restrict__ A, const double *__restrict__ B,
                          double beta, const double *__restrict__ M, int nl, int R) {
+  pdl_entry();
   __shared__ double Ms[kMaxR * kMaxR];
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) Ms[e] = M[e];
   __syncthreads();
@@ -1919,6 +1946,7 @@ __global__ void k_rowmat(double *__restrict__ out, const double *__restrict__ A,
 // partial[pair][block] of column dot products A[:,i]^T B[:,j]  (pair = i*R + j).
 __global__ void k_colpair(const double *__restrict__ A, const double *__restrict__ B, int nl, int R,
                           double *__restrict__ partial) {
+  pdl_entry();
   __shared__ double red[kBlock / 32];
   const int pair = blockIdx.y;
   const int i = pair / R, j = pair % R;
@@ -1945,6 +1973,7 @@ __global__ void k_colstats(const int *__restrict__ rp, const int *__restrict__ c
                            const double *__restrict__ ldiag, const double *__restrict__ U, const double *__restrict__ Ug,
                            long long ldg, int k0, const double *__restrict__ lam, int nl, long long rb, int R,
                            int which, double *__restrict__ partial) {
+  pdl_entry();
   __shared__ double red[kBlock / 32];
   const int kcol = k0 + (int)blockIdx.y;
   const double *Ufull = Ug + (long long)blockIdx.y * ldg;
@@ -1991,6 +2020,7 @@ __global__ void k_colstats(const int *__restrict__ rp, const int *__restrict__ c
 // reader ranks' gathered region at global indices), then a barrier collective.
 __global__ void k_push_col(const double *__restrict__ Ucol, double *__restrict__ xg, int nl, long long rb,
                            XSlot *slot, DevScalars *sc, Net net) {
+  pdl_entry();
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x)
     gstore(net, xg + rb + r, r, Ucol[r]);
   if (ticket_only(slot) && threadIdx.x == 0) {
@@ -2010,6 +2040,7 @@ template <bool UNI>
 __global__ void __launch_bounds__(kBlock) k_apply_d(Csr C, Rows RL, const double *__restrict__ d,
                                                     const double *__restrict__ X, int nl, long long rb,
                                                     double *__restrict__ y) {
+  pdl_entry();
   EpiY epi{y};
 #if SCG_ENGINE == 1
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -2024,12 +2055,14 @@ __global__ void __launch_bounds__(kBlock) k_apply_d(Csr C, Rows RL, const double
 
 // out[orig[r]] = in[r]: device rows back to input order (outputs).
 __global__ void k_unperm(double *__restrict__ out, const double *__restrict__ in, const int *__restrict__ orig, int nl) {
+  pdl_entry();
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) out[orig[r]] = in[r];
 }
 
 // Self-test: div_rn against the hardware IEEE division on pseudo-random operands
 // (mantissas drawn uniformly, including the extremes 1 and 2 - ulp), exponents in +-60.
 __global__ void k_selftest_div(long long n, uint64_t seed, unsigned long long *mismatch) {
+  pdl_entry();
   unsigned long long bad = 0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     scg_philox_out o = scg_draw(seed, 77u, 0u, (uint64_t)i);

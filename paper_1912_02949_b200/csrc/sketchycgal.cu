@@ -117,6 +117,7 @@ struct scg_ctx {
   uint64_t seed = 0;
   // sharding: world ranks; this context holds shards sh (all of them when emulating)
   int world = 1, mode = 0;  // mode 0: single, 1: emulated shards, 2: one rank of a multi-process job
+  bool pdl = true;          // programmatic dependent launches (SCG_PDL=0 disables)
   int rank = 0;
   std::vector<int64_t> splits;
   std::vector<Shard *> sh;
@@ -144,6 +145,8 @@ struct scg_ctx {
   std::vector<EvPair> pending;
   std::vector<cudaEvent_t> evpool;
   int64_t kl[KC_COUNT] = {0};
+  int64_t ks[KC_COUNT] = {0};  // launches timed (every prof_every-th launch of each class)
+  int prof_every = 16;
   double kms[KC_COUNT] = {0};
   double kbytes_sum[KC_COUNT] = {0};
   // errors
@@ -216,7 +219,10 @@ cudaEvent_t ev_get(scg_ctx *c) {
 
 template <typename Kern, typename... Args>
 void launch_smem(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 block, size_t smem, Args... args) {
-  const bool prof = (c->flags & SCG_PROFILE) != 0;
+  // SCG_PROFILE: CUDA events around every prof_every-th launch of each kernel class (events
+  // between kernels serialize programmatic launches; timing all of them costs ~5% on c3)
+  const bool prof = (c->flags & SCG_PROFILE) != 0 && c->kl[cls] % c->prof_every == 0;
+  if (prof) c->ks[cls]++;
   EvPair p{};
   if (prof) {
     if (c->pending.size() >= 8192) ev_flush(c);
@@ -225,7 +231,21 @@ void launch_smem(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 b
     p.cls = cls;
     cudaEventRecord(p.a, c->stream);
   }
-  kern<<<grid, block, smem, c->stream>>>(args...);
+  if (c->pdl) {  // programmatic dependent launch (kernels.cuh pdl_entry)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+  } else {
+    kern<<<grid, block, smem, c->stream>>>(args...);
+  }
   if (prof) {
     cudaEventRecord(p.b, c->stream);
     c->pending.push_back(p);
@@ -1037,6 +1057,10 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   c->b = scale ? 1.0 / (double)n : 1.0;
   c->lnN = std::log((double)n);
   c->log_cap = 1024;
+  {
+    const char *e = std::getenv("SCG_PDL");
+    c->pdl = !(e && e[0] == '0');
+  }
   c->npad = (n + 4 + kWin - 1) / kWin * kWin;  // >= 16 bytes of slack for the bulk copies
 
   // ---- sharding mode and row splits
@@ -1179,8 +1203,12 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   pull_all(c, FK_RHO0, 1, E1, FinArgs{});
   if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) return bad(SCG_ECUDA);
   tick("layout+omega");
-  for (int k = 0; k < KC_COUNT; ++k) { c->kl[k] = 0; c->kms[k] = 0; c->kbytes_sum[k] = 0; }
+  for (int k = 0; k < KC_COUNT; ++k) { c->kl[k] = 0; c->ks[k] = 0; c->kms[k] = 0; c->kbytes_sum[k] = 0; }
   c->launches = 0;
+  {
+    const char *e = std::getenv("SCG_PROF_EVERY");
+    if (e && std::atoi(e) > 0) c->prof_every = std::atoi(e);
+  }
   *out = c;
   return SCG_OK;
 }
@@ -1730,7 +1758,7 @@ int32_t sketchycgal_kernel_stats(scg_ctx *c, scg_kstat *out, int32_t max) {
     std::memset(&out[cnt], 0, sizeof(scg_kstat));
     std::snprintf(out[cnt].name, sizeof(out[cnt].name), "%s", kKClassName[k]);
     out[cnt].launches = c->kl[k];
-    out[cnt].total_ms = c->kms[k];
+    out[cnt].total_ms = c->ks[k] ? c->kms[k] * (double)c->kl[k] / (double)c->ks[k] : 0.0;  // extrapolated
     out[cnt].bytes_per_launch = c->kl[k] ? c->kbytes_sum[k] / (double)c->kl[k] : 0.0;
     ++cnt;
   }
@@ -1740,7 +1768,7 @@ int32_t sketchycgal_kernel_stats(scg_ctx *c, scg_kstat *out, int32_t max) {
 void sketchycgal_reset_stats(scg_ctx *c) {
   if (!c) return;
   ev_flush(c);
-  for (int k = 0; k < KC_COUNT; ++k) { c->kl[k] = 0; c->kms[k] = 0; c->kbytes_sum[k] = 0; }
+  for (int k = 0; k < KC_COUNT; ++k) { c->kl[k] = 0; c->ks[k] = 0; c->kms[k] = 0; c->kbytes_sum[k] = 0; }
   c->launches = 0;
 }
 
