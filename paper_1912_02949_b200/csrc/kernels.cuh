@@ -439,17 +439,32 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
       for (int u = 0; u < 4; ++u)
         if (u < w) stepv(c0[u], g0[u], v0[u]);
     }
-    for (int j0 = 4; j0 < w; j0 += 4) {  // rows longer than four slots
-      int cx[4];
-      double gx[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) cx[u] = j0 + u < w ? __ldg(&RL.scol[m0.x + (j0 + u) * 32 + lane]) : -1;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) gx[u] = cx[u] != -1 ? __ldg(&X[cx[u] & 0x7fffffff]) : 0.0;
+    if (w > 4) {  // rows longer than four slots: the next chunk's columns load while this chunk runs
+      int cn[4];
+      double vn[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        if (UNI) step(cx[u], gx[u]);
-        else stepv(cx[u], gx[u], cx[u] != -1 ? __ldg(&RL.sval[m0.x + (j0 + u) * 32 + lane]) : 0.0);
+        cn[u] = 4 + u < w ? __ldg(&RL.scol[m0.x + (4 + u) * 32 + lane]) : -1;
+        vn[u] = (!UNI && cn[u] != -1) ? __ldg(&RL.sval[m0.x + (4 + u) * 32 + lane]) : 0.0;
+      }
+      for (int j0 = 4; j0 < w; j0 += 4) {
+        int cx[4];
+        double gx[4], vx[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { cx[u] = cn[u]; vx[u] = vn[u]; }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) gx[u] = cx[u] != -1 ? __ldg(&X[cx[u] & 0x7fffffff]) : 0.0;
+        const int j1 = j0 + 4;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          cn[u] = j1 + u < w ? __ldg(&RL.scol[m0.x + (j1 + u) * 32 + lane]) : -1;
+          vn[u] = (!UNI && cn[u] != -1) ? __ldg(&RL.sval[m0.x + (j1 + u) * 32 + lane]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (UNI) step(cx[u], gx[u]);
+          else stepv(cx[u], gx[u], vx[u]);
+        }
       }
     }
     if (ok) epi(o);
