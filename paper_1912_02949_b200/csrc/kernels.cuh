@@ -23,6 +23,10 @@ namespace scg {
 constexpr int kMaxQ = 128;   // Lanczos bound cap (max q_t in configs[0..4] is 94)
 constexpr int kMaxR = 64;    // sketch rank cap (BASELINE: R <= 50)
 constexpr int kBlock = 256;
+#ifndef SCG_BLOCK_A
+#define SCG_BLOCK_A 256
+#endif
+constexpr int kBlockA = SCG_BLOCK_A;  // threads per block of k_lanczos_a (the SpMV of pass 1)
 
 // Device-resident scalars of the current iteration.
 struct DevScalars {
@@ -1350,7 +1354,7 @@ struct EpiA {
 };
 
 template <bool UNI>
-__global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
+__global__ void __launch_bounds__(kBlockA, UNI ? SCG_MINB * kBlock / kBlockA : 2 * kBlock / kBlockA) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ X, int nl, long long rb, int i,
                                                          double *__restrict__ a, XSlot *slot, DevScalars *sc,
                                                          Net net) {

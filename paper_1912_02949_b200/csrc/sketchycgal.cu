@@ -101,7 +101,7 @@ struct Shard {
   int64_t halo_rows = 0;
   // grids
   int grid_rows = 1, grid_primal = 1, grid_tiles = 1, grid_b = 1, grid_comb = 1, grid_dual = 1, grid_norm = 1,
-      grid_mon = 1, grid_flush = 1;
+      grid_mon = 1, grid_flush = 1, grid_a = 1;
   double kb[KC_COUNT] = {0};  // algorithmic bytes of one launch of each class
 };
 
@@ -796,6 +796,14 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
                      : SCG_ENGINE == 2 ? (int)std::max<int64_t>((nl + kCW - 1) / kCW, (s->nlong + 7) / 8)
                                        : (int)std::max<int64_t>((s->nslice + 7) / 8, (s->nlong + 7) / 8);
     s->grid_tiles = std::max(1, std::min(need, std::max(1, oa) * c->nsm));
+    {  // k_lanczos_a may use its own block size (kBlockA)
+      int oA = 1;
+      if (U) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oA, k_lanczos_a<true>, kBlockA, s->smem1);
+      else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oA, k_lanczos_a<false>, kBlockA, s->smem1);
+      const int needA = SCG_ENGINE == 0 ? (int)std::max<int64_t>((s->nslice + kBlockA / 32 - 1) / (kBlockA / 32), 1)
+                                        : need;
+      s->grid_a = std::max(1, std::min(needA, std::max(1, oA) * c->nsm));
+    }
     s->grid_mon = std::max(1, std::min(need, std::max(1, om) * c->nsm));
     if (std::getenv("SCG_DEBUG"))
       std::fprintf(stderr, "[scg] shard %d: nl=%lld tiles=%d long=%d uni=%d H=%d out=%lld/%lld smem1=%zu occ_a=%d occ_m=%d grid=%d\n",
@@ -1274,7 +1282,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
         Csr C{s->rp, s->col, s->val};
         Rows TT = rows_of(s, c->n);
         auto kA = s->sell_uniform ? k_lanczos_a<true> : k_lanczos_a<false>;
-        launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->grid_tiles), dim3(kBlock), s->smem1, C, TT,
+        launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->grid_a), dim3(kBlockA), s->smem1, C, TT,
                (const double *)s->d, (const double *)slot(s, i), (int)s->nl, (long long)s->rb, i, s->a,
                s->slots + SLOT_OM, s->sc, net_of(c, s, E));
       }
