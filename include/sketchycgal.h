@@ -75,7 +75,9 @@ enum {
 /* This rank's rows [row_begin, row_end) of the symmetric weighted Laplacian
  * L = sum_{ij in E} w_ij (e_i - e_j)(e_i - e_j)^T  (eqn:comb-laplacian).
  * Off-diagonal entries are L_ij = -w_ij (any sign: signed weights are accepted).
- * Columns must be strictly ascending within a row and global (0..n_global-1). */
+ * Columns must be strictly ascending within a row and global (0..n_global-1).  The pattern
+ * must be symmetric (row-sharded runs derive the halo from it; an emulated-shard init
+ * checks it and returns SCG_EINVAL, a multi-process rank cannot see the other rows). */
 typedef struct {
   int64_t n_global;
   int64_t row_begin, row_end;

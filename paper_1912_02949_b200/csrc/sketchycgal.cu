@@ -410,6 +410,22 @@ scg_status validate_rows(scg_ctx *c, const int64_t *rp, const int32_t *colp, con
   return SCG_OK;
 }
 
+// Structural symmetry of the full CSR (every stored (r, c) has a stored (c, r)): the halo
+// plan derives the reader ranks of row r from row r's own columns, which is exact only for
+// a symmetric pattern (L is symmetric, eqn:comb-laplacian P:97-100).
+bool csr_symmetric(const int64_t *rp, const int32_t *col, int64_t n) {
+  int bad = 0;
+#pragma omp parallel for schedule(static, 4096) reduction(| : bad)
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t k = rp[r]; k < rp[r + 1] && !bad; ++k) {
+      const int64_t c2 = col[k];
+      const int32_t *b = col + rp[c2], *e = col + rp[c2 + 1];
+      const int32_t *f = std::lower_bound(b, e, (int32_t)r);
+      if (f == e || *f != r) bad = 1;
+    }
+  return !bad;
+}
+
 // Host part of shard construction: split this shard's rows into off-diagonal
 // weights w = -L_rj and the diagonal, the long-row list, the SELL-32-sigma layout of
 // the short rows and the halo mask; then allocate and upload.  rp/colp/valp point at
@@ -1100,6 +1116,8 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   {
     const int64_t nrows = L->row_end - L->row_begin;
     if (validate_rows(c, L->row_ptr, L->col_idx, L->val, nrows)) return bad(SCG_EINVAL);
+    // sharded runs need a symmetric pattern (halo plan); checkable here when all rows are given
+    if (c->mode == 1 && !csr_symmetric(L->row_ptr, L->col_idx, n)) return bad(SCG_EINVAL);
   }
 
   // ---- device setup

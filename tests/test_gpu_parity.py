@@ -338,3 +338,22 @@ def test_trace_bounded_lmo(gpu, graph, shards):
     lam_tc = oracle.trace_correct(lam_o, o.tau) * L.n
     np.testing.assert_allclose(lam, lam_tc, rtol=1e-9)
     assert abs(lam.sum() - o.tau * L.n) <= 1e-9 * abs(o.tau * L.n)
+
+
+def test_sharded_rejects_asymmetric_pattern(gpu):
+    """The halo plan is exact only for a symmetric pattern: an emulated-shard init rejects an
+    asymmetric CSR (SCG_EINVAL), a single-GPU init accepts it."""
+    L = si.laplacian("c1")
+    rp, col, val = L.row_ptr.copy(), L.col.copy(), L.val.copy()
+    # drop one off-diagonal entry of row 5 (not its transpose): structurally asymmetric
+    r = 5
+    a, b = int(rp[r]), int(rp[r + 1])
+    k = next(k for k in range(a, b) if col[k] != r)
+    keep = np.ones(len(col), dtype=bool)
+    keep[k] = False
+    rp2 = rp.copy()
+    rp2[r + 1:] -= 1
+    bad = si.CSR(L.n, rp2, col[keep], val[keep])
+    with pytest.raises(gpu.ScgError):
+        gpu.SketchyCGAL(bad, R=4, seed=1, shards=2)
+    gpu.SketchyCGAL(bad, R=4, seed=1).close()
