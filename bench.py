@@ -130,7 +130,9 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "iterations/s", "n_gpus": world,
             "steps": iters, "warmup": 0, "ms_per_step": 1e3 / cb["value"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config_dict(args.config, L, world, 1, iters),
+            # same workload/config as our arm (t = W+1..W+K); the bounded sample actually timed is
+            # described in cpu_baseline.sample
+            "config": _config_dict(args.config, L, world, args.warmup + 1, args.warmup + args.steps),
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
