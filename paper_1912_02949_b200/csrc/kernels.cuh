@@ -1271,8 +1271,8 @@ __global__ void k_frob(const double *__restrict__ w, long long nnz, const double
   xwin_init(acc[0]);
   int err = 0;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
-  for (long long k = tid; k < nnz; k += st) xwin_add(acc[0], w[k] * w[k], err, xb.l[0]);
-  for (long long r = tid; r < nl; r += st) xwin_add(acc[0], diag[r] * diag[r], err, xb.l[0]);
+  for (long long k = tid; k < nnz; k += st) xwin_add_nn(acc[0], w[k] * w[k], err, xb.l[0]);
+  for (long long r = tid; r < nl; r += st) xwin_add_nn(acc[0], diag[r] * diag[r], err, xb.l[0]);
   if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0) {
     FinArgs f{};
     f.out = out;
@@ -1326,7 +1326,7 @@ __global__ void __launch_bounds__(kBlock) k_gen_start(double *__restrict__ g, in
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
     const double v = scg_lanczos_start(seed, t, rb + orig[r]);
     gstore(net, g + rb + r, r, v);
-    xwin_add(acc[0], v * v, err, xb.l[0]);
+    xwin_add_nn(acc[0], v * v, err, xb.l[0]);
   }
   if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
     emit<1>(slot, sc, net, FK_RHO0, FinArgs{}, nullptr);
@@ -1388,7 +1388,10 @@ __global__ void __launch_bounds__(kBlockA, UNI ? SCG_MINB * kBlock / kBlockA : 2
 
 // Step i, part B (Alg. 2 lines 6-7): w_{i+1} = fma(-rho_{i-1}, v_{i-1}, fma(-omega_i, v_i, a)),
 // rho_i = ||w_{i+1}|| (exact); breakdown test.  Writes the un-normalized w_{i+1}.
-__global__ void __launch_bounds__(kBlock, 4) k_lanczos_b(const double *__restrict__ a, const double *Xi,
+#ifndef SCG_MINB_B
+#define SCG_MINB_B 4
+#endif
+__global__ void __launch_bounds__(kBlock, SCG_MINB_B) k_lanczos_b(const double *__restrict__ a, const double *Xi,
                                                       const double *Xim1, double *Xip1, int nl, long long rb,
                                                       int i, XSlot *slot, DevScalars *sc, Net net) {
   pdl_entry();
@@ -1408,7 +1411,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_lanczos_b(const double *__restric
     double w = fma(-om, vi, av);
     if (i >= 2) w = fma(-den, (xm) * rdenm, w);  // rho_{i-1} = rho[i-1] = den
     gstore(net, Xip1 + rb + r, r, w);
-    xwin_add(acc[0], w * w, err, xb.l[0]);
+    xwin_add_nn(acc[0], w * w, err, xb.l[0]);
   };
   if ((rb & 1) == 0) {
     // 16-byte vectors: thread handles row pairs (2p, 2p+1), two pairs in flight
@@ -1461,6 +1464,88 @@ __global__ void __launch_bounds__(kBlock, 4) k_lanczos_b(const double *__restric
         if (r < nl) row(r, av[u], xi[u], xm[u]);
       }
     }
+  }
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0) {
+    FinArgs f{};
+    f.i = i;
+    emit<1>(slot, sc, net, FK_RHO, f, nullptr);
+  }
+}
+
+// TMA-staged variant of k_lanczos_b (the same arithmetic, row by row): tiles of kBT rows of
+// a, X_i and X_{i-1} are bulk-copied (cp.async.bulk, mbarrier completion) into shared
+// memory, kBS stages deep, by one thread; the block computes the tile from shared memory.
+// The bytes in flight live in shared memory, not registers, so the exact-sum window keeps
+// its registers without limiting the memory-level parallelism.
+#ifndef SCG_BT
+#define SCG_BT 2048
+#endif
+#ifndef SCG_BS
+#define SCG_BS 3
+#endif
+constexpr int kBT = SCG_BT;  // rows per tile
+constexpr int kBS = SCG_BS;  // stages
+struct __align__(16) BStage {
+  double a[kBT + 2], xi[kBT + 4], xm[kBT + 4];
+};
+struct __align__(16) BSmem {
+  BStage st[kBS];
+  unsigned long long bar[kBS];
+};
+
+__global__ void __launch_bounds__(kBlock, 2) k_lanczos_b_tma(const double *__restrict__ a, const double *Xi,
+                                                            const double *Xim1, double *Xip1, int nl, long long rb,
+                                                            int i, XSlot *slot, DevScalars *sc, Net net) {
+  pdl_entry();
+  if (sc->brk) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  BSmem &sm = *reinterpret_cast<BSmem *>(smraw);
+  const double om = sc->om[i - 1];
+  const double den = sc->rho[i - 1];
+  const double denm = i >= 2 ? sc->rho[i - 2] : 1.0;
+  const double rden = 1.0 / den, rdenm = 1.0 / denm;
+  __shared__ XBlk<1> xb;
+  xblk_init<1>(xb);
+  XWin acc[1];
+  xwin_init(acc[0]);
+  int err = 0;
+  const int ntile = (nl + kBT - 1) / kBT;
+  const int J = ntile > (int)blockIdx.x ? (ntile - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  auto tile = [&](int j) { return (int)blockIdx.x + j * (int)gridDim.x; };
+  auto issue = [&](int j, int q) {
+    const long long r0 = (long long)tile(j) * kBT, r1 = min((long long)nl, r0 + kBT);
+    uint32_t bytes = seg_bytes<8>(r0, r1) + seg_bytes<8>(rb + r0, rb + r1);
+    if (i >= 2) bytes += seg_bytes<8>(rb + r0, rb + r1);
+    mbar_arrive_tx(&sm.bar[q], bytes);
+    bulk_seg<8>(sm.st[q].a, a, r0, r1, &sm.bar[q]);
+    bulk_seg<8>(sm.st[q].xi, Xi, rb + r0, rb + r1, &sm.bar[q]);
+    if (i >= 2) bulk_seg<8>(sm.st[q].xm, Xim1, rb + r0, rb + r1, &sm.bar[q]);
+  };
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kBS; ++q) mbar_init(&sm.bar[q], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = 0; q < kBS && q < J; ++q) issue(q, q);
+  for (int j = 0; j < J; ++j) {
+    const int q = j % kBS;
+    mbar_wait(&sm.bar[q], (uint32_t)((j / kBS) & 1));
+    const long long r0 = (long long)tile(j) * kBT;
+    const int nr = (int)min((long long)kBT, (long long)nl - r0);
+    const double *ap = sm.st[q].a + seg_shift<8>(r0);
+    const double *xp = sm.st[q].xi + seg_shift<8>(rb + r0);
+    const double *mp = sm.st[q].xm + seg_shift<8>(rb + r0);
+    for (int u = threadIdx.x; u < nr; u += blockDim.x) {
+      const int r = (int)r0 + u;
+      const double vi = (xp[u]) * rden;
+      double w = fma(-om, vi, ap[u]);
+      if (i >= 2) w = fma(-den, (mp[u]) * rdenm, w);  // rho_{i-1} = rho[i-1] = den
+      gstore(net, Xip1 + rb + r, r, w);
+      xwin_add_nn(acc[0], w * w, err, xb.l[0]);
+    }
+    __syncthreads();  // stage q consumed
+    if (threadIdx.x == 0 && j + kBS < J) issue(j + kBS, q);
   }
   if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0) {
     FinArgs f{};
@@ -1676,7 +1761,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict_
     }
     for (; j < k; ++j) xr = fma(s_s[j], __ldg(w + (long long)j * ldw) * s_rr[j], xr);
     gstore(net, x + rb + r, r, xr);
-    xwin_add(acc[0], xr * xr, err, xb.l[0]);
+    xwin_add_nn(acc[0], xr * xr, err, xb.l[0]);
   }
   if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
     emit<1>(slot, sc, net, FK_NUX, FinArgs{}, nullptr);
@@ -1708,7 +1793,7 @@ __global__ void __launch_bounds__(kBlock) k_norm_x(const double *__restrict__ g,
         double xr = xv[u];
         if (k1) xr = s1 * (xr * rden);
         if (k1 || net.P > 1) gstore(net, x + rb + r, r, xr);  // P > 1: publish x's halo for the monitor
-        xwin_add(acc[0], xr * xr, err, xb.l[0]);
+        xwin_add_nn(acc[0], xr * xr, err, xb.l[0]);
       }
     }
   }
@@ -1727,7 +1812,7 @@ struct EpiM {
     v[o.r] = o.xr;
     xwin_add(acc[0], o.xr * o.s[0], err, blk[0]);
     xwin_add(acc[1], o.xr * o.s[1], err, blk[1]);
-    xwin_add(acc[2], o.xr * o.xr, err, blk[2]);
+    xwin_add_nn(acc[2], o.xr * o.xr, err, blk[2]);
   }
 };
 
@@ -1805,7 +1890,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
             const double zr = hoff ? A.one_m_eta * zv[h] : fma(A.eta, hv, A.one_m_eta * zv[h]);
             z[r] = zr;
             const double e = zr - A.b;
-            xwin_add(acc[0], e * e, err, xb.l[0]);
+            xwin_add_nn(acc[0], e * e, err, xb.l[0]);
           }
 #pragma unroll
           for (int u = 0; u < 16; ++u) gp[u] = fma(vr[h], om[h][u], gp[u]);
@@ -1886,10 +1971,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
         d[r] = fma(A.beta_next, e, yr) + cd[u];
         const double gv = scg_lanczos_start(seed, A.t + 1, rb + og[u]);
         gstore(net, g + rb + r, r, gv);
-        xwin_add(acc[0], gv * gv, err, xb.l[0]);
+        xwin_add_nn(acc[0], gv * gv, err, xb.l[0]);
         xwin_add(acc[1], yr, err, xb.l[1]);
         xwin_add(acc[2], yr * zr[u], err, xb.l[2]);
-        xwin_add(acc[3], zr[u] * zr[u], err, xb.l[3]);
+        xwin_add_nn(acc[3], zr[u] * zr[u], err, xb.l[3]);
         xwin_add(acc[4], zr[u], err, xb.l[4]);
       }
     }

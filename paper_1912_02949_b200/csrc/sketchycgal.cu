@@ -101,7 +101,7 @@ struct Shard {
   int64_t halo_rows = 0;
   // grids
   int grid_rows = 1, grid_primal = 1, grid_tiles = 1, grid_b = 1, grid_comb = 1, grid_dual = 1, grid_norm = 1,
-      grid_mon = 1, grid_flush = 1, grid_a = 1;
+      grid_mon = 1, grid_flush = 1, grid_a = 1, grid_btma = 1;
   double kb[KC_COUNT] = {0};  // algorithmic bytes of one launch of each class
 };
 
@@ -118,6 +118,7 @@ struct scg_ctx {
   // sharding: world ranks; this context holds shards sh (all of them when emulating)
   int world = 1, mode = 0;  // mode 0: single, 1: emulated shards, 2: one rank of a multi-process job
   bool pdl = true;          // programmatic dependent launches (SCG_PDL=0 disables)
+  bool btma = false;        // TMA-staged k_lanczos_b (SCG_BTMA=1; measured slower: 115-166 vs 106 us on c3)
   int rank = 0;
   std::vector<int64_t> splits;
   std::vector<Shard *> sh;
@@ -533,6 +534,9 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   s->grid_dual = grid_for(nl, std::max(1, occ) * c->nsm);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_norm_x, kBlock, 0);
   s->grid_norm = grid_for(nl, std::max(1, occ) * c->nsm);
+  cudaFuncSetAttribute((const void *)k_lanczos_b_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BSmem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_b_tma, kBlock, sizeof(BSmem));
+  s->grid_btma = (int)std::max<int64_t>(1, std::min<int64_t>((nl + kBT - 1) / kBT, (int64_t)std::max(1, occ) * c->nsm));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sketch_flush, kBlock, 0);
   s->grid_flush = grid_for(nl, std::max(1, occ) * c->nsm);
   if (!alloc((void **)&s->gpart, sizeof(double) * (size_t)s->grid_primal * R)) return fail(c, SCG_ENOMEM, "gpart");
@@ -1084,6 +1088,8 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   {
     const char *e = std::getenv("SCG_PDL");
     c->pdl = !(e && e[0] == '0');
+    const char *eb = std::getenv("SCG_BTMA");
+    c->btma = eb && eb[0] == '1';
   }
   c->npad = (n + 4 + kWin - 1) / kWin * kWin;  // >= 16 bytes of slack for the bulk copies
 
@@ -1311,9 +1317,14 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
         E = ++c->epoch;
         for (Shard *s : c->sh) {
           const double *Xim1 = (i == 1) ? nullptr : slot(s, i - 1);
-          launch(c, KC_LANCZOS_B, s->kb[KC_LANCZOS_B], k_lanczos_b, dim3(s->grid_b), dim3(kBlock),
-                 (const double *)s->a, (const double *)slot(s, i), Xim1, slot(s, i + 1), (int)s->nl, (long long)s->rb,
-                 i, s->slots + SLOT_RHO, s->sc, net_of(c, s, E));
+          if (c->btma)
+            launch_smem(c, KC_LANCZOS_B, s->kb[KC_LANCZOS_B], k_lanczos_b_tma, dim3(s->grid_btma), dim3(kBlock),
+                        sizeof(BSmem), (const double *)s->a, (const double *)slot(s, i), Xim1, slot(s, i + 1),
+                        (int)s->nl, (long long)s->rb, i, s->slots + SLOT_RHO, s->sc, net_of(c, s, E));
+          else
+            launch(c, KC_LANCZOS_B, s->kb[KC_LANCZOS_B], k_lanczos_b, dim3(s->grid_b), dim3(kBlock),
+                   (const double *)s->a, (const double *)slot(s, i), Xim1, slot(s, i + 1), (int)s->nl, (long long)s->rb,
+                   i, s->slots + SLOT_RHO, s->sc, net_of(c, s, E));
         }
         pull_all(c, FK_RHO, 1, E, f);
       }

@@ -122,6 +122,39 @@ __device__ __forceinline__ void xwin_add(XWin &a, double p, int &err, long long 
   }
 }
 
+// xwin_add for summands known to be >= 0 (squares): the same exact result without the
+// sign handling (a product x*x is never negative; -0 contributes nothing either way).
+__device__ __forceinline__ void xwin_add_nn(XWin &a, double p, int &err, long long *blk) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(p) & 0x7fffffffffffffffull;
+  if (b == 0ull) return;
+  int e = (int)(b >> 52);
+  if (e >= 1123) { err = 1; return; }
+  unsigned long long m = b & 0x000fffffffffffffull;
+  if (e) m |= 0x0010000000000000ull; else e = 1;
+  int s = e - 1075 - kLsbExp;
+  if (s < 0) {
+    const int sh = -s;
+    m = sh >= 64 ? 0ull : (m >> sh);
+    s = 0;
+    if (!m) return;
+  }
+  const int q = s >> 5, r = s & 31;
+  const unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
+  const long long s0 = (long long)(lo << r);
+  const long long s1 = (long long)__funnelshift_l(lo, hi, r);
+  const long long s2 = (long long)__funnelshift_l(hi, 0u, r);
+  if (a.qa < 0) a.qa = q < 1 ? 0 : (q > 6 ? 5 : q - 1);
+  const int d = q - a.qa;
+  if (d == 0) { a.w0 += s0; a.w1 += s1; a.w2 += s2; }
+  else if (d == 1) { a.w1 += s0; a.w2 += s1; a.w3 += s2; }
+  else if (d == 2) { a.w2 += s0; a.w3 += s1; a.w4 += s2; }
+  else {
+    atomicAdd(reinterpret_cast<unsigned long long *>(&blk[q]), (unsigned long long)s0);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&blk[q + 1]), (unsigned long long)s1);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&blk[q + 2]), (unsigned long long)s2);
+  }
+}
+
 // Flush a thread's window into the block accumulator (all 32 lanes of the warp call this).
 __device__ __forceinline__ void xwin_flush(const XWin &a, long long *blk) {
   const int qa0 = __shfl_sync(0xffffffffu, a.qa, 0);
