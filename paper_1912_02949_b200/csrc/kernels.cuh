@@ -1975,7 +1975,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
         xwin_add(acc[1], yr, err, xb.l[1]);
         xwin_add(acc[2], yr * zr[u], err, xb.l[2]);
         xwin_add_nn(acc[3], zr[u] * zr[u], err, xb.l[3]);
-        xwin_add(acc[4], zr[u], err, xb.l[4]);
+        xwin_add_nn(acc[4], zr[u], err, xb.l[4]);  // z >= 0 (convex combination of alpha v o v)
       }
     }
   }

@@ -97,9 +97,10 @@ __device__ __forceinline__ bool xs_split(double p, int &q, long long &s0, long l
   }
   q = s >> 5;
   const int r = s & 31;
-  s0 = (long long)(unsigned int)(m << r);
-  s1 = (long long)(r ? (unsigned int)(m >> (32 - r)) : (unsigned int)(m >> 32));
-  s2 = (long long)(r ? (unsigned int)(m >> (64 - r)) : 0u);
+  const unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
+  s0 = (long long)(lo << r);
+  s1 = (long long)__funnelshift_l(lo, hi, r);
+  s2 = (long long)__funnelshift_l(hi, 0u, r);
   if (b >> 63) { s0 = -s0; s1 = -s1; s2 = -s2; }
   return true;
 }
