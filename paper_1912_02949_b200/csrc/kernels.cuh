@@ -231,28 +231,36 @@ __device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double
   const int lane = threadIdx.x & 31;
   const int e0 = __ldg(&C.rp[r]), e1 = __ldg(&C.rp[r + 1]);
   const double rden = 1.0 / den;
-  constexpr int kLR = 4;
-  double mq[kLR], xq[kLR];
+  // columns (and values) are loaded kLC rounds ahead, the gathers x[col] kLR rounds ahead,
+  // so a round never waits on a load chain issued in the same round
+  constexpr int kLR = 4, kLC = 8;
+  int cq[kLC];
+  double mq[kLC], xq[kLR];
 #pragma unroll
-  for (int u = 0; u < kLR; ++u) {
+  for (int u = 0; u < kLC; ++u) {
     const int e = e0 + 32 * u + lane;
-    mq[u] = 0.0;
-    xq[u] = 0.0;
-    if (e < e1) { mq[u] = __ldg(&C.val[e]); xq[u] = __ldg(&X[__ldg(&C.col[e])]); }
+    cq[u] = e < e1 ? __ldg(&C.col[e]) : -1;
+    mq[u] = e < e1 ? __ldg(&C.val[e]) : 0.0;
   }
+#pragma unroll
+  for (int u = 0; u < kLR; ++u) xq[u] = cq[u] >= 0 ? __ldg(&X[cq[u]]) : 0.0;
   double part[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) part[c] = 0.0;
   for (int base = e0; base < e1; base += 32) {
     const bool have = base + lane < e1;
     const double m = mq[0], x = (xq[0]) * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
+    // gather of round k + kLR (its column arrived kLC - kLR rounds ago)
+    const double xn = cq[kLR] >= 0 ? __ldg(&X[cq[kLR]]) : 0.0;
 #pragma unroll
-    for (int u = 0; u + 1 < kLR; ++u) { mq[u] = mq[u + 1]; xq[u] = xq[u + 1]; }
+    for (int u = 0; u + 1 < kLR; ++u) xq[u] = xq[u + 1];
+    xq[kLR - 1] = xn;
+#pragma unroll
+    for (int u = 0; u + 1 < kLC; ++u) { cq[u] = cq[u + 1]; mq[u] = mq[u + 1]; }
     {
-      const int e = base + 32 * kLR + lane;
-      mq[kLR - 1] = 0.0;
-      xq[kLR - 1] = 0.0;
-      if (e < e1) { mq[kLR - 1] = __ldg(&C.val[e]); xq[kLR - 1] = __ldg(&X[__ldg(&C.col[e])]); }
+      const int e = base + 32 * kLC + lane;
+      cq[kLC - 1] = e < e1 ? __ldg(&C.col[e]) : -1;
+      mq[kLC - 1] = e < e1 ? __ldg(&C.val[e]) : 0.0;
     }
     if (have)
 #pragma unroll
