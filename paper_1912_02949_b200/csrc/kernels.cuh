@@ -208,7 +208,10 @@ struct Rows {
   int ntiles;
   const int *cout;      // engine 2: out list offsets per chunk
   long long nglob;
+  unsigned *work;       // non-null: dynamic slice distribution (chunks of kDynCh slices from this
+                        // counter; zeroed again by the kernel's last block) -- skewed graphs
 };
+constexpr int kDynCh = 8;
 
 constexpr int kWin = 1024;  // rows per window (= SELL sorting window sigma)
 
@@ -358,10 +361,22 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
   // Width-specialized three-stage pipeline: while slice i is computed, the gathers and
   // own entries of slice i+1, the columns of slice i+2 and the meta of slice i+3 are in
   // flight; every stage runs only the slots of its slice's width (warp-uniform switch).
+  // static: each block owns a contiguous slice range, its warps interleave (L1 locality);
+  // dynamic (RL.work): warps take chunks of kDynCh consecutive slices from a counter
   const int per = (RL.nslice + gridDim.x - 1) / gridDim.x;
-  const int ns = min(RL.nslice, (int)(blockIdx.x + 1) * per);
-  const int wstep = blockDim.x >> 5;
+  int ns = min(RL.nslice, (int)(blockIdx.x + 1) * per);
+  int wstep = blockDim.x >> 5;
   int sl = blockIdx.x * per + (threadIdx.x >> 5);
+  auto grab = [&]() {
+    unsigned c = 0;
+    if (lane == 0) c = atomicAdd(RL.work, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    sl = (int)c * kDynCh;
+    ns = min(RL.nslice, sl + kDynCh);
+    wstep = 1;
+  };
+  if (RL.work) grab();
+  while (sl < ns) {
   auto mload = [&](int q) -> int2 { return q < ns ? __ldg(&RL.meta[q]) : make_int2(0, 0); };
   auto cload = [&](int2 m, int (&cv)[4], double (&vv)[4]) {
     const int w = m.y & 0xff;
@@ -489,6 +504,9 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
     }
     xo0 = xo1; d00 = d01;
   }
+  if (!RL.work) break;
+  grab();
+  }  // while (chunks)
   return;
   }
 #endif
@@ -1388,6 +1406,7 @@ __global__ void __launch_bounds__(kBlockA, UNI ? SCG_MINB * kBlock / kBlockA : 2
   int err = epi.err;
   XWin (&acc)[1] = epi.acc;
   if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0) {
+    if (RL.work) *RL.work = 0u;  // every warp has stopped taking chunks
     FinArgs f{};
     f.i = i;
     emit<1>(slot, sc, net, FK_OM, f, nullptr);

@@ -83,6 +83,8 @@ struct Shard {
   int *tcol = nullptr;
   double *tval = nullptr;
   int *tout = nullptr, *cout = nullptr;
+  unsigned *work = nullptr;  // dynamic slice counter of k_lanczos_a (graphs with long rows)
+  bool dyn = false;
   TileDesc *tdesc = nullptr;
   int ntiles = 0, tile_h = 0;
   long long tile_out = 0;
@@ -261,9 +263,10 @@ void launch(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 block,
   launch_smem(c, cls, bytes, kern, grid, block, 0, args...);
 }
 
-Rows rows_of(const Shard *s, int64_t n) {
+Rows rows_of(const Shard *s, int64_t n, bool dyn = false) {
   Rows r{};
   r.nglob = n;
+  r.work = dyn ? s->work : nullptr;
   r.longrows = s->longrows;
   r.nlong = s->nlong;
   r.perm = s->sell_perm;
@@ -329,7 +332,7 @@ void free_shard(Shard *s) {
   void *ptrs[] = {s->rp, s->col, s->val, s->wts, s->ldiag, s->cdiag, s->d, s->z, s->y, s->a, s->v, s->G,
                   s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
                   s->sc, s->slots, s->dlog, s->longrows, s->sell_perm, s->sell_col, s->sell_meta, s->sell_val,
-                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tout, s->tdesc, s->orig, s->cout, s->V, s->ckr};
+                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tout, s->tdesc, s->orig, s->cout, s->V, s->ckr, s->work};
   for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -515,7 +518,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
             alloc((void **)&s->dlog, sizeof(scg_iter_rec) * c->log_cap) &&
             alloc((void **)&s->longrows, sizeof(int) * h_long.size()) &&
             alloc((void **)&s->mb, sizeof(Mailbox)) && alloc((void **)&s->peerG, sizeof(double *) * kMaxRanks) &&
-            alloc((void **)&s->orig, sizeof(int) * (size_t)nl) &&
+            alloc((void **)&s->orig, sizeof(int) * (size_t)nl) && alloc((void **)&s->work, sizeof(unsigned)) &&
             alloc((void **)&s->peerMB, sizeof(Mailbox *) * kMaxRanks);
   if (!ok) return fail(c, SCG_ENOMEM, "device allocation");
   if (c->world > 1 && !alloc((void **)&s->mask, (size_t)nl)) return fail(c, SCG_ENOMEM, "halo mask");
@@ -552,6 +555,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   if (c->world > 1) CK(cudaMemcpyAsync(s->mask, h_mask.data(), (size_t)nl, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(s->orig, s->origloc.data(), sizeof(int) * (size_t)nl, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(s->sc, 0, sizeof(DevScalars), st));
+  CK(cudaMemsetAsync(s->work, 0, sizeof(unsigned), st));
   CK(cudaMemsetAsync(s->slots, 0, sizeof(XSlot) * SLOT_COUNT, st));
   CK(cudaMemsetAsync(s->mb, 0, sizeof(Mailbox), st));
   CK(cudaMemsetAsync(s->z, 0, nlb, st));
@@ -830,6 +834,11 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
                    s->rank, (long long)nl, s->ntiles, s->nlong, (int)U, s->tile_h, s->tile_out, (long long)s->nnz_off,
                    s->smem1, oa, om, s->grid_tiles);
   }
+  // dynamic slice distribution for skewed graphs (long rows present): warps that carry hub
+  // rows take fewer slices.  Off for graphs without long rows (static ranges keep L1 locality).
+  s->dyn = SCG_ENGINE == 0 && SCG_PIPE == 3 && s->nlong > 0 && std::getenv("SCG_DYN") == nullptr
+               ? true
+               : (std::getenv("SCG_DYN") && std::getenv("SCG_DYN")[0] == '1' && SCG_ENGINE == 0 && SCG_PIPE == 3);
   // algorithmic bytes per launch
   const double N = (double)c->n, NL = (double)nl;
   const double mat = matbytes;
@@ -1304,7 +1313,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       unsigned long long E = ++c->epoch;
       for (Shard *s : c->sh) {
         Csr C{s->rp, s->col, s->val};
-        Rows TT = rows_of(s, c->n);
+        Rows TT = rows_of(s, c->n, s->dyn);
         auto kA = s->sell_uniform ? k_lanczos_a<true> : k_lanczos_a<false>;
         launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->grid_a), dim3(kBlockA), s->smem1, C, TT,
                (const double *)s->d, (const double *)slot(s, i), (int)s->nl, (long long)s->rb, i, s->a,
