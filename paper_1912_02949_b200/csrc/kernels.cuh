@@ -391,24 +391,25 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
       for (int u = 0; u < 4; ++u) vv[u] = w > u ? __ldg(vp + 32 * u) : 0.0;
     }
   };
+  // padding slots hold the dummy column n (gathered value +0, negative coefficient): no test
   auto gload = [&](int2 m, const int (&cv)[4], double (&gv)[4]) {
     switch (m.y & 0xff) {
       case 0: break;
-      case 1: gv[0] = cv[0] != -1 ? __ldg(&X[cv[0] & 0x7fffffff]) : 0.0; break;
+      case 1: gv[0] = __ldg(&X[cv[0] & 0x7fffffff]); break;
       case 2:
-        gv[0] = cv[0] != -1 ? __ldg(&X[cv[0] & 0x7fffffff]) : 0.0;
-        gv[1] = cv[1] != -1 ? __ldg(&X[cv[1] & 0x7fffffff]) : 0.0;
+        gv[0] = __ldg(&X[cv[0] & 0x7fffffff]);
+        gv[1] = __ldg(&X[cv[1] & 0x7fffffff]);
         break;
       case 3:
-        gv[0] = cv[0] != -1 ? __ldg(&X[cv[0] & 0x7fffffff]) : 0.0;
-        gv[1] = cv[1] != -1 ? __ldg(&X[cv[1] & 0x7fffffff]) : 0.0;
-        gv[2] = cv[2] != -1 ? __ldg(&X[cv[2] & 0x7fffffff]) : 0.0;
+        gv[0] = __ldg(&X[cv[0] & 0x7fffffff]);
+        gv[1] = __ldg(&X[cv[1] & 0x7fffffff]);
+        gv[2] = __ldg(&X[cv[2] & 0x7fffffff]);
         break;
       default:
-        gv[0] = cv[0] != -1 ? __ldg(&X[cv[0] & 0x7fffffff]) : 0.0;
-        gv[1] = cv[1] != -1 ? __ldg(&X[cv[1] & 0x7fffffff]) : 0.0;
-        gv[2] = cv[2] != -1 ? __ldg(&X[cv[2] & 0x7fffffff]) : 0.0;
-        gv[3] = cv[3] != -1 ? __ldg(&X[cv[3] & 0x7fffffff]) : 0.0;
+        gv[0] = __ldg(&X[cv[0] & 0x7fffffff]);
+        gv[1] = __ldg(&X[cv[1] & 0x7fffffff]);
+        gv[2] = __ldg(&X[cv[2] & 0x7fffffff]);
+        gv[3] = __ldg(&X[cv[3] & 0x7fffffff]);
         break;
     }
   };
@@ -443,14 +444,13 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
     o.r = p;
     o.xr = xo0 * rden;
     o.s[0] = d00 * o.xr;
-    auto step = [&](int c, double g) {
-      if (c != -1) {
-        const double mm = UNI ? (c < 0 ? -RL.m0 : RL.m0) : 0.0;
-        o.s[0] = fma(mm, g * rden, o.s[0]);  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
-      }
+    auto step = [&](int c, double g) {  // c is a real entry or the dummy padding entry
+      const double mm = UNI ? (c < 0 ? -RL.m0 : RL.m0) : 0.0;
+      o.s[0] = fma(mm, g * rden, o.s[0]);  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
     };
     auto stepv = [&](int c, double g, double vv) {
-      if (c != -1) o.s[0] = fma(vv, g * rden, o.s[0]);
+      (void)c;
+      o.s[0] = fma(vv, g * rden, o.s[0]);
     };
     const int w = m0.y & 0xff;
     if (UNI) {
@@ -488,10 +488,11 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
           vn[u] = (!UNI && cn[u] != -1) ? __ldg(&RL.sval[m0.x + (j1 + u) * 32 + lane]) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (UNI) step(cx[u], gx[u]);
-          else stepv(cx[u], gx[u], vx[u]);
-        }
+        for (int u = 0; u < 4; ++u)
+          if (cx[u] != -1) {  // slots beyond the slice width are not loaded
+            if (UNI) step(cx[u], gx[u]);
+            else stepv(cx[u], gx[u], vx[u]);
+          }
       }
     }
     if (ok) epi(o);

@@ -730,8 +730,13 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
       slots += (size_t)swid[(size_t)q] * 32;
       if (slots >= (size_t)INT32_MAX) return fail(c, SCG_EINVAL, "SELL layout too large");
     }
-    scol.assign(slots, -1);
-    if (!uni) sval.assign(slots, 0.0);
+    // padding slots (rows shorter than their slice, long-row lanes): engine 0 points them at the
+    // dummy column n, whose gathered value is +0 in every gathered vector (zeroed slack), with a
+    // negative coefficient: fma(-m, +0, acc) == acc exactly for every acc (also +-0), so the
+    // kernel needs no per-slot padding test.  Other engines keep -1.
+    const int padc = SCG_ENGINE == 0 ? (uni ? (int)((unsigned)c->n | 0x80000000u) : (int)c->n) : -1;
+    scol.assign(slots, padc);
+    if (!uni) sval.assign(slots, -0.0);
     // pass 2: fill the slots (parallel; serial for engine 2, whose out lists grow per chunk)
     auto fill = [&](int64_t q) {
       const int width = swid[(size_t)q], nskip = sskip[(size_t)q];
@@ -862,6 +867,9 @@ scg_status alloc_G(scg_ctx *c, Shard *s, int cap) {
   double *G = nullptr;
   CK(cudaMalloc(&G, bytes));
   CK(cudaMemsetAsync(G, 0, sizeof(double) * (size_t)c->npad * 2, c->stream));
+  // slack [n, npad) of every slot reads as +0 (the SELL padding's dummy column n)
+  CK(cudaMemset2DAsync(G + c->n, sizeof(double) * (size_t)c->npad, 0, sizeof(double) * (size_t)(c->npad - c->n),
+                       (size_t)(1 + cap), c->stream));
   if (s->G) {  // keep W slot 0 (the start vector g of the next iteration)
     CK(cudaMemcpyAsync(G + c->npad, s->G + c->npad, sizeof(double) * c->npad, cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1522,6 +1530,7 @@ scg_status sketchycgal_apply_D(scg_ctx *c, const double *xh, double *yh) {
   if (st) return st;
   double *dx = nullptr, *dy = nullptr;
   CK(cudaMalloc(&dx, sizeof(double) * c->npad));
+  CK(cudaMemset(dx, 0, sizeof(double) * c->npad));
   {  // x in input order -> device labels
     std::vector<double> xr((size_t)c->n);
     for (int64_t g = 0; g < c->n; ++g) xr[(size_t)c->gmap[(size_t)g]] = xh[g];
