@@ -1658,8 +1658,10 @@ __global__ void k_tridiag(DevScalars *sc, int q) {
   if (lane != 0) return;
   const double th = (lo + hi) * 0.5;
   sc->theta = th;
-  double u0[kMaxQ], u1[kMaxQ], u2[kMaxQ], mul[kMaxQ], xv[kMaxQ], s[kMaxQ];
-  int swp[kMaxQ];
+  // working arrays of the sequential part in shared memory (a local-memory stack would start
+  // cold in L1 at every launch)
+  __shared__ double u0[kMaxQ], u1[kMaxQ], u2[kMaxQ], mul[kMaxQ], xv[kMaxQ], s[kMaxQ], ru0[kMaxQ];
+  __shared__ int swp[kMaxQ];
   const double tiny = NT * 0x1p-60;
   double c0 = om[0] - th, c1 = rho[0], c2 = 0.0;
   for (int i = 0; i < k - 1; ++i) {
@@ -1682,6 +1684,10 @@ __global__ void k_tridiag(DevScalars *sc, int q) {
   u0[k - 1] = c0; u1[k - 1] = 0.0; u2[k - 1] = 0.0;
   for (int i = 0; i < k; ++i)
     if (fabs(u0[i]) < tiny) u0[i] = u0[i] < 0.0 ? -tiny : tiny;
+  // the three back substitutions divide by the same pivots: RN(1/u0) once, then the
+  // shared-divisor IEEE division div_rn (bitwise RN(t/u0) for normal-range operands,
+  // self-tested; hardware division outside that range)
+  for (int i = 0; i < k; ++i) ru0[i] = 1.0 / u0[i];
   for (int j = 0; j < k; ++j) s[j] = (double)(j % 5 + 1) * 0.25;
   for (int it = 0; it < 3; ++it) {
     for (int j = 0; j < k; ++j) xv[j] = s[j];
@@ -1693,7 +1699,9 @@ __global__ void k_tridiag(DevScalars *sc, int q) {
       double t = xv[i];
       if (i + 1 < k) t = fma(-u1[i], xv[i + 1], t);
       if (i + 2 < k) t = fma(-u2[i], xv[i + 2], t);
-      xv[i] = t / u0[i];
+      const double at = fabs(t), au = fabs(u0[i]);
+      xv[i] = (at > 0x1p-400 && at < 0x1p400 && au > 0x1p-400 && au < 0x1p400) ? div_rn(t, u0[i], ru0[i])
+                                                                            : t / u0[i];
     }
     double mx = 0.0;
     for (int j = 0; j < k; ++j) mx = fabs(xv[j]) > mx ? fabs(xv[j]) : mx;
