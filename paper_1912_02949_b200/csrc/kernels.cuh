@@ -357,7 +357,7 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
   }
   const double rden = 1.0 / den;
 #if SCG_PIPE == 3
-  if (NC == 1) {
+  {
   // Width-specialized three-stage pipeline: while slice i is computed, the gathers and
   // own entries of slice i+1, the columns of slice i+2 and the meta of slice i+3 are in
   // flight; every stage runs only the slots of its slice's width (warp-uniform switch).
@@ -413,11 +413,16 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
         break;
     }
   };
-  auto oload = [&](int q, int2 m, double &xo, double &dd) {
+  auto oload = [&](int q, int2 m, double &xo, double &dd, double &dd1) {
     const int p = q * 32 + lane;
     xo = 0.0;
     dd = 0.0;
-    if (q < ns && p < nl && lane >= (m.y >> 8)) { xo = X[rb + p]; dd = diag0[p]; }
+    dd1 = 0.0;
+    if (q < ns && p < nl && lane >= (m.y >> 8)) {
+      xo = X[rb + p];
+      dd = diag0[p];
+      if (NC > 1) dd1 = diag1[p];
+    }
   };
   int2 m0 = mload(sl), m1 = mload(sl + wstep), m2 = mload(sl + 2 * wstep);
   int c0[4], c1[4];
@@ -425,18 +430,18 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
   cload(m0, c0, v0);
   cload(m1, c1, v1);
   double g0[4] = {0.0, 0.0, 0.0, 0.0};
-  double xo0, d00;
+  double xo0, d00, d10;
   gload(m0, c0, g0);
-  oload(sl, m0, xo0, d00);
+  oload(sl, m0, xo0, d00, d10);
   for (; sl < ns; sl += wstep) {
     const int2 m3 = mload(sl + 3 * wstep);
     int c2[4];
     double v2[4];
     cload(m2, c2, v2);
     double g1[4] = {0.0, 0.0, 0.0, 0.0};
-    double xo1, d01;
+    double xo1, d01, d11;
     gload(m1, c1, g1);
-    oload(sl + wstep, m1, xo1, d01);
+    oload(sl + wstep, m1, xo1, d01, d11);
     // compute slice i
     const int p = sl * 32 + lane;
     const bool ok = p < nl && lane >= (m0.y >> 8);
@@ -444,13 +449,18 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
     o.r = p;
     o.xr = xo0 * rden;
     o.s[0] = d00 * o.xr;
+    if (NC > 1) o.s[NC - 1] = d10 * o.xr;
     auto step = [&](int c, double g) {  // c is a real entry or the dummy padding entry
       const double mm = UNI ? (c < 0 ? -RL.m0 : RL.m0) : 0.0;
-      o.s[0] = fma(mm, g * rden, o.s[0]);  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
+      const double x = g * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
+#pragma unroll
+      for (int t = 0; t < NC; ++t) o.s[t] = fma(mm, x, o.s[t]);
     };
     auto stepv = [&](int c, double g, double vv) {
       (void)c;
-      o.s[0] = fma(vv, g * rden, o.s[0]);
+      const double x = g * rden;
+#pragma unroll
+      for (int t = 0; t < NC; ++t) o.s[t] = fma(vv, x, o.s[t]);
     };
     const int w = m0.y & 0xff;
     if (UNI) {
@@ -503,7 +513,7 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
       c0[u] = c1[u]; c1[u] = c2[u]; g0[u] = g1[u];
       if (!UNI) { v0[u] = v1[u]; v1[u] = v2[u]; }
     }
-    xo0 = xo1; d00 = d01;
+    xo0 = xo1; d00 = d01; d10 = d11;
   }
   if (!RL.work) break;
   grab();
@@ -1879,8 +1889,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
 #endif
   int err = epi.err;
   XWin (&acc)[3] = epi.acc;
-  if (commit_and_ticket<3>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
+  if (commit_and_ticket<3>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0) {
+    if (RL.work) *RL.work = 0u;  // every warp has stopped taking chunks
     emit<3>(slot, sc, net, FK_MON, FinArgs{}, nullptr);
+  }
 }
 
 // ---------------------------------------------------------------- primal / dual / sketch

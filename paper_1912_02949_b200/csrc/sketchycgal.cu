@@ -1383,7 +1383,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     unsigned long long E = ++c->epoch;
     for (Shard *s : c->sh) {
       Csr C{s->rp, s->col, s->val};
-      Rows TT = rows_of(s, c->n);
+      Rows TT = rows_of(s, c->n, s->dyn);
       auto kM = s->sell_uniform ? k_monitor<true> : k_monitor<false>;
       launch_smem(c, KC_MONITOR, s->kb[KC_MONITOR], kM, dim3(s->grid_mon), dim3(kBlock), s->smem2, C, TT, (const double *)s->d,
              (const double *)s->cdiag, (const double *)c->xg(s), c->vslot(s, js), (int)s->nl, (long long)s->rb,
