@@ -109,6 +109,26 @@ struct Net {
 #ifndef SCG_STCS
 #define SCG_STCS 0  // 1: evict-first (st.global.cs) stores of the Lanczos outputs
 #endif
+// Store v at dst (this rank's gathered region) and into the reader ranks' copies given the
+// row's reader mask m (loaded by the caller together with the row's data).
+__device__ __forceinline__ void gstore_m(const Net &net, double *dst, unsigned m, double v) {
+#if SCG_STCS
+  __stcs(dst, v);
+#else
+  *dst = v;
+#endif
+  if (m) {
+    const long long off = dst - net.G;
+    while (m) {
+      const int q = __ffs(m) - 1;
+      m &= m - 1;
+      net.peerG[q][off] = v;
+    }
+  }
+}
+// Mask byte of own row r (0 when P == 1).
+__device__ __forceinline__ unsigned gmask(const Net &net, int r) { return net.mask ? (unsigned)net.mask[r] : 0u; }
+
 // Store v at dst (this rank's gathered region, own row r) and into every reader rank's copy.
 __device__ __forceinline__ void gstore(const Net &net, double *dst, int r, double v) {
 #if SCG_STCS
@@ -1074,6 +1094,9 @@ struct XBlk {
   long long l[NS][kLimbs];
 };
 
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
 template <int NS>
 __device__ __forceinline__ void xblk_init(XBlk<NS> &b) {
   for (int i = threadIdx.x; i < NS * kLimbs; i += blockDim.x) (&b.l[0][0])[i] = 0;
@@ -1083,8 +1106,9 @@ __device__ __forceinline__ void xblk_init(XBlk<NS> &b) {
 // Flush every thread's window into the block accumulator, add the block total to
 // the global slot (exact integer atomics), and take a ticket: returns true in the
 // last block to finish (which then finalizes the slot).
-// With P > 1 every thread first fences its peer stores at system scope, so the
-// mailbox flag the last block raises afterwards orders them for the readers.
+// Thread 0 fences after the block barrier (fences are cumulative): at system scope with
+// P > 1, so the mailbox flag the last block raises afterwards orders the block's peer
+// halo stores for the readers.  An acq_rel fence is enough for this release pattern.
 template <int NS>
 __device__ __forceinline__ bool commit_and_ticket(XWin (&acc)[NS], XBlk<NS> &blk, XSlot *slot, int err,
                                                   DevScalars *sc, int P = 1) {
@@ -1097,10 +1121,12 @@ __device__ __forceinline__ bool commit_and_ticket(XWin (&acc)[NS], XBlk<NS> &blk
     const long long v = blk.l[s][i];
     if (v != 0) atomicAdd(reinterpret_cast<unsigned long long *>(&slot->limbs[s][i]), (unsigned long long)v);
   }
-  if (P > 1) __threadfence_system();
-  else __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(&slot->counter, 1u) == gridDim.x - 1);
+  __syncthreads();  // the block's stores (incl. peer halo stores) precede thread 0's fence (cumulative)
+  if (threadIdx.x == 0) {
+    if (P > 1) fence_acq_rel_sys();
+    else fence_acq_rel_gpu();
+    s_last = (atomicAdd(&slot->counter, 1u) == gridDim.x - 1);
+  }
   __syncthreads();
   return s_last != 0;
 }
@@ -1109,9 +1135,11 @@ __device__ __forceinline__ bool commit_and_ticket(XWin (&acc)[NS], XBlk<NS> &blk
 // pass-2 barrier of the regenerate mode).
 __device__ __forceinline__ bool ticket_only(XSlot *slot) {
   __shared__ int s_last;
-  __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(&slot->counter, 1u) == gridDim.x - 1);
+  if (threadIdx.x == 0) {
+    fence_acq_rel_sys();
+    s_last = (atomicAdd(&slot->counter, 1u) == gridDim.x - 1);
+  }
   __syncthreads();
   return s_last != 0;
 }
@@ -1444,11 +1472,11 @@ __global__ void __launch_bounds__(kBlock, SCG_MINB_B) k_lanczos_b(const double *
   xwin_init(acc[0]);
   int err = 0;
   const int stride = gridDim.x * blockDim.x;
-  auto row = [&](int r, double av, double xi, double xm) {
+  auto row = [&](int r, double av, double xi, double xm, unsigned mk) {
     const double vi = (xi) * rden;
     double w = fma(-om, vi, av);
     if (i >= 2) w = fma(-den, (xm) * rdenm, w);  // rho_{i-1} = rho[i-1] = den
-    gstore(net, Xip1 + rb + r, r, w);
+    gstore_m(net, Xip1 + rb + r, mk, w);
     xwin_add_nn(acc[0], w * w, err, xb.l[0]);
   };
   if ((rb & 1) == 0) {
@@ -1462,6 +1490,7 @@ __global__ void __launch_bounds__(kBlock, SCG_MINB_B) k_lanczos_b(const double *
 #endif
     for (int p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += SCG_BU * stride) {
       double2 av[SCG_BU], xi[SCG_BU], xm[SCG_BU];
+      unsigned mk[SCG_BU];
 #pragma unroll
       for (int u = 0; u < SCG_BU; ++u) {
         const int p = p0 + u * stride;
@@ -1469,24 +1498,26 @@ __global__ void __launch_bounds__(kBlock, SCG_MINB_B) k_lanczos_b(const double *
           av[u] = __ldcs(&a2[p]);  // a is dead after this step: evict first
           xi[u] = xi2[p];
           xm[u] = i >= 2 ? xm2[p] : make_double2(0.0, 0.0);
+          mk[u] = net.mask ? (unsigned)reinterpret_cast<const unsigned short *>(net.mask)[p] : 0u;
         }
       }
 #pragma unroll
       for (int u = 0; u < SCG_BU; ++u) {
         const int p = p0 + u * stride;
         if (p < np) {
-          row(2 * p, av[u].x, xi[u].x, xm[u].x);
-          row(2 * p + 1, av[u].y, xi[u].y, xm[u].y);
+          row(2 * p, av[u].x, xi[u].x, xm[u].x, mk[u] & 0xffu);
+          row(2 * p + 1, av[u].y, xi[u].y, xm[u].y, mk[u] >> 8);
         }
       }
     }
     if ((nl & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
       const int r = nl - 1;
-      row(r, a[r], Xi[rb + r], i >= 2 ? Xim1[rb + r] : 0.0);
+      row(r, a[r], Xi[rb + r], i >= 2 ? Xim1[rb + r] : 0.0, gmask(net, r));
     }
   } else {
     for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < nl; r0 += 4 * stride) {
       double av[4], xi[4], xm[4];
+      unsigned mk[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int r = r0 + u * stride;
@@ -1494,12 +1525,13 @@ __global__ void __launch_bounds__(kBlock, SCG_MINB_B) k_lanczos_b(const double *
           av[u] = a[r];
           xi[u] = Xi[rb + r];
           xm[u] = i >= 2 ? Xim1[rb + r] : 0.0;
+          mk[u] = gmask(net, r);
         }
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int r = r0 + u * stride;
-        if (r < nl) row(r, av[u], xi[u], xm[u]);
+        if (r < nl) row(r, av[u], xi[u], xm[u], mk[u]);
       }
     }
   }
@@ -1795,6 +1827,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict_
   xwin_init(acc[0]);
   int err = 0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const unsigned mk = gmask(net, r);  // issued with the row's loads
     const double *w = Wst + rb + r;
     double xr = s_s[0] * (__ldg(w) * s_rr[0]);
     int j = 1;
@@ -1806,7 +1839,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict_
       for (int u = 0; u < 4; ++u) xr = fma(s_s[j + u], (wv[u]) * s_rr[j + u], xr);
     }
     for (; j < k; ++j) xr = fma(s_s[j], __ldg(w + (long long)j * ldw) * s_rr[j], xr);
-    gstore(net, x + rb + r, r, xr);
+    gstore_m(net, x + rb + r, mk, xr);
     xwin_add_nn(acc[0], xr * xr, err, xb.l[0]);
   }
   if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
@@ -2004,10 +2037,11 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
   for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < nl; r0 += 2 * stride) {
     double zr[2], yv[2], cd[2];
     int og[2];
+    unsigned mk[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int r = r0 + u * stride;
-      if (r < nl) { zr[u] = z[r]; yv[u] = y[r]; cd[u] = cdiag[r]; og[u] = orig[r]; }
+      if (r < nl) { zr[u] = z[r]; yv[u] = y[r]; cd[u] = cdiag[r]; og[u] = orig[r]; mk[u] = gmask(net, r); }
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -2018,7 +2052,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
         y[r] = yr;
         d[r] = fma(A.beta_next, e, yr) + cd[u];
         const double gv = scg_lanczos_start(seed, A.t + 1, rb + og[u]);
-        gstore(net, g + rb + r, r, gv);
+        gstore_m(net, g + rb + r, mk[u], gv);
         xwin_add_nn(acc[0], gv * gv, err, xb.l[0]);
         xwin_add(acc[1], yr, err, xb.l[1]);
         xwin_add(acc[2], yr * zr[u], err, xb.l[2]);

@@ -172,10 +172,27 @@ __device__ __forceinline__ void xwin_flush(const XWin &a, long long *blk) {
 #pragma unroll
       for (int j = 0; j < 5; ++j)
         if (w[j]) atomicAdd(reinterpret_cast<unsigned long long *>(&blk[qa0 + j]), (unsigned long long)w[j]);
-  } else if (a.qa >= 0) {
+  } else {
+    // Lanes anchored at different digit classes: reduce each anchor group with shuffles
+    // (a few rounds; one per distinct anchor) instead of 32 lanes spinning on the same
+    // shared limb (64-bit shared atomics are CAS loops on sm_100).
+    unsigned pending = __ballot_sync(0xffffffffu, a.qa >= 0);
+    while (pending) {
+      const int ql = __shfl_sync(0xffffffffu, a.qa, __ffs(pending) - 1);
+      const bool in = a.qa == ql;
+      pending &= ~__ballot_sync(0xffffffffu, in);
+      long long v[5];
 #pragma unroll
-    for (int j = 0; j < 5; ++j)
-      if (w[j]) atomicAdd(reinterpret_cast<unsigned long long *>(&blk[a.qa + j]), (unsigned long long)w[j]);
+      for (int j = 0; j < 5; ++j) {
+        v[j] = in ? w[j] : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_down_sync(0xffffffffu, v[j], o);
+      }
+      if (mine)
+#pragma unroll
+        for (int j = 0; j < 5; ++j)
+          if (v[j]) atomicAdd(reinterpret_cast<unsigned long long *>(&blk[ql + j]), (unsigned long long)v[j]);
+    }
   }
 }
 

@@ -1,0 +1,53 @@
+"""Projection of multi-GPU strong scaling from EMULATED shards (no multi-GPU box in this pool).
+
+P row shards of configs[3] run inside one context on one B200 (the same kernels, halo peer
+stores and mailbox collectives as one process per GPU; launched in turn on one stream).  The
+sampled CUDA-event time of every kernel class, divided by the P shards that launched it, is
+the per-GPU device time of one rank; the projection adds, per collective, a measured-nowhere
+allowance (NVLINK_US below) for the flag round trip over NVLink.  This is a MODEL, printed as
+such, not a multi-GPU measurement.
+Usage: python tools/scaling_projection.py [P ...]   (default 1 2 4)"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_1912_02949_b200 as scg
+import scg_inputs as si
+
+NVLINK_US = 3.0  # assumed flag round trip per collective (publish + acquire over NVSwitch)
+cfg = os.environ.get("CFG", "c3")
+L = si.laplacian(cfg)
+c = si.CONFIGS[cfg]
+W, K = 3, int(os.environ.get("STEPS", "60"))
+res = {}
+for P in [int(a) for a in sys.argv[1:]] or [1, 2, 4]:
+    s = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], profile=True, shards=P)
+    s.step(W)
+    s.synchronize()
+    s.reset_stats()
+    t0 = time.perf_counter()
+    s.step(K)
+    s.synchronize()
+    wall = time.perf_counter() - t0
+    st = {k["name"]: k for k in s.kernel_stats() if k["launches"] > 0}
+    per_gpu_ms = 0.0
+    for name, k in st.items():
+        per_gpu_ms += k["total_ms"] / (P if name != "pull_collective" else P)
+    pulls = st.get("pull_collective", {"launches": 0})["launches"] / max(P, 1)
+    proj_ms = per_gpu_ms + pulls * NVLINK_US / 1e3
+    res[P] = {"emulated_wall_s": round(wall, 3), "per_gpu_device_ms": round(per_gpu_ms, 2),
+              "collectives": int(pulls), "projected_ms": round(proj_ms, 2),
+              "projected_it_per_s": round(K / (proj_ms / 1e3), 2),
+              "kernels_us_per_launch": {n: round(1e3 * k["total_ms"] / k["launches"], 1) for n, k in st.items()}}
+    s.close()
+    torch.cuda.empty_cache()
+base = res[min(res)]["projected_it_per_s"]
+for P, r in res.items():
+    r["projected_strong_efficiency"] = round(r["projected_it_per_s"] / (base * P), 3)
+print(json.dumps({"config": cfg, "window": [W + 1, W + K], "nvlink_us_per_collective_assumed": NVLINK_US,
+                  "model": "per-GPU device time of the emulated shards + assumed NVLink flag latency per collective",
+                  "P": res}, indent=1))
