@@ -119,7 +119,7 @@ struct scg_ctx {
   uint64_t seed = 0;
   // sharding: world ranks; this context holds shards sh (all of them when emulating)
   int world = 1, mode = 0;  // mode 0: single, 1: emulated shards, 2: one rank of a multi-process job
-  bool pdl = true;          // programmatic dependent launches (SCG_PDL=0 disables)
+  bool pdl = true;          // programmatic dependent launches (n < 2^18; SCG_PDL=0/1 forces)
   bool btma = false;        // TMA-staged k_lanczos_b (SCG_BTMA=1; measured slower: 115-166 vs 106 us on c3)
   int rank = 0;
   std::vector<int64_t> splits;
@@ -1103,8 +1103,11 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   c->lnN = std::log((double)n);
   c->log_cap = 1024;
   {
+    // Programmatic dependent launches pay off while launch latency dominates (measured, no
+    // profiling events: c0 +9%, c1 +23%) and cost on large graphs (c2 -15%, c3 -17%), so they
+    // are on below 2^18 vertices; SCG_PDL=0/1 forces them off/on.
     const char *e = std::getenv("SCG_PDL");
-    c->pdl = !(e && e[0] == '0');
+    c->pdl = e && (e[0] == '0' || e[0] == '1') ? e[0] == '1' : n < (int64_t)1 << 18;
     const char *eb = std::getenv("SCG_BTMA");
     c->btma = eb && eb[0] == '1';
   }
