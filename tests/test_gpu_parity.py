@@ -125,6 +125,17 @@ def test_isolated_vertices_and_heavy_row(gpu):
     _assert_trajectory(g, o, 30)
 
 
+@pytest.mark.parametrize("cfg,T,pdl", [("c0", 200, "0"), ("c2", 2, "1")])
+def test_launch_policy_forced_bitwise(gpu, cfg, T, pdl, monkeypatch):
+    """The launch policy (programmatic dependent launches below 2^18 vertices) forced the
+    other way: the same bitwise trajectory as the oracle."""
+    monkeypatch.setenv("SCG_PDL", pdl)
+    L = si.laplacian(cfg)
+    c = si.CONFIGS[cfg]
+    g, o = _run_pair(gpu, L, c["R"], T, seed=c["seed"])
+    _assert_trajectory(g, o, T)
+
+
 def test_steps_resume_equals_single_call(gpu):
     L = si.laplacian("c0")
     a = gpu.SketchyCGAL(L, R=4, seed=5)
