@@ -29,6 +29,9 @@ constexpr int kBlock = 256;
 constexpr int kBlockA = SCG_BLOCK_A;  // threads per block of k_lanczos_a (the SpMV of pass 1)
 
 // Device-resident scalars of the current iteration.
+#ifndef SCG_TAILPROF
+#define SCG_TAILPROF 0  // 1: time the last block's emit (globaltimer), printed every 512 launches per kind
+#endif
 struct DevScalars {
   double om[kMaxQ];        // omega_i, i = 1..k  (om[i-1])
   double rho[kMaxQ + 1];   // rho[0] = ||g|| (start-vector norm), rho[i] = rho_i  (Alg. 2 line 7)
@@ -37,6 +40,9 @@ struct DevScalars {
   double theta, nu_x, xi, c, vv, nz, gamma, p, tau;
   double my[4];            // sums over the state (y_t, z_t) of the NEXT iteration: y, y.z, z.z, z (k_dual_sketch)
   int k, brk, err, pad;
+#if SCG_TAILPROF
+  unsigned long long dbg_ns[16], dbg_cnt[16];
+#endif
 };
 
 // Exact-sum slot: up to 3 accumulators + a block ticket counter.
@@ -1260,17 +1266,40 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 
 // Last block, thread 0: take this rank's limbs (resetting the slot) and either
 // finalize (P == 1) or publish them to every rank's mailbox (P > 1).
+#if SCG_TAILPROF
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 template <int NS>
 __device__ __forceinline__ void emit(XSlot *slot, DevScalars *sc, const Net &net, int kind, const FinArgs &f,
                                      const double *gk) {
-  __threadfence();
+#if SCG_TAILPROF
+  const unsigned long long t0 = gtimer();
+#endif
+  // acquire side of the block ticket: every block's limb atomics (performed in L2) precede
+  // these L2 loads; the slot is idle until the next launch, so plain stores reset it
+  fence_acq_rel_gpu();
   long long L[kMaxSums][kLimbs];
+#pragma unroll
   for (int s = 0; s < kMaxSums; ++s)
-    for (int i = 0; i < kLimbs; ++i)
-      L[s][i] = s < NS ? (long long)atomicExch(reinterpret_cast<unsigned long long *>(&slot->limbs[s][i]), 0ull) : 0ll;
+#pragma unroll
+    for (int i = 0; i < kLimbs; ++i) L[s][i] = s < NS ? __ldcg(&slot->limbs[s][i]) : 0ll;
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+#pragma unroll
+    for (int i = 0; i < kLimbs; ++i) slot->limbs[s][i] = 0;
   slot->counter = 0;
   if (net.P <= 1) {
     finalize(kind, sc, L, gk, f);
+#if SCG_TAILPROF
+    sc->dbg_ns[kind] += gtimer() - t0;
+    if ((++sc->dbg_cnt[kind] & 511) == 0)
+      printf("[tail] kind %d: %llu launches, mean emit %.2f us\n", kind, sc->dbg_cnt[kind],
+             1e-3 * (double)sc->dbg_ns[kind] / (double)sc->dbg_cnt[kind]);
+#endif
     return;
   }
   const int e = (int)(net.E & 3ull);

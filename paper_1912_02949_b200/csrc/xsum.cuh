@@ -196,65 +196,77 @@ __device__ __forceinline__ void xwin_flush(const XWin &a, long long *blk) {
   }
 }
 
-// bits [lo, lo+cnt) (cnt <= 64) of the magnitude held in 32-bit digits mag[0..nd)
-__device__ __forceinline__ unsigned long long xs_bits(const unsigned int *mag, int nd, int lo, int cnt) {
-  const int di = lo >> 5, off = lo & 31;
-  unsigned int w0 = (di >= 0 && di < nd) ? mag[di] : 0u;
-  unsigned int w1 = (di + 1 >= 0 && di + 1 < nd) ? mag[di + 1] : 0u;
-  unsigned int w2 = (di + 2 >= 0 && di + 2 < nd) ? mag[di + 2] : 0u;
-  unsigned __int128 w = ((unsigned __int128)w2 << 64) | ((unsigned __int128)w1 << 32) | (unsigned __int128)w0;
-  unsigned long long out = (unsigned long long)(w >> off);
-  return cnt >= 64 ? out : (out & ((1ull << cnt) - 1ull));
-}
-
-// true iff any of the bits [0, hi) is set
-__device__ __forceinline__ bool xs_any_below(const unsigned int *mag, int nd, int hi) {
-  const int full = hi >> 5;
-  for (int i = 0; i < full && i < nd; ++i)
-    if (mag[i]) return true;
-  const int rem = hi & 31;
-  if (rem && full < nd && (mag[full] & ((1u << rem) - 1u))) return true;
-  return false;
-}
-
 // Round the exact value held in limbs to the nearest double (ties to even).
+// Register-only: every array index below is a compile-time constant (fully unrolled loops,
+// selects instead of dynamic indexing), so nothing goes through local memory -- this runs
+// on one thread at the end of every reduction, on the critical path.
 __device__ __noinline__ double xacc_round(const long long *limbs) {
   long long d[kLimbs];
+#pragma unroll
   for (int i = 0; i < kLimbs; ++i) d[i] = limbs[i];
   // carry-normalize digits 0..8 into [0, 2^32)
+#pragma unroll
   for (int i = 0; i < kLimbs - 1; ++i) {
-    long long c = d[i] >> 32;  // arithmetic shift = floor division
+    const long long c = d[i] >> 32;  // arithmetic shift = floor division
     d[i] -= c * 4294967296ll;
     d[i + 1] += c;
   }
-  bool neg = d[kLimbs - 1] < 0;
+  const bool neg = d[kLimbs - 1] < 0;
   if (neg) {  // negate every limb and renormalize: value becomes non-negative
+#pragma unroll
     for (int i = 0; i < kLimbs; ++i) d[i] = -d[i];
+#pragma unroll
     for (int i = 0; i < kLimbs - 1; ++i) {
-      long long c = d[i] >> 32;
+      const long long c = d[i] >> 32;
       d[i] -= c * 4294967296ll;
       d[i + 1] += c;
     }
   }
   constexpr int ND = kLimbs + 1;
   unsigned int mag[ND];
+#pragma unroll
   for (int i = 0; i < kLimbs - 1; ++i) mag[i] = (unsigned int)d[i];
   mag[kLimbs - 1] = (unsigned int)((unsigned long long)d[kLimbs - 1] & 0xffffffffull);
   mag[kLimbs] = (unsigned int)((unsigned long long)d[kLimbs - 1] >> 32);
   int top = -1;
-  for (int i = ND - 1; i >= 0; --i)
-    if (mag[i]) { top = i; break; }
+  unsigned int mtop = 0u;
+#pragma unroll
+  for (int i = 0; i < ND; ++i)
+    if (mag[i]) { top = i; mtop = mag[i]; }
   if (top < 0) return 0.0;
-  const int B = top * 32 + (31 - __clz(mag[top]));  // highest set bit
+  const int B = top * 32 + (31 - __clz(mtop));  // highest set bit
+  // word j of the magnitude (0 outside [0, ND)), by select
+  auto word = [&](int j) -> unsigned int {
+    unsigned int w = 0u;
+#pragma unroll
+    for (int i = 0; i < ND; ++i) w = (i == j) ? mag[i] : w;
+    return w;
+  };
+  // bits [lo, lo + cnt) (cnt <= 64, lo >= 0)
+  auto bits = [&](int lo, int cnt) -> unsigned long long {
+    const int di = lo >> 5, off = lo & 31;
+    const unsigned __int128 w = ((unsigned __int128)word(di + 2) << 64) | ((unsigned __int128)word(di + 1) << 32) |
+                                (unsigned __int128)word(di);
+    const unsigned long long out = (unsigned long long)(w >> off);
+    return cnt >= 64 ? out : (out & ((1ull << cnt) - 1ull));
+  };
   double res;
   if (B <= 52) {
-    unsigned long long M = xs_bits(mag, ND, 0, B + 1);
+    const unsigned long long M = bits(0, B + 1);
     res = (double)M * 0x1p-200;  // exact: M < 2^53, result normal
   } else {
     const int shift = B - 52;  // bits dropped
-    unsigned long long keep = xs_bits(mag, ND, shift, 53);
-    unsigned long long rbit = xs_bits(mag, ND, shift - 1, 1);
-    const bool sticky = xs_any_below(mag, ND, shift - 1);
+    unsigned long long keep = bits(shift, 53);
+    const unsigned long long rbit = bits(shift - 1, 1);
+    // sticky: any of the bits [0, shift - 1)
+    const int hi = shift - 1, full = hi >> 5, rem = hi & 31;
+    unsigned int any = 0u;
+#pragma unroll
+    for (int i = 0; i < ND; ++i) {
+      any |= (i < full) ? mag[i] : 0u;
+      any |= (i == full && rem) ? (mag[i] & ((1u << rem) - 1u)) : 0u;
+    }
+    const bool sticky = any != 0u;
     if (rbit && (sticky || (keep & 1ull))) keep += 1ull;
     // value = keep * 2^(shift - 200); build the power of two from its exponent bits
     const int ex = shift + kLsbExp;  // in [-147, 160]
