@@ -1112,12 +1112,15 @@ __device__ __forceinline__ void xblk_init(XBlk<NS> &b) {
 // Flush every thread's window into the block accumulator, add the block total to
 // the global slot (exact integer atomics), and take a ticket: returns true in the
 // last block to finish (which then finalizes the slot).
-// Thread 0 fences after the block barrier (fences are cumulative): at system scope with
-// P > 1, so the mailbox flag the last block raises afterwards orders the block's peer
-// halo stores for the readers.  An acq_rel fence is enough for this release pattern.
+// Thread 0 fences after the block barrier (fences are cumulative): at system scope when
+// P > 1 and the block stored into peer memory, so the mailbox flag the last block raises
+// afterwards orders the block's halo stores for the readers.  An acq_rel fence is enough
+// for this release pattern.
+// peer: nonzero in a thread that stored into a peer rank's memory; only blocks with such a
+// thread need the system-scope fence (the others' stores are read on this GPU only).
 template <int NS>
 __device__ __forceinline__ bool commit_and_ticket(XWin (&acc)[NS], XBlk<NS> &blk, XSlot *slot, int err,
-                                                  DevScalars *sc, int P = 1) {
+                                                  DevScalars *sc, int P = 1, unsigned peer = 1u) {
   __shared__ int s_last;
 #pragma unroll
   for (int s = 0; s < NS; ++s) xwin_flush(acc[s], blk.l[s]);
@@ -1127,9 +1130,12 @@ __device__ __forceinline__ bool commit_and_ticket(XWin (&acc)[NS], XBlk<NS> &blk
     const long long v = blk.l[s][i];
     if (v != 0) atomicAdd(reinterpret_cast<unsigned long long *>(&slot->limbs[s][i]), (unsigned long long)v);
   }
-  __syncthreads();  // the block's stores (incl. peer halo stores) precede thread 0's fence (cumulative)
+  // the block's stores (incl. peer halo stores) precede thread 0's fence (cumulative)
+  int sys = 0;
+  if (P > 1) sys = __syncthreads_or(peer != 0u);
+  else __syncthreads();
   if (threadIdx.x == 0) {
-    if (P > 1) fence_acq_rel_sys();
+    if (sys) fence_acq_rel_sys();
     else fence_acq_rel_gpu();
     s_last = (atomicAdd(&slot->counter, 1u) == gridDim.x - 1);
   }
@@ -1473,7 +1479,7 @@ __global__ void __launch_bounds__(kBlockA, UNI ? SCG_MINB * kBlock / kBlockA : 2
 #endif
   int err = epi.err;
   XWin (&acc)[1] = epi.acc;
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0) {
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P, 0u) && threadIdx.x == 0) {
     if (RL.work) *RL.work = 0u;  // every warp has stopped taking chunks
     FinArgs f{};
     f.i = i;
@@ -1501,11 +1507,13 @@ __global__ void __launch_bounds__(kBlock, SCG_MINB_B) k_lanczos_b(const double *
   xwin_init(acc[0]);
   int err = 0;
   const int stride = gridDim.x * blockDim.x;
+  unsigned peer = 0u;
   auto row = [&](int r, double av, double xi, double xm, unsigned mk) {
     const double vi = (xi) * rden;
     double w = fma(-om, vi, av);
     if (i >= 2) w = fma(-den, (xm) * rdenm, w);  // rho_{i-1} = rho[i-1] = den
     gstore_m(net, Xip1 + rb + r, mk, w);
+    peer |= mk;
     xwin_add_nn(acc[0], w * w, err, xb.l[0]);
   };
   if ((rb & 1) == 0) {
@@ -1564,7 +1572,7 @@ __global__ void __launch_bounds__(kBlock, SCG_MINB_B) k_lanczos_b(const double *
       }
     }
   }
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0) {
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P, peer) && threadIdx.x == 0) {
     FinArgs f{};
     f.i = i;
     emit<1>(slot, sc, net, FK_RHO, f, nullptr);
@@ -1855,6 +1863,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict_
   XWin acc[1];
   xwin_init(acc[0]);
   int err = 0;
+  unsigned peer = 0u;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
     const unsigned mk = gmask(net, r);  // issued with the row's loads
     const double *w = Wst + rb + r;
@@ -1869,9 +1878,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict_
     }
     for (; j < k; ++j) xr = fma(s_s[j], __ldg(w + (long long)j * ldw) * s_rr[j], xr);
     gstore_m(net, x + rb + r, mk, xr);
+    peer |= mk;
     xwin_add_nn(acc[0], xr * xr, err, xb.l[0]);
   }
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P, peer) && threadIdx.x == 0)
     emit<1>(slot, sc, net, FK_NUX, FinArgs{}, nullptr);
 }
 
@@ -1951,7 +1961,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
 #endif
   int err = epi.err;
   XWin (&acc)[3] = epi.acc;
-  if (commit_and_ticket<3>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0) {
+  if (commit_and_ticket<3>(acc, xb, slot, err, sc, net.P, 0u) && threadIdx.x == 0) {
     if (RL.work) *RL.work = 0u;  // every warp has stopped taking chunks
     emit<3>(slot, sc, net, FK_MON, FinArgs{}, nullptr);
   }
@@ -2022,7 +2032,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
     gpart[(long long)blockIdx.x * R + threadIdx.x] = t;
   }
   __syncthreads();
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P)) {
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P, 0u)) {
     __shared__ double gsum[kMaxR];
     // sum block partials in a fixed order: thread k sums column k over blocks
     if (threadIdx.x < R) {
@@ -2062,6 +2072,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
 #pragma unroll
   for (int q = 0; q < 5; ++q) xwin_init(acc[q]);
   int err = 0;
+  unsigned peer = 0u;
   const int stride = gridDim.x * blockDim.x;
   for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < nl; r0 += 2 * stride) {
     double zr[2], yv[2], cd[2];
@@ -2082,6 +2093,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
         d[r] = fma(A.beta_next, e, yr) + cd[u];
         const double gv = scg_lanczos_start(seed, A.t + 1, rb + og[u]);
         gstore_m(net, g + rb + r, mk[u], gv);
+        peer |= mk[u];
         xwin_add_nn(acc[0], gv * gv, err, xb.l[0]);
         xwin_add(acc[1], yr, err, xb.l[1]);
         xwin_add(acc[2], yr * zr[u], err, xb.l[2]);
@@ -2090,7 +2102,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
       }
     }
   }
-  if (commit_and_ticket<5>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
+  if (commit_and_ticket<5>(acc, xb, slot, err, sc, net.P, peer) && threadIdx.x == 0)
     emit<5>(slot, sc, net, FK_RHO0M, FinArgs{}, nullptr);
 }
 
