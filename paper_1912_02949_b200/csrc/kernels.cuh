@@ -1487,6 +1487,225 @@ __global__ void __launch_bounds__(kBlockA, UNI ? SCG_MINB * kBlock / kBlockA : 2
   }
 }
 
+// ---------------------------------------------------------------- warp-specialized TMA SpMV
+// k_lanczos_a for uniform weights and static slice ranges with one producer warp and
+// kWsCons consumer warps per block.  The producer streams each stage -- the metas, the
+// columns, the own entries and the diagonal of kWsCons consecutive slices, all contiguous in
+// HBM -- into a kWsD-deep shared ring with cp.async.bulk (one thread, completion counted on
+// the stage's "full" mbarrier); consumer warp w takes slice w of every stage, copies what
+// it needs into registers, releases the stage ("empty" mbarrier, one arrival per warp) and
+// issues its gathers one slice ahead.  Every DRAM stream is in flight kWsD stages ahead
+// without holding registers; only the gathers (L1/L2) use the register pipeline.  The
+// per-row arithmetic is spmv_rows' (CAC-3) exactly.
+constexpr int kWsCons = 8;
+constexpr int kWsThreads = 32 * (kWsCons + 1);
+constexpr int kWsD = 4;
+constexpr int kWsCap = 2048;  // column slots per stage (larger stages read columns from HBM)
+struct __align__(16) WsStage {
+  int cols[kWsCap];
+  double x[kWsCons * 32 + 2];  // own entries from a 16-byte aligned start (xsh = 0 or 1)
+  double d[kWsCons * 32];
+  int2 meta[kWsCons];
+  int cbase, ovf, xsh, pad;
+};
+struct __align__(16) WsSmem {
+  WsStage st[kWsD];
+  unsigned long long full[kWsD], empty[kWsD];
+};
+#ifndef SCG_WS_MINB
+#define SCG_WS_MINB 3  // 72 registers, 3 blocks/SM (measured: 2 blocks/SM 190 us, 3: 165 us on c3)
+#endif
+
+template <bool UNI>
+__global__ void __launch_bounds__(kWsThreads, SCG_WS_MINB) k_lanczos_a_ws(Csr C, Rows RL, const double *__restrict__ d,
+                                                                       const double *__restrict__ X, int nl,
+                                                                       long long rb, int i, double *__restrict__ a,
+                                                                       XSlot *slot, DevScalars *sc, Net net) {
+  pdl_entry();
+  if (sc->brk) return;
+  const double den = sc->rho[i - 1];
+  __shared__ XBlk<1> xb;
+  xblk_init<1>(xb);
+  extern __shared__ __align__(128) unsigned char smraw[];
+  WsSmem &sm = *reinterpret_cast<WsSmem *>(smraw);
+  EpiA epi;
+  epi.a = a;
+  epi.blk = xb.l[0];
+  xwin_init(epi.acc[0]);
+  epi.err = 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < kWsCons) {  // long rows (> 32 entries, reading R27): consumer warps, grid-wide
+    const int nw = gridDim.x * kWsCons;
+    for (int w = blockIdx.x * kWsCons + warp; w < RL.nlong; w += nw) {
+      RowOut<1> o;
+      long_row_chain<1>(C, RL.longrows[w], X, den, d, nullptr, rb, o);
+      if (lane == 0) epi(o);
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kWsD; ++k) {
+      mbar_init(&sm.full[k], 1);
+      mbar_init(&sm.empty[k], kWsCons);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int per = (RL.nslice + gridDim.x * kWsCons - 1) / (gridDim.x * kWsCons) * kWsCons;
+  const int s_beg = min(RL.nslice, (int)blockIdx.x * per), s_end = min(RL.nslice, s_beg + per);
+  const int nst = (s_end - s_beg + kWsCons - 1) / kWsCons;
+  const double rden = 1.0 / den, m0v = RL.m0;
+  if (warp == kWsCons) {
+    // ---- producer: metas come 32 slices (4 stages) per coalesced load, one batch ahead
+    auto mbatch = [&](int b) -> int2 {
+      const int q = s_beg + 32 * b + lane;
+      return q < s_end ? __ldg(&RL.meta[q]) : make_int2(0, 0);
+    };
+    int2 mcur = mbatch(0), mnext = mbatch(1);
+    for (int j = 0; j < nst; ++j) {
+      const int sl = j % kWsD;
+      if (j > 0 && (j & 3) == 0) {
+        mcur = mnext;
+        mnext = mbatch((j >> 2) + 1);
+      }
+      if (j >= kWsD) mbar_wait(&sm.empty[sl], (uint32_t)(((j / kWsD) - 1) & 1));
+      WsStage &st = sm.st[sl];
+      const int s0 = s_beg + kWsCons * j;
+      const int nsl = min(kWsCons, s_end - s0);
+      const int src = kWsCons * (j & 3);
+      const int2 mv = make_int2(__shfl_sync(0xffffffffu, mcur.x, src + (lane & 7)),
+                                __shfl_sync(0xffffffffu, mcur.y, src + (lane & 7)));
+      const int first = __shfl_sync(0xffffffffu, mcur.x, src);
+      const int lx = __shfl_sync(0xffffffffu, mcur.x, src + nsl - 1);
+      const int ly = __shfl_sync(0xffffffffu, mcur.y, src + nsl - 1);
+      const int cints = lx + 32 * (ly & 0xff) - first;
+      const int ovf = cints > kWsCap ? 1 : 0;
+      const long long r0 = (long long)s0 * 32;
+      const int nr = (int)min((long long)kWsCons * 32, (long long)nl - r0);
+      const double *xs = X + rb + r0;
+      const int xsh = (int)(((unsigned long long)(size_t)xs >> 3) & 1ull);
+      const uint32_t xbytes = (uint32_t)(((nr + xsh) * 8 + 15) & ~15);
+      const uint32_t dbytes = (uint32_t)((nr * 8 + 15) & ~15);
+      if (lane < kWsCons) st.meta[lane] = lane < nsl ? mv : make_int2(0, 0);
+      if (lane == 0) {
+        st.cbase = first;
+        st.ovf = ovf;
+        st.xsh = xsh;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t cb = ovf ? 0u : (uint32_t)cints * 4u;
+        mbar_arrive_tx(&sm.full[sl], cb + xbytes + dbytes);
+        if (cb) bulk_g2s(st.cols, RL.scol + first, cb, &sm.full[sl]);
+        bulk_g2s(st.x, xs - xsh, xbytes, &sm.full[sl]);
+        bulk_g2s(st.d, d + r0, dbytes, &sm.full[sl]);
+      }
+    }
+  } else {
+    // ---- consumer warp: slice "warp" of every stage
+    auto take = [&](int j, int2 &m, int (&c)[4], double (&g)[4], double &xo, double &dd) {
+      const int sl = j % kWsD;
+      mbar_wait(&sm.full[sl], (uint32_t)((j / kWsD) & 1));
+      const WsStage &st = sm.st[sl];
+      m = st.meta[warp];
+      const int w = m.y & 0xff;
+      if (!st.ovf) {
+        const int *cp = st.cols + (m.x - st.cbase) + lane;
+        c[0] = w > 0 ? cp[0] : 0;
+        c[1] = w > 1 ? cp[32] : 0;
+        c[2] = w > 2 ? cp[64] : 0;
+        c[3] = w > 3 ? cp[96] : 0;
+      } else {
+        const int *cp = RL.scol + m.x + lane;
+        c[0] = w > 0 ? __ldg(cp) : 0;
+        c[1] = w > 1 ? __ldg(cp + 32) : 0;
+        c[2] = w > 2 ? __ldg(cp + 64) : 0;
+        c[3] = w > 3 ? __ldg(cp + 96) : 0;
+      }
+      xo = st.x[st.xsh + warp * 32 + lane];
+      dd = st.d[warp * 32 + lane];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[sl]);  // the stage's data is in registers now
+      switch (w) {
+        case 0: break;
+        case 1: g[0] = __ldg(&X[c[0] & 0x7fffffff]); break;
+        case 2:
+          g[0] = __ldg(&X[c[0] & 0x7fffffff]);
+          g[1] = __ldg(&X[c[1] & 0x7fffffff]);
+          break;
+        case 3:
+          g[0] = __ldg(&X[c[0] & 0x7fffffff]);
+          g[1] = __ldg(&X[c[1] & 0x7fffffff]);
+          g[2] = __ldg(&X[c[2] & 0x7fffffff]);
+          break;
+        default:
+          g[0] = __ldg(&X[c[0] & 0x7fffffff]);
+          g[1] = __ldg(&X[c[1] & 0x7fffffff]);
+          g[2] = __ldg(&X[c[2] & 0x7fffffff]);
+          g[3] = __ldg(&X[c[3] & 0x7fffffff]);
+          break;
+      }
+    };
+    int2 m0 = make_int2(0, 0);
+    int c0[4] = {0, 0, 0, 0};
+    double g0[4] = {0.0, 0.0, 0.0, 0.0}, x0 = 0.0, d0 = 0.0;
+    if (nst > 0) take(0, m0, c0, g0, x0, d0);
+    for (int j = 0; j < nst; ++j) {
+      int2 m1 = make_int2(0, 0);
+      int c1[4] = {0, 0, 0, 0};
+      double g1[4] = {0.0, 0.0, 0.0, 0.0}, x1 = 0.0, d1 = 0.0;
+      if (j + 1 < nst) take(j + 1, m1, c1, g1, x1, d1);  // gathers of the next slice in flight
+      const int q = s_beg + kWsCons * j + warp;
+      const int p = q * 32 + lane;
+      const bool ok = q < s_end && p < nl && lane >= (m0.y >> 8);
+      RowOut<1> o;
+      o.r = p;
+      o.xr = x0 * rden;
+      o.s[0] = d0 * o.xr;
+      auto step = [&](int cc, double gv) {
+        const double mm = cc < 0 ? -m0v : m0v;
+        o.s[0] = fma(mm, gv * rden, o.s[0]);  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
+      };
+      const int w = m0.y & 0xff;
+      switch (w) {
+        case 0: break;
+        case 1: step(c0[0], g0[0]); break;
+        case 2: step(c0[0], g0[0]); step(c0[1], g0[1]); break;
+        case 3: step(c0[0], g0[0]); step(c0[1], g0[1]); step(c0[2], g0[2]); break;
+        default: step(c0[0], g0[0]); step(c0[1], g0[1]); step(c0[2], g0[2]); step(c0[3], g0[3]); break;
+      }
+      if (w > 4) {  // rows longer than four slots: remaining chunks from HBM
+        for (int j0 = 4; j0 < w; j0 += 4) {
+          int cx[4];
+          double gx[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) cx[u] = j0 + u < w ? __ldg(&RL.scol[m0.x + (j0 + u) * 32 + lane]) : -1;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) gx[u] = cx[u] != -1 ? __ldg(&X[cx[u] & 0x7fffffff]) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (cx[u] != -1) step(cx[u], gx[u]);
+        }
+      }
+      if (ok) epi(o);
+      m0 = m1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        c0[u] = c1[u];
+        g0[u] = g1[u];
+      }
+      x0 = x1;
+      d0 = d1;
+    }
+  }
+  int err = epi.err;
+  XWin (&acc)[1] = epi.acc;
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P, 0u) && threadIdx.x == 0) {
+    FinArgs f{};
+    f.i = i;
+    emit<1>(slot, sc, net, FK_OM, f, nullptr);
+  }
+}
+
 // Step i, part B (Alg. 2 lines 6-7): w_{i+1} = fma(-rho_{i-1}, v_{i-1}, fma(-omega_i, v_i, a)),
 // rho_i = ||w_{i+1}|| (exact); breakdown test.  Writes the un-normalized w_{i+1}.
 #ifndef SCG_MINB_B

@@ -102,6 +102,8 @@ struct Shard {
   std::vector<void *> ipc_opened;
   int64_t halo_rows = 0;
   // grids
+  bool ws = false;  // k_lanczos_a as the warp-specialized TMA kernel (SCG_WS=1)
+  int grid_ws = 1;
   int grid_rows = 1, grid_primal = 1, grid_tiles = 1, grid_b = 1, grid_comb = 1, grid_dual = 1, grid_norm = 1,
       grid_mon = 1, grid_flush = 1, grid_a = 1, grid_btma = 1;
   double kb[KC_COUNT] = {0};  // algorithmic bytes of one launch of each class
@@ -844,6 +846,21 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
   s->dyn = SCG_ENGINE == 0 && SCG_PIPE == 3 && s->nlong > 0 && std::getenv("SCG_DYN") == nullptr
                ? true
                : (std::getenv("SCG_DYN") && std::getenv("SCG_DYN")[0] == '1' && SCG_ENGINE == 0 && SCG_PIPE == 3);
+  // warp-specialized TMA k_lanczos_a (uniform weights, static slice ranges)
+  s->ws = SCG_ENGINE == 0 && s->sell_uniform && !s->dyn && std::getenv("SCG_WS") && std::getenv("SCG_WS")[0] == '1';
+  if (s->ws) {
+    const int wsb = (int)sizeof(WsSmem);
+    cudaFuncSetAttribute((const void *)k_lanczos_a_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, wsb);
+    const int pct = std::min(100, (SCG_WS_MINB * (wsb + 4096) * 100 + 233471) / 233472);
+    cudaFuncSetAttribute((const void *)k_lanczos_a_ws<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    int ow = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ow, k_lanczos_a_ws<true>, kWsThreads, wsb);
+    const int need = (int)std::max<int64_t>((s->nslice + kWsCons - 1) / kWsCons, 1);
+    s->grid_ws = std::max(1, std::min(need, std::max(1, ow) * c->nsm));
+    if (std::getenv("SCG_DEBUG"))
+      std::fprintf(stderr, "[scg] shard %d: warp-specialized k_lanczos_a, smem %d B, %d blocks/SM, grid %d\n", s->rank, wsb,
+                   ow, s->grid_ws);
+  }
   // algorithmic bytes per launch
   const double N = (double)c->n, NL = (double)nl;
   const double mat = matbytes;
@@ -1326,9 +1343,14 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
         Csr C{s->rp, s->col, s->val};
         Rows TT = rows_of(s, c->n, s->dyn);
         auto kA = s->sell_uniform ? k_lanczos_a<true> : k_lanczos_a<false>;
-        launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->grid_a), dim3(kBlockA), s->smem1, C, TT,
-               (const double *)s->d, (const double *)slot(s, i), (int)s->nl, (long long)s->rb, i, s->a,
-               s->slots + SLOT_OM, s->sc, net_of(c, s, E));
+        if (s->ws)
+          launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], k_lanczos_a_ws<true>, dim3(s->grid_ws), dim3(kWsThreads),
+                      sizeof(WsSmem), C, TT, (const double *)s->d, (const double *)slot(s, i), (int)s->nl,
+                      (long long)s->rb, i, s->a, s->slots + SLOT_OM, s->sc, net_of(c, s, E));
+        else
+          launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->grid_a), dim3(kBlockA), s->smem1, C, TT,
+                      (const double *)s->d, (const double *)slot(s, i), (int)s->nl, (long long)s->rb, i, s->a,
+                      s->slots + SLOT_OM, s->sc, net_of(c, s, E));
       }
       FinArgs f{};
       f.i = i;

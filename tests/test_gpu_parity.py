@@ -136,6 +136,17 @@ def test_launch_policy_forced_bitwise(gpu, cfg, T, pdl, monkeypatch):
     _assert_trajectory(g, o, T)
 
 
+@pytest.mark.parametrize("cfg,T", [("c0", 300), ("c3", 1)])
+def test_warp_specialized_spmv_engine_bitwise(gpu, cfg, T, monkeypatch):
+    """The opt-in warp-specialized TMA k_lanczos_a (SCG_WS=1: producer warp + mbarrier ring)
+    gives the same bitwise trajectory."""
+    monkeypatch.setenv("SCG_WS", "1")
+    L = si.laplacian(cfg)
+    c = si.CONFIGS[cfg]
+    g, o = _run_pair(gpu, L, c["R"], T, seed=c["seed"])
+    _assert_trajectory(g, o, T)
+
+
 def test_steps_resume_equals_single_call(gpu):
     L = si.laplacian("c0")
     a = gpu.SketchyCGAL(L, R=4, seed=5)
