@@ -1798,6 +1798,151 @@ __global__ void __launch_bounds__(kBlock, SCG_MINB_B) k_lanczos_b(const double *
   }
 }
 
+// ---------------------------------------------------------------- fused Lanczos pass 1
+// Alg. 2 lines 1-9, all q steps in ONE persistent launch (one GPU): step i is phase A
+// (a = D_t v_i, omega_i = <v_i, a>: the k_lanczos_a work) and phase B (w_{i+1} =
+// a - omega_i v_i - rho_{i-1} v_{i-1}, rho_i = ||w_{i+1}||: the k_lanczos_b work), each closed
+// by a grid barrier built on the exact-sum ticket: the last block to commit finalizes the sum
+// (emit, the same code and bits as the two-kernel path) and releases a monotonic flag that the
+// other blocks' thread 0 waits for (acquire; the fence also invalidates this SM's L1, so the
+// next phase's loads see the other blocks' stores).  The grid is co-resident (cooperative
+// launch).  A barrier that does not open within ~2^34 cycles sets sc->err |= 4 and ends the
+// kernel instead of hanging.  Per-row arithmetic and every exact sum are those of
+// k_lanczos_a / k_lanczos_b: bitwise the same iterates.
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <bool UNI>
+__global__ void __launch_bounds__(kBlockA, UNI ? SCG_MINB * kBlock / kBlockA : 2 * kBlock / kBlockA)
+    k_lanczos_pass1(Csr C, Rows RL, const double *__restrict__ d, double *G, long long npad, int store, int q,
+                    int nl, double *a, XSlot *slot_om, XSlot *slot_rho, DevScalars *sc, Net net,
+                    unsigned long long *gflag, unsigned long long ebase) {
+  pdl_entry();
+  __shared__ XBlk<1> xb;
+  __shared__ int s_go;
+  auto vslot = [&](int j) -> double * {  // buffer of w_j (the host's slot(s, j))
+    if (store) return G + (long long)j * npad;
+    return j == 1 ? G + npad : G + (long long)(2 + (j & 1)) * npad;
+  };
+  unsigned long long ph = ebase;
+  // close a phase: the last block finalizes (fin) and opens the barrier, the others wait
+  auto barrier = [&](bool last, auto fin) -> bool {
+    ++ph;
+    if (last) {
+      if (threadIdx.x == 0) {
+        fin();
+        st_release_gpu(gflag, ph);
+      }
+      __syncthreads();
+      return true;
+    }
+    if (threadIdx.x == 0) {
+      int ok = 1;
+      const long long t0 = clock64();
+      while (ld_acquire_gpu(gflag) < ph) {
+        if (clock64() - t0 > (1ll << 34)) {
+          atomicOr(&sc->err, 4);
+          ok = 0;
+          break;
+        }
+        __nanosleep(64);
+      }
+      s_go = ok;
+    }
+    __syncthreads();
+    return s_go != 0;
+  };
+  for (int i = 1; i <= q; ++i) {
+    if (sc->brk) break;  // Alg. 2 line 8 break (read after the barrier: the same on every block)
+    // ---- phase A (k_lanczos_a)
+    {
+      const double den = sc->rho[i - 1];
+      xblk_init<1>(xb);
+      EpiA epi;
+      epi.a = a;
+      epi.blk = xb.l[0];
+      xwin_init(epi.acc[0]);
+      epi.err = 0;
+      spmv_rows<1, UNI>(C, RL, vslot(i), den, d, nullptr, 0, nl, epi);
+      int err = epi.err;
+      XWin (&acc)[1] = epi.acc;
+      const bool last = commit_and_ticket<1>(acc, xb, slot_om, err, sc, 1, 0u);
+      if (!barrier(last, [&]() {
+            if (RL.work) *RL.work = 0u;
+            FinArgs f{};
+            f.i = i;
+            emit<1>(slot_om, sc, net, FK_OM, f, nullptr);
+          }))
+        return;
+    }
+    if (i == q) break;
+    // ---- phase B (k_lanczos_b, vector path: one GPU, rb = 0)
+    {
+      const double om = sc->om[i - 1];
+      const double den = sc->rho[i - 1];
+      const double denm = i >= 2 ? sc->rho[i - 2] : 1.0;
+      const double rden = 1.0 / den, rdenm = 1.0 / denm;
+      const double *Xi = vslot(i);
+      const double *Xim1 = i >= 2 ? vslot(i - 1) : nullptr;
+      double *Xip1 = vslot(i + 1);
+      xblk_init<1>(xb);
+      XWin acc[1];
+      xwin_init(acc[0]);
+      int err = 0;
+      const int stride = gridDim.x * blockDim.x;
+      auto row = [&](int r, double av, double xi, double xm) {
+        const double vi = (xi) * rden;
+        double w = fma(-om, vi, av);
+        if (i >= 2) w = fma(-den, (xm) * rdenm, w);  // rho_{i-1} = rho[i-1] = den
+        Xip1[r] = w;
+        xwin_add_nn(acc[0], w * w, err, xb.l[0]);
+      };
+      const int np = nl >> 1;
+      const double2 *a2 = reinterpret_cast<const double2 *>(a);
+      const double2 *xi2 = reinterpret_cast<const double2 *>(Xi);
+      const double2 *xm2 = reinterpret_cast<const double2 *>(Xim1 ? Xim1 : Xi);
+      constexpr int BU = 1;
+      for (int p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += BU * stride) {
+        double2 av[BU], xv[BU], xm[BU];
+#pragma unroll
+        for (int u = 0; u < BU; ++u) {
+          const int p = p0 + u * stride;
+          if (p < np) {
+            av[u] = __ldcs(&a2[p]);
+            xv[u] = xi2[p];
+            xm[u] = i >= 2 ? xm2[p] : make_double2(0.0, 0.0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < BU; ++u) {
+          const int p = p0 + u * stride;
+          if (p < np) {
+            row(2 * p, av[u].x, xv[u].x, xm[u].x);
+            row(2 * p + 1, av[u].y, xv[u].y, xm[u].y);
+          }
+        }
+      }
+      if ((nl & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int r = nl - 1;
+        row(r, a[r], Xi[r], i >= 2 ? Xim1[r] : 0.0);
+      }
+      const bool last = commit_and_ticket<1>(acc, xb, slot_rho, err, sc, 1, 0u);
+      if (!barrier(last, [&]() {
+            FinArgs f{};
+            f.i = i;
+            emit<1>(slot_rho, sc, net, FK_RHO, f, nullptr);
+          }))
+        return;
+    }
+  }
+}
+
 // TMA-staged variant of k_lanczos_b (the same arithmetic, row by row): tiles of kBT rows of
 // a, X_i and X_{i-1} are bulk-copied (cp.async.bulk, mbarrier completion) into shared
 // memory, kBS stages deep, by one thread; the block computes the tile from shared memory.

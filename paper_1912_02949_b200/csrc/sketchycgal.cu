@@ -39,11 +39,12 @@ namespace {
 
 enum KClass {
   KC_LANCZOS_A = 0, KC_LANCZOS_B, KC_TRIDIAG, KC_LANCZOS_C, KC_NORM_X, KC_COMBINE, KC_MONITOR, KC_PRIMAL,
-  KC_DUAL_SKETCH, KC_SKETCH, KC_PULL, KC_OTHER, KC_COUNT
+  KC_DUAL_SKETCH, KC_SKETCH, KC_PULL, KC_OTHER, KC_PASS1, KC_COUNT
 };
 const char *kKClassName[KC_COUNT] = {"lanczos_a_spmv_dot", "lanczos_b_axpy_norm", "tridiag_mineig",
                                      "lanczos_c_spmv_regen", "norm_x", "combine_stored", "monitor_spmv",
-                                     "primal_z_gpart", "dual_next_g", "sketch_flush", "pull_collective", "other"};
+                                     "primal_z_gpart", "dual_next_g", "sketch_flush", "pull_collective", "other",
+                                     "lanczos_pass1_fused"};
 
 struct EvPair {
   cudaEvent_t a, b;
@@ -102,6 +103,7 @@ struct Shard {
   std::vector<void *> ipc_opened;
   int64_t halo_rows = 0;
   // grids
+  unsigned long long *gflag = nullptr;  // grid-barrier flag of the fused pass-1 kernel
   bool ws = false;  // k_lanczos_a as the warp-specialized TMA kernel (SCG_WS=1)
   int grid_ws = 1;
   int grid_rows = 1, grid_primal = 1, grid_tiles = 1, grid_b = 1, grid_comb = 1, grid_dual = 1, grid_norm = 1,
@@ -121,6 +123,8 @@ struct scg_ctx {
   uint64_t seed = 0;
   // sharding: world ranks; this context holds shards sh (all of them when emulating)
   int world = 1, mode = 0;  // mode 0: single, 1: emulated shards, 2: one rank of a multi-process job
+  bool fused = false;        // one GPU: Lanczos pass 1 as one persistent kernel (SCG_FUSED=1)
+  unsigned long long gphase = 0;  // grid-barrier phases issued so far (fused pass 1)
   bool pdl = true;          // programmatic dependent launches (n < 2^18; SCG_PDL=0/1 forces)
   bool btma = false;        // TMA-staged k_lanczos_b (SCG_BTMA=1; measured slower: 115-166 vs 106 us on c3)
   int rank = 0;
@@ -265,6 +269,47 @@ void launch(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 block,
   launch_smem(c, cls, bytes, kern, grid, block, 0, args...);
 }
 
+// Cooperative launch (every block co-resident: the fused pass-1 kernel's grid barriers),
+// with the programmatic-serialization attribute when enabled; same profiling as launch_smem.
+template <typename Kern, typename... Args>
+void launch_coop(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 block, Args... args) {
+  const bool prof = (c->flags & SCG_PROFILE) != 0 && c->kl[cls] % c->prof_every == 0;
+  if (prof) c->ks[cls]++;
+  EvPair p{};
+  if (prof) {
+    if (c->pending.size() >= 8192) ev_flush(c);
+    p.a = ev_get(c);
+    p.b = ev_get(c);
+    p.cls = cls;
+    cudaEventRecord(p.a, c->stream);
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeCooperative;
+  attr[na].val.cooperative = 1;
+  ++na;
+  if (c->pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+  if (prof) {
+    cudaEventRecord(p.b, c->stream);
+    c->pending.push_back(p);
+  }
+  c->kl[cls]++;
+  c->kbytes_sum[cls] += bytes;
+  c->launches++;
+}
+
 Rows rows_of(const Shard *s, int64_t n, bool dyn = false) {
   Rows r{};
   r.nglob = n;
@@ -334,7 +379,7 @@ void free_shard(Shard *s) {
   void *ptrs[] = {s->rp, s->col, s->val, s->wts, s->ldiag, s->cdiag, s->d, s->z, s->y, s->a, s->v, s->G,
                   s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
                   s->sc, s->slots, s->dlog, s->longrows, s->sell_perm, s->sell_col, s->sell_meta, s->sell_val,
-                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tout, s->tdesc, s->orig, s->cout, s->V, s->ckr, s->work};
+                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tout, s->tdesc, s->orig, s->cout, s->V, s->ckr, s->work, s->gflag};
   for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -521,7 +566,8 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
             alloc((void **)&s->longrows, sizeof(int) * h_long.size()) &&
             alloc((void **)&s->mb, sizeof(Mailbox)) && alloc((void **)&s->peerG, sizeof(double *) * kMaxRanks) &&
             alloc((void **)&s->orig, sizeof(int) * (size_t)nl) && alloc((void **)&s->work, sizeof(unsigned)) &&
-            alloc((void **)&s->peerMB, sizeof(Mailbox *) * kMaxRanks);
+            alloc((void **)&s->peerMB, sizeof(Mailbox *) * kMaxRanks) &&
+            alloc((void **)&s->gflag, sizeof(unsigned long long));
   if (!ok) return fail(c, SCG_ENOMEM, "device allocation");
   if (c->world > 1 && !alloc((void **)&s->mask, (size_t)nl)) return fail(c, SCG_ENOMEM, "halo mask");
 
@@ -557,6 +603,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   if (c->world > 1) CK(cudaMemcpyAsync(s->mask, h_mask.data(), (size_t)nl, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(s->orig, s->origloc.data(), sizeof(int) * (size_t)nl, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(s->sc, 0, sizeof(DevScalars), st));
+  CK(cudaMemsetAsync(s->gflag, 0, sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(s->work, 0, sizeof(unsigned), st));
   CK(cudaMemsetAsync(s->slots, 0, sizeof(XSlot) * SLOT_COUNT, st));
   CK(cudaMemsetAsync(s->mb, 0, sizeof(Mailbox), st));
@@ -1125,6 +1172,8 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
     // are on below 2^18 vertices; SCG_PDL=0/1 forces them off/on.
     const char *e = std::getenv("SCG_PDL");
     c->pdl = e && (e[0] == '0' || e[0] == '1') ? e[0] == '1' : n < (int64_t)1 << 18;
+    const char *eu = std::getenv("SCG_FUSED");
+    c->fused = eu && eu[0] == '1';
     const char *eb = std::getenv("SCG_BTMA");
     c->btma = eb && eb[0] == '1';
   }
@@ -1337,6 +1386,18 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       return j == 1 ? c->wslot(s, 0) : c->wslot(s, 1 + (j & 1));
     };
     // ---- Lanczos pass 1 (Alg. 2 lines 1-9)
+    if (c->fused && c->world == 1 && SCG_ENGINE == 0) {  // all q steps in one persistent launch
+      Shard *s = c->sh[0];
+      Csr C{s->rp, s->col, s->val};
+      Rows TT = rows_of(s, c->n, s->dyn);
+      auto kP = s->sell_uniform ? k_lanczos_pass1<true> : k_lanczos_pass1<false>;
+      const unsigned long long E = ++c->epoch;
+      const unsigned long long eb = c->gphase;
+      c->gphase += 2ull * (unsigned long long)q;
+      launch_coop(c, KC_PASS1, q * s->kb[KC_LANCZOS_A] + (q - 1) * s->kb[KC_LANCZOS_B], kP, dim3(s->grid_a),
+                  dim3(kBlockA), C, TT, (const double *)s->d, s->G, (long long)c->npad, c->store ? 1 : 0, q,
+                  (int)s->nl, s->a, s->slots + SLOT_OM, s->slots + SLOT_RHO, s->sc, net_of(c, s, E), s->gflag, eb);
+    } else
     for (int i = 1; i <= q; ++i) {
       unsigned long long E = ++c->epoch;
       for (Shard *s : c->sh) {

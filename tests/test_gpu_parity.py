@@ -147,6 +147,28 @@ def test_warp_specialized_spmv_engine_bitwise(gpu, cfg, T, monkeypatch):
     _assert_trajectory(g, o, T)
 
 
+@pytest.mark.parametrize("cfg,T", [("c0", 300), ("c2", 2), ("c3", 1)])
+def test_fused_pass1_kernel_bitwise(gpu, cfg, T, monkeypatch):
+    """The opt-in persistent pass-1 kernel (SCG_FUSED=1: all q Lanczos steps in one cooperative
+    launch, grid barriers on the exact-sum tickets) gives the same bitwise trajectory."""
+    monkeypatch.setenv("SCG_FUSED", "1")
+    L = si.laplacian(cfg)
+    c = si.CONFIGS[cfg]
+    g, o = _run_pair(gpu, L, c["R"], T, seed=c["seed"])
+    _assert_trajectory(g, o, T)
+
+
+@pytest.mark.parametrize("regenerate", [False, True])
+def test_fused_pass1_breakdown_and_regenerate(gpu, regenerate, monkeypatch):
+    """Fused pass 1 through a Lanczos breakdown (K_8, k = 2 < q) in both Lanczos modes."""
+    monkeypatch.setenv("SCG_FUSED", "1")
+    n = 8
+    i, j = np.triu_indices(n, 1)
+    L = si.laplacian_from_edges(n, i, j, np.ones(len(i)))
+    g, o = _run_pair(gpu, L, 3, 25, seed=2, regenerate=regenerate)
+    _assert_trajectory(g, o, 25)
+
+
 def test_steps_resume_equals_single_call(gpu):
     L = si.laplacian("c0")
     a = gpu.SketchyCGAL(L, R=4, seed=5)
