@@ -1903,29 +1903,32 @@ __global__ void __launch_bounds__(kBlockA, UNI ? SCG_MINB * kBlock / kBlockA : 2
         Xip1[r] = w;
         xwin_add_nn(acc[0], w * w, err, xb.l[0]);
       };
-      const int np = nl >> 1;
       const double2 *a2 = reinterpret_cast<const double2 *>(a);
       const double2 *xi2 = reinterpret_cast<const double2 *>(Xi);
       const double2 *xm2 = reinterpret_cast<const double2 *>(Xim1 ? Xim1 : Xi);
-      constexpr int BU = 1;
-      for (int p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += BU * stride) {
-        double2 av[BU], xv[BU], xm[BU];
-#pragma unroll
-        for (int u = 0; u < BU; ++u) {
-          const int p = p0 + u * stride;
-          if (p < np) {
-            av[u] = __ldcs(&a2[p]);
-            xv[u] = xi2[p];
-            xm[u] = i >= 2 ? xm2[p] : make_double2(0.0, 0.0);
-          }
+      // this block's phase-A rows (static slice ranges), walked backwards: the a / v_i entries
+      // phase A touched last are still in L2, and the next phase A meets w_{i+1}'s last-written
+      // rows first (any order: the rho sum is exact)
+      const int per = (RL.nslice + gridDim.x - 1) / gridDim.x;
+      const int pb = (int)min((long long)nl, (long long)blockIdx.x * per * 32) >> 1;
+      const int pe = (int)min((long long)nl, (long long)(blockIdx.x + 1) * per * 32) >> 1;
+      if (RL.work == nullptr) {
+#pragma unroll 2
+        for (int p = pe - 1 - (int)threadIdx.x; p >= pb; p -= blockDim.x) {
+          const double2 av = __ldcs(&a2[p]);
+          const double2 xv = xi2[p];
+          const double2 xm = i >= 2 ? xm2[p] : make_double2(0.0, 0.0);
+          row(2 * p, av.x, xv.x, xm.x);
+          row(2 * p + 1, av.y, xv.y, xm.y);
         }
-#pragma unroll
-        for (int u = 0; u < BU; ++u) {
-          const int p = p0 + u * stride;
-          if (p < np) {
-            row(2 * p, av[u].x, xv[u].x, xm[u].x);
-            row(2 * p + 1, av[u].y, xv[u].y, xm[u].y);
-          }
+      } else {  // dynamic slice distribution in phase A: plain grid-stride pairs
+        const int np = nl >> 1;
+        for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += stride) {
+          const double2 av = __ldcs(&a2[p]);
+          const double2 xv = xi2[p];
+          const double2 xm = i >= 2 ? xm2[p] : make_double2(0.0, 0.0);
+          row(2 * p, av.x, xv.x, xm.x);
+          row(2 * p + 1, av.y, xv.y, xm.y);
         }
       }
       if ((nl & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
