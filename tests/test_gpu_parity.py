@@ -158,6 +158,20 @@ def test_fused_pass1_kernel_bitwise(gpu, cfg, T, monkeypatch):
     _assert_trajectory(g, o, T)
 
 
+@pytest.mark.parametrize("P", [2, 3])
+def test_warp_specialized_sharded_bitwise(gpu, P, monkeypatch):
+    """The warp-specialized SpMV under emulated row shards (odd row bases: the 16-byte aligned
+    bulk copy of the own entries starts one element early; peer halo stores elsewhere)."""
+    monkeypatch.setenv("SCG_WS", "1")
+    L = si.laplacian("c0")
+    T = 200
+    g = gpu.SketchyCGAL(L, R=10, seed=0, shards=P)
+    g.step(T)
+    o = oracle.Oracle(L, 10, seed=0, logcap=T)
+    o.step(T)
+    _assert_trajectory(g, o, T)
+
+
 @pytest.mark.parametrize("regenerate", [False, True])
 def test_fused_pass1_breakdown_and_regenerate(gpu, regenerate, monkeypatch):
     """Fused pass 1 through a Lanczos breakdown (K_8, k = 2 < q) in both Lanczos modes."""
