@@ -60,13 +60,25 @@ struct Csr {
 };
 
 // Programmatic dependent launch: every kernel is launched with programmatic stream
-// serialization, waits at entry until the previous grid has completed and flushed
-// (griddepcontrol.wait), then lets the next grid be scheduled while it runs.  Launch
-// latency and block scheduling overlap the previous kernel's tail; all data dependences
-// are honored by the wait.  (No-ops when launched without the attribute.)
+// serialization and waits at entry until the previous grid has completed and flushed
+// (griddepcontrol.wait).  Kernels with exact sums let the next grid be scheduled when a
+// block reaches its commit (pdl_trigger: the main work is done), the others at exit, so the
+// next launch overlaps the tail (ticket, finalize) without the dependent grid's blocks
+// holding SM slots during the main work.  All data dependences are honored by the wait.
+// (No-ops when launched without the attribute.)
+#ifndef SCG_PDL_LATE
+#define SCG_PDL_LATE 1  // kernels with exact sums let the next grid launch only at their block commit
+#endif                  // (0: right after the wait -- measured 17% slower on c3)
 __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#if !SCG_PDL_LATE
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#if SCG_PDL_LATE
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 }
 
 // Host-computed scalars of iteration t (CAC-6).
@@ -1122,6 +1134,7 @@ template <int NS>
 __device__ __forceinline__ bool commit_and_ticket(XWin (&acc)[NS], XBlk<NS> &blk, XSlot *slot, int err,
                                                   DevScalars *sc, int P = 1, unsigned peer = 1u) {
   __shared__ int s_last;
+  pdl_trigger();  // the block's main work is done: the next grid may start launching
 #pragma unroll
   for (int s = 0; s < NS; ++s) xwin_flush(acc[s], blk.l[s]);
   if (__syncthreads_or(err) && threadIdx.x == 0) atomicOr(&sc->err, 1);

@@ -125,7 +125,7 @@ struct scg_ctx {
   int world = 1, mode = 0;  // mode 0: single, 1: emulated shards, 2: one rank of a multi-process job
   bool fused = false;        // one GPU: Lanczos pass 1 as one persistent kernel (SCG_FUSED=1)
   unsigned long long gphase = 0;  // grid-barrier phases issued so far (fused pass 1)
-  bool pdl = true;          // programmatic dependent launches (n < 2^18; SCG_PDL=0/1 forces)
+  bool pdl = true;          // programmatic dependent launches (SCG_PDL=0 disables)
   bool btma = false;        // TMA-staged k_lanczos_b (SCG_BTMA=1; measured slower: 115-166 vs 106 us on c3)
   int rank = 0;
   std::vector<int64_t> splits;
@@ -1167,11 +1167,11 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   c->lnN = std::log((double)n);
   c->log_cap = 1024;
   {
-    // Programmatic dependent launches pay off while launch latency dominates (measured, no
-    // profiling events: c0 +9%, c1 +23%) and cost on large graphs (c2 -15%, c3 -17%), so they
-    // are on below 2^18 vertices; SCG_PDL=0/1 forces them off/on.
+    // Programmatic dependent launches (triggered at the block commit, SCG_PDL_LATE), measured
+    // without profiling events against no PDL: c0 +8%, c1 +23%, c2 +0%, c3 +0.5% (triggered
+    // at kernel entry instead they cost c3 17%: profiles/r01/pdl_policy.txt).  SCG_PDL=0 disables.
     const char *e = std::getenv("SCG_PDL");
-    c->pdl = e && (e[0] == '0' || e[0] == '1') ? e[0] == '1' : n < (int64_t)1 << 18;
+    c->pdl = !(e && e[0] == '0');
     const char *eu = std::getenv("SCG_FUSED");
     c->fused = eu && eu[0] == '1';
     const char *eb = std::getenv("SCG_BTMA");

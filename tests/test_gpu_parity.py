@@ -127,8 +127,8 @@ def test_isolated_vertices_and_heavy_row(gpu):
 
 @pytest.mark.parametrize("cfg,T,pdl", [("c0", 200, "0"), ("c2", 2, "1")])
 def test_launch_policy_forced_bitwise(gpu, cfg, T, pdl, monkeypatch):
-    """The launch policy (programmatic dependent launches below 2^18 vertices) forced the
-    other way: the same bitwise trajectory as the oracle."""
+    """Programmatic dependent launches (default on) forced off, and explicitly on: the same
+    bitwise trajectory as the oracle."""
     monkeypatch.setenv("SCG_PDL", pdl)
     L = si.laplacian(cfg)
     c = si.CONFIGS[cfg]
