@@ -170,6 +170,22 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T);
  * meeting the rule.  Errors: SCG_EINVAL (T_max < 0, eps <= 0, check_every < 1). */
 scg_status sketchycgal_run(scg_ctx *c, int64_t T_max, double eps, int64_t check_every, int64_t *t_stop);
 
+/* Standard-form driver (Remark "Standard-form SDP"): a sequence of
+ * trace-bounded SDPs tr X <= alpha_i (SCG_TRACE_LE forced) with
+ * alpha_0 = alpha0 and alpha_{i+1} = 2 alpha_i, each solved from scratch for T iterations, until
+ * the implicit objective tr(L X_T) of round i equals round i-1's: |o_i - o_{i-1}| <= rtol |o_i|
+ * (the paper's "=" for approximate solutions, reading R31), or max_rounds rounds.
+ *   out:       the context of the last round (caller destroys; reconstruct / round / ... apply)
+ *   L, R, beta0, seed, flags, device, cuda_stream: as sketchycgal_maxcut_init (one GPU: no dist)
+ *   alphas, objs: host arrays of max_rounds doubles: alpha_i and o_i of every round run
+ *   rounds:    rounds run;  converged: 1 if the equality test stopped the sequence, else 0
+ * Errors: SCG_EINVAL for alpha0 <= 0, T < 1, rtol < 0, max_rounds < 1 or NULL outputs; any
+ * error of a round's init / step is returned with *out = NULL. */
+scg_status sketchycgal_maxcut_alpha_doubling(scg_ctx **out, const scg_csr *L, int32_t R, double alpha0,
+                                             double beta0, uint64_t seed, uint32_t flags, int32_t device,
+                                             void *cuda_stream, int64_t T, double rtol, int32_t max_rounds,
+                                             double *alphas, double *objs, int32_t *rounds, int32_t *converged);
+
 /* Block until all queued work is done; reports deferred device errors. */
 scg_status sketchycgal_synchronize(scg_ctx *c);
 

@@ -333,6 +333,27 @@ def nystrom_reconstruct(S, Omega, tau: float | None = None, max_retry: int = 40)
     return U, Lam, err
 
 
+def alpha_doubling(L, R: int, alpha0: float, T: int, rtol: float = 1e-2, max_rounds: int = 8,
+                   beta0: float = 1.0, seed: int = 0, scale: bool = True):
+    """Remark "Standard-form SDP", steps 1-4 as printed: solve the trace-bounded
+    SDP tr X <= alpha_i for T iterations, stop when its primal objective equals
+    the previous round's -- for these approximate solutions: within rtol relative (DESIGN.md
+    reading R31) -- else alpha_{i+1} = 2 alpha_i.  Returns (last Oracle, alphas, objectives,
+    converged); the objective is the implicit tr(L X_T) in original units."""
+    alphas, objs = [], []
+    alpha = float(alpha0)
+    o = None
+    for i in range(int(max_rounds)):
+        o = Oracle(L, R, alpha=alpha, beta0=beta0, seed=seed, scale=scale, logcap=T, trace_le=True)
+        o.step(T)
+        alphas.append(alpha)
+        objs.append(o.implicit_objective())
+        if i > 0 and abs(objs[i] - objs[i - 1]) <= rtol * abs(objs[i]):
+            return o, np.array(alphas), np.array(objs), True
+        alpha = 2.0 * alpha
+    return o, np.array(alphas), np.array(objs), False
+
+
 def trace_correct(Lam, alpha: float):
     """Alg. 4 line 13: Lam + (alpha - tr Lam) I / R."""
     Lam = np.asarray(Lam, dtype=np.float64)

@@ -96,7 +96,8 @@ EXPORTS = ["sketchycgal_maxcut_init", "sketchycgal_step", "sketchycgal_synchroni
            "sketchycgal_get_state", "sketchycgal_apply_D", "sketchycgal_iterations", "sketchycgal_launch_count",
            "sketchycgal_kernel_stats", "sketchycgal_reset_stats", "sketchycgal_nccl_unique_id",
            "sketchycgal_row_splits", "sketchycgal_halo_plan", "sketchycgal_run",
-           "sketchycgal_selftest_division", "sketchycgal_last_error", "sketchycgal_destroy"]
+           "sketchycgal_selftest_division", "sketchycgal_last_error", "sketchycgal_destroy",
+           "sketchycgal_maxcut_alpha_doubling"]
 
 _lib = None
 
@@ -125,6 +126,10 @@ def open_library(path: str = LIB_PATH):
     lib.sketchycgal_reset_stats.argtypes = [P]
     lib.sketchycgal_run.restype = ctypes.c_int
     lib.sketchycgal_run.argtypes = [P, I64, D, I64, ctypes.POINTER(I64)]
+    lib.sketchycgal_maxcut_alpha_doubling.restype = ctypes.c_int
+    lib.sketchycgal_maxcut_alpha_doubling.argtypes = [ctypes.POINTER(P), ctypes.POINTER(Csr), I32, D, D,
+                                                      ctypes.c_uint64, ctypes.c_uint32, I32, P, I64, D, I32, P, P,
+                                                      ctypes.POINTER(I32), ctypes.POINTER(I32)]
     lib.sketchycgal_row_splits.restype = ctypes.c_int
     lib.sketchycgal_row_splits.argtypes = [P, I64, I32, P]
     lib.sketchycgal_halo_plan.restype = I64
@@ -250,6 +255,35 @@ class SketchyCGAL:
                                               flags, dptr, int(device), stream)
         if st != 0:
             raise ScgError(f"sketchycgal_maxcut_init: {STATUS.get(st, st)}")
+
+    @classmethod
+    def alpha_doubling(cls, L, R: int, alpha0: float, T: int, rtol: float = 1e-2, max_rounds: int = 8,
+                       beta0: float = 1.0, seed: int = 0, scale: bool = True, trace_correct: bool = True,
+                       device: int = 0, stream=None):
+        """Standard-form driver through ``sketchycgal_maxcut_alpha_doubling``:
+        trace-bounded solves tr X <= alpha_i, alpha_{i+1} = 2 alpha_i, until the implicit objective
+        repeats within ``rtol``.  Returns (context of the last round, alphas, objectives, converged)."""
+        self = cls.__new__(cls)
+        self.lib = load()
+        self.n, self.R = int(L.n), int(R)
+        self._splits = None
+        self.row_begin, self.row_end, self.nl = 0, self.n, self.n
+        rp, col, val = _c64(L.row_ptr, np.int64), _c64(L.col, np.int32), _c64(L.val, np.float64)
+        self._keep = (rp, col, val)
+        csr = Csr(self.n, 0, self.n, rp.ctypes.data, col.ctypes.data, val.ctypes.data, 1)
+        flags = (SCG_SCALE if scale else 0) | (SCG_TRACE_CORRECT if trace_correct else 0)
+        alphas = np.zeros(int(max_rounds))
+        objs = np.zeros(int(max_rounds))
+        rounds, conv = ctypes.c_int32(0), ctypes.c_int32(0)
+        self._h = ctypes.c_void_p()
+        st = self.lib.sketchycgal_maxcut_alpha_doubling(
+            ctypes.byref(self._h), ctypes.byref(csr), self.R, float(alpha0), float(beta0), int(seed), flags,
+            int(device), stream, int(T), float(rtol), int(max_rounds), alphas.ctypes.data, objs.ctypes.data,
+            ctypes.byref(rounds), ctypes.byref(conv))
+        if st != 0:
+            raise ScgError(f"sketchycgal_maxcut_alpha_doubling: {STATUS.get(st, st)}")
+        k = rounds.value
+        return self, alphas[:k].copy(), objs[:k].copy(), bool(conv.value)
 
     def _check(self, st, what):
         if st != 0:

@@ -1813,6 +1813,45 @@ static scg_status colstats(scg_ctx *c, int which, const double *lam_host, std::v
   return host_allreduce(c, outk);
 }
 
+scg_status sketchycgal_maxcut_alpha_doubling(scg_ctx **out, const scg_csr *L, int32_t R, double alpha0,
+                                             double beta0, uint64_t seed, uint32_t flags, int32_t device,
+                                             void *cuda_stream, int64_t T, double rtol, int32_t max_rounds,
+                                             double *alphas, double *objs, int32_t *rounds, int32_t *converged) {
+  if (!out || !L || !(alpha0 > 0) || T < 1 || !(rtol >= 0) || max_rounds < 1 || !alphas || !objs || !rounds ||
+      !converged)
+    return SCG_EINVAL;
+  *out = nullptr;
+  *rounds = 0;
+  *converged = 0;
+  double alpha = alpha0;
+  scg_ctx *prev = nullptr;
+  for (int32_t i = 0; i < max_rounds; ++i) {
+    scg_ctx *c = nullptr;
+    scg_status st = sketchycgal_maxcut_init(&c, L, R, alpha, beta0, seed, flags | SCG_TRACE_LE, nullptr, device,
+                                            cuda_stream);
+    double ob[2] = {0.0, 0.0};
+    if (!st) st = sketchycgal_step(c, T);
+    if (!st) st = sketchycgal_objective(c, ob);
+    if (st) {
+      if (c) sketchycgal_destroy(c);
+      if (prev) sketchycgal_destroy(prev);
+      return st;
+    }
+    alphas[i] = alpha;
+    objs[i] = ob[0];
+    *rounds = i + 1;
+    if (prev) sketchycgal_destroy(prev);
+    prev = c;
+    if (i > 0 && std::fabs(objs[i] - objs[i - 1]) <= rtol * std::fabs(objs[i])) {  // step 3 (reading R31)
+      *converged = 1;
+      break;
+    }
+    alpha = 2.0 * alpha;  // step 4
+  }
+  *out = prev;
+  return SCG_OK;
+}
+
 scg_status sketchycgal_objective(scg_ctx *c, double out[2]) {
   if (!c || !out) return SCG_EINVAL;
   scg_status st = sketchycgal_synchronize(c);

@@ -436,3 +436,24 @@ def test_bench_launch_configuration_bitwise(gpu):
     o = oracle.Oracle(L, 10, seed=1, logcap=200)
     o.step(200)
     _assert_trajectory(g, o, 200)
+
+
+@pytest.mark.parametrize("graph,alpha0,T", [("c5", 1.25, 3000), ("c0", 400.0, 200)])
+def test_alpha_doubling_driver_matches_oracle(gpu, graph, alpha0, T):
+    """Standard-form driver through the C ABI against the oracle's: the same
+    alpha sequence, stopping round and decision; per-round implicit objectives to rounding."""
+    if graph == "c5":
+        n = 5
+        i = np.arange(n)
+        L = si.laplacian_from_edges(n, i, (i + 1) % n, np.ones(n))
+        R, seed = 3, 5
+    else:
+        L = si.laplacian("c0")
+        R, seed = 10, 0
+    g, al, ob, conv = gpu.SketchyCGAL.alpha_doubling(L, R, alpha0=alpha0, T=T, rtol=1e-2, max_rounds=5, seed=seed)
+    o, al_o, ob_o, conv_o = oracle.alpha_doubling(L, R, alpha0=alpha0, T=T, rtol=1e-2, max_rounds=5, seed=seed)
+    np.testing.assert_array_equal(al, al_o)
+    assert conv == conv_o
+    np.testing.assert_allclose(ob, ob_o, rtol=1e-12, atol=0)
+    np.testing.assert_array_equal(g.state("z"), o.z)  # the last round's iterate, bitwise
+    g.close()

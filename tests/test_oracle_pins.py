@@ -530,3 +530,25 @@ def test_trace_bounded_sdp_value_and_trace():
     oe = oracle.Oracle(L, 3, seed=5, logcap=1)
     oe.step(3000)
     assert abs(o.implicit_objective() - oe.implicit_objective()) / sdp < 3e-3
+
+
+def test_alpha_doubling_standard_form_driver():
+    """Remark "Standard-form SDP" on C5 (closed-form SDP value, P-independent):
+    diag X = 1 forces tr X = n, so a bound alpha < n scales the optimum to (alpha / n) X* with
+    objective (alpha / n) * SDP, and every alpha >= n gives the SDP itself.  From alpha0 = n/4 the
+    driver doubles through n/4, n/2, n and stops at 2n (objective repeated within rtol) with the
+    SDP value; from alpha0 >= n it stops after two rounds."""
+    n = 5
+    L = _edges_graph(n, [(k, (k + 1) % n) for k in range(n)])
+    sdp = 2 * n * (1 + math.cos(math.pi / n))
+    o, al, ob, conv = oracle.alpha_doubling(L, 3, alpha0=n / 4, T=3000, rtol=1e-2, seed=5)
+    assert conv
+    np.testing.assert_array_equal(al, (n / 4) * 2.0 ** np.arange(4))
+    for a, v in zip(al, ob):
+        assert abs(v - min(a / n, 1.0) * sdp) <= 3e-3 * sdp
+    assert o.alpha_orig == 2 * n
+    o2, al2, ob2, conv2 = oracle.alpha_doubling(L, 3, alpha0=1.05 * n, T=3000, rtol=1e-2, seed=5)
+    assert conv2 and len(al2) == 2 and abs(ob2[-1] - sdp) <= 3e-3 * sdp
+    # max_rounds caps an unconverged sequence
+    _, al3, _, conv3 = oracle.alpha_doubling(L, 3, alpha0=n / 4, T=3000, rtol=1e-2, seed=5, max_rounds=2)
+    assert not conv3 and len(al3) == 2
