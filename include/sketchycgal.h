@@ -69,6 +69,9 @@ enum {
                                    the LMO is H = alpha v v^T if xi_t < 0, else 0; e.g. the
                                    DIMACS-style MaxCut setup alpha = 1.05 n.  Trace correction then
                                    uses the tracked trace tau instead of alpha (reading R29) */
+  SCG_INEQ = 1u << 4,           /* general template with K = {u <= b}: diag X <= 1
+                                   instead of diag X = 1; b is replaced by the slack w = min(z + y/beta, b) in D_t
+                                   and in the dual update (reading R32); the gap / bound records are NaN */
   SCG_PROFILE = 1u << 8         /* record CUDA events around every kernel launch (bench / kernel stats) */
 };
 

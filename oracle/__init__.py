@@ -189,7 +189,8 @@ class Oracle:
     """Alg. 4 SketchyCGAL for MaxCut (C = -L, A = diag, b = 1, alpha = n)."""
 
     def __init__(self, L, R: int, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
-                 scale: bool = True, qfix: int = 0, logcap: int = 0, vhist: int = 0, trace_le: bool = False):
+                 scale: bool = True, qfix: int = 0, logcap: int = 0, vhist: int = 0, trace_le: bool = False,
+                 ineq: bool = False):
         self.L = L
         self.n = L.n
         self.R = int(R)
@@ -202,8 +203,10 @@ class Oracle:
         self._val = _f64(L.val)
         self._h = _load().oracle_create(self.n, self._rp.ctypes.data, self._col.ctypes.data, self._val.ctypes.data,
                                         self.R, self.alpha_orig, float(beta0), int(seed), 1 if scale else 0,
-                                        int(qfix), self.logcap, self.vhist_cap, 1 if trace_le else 0)
+                                        int(qfix), self.logcap, self.vhist_cap,
+                                        (1 if trace_le else 0) | (2 if ineq else 0))
         self.trace_le = bool(trace_le)
+        self.ineq = bool(ineq)
         self.beta0 = float(beta0)
 
     def __del__(self):

@@ -420,6 +420,7 @@ typedef struct {
   double alpha_orig, alpha, beta0, bval, nrmL;
   int scale;
   int trace_le; /* tr X <= alpha: H = alpha v v* if xi < 0, else 0 */
+  int ineq;     /* general template with K = {u <= b}: diag X <= 1 */
   uint64_t seed;
   int qfix; /* test-only: fixed Lanczos bound (may be n); 0 = schedule */
   int64_t t; /* iterations done */
@@ -445,7 +446,8 @@ void *oracle_create(int64_t n, const int64_t *rp_L, const int32_t *col_L, const 
                     int64_t vhist_cap, int trace_le) {
   oracle_t *o = (oracle_t *)calloc(1, sizeof(oracle_t));
   o->n = n; o->R = R; o->beta0 = beta0; o->seed = seed; o->scale = scale; o->qfix = qfix;
-  o->trace_le = trace_le;
+  o->trace_le = trace_le & 1;      /* bit 0: trace-bounded set */
+  o->ineq = (trace_le >> 1) & 1;    /* bit 1: inequality constraints A X <= b */
   o->alpha_orig = alpha;
   /* ||C||_F = ||L||_F over all stored entries (CAC-2), scaling P:1805-1814 (reading A13) */
   int err = 0;
@@ -540,8 +542,13 @@ int oracle_step(void *h, int64_t T) {
     const double S_z = o_dot(o->z, o->ones, n, &gerr);
     const double p_t = o->p;
     o->err |= gerr;
-    /* line 6: D = C + A*(y + beta (z - b)) ; diagonal of D (primitive 2) */
-    for (int64_t r = 0; r < n; ++r) o->d[r] = fma(beta, o->z[r] - o->bval, o->y[r]) + o->cdiag[r];
+    /* line 6: D = C + A*(y + beta (z - b)) ; diagonal of D (primitive 2).
+     * General template, K = {u <= b}: b is replaced by the slack
+     * w_t = proj_K(z_t + y_t / beta_t) = min(z_t + y_t / beta_t, b), elementwise (reading R32). */
+    for (int64_t r = 0; r < n; ++r) {
+      const double wr = o->ineq ? fmin(o->z[r] + o->y[r] / beta, o->bval) : o->bval;
+      o->d[r] = fma(beta, o->z[r] - wr, o->y[r]) + o->cdiag[r];
+    }
     for (int64_t r = 0; r < n; ++r) o->g[r] = scg_lanczos_start(o->seed, t, r);
     o_lanczos_res res;
     memset(&res, 0, sizeof(res));
@@ -562,8 +569,14 @@ int oracle_step(void *h, int64_t T) {
       double h = o->alpha * (o->v[r] * o->v[r]);
       o->z[r] = hoff ? one_m_eta * o->z[r] : fma(eta, h, one_m_eta * o->z[r]);
     }
-    /* line 8: gamma from ||z - b||^2, y <- y + gamma (z - b) */
-    for (int64_t r = 0; r < n; ++r) o->a[r] = o->z[r] - o->bval;
+    /* line 8: gamma from ||z - b||^2, y <- y + gamma (z - b).  General template:
+     * b is replaced by wbar_t = proj_K(z_{t+1} + y_t / beta_{t+1}) and the step rule keeps the
+     * form gamma ||z - wbar||^2 <= beta_t eta_t^2 alpha^2 ||A||^2 (reading R32). */
+    const double beta1 = o->beta0 * sqrt((double)(t + 2));
+    for (int64_t r = 0; r < n; ++r) {
+      const double wb = o->ineq ? fmin(o->z[r] + o->y[r] / beta1, o->bval) : o->bval;
+      o->a[r] = o->z[r] - wb;
+    }
     double nz = o_dot(o->a, o->a, n, &err);
     double gamma = oracle_gamma(t, o->alpha, o->beta0, nz);
     for (int64_t r = 0; r < n; ++r) o->y[r] = fma(gamma, o->a[r], o->y[r]);
@@ -593,6 +606,7 @@ int oracle_step(void *h, int64_t T) {
       L[10] = ((p_t + S_yz) + beta * (S_zz - o->bval * S_z)) - ax;
       const double nbb = ((double)n * o->bval) * o->bval;
       L[11] = ((p_t + o->bval * S_y) + (0.5 * beta) * (S_zz - nbb)) - ax;
+      if (o->ineq) L[10] = L[11] = NAN; /* the gap / bound formulas are for A X = b (reading R32) */
     }
     if (o->vhist && t - 1 < o->vhist_cap) memcpy(o->vhist + (t - 1) * n, o->v, sizeof(double) * (size_t)n);
     o->t = t;

@@ -26,6 +26,7 @@ SCG_SCALE = 1 << 0
 SCG_TRACE_CORRECT = 1 << 1
 SCG_REGENERATE = 1 << 2
 SCG_TRACE_LE = 1 << 3
+SCG_INEQ = 1 << 4
 SCG_PROFILE = 1 << 8
 
 STATUS = {0: "SCG_OK", -1: "SCG_EINVAL", -2: "SCG_ENOMEM", -3: "SCG_ECUDA", -4: "SCG_ENCCL", -5: "SCG_ECHOL",
@@ -215,7 +216,7 @@ class SketchyCGAL:
     def __init__(self, L, R: int, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
                  scale: bool = True, trace_correct: bool = True, profile: bool = False, device: int = 0,
                  stream=None, regenerate: bool = False, trace_le: bool = False, shards: int = 1, splits=None,
-                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None, ineq: bool = False):
         self.lib = load()
         self.n = int(L.n)
         self.R = int(R)
@@ -244,7 +245,7 @@ class SketchyCGAL:
         csr = Csr(self.n, self.row_begin, self.row_end, rp.ctypes.data, col.ctypes.data, val.ctypes.data, 1)
         flags = (SCG_SCALE if scale else 0) | (SCG_TRACE_CORRECT if trace_correct else 0) | \
                 (SCG_PROFILE if profile else 0) | (SCG_REGENERATE if regenerate else 0) | \
-                (SCG_TRACE_LE if trace_le else 0)
+                (SCG_TRACE_LE if trace_le else 0) | (SCG_INEQ if ineq else 0)
         self._h = ctypes.c_void_p()
         dptr = None
         if dist is not None:

@@ -86,6 +86,7 @@ struct IterArgs {
   long long t;
   int q;
   int trace_le;  // SCG_TRACE_LE: H = 0 when xi_t >= 0
+  int ineq;      // SCG_INEQ: K = {u <= b}, slack w = min(z + y / beta, b) (reading R32)
   double eta, one_m_eta, alpha, b, beta0, sq, beta_next, nbb;  // nbb = fl(fl(n b) b) = ||b||^2
 };
 
@@ -1265,8 +1266,8 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
       rec.znorm = sqrt(nz);
       rec.gamma = sc->gamma;
       rec.tau = sc->tau;
-      rec.gap = gapv;
-      rec.bound = boundv;
+      rec.gap = A.ineq ? NAN : gapv;  // the gap / bound formulas are for A X = b (reading R32)
+      rec.bound = A.ineq ? NAN : boundv;
       f.log[A.t - 1] = rec;
       break;
     }
@@ -1420,10 +1421,12 @@ __global__ void k_omega(double *__restrict__ Om, int nl, long long rb, int R, ui
 
 // d = fl(fma(beta, fl(z - b), y) + C_rr) (primitive 2 with y + beta (z - b)).
 __global__ void k_init_d(const double *__restrict__ z, const double *__restrict__ y, const double *__restrict__ cdiag,
-                         double *__restrict__ d, int nl, double b, double beta) {
+                         double *__restrict__ d, int nl, double b, double beta, int ineq) {
   pdl_entry();
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x)
-    d[r] = fma(beta, z[r] - b, y[r]) + cdiag[r];
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double w = ineq ? fmin(z[r] + y[r] / beta, b) : b;  // slack w_1 = proj_K(z + y / beta)
+    d[r] = fma(beta, z[r] - w, y[r]) + cdiag[r];
+  }
 }
 
 // Lanczos start vector g = randn (Alg. 2 line 1) for iteration t and ||g||^2 (exact).
@@ -2351,6 +2354,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
 // z <- (1-eta) z + eta alpha (v o v) (Alg. 4 line 8, primitive 3), ||z - b||^2 (exact),
 // per-block partials of g = v^T Omega (fp64, fixed tree; off the feedback path).
 __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__ v, double *__restrict__ z,
+                                                   const double *__restrict__ y,
                                                    const double *__restrict__ Om, int nl, int R, IterArgs A,
                                                    double *__restrict__ gpart, XSlot *slot, DevScalars *sc,
                                                    scg_iter_rec *log, Net net) {
@@ -2389,7 +2393,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
             // trace-bounded LMO with xi_t >= 0: H = 0
             const double zr = hoff ? A.one_m_eta * zv[h] : fma(A.eta, hv, A.one_m_eta * zv[h]);
             z[r] = zr;
-            const double e = zr - A.b;
+            // z_{t+1} - b, or z_{t+1} - wbar_t with wbar_t = min(z_{t+1} + y_t / beta_{t+1}, b)
+            const double e = zr - (A.ineq ? fmin(zr + y[r] / A.beta_next, A.b) : A.b);
             xwin_add_nn(acc[0], e * e, err, xb.l[0]);
           }
 #pragma unroll
@@ -2467,10 +2472,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
     for (int u = 0; u < 2; ++u) {
       const int r = r0 + u * stride;
       if (r < nl) {
-        const double e = zr[u] - A.b;
+        // dual update with wbar_t (b when A X = b) and the next diagonal with w_{t+1}
+        const double e = zr[u] - (A.ineq ? fmin(zr[u] + yv[u] / A.beta_next, A.b) : A.b);
         const double yr = fma(gam, e, yv[u]);
         y[r] = yr;
-        d[r] = fma(A.beta_next, e, yr) + cd[u];
+        const double e1 = A.ineq ? zr[u] - fmin(zr[u] + yr / A.beta_next, A.b) : e;
+        d[r] = fma(A.beta_next, e1, yr) + cd[u];
         const double gv = scg_lanczos_start(seed, A.t + 1, rb + og[u]);
         gstore_m(net, g + rb + r, mk[u], gv);
         peer |= mk[u];

@@ -1312,7 +1312,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
            (const int *)s->orig);
     const double beta1 = beta0 * std::sqrt(2.0);
     launch(c, KC_OTHER, 0.0, k_init_d, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z, (const double *)s->y,
-           (const double *)s->cdiag, s->d, (int)s->nl, c->b, beta1);
+           (const double *)s->cdiag, s->d, (int)s->nl, c->b, beta1, (c->flags & SCG_INEQ) ? 1 : 0);
   }
   const unsigned long long E1 = ++c->epoch;
   for (Shard *s : c->sh)
@@ -1363,6 +1363,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     A.beta_next = c->beta0 * std::sqrt((double)(t + 2));
     A.nbb = ((double)c->n * c->b) * c->b;
     A.trace_le = (c->flags & SCG_TRACE_LE) ? 1 : 0;
+    A.ineq = (c->flags & SCG_INEQ) ? 1 : 0;
     int64_t q = (int64_t)std::ceil(std::sqrt(std::sqrt((double)t)) * c->lnN);
     if (q < 2) q = 2;
     if (q > c->n - 1) q = c->n - 1;
@@ -1479,7 +1480,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     E = ++c->epoch;
     for (Shard *s : c->sh)
       launch(c, KC_PRIMAL, s->kb[KC_PRIMAL], k_primal, dim3(s->grid_primal), dim3(kBlock), (const double *)c->vslot(s, js), s->z,
-             (const double *)s->Om, (int)s->nl, c->R, A, s->gpart, s->slots + SLOT_NZ, s->sc, s->dlog, net_of(c, s, E));
+             (const double *)s->y, (const double *)s->Om, (int)s->nl, c->R, A, s->gpart, s->slots + SLOT_NZ, s->sc, s->dlog, net_of(c, s, E));
     {
       FinArgs f{};
       f.R = c->R;

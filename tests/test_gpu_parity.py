@@ -457,3 +457,24 @@ def test_alpha_doubling_driver_matches_oracle(gpu, graph, alpha0, T):
     np.testing.assert_allclose(ob, ob_o, rtol=1e-12, atol=0)
     np.testing.assert_array_equal(g.state("z"), o.z)  # the last round's iterate, bitwise
     g.close()
+
+
+@pytest.mark.parametrize("graph,shards,trace_le", [("c0", 1, False), ("c0", 2, False), ("c5", 1, True),
+                                                   ("c1", 1, False)])
+def test_inequality_template_bitwise(gpu, graph, shards, trace_le):
+    """General template with K = {u <= b} (SCG_INEQ): slack w = min(z + y/beta, b) in
+    D_t and in the dual update; every iterate bitwise against the oracle (sharded too)."""
+    if graph == "c5":
+        n = 5
+        i = np.arange(n)
+        L = si.laplacian_from_edges(n, i, (i + 1) % n, np.ones(n))
+        R, seed, T, alpha = 3, 5, 400, 2.5
+    else:
+        L = si.laplacian(graph)
+        c = si.CONFIGS[graph]
+        R, seed, T, alpha = c["R"], c["seed"], 200, None
+    g = gpu.SketchyCGAL(L, R=R, seed=seed, alpha=alpha, ineq=True, trace_le=trace_le, shards=shards)
+    g.step(T)
+    o = oracle.Oracle(L, R, seed=seed, alpha=alpha, logcap=T, ineq=True, trace_le=trace_le)
+    o.step(T)
+    _assert_trajectory(g, o, T)

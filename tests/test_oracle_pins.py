@@ -552,3 +552,23 @@ def test_alpha_doubling_standard_form_driver():
     # max_rounds caps an unconverged sequence
     _, al3, _, conv3 = oracle.alpha_doubling(L, 3, alpha0=n / 4, T=3000, rtol=1e-2, seed=5, max_rounds=2)
     assert not conv3 and len(al3) == 2
+
+
+def test_inequality_template_closed_forms():
+    """General template with K = {u <= b} (SCG_INEQ): MaxCut with
+    diag X <= 1.  On C5 the optimum still has diag X = 1 (L is psd), so the closed-form SDP value
+    is recovered; with tr X <= n/2 as well, the equality problem is infeasible while the
+    inequality one has the vertex-transitive optimum (1/2) X*, value SDP/2, and a feasible
+    iterate (z <= b).  The gap / bound records (equality-only formulas) are NaN."""
+    n = 5
+    L = _edges_graph(n, [(k, (k + 1) % n) for k in range(n)])
+    sdp = 2 * n * (1 + math.cos(math.pi / n))
+    o = oracle.Oracle(L, 3, seed=5, logcap=3000, ineq=True)
+    o.step(3000)
+    assert abs(o.implicit_objective() - sdp) <= 3e-3 * sdp
+    assert np.all(np.isnan(o.log[:, 10:12]))
+    h = oracle.Oracle(L, 3, seed=5, logcap=3000, ineq=True, trace_le=True, alpha=n / 2)
+    h.step(3000)
+    assert abs(h.implicit_objective() - sdp / 2) <= 3e-3 * sdp
+    z = h.z * (h.alpha_orig / h.alpha)  # diag X_T in original units
+    assert np.all(z <= 1.0 + 1e-3) and abs(z.sum() - n / 2) <= 1e-2 * n
