@@ -189,6 +189,14 @@ scg_status sketchycgal_maxcut_alpha_doubling(scg_ctx **out, const scg_csr *L, in
                                              void *cuda_stream, int64_t T, double rtol, int32_t max_rounds,
                                              double *alphas, double *objs, int32_t *rounds, int32_t *converged);
 
+/* Convex inclusion A X in K for the box K = {u : lo <= u_i <= hi} (general template,
+ * PAPER.md:3909-3941; the l_inf ball |u - b| <= delta of P:3915-3918 is lo = 1 - delta,
+ * hi = 1 + delta; lo = -INFINITY, hi = 1 is SCG_INEQ).  Original units (the MaxCut b is 1).
+ * Call after init and before the first step (recomputes D_1's diagonal); SCG_EINVAL
+ * otherwise, for NaN bounds, lo > hi or hi = -inf.  Reading R32: slack
+ * w = min(max(z + y / beta, lo), hi); the gap / bound records are NaN. */
+scg_status sketchycgal_set_box(scg_ctx *c, double lo, double hi);
+
 /* Block until all queued work is done; reports deferred device errors. */
 scg_status sketchycgal_synchronize(scg_ctx *c);
 

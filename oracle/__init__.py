@@ -74,6 +74,8 @@ def _load():
         lib.oracle_destroy.argtypes = [P]
         lib.oracle_step.restype = ctypes.c_int
         lib.oracle_step.argtypes = [P, I64]
+        lib.oracle_set_box.restype = ctypes.c_int
+        lib.oracle_set_box.argtypes = [P, ctypes.c_double, ctypes.c_double]
         lib.oracle_t_done.restype = I64
         lib.oracle_t_done.argtypes = [P]
         lib.oracle_scalar.restype = D
@@ -190,7 +192,7 @@ class Oracle:
 
     def __init__(self, L, R: int, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
                  scale: bool = True, qfix: int = 0, logcap: int = 0, vhist: int = 0, trace_le: bool = False,
-                 ineq: bool = False):
+                 ineq: bool = False, box: tuple | None = None):
         self.L = L
         self.n = L.n
         self.R = int(R)
@@ -206,7 +208,10 @@ class Oracle:
                                         int(qfix), self.logcap, self.vhist_cap,
                                         (1 if trace_le else 0) | (2 if ineq else 0))
         self.trace_le = bool(trace_le)
-        self.ineq = bool(ineq)
+        self.ineq = bool(ineq) or box is not None
+        if box is not None:  # K = {lo <= u <= hi}, original units
+            if _load().oracle_set_box(self._h, float(box[0]), float(box[1])) != 0:
+                raise ValueError("oracle_set_box: after the first step or lo > hi")
         self.beta0 = float(beta0)
 
     def __del__(self):

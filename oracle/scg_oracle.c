@@ -420,7 +420,8 @@ typedef struct {
   double alpha_orig, alpha, beta0, bval, nrmL;
   int scale;
   int trace_le; /* tr X <= alpha: H = alpha v v* if xi < 0, else 0 */
-  int ineq;     /* general template with K = {u <= b}: diag X <= 1 */
+  int ineq;     /* general template with a box K = {lo <= u <= hi} */
+  double lo, hi; /* scaled units; bit 1 of the mode (SCG_INEQ): lo = -inf, hi = b */
   uint64_t seed;
   int qfix; /* test-only: fixed Lanczos bound (may be n); 0 = schedule */
   int64_t t; /* iterations done */
@@ -460,6 +461,8 @@ void *oracle_create(int64_t n, const int64_t *rp_L, const int32_t *col_L, const 
   }
   if (scale) { o->alpha = alpha / (double)n; o->bval = 1.0 / (double)n; } /* X~ = X / n (A13) */
   else { o->alpha = alpha; o->bval = 1.0; }
+  o->lo = -INFINITY;
+  o->hi = o->bval;
   /* split L into off-diagonal C entries and diagonal: C = -L, scaled C / ||C||_F */
   int64_t nnz_off = 0;
   for (int64_t r = 0; r < n; ++r)
@@ -514,6 +517,16 @@ void oracle_destroy(void *h) {
   free(o);
 }
 
+/* Box K = {lo <= u <= hi} in original units; before the first step. */
+int oracle_set_box(void *h, double lo, double hi) {
+  oracle_t *o = (oracle_t *)h;
+  if (o->t != 0 || !(lo <= hi)) return -1;
+  o->ineq = 1;
+  o->lo = o->scale ? lo / (double)o->n : lo;
+  o->hi = o->scale ? hi / (double)o->n : hi;
+  return 0;
+}
+
 int oracle_step(void *h, int64_t T) {
   oracle_t *o = (oracle_t *)h;
   int64_t n = o->n;
@@ -544,9 +557,9 @@ int oracle_step(void *h, int64_t T) {
     o->err |= gerr;
     /* line 6: D = C + A*(y + beta (z - b)) ; diagonal of D (primitive 2).
      * General template, K = {u <= b}: b is replaced by the slack
-     * w_t = proj_K(z_t + y_t / beta_t) = min(z_t + y_t / beta_t, b), elementwise (reading R32). */
+     * w_t = proj_K(z_t + y_t / beta_t) = min(max(z_t + y_t / beta_t, lo), hi), elementwise (R32). */
     for (int64_t r = 0; r < n; ++r) {
-      const double wr = o->ineq ? fmin(o->z[r] + o->y[r] / beta, o->bval) : o->bval;
+      const double wr = o->ineq ? fmin(fmax(o->z[r] + o->y[r] / beta, o->lo), o->hi) : o->bval;
       o->d[r] = fma(beta, o->z[r] - wr, o->y[r]) + o->cdiag[r];
     }
     for (int64_t r = 0; r < n; ++r) o->g[r] = scg_lanczos_start(o->seed, t, r);
@@ -574,7 +587,7 @@ int oracle_step(void *h, int64_t T) {
      * form gamma ||z - wbar||^2 <= beta_t eta_t^2 alpha^2 ||A||^2 (reading R32). */
     const double beta1 = o->beta0 * sqrt((double)(t + 2));
     for (int64_t r = 0; r < n; ++r) {
-      const double wb = o->ineq ? fmin(o->z[r] + o->y[r] / beta1, o->bval) : o->bval;
+      const double wb = o->ineq ? fmin(fmax(o->z[r] + o->y[r] / beta1, o->lo), o->hi) : o->bval;
       o->a[r] = o->z[r] - wb;
     }
     double nz = o_dot(o->a, o->a, n, &err);

@@ -98,7 +98,7 @@ EXPORTS = ["sketchycgal_maxcut_init", "sketchycgal_step", "sketchycgal_synchroni
            "sketchycgal_kernel_stats", "sketchycgal_reset_stats", "sketchycgal_nccl_unique_id",
            "sketchycgal_row_splits", "sketchycgal_halo_plan", "sketchycgal_run",
            "sketchycgal_selftest_division", "sketchycgal_last_error", "sketchycgal_destroy",
-           "sketchycgal_maxcut_alpha_doubling"]
+           "sketchycgal_maxcut_alpha_doubling", "sketchycgal_set_box"]
 
 _lib = None
 
@@ -127,6 +127,8 @@ def open_library(path: str = LIB_PATH):
     lib.sketchycgal_reset_stats.argtypes = [P]
     lib.sketchycgal_run.restype = ctypes.c_int
     lib.sketchycgal_run.argtypes = [P, I64, D, I64, ctypes.POINTER(I64)]
+    lib.sketchycgal_set_box.restype = ctypes.c_int
+    lib.sketchycgal_set_box.argtypes = [P, D, D]
     lib.sketchycgal_maxcut_alpha_doubling.restype = ctypes.c_int
     lib.sketchycgal_maxcut_alpha_doubling.argtypes = [ctypes.POINTER(P), ctypes.POINTER(Csr), I32, D, D,
                                                       ctypes.c_uint64, ctypes.c_uint32, I32, P, I64, D, I32, P, P,
@@ -216,7 +218,8 @@ class SketchyCGAL:
     def __init__(self, L, R: int, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
                  scale: bool = True, trace_correct: bool = True, profile: bool = False, device: int = 0,
                  stream=None, regenerate: bool = False, trace_le: bool = False, shards: int = 1, splits=None,
-                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None, ineq: bool = False):
+                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None, ineq: bool = False,
+                 box: tuple | None = None):
         self.lib = load()
         self.n = int(L.n)
         self.R = int(R)
@@ -256,6 +259,8 @@ class SketchyCGAL:
                                               flags, dptr, int(device), stream)
         if st != 0:
             raise ScgError(f"sketchycgal_maxcut_init: {STATUS.get(st, st)}")
+        if box is not None:  # K = {lo <= u <= hi}
+            self._check(self.lib.sketchycgal_set_box(self._h, float(box[0]), float(box[1])), "sketchycgal_set_box")
 
     @classmethod
     def alpha_doubling(cls, L, R: int, alpha0: float, T: int, rtol: float = 1e-2, max_rounds: int = 8,

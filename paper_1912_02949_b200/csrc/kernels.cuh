@@ -86,7 +86,8 @@ struct IterArgs {
   long long t;
   int q;
   int trace_le;  // SCG_TRACE_LE: H = 0 when xi_t >= 0
-  int ineq;      // SCG_INEQ: K = {u <= b}, slack w = min(z + y / beta, b) (reading R32)
+  int ineq;      // box K = {lo <= u <= hi} (SCG_INEQ: lo = -inf, hi = b): slack w = min(max(z + y/beta, lo), hi)
+  double lo, hi; //   (reading R32)
   double eta, one_m_eta, alpha, b, beta0, sq, beta_next, nbb;  // nbb = fl(fl(n b) b) = ||b||^2
 };
 
@@ -1421,10 +1422,10 @@ __global__ void k_omega(double *__restrict__ Om, int nl, long long rb, int R, ui
 
 // d = fl(fma(beta, fl(z - b), y) + C_rr) (primitive 2 with y + beta (z - b)).
 __global__ void k_init_d(const double *__restrict__ z, const double *__restrict__ y, const double *__restrict__ cdiag,
-                         double *__restrict__ d, int nl, double b, double beta, int ineq) {
+                         double *__restrict__ d, int nl, double b, double beta, int ineq, double lo, double hi) {
   pdl_entry();
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
-    const double w = ineq ? fmin(z[r] + y[r] / beta, b) : b;  // slack w_1 = proj_K(z + y / beta)
+    const double w = ineq ? fmin(fmax(z[r] + y[r] / beta, lo), hi) : b;  // slack w_1 = proj_K(z + y / beta)
     d[r] = fma(beta, z[r] - w, y[r]) + cdiag[r];
   }
 }
@@ -2393,8 +2394,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
             // trace-bounded LMO with xi_t >= 0: H = 0
             const double zr = hoff ? A.one_m_eta * zv[h] : fma(A.eta, hv, A.one_m_eta * zv[h]);
             z[r] = zr;
-            // z_{t+1} - b, or z_{t+1} - wbar_t with wbar_t = min(z_{t+1} + y_t / beta_{t+1}, b)
-            const double e = zr - (A.ineq ? fmin(zr + y[r] / A.beta_next, A.b) : A.b);
+            // z_{t+1} - b, or z_{t+1} - wbar_t, wbar_t = proj_K(z_{t+1} + y_t / beta_{t+1})
+            const double e = zr - (A.ineq ? fmin(fmax(zr + y[r] / A.beta_next, A.lo), A.hi) : A.b);
             xwin_add_nn(acc[0], e * e, err, xb.l[0]);
           }
 #pragma unroll
@@ -2473,10 +2474,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
       const int r = r0 + u * stride;
       if (r < nl) {
         // dual update with wbar_t (b when A X = b) and the next diagonal with w_{t+1}
-        const double e = zr[u] - (A.ineq ? fmin(zr[u] + yv[u] / A.beta_next, A.b) : A.b);
+        const double e = zr[u] - (A.ineq ? fmin(fmax(zr[u] + yv[u] / A.beta_next, A.lo), A.hi) : A.b);
         const double yr = fma(gam, e, yv[u]);
         y[r] = yr;
-        const double e1 = A.ineq ? zr[u] - fmin(zr[u] + yr / A.beta_next, A.b) : e;
+        const double e1 = A.ineq ? zr[u] - fmin(fmax(zr[u] + yr / A.beta_next, A.lo), A.hi) : e;
         d[r] = fma(A.beta_next, e1, yr) + cd[u];
         const double gv = scg_lanczos_start(seed, A.t + 1, rb + og[u]);
         gstore_m(net, g + rb + r, mk[u], gv);

@@ -123,6 +123,8 @@ struct scg_ctx {
   uint64_t seed = 0;
   // sharding: world ranks; this context holds shards sh (all of them when emulating)
   int world = 1, mode = 0;  // mode 0: single, 1: emulated shards, 2: one rank of a multi-process job
+  bool box = false;           // constraint set K = {klo <= u <= khi} (scaled units): SCG_INEQ or sketchycgal_set_box
+  double klo = 0.0, khi = 0.0;
   bool fused = false;        // one GPU: Lanczos pass 1 as one persistent kernel (SCG_FUSED=1)
   unsigned long long gphase = 0;  // grid-barrier phases issued so far (fused pass 1)
   bool pdl = true;          // programmatic dependent launches (SCG_PDL=0 disables)
@@ -1164,6 +1166,11 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   const bool scale = (flags & SCG_SCALE) != 0;
   c->alpha = scale ? alpha / (double)n : alpha;  // X~ = X / n (= 1 for the MaxCut trace n)
   c->b = scale ? 1.0 / (double)n : 1.0;
+  if (flags & SCG_INEQ) {  // K = {u <= b} (reading R32)
+    c->box = true;
+    c->klo = -INFINITY;
+    c->khi = c->b;
+  }
   c->lnN = std::log((double)n);
   c->log_cap = 1024;
   {
@@ -1312,7 +1319,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
            (const int *)s->orig);
     const double beta1 = beta0 * std::sqrt(2.0);
     launch(c, KC_OTHER, 0.0, k_init_d, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z, (const double *)s->y,
-           (const double *)s->cdiag, s->d, (int)s->nl, c->b, beta1, (c->flags & SCG_INEQ) ? 1 : 0);
+           (const double *)s->cdiag, s->d, (int)s->nl, c->b, beta1, c->box ? 1 : 0, c->klo, c->khi);
   }
   const unsigned long long E1 = ++c->epoch;
   for (Shard *s : c->sh)
@@ -1363,7 +1370,9 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     A.beta_next = c->beta0 * std::sqrt((double)(t + 2));
     A.nbb = ((double)c->n * c->b) * c->b;
     A.trace_le = (c->flags & SCG_TRACE_LE) ? 1 : 0;
-    A.ineq = (c->flags & SCG_INEQ) ? 1 : 0;
+    A.ineq = c->box ? 1 : 0;
+    A.lo = c->klo;
+    A.hi = c->khi;
     int64_t q = (int64_t)std::ceil(std::sqrt(std::sqrt((double)t)) * c->lnN);
     if (q < 2) q = 2;
     if (q > c->n - 1) q = c->n - 1;
@@ -1851,6 +1860,19 @@ scg_status sketchycgal_maxcut_alpha_doubling(scg_ctx **out, const scg_csr *L, in
   }
   *out = prev;
   return SCG_OK;
+}
+
+scg_status sketchycgal_set_box(scg_ctx *c, double lo, double hi) {
+  if (!c || c->t != 0 || std::isnan(lo) || std::isnan(hi) || !(lo <= hi) || !(hi > -INFINITY)) return SCG_EINVAL;
+  const bool scale = (c->flags & SCG_SCALE) != 0;
+  c->box = true;
+  c->klo = scale ? lo / (double)c->n : lo;  // scaled units like b = 1/n
+  c->khi = scale ? hi / (double)c->n : hi;
+  const double beta1 = c->beta0 * std::sqrt(2.0);
+  for (Shard *s : c->sh)  // D_1's diagonal with the slack w_1 = proj_K(z_1 + y_1 / beta_1)
+    launch(c, KC_OTHER, 0.0, k_init_d, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z, (const double *)s->y,
+           (const double *)s->cdiag, s->d, (int)s->nl, c->b, beta1, 1, c->klo, c->khi);
+  return sketchycgal_synchronize(c);
 }
 
 scg_status sketchycgal_objective(scg_ctx *c, double out[2]) {

@@ -478,3 +478,27 @@ def test_inequality_template_bitwise(gpu, graph, shards, trace_le):
     o = oracle.Oracle(L, R, seed=seed, alpha=alpha, logcap=T, ineq=True, trace_le=trace_le)
     o.step(T)
     _assert_trajectory(g, o, T)
+
+
+@pytest.mark.parametrize("graph,box,shards", [("c0", (0.8, 1.2), 1), ("c0", (0.8, 1.2), 3), ("c5", (0.7, 1.3), 1)])
+def test_box_constraint_set_bitwise(gpu, graph, box, shards):
+    """Box K = {lo <= u <= hi} through sketchycgal_set_box: every iterate bitwise
+    against the oracle; the setter refuses NaN / inverted bounds and calls after the first step."""
+    if graph == "c5":
+        n = 5
+        i = np.arange(n)
+        L = si.laplacian_from_edges(n, i, (i + 1) % n, np.ones(n))
+        R, seed, T = 3, 5, 400
+    else:
+        L = si.laplacian(graph)
+        R, seed, T = 10, 0, 200
+    alpha = 1.05 * L.n * box[1]
+    g = gpu.SketchyCGAL(L, R=R, seed=seed, alpha=alpha, trace_le=True, box=box, shards=shards)
+    g.step(T)
+    o = oracle.Oracle(L, R, seed=seed, alpha=alpha, logcap=T, trace_le=True, box=box)
+    o.step(T)
+    _assert_trajectory(g, o, T)
+    assert g.lib.sketchycgal_set_box(g._h, 0.5, 1.5) != 0  # after the first step
+    h = gpu.SketchyCGAL(L, R=R, seed=seed)
+    assert h.lib.sketchycgal_set_box(h._h, 1.5, 0.5) != 0
+    assert h.lib.sketchycgal_set_box(h._h, float("nan"), 1.0) != 0

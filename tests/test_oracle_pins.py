@@ -572,3 +572,32 @@ def test_inequality_template_closed_forms():
     assert abs(h.implicit_objective() - sdp / 2) <= 3e-3 * sdp
     z = h.z * (h.alpha_orig / h.alpha)  # diag X_T in original units
     assert np.all(z <= 1.0 + 1e-3) and abs(z.sum() - n / 2) <= 1e-2 * n
+
+
+def test_box_constraint_set_closed_forms():
+    """Box K = {lo <= u <= hi} (the l_inf ball |u - 1| <= delta of P:3915-3918): on C5 with
+    diag X in [1 - delta, 1 + delta] and tr X <= 1.05 n (1 + delta) the optimum is (1 + delta) X*,
+    value (1 + delta) SDP.  Special cases: lo = hi = 1 is the equality problem (every record but
+    the NaN gap / bound bitwise), lo = -inf, hi = 1 is SCG_INEQ (bitwise)."""
+    n = 5
+    L = _edges_graph(n, [(k, (k + 1) % n) for k in range(n)])
+    sdp = 2 * n * (1 + math.cos(math.pi / n))
+    for d in (0.1, 0.3):
+        o = oracle.Oracle(L, 3, seed=5, logcap=3000, box=(1 - d, 1 + d), trace_le=True, alpha=1.05 * n * (1 + d))
+        o.step(3000)
+        assert abs(o.implicit_objective() - (1 + d) * sdp) <= 3e-3 * sdp
+        z = o.z * (o.alpha_orig / o.alpha)
+        assert np.all(np.abs(z - (1 + d)) <= 5e-3)
+    e = oracle.Oracle(L, 3, seed=5, logcap=300)
+    e.step(300)
+    b = oracle.Oracle(L, 3, seed=5, logcap=300, box=(1.0, 1.0))
+    b.step(300)
+    np.testing.assert_array_equal(b.log[:, :10], e.log[:, :10])
+    np.testing.assert_array_equal(b.z, e.z)
+    assert np.all(np.isnan(b.log[:, 10:12]))
+    i1 = oracle.Oracle(L, 3, seed=5, logcap=300, box=(-np.inf, 1.0))
+    i1.step(300)
+    i2 = oracle.Oracle(L, 3, seed=5, logcap=300, ineq=True)
+    i2.step(300)
+    np.testing.assert_array_equal(i1.log, i2.log)
+    np.testing.assert_array_equal(i1.y, i2.y)
