@@ -2354,6 +2354,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
 // ---------------------------------------------------------------- primal / dual / sketch
 // z <- (1-eta) z + eta alpha (v o v) (Alg. 4 line 8, primitive 3), ||z - b||^2 (exact),
 // per-block partials of g = v^T Omega (fp64, fixed tree; off the feedback path).
+template <bool BOX>  // box constraint set (A.ineq): compiled out of the equality instantiation
 __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__ v, double *__restrict__ z,
                                                    const double *__restrict__ y,
                                                    const double *__restrict__ Om, int nl, int R, IterArgs A,
@@ -2395,7 +2396,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
             const double zr = hoff ? A.one_m_eta * zv[h] : fma(A.eta, hv, A.one_m_eta * zv[h]);
             z[r] = zr;
             // z_{t+1} - b, or z_{t+1} - wbar_t, wbar_t = proj_K(z_{t+1} + y_t / beta_{t+1})
-            const double e = zr - (A.ineq ? fmin(fmax(zr + y[r] / A.beta_next, A.lo), A.hi) : A.b);
+            const double e = zr - (BOX ? fmin(fmax(zr + y[r] / A.beta_next, A.lo), A.hi) : A.b);
             xwin_add_nn(acc[0], e * e, err, xb.l[0]);
           }
 #pragma unroll
@@ -2440,6 +2441,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
 // y <- y + gamma (z - b) (Alg. 4 line 9); d for t+1; next start vector g_{t+1} and
 // ||g_{t+1}||^2 (exact).  The sketch update of Alg. 4 line 10 is deferred (k_sketch_flush):
 // this kernel records its coefficients ck = fl(eta alpha) g_k in the ring slot js.
+template <bool BOX>  // box constraint set (A.ineq): compiled out of the equality instantiation
 __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restrict__ z, double *__restrict__ y,
                                                         double *__restrict__ d, const double *__restrict__ cdiag,
                                                         double *__restrict__ ckr, int js,
@@ -2474,10 +2476,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
       const int r = r0 + u * stride;
       if (r < nl) {
         // dual update with wbar_t (b when A X = b) and the next diagonal with w_{t+1}
-        const double e = zr[u] - (A.ineq ? fmin(fmax(zr[u] + yv[u] / A.beta_next, A.lo), A.hi) : A.b);
+        const double e = zr[u] - (BOX ? fmin(fmax(zr[u] + yv[u] / A.beta_next, A.lo), A.hi) : A.b);
         const double yr = fma(gam, e, yv[u]);
         y[r] = yr;
-        const double e1 = A.ineq ? zr[u] - fmin(fmax(zr[u] + yr / A.beta_next, A.lo), A.hi) : e;
+        const double e1 = BOX ? zr[u] - fmin(fmax(zr[u] + yr / A.beta_next, A.lo), A.hi) : e;
         d[r] = fma(A.beta_next, e1, yr) + cd[u];
         const double gv = scg_lanczos_start(seed, A.t + 1, rb + og[u]);
         gstore_m(net, g + rb + r, mk[u], gv);

@@ -577,13 +577,13 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_a<true>, kBlock, 0);
   s->grid_rows = grid_for(nl, std::max(1, occ) * c->nsm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_primal, kBlock, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_primal<false>, kBlock, 0);
   s->grid_primal = grid_for(nl, std::max(1, occ) * c->nsm);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_b, kBlock, 0);
   s->grid_b = grid_for(nl, std::max(1, occ) * c->nsm);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_combine, kBlock, 0);
   s->grid_comb = grid_for(nl, std::max(1, occ) * c->nsm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dual_sketch, kBlock, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dual_sketch<false>, kBlock, 0);
   s->grid_dual = grid_for(nl, std::max(1, occ) * c->nsm);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_norm_x, kBlock, 0);
   s->grid_norm = grid_for(nl, std::max(1, occ) * c->nsm);
@@ -1488,7 +1488,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     pull_all(c, FK_MON, 3, E, FinArgs{});
     E = ++c->epoch;
     for (Shard *s : c->sh)
-      launch(c, KC_PRIMAL, s->kb[KC_PRIMAL], k_primal, dim3(s->grid_primal), dim3(kBlock), (const double *)c->vslot(s, js), s->z,
+      launch(c, KC_PRIMAL, s->kb[KC_PRIMAL], c->box ? k_primal<true> : k_primal<false>, dim3(s->grid_primal), dim3(kBlock), (const double *)c->vslot(s, js), s->z,
              (const double *)s->y, (const double *)s->Om, (int)s->nl, c->R, A, s->gpart, s->slots + SLOT_NZ, s->sc, s->dlog, net_of(c, s, E));
     {
       FinArgs f{};
@@ -1498,7 +1498,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     }
     E = ++c->epoch;
     for (Shard *s : c->sh)
-      launch(c, KC_DUAL_SKETCH, s->kb[KC_DUAL_SKETCH], k_dual_sketch, dim3(s->grid_dual), dim3(kBlock),
+      launch(c, KC_DUAL_SKETCH, s->kb[KC_DUAL_SKETCH], c->box ? k_dual_sketch<true> : k_dual_sketch<false>, dim3(s->grid_dual), dim3(kBlock),
              (const double *)s->z, s->y, s->d, (const double *)s->cdiag, s->ckr, js, c->wslot(s, 0),
              (int)s->nl, (long long)s->rb, c->R, A, c->seed, s->slots + SLOT_NU0, s->sc, net_of(c, s, E),
              (const int *)s->orig);
