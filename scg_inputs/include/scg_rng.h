@@ -159,27 +159,35 @@ SCG_RNG_FN double scg_sin_small(double th) {
   return SCG_FMA(p * t2, th, th);
 }
 
-/* cos(2 pi u) for u in [0, 1): quadrant reduction is exact (4u exact). */
+/* cos(2 pi u) for u in [0, 1): quadrant reduction is exact (4u exact).  With f the
+ * fraction within the quadrant and th = (pi/2) f (f <= 1/2) or (pi/2)(1 - f) (f > 1/2), the
+ * value is +-cos_small(th) or +-sin_small(th); only that one polynomial is evaluated, with its
+ * coefficients selected per call (so a GPU warp runs one polynomial whatever its lanes need).
+ * The sine's leading step fma(0, t2, s0) = s0 is exact, so both are the operations of
+ * scg_cos_small / scg_sin_small above, bit for bit. */
 SCG_RNG_FN double scg_cos_2pi(double u) {
   double x = 4.0 * u;
-  int q = (int)x;  /* 0..3 */
+  int q = (int)x;           /* 0..3 */
   double f = x - (double)q; /* exact, in [0,1) */
-  double c, s; /* cos(pi/2 f), sin(pi/2 f) */
-  if (f <= 0.5) {
-    double th = 0x1.921fb54442d18p+0 * f;
-    c = scg_cos_small(th);
-    s = scg_sin_small(th);
-  } else {
-    double th = 0x1.921fb54442d18p+0 * (1.0 - f);
-    c = scg_sin_small(th);
-    s = scg_cos_small(th);
-  }
-  switch (q) {
-    case 0: return c;
-    case 1: return -s;
-    case 2: return -c;
-    default: return s;
-  }
+  const int hi = f > 0.5;
+  const double th = 0x1.921fb54442d18p+0 * (hi ? (1.0 - f) : f);
+  /* q even needs cos(pi/2 f), q odd sin(pi/2 f); above 1/2 the two swap */
+  const int use_cos = ((q & 1) == 0) != hi;
+  const double t2 = th * th;
+  double p = use_cos ? 0x1.e542ba4020225p-62 : 0.0;
+  p = SCG_FMA(p, t2, use_cos ? -0x1.6827863b97d97p-53 : 0x1.71b8ef6dcf572p-66);
+  p = SCG_FMA(p, t2, use_cos ? 0x1.ae7f3e733b81fp-45 : -0x1.2f49b46814157p-57);
+  p = SCG_FMA(p, t2, use_cos ? -0x1.93974a8c07c9dp-37 : 0x1.952c77030ad4ap-49);
+  p = SCG_FMA(p, t2, use_cos ? 0x1.1eed8eff8d898p-29 : -0x1.ae7f3e733b81fp-41);
+  p = SCG_FMA(p, t2, use_cos ? -0x1.27e4fb7789f5cp-22 : 0x1.6124613a86d09p-33);
+  p = SCG_FMA(p, t2, use_cos ? 0x1.a01a01a01a01ap-16 : -0x1.ae64567f544e4p-26);
+  p = SCG_FMA(p, t2, use_cos ? -0x1.6c16c16c16c17p-10 : 0x1.71de3a556c734p-19);
+  p = SCG_FMA(p, t2, use_cos ? 0x1.5555555555555p-5 : -0x1.a01a01a01a01ap-13);
+  p = SCG_FMA(p, t2, use_cos ? -0x1.0000000000000p-1 : 0x1.1111111111111p-7);
+  /* the sine has one coefficient less: its last step here is its -1/6 */
+  const double v = use_cos ? SCG_FMA(p, t2, 1.0)
+                           : SCG_FMA(SCG_FMA(p, t2, -0x1.5555555555555p-3) * t2, th, th);
+  return (q == 1 || q == 2) ? -v : v;
 }
 
 /* One standard normal per counter (Box-Muller, cosine branch). */
