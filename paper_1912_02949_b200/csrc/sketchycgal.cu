@@ -37,6 +37,29 @@ using namespace scg_host;
 
 namespace {
 
+// Host vectors of the init passes without value-initialization: the first touch (and its page
+// faults) happens in the parallel fill loops instead of a serial zeroing pass.
+template <class T>
+struct noinit_alloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = noinit_alloc<U>;
+  };
+  noinit_alloc() = default;
+  template <class U>
+  noinit_alloc(const noinit_alloc<U> &) noexcept {}
+  template <class U>
+  void construct(U *p) noexcept {
+    ::new ((void *)p) U;
+  }
+  template <class U, class... A>
+  void construct(U *p, A &&...a) {
+    ::new ((void *)p) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using hvec = std::vector<T, noinit_alloc<T>>;
+
 enum KClass {
   KC_LANCZOS_A = 0, KC_LANCZOS_B, KC_TRIDIAG, KC_LANCZOS_C, KC_NORM_X, KC_COMBINE, KC_MONITOR, KC_PRIMAL,
   KC_DUAL_SKETCH, KC_SKETCH, KC_PULL, KC_OTHER, KC_PASS1, KC_COUNT
@@ -93,8 +116,8 @@ struct Shard {
   // row relabeling (SELL engine): local row nu holds input row rb + origloc[nu]
   std::vector<int> origloc;
   int *orig = nullptr;            // device copy of origloc
-  std::vector<int> h_rp, h_col;   // host CSR (device labels) kept from build_shard to build_layout
-  std::vector<double> h_w;
+  hvec<int> h_rp, h_col;   // host CSR (device labels) kept from build_shard to build_layout
+  hvec<double> h_w;
   // sharding
   unsigned char *mask = nullptr;  // device [nl], nullptr when world == 1
   Mailbox *mb = nullptr;
@@ -483,16 +506,28 @@ bool csr_symmetric(const int64_t *rp, const int32_t *col, int64_t n) {
 // weights w = -L_rj and the diagonal, the long-row list, the SELL-32-sigma layout of
 // the short rows and the halo mask; then allocate and upload.  rp/colp/valp point at
 // this shard's rows (rp[0] may be nonzero).
+// SCG_DEBUG: split timings of the host init stages
+void dbg_split(const char *what) {
+  static const bool on = std::getenv("SCG_DEBUG") != nullptr;
+  static auto t0 = std::chrono::steady_clock::now();
+  if (!on) return;
+  const auto t1 = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[scg]   %-22s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+  t0 = t1;
+}
+
 scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *colp, const double *valp,
                        int has_diagonal) {
+  dbg_split("shard: start");
   const int64_t nl = s->nl, rb = s->rb;
   const int R = c->R;
   const int64_t base = rp[0];
   // device row nu is input row r = origloc[nu]; its entries stay in the input (ascending
   // input column) order -- the CAC-3 chain order -- with columns relabeled by gmap.
   // Two parallel passes: count off-diagonal entries per row, then fill.
-  std::vector<int> &h_rp = s->h_rp;
-  h_rp.assign((size_t)nl + 1, 0);
+  hvec<int> &h_rp = s->h_rp;
+  h_rp.resize((size_t)nl + 1);  // entry nu + 1 written by the count pass below
+  h_rp[0] = 0;
 #pragma omp parallel for schedule(static, 4096)
   for (int64_t nu = 0; nu < nl; ++nu) {
     const int64_t r = s->origloc[(size_t)nu];
@@ -500,17 +535,18 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
     for (int64_t k = rp[r]; k < rp[r + 1]; ++k) cnt += colp[k - base] != r + rb;
     h_rp[(size_t)nu + 1] = cnt;
   }
+  dbg_split("shard: count");
   int64_t cnt_off = 0;
   for (int64_t nu = 0; nu < nl; ++nu) {
     cnt_off += h_rp[(size_t)nu + 1];
     if (cnt_off >= (1ll << 31)) return fail(c, SCG_EINVAL, "too many nonzeros for int32 row pointers");
     h_rp[(size_t)nu + 1] = (int)cnt_off;
   }
-  std::vector<int> &h_col = s->h_col;
-  std::vector<double> &h_w = s->h_w;
+  hvec<int> &h_col = s->h_col;
+  hvec<double> &h_w = s->h_w;
   h_col.resize((size_t)cnt_off);
   h_w.resize((size_t)cnt_off);
-  std::vector<double> h_diag((size_t)nl, 0.0);
+  hvec<double> h_diag((size_t)nl);  // every entry is written by the fill pass
   std::vector<unsigned char> h_mask;
   if (c->world > 1) h_mask.assign((size_t)nl, 0);
   long long halo = 0;
@@ -543,6 +579,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
       halo += m != 0;
     }
   }
+  dbg_split("shard: fill");
   s->halo_rows = halo;
   s->nnz_off = cnt_off;
   std::vector<int> h_long;
@@ -572,6 +609,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
             alloc((void **)&s->gflag, sizeof(unsigned long long));
   if (!ok) return fail(c, SCG_ENOMEM, "device allocation");
   if (c->world > 1 && !alloc((void **)&s->mask, (size_t)nl)) return fail(c, SCG_ENOMEM, "halo mask");
+  dbg_split("shard: long rows+malloc");
 
   // grid sizes from occupancy
   int occ = 1;
@@ -613,6 +651,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   CK(cudaMemsetAsync(s->y, 0, nlb, st));
   CK(cudaMemsetAsync(s->S, 0, nlb * R, st));
   CK(cudaStreamSynchronize(st));  // host vectors go out of scope (the SELL layout follows in build_sell)
+  dbg_split("shard: grids+H2D+memsets");
   return SCG_OK;
 }
 
@@ -622,8 +661,8 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
 scg_status build_layout(scg_ctx *c, Shard *s) {
   const int64_t nl = s->nl;
   const bool scale = (c->flags & SCG_SCALE) != 0;
-  const std::vector<int> &h_rp = s->h_rp, &h_col = s->h_col;
-  const std::vector<double> &h_w = s->h_w;
+  const hvec<int> &h_rp = s->h_rp, &h_col = s->h_col;
+  const hvec<double> &h_w = s->h_w;
   cudaStream_t st = c->stream;
   const long long cnt_off = s->nnz_off;
   const double w0 = cnt_off > 0 ? std::fabs(h_w[0]) : 0.0;
@@ -736,9 +775,9 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
     // rows are already sorted by length within windows of kSigma rows (relabel_perm), so a
     // slice is 32 consecutive rows; leading long rows (warp engine) are skipped lanes
     const int64_t nsl = (nl + 31) / 32;
-    std::vector<int> scol;
+    hvec<int> scol;  // every slot is written by the fill pass (padding included)
     std::vector<int2> meta;
-    std::vector<double> sval;
+    hvec<double> sval;
     // engine 2 (SELL-W): entries coded relative to their chunk's window / out list
     std::vector<int> tout, cout;
     const int64_t n = c->n, rb = s->rb;
@@ -786,20 +825,24 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
     // negative coefficient: fma(-m, +0, acc) == acc exactly for every acc (also +-0), so the
     // kernel needs no per-slot padding test.  Other engines keep -1.
     const int padc = SCG_ENGINE == 0 ? (uni ? (int)((unsigned)c->n | 0x80000000u) : (int)c->n) : -1;
-    scol.assign(slots, padc);
-    if (!uni) sval.assign(slots, -0.0);
-    // pass 2: fill the slots (parallel; serial for engine 2, whose out lists grow per chunk)
+    scol.resize(slots);
+    if (!uni) sval.resize(slots);
+    // pass 2: fill every slot, padding included (parallel; serial for engine 2, whose out
+    // lists grow per chunk)
     auto fill = [&](int64_t q) {
       const int width = swid[(size_t)q], nskip = sskip[(size_t)q];
       const size_t b0 = (size_t)meta[(size_t)q].x;
       for (int j = 0; j < width; ++j)
-        for (int l = nskip; l < 32; ++l) {
+        for (int l = 0; l < 32; ++l) {
           const int64_t r = q * 32 + l;
-          if (r >= nl) break;
-          const int e = h_rp[(size_t)r] + j;
-          if (e < h_rp[(size_t)r + 1]) {
-            scol[b0 + (size_t)j * 32 + l] = code_of(e);
-            if (!uni) sval[b0 + (size_t)j * 32 + l] = valof(e);
+          const size_t slot = b0 + (size_t)j * 32 + l;
+          const int e = (l >= nskip && r < nl) ? h_rp[(size_t)r] + j : -1;
+          if (e >= 0 && e < h_rp[(size_t)r + 1]) {
+            scol[slot] = code_of(e);
+            if (!uni) sval[slot] = valof(e);
+          } else {
+            scol[slot] = padc;
+            if (!uni) sval[slot] = -0.0;
           }
         }
     };
@@ -921,8 +964,8 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
   s->kb[KC_MONITOR] = mat + 16.0 * NL + 8.0 * gath + 8.0 * NL;
   s->kb[KC_PRIMAL] = 24.0 * NL + 8.0 * NL * c->R;
   s->kb[KC_DUAL_SKETCH] = 60.0 * NL;  // z, y, cdiag, orig read; y, d, g written
-  std::vector<int>().swap(s->h_col);  // host copies no longer needed
-  std::vector<double>().swap(s->h_w);
+  hvec<int>().swap(s->h_col);  // host copies no longer needed
+  hvec<double>().swap(s->h_w);
   return SCG_OK;
 }
 
