@@ -417,9 +417,28 @@ void free_shard(Shard *s) {
 // order (ascending INPUT column) and every exact sum are unchanged, so results are
 // bitwise those of the input labeling; the seeded streams and all outputs use input ids.
 constexpr int64_t kSortWin = 256;
-void relabel_perm(const int64_t *rp, int64_t nl, std::vector<int> &origloc) {
+void relabel_perm(const int64_t *rp, const int32_t *colp, int64_t nl, int64_t rb, bool halo_first,
+                  std::vector<int> &origloc) {
   origloc.resize((size_t)nl);
   for (int64_t r = 0; r < nl; ++r) origloc[(size_t)r] = (int)r;
+  if (halo_first) {
+    // sharded: the rows other ranks read (a column outside this shard; L is symmetric) first,
+    // in input order, then the interior rows -- so that only the first blocks of the kernels
+    // producing gathered vectors store into peer memory and need the system-scope fence
+    // (commit_and_ticket's peer flag).  A symmetric permutation: results are bitwise unchanged.
+    const int64_t base = rp[0];
+    std::vector<unsigned char> halo((size_t)nl, 0);
+#pragma omp parallel for schedule(static, 4096)
+    for (int64_t r = 0; r < nl; ++r)
+      for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+        const int64_t cc = colp[k - base];
+        if (cc < rb || cc >= rb + nl) {
+          halo[(size_t)r] = 1;
+          break;
+        }
+      }
+    std::stable_partition(origloc.begin(), origloc.end(), [&](int r) { return halo[(size_t)r] != 0; });
+  }
 #if SCG_ENGINE != 1
 #pragma omp parallel for schedule(static, 64)
   for (int64_t w = 0; w < nl; w += kSortWin) {
@@ -1290,7 +1309,9 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
     s->rb = c->splits[(size_t)s->rank];
     s->nl = c->splits[(size_t)s->rank + 1] - s->rb;
     const int64_t off = c->mode == 2 ? 0 : s->rb;  // index of this shard's first row in L->row_ptr
-    relabel_perm(L->row_ptr + off, s->nl, s->origloc);
+    relabel_perm(L->row_ptr + off, L->col_idx + L->row_ptr[off], s->nl, s->rb,
+                 world > 1 && !(std::getenv("SCG_HALO_FIRST") && std::getenv("SCG_HALO_FIRST")[0] == '0'),
+                 s->origloc);
   }
   tick("device+relabel");
   if ((st = build_gmap(c))) return bad(st);
