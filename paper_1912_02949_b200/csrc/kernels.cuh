@@ -1279,6 +1279,11 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
 __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// A strong relaxed store: after a fence.sc.sys it completes a release pattern without the
+// per-store membar st.release.sys carries (one fence for all P flags instead of P + 1).
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -1331,8 +1336,14 @@ __device__ __forceinline__ void emit(XSlot *slot, DevScalars *sc, const Net &net
       for (int i = 0; i < kLimbs; ++i) m->limbs[e][net.me][s][i] = L[s][i];
     for (int k = 0; k < nf; ++k) m->fv[e][net.me][k] = gk[k];
   }
-  __threadfence_system();
-  for (int q = 0; q < net.P; ++q) st_release_sys(&net.peerMB[q]->flag[e][net.me], net.E);
+  __threadfence_system();  // releases the limbs above (and, cumulatively, the halo stores) ...
+  for (int q = 0; q < net.P; ++q) st_relaxed_sys(&net.peerMB[q]->flag[e][net.me], net.E);  // ... with these flags
+#if SCG_TAILPROF
+  sc->dbg_ns[kind] += gtimer() - t0;
+  if ((++sc->dbg_cnt[kind] & 511) == 0)
+    printf("[tail P>1] kind %d: %llu launches, mean emit %.2f us\n", kind, sc->dbg_cnt[kind],
+           1e-3 * (double)sc->dbg_ns[kind] / (double)sc->dbg_cnt[kind]);
+#endif
 }
 
 // P > 1: wait for every rank's contribution to collective net.E, add, finalize.
