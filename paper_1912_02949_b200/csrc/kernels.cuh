@@ -1351,38 +1351,56 @@ __device__ __forceinline__ void emit(XSlot *slot, DevScalars *sc, const Net &net
 // instead of hanging the GPU.
 __global__ void k_pull(int kind, int ns, Net net, DevScalars *sc, FinArgs f) {
   pdl_entry();
-  if (threadIdx.x != 0) return;
+  // one warp: lane p waits for rank p's flag, the limb sums are spread over the lanes (exact
+  // integer adds in any order), lane 0 gathers them and finalizes
+  const int lane = threadIdx.x;
   if (sc->err & 2) return;  // an earlier collective timed out: fail fast (reported by synchronize)
   if ((kind == FK_OM || kind == FK_RHO) && sc->brk) return;  // producer skipped (Lanczos break)
   if (kind == FK_BAR && f.i >= sc->k) return;
   const int e = (int)(net.E & 3ull);
   Mailbox *m = net.mb;
-  const long long t0 = clock64();
-  for (int p = 0; p < net.P; ++p) {
-    while (ld_acquire_sys(&m->flag[e][p]) != net.E) {
+  int ok = 1;
+  if (lane < net.P) {
+    const long long t0 = clock64();
+    while (ld_acquire_sys(&m->flag[e][lane]) != net.E) {
       if (clock64() - t0 > (1ll << 34)) {
-        atomicOr(&sc->err, 2);
-        return;
+        ok = 0;
+        break;
       }
       __nanosleep(32);
     }
   }
+  if (!__all_sync(0xffffffffu, ok)) {
+    if (lane == 0) atomicOr(&sc->err, 2);
+    return;
+  }
+  __syncwarp();  // every flag acquired by some lane precedes lane 0's reads below
+  long long part[2] = {0, 0};  // entries lane and lane + 32 of the ns x kLimbs sums
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int idx = lane + 32 * h;
+    if (idx < ns * kLimbs)
+      for (int p = 0; p < net.P; ++p) part[h] += __ldcv(&m->limbs[e][p][idx / kLimbs][idx % kLimbs]);
+  }
+  double gpart[2] = {0.0, 0.0};  // g_k = sum over ranks in rank order, k = lane, lane + 32
+  if (kind == FK_NZ)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = lane + 32 * h;
+      if (k < f.R)
+        for (int p = 0; p < net.P; ++p) gpart[h] += __ldcv(&m->fv[e][p][k]);
+    }
   long long L[kMaxSums][kLimbs];
   double gk[kMaxR];
-  for (int s = 0; s < kMaxSums; ++s)
-    for (int i = 0; i < kLimbs; ++i) {
-      long long acc = 0;
-      if (s < ns)
-        for (int p = 0; p < net.P; ++p) acc += __ldcv(&m->limbs[e][p][s][i]);
-      L[s][i] = acc;
-    }
-  if (kind == FK_NZ)
-    for (int k = 0; k < f.R; ++k) {
-      double t = 0.0;
-      for (int p = 0; p < net.P; ++p) t += __ldcv(&m->fv[e][p][k]);
-      gk[k] = t;
-    }
-  finalize(kind, sc, L, gk, f);
+  for (int idx = 0; idx < kMaxSums * kLimbs; ++idx) {
+    const long long v = __shfl_sync(0xffffffffu, part[idx >> 5], idx & 31);
+    if (lane == 0) L[idx / kLimbs][idx % kLimbs] = idx < ns * kLimbs ? v : 0ll;
+  }
+  for (int k = 0; k < kMaxR && k < 64; ++k) {
+    const double v = __shfl_sync(0xffffffffu, gpart[k >> 5], k & 31);
+    if (lane == 0) gk[k] = v;
+  }
+  if (lane == 0) finalize(kind, sc, L, gk, f);
 }
 
 // ---------------------------------------------------------------- init kernels
