@@ -88,14 +88,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def _ncu_traffic(kernel_name: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary, if any."""
+def _ncu_traffic(kernel_name: str, cfg: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary of the SAME
+    workload (profiles/ncu_full_summary.json "workload" must equal --config), else None."""
     path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
     try:
         with open(path) as f:
             js = json.load(f)
         ent = js.get("kernels", {}).get(kernel_name)
-        if ent and js.get("workload") == "c3":
+        if ent and js.get("workload") == cfg:
             return float(ent["dram_bytes"])
     except Exception:
         pass
@@ -211,7 +212,7 @@ def run_ours(args, rank, world, local_rank):
         return s["bytes_per_launch"] * s["launches"] / (s["total_ms"] / 1e3) / 1e9 if s["total_ms"] > 0 else 0.0
 
     achieved = gbs(top)
-    traffic = _ncu_traffic(top["name"])
+    traffic = _ncu_traffic(top["name"], args.config)
     matvecs = float(np.sum(lg[:, 2] + (lg[:, 2] - 1) + 1))
     spmv = [s for s in ks if s["name"].startswith(("lanczos_a", "lanczos_pass1"))][0]
     kernels = {s["name"]: {"launches": s["launches"], "avg_us": 1e3 * s["total_ms"] / s["launches"],

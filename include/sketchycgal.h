@@ -72,7 +72,15 @@ enum {
   SCG_INEQ = 1u << 4,           /* general template with K = {u <= b}: diag X <= 1
                                    instead of diag X = 1; b is replaced by the slack w = min(z + y/beta, b) in D_t
                                    and in the dual update (reading R32); the gap / bound records are NaN */
-  SCG_PROFILE = 1u << 8         /* record CUDA events around every kernel launch (bench / kernel stats) */
+  SCG_PROFILE = 1u << 8,        /* record CUDA events around every 16th launch of each kernel class (bench /
+                                   kernel stats) */
+  /* execution options: none changes a single bit of the results (every variant is checked bitwise
+     against the oracle by tests/test_gpu_parity.py); the defaults are the fastest measured on B200 */
+  SCG_NO_PDL = 1u << 9,         /* launch without programmatic dependent launch (default: PDL on) */
+  SCG_FUSED_PASS1 = 1u << 10,   /* one GPU: all q steps of Lanczos pass 1 in one persistent cooperative kernel */
+  SCG_WS_SPMV = 1u << 11,       /* uniform weights: warp-specialized TMA SpMV (producer warp + mbarrier ring) */
+  SCG_TMA_B = 1u << 12,         /* TMA-staged recurrence kernel (bulk copies into shared memory) */
+  SCG_DEBUG_LOG = 1u << 13      /* host init stage timings and layout facts on stderr */
 };
 
 /* This rank's rows [row_begin, row_end) of the symmetric weighted Laplacian
@@ -140,7 +148,7 @@ typedef struct {
   char name[32];
   int64_t launches;
   double total_ms;          /* CUDA-event time on the context stream: every 16th launch of the class is
-                               timed (env SCG_PROF_EVERY), the sum extrapolated to all launches */
+                               timed, the sum extrapolated to all launches */
   double bytes_per_launch;  /* algorithmic HBM bytes of one launch */
 } scg_kstat;
 

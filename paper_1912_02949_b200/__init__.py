@@ -28,6 +28,11 @@ SCG_REGENERATE = 1 << 2
 SCG_TRACE_LE = 1 << 3
 SCG_INEQ = 1 << 4
 SCG_PROFILE = 1 << 8
+SCG_NO_PDL = 1 << 9
+SCG_FUSED_PASS1 = 1 << 10
+SCG_WS_SPMV = 1 << 11
+SCG_TMA_B = 1 << 12
+SCG_DEBUG_LOG = 1 << 13
 
 STATUS = {0: "SCG_OK", -1: "SCG_EINVAL", -2: "SCG_ENOMEM", -3: "SCG_ECUDA", -4: "SCG_ENCCL", -5: "SCG_ECHOL",
           -6: "SCG_ESTATE", -7: "SCG_ERANGE", -8: "SCG_EUNSUPPORTED"}
@@ -213,13 +218,18 @@ class SketchyCGAL:
     Multi-process (one process per GPU): pass ``rank``, ``world``, ``splits`` (world+1
     row offsets) and ``nccl_id`` (the 128 bytes of ``nccl_unique_id()`` from rank 0);
     ``L`` may be the full CSR, the rank's rows are taken from it.
+
+    Execution options (bitwise-neutral): ``pdl`` (programmatic dependent
+    launches, default on), ``fused_pass1`` (persistent pass-1 kernel), ``ws_spmv``
+    (warp-specialized TMA SpMV), ``tma_b`` (TMA-staged recurrence kernel), ``debug_log``.
     """
 
     def __init__(self, L, R: int, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
                  scale: bool = True, trace_correct: bool = True, profile: bool = False, device: int = 0,
                  stream=None, regenerate: bool = False, trace_le: bool = False, shards: int = 1, splits=None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None, ineq: bool = False,
-                 box: tuple | None = None):
+                 box: tuple | None = None, pdl: bool = True, fused_pass1: bool = False, ws_spmv: bool = False,
+                 tma_b: bool = False, debug_log: bool = False):
         self.lib = load()
         self.n = int(L.n)
         self.R = int(R)
@@ -248,7 +258,9 @@ class SketchyCGAL:
         csr = Csr(self.n, self.row_begin, self.row_end, rp.ctypes.data, col.ctypes.data, val.ctypes.data, 1)
         flags = (SCG_SCALE if scale else 0) | (SCG_TRACE_CORRECT if trace_correct else 0) | \
                 (SCG_PROFILE if profile else 0) | (SCG_REGENERATE if regenerate else 0) | \
-                (SCG_TRACE_LE if trace_le else 0) | (SCG_INEQ if ineq else 0)
+                (SCG_TRACE_LE if trace_le else 0) | (SCG_INEQ if ineq else 0) | (0 if pdl else SCG_NO_PDL) | \
+                (SCG_FUSED_PASS1 if fused_pass1 else 0) | (SCG_WS_SPMV if ws_spmv else 0) | \
+                (SCG_TMA_B if tma_b else 0) | (SCG_DEBUG_LOG if debug_log else 0)
         self._h = ctypes.c_void_p()
         dptr = None
         if dist is not None:

@@ -23,15 +23,9 @@ namespace scg {
 constexpr int kMaxQ = 128;   // Lanczos bound cap (max q_t in configs[0..4] is 94)
 constexpr int kMaxR = 64;    // sketch rank cap (BASELINE: R <= 50)
 constexpr int kBlock = 256;
-#ifndef SCG_BLOCK_A
-#define SCG_BLOCK_A 256
-#endif
-constexpr int kBlockA = SCG_BLOCK_A;  // threads per block of k_lanczos_a (the SpMV of pass 1)
+constexpr int kBlockA = 256;  // threads per block of k_lanczos_a (the SpMV of pass 1)
 
 // Device-resident scalars of the current iteration.
-#ifndef SCG_TAILPROF
-#define SCG_TAILPROF 0  // 1: time the last block's emit (globaltimer), printed every 512 launches per kind
-#endif
 struct DevScalars {
   double om[kMaxQ];        // omega_i, i = 1..k  (om[i-1])
   double rho[kMaxQ + 1];   // rho[0] = ||g|| (start-vector norm), rho[i] = rho_i  (Alg. 2 line 7)
@@ -40,9 +34,6 @@ struct DevScalars {
   double theta, nu_x, xi, c, vv, nz, gamma, p, tau;
   double my[4];            // sums over the state (y_t, z_t) of the NEXT iteration: y, y.z, z.z, z (k_dual_sketch)
   int k, brk, err, pad;
-#if SCG_TAILPROF
-  unsigned long long dbg_ns[16], dbg_cnt[16];
-#endif
 };
 
 // Exact-sum slot: up to 3 accumulators + a block ticket counter.
@@ -66,20 +57,10 @@ struct Csr {
 // next launch overlaps the tail (ticket, finalize) without the dependent grid's blocks
 // holding SM slots during the main work.  All data dependences are honored by the wait.
 // (No-ops when launched without the attribute.)
-#ifndef SCG_PDL_LATE
-#define SCG_PDL_LATE 1  // kernels with exact sums let the next grid launch only at their block commit
-#endif                  // (0: right after the wait -- measured 17% slower on c3)
-__device__ __forceinline__ void pdl_entry() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#if !SCG_PDL_LATE
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
-}
-__device__ __forceinline__ void pdl_trigger() {
-#if SCG_PDL_LATE
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
-}
+// (Triggering right after the wait instead was measured 17% slower on configs[3]: the dependent
+// grid's blocks then hold SM slots during the whole main loop.)
+__device__ __forceinline__ void pdl_entry() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Host-computed scalars of iteration t (CAC-6).
 struct IterArgs {
@@ -126,17 +107,10 @@ struct Net {
   unsigned long long E;       // epoch of the collective this launch takes part in
 };
 
-#ifndef SCG_STCS
-#define SCG_STCS 0  // 1: evict-first (st.global.cs) stores of the Lanczos outputs
-#endif
 // Store v at dst (this rank's gathered region) and into the reader ranks' copies given the
 // row's reader mask m (loaded by the caller together with the row's data).
 __device__ __forceinline__ void gstore_m(const Net &net, double *dst, unsigned m, double v) {
-#if SCG_STCS
-  __stcs(dst, v);
-#else
   *dst = v;
-#endif
   if (m) {
     const long long off = dst - net.G;
     while (m) {
@@ -151,11 +125,7 @@ __device__ __forceinline__ unsigned gmask(const Net &net, int r) { return net.ma
 
 // Store v at dst (this rank's gathered region, own row r) and into every reader rank's copy.
 __device__ __forceinline__ void gstore(const Net &net, double *dst, int r, double v) {
-#if SCG_STCS
-  __stcs(dst, v);
-#else
   *dst = v;
-#endif
   if (net.mask) {
     unsigned m = net.mask[r];
     if (m) {
@@ -194,66 +164,33 @@ __device__ __forceinline__ double div_rn(double a, double b, double rb) {
 }
 
 // ---------------------------------------------------------------- row engine
-// Rows with at most kLongRow off-diagonal entries are "short": one thread owns a
-// row and runs its sequential CAC-3 chain, loading kChunk entries (col, val, then
-// the gathered x[col]) at a time with all loads of a chunk in flight, and two rows
-// per thread in flight (memory-level parallelism for the HBM-bound SpMV).  Longer
-// rows are "long": a warp loads 32 entries per round (coalesced) and lane 0 runs
-// the chain; long rows are listed at init (longest first) and taken by the first
-// warps of the grid so they start early.
-#ifndef SCG_RPT
-#define SCG_RPT 1
-#endif
-#ifndef SCG_CH
-#define SCG_CH 4
-#endif
-#ifndef SCG_ENGINE
-#define SCG_ENGINE 0  // short-row SpMV engine: 0 = SELL-32-sigma register pipeline, 1 = window/tile-staged CSR (TMA)
-#endif
-#ifndef SCG_PIPE
-#define SCG_PIPE 3  // 3: width-specialized 3-stage pipeline (default), 2: width-specialized 2-stage,
-                    // 1: predicated 3-stage, 0: unpipelined
-#endif
-#ifndef SCG_MINB
-#define SCG_MINB 3  // min blocks per SM of the uniform-weight SpMV kernels (register cap 80)
-#endif
+// Rows with at most kLongRow off-diagonal entries are "short": they live in a SELL-32-sigma
+// layout (slices of 32 consecutive relabeled rows, one lane per row) walked by a
+// three-stage register pipeline (spmv_rows).  Longer rows are "long": a warp loads 32
+// entries per round (coalesced) and the lanes run the strided partial chains of reading
+// R27; long rows are listed at init (longest first) and taken by the first warps of the
+// grid so they start early.
+constexpr int kMinBlocksUni = 3;  // min blocks per SM of the uniform-weight SpMV kernels (80-register cap)
 constexpr int kLongRow = 32;
-constexpr int kChunk = SCG_CH;   // entries of a row loaded per round
-constexpr int kRpt = SCG_RPT;    // rows per thread in flight
 
 struct Rows {
   const int *longrows;  // local ids of long rows
   int nlong;
   // SELL-32-sigma layout of the short rows.  Rows are relabeled at init so that each
-  // window of kSigma rows is sorted by length (long rows first): slice s covers the 32
+  // window of kSortWin rows is sorted by length (long rows first): slice s covers the 32
   // consecutive rows 32 s .. 32 s + 31; slot j of lane l is at meta[s].x + 32 j + l;
   // meta[s].y = width | (number of leading long-row lanes, skipped) << 8.
-  const int *perm;      // unused (identity after relabeling)
   const int2 *meta;
-  const int *scol;      // column | 0x80000000 for a negative uniform value; -1 = padding
+  const int *scol;      // column | 0x80000000 for a negative uniform value; padding = dummy column n
   const double *sval;   // per-slot values, or nullptr when all |C_rj| equal m0
   double m0;
   int nslice;
-  // windows of kWin consecutive rows (the SELL sorting windows): window w holds
-  // slices [wstart[w], wstart[w+1])
-  const int *wstart;
-  int nwin;
-  // tile-staged CSR layout of the short rows (SCG_ENGINE 1): trp[r] = offset of row r's
-  // entries in tcol/tval, bit 31 of trp[r+1] set iff row r is long (no entries here)
-  const unsigned *trp;
-  const int *tcol;      // entry code (see the tile engine below)
-  const double *tval;   // values, or nullptr when all |C_rj| equal m0
-  const int *tout;      // out-of-window columns of every tile (engine 1) / chunk (engine 2)
-  const struct TileDesc *tdesc;
-  int ntiles;
-  const int *cout;      // engine 2: out list offsets per chunk
-  long long nglob;
   unsigned *work;       // non-null: dynamic slice distribution (chunks of kDynCh slices from this
                         // counter; zeroed again by the kernel's last block) -- skewed graphs
 };
 constexpr int kDynCh = 8;
 
-constexpr int kWin = 1024;  // rows per window (= SELL sorting window sigma)
+constexpr int kWin = 1024;  // vector padding granularity (rows)
 
 template <int NC>
 struct RowOut {
@@ -322,33 +259,6 @@ __device__ __forceinline__ void long_row_chain(const Csr &C, int r, const double
   if (NC > 1) o.s[NC - 1] = diag1[r] * o.xr + part[NC - 1];
 }
 
-template <bool UNI>
-__device__ __forceinline__ void sell_load_chunk(const Rows &RL, int2 mt, int j0, int lane, int (&cc)[kChunk],
-                                                double (&vv)[kChunk]) {
-#pragma unroll
-  for (int u = 0; u < kChunk; ++u) {
-    cc[u] = -1;
-    if (j0 + u < mt.y) {
-      const int e = mt.x + (j0 + u) * 32 + lane;
-      cc[u] = __ldg(&RL.scol[e]);
-      if (!UNI) vv[u] = __ldg(&RL.sval[e]);
-    }
-  }
-}
-
-template <int NC, bool UNI>
-__device__ __forceinline__ void sell_fma_chunk(const Rows &RL, const int (&cc)[kChunk], const double (&vv)[kChunk],
-                                               const double (&xg)[kChunk], double den, double rden,
-                                               RowOut<NC> &o) {
-#pragma unroll
-  for (int u = 0; u < kChunk; ++u)
-    if (cc[u] != -1) {
-      const double m = UNI ? (cc[u] < 0 ? -RL.m0 : RL.m0) : vv[u];
-      const double x = (xg[u]) * rden;  // v = w / rho (Alg. 2 line 9), formed on the fly
-#pragma unroll
-      for (int c = 0; c < NC; ++c) o.s[c] = fma(m, x, o.s[c]);
-    }
-}
 
 // ---------------------------------------------------------------- TMA / mbarrier / cp.async helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -396,7 +306,6 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
     if (lane == 0) epi(o);
   }
   const double rden = 1.0 / den;
-#if SCG_PIPE == 3
   {
   // Width-specialized three-stage pipeline: while slice i is computed, the gathers and
   // own entries of slice i+1, the columns of slice i+2 and the meta of slice i+3 are in
@@ -560,202 +469,10 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
   }  // while (chunks)
   return;
   }
-#endif
-#if SCG_PIPE == 2
-  if (NC == 1) {
-  // Width-specialized slices: each warp walks a contiguous range of slices; the meta and
-  // the first four column slots of the next slice are loaded while the current slice is
-  // computed; a warp-uniform switch on the slice width runs straight-line code (no
-  // predicated padding slots) for widths 0..4, a chunked loop above.
-  const int per = (RL.nslice + gridDim.x - 1) / gridDim.x;
-  const int ns = min(RL.nslice, (int)(blockIdx.x + 1) * per);
-  const int wstep = blockDim.x >> 5;
-  int sl = blockIdx.x * per + (threadIdx.x >> 5);
-  int2 mn = sl < ns ? __ldg(&RL.meta[sl]) : make_int2(0, 0);
-  int2 mn2 = sl + wstep < ns ? __ldg(&RL.meta[sl + wstep]) : make_int2(0, 0);  // meta two slices ahead
-  int cn0 = -1, cn1 = -1, cn2 = -1, cn3 = -1;
-  auto prefetch = [&](int2 m) {
-    const int w = m.y & 0xff;
-    const int *cp = RL.scol + m.x + lane;
-    cn0 = w > 0 ? __ldg(cp) : -1;
-    cn1 = w > 1 ? __ldg(cp + 32) : -1;
-    cn2 = w > 2 ? __ldg(cp + 64) : -1;
-    cn3 = w > 3 ? __ldg(cp + 96) : -1;
-  };
-  prefetch(mn);
-  for (; sl < ns; sl += wstep) {
-    const int2 m = mn;
-    const int c0 = cn0, c1 = cn1, c2 = cn2, c3 = cn3;
-    mn = mn2;
-    const int sn2 = sl + 2 * wstep;
-    mn2 = sn2 < ns ? __ldg(&RL.meta[sn2]) : make_int2(0, 0);
-    prefetch(mn);
-    const int w = m.y & 0xff;
-    const int p = sl * 32 + lane;
-    const bool ok = p < nl && lane >= (m.y >> 8);
-    double xo = 0.0, dd0 = 0.0, dd1 = 0.0;
-    if (ok) { xo = X[rb + p]; dd0 = diag0[p]; if (NC > 1) dd1 = diag1[p]; }
-    auto gat = [&](int c) -> double { return c != -1 ? __ldg(&X[c & 0x7fffffff]) : 0.0; };
-    auto val = [&](int c, int j) -> double {
-      return UNI ? (c < 0 ? -RL.m0 : RL.m0) : __ldg(&RL.sval[m.x + j * 32 + lane]);
-    };
-    RowOut<NC> o;
-    o.r = p;
-    auto step = [&](int c, double g, int j) {
-      if (c != -1) {
-        const double mm = val(c, j);
-        const double x = g * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
-#pragma unroll
-        for (int t = 0; t < NC; ++t) o.s[t] = fma(mm, x, o.s[t]);
-      }
-    };
-    auto init = [&]() {
-      o.xr = xo * rden;
-      o.s[0] = dd0 * o.xr;
-      if (NC > 1) o.s[NC - 1] = dd1 * o.xr;
-    };
-    switch (w) {
-      case 0: init(); break;
-      case 1: { const double g0 = gat(c0); init(); step(c0, g0, 0); } break;
-      case 2: { const double g0 = gat(c0), g1 = gat(c1); init(); step(c0, g0, 0); step(c1, g1, 1); } break;
-      case 3: {
-        const double g0 = gat(c0), g1 = gat(c1), g2 = gat(c2);
-        init(); step(c0, g0, 0); step(c1, g1, 1); step(c2, g2, 2);
-      } break;
-      case 4: {
-        const double g0 = gat(c0), g1 = gat(c1), g2 = gat(c2), g3 = gat(c3);
-        init(); step(c0, g0, 0); step(c1, g1, 1); step(c2, g2, 2); step(c3, g3, 3);
-      } break;
-      default: {
-        const double g0 = gat(c0), g1 = gat(c1), g2 = gat(c2), g3 = gat(c3);
-        init(); step(c0, g0, 0); step(c1, g1, 1); step(c2, g2, 2); step(c3, g3, 3);
-        for (int j0 = 4; j0 < w; j0 += 4) {
-          int cx[4];
-          double gx[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) cx[u] = j0 + u < w ? __ldg(&RL.scol[m.x + (j0 + u) * 32 + lane]) : -1;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) gx[u] = gat(cx[u]);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) step(cx[u], gx[u], j0 + u);
-        }
-      } break;
-    }
-    if (ok) epi(o);
-  }
-  return;
-  }
-#endif
-#if SCG_PIPE == 0
-  // SELL slices, one per warp step; latency hidden by occupancy (few registers)
-  for (int sl = gw; sl < RL.nslice; sl += nw) {
-    const int2 m0 = __ldg(&RL.meta[sl]);
-    const int p0 = sl * 32 + lane;
-    const bool ok = p0 < nl && lane >= (m0.y >> 8);
-    const int2 mw = make_int2(m0.x, m0.y & 0xff);
-    RowOut<NC> o;
-    o.r = p0;
-    double xo = 0.0, d0 = 0.0, d1 = 0.0;
-    if (ok) { xo = X[rb + p0]; d0 = diag0[p0]; if (NC > 1) d1 = diag1[p0]; }
-    o.xr = (xo) * rden;
-    o.s[0] = d0 * o.xr;
-    if (NC > 1) o.s[NC - 1] = d1 * o.xr;
-    for (int j0 = 0; j0 < mw.y; j0 += kChunk) {
-      int cx[kChunk];
-      double vx[kChunk], xx[kChunk];
-      sell_load_chunk<UNI>(RL, mw, j0, lane, cx, vx);
-#pragma unroll
-      for (int u = 0; u < kChunk; ++u)
-        if (cx[u] != -1) xx[u] = __ldg(&X[cx[u] & 0x7fffffff]);
-      sell_fma_chunk<NC, UNI>(RL, cx, vx, xx, den, rden, o);
-    }
-    if (ok) epi(o);
-  }
-#else
-  // SELL slices, software-pipelined three deep: in the step that computes slice i
-  // the gathers and own-row loads of slice i+1, the column loads of slice i+2 and
-  // the meta load of slice i+3 are issued, so a step never waits on a load issued
-  // in the same step.  Slice sl covers rows 32 sl + lane (consecutive: coalesced
-  // own-entry, diagonal and output accesses).
-  const int2 *__restrict__ meta = RL.meta;
-  // each block owns a contiguous range of slices (neighbouring rows share their
-  // gathered entries in the SM's L1); its warps interleave within the range
-  const int per = (RL.nslice + gridDim.x - 1) / gridDim.x;
-  const int ns = min(RL.nslice, (int)(blockIdx.x + 1) * per);
-  const int wstep = blockDim.x >> 5;
-  int sl = blockIdx.x * per + (threadIdx.x >> 5);
-  auto mload = [&](int q) -> int2 { return q < ns ? __ldg(&meta[q]) : make_int2(0, 0); };
-  auto width = [](int2 m) { return make_int2(m.x, m.y & 0xff); };
-  int2 m0 = mload(sl), m1 = mload(sl + wstep), m2 = mload(sl + 2 * wstep), m3 = mload(sl + 3 * wstep);
-  int c0[kChunk], c1[kChunk], c2[kChunk];
-  double v0[kChunk], v1[kChunk], v2[kChunk];
-  sell_load_chunk<UNI>(RL, width(m0), 0, lane, c0, v0);
-  sell_load_chunk<UNI>(RL, width(m1), 0, lane, c1, v1);
-  sell_load_chunk<UNI>(RL, width(m2), 0, lane, c2, v2);
-  double g0[kChunk], g1[kChunk];
-#pragma unroll
-  for (int u = 0; u < kChunk; ++u)
-    if (c0[u] != -1) g0[u] = __ldg(&X[c0[u] & 0x7fffffff]);
-  auto own = [&](int q, int2 m, double &xo, double &dd0, double &dd1) {
-    const int p = q * 32 + lane;
-    if (q < ns && p < nl && lane >= (m.y >> 8)) { xo = X[rb + p]; dd0 = diag0[p]; if (NC > 1) dd1 = diag1[p]; }
-  };
-  double xo0 = 0.0, d00 = 0.0, d10 = 0.0, xo1 = 0.0, d01 = 0.0, d11 = 0.0;
-  own(sl, m0, xo0, d00, d10);
-  while (sl < ns) {
-    // stage 1: gathers and own-row loads of slice i+1
-#pragma unroll
-    for (int u = 0; u < kChunk; ++u)
-      if (c1[u] != -1) g1[u] = __ldg(&X[c1[u] & 0x7fffffff]);
-    xo1 = 0.0; d01 = 0.0; d11 = 0.0;
-    own(sl + wstep, m1, xo1, d01, d11);
-    // stage 2: columns of slice i+3 (meta known), stage 3: meta of slice i+4
-    int c3[kChunk];
-    double v3[kChunk];
-    sell_load_chunk<UNI>(RL, width(m3), 0, lane, c3, v3);
-    const int2 m4 = mload(sl + 4 * wstep);
-    // stage 0: compute slice i
-    const int p0 = sl * 32 + lane;
-    const bool ok = p0 < nl && lane >= (m0.y >> 8);
-    RowOut<NC> o;
-    o.r = p0;
-    o.xr = (xo0) * rden;
-    o.s[0] = d00 * o.xr;
-    if (NC > 1) o.s[NC - 1] = d10 * o.xr;
-    sell_fma_chunk<NC, UNI>(RL, c0, v0, g0, den, rden, o);
-    const int2 mw = width(m0);
-    for (int j0 = kChunk; j0 < mw.y; j0 += kChunk) {  // rows longer than one chunk
-      int cx[kChunk];
-      double vx[kChunk], xx[kChunk];
-      sell_load_chunk<UNI>(RL, mw, j0, lane, cx, vx);
-#pragma unroll
-      for (int u = 0; u < kChunk; ++u)
-        if (cx[u] != -1) xx[u] = __ldg(&X[cx[u] & 0x7fffffff]);
-      sell_fma_chunk<NC, UNI>(RL, cx, vx, xx, den, rden, o);
-    }
-    if (ok) epi(o);
-    // rotate the pipeline
-    m0 = m1; m1 = m2; m2 = m3; m3 = m4;
-#pragma unroll
-    for (int u = 0; u < kChunk; ++u) {
-      c0[u] = c1[u]; c1[u] = c2[u]; c2[u] = c3[u];
-      v0[u] = v1[u]; v1[u] = v2[u]; v2[u] = v3[u];
-      g0[u] = g1[u];
-    }
-    xo0 = xo1; d00 = d01; d10 = d11;
-    sl += wstep;
-  }
-#endif
   (void)nl;
 }
 
 
-__device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // Elements [i0, i1) of a global array (element size ES) are copied as the 16-byte
 // aligned byte range around them; sdst then holds the array from the aligned element
@@ -773,339 +490,6 @@ __device__ __forceinline__ void bulk_seg(void *sdst, const void *gbase, long lon
 }
 template <int ES>
 __device__ __forceinline__ int seg_shift(long long i0) { return (int)(((i0 * ES) & 15ll) / ES); }
-
-// ---------------------------------------------------------------- tile-staged CSR engine (SCG_ENGINE 1)
-// The short rows are cut (on the host) into tiles of <= kTR consecutive rows.  Each
-// tile has an index WINDOW [wlo, whi) of the gathered vector that contains its own
-// rows and, for graphs with locality (Morton-ordered geometric graphs, tori, rings),
-// most of its columns.  Entry encoding (tcol): bit 31 = sign of a uniform value;
-// bit 30 clear: bits 0..29 = column - wlo (read from the staged window); bit 30 set:
-// bits 0..29 = index into the tile's out-of-window list (tout, absolute columns).
-// A block walks its tiles (k = blockIdx.x + j gridDim.x) through a kNS-stage
-// shared-memory pipeline, so in-flight loads cost no registers:
-//   stage S (tile j+kNS-1): one thread issues TMA bulk copies (cp.async.bulk,
-//     mbarrier completion) of the tile's row offsets, entries (+ values), out list,
-//     window of the gathered vector and diagonal(s) -- all contiguous;
-//   stage G (tile j+kNS-2): cp.async (LDGSTS) gathers of the out-of-window entries;
-//   stage C (tile j): thread-per-row CAC-3 chains from shared memory, then the epilogue.
-// Long rows (> kLongRow entries) are done first by warps of the grid (warp per row).
-constexpr int kTR = 256;  // rows per tile = threads per block of the tile engine
-#ifndef SCG_NS
-#define SCG_NS 3
-#endif
-constexpr int kNS = SCG_NS;  // >= 2: structure leads by kNS-1 tiles, gathers by kNS-2
-static_assert(kNS >= 2, "tile pipeline needs two stages");
-#ifndef SCG_HALO
-#define SCG_HALO 256
-#endif
-constexpr int kH = SCG_HALO;                    // window reach beyond the tile's rows (host side)
-constexpr int kWinCap = kTR + 2 * kH;           // window elements
-constexpr int kOutCap = 512;                    // out-of-window entries per tile
-template <bool UNI>
-struct TileCap {
-  static constexpr int v = UNI ? 1024 : 768;
-};
-
-struct TileDesc {  // host-built, one per tile
-  int r0, r1, e0, e1;   // rows [r0, r1) (local), entries [e0, e1)
-  int o0, o1, wlo, whi; // out list [o0, o1); window [wlo, whi) of GLOBAL indices
-};
-
-template <int NC, bool UNI>
-struct __align__(16) TileBuf {
-  unsigned rp[kTR + 8];
-  int col[TileCap<UNI>::v + 8];
-  double val[UNI ? 2 : TileCap<UNI>::v + 4];
-  int out[kOutCap + 8];
-  double win[kWinCap + 4];
-  double d0[kTR + 4];
-  double d1[NC > 1 ? kTR + 4 : 2];
-  double gx[kOutCap];
-};
-
-constexpr int kTLCap = 96;  // tile descriptors of one block held in shared memory
-
-template <int NC, bool UNI>
-struct __align__(16) TileSmem {
-  TileBuf<NC, UNI> sb[kNS];
-  TileDesc tl[kTLCap];
-  unsigned long long bar[kNS];
-};
-
-template <int NC, bool UNI>
-__device__ __forceinline__ void tile_issue(const Rows &RL, const double *X, const double *diag0, const double *diag1,
-                                           const TileDesc &T, TileBuf<NC, UNI> &b, unsigned long long *bar) {
-  uint32_t bytes = seg_bytes<4>(T.r0, T.r1 + 1) + seg_bytes<4>(T.e0, T.e1) + seg_bytes<4>(T.o0, T.o1) +
-                   seg_bytes<8>(T.wlo, T.whi) + seg_bytes<8>(T.r0, T.r1);
-  if (!UNI) bytes += seg_bytes<8>(T.e0, T.e1);
-  if (NC > 1) bytes += seg_bytes<8>(T.r0, T.r1);
-  mbar_arrive_tx(bar, bytes);
-  bulk_seg<4>(b.rp, RL.trp, T.r0, T.r1 + 1, bar);
-  bulk_seg<4>(b.col, RL.tcol, T.e0, T.e1, bar);
-  if (!UNI) bulk_seg<8>(b.val, RL.tval, T.e0, T.e1, bar);
-  bulk_seg<4>(b.out, RL.tout, T.o0, T.o1, bar);
-  bulk_seg<8>(b.win, X, T.wlo, T.whi, bar);
-  bulk_seg<8>(b.d0, diag0, T.r0, T.r1, bar);
-  if (NC > 1) bulk_seg<8>(b.d1, diag1, T.r0, T.r1, bar);
-}
-
-template <int NC, bool UNI>
-__device__ __forceinline__ void tile_gather(const double *__restrict__ X, const TileDesc &T, TileBuf<NC, UNI> &b) {
-  const int no = T.o1 - T.o0;
-  const int *op = b.out + seg_shift<4>(T.o0);
-  for (int k = threadIdx.x; k < no; k += kTR) cp_async8(b.gx + k, X + op[k]);
-}
-
-template <int NC, bool UNI, class Epi>
-__device__ __forceinline__ void tile_compute(const Rows &RL, const TileDesc &T, const TileBuf<NC, UNI> &b,
-                                             double rden, long long rb, Epi &epi) {
-  const int i = threadIdx.x;
-  if (i >= T.r1 - T.r0) return;
-  const int shr = seg_shift<4>(T.r0);
-  const unsigned ra = b.rp[shr + i], rn = b.rp[shr + i + 1];
-  if (rn >> 31) return;  // long row: done by the warp engine
-  const int e0 = (int)(ra & 0x7fffffffu) - T.e0, e1 = (int)(rn & 0x7fffffffu) - T.e0;
-  const int *colp = b.col + seg_shift<4>(T.e0);
-  const double *valp = b.val + seg_shift<8>(T.e0);
-  const double *wp = b.win + seg_shift<8>(T.wlo);
-  RowOut<NC> o;
-  o.r = T.r0 + i;
-  o.xr = wp[(int)(rb + T.r0 + i - T.wlo)] * rden;
-  const int shd = seg_shift<8>(T.r0);
-  o.s[0] = b.d0[shd + i] * o.xr;
-  if (NC > 1) o.s[NC - 1] = b.d1[shd + i] * o.xr;
-  for (int e = e0; e < e1; ++e) {
-    const int c = colp[e];
-    const int idx = c & 0x3fffffff;
-    const double g = (c & 0x40000000) ? b.gx[idx] : wp[idx];
-    const double m = UNI ? (c < 0 ? -RL.m0 : RL.m0) : valp[e];
-    const double x = g * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc) o.s[cc] = fma(m, x, o.s[cc]);
-  }
-  epi(o);
-}
-
-template <int NC, bool UNI, class Epi>
-__device__ __forceinline__ void spmv_tiles(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
-                                           const double *__restrict__ diag0, const double *__restrict__ diag1,
-                                           long long rb, Epi &epi, TileSmem<NC, UNI> &sm) {
-  const int lane = threadIdx.x & 31;
-  const int J = RL.ntiles > (int)blockIdx.x ? (RL.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  // this block's tile descriptors (tiles blockIdx.x + j gridDim.x) into shared memory
-  for (int j = threadIdx.x; j < J && j < kTLCap; j += blockDim.x)
-    sm.tl[j] = RL.tdesc[(int)blockIdx.x + j * (int)gridDim.x];
-  auto desc = [&](int j) -> const TileDesc & {
-    return j < kTLCap ? sm.tl[j] : RL.tdesc[(int)blockIdx.x + j * (int)gridDim.x];
-  };
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < kNS; ++q) mbar_init(&sm.bar[q], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int q = 0; q < kNS - 1 && q < J; ++q) tile_issue<NC, UNI>(RL, X, diag0, diag1, desc(q), sm.sb[q], &sm.bar[q]);
-  {  // long rows (warp per row) while the first tiles stream in
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwg = (gridDim.x * blockDim.x) >> 5;
-    for (int w = gw; w < RL.nlong; w += nwg) {
-      RowOut<NC> o;
-      long_row_chain<NC>(C, RL.longrows[w], X, den, diag0, diag1, rb, o);
-      if (lane == 0) epi(o);
-    }
-  }
-  const double rden = 1.0 / den;
-  for (int q = 0; q < kNS - 2; ++q) {
-    if (q < J) {
-      mbar_wait(&sm.bar[q], 0u);
-      tile_gather<NC, UNI>(X, desc(q), sm.sb[q]);
-    }
-    cp_async_commit();
-  }
-  for (int j = 0; j < J; ++j) {
-    if (threadIdx.x == 0 && j + kNS - 1 < J) {  // structure of tile j+kNS-1 (its slot held tile j-1)
-      const int q = (j + kNS - 1) % kNS;
-      tile_issue<NC, UNI>(RL, X, diag0, diag1, desc(j + kNS - 1), sm.sb[q], &sm.bar[q]);
-    }
-    if (j + kNS - 2 < J) {  // out-of-window gathers of tile j+kNS-2
-      const int q = (j + kNS - 2) % kNS;
-      mbar_wait(&sm.bar[q], (uint32_t)(((j + kNS - 2) / kNS) & 1));
-      tile_gather<NC, UNI>(X, desc(j + kNS - 2), sm.sb[q]);
-    }
-    cp_async_commit();
-    cp_async_wait<kNS - 2>();  // this thread's gathers of tile j
-    __syncthreads();           // everyone's
-    tile_compute<NC, UNI>(RL, desc(j), sm.sb[j % kNS], rden, rb, epi);
-    __syncthreads();  // slot of tile j free
-  }
-  cp_async_wait<0>();
-}
-
-// ---------------------------------------------------------------- SELL-W engine (SCG_ENGINE 2)
-// SELL slices (32 consecutive relabeled rows, column-major slots: coalesced column
-// loads) processed in chunks of kCW rows.  Per chunk one thread issues TMA bulk copies
-// of the chunk's WINDOW of the gathered vector X[wlo, whi) (global ids, wlo = chunk
-// start - kHW), its diagonal(s) and slice metadata, and the chunk's list of
-// out-of-window columns; once those land, the block issues cp.async gathers of the
-// out-of-window entries.  Entry codes (scol): bit 31 sign of a uniform value; bit 30
-// clear: bits 0..29 = column - wlo (window); bit 30 set, bit 29 clear: index into the
-// chunk's out list; bits 30 and 29 set: bits 0..28 = absolute column (list overflow,
-// plain global gather).  Two chunk stages, so the next chunk streams in while this
-// one is computed; only the column stream and the output remain in the compute phase.
-constexpr int kCW = 1024;   // rows per chunk (32 slices)
-#ifndef SCG_HW
-#define SCG_HW 256
-#endif
-constexpr int kHW = SCG_HW;  // window reach beyond the chunk
-constexpr int kExtCap = 1024;
-constexpr int kCS = 2;       // chunk stages
-
-template <int NC>
-struct __align__(16) SellWBuf {
-  double win[kCW + 2 * kHW + 4];
-  double d0[kCW + 4];
-  double d1[NC > 1 ? kCW + 4 : 2];
-  int2 meta[kCW / 32 + 2];
-  int ol[kExtCap + 4];
-  double ext[kExtCap];
-};
-template <int NC>
-struct __align__(16) SellWSmem {
-  SellWBuf<NC> b[kCS];
-  unsigned long long bar[kCS];
-};
-
-struct ChunkGeo {
-  long long wlo, whi;  // window (global ids)
-  int r0, r1;          // rows (local)
-  int s0, s1;          // slices
-  int o0, o1;          // out list
-};
-__device__ __forceinline__ ChunkGeo chunk_geo(const Rows &RL, int k, int nl, long long rb, long long n) {
-  ChunkGeo g;
-  g.r0 = k * kCW;
-  g.r1 = min(nl, g.r0 + kCW);
-  g.s0 = k * (kCW / 32);
-  g.s1 = min(RL.nslice, g.s0 + kCW / 32);
-  g.wlo = rb + g.r0 - kHW;
-  if (g.wlo < 0) g.wlo = 0;
-  g.whi = rb + g.r0 + kCW + kHW;
-  if (g.whi > n) g.whi = n;
-  g.o0 = __ldg(&RL.cout[k]);
-  g.o1 = __ldg(&RL.cout[k + 1]);
-  return g;
-}
-
-template <int NC>
-__device__ __forceinline__ void chunk_issue(const Rows &RL, const double *X, const double *diag0,
-                                            const double *diag1, const ChunkGeo &g, SellWBuf<NC> &b,
-                                            unsigned long long *bar) {
-  uint32_t bytes = seg_bytes<8>(g.wlo, g.whi) + seg_bytes<8>(g.r0, g.r1) + seg_bytes<8>(g.s0, g.s1) +
-                   seg_bytes<4>(g.o0, g.o1);
-  if (NC > 1) bytes += seg_bytes<8>(g.r0, g.r1);
-  mbar_arrive_tx(bar, bytes);
-  bulk_seg<8>(b.win, X, g.wlo, g.whi, bar);
-  bulk_seg<8>(b.d0, diag0, g.r0, g.r1, bar);
-  if (NC > 1) bulk_seg<8>(b.d1, diag1, g.r0, g.r1, bar);
-  bulk_seg<8>(b.meta, RL.meta, g.s0, g.s1, bar);
-  bulk_seg<4>(b.ol, RL.tout, g.o0, g.o1, bar);
-}
-
-template <int NC, bool UNI, class Epi>
-__device__ __forceinline__ void spmv_sellw(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
-                                           const double *__restrict__ diag0, const double *__restrict__ diag1,
-                                           long long rb, int nl, Epi &epi, SellWSmem<NC> &sm) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const long long n = RL.nglob;
-  const int nch = (nl + kCW - 1) / kCW;
-  const int per = (nch + gridDim.x - 1) / gridDim.x;
-  const int k0 = blockIdx.x * per, k1 = min(nch, k0 + per);
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < kCS; ++q) mbar_init(&sm.bar[q], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int q = 0; q < kCS && k0 + q < k1; ++q)
-      chunk_issue<NC>(RL, X, diag0, diag1, chunk_geo(RL, k0 + q, nl, rb, n), sm.b[q], &sm.bar[q]);
-  {  // long rows (warp per row) while the first chunks stream in
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwg = (gridDim.x * blockDim.x) >> 5;
-    for (int w = gw; w < RL.nlong; w += nwg) {
-      RowOut<NC> o;
-      long_row_chain<NC>(C, RL.longrows[w], X, den, diag0, diag1, rb, o);
-      if (lane == 0) epi(o);
-    }
-  }
-  const double rden = 1.0 / den;
-  for (int k = k0; k < k1; ++k) {
-    const int q = (k - k0) % kCS;
-    SellWBuf<NC> &b = sm.b[q];
-    const ChunkGeo g = chunk_geo(RL, k, nl, rb, n);
-    mbar_wait(&sm.bar[q], (uint32_t)(((k - k0) / kCS) & 1));
-    {  // out-of-window gathers of this chunk
-      const int no = g.o1 - g.o0;
-      const int *op = b.ol + seg_shift<4>(g.o0);
-      for (int t = threadIdx.x; t < no; t += blockDim.x) cp_async8(b.ext + t, X + op[t]);
-      cp_async_commit();
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const double *wp = b.win + seg_shift<8>(g.wlo);
-    const double *dp0 = b.d0 + seg_shift<8>(g.r0);
-    const double *dp1 = b.d1 + seg_shift<8>(g.r0);
-    const int2 *mp = b.meta + seg_shift<8>(g.s0);
-    // slices of this chunk: warp w takes s0 + w, s0 + w + nwarp, ...; the columns of the
-    // warp's next slice are loaded while the current one is computed
-    int sl = g.s0 + warp;
-    int cn[kChunk];
-    int2 mn = sl < g.s1 ? mp[sl - g.s0] : make_int2(0, 0);
-#pragma unroll
-    for (int u = 0; u < kChunk; ++u) cn[u] = (u < (mn.y & 0xff)) ? __ldg(&RL.scol[mn.x + u * 32 + lane]) : 0;
-    for (; sl < g.s1; sl += nwarp) {
-      const int2 m = mn;
-      int cc[kChunk];
-#pragma unroll
-      for (int u = 0; u < kChunk; ++u) cc[u] = cn[u];
-      const int sn = sl + nwarp;
-      mn = sn < g.s1 ? mp[sn - g.s0] : make_int2(0, 0);
-#pragma unroll
-      for (int u = 0; u < kChunk; ++u) cn[u] = (u < (mn.y & 0xff)) ? __ldg(&RL.scol[mn.x + u * 32 + lane]) : 0;
-      const int width = m.y & 0xff;
-      const int p = sl * 32 + lane;
-      if (p >= nl || lane < (m.y >> 8)) continue;
-      RowOut<NC> o;
-      o.r = p;
-      o.xr = wp[(int)(rb + p - g.wlo)] * rden;
-      o.s[0] = dp0[p - g.r0] * o.xr;
-      if (NC > 1) o.s[NC - 1] = dp1[p - g.r0] * o.xr;
-      for (int j = 0; j < width; ++j) {
-        int c;
-        if (j < kChunk) {
-#pragma unroll
-          for (int u = 0; u < kChunk; ++u)
-            if (u == j) c = cc[u];
-        } else {
-          c = __ldg(&RL.scol[m.x + j * 32 + lane]);
-        }
-        if (c == -1) break;  // padding (rows end at their length)
-        const int v = c & 0x3fffffff;
-        double gv;
-        if (!(c & 0x40000000)) gv = wp[v];
-        else if (!(c & 0x20000000)) gv = b.ext[v];
-        else gv = __ldg(&X[v & 0x1fffffff]);
-        const double mm = UNI ? (c < 0 ? -RL.m0 : RL.m0) : __ldg(&RL.sval[m.x + j * 32 + lane]);
-        const double x = gv * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
-#pragma unroll
-        for (int t = 0; t < NC; ++t) o.s[t] = fma(mm, x, o.s[t]);
-      }
-      epi(o);
-    }
-    __syncthreads();  // chunk buffer free
-    if (threadIdx.x == 0 && k + kCS < k1)
-      chunk_issue<NC>(RL, X, diag0, diag1, chunk_geo(RL, k + kCS, nl, rb, n), sm.b[q], &sm.bar[q]);
-  }
-}
 
 // ---------------------------------------------------------------- block reduction
 // Block-level exact accumulators (shared memory) for NS sums.
@@ -1152,7 +536,12 @@ __device__ __forceinline__ bool commit_and_ticket(XWin (&acc)[NS], XBlk<NS> &blk
   if (threadIdx.x == 0) {
     if (sys) fence_acq_rel_sys();
     else fence_acq_rel_gpu();
-    s_last = (atomicAdd(&slot->counter, 1u) == gridDim.x - 1);
+    const bool last = atomicAdd(&slot->counter, 1u) == gridDim.x - 1;
+    // acquire side: every other block's partials (limb atomics and plain stores such as
+    // k_primal's gpart) precede the ticket it took; this fence, then the block barrier,
+    // orders them before the last block's reads
+    if (last) fence_acq_rel_gpu();
+    s_last = last;
   }
   __syncthreads();
   return s_last != 0;
@@ -1165,7 +554,9 @@ __device__ __forceinline__ bool ticket_only(XSlot *slot) {
   __syncthreads();
   if (threadIdx.x == 0) {
     fence_acq_rel_sys();
-    s_last = (atomicAdd(&slot->counter, 1u) == gridDim.x - 1);
+    const bool last = atomicAdd(&slot->counter, 1u) == gridDim.x - 1;
+    if (last) fence_acq_rel_gpu();
+    s_last = last;
   }
   __syncthreads();
   return s_last != 0;
@@ -1292,19 +683,9 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 
 // Last block, thread 0: take this rank's limbs (resetting the slot) and either
 // finalize (P == 1) or publish them to every rank's mailbox (P > 1).
-#if SCG_TAILPROF
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#endif
 template <int NS>
 __device__ __forceinline__ void emit(XSlot *slot, DevScalars *sc, const Net &net, int kind, const FinArgs &f,
                                      const double *gk) {
-#if SCG_TAILPROF
-  const unsigned long long t0 = gtimer();
-#endif
   // acquire side of the block ticket: every block's limb atomics (performed in L2) precede
   // these L2 loads; the slot is idle until the next launch, so plain stores reset it
   fence_acq_rel_gpu();
@@ -1320,12 +701,6 @@ __device__ __forceinline__ void emit(XSlot *slot, DevScalars *sc, const Net &net
   slot->counter = 0;
   if (net.P <= 1) {
     finalize(kind, sc, L, gk, f);
-#if SCG_TAILPROF
-    sc->dbg_ns[kind] += gtimer() - t0;
-    if ((++sc->dbg_cnt[kind] & 511) == 0)
-      printf("[tail] kind %d: %llu launches, mean emit %.2f us\n", kind, sc->dbg_cnt[kind],
-             1e-3 * (double)sc->dbg_ns[kind] / (double)sc->dbg_cnt[kind]);
-#endif
     return;
   }
   const int e = (int)(net.E & 3ull);
@@ -1338,12 +713,6 @@ __device__ __forceinline__ void emit(XSlot *slot, DevScalars *sc, const Net &net
   }
   __threadfence_system();  // releases the limbs above (and, cumulatively, the halo stores) ...
   for (int q = 0; q < net.P; ++q) st_relaxed_sys(&net.peerMB[q]->flag[e][net.me], net.E);  // ... with these flags
-#if SCG_TAILPROF
-  sc->dbg_ns[kind] += gtimer() - t0;
-  if ((++sc->dbg_cnt[kind] & 511) == 0)
-    printf("[tail P>1] kind %d: %llu launches, mean emit %.2f us\n", kind, sc->dbg_cnt[kind],
-           1e-3 * (double)sc->dbg_ns[kind] / (double)sc->dbg_cnt[kind]);
-#endif
 }
 
 // P > 1: wait for every rank's contribution to collective net.E, add, finalize.
@@ -1488,19 +857,13 @@ struct EpiA {
   XWin acc[1];
   int err;
   __device__ __forceinline__ void operator()(const RowOut<1> &o) {
-#if SCG_STCS
-    __stcs(&a[o.r], o.s[0]);
-#else
     a[o.r] = o.s[0];
-#endif
-#ifndef SCG_EXP_NODOT
     xwin_add(acc[0], o.xr * o.s[0], err, blk);
-#endif
   }
 };
 
 template <bool UNI>
-__global__ void __launch_bounds__(kBlockA, UNI ? SCG_MINB * kBlock / kBlockA : 2 * kBlock / kBlockA) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
+__global__ void __launch_bounds__(kBlockA, UNI ? kMinBlocksUni : 2) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ X, int nl, long long rb, int i,
                                                          double *__restrict__ a, XSlot *slot, DevScalars *sc,
                                                          Net net) {
@@ -1514,15 +877,7 @@ __global__ void __launch_bounds__(kBlockA, UNI ? SCG_MINB * kBlock / kBlockA : 2
   epi.blk = xb.l[0];
   xwin_init(epi.acc[0]);
   epi.err = 0;
-#if SCG_ENGINE == 1
-  extern __shared__ __align__(128) unsigned char smraw[];
-  spmv_tiles<1, UNI>(C, RL, X, den, d, nullptr, rb, epi, *reinterpret_cast<TileSmem<1, UNI> *>(smraw));
-#elif SCG_ENGINE == 2
-  extern __shared__ __align__(128) unsigned char smraw[];
-  spmv_sellw<1, UNI>(C, RL, X, den, d, nullptr, rb, nl, epi, *reinterpret_cast<SellWSmem<1> *>(smraw));
-#else
   spmv_rows<1, UNI>(C, RL, X, den, d, nullptr, rb, nl, epi);
-#endif
   int err = epi.err;
   XWin (&acc)[1] = epi.acc;
   if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P, 0u) && threadIdx.x == 0) {
@@ -1558,12 +913,10 @@ struct __align__(16) WsSmem {
   WsStage st[kWsD];
   unsigned long long full[kWsD], empty[kWsD];
 };
-#ifndef SCG_WS_MINB
-#define SCG_WS_MINB 3  // 72 registers, 3 blocks/SM (measured: 2 blocks/SM 190 us, 3: 165 us on c3)
-#endif
+constexpr int kWsMinBlocks = 3;  // 72 registers, 3 blocks/SM (measured: 2 blocks/SM 190 us, 3: 165 us on c3)
 
 template <bool UNI>
-__global__ void __launch_bounds__(kWsThreads, SCG_WS_MINB) k_lanczos_a_ws(Csr C, Rows RL, const double *__restrict__ d,
+__global__ void __launch_bounds__(kWsThreads, kWsMinBlocks) k_lanczos_a_ws(Csr C, Rows RL, const double *__restrict__ d,
                                                                        const double *__restrict__ X, int nl,
                                                                        long long rb, int i, double *__restrict__ a,
                                                                        XSlot *slot, DevScalars *sc, Net net) {
@@ -1754,10 +1107,9 @@ __global__ void __launch_bounds__(kWsThreads, SCG_WS_MINB) k_lanczos_a_ws(Csr C,
 
 // Step i, part B (Alg. 2 lines 6-7): w_{i+1} = fma(-rho_{i-1}, v_{i-1}, fma(-omega_i, v_i, a)),
 // rho_i = ||w_{i+1}|| (exact); breakdown test.  Writes the un-normalized w_{i+1}.
-#ifndef SCG_MINB_B
-#define SCG_MINB_B 4
-#endif
-__global__ void __launch_bounds__(kBlock, SCG_MINB_B) k_lanczos_b(const double *__restrict__ a, const double *Xi,
+constexpr int kMinBlocksB = 4;
+constexpr int kBU = 2;  // row pairs in flight per thread
+__global__ void __launch_bounds__(kBlock, kMinBlocksB) k_lanczos_b(const double *__restrict__ a, const double *Xi,
                                                       const double *Xim1, double *Xip1, int nl, long long rb,
                                                       int i, XSlot *slot, DevScalars *sc, Net net) {
   pdl_entry();
@@ -1787,14 +1139,11 @@ __global__ void __launch_bounds__(kBlock, SCG_MINB_B) k_lanczos_b(const double *
     const double2 *a2 = reinterpret_cast<const double2 *>(a);
     const double2 *xi2 = reinterpret_cast<const double2 *>(Xi + rb);
     const double2 *xm2 = reinterpret_cast<const double2 *>(Xim1 ? Xim1 + rb : Xi + rb);
-#ifndef SCG_BU
-#define SCG_BU 2
-#endif
-    for (int p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += SCG_BU * stride) {
-      double2 av[SCG_BU], xi[SCG_BU], xm[SCG_BU];
-      unsigned mk[SCG_BU];
+    for (int p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += kBU * stride) {
+      double2 av[kBU], xi[kBU], xm[kBU];
+      unsigned mk[kBU];
 #pragma unroll
-      for (int u = 0; u < SCG_BU; ++u) {
+      for (int u = 0; u < kBU; ++u) {
         const int p = p0 + u * stride;
         if (p < np) {
           av[u] = __ldcs(&a2[p]);  // a is dead after this step: evict first
@@ -1804,7 +1153,7 @@ __global__ void __launch_bounds__(kBlock, SCG_MINB_B) k_lanczos_b(const double *
         }
       }
 #pragma unroll
-      for (int u = 0; u < SCG_BU; ++u) {
+      for (int u = 0; u < kBU; ++u) {
         const int p = p0 + u * stride;
         if (p < np) {
           row(2 * p, av[u].x, xi[u].x, xm[u].x, mk[u] & 0xffu);
@@ -1865,7 +1214,7 @@ __device__ __forceinline__ void st_release_gpu(unsigned long long *p, unsigned l
 }
 
 template <bool UNI>
-__global__ void __launch_bounds__(kBlockA, UNI ? SCG_MINB * kBlock / kBlockA : 2 * kBlock / kBlockA)
+__global__ void __launch_bounds__(kBlockA, UNI ? kMinBlocksUni : 2)
     k_lanczos_pass1(Csr C, Rows RL, const double *__restrict__ d, double *G, long long npad, int store, int q,
                     int nl, double *a, XSlot *slot_om, XSlot *slot_rho, DevScalars *sc, Net net,
                     unsigned long long *gflag, unsigned long long ebase) {
@@ -1997,14 +1346,8 @@ __global__ void __launch_bounds__(kBlockA, UNI ? SCG_MINB * kBlock / kBlockA : 2
 // memory, kBS stages deep, by one thread; the block computes the tile from shared memory.
 // The bytes in flight live in shared memory, not registers, so the exact-sum window keeps
 // its registers without limiting the memory-level parallelism.
-#ifndef SCG_BT
-#define SCG_BT 2048
-#endif
-#ifndef SCG_BS
-#define SCG_BS 3
-#endif
-constexpr int kBT = SCG_BT;  // rows per tile
-constexpr int kBS = SCG_BS;  // stages
+constexpr int kBT = 2048;  // rows per tile
+constexpr int kBS = 3;     // stages
 struct __align__(16) BStage {
   double a[kBT + 2], xi[kBT + 4], xm[kBT + 4];
 };
@@ -2231,7 +1574,7 @@ struct EpiC {
 };
 
 template <bool UNI>
-__global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_c(Csr C, Rows RL, const double *__restrict__ d,
+__global__ void __launch_bounds__(kBlock, UNI ? kMinBlocksUni : 2) k_lanczos_c(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ Xj, const double *Xjm1,
                                                          double *Xjp1, double *__restrict__ x, int nl, long long rb,
                                                          int j, DevScalars *sc, XSlot *slot, Net net) {
@@ -2239,15 +1582,7 @@ __global__ void __launch_bounds__(kBlock, UNI ? SCG_MINB : 2) k_lanczos_c(Csr C,
   if (j >= sc->k) return;  // sc->k holds the effective k after k_tridiag
   EpiC epi{Xjm1, Xjp1, x, rb, &net, j, sc->om[j - 1], sc->rho[j - 1], j >= 2 ? sc->rho[j - 2] : 1.0, sc->rho[j],
            sc->s[0], sc->s[j], 1.0 / sc->rho[j], 1.0 / (j >= 2 ? sc->rho[j - 2] : 1.0)};
-#if SCG_ENGINE == 1
-  extern __shared__ __align__(128) unsigned char smraw[];
-  spmv_tiles<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, epi, *reinterpret_cast<TileSmem<1, UNI> *>(smraw));
-#elif SCG_ENGINE == 2
-  extern __shared__ __align__(128) unsigned char smraw[];
-  spmv_sellw<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, nl, epi, *reinterpret_cast<SellWSmem<1> *>(smraw));
-#else
   spmv_rows<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, nl, epi);
-#endif
   // P > 1: the next step gathers w_{j+1} -- a barrier collective (no sums)
   if (net.P > 1 && ticket_only(slot) && threadIdx.x == 0) {
     FinArgs f{};
@@ -2264,11 +1599,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict_
                                                        double *__restrict__ x, int nl, long long rb, XSlot *slot,
                                                        DevScalars *sc, Net net) {
   pdl_entry();
-  __shared__ double s_s[kMaxQ], s_r[kMaxQ], s_rr[kMaxQ];
+  __shared__ double s_s[kMaxQ], s_rr[kMaxQ];
   const int k = sc->k;
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     s_s[j] = sc->s[j];
-    s_r[j] = sc->rho[j];
     s_rr[j] = 1.0 / sc->rho[j];
   }
   __shared__ XBlk<1> xb;
@@ -2363,15 +1697,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
   xwin_init(epi.acc[1]);
   xwin_init(epi.acc[2]);
   epi.err = 0;
-#if SCG_ENGINE == 1
-  extern __shared__ __align__(128) unsigned char smraw[];
-  spmv_tiles<2, UNI>(C, RL, x, nu, d, cdiag, rb, epi, *reinterpret_cast<TileSmem<2, UNI> *>(smraw));
-#elif SCG_ENGINE == 2
-  extern __shared__ __align__(128) unsigned char smraw[];
-  spmv_sellw<2, UNI>(C, RL, x, nu, d, cdiag, rb, nl, epi, *reinterpret_cast<SellWSmem<2> *>(smraw));
-#else
   spmv_rows<2, UNI>(C, RL, x, nu, d, cdiag, rb, nl, epi);
-#endif
   int err = epi.err;
   XWin (&acc)[3] = epi.acc;
   if (commit_and_ticket<3>(acc, xb, slot, err, sc, net.P, 0u) && threadIdx.x == 0) {
@@ -2688,15 +2014,7 @@ __global__ void __launch_bounds__(kBlock) k_apply_d(Csr C, Rows RL, const double
                                                     double *__restrict__ y) {
   pdl_entry();
   EpiY epi{y};
-#if SCG_ENGINE == 1
-  extern __shared__ __align__(128) unsigned char smraw[];
-  spmv_tiles<1, UNI>(C, RL, X, 1.0, d, nullptr, rb, epi, *reinterpret_cast<TileSmem<1, UNI> *>(smraw));
-#elif SCG_ENGINE == 2
-  extern __shared__ __align__(128) unsigned char smraw[];
-  spmv_sellw<1, UNI>(C, RL, X, 1.0, d, nullptr, rb, nl, epi, *reinterpret_cast<SellWSmem<1> *>(smraw));
-#else
   spmv_rows<1, UNI>(C, RL, X, 1.0, d, nullptr, rb, nl, epi);
-#endif
 }
 
 // out[orig[r]] = in[r]: device rows back to input order (outputs).

@@ -96,23 +96,14 @@ struct Shard {
   scg_iter_rec *dlog = nullptr;
   int *longrows = nullptr;
   int nlong = 0;
-  int *sell_perm = nullptr, *sell_col = nullptr;
+  int *sell_col = nullptr;
   int2 *sell_meta = nullptr;
   double *sell_val = nullptr;
   double sell_m0 = 0.0, sell_slots = 0.0;
   bool sell_uniform = false;
-  int nslice = 0, nwin = 0;
-  int *sell_wstart = nullptr;
-  unsigned *trp = nullptr;  // tile-staged CSR (SCG_ENGINE 1)
-  int *tcol = nullptr;
-  double *tval = nullptr;
-  int *tout = nullptr, *cout = nullptr;
+  int nslice = 0;
   unsigned *work = nullptr;  // dynamic slice counter of k_lanczos_a (graphs with long rows)
   bool dyn = false;
-  TileDesc *tdesc = nullptr;
-  int ntiles = 0, tile_h = 0;
-  long long tile_out = 0;
-  size_t smem1 = 0, smem2 = 0;
   // row relabeling (SELL engine): local row nu holds input row rb + origloc[nu]
   std::vector<int> origloc;
   int *orig = nullptr;            // device copy of origloc
@@ -127,9 +118,9 @@ struct Shard {
   int64_t halo_rows = 0;
   // grids
   unsigned long long *gflag = nullptr;  // grid-barrier flag of the fused pass-1 kernel
-  bool ws = false;  // k_lanczos_a as the warp-specialized TMA kernel (SCG_WS=1)
+  bool ws = false;  // k_lanczos_a as the warp-specialized TMA kernel (SCG_WS_SPMV)
   int grid_ws = 1;
-  int grid_rows = 1, grid_primal = 1, grid_tiles = 1, grid_b = 1, grid_comb = 1, grid_dual = 1, grid_norm = 1,
+  int grid_rows = 1, grid_primal = 1, grid_spmv = 1, grid_b = 1, grid_comb = 1, grid_dual = 1, grid_norm = 1,
       grid_mon = 1, grid_flush = 1, grid_a = 1, grid_btma = 1;
   double kb[KC_COUNT] = {0};  // algorithmic bytes of one launch of each class
 };
@@ -148,10 +139,10 @@ struct scg_ctx {
   int world = 1, mode = 0;  // mode 0: single, 1: emulated shards, 2: one rank of a multi-process job
   bool box = false;           // constraint set K = {klo <= u <= khi} (scaled units): SCG_INEQ or sketchycgal_set_box
   double klo = 0.0, khi = 0.0;
-  bool fused = false;        // one GPU: Lanczos pass 1 as one persistent kernel (SCG_FUSED=1)
+  bool fused = false;        // one GPU: Lanczos pass 1 as one persistent kernel (SCG_FUSED_PASS1)
   unsigned long long gphase = 0;  // grid-barrier phases issued so far (fused pass 1)
-  bool pdl = true;          // programmatic dependent launches (SCG_PDL=0 disables)
-  bool btma = false;        // TMA-staged k_lanczos_b (SCG_BTMA=1; measured slower: 115-166 vs 106 us on c3)
+  bool pdl = true;          // programmatic dependent launches (SCG_NO_PDL disables)
+  bool btma = false;        // TMA-staged k_lanczos_b (SCG_TMA_B; measured slower: 115-166 vs 93 us on c3)
   int rank = 0;
   std::vector<int64_t> splits;
   std::vector<Shard *> sh;
@@ -335,27 +326,16 @@ void launch_coop(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 b
   c->launches++;
 }
 
-Rows rows_of(const Shard *s, int64_t n, bool dyn = false) {
+Rows rows_of(const Shard *s, bool dyn = false) {
   Rows r{};
-  r.nglob = n;
   r.work = dyn ? s->work : nullptr;
   r.longrows = s->longrows;
   r.nlong = s->nlong;
-  r.perm = s->sell_perm;
   r.meta = s->sell_meta;
   r.scol = s->sell_col;
   r.sval = s->sell_val;
   r.m0 = s->sell_m0;
   r.nslice = s->nslice;
-  r.wstart = s->sell_wstart;
-  r.nwin = s->nwin;
-  r.trp = s->trp;
-  r.tcol = s->tcol;
-  r.tval = s->tval;
-  r.tout = s->tout;
-  r.tdesc = s->tdesc;
-  r.cout = s->cout;
-  r.ntiles = s->ntiles;
   return r;
 }
 
@@ -403,8 +383,8 @@ scg_status host_allreduce(scg_ctx *c, std::vector<double> &v) {
 void free_shard(Shard *s) {
   void *ptrs[] = {s->rp, s->col, s->val, s->wts, s->ldiag, s->cdiag, s->d, s->z, s->y, s->a, s->v, s->G,
                   s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
-                  s->sc, s->slots, s->dlog, s->longrows, s->sell_perm, s->sell_col, s->sell_meta, s->sell_val,
-                  s->sell_wstart, s->mask, s->mb, s->peerG, s->peerMB, s->trp, s->tcol, s->tval, s->tout, s->tdesc, s->orig, s->cout, s->V, s->ckr, s->work, s->gflag};
+                  s->sc, s->slots, s->dlog, s->longrows, s->sell_col, s->sell_meta, s->sell_val,
+                  s->mask, s->mb, s->peerG, s->peerMB, s->orig, s->V, s->ckr, s->work, s->gflag};
   for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -439,14 +419,12 @@ void relabel_perm(const int64_t *rp, const int32_t *colp, int64_t nl, int64_t rb
       }
     std::stable_partition(origloc.begin(), origloc.end(), [&](int r) { return halo[(size_t)r] != 0; });
   }
-#if SCG_ENGINE != 1
 #pragma omp parallel for schedule(static, 64)
   for (int64_t w = 0; w < nl; w += kSortWin) {
     const int64_t e = std::min<int64_t>(nl, w + kSortWin);
     std::stable_sort(origloc.begin() + w, origloc.begin() + e,
                      [&](int x, int y) { return rp[x + 1] - rp[x] > rp[y + 1] - rp[y]; });
   }
-#endif
 }
 
 // gmap[input id] = device label, for every vertex (all ranks' permutations).
@@ -525,11 +503,13 @@ bool csr_symmetric(const int64_t *rp, const int32_t *col, int64_t n) {
 // weights w = -L_rj and the diagonal, the long-row list, the SELL-32-sigma layout of
 // the short rows and the halo mask; then allocate and upload.  rp/colp/valp point at
 // this shard's rows (rp[0] may be nonzero).
-// SCG_DEBUG: split timings of the host init stages
-void dbg_split(const char *what) {
-  static const bool on = std::getenv("SCG_DEBUG") != nullptr;
+template <class... A>
+void dbg_log(const scg_ctx *c, const char *fmt, A... a) {  // SCG_DEBUG_LOG: layout facts on stderr
+  if (c->flags & SCG_DEBUG_LOG) std::fprintf(stderr, fmt, a...);
+}
+void dbg_split(const scg_ctx *c, const char *what) {  // SCG_DEBUG_LOG: host init stage timings
   static auto t0 = std::chrono::steady_clock::now();
-  if (!on) return;
+  if (!(c->flags & SCG_DEBUG_LOG)) return;
   const auto t1 = std::chrono::steady_clock::now();
   std::fprintf(stderr, "[scg]   %-22s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
   t0 = t1;
@@ -537,7 +517,7 @@ void dbg_split(const char *what) {
 
 scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *colp, const double *valp,
                        int has_diagonal) {
-  dbg_split("shard: start");
+  dbg_split(c, "shard: start");
   const int64_t nl = s->nl, rb = s->rb;
   const int R = c->R;
   const int64_t base = rp[0];
@@ -554,7 +534,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
     for (int64_t k = rp[r]; k < rp[r + 1]; ++k) cnt += colp[k - base] != r + rb;
     h_rp[(size_t)nu + 1] = cnt;
   }
-  dbg_split("shard: count");
+  dbg_split(c, "shard: count");
   int64_t cnt_off = 0;
   for (int64_t nu = 0; nu < nl; ++nu) {
     cnt_off += h_rp[(size_t)nu + 1];
@@ -598,7 +578,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
       halo += m != 0;
     }
   }
-  dbg_split("shard: fill");
+  dbg_split(c, "shard: fill");
   s->halo_rows = halo;
   s->nnz_off = cnt_off;
   std::vector<int> h_long;
@@ -628,7 +608,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
             alloc((void **)&s->gflag, sizeof(unsigned long long));
   if (!ok) return fail(c, SCG_ENOMEM, "device allocation");
   if (c->world > 1 && !alloc((void **)&s->mask, (size_t)nl)) return fail(c, SCG_ENOMEM, "halo mask");
-  dbg_split("shard: long rows+malloc");
+  dbg_split(c, "shard: long rows+malloc");
 
   // grid sizes from occupancy
   int occ = 1;
@@ -670,12 +650,12 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   CK(cudaMemsetAsync(s->y, 0, nlb, st));
   CK(cudaMemsetAsync(s->S, 0, nlb * R, st));
   CK(cudaStreamSynchronize(st));  // host vectors go out of scope (the SELL layout follows in build_sell)
-  dbg_split("shard: grids+H2D+memsets");
+  dbg_split(c, "shard: grids+H2D+memsets");
   return SCG_OK;
 }
 
 // Short-row layout of the SpMV engine (needs ||L||_F for the values), built on the host
-// from the device CSR copy: the tile-staged CSR (SCG_ENGINE 1) or SELL-32-sigma (0).
+// from the device CSR copy: SELL-32-sigma.
 // Values are scaled exactly as k_scale_c forms them (one IEEE division each).
 scg_status build_layout(scg_ctx *c, Shard *s) {
   const int64_t nl = s->nl;
@@ -699,120 +679,13 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
   };
   auto valof = [&](int64_t e) { return scale ? h_w[(size_t)e] / c->nrmL : h_w[(size_t)e]; };
   double matbytes = 0.0;
-#if SCG_ENGINE == 1
   {
-    const int cap = uni ? TileCap<true>::v : TileCap<false>::v;
-    const int64_t n = c->n, rb = s->rb;
-    // window reach: kH when it captures most columns (graphs with locality), else own rows only
-    auto in_win = [&](int64_t g0, int64_t h, int64_t col) { return col >= g0 - h && col < g0 + kTR + h; };
-    int64_t H = kH;
-    {
-      long long inw = 0, tot = 0;
-      for (int64_t r0 = 0; r0 < nl; r0 += kTR)
-        for (int64_t r = r0; r < std::min<int64_t>(nl, r0 + kTR); ++r)
-          for (int e = h_rp[(size_t)r]; e < h_rp[(size_t)r + 1]; ++e) { inw += in_win(rb + r0, kH, h_col[(size_t)e]); ++tot; }
-      if (tot > 0 && 4 * inw < tot) H = 0;
-    }
-    std::vector<unsigned> trp((size_t)nl + 1 + 4, 0u);
-    std::vector<int> tcol, tout;
-    std::vector<double> tval;
-    std::vector<TileDesc> tdesc;
-    TileDesc cur{};
-    int rows_in = 0, nnz_in = 0, out_in = 0;
-    auto close_tile = [&](int64_t r_end) {
-      cur.r1 = (int)r_end;
-      cur.e1 = (int)tcol.size();
-      cur.o1 = (int)tout.size();
-      tdesc.push_back(cur);
-    };
-    for (int64_t r = 0; r < nl; ++r) {
-      const int len = h_rp[(size_t)r + 1] - h_rp[(size_t)r];
-      const bool lng = len > kLongRow;
-      const int add = lng ? 0 : len;
-      int add_out = 0;
-      if (!lng && rows_in > 0)
-        for (int e = h_rp[(size_t)r]; e < h_rp[(size_t)r + 1]; ++e) add_out += !in_win(rb + cur.r0, H, h_col[(size_t)e]);
-      if (r == 0 || rows_in == kTR || nnz_in + add > cap || out_in + add_out > kOutCap) {
-        if (r > 0) close_tile(r);
-        cur = TileDesc{};
-        cur.r0 = (int)r;
-        cur.e0 = (int)tcol.size();
-        cur.o0 = (int)tout.size();
-        const int64_t g0 = rb + r;
-        cur.wlo = (int)std::max<int64_t>(0, g0 - H);
-        cur.whi = (int)std::min<int64_t>(n, g0 + kTR + H);
-        rows_in = nnz_in = out_in = 0;
-      }
-      trp[(size_t)r] |= (unsigned)tcol.size();
-      if (!lng)
-        for (int e = h_rp[(size_t)r]; e < h_rp[(size_t)r + 1]; ++e) {
-          const int64_t cc = h_col[(size_t)e];
-          int code;
-          if (in_win(rb + cur.r0, H, cc)) code = (int)(cc - cur.wlo);
-          else {
-            code = 0x40000000 | (int)(tout.size() - (size_t)cur.o0);
-            tout.push_back((int)cc);
-            ++out_in;
-          }
-          if (uni && h_w[(size_t)e] < 0) code = (int)((unsigned)code | 0x80000000u);
-          tcol.push_back(code);
-          if (!uni) tval.push_back(valof(e));
-        }
-      trp[(size_t)r + 1] = (unsigned)tcol.size() | (lng ? 0x80000000u : 0u);
-      ++rows_in;
-      nnz_in += add;
-    }
-    close_tile(nl);
-    if (tcol.size() >= (size_t)INT32_MAX || tout.size() >= (size_t)INT32_MAX) return fail(c, SCG_EINVAL, "tile layout too large");
-    s->ntiles = (int)tdesc.size();
-    const size_t nnz_s = tcol.size(), nout = tout.size();
-    tcol.resize(nnz_s + 4, 0);
-    tout.resize(nout + 4, 0);
-    if (!uni) tval.resize(nnz_s + 2, 0.0);
-    if (!alloc((void **)&s->trp, sizeof(unsigned) * trp.size()) || !alloc((void **)&s->tcol, sizeof(int) * tcol.size()) ||
-        !alloc((void **)&s->tout, sizeof(int) * tout.size()) ||
-        !alloc((void **)&s->tdesc, sizeof(TileDesc) * tdesc.size()) ||
-        (!uni && !alloc((void **)&s->tval, sizeof(double) * tval.size())))
-      return fail(c, SCG_ENOMEM, "tile layout");
-    CK(cudaMemcpyAsync(s->trp, trp.data(), sizeof(unsigned) * trp.size(), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(s->tcol, tcol.data(), sizeof(int) * tcol.size(), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(s->tout, tout.data(), sizeof(int) * tout.size(), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(s->tdesc, tdesc.data(), sizeof(TileDesc) * tdesc.size(), cudaMemcpyHostToDevice, st));
-    if (!uni) CK(cudaMemcpyAsync(s->tval, tval.data(), sizeof(double) * tval.size(), cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));
-    const long long nnz_long = (long long)cnt_off - (long long)nnz_s;
-    // algorithmic matrix bytes: row offsets, entry codes (+ values), out list, long rows
-    matbytes = 4.0 * (double)(nl + 1) + (double)nnz_s * (uni ? 4.0 : 12.0) + 4.0 * (double)nout +
-               32.0 * s->ntiles + 12.0 * (double)nnz_long + 8.0 * s->nlong;
-    s->tile_h = (int)H;
-    s->tile_out = (long long)nout;
-    s->smem1 = uni ? sizeof(TileSmem<1, true>) : sizeof(TileSmem<1, false>);
-    s->smem2 = uni ? sizeof(TileSmem<2, true>) : sizeof(TileSmem<2, false>);
-  }
-#else
-  {
-    // rows are already sorted by length within windows of kSigma rows (relabel_perm), so a
+    // rows are already sorted by length within windows of kSortWin rows (relabel_perm), so a
     // slice is 32 consecutive rows; leading long rows (warp engine) are skipped lanes
     const int64_t nsl = (nl + 31) / 32;
     hvec<int> scol;  // every slot is written by the fill pass (padding included)
     std::vector<int2> meta;
     hvec<double> sval;
-    // engine 2 (SELL-W): entries coded relative to their chunk's window / out list
-    std::vector<int> tout, cout;
-    const int64_t n = c->n, rb = s->rb;
-    int64_t wlo = 0, whi = 0;
-    int ocount = 0;
-    auto code_of = [&](int64_t e) -> int {
-      if (SCG_ENGINE != 2) return enc(e);
-      const int64_t cc = h_col[(size_t)e];
-      int code;
-      if (cc >= wlo && cc < whi) code = (int)(cc - wlo);
-      else if (ocount < kExtCap) { code = 0x40000000 | ocount++; tout.push_back((int)cc); }
-      else code = 0x60000000 | (int)cc;
-      if (uni && h_w[(size_t)e] < 0) code = (int)((unsigned)code | 0x80000000u);
-      return code;
-    };
-    if (SCG_ENGINE == 2 && n >= (1ll << 29)) return fail(c, SCG_EINVAL, "SELL-W: n must be < 2^29");
     // pass 1 (parallel): slice widths and leading long lanes; slot bases by prefix sum
     std::vector<int> swid((size_t)nsl), sskip((size_t)nsl);
     int badlong = 0;
@@ -839,16 +712,16 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
       slots += (size_t)swid[(size_t)q] * 32;
       if (slots >= (size_t)INT32_MAX) return fail(c, SCG_EINVAL, "SELL layout too large");
     }
-    // padding slots (rows shorter than their slice, long-row lanes): engine 0 points them at the
-    // dummy column n, whose gathered value is +0 in every gathered vector (zeroed slack), with a
-    // negative coefficient: fma(-m, +0, acc) == acc exactly for every acc (also +-0), so the
-    // kernel needs no per-slot padding test.  Other engines keep -1.
-    const int padc = SCG_ENGINE == 0 ? (uni ? (int)((unsigned)c->n | 0x80000000u) : (int)c->n) : -1;
+    // padding slots (rows shorter than their slice, long-row lanes) point at the dummy column n,
+    // whose gathered value is +0 in every gathered vector (zeroed slack), with a negative
+    // coefficient: fma(-m, +0, acc) == acc exactly for every acc (also +-0), so the kernel needs
+    // no per-slot padding test.
+    const int padc = uni ? (int)((unsigned)c->n | 0x80000000u) : (int)c->n;
     scol.resize(slots);
     if (!uni) sval.resize(slots);
-    // pass 2: fill every slot, padding included (parallel; serial for engine 2, whose out
-    // lists grow per chunk)
-    auto fill = [&](int64_t q) {
+    // pass 2 (parallel): fill every slot, padding included
+#pragma omp parallel for schedule(static, 1024)
+    for (int64_t q = 0; q < nsl; ++q) {
       const int width = swid[(size_t)q], nskip = sskip[(size_t)q];
       const size_t b0 = (size_t)meta[(size_t)q].x;
       for (int j = 0; j < width; ++j)
@@ -857,41 +730,15 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
           const size_t slot = b0 + (size_t)j * 32 + l;
           const int e = (l >= nskip && r < nl) ? h_rp[(size_t)r] + j : -1;
           if (e >= 0 && e < h_rp[(size_t)r + 1]) {
-            scol[slot] = code_of(e);
+            scol[slot] = enc(e);
             if (!uni) sval[slot] = valof(e);
           } else {
             scol[slot] = padc;
             if (!uni) sval[slot] = -0.0;
           }
         }
-    };
-    if (SCG_ENGINE == 2) {
-      for (int64_t q = 0; q < nsl; ++q) {
-        if (q % (kCW / 32) == 0) {  // new chunk
-          const int64_t r0 = q * 32;
-          wlo = std::max<int64_t>(0, rb + r0 - kHW);
-          whi = std::min<int64_t>(n, rb + r0 + kCW + kHW);
-          cout.push_back((int)tout.size());
-          ocount = 0;
-        }
-        fill(q);
-      }
-    } else {
-#pragma omp parallel for schedule(static, 1024)
-      for (int64_t q = 0; q < nsl; ++q) fill(q);
     }
     s->nslice = (int)meta.size();
-    s->nwin = 0;
-    if (SCG_ENGINE == 2) {
-      cout.push_back((int)tout.size());
-      s->tile_out = (long long)tout.size();
-      tout.resize(tout.size() + 4, 0);
-      meta.resize(meta.size() + 2, make_int2(0, 0));  // bulk-copy slack
-      if (!alloc((void **)&s->tout, sizeof(int) * tout.size()) || !alloc((void **)&s->cout, sizeof(int) * cout.size()))
-        return fail(c, SCG_ENOMEM, "SELL-W layout");
-      CK(cudaMemcpyAsync(s->tout, tout.data(), sizeof(int) * tout.size(), cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(s->cout, cout.data(), sizeof(int) * cout.size(), cudaMemcpyHostToDevice, st));
-    }
     if (!alloc((void **)&s->sell_meta, sizeof(int2) * meta.size()) ||
         !alloc((void **)&s->sell_col, sizeof(int) * scol.size()) ||
         (!uni && !alloc((void **)&s->sell_val, sizeof(double) * sval.size())))
@@ -903,74 +750,41 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
     CK(cudaStreamSynchronize(st));
     s->sell_slots = (double)scol.size();
     matbytes = s->sell_slots * (uni ? 4.0 : 12.0) + 8.0 * s->nslice;
-#if SCG_ENGINE == 2
-    matbytes += 4.0 * (double)s->tile_out + 4.0 * (double)((nl + kCW - 1) / kCW);
-    s->smem1 = sizeof(SellWSmem<1>);
-    s->smem2 = sizeof(SellWSmem<2>);
-#else
-    s->smem1 = s->smem2 = 0;
-#endif
   }
-#endif
   {  // grids of the SpMV kernels
     const bool U = s->sell_uniform;
-    auto setsm = [&](const void *k, size_t b) {
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
-      if (b > 0) cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-    };
     int oa = 1, om = 1;
     if (U) {
-      setsm((const void *)k_lanczos_a<true>, s->smem1);
-      setsm((const void *)k_lanczos_c<true>, s->smem1);
-      setsm((const void *)k_apply_d<true>, s->smem1);
-      setsm((const void *)k_monitor<true>, s->smem2);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<true>, kBlock, s->smem1);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<true>, kBlock, s->smem2);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<true>, kBlock, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<true>, kBlock, 0);
     } else {
-      setsm((const void *)k_lanczos_a<false>, s->smem1);
-      setsm((const void *)k_lanczos_c<false>, s->smem1);
-      setsm((const void *)k_apply_d<false>, s->smem1);
-      setsm((const void *)k_monitor<false>, s->smem2);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<false>, kBlock, s->smem1);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<false>, kBlock, s->smem2);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<false>, kBlock, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<false>, kBlock, 0);
     }
-    const int need = SCG_ENGINE == 1   ? std::max(s->ntiles, (s->nlong + 7) / 8)
-                     : SCG_ENGINE == 2 ? (int)std::max<int64_t>((nl + kCW - 1) / kCW, (s->nlong + 7) / 8)
-                                       : (int)std::max<int64_t>((s->nslice + 7) / 8, (s->nlong + 7) / 8);
-    s->grid_tiles = std::max(1, std::min(need, std::max(1, oa) * c->nsm));
-    {  // k_lanczos_a may use its own block size (kBlockA)
-      int oA = 1;
-      if (U) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oA, k_lanczos_a<true>, kBlockA, s->smem1);
-      else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oA, k_lanczos_a<false>, kBlockA, s->smem1);
-      const int needA = SCG_ENGINE == 0 ? (int)std::max<int64_t>((s->nslice + kBlockA / 32 - 1) / (kBlockA / 32), 1)
-                                        : need;
-      s->grid_a = std::max(1, std::min(needA, std::max(1, oA) * c->nsm));
-    }
+    const int need = (int)std::max<int64_t>((s->nslice + 7) / 8, (s->nlong + 7) / 8);
+    s->grid_spmv = std::max(1, std::min(need, std::max(1, oa) * c->nsm));
+    const int needA = (int)std::max<int64_t>((s->nslice + kBlockA / 32 - 1) / (kBlockA / 32), 1);
+    s->grid_a = std::max(1, std::min(needA, std::max(1, oa) * c->nsm));
     s->grid_mon = std::max(1, std::min(need, std::max(1, om) * c->nsm));
-    if (std::getenv("SCG_DEBUG"))
-      std::fprintf(stderr, "[scg] shard %d: nl=%lld tiles=%d long=%d uni=%d H=%d out=%lld/%lld smem1=%zu occ_a=%d occ_m=%d grid=%d\n",
-                   s->rank, (long long)nl, s->ntiles, s->nlong, (int)U, s->tile_h, s->tile_out, (long long)s->nnz_off,
-                   s->smem1, oa, om, s->grid_tiles);
+    dbg_log(c, "[scg] shard %d: nl=%lld long=%d uni=%d occ_a=%d occ_m=%d grid_a=%d\n", s->rank, (long long)nl, s->nlong,
+            (int)U, oa, om, s->grid_a);
   }
   // dynamic slice distribution for skewed graphs (long rows present): warps that carry hub
   // rows take fewer slices.  Off for graphs without long rows (static ranges keep L1 locality).
-  s->dyn = SCG_ENGINE == 0 && SCG_PIPE == 3 && s->nlong > 0 && std::getenv("SCG_DYN") == nullptr
-               ? true
-               : (std::getenv("SCG_DYN") && std::getenv("SCG_DYN")[0] == '1' && SCG_ENGINE == 0 && SCG_PIPE == 3);
-  // warp-specialized TMA k_lanczos_a (uniform weights, static slice ranges)
-  s->ws = SCG_ENGINE == 0 && s->sell_uniform && !s->dyn && std::getenv("SCG_WS") && std::getenv("SCG_WS")[0] == '1';
+  s->dyn = s->nlong > 0;
+  // warp-specialized TMA k_lanczos_a (uniform weights, static slice ranges; SCG_WS_SPMV)
+  s->ws = s->sell_uniform && !s->dyn && (c->flags & SCG_WS_SPMV);
   if (s->ws) {
     const int wsb = (int)sizeof(WsSmem);
     cudaFuncSetAttribute((const void *)k_lanczos_a_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, wsb);
-    const int pct = std::min(100, (SCG_WS_MINB * (wsb + 4096) * 100 + 233471) / 233472);
+    const int pct = std::min(100, (kWsMinBlocks * (wsb + 4096) * 100 + 233471) / 233472);
     cudaFuncSetAttribute((const void *)k_lanczos_a_ws<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
     int ow = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ow, k_lanczos_a_ws<true>, kWsThreads, wsb);
     const int need = (int)std::max<int64_t>((s->nslice + kWsCons - 1) / kWsCons, 1);
     s->grid_ws = std::max(1, std::min(need, std::max(1, ow) * c->nsm));
-    if (std::getenv("SCG_DEBUG"))
-      std::fprintf(stderr, "[scg] shard %d: warp-specialized k_lanczos_a, smem %d B, %d blocks/SM, grid %d\n", s->rank, wsb,
-                   ow, s->grid_ws);
+    dbg_log(c, "[scg] shard %d: warp-specialized k_lanczos_a, smem %d B, %d blocks/SM, grid %d\n", s->rank, wsb, ow,
+            s->grid_ws);
   }
   // algorithmic bytes per launch
   const double N = (double)c->n, NL = (double)nl;
@@ -1205,7 +1019,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
     return st;
   };
   if (!L || !L->row_ptr || !L->col_idx || !L->val) return bad(SCG_EINVAL);
-  const bool dbg = std::getenv("SCG_DEBUG") != nullptr;
+  const bool dbg = (flags & SCG_DEBUG_LOG) != 0;
   auto t_0 = std::chrono::steady_clock::now();
   auto tick = [&](const char *what) {
     if (!dbg) return;
@@ -1236,15 +1050,12 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   c->lnN = std::log((double)n);
   c->log_cap = 1024;
   {
-    // Programmatic dependent launches (triggered at the block commit, SCG_PDL_LATE), measured
-    // without profiling events against no PDL: c0 +8%, c1 +23%, c2 +0%, c3 +0.5% (triggered
-    // at kernel entry instead they cost c3 17%: profiles/r01/pdl_policy.txt).  SCG_PDL=0 disables.
-    const char *e = std::getenv("SCG_PDL");
-    c->pdl = !(e && e[0] == '0');
-    const char *eu = std::getenv("SCG_FUSED");
-    c->fused = eu && eu[0] == '1';
-    const char *eb = std::getenv("SCG_BTMA");
-    c->btma = eb && eb[0] == '1';
+    // Programmatic dependent launches (triggered at the block commit), measured without
+    // profiling events against no PDL: c0 +8%, c1 +23%, c2 +0%, c3 +0.5% (triggered at kernel
+    // entry instead they cost c3 17%: profiles/r01/pdl_policy.txt).  SCG_NO_PDL disables.
+    c->pdl = (flags & SCG_NO_PDL) == 0;
+    c->fused = (flags & SCG_FUSED_PASS1) != 0;
+    c->btma = (flags & SCG_TMA_B) != 0;
   }
   c->npad = (n + 4 + kWin - 1) / kWin * kWin;  // >= 16 bytes of slack for the bulk copies
 
@@ -1310,7 +1121,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
     s->nl = c->splits[(size_t)s->rank + 1] - s->rb;
     const int64_t off = c->mode == 2 ? 0 : s->rb;  // index of this shard's first row in L->row_ptr
     relabel_perm(L->row_ptr + off, L->col_idx + L->row_ptr[off], s->nl, s->rb,
-                 world > 1 && !(std::getenv("SCG_HALO_FIRST") && std::getenv("SCG_HALO_FIRST")[0] == '0'),
+                 world > 1,
                  s->origloc);
   }
   tick("device+relabel");
@@ -1349,7 +1160,7 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   if (c->mode == 2) {  // agree on the storage mode (all ranks store, or none)
     std::vector<double> v{c->store ? 0.0 : 1.0};
     if ((st = host_allreduce(c, v))) return bad(st);
-    if (v[0] != 0.0 && c->store) return bad(fail(c, SCG_ENOMEM, "Lanczos store does not fit on every rank"));
+    if (v[0] != 0.0) c->store = false;  // some rank cannot store: all ranks run the two-pass form
   }
 #endif
 
@@ -1394,10 +1205,6 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   tick("layout+omega");
   for (int k = 0; k < KC_COUNT; ++k) { c->kl[k] = 0; c->ks[k] = 0; c->kms[k] = 0; c->kbytes_sum[k] = 0; }
   c->launches = 0;
-  {
-    const char *e = std::getenv("SCG_PROF_EVERY");
-    if (e && std::atoi(e) > 0) c->prof_every = std::atoi(e);
-  }
   *out = c;
   return SCG_OK;
 }
@@ -1460,10 +1267,10 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       return j == 1 ? c->wslot(s, 0) : c->wslot(s, 1 + (j & 1));
     };
     // ---- Lanczos pass 1 (Alg. 2 lines 1-9)
-    if (c->fused && c->world == 1 && SCG_ENGINE == 0) {  // all q steps in one persistent launch
+    if (c->fused && c->world == 1) {  // all q steps in one persistent launch
       Shard *s = c->sh[0];
       Csr C{s->rp, s->col, s->val};
-      Rows TT = rows_of(s, c->n, s->dyn);
+      Rows TT = rows_of(s, s->dyn);
       auto kP = s->sell_uniform ? k_lanczos_pass1<true> : k_lanczos_pass1<false>;
       const unsigned long long E = ++c->epoch;
       const unsigned long long eb = c->gphase;
@@ -1476,14 +1283,14 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       unsigned long long E = ++c->epoch;
       for (Shard *s : c->sh) {
         Csr C{s->rp, s->col, s->val};
-        Rows TT = rows_of(s, c->n, s->dyn);
+        Rows TT = rows_of(s, s->dyn);
         auto kA = s->sell_uniform ? k_lanczos_a<true> : k_lanczos_a<false>;
         if (s->ws)
           launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], k_lanczos_a_ws<true>, dim3(s->grid_ws), dim3(kWsThreads),
                       sizeof(WsSmem), C, TT, (const double *)s->d, (const double *)slot(s, i), (int)s->nl,
                       (long long)s->rb, i, s->a, s->slots + SLOT_OM, s->sc, net_of(c, s, E));
         else
-          launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->grid_a), dim3(kBlockA), s->smem1, C, TT,
+          launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->grid_a), dim3(kBlockA), 0, C, TT,
                       (const double *)s->d, (const double *)slot(s, i), (int)s->nl, (long long)s->rb, i, s->a,
                       s->slots + SLOT_OM, s->sc, net_of(c, s, E));
       }
@@ -1520,10 +1327,10 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
         const unsigned long long E = ++c->epoch;
         for (Shard *s : c->sh) {
           Csr C{s->rp, s->col, s->val};
-          Rows TT = rows_of(s, c->n);
+          Rows TT = rows_of(s);
           auto kC = s->sell_uniform ? k_lanczos_c<true> : k_lanczos_c<false>;
           const double *Xjm1 = (j == 1) ? nullptr : slot(s, j - 1);
-          launch_smem(c, KC_LANCZOS_C, s->kb[KC_LANCZOS_C], kC, dim3(s->grid_tiles), dim3(kBlock), s->smem1, C, TT,
+          launch_smem(c, KC_LANCZOS_C, s->kb[KC_LANCZOS_C], kC, dim3(s->grid_spmv), dim3(kBlock), 0, C, TT,
                  (const double *)s->d, (const double *)slot(s, j), Xjm1, slot(s, j + 1), c->xg(s), (int)s->nl,
                  (long long)s->rb, j, s->sc, s->slots + SLOT_BAR, net_of(c, s, E));
         }
@@ -1543,9 +1350,9 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     unsigned long long E = ++c->epoch;
     for (Shard *s : c->sh) {
       Csr C{s->rp, s->col, s->val};
-      Rows TT = rows_of(s, c->n, s->dyn);
+      Rows TT = rows_of(s, s->dyn);
       auto kM = s->sell_uniform ? k_monitor<true> : k_monitor<false>;
-      launch_smem(c, KC_MONITOR, s->kb[KC_MONITOR], kM, dim3(s->grid_mon), dim3(kBlock), s->smem2, C, TT, (const double *)s->d,
+      launch_smem(c, KC_MONITOR, s->kb[KC_MONITOR], kM, dim3(s->grid_mon), dim3(kBlock), 0, C, TT, (const double *)s->d,
              (const double *)s->cdiag, (const double *)c->xg(s), c->vslot(s, js), (int)s->nl, (long long)s->rb,
              s->slots + SLOT_MON, s->sc, net_of(c, s, E));
     }
@@ -1700,8 +1507,8 @@ scg_status sketchycgal_apply_D(scg_ctx *c, const double *xh, double *yh) {
   for (Shard *s : c->sh) {
     CK(cudaMalloc(&dy, sizeof(double) * std::max<int64_t>(1, s->nl)));
     Csr C{s->rp, s->col, s->val};
-    Rows TT = rows_of(s, c->n);
-    launch_smem(c, KC_OTHER, 0.0, s->sell_uniform ? k_apply_d<true> : k_apply_d<false>, dim3(s->grid_tiles), dim3(kBlock), s->smem1,
+    Rows TT = rows_of(s);
+    launch_smem(c, KC_OTHER, 0.0, s->sell_uniform ? k_apply_d<true> : k_apply_d<false>, dim3(s->grid_spmv), dim3(kBlock), 0,
            C, TT, (const double *)s->d, (const double *)dx, (int)s->nl, (long long)s->rb, dy);
     CK(cudaStreamSynchronize(c->stream));
     if ((st = fetch_rows(c, s, dy, yh, off))) return st;
@@ -1870,18 +1677,25 @@ static scg_status colstats(scg_ctx *c, int which, const double *lam_host, std::v
   if (which == 2 || c->world == 1) {
     for (Shard *s : c->sh)
       if ((st = run(s, s->U, (long long)s->nl, 0, ny))) return st;
-  } else {  // sharded: gather one column at a time into the x slot (halo stores + barrier)
+  } else {
+    // sharded: gather one column at a time (halo stores + barrier) into alternating buffers --
+    // the x slot for even k, W slot 1 for odd k (both free between iterations; every iteration
+    // writes them before reading).  A rank may push column k+1 into a peer's buffer while that
+    // peer still reads column k; it pushes column k+2 into the same buffer only after its pull of
+    // collective k+1, which waits for the peer's push of k+1, enqueued after the peer's column-k
+    // statistics.
+    auto gbuf = [&](const Shard *s, int k) { return (k & 1) ? c->wslot(s, 1) : c->xg(s); };
     for (int k = 0; k < R; ++k) {
       const unsigned long long E = ++c->epoch;
       for (Shard *s : c->sh)
         launch(c, KC_OTHER, 0.0, k_push_col, dim3(grid_for(s->nl, 4 * c->nsm)), dim3(kBlock),
-               (const double *)(s->U + (long long)k * s->nl), c->xg(s), (int)s->nl, (long long)s->rb,
+               (const double *)(s->U + (long long)k * s->nl), gbuf(s, k), (int)s->nl, (long long)s->rb,
                s->slots + SLOT_BAR, s->sc, net_of(c, s, E));
       FinArgs f{};
       f.i = -1;
       pull_all(c, FK_BAR, 0, E, f);
       for (Shard *s : c->sh)
-        if ((st = run(s, c->xg(s), 0, k, 1))) return st;
+        if ((st = run(s, gbuf(s, k), 0, k, 1))) return st;
     }
   }
   return host_allreduce(c, outk);

@@ -15,8 +15,8 @@ import scg_inputs as si
 pytestmark = pytest.mark.gpu
 
 
-def _run_pair(gpu, L, R, T, seed, scale=True, regenerate=False):
-    g = gpu.SketchyCGAL(L, R=R, seed=seed, scale=scale, regenerate=regenerate)
+def _run_pair(gpu, L, R, T, seed, scale=True, regenerate=False, **opts):
+    g = gpu.SketchyCGAL(L, R=R, seed=seed, scale=scale, regenerate=regenerate, **opts)
     g.step(T)
     o = oracle.Oracle(L, R, seed=seed, scale=scale, logcap=T)
     o.step(T)
@@ -125,47 +125,43 @@ def test_isolated_vertices_and_heavy_row(gpu):
     _assert_trajectory(g, o, 30)
 
 
-@pytest.mark.parametrize("cfg,T,pdl", [("c0", 200, "0"), ("c2", 2, "1")])
-def test_launch_policy_forced_bitwise(gpu, cfg, T, pdl, monkeypatch):
-    """Programmatic dependent launches (default on) forced off, and explicitly on: the same
-    bitwise trajectory as the oracle."""
-    monkeypatch.setenv("SCG_PDL", pdl)
+@pytest.mark.parametrize("cfg,T,pdl", [("c0", 200, False), ("c2", 2, True)])
+def test_launch_policy_forced_bitwise(gpu, cfg, T, pdl):
+    """Programmatic dependent launches (default on) off (SCG_NO_PDL), and on: the same bitwise
+    trajectory as the oracle."""
     L = si.laplacian(cfg)
     c = si.CONFIGS[cfg]
-    g, o = _run_pair(gpu, L, c["R"], T, seed=c["seed"])
+    g, o = _run_pair(gpu, L, c["R"], T, seed=c["seed"], pdl=pdl)
     _assert_trajectory(g, o, T)
 
 
 @pytest.mark.parametrize("cfg,T", [("c0", 300), ("c3", 1)])
-def test_warp_specialized_spmv_engine_bitwise(gpu, cfg, T, monkeypatch):
-    """The opt-in warp-specialized TMA k_lanczos_a (SCG_WS=1: producer warp + mbarrier ring)
+def test_warp_specialized_spmv_engine_bitwise(gpu, cfg, T):
+    """The opt-in warp-specialized TMA k_lanczos_a (SCG_WS_SPMV: producer warp + mbarrier ring)
     gives the same bitwise trajectory."""
-    monkeypatch.setenv("SCG_WS", "1")
     L = si.laplacian(cfg)
     c = si.CONFIGS[cfg]
-    g, o = _run_pair(gpu, L, c["R"], T, seed=c["seed"])
+    g, o = _run_pair(gpu, L, c["R"], T, seed=c["seed"], ws_spmv=True)
     _assert_trajectory(g, o, T)
 
 
 @pytest.mark.parametrize("cfg,T", [("c0", 300), ("c2", 2), ("c3", 1)])
-def test_fused_pass1_kernel_bitwise(gpu, cfg, T, monkeypatch):
-    """The opt-in persistent pass-1 kernel (SCG_FUSED=1: all q Lanczos steps in one cooperative
+def test_fused_pass1_kernel_bitwise(gpu, cfg, T):
+    """The opt-in persistent pass-1 kernel (SCG_FUSED_PASS1: all q Lanczos steps in one cooperative
     launch, grid barriers on the exact-sum tickets) gives the same bitwise trajectory."""
-    monkeypatch.setenv("SCG_FUSED", "1")
     L = si.laplacian(cfg)
     c = si.CONFIGS[cfg]
-    g, o = _run_pair(gpu, L, c["R"], T, seed=c["seed"])
+    g, o = _run_pair(gpu, L, c["R"], T, seed=c["seed"], fused_pass1=True)
     _assert_trajectory(g, o, T)
 
 
 @pytest.mark.parametrize("P", [2, 3])
-def test_warp_specialized_sharded_bitwise(gpu, P, monkeypatch):
+def test_warp_specialized_sharded_bitwise(gpu, P):
     """The warp-specialized SpMV under emulated row shards (odd row bases: the 16-byte aligned
     bulk copy of the own entries starts one element early; peer halo stores elsewhere)."""
-    monkeypatch.setenv("SCG_WS", "1")
     L = si.laplacian("c0")
     T = 200
-    g = gpu.SketchyCGAL(L, R=10, seed=0, shards=P)
+    g = gpu.SketchyCGAL(L, R=10, seed=0, shards=P, ws_spmv=True)
     g.step(T)
     o = oracle.Oracle(L, 10, seed=0, logcap=T)
     o.step(T)
@@ -173,13 +169,12 @@ def test_warp_specialized_sharded_bitwise(gpu, P, monkeypatch):
 
 
 @pytest.mark.parametrize("regenerate", [False, True])
-def test_fused_pass1_breakdown_and_regenerate(gpu, regenerate, monkeypatch):
+def test_fused_pass1_breakdown_and_regenerate(gpu, regenerate):
     """Fused pass 1 through a Lanczos breakdown (K_8, k = 2 < q) in both Lanczos modes."""
-    monkeypatch.setenv("SCG_FUSED", "1")
     n = 8
     i, j = np.triu_indices(n, 1)
     L = si.laplacian_from_edges(n, i, j, np.ones(len(i)))
-    g, o = _run_pair(gpu, L, 3, 25, seed=2, regenerate=regenerate)
+    g, o = _run_pair(gpu, L, 3, 25, seed=2, regenerate=regenerate, fused_pass1=True)
     _assert_trajectory(g, o, 25)
 
 

@@ -4,6 +4,6 @@ TAG=${1:-p}; KRE=${2:-k_lanczos_a}; SKIP=${3:-40}
 O=gpurun_out/$TAG; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e ${BENCH_ARGS}"
-SCG_DEBUG=1 $CMD > $O/plain.json 2> $O/plain.err && \
+$CMD > $O/plain.json 2> $O/plain.err && \
 ncu --set full --clock-control none --import-source on -k regex:$KRE -s $SKIP -c 1 -o $O/prof $CMD > $O/ncu_full.log 2>&1
 echo "exit $?" >> $O/plain.err
