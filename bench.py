@@ -103,22 +103,63 @@ def _ncu_traffic(kernel_name: str, cfg: str):
     return None
 
 
-def cpu_oracle_sample(cfg: str, L, iters: int):
-    """Time the oracle (as it stands, single-threaded C) on `iters` iterations of the workload."""
+def host_info():
+    """nproc and the CPU model name of the box the oracle runs on."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+# timed oracle windows (SURVEY.md section 8(d)): the first iterations of each workload
+ORACLE_WINDOW = {"c0": 1000, "c1": 5000, "c2": 100, "c3": 10, "c4": 5}
+
+
+def cpu_oracle_sample(cfg: str, L, t_last: int, threads: int = 0, t_first: int = 1):
+    """Time the oracle as it stands (C, OpenMP row loops and exact sums; `threads` <= 0: all cores) on
+    iterations t_first..t_last of the workload; iterations before t_first run untimed."""
     import oracle
     import scg_inputs as si
     c = si.CONFIGS[cfg]
+    nth = oracle.set_threads(threads)
     t0 = time.perf_counter()
-    o = oracle.Oracle(L, c["R"], seed=c["seed"], logcap=iters)
+    o = oracle.Oracle(L, c["R"], seed=c["seed"], logcap=t_last)
+    if t_first > 1:
+        o.step(t_first - 1)
     t1 = time.perf_counter()
-    o.step(iters)
+    o.step(t_last - t_first + 1)
     t2 = time.perf_counter()
-    lg = o.log
-    matvecs = float(np.sum(2 * lg[:, 2] - 1 + 1))
-    return dict(value=iters / (t2 - t1), unit="iterations/s", cores=1, kind="oracle",
-                sample=f"oracle (C, 1 thread) on {cfg} iterations t=1..{iters} (q_t={int(lg[0, 1])}..{int(lg[-1, 1])}),"
-                       f" {t2 - t1:.1f} s; setup {t1 - t0:.1f} s excluded",
-                lanczos_matvecs_per_s=matvecs / (t2 - t1), seconds=t2 - t1)
+    oracle.set_threads(0)
+    lg = o.log[t_first - 1:t_last]
+    iters = t_last - t_first + 1
+    matvecs = float(np.sum(2 * lg[:, 2]))
+    return dict(value=iters / (t2 - t1), unit="iterations/s", cores=nth, kind="oracle",
+                sample=f"oracle (C, {nth} OpenMP threads) on {cfg} iterations t={t_first}..{t_last} "
+                       f"(q_t={int(lg[0, 1])}..{int(lg[-1, 1])}), {t2 - t1:.1f} s timed; setup"
+                       f"{' and t=1..%d' % (t_first - 1) if t_first > 1 else ''} {t1 - t0:.1f} s excluded",
+                lanczos_matvecs_per_s=matvecs / (t2 - t1), seconds=t2 - t1, t_window=[t_first, t_last])
+
+
+def cpu_baseline_block(cfg, L, gpu_window_rate=None):
+    """The oracle on all host cores over the workload's window, the same at 1 thread on a
+    bounded prefix of it, the host description, and the GPU rate over the same window beside it."""
+    tw = ORACLE_WINDOW.get(cfg, 10)
+    allc = cpu_oracle_sample(cfg, L, tw, threads=0)
+    one = cpu_oracle_sample(cfg, L, min(tw, 2 if cfg in ("c3", "c4") else tw), threads=1)
+    cb = {k: allc[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    cb["one_thread"] = {k: one[k] for k in ("value", "unit", "cores", "sample")}
+    cb["host"] = host_info()
+    cb["t_window"] = allc["t_window"]
+    if gpu_window_rate is not None:
+        cb["gpu_same_window"] = {"value": gpu_window_rate, "unit": "iterations/s", "t_window": [1, tw],
+                                 "note": "fresh context, CUDA events around sketchycgal_step over t=1..%d" % tw}
+        cb["gpu_over_oracle_all_cores"] = gpu_window_rate / allc["value"]
+    return cb
 
 
 def run_reference(args, rank, world):
@@ -126,15 +167,18 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     L = si.laplacian(args.config)
+    # the same window as our arm (t = W+1 ..), bounded: W untimed iterations, then at most --ref-iters
+    # timed ones, on all host cores
     iters = max(1, min(args.steps, args.ref_iters))
-    cb = cpu_oracle_sample(args.config, L, iters)
+    cb = cpu_oracle_sample(args.config, L, args.warmup + iters, threads=0, t_first=args.warmup + 1)
+    cb["host"] = host_info()
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "iterations/s", "n_gpus": world,
-            "steps": iters, "warmup": 0, "ms_per_step": 1e3 / cb["value"], "higher_is_better": True,
+            "steps": iters, "warmup": args.warmup, "ms_per_step": 1e3 / cb["value"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             # same workload/config as our arm (t = W+1..W+K); the bounded sample actually timed is
             # described in cpu_baseline.sample
             "config": _config_dict(args.config, L, world, args.warmup + 1, args.warmup + args.steps),
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "host")},
             "e2e": {"value": cb["value"], "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -230,8 +274,8 @@ def run_ours(args, rank, world, local_rank):
         e2e = run_e2e(scg, si, L, c, K, W, local_rank, dkw, world)
     cb = None
     if rank == 0 and not args.no_cpu:
-        cb = cpu_oracle_sample(args.config, L, args.ref_iters)
-        cb = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        gw = gpu_window_rate(scg, L, c, ORACLE_WINDOW.get(args.config, 10), local_rank) if world == 1 else None
+        cb = cpu_baseline_block(args.config, L, gw)
     line = {"metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": _config_dict(args.config, L, world, W + 1, W + K),
@@ -248,6 +292,23 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
+
+
+def gpu_window_rate(scg, L, c, tw, dev):
+    """GPU iterations/s over t = 1..tw (a fresh context; CUDA events on its stream)."""
+    import torch
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        s = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], device=dev, stream=ctypes_stream(stream))
+        s.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s.step(tw)
+        e1.record(stream)
+        e1.synchronize()
+        s.synchronize()
+        s.close()
+    return tw / (e0.elapsed_time(e1) / 1e3)
 
 
 def ctypes_stream(stream):
@@ -307,7 +368,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-iters", type=int, default=1)
+    ap.add_argument("--ref-iters", type=int, default=5, help="--impl reference: timed oracle iterations")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="no per-kernel events (no roofline line)")

@@ -205,6 +205,14 @@ scg_status sketchycgal_maxcut_alpha_doubling(scg_ctx **out, const scg_csr *L, in
  * w = min(max(z + y / beta, lo), hi); the gap / bound records are NaN. */
 scg_status sketchycgal_set_box(scg_ctx *c, double lo, double hi);
 
+/* Fixed Lanczos bound: every later iteration runs Alg. 2 with q instead of the schedule
+ * q_t = min(n - 1, max(2, ceil(t^(1/4) ln n))) (ApproxMinEvec takes q as an input, PAPER.md:1068-1086;
+ * Fact 4.1, gives the q for a target accuracy).  q = 0 restores the schedule.
+ * 1 <= q <= min(n, 255) (q = n spans the full Krylov space, SPEC-style exact checks).
+ * Errors: SCG_EINVAL.  (sketchycgal_step returns SCG_EUNSUPPORTED instead of truncating when the
+ * schedule's q_t exceeds the device bound 255: t > 47,000 iterations at n = 2^25.) */
+scg_status sketchycgal_set_lanczos_q(scg_ctx *c, int32_t q);
+
 /* Block until all queued work is done; reports deferred device errors. */
 scg_status sketchycgal_synchronize(scg_ctx *c);
 

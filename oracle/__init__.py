@@ -43,8 +43,8 @@ def build(force: bool = False) -> str:
             and os.path.getmtime(_LIB) >= max(os.path.getmtime(src), os.path.getmtime(hdr))):
         return _LIB
     tmp = _LIB + f".tmp{os.getpid()}"
-    subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math",
-                           src, "-o", tmp, "-lm"])
+    subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off",
+                           "-fno-fast-math", src, "-o", tmp, "-lm"])
     os.replace(tmp, _LIB)
     return _LIB
 
@@ -81,12 +81,20 @@ def _load():
         lib.oracle_scalar.restype = D
         lib.oracle_scalar.argtypes = [P, ctypes.c_int]
         lib.oracle_get.argtypes = [P, ctypes.c_int, P]
+        lib.oracle_set_threads.restype = ctypes.c_int
+        lib.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = lib
     return _lib
 
 
 def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def set_threads(n: int = 0) -> int:
+    """OpenMP threads of the oracle's row loops and exact sums (n <= 0: all cores).  The thread
+    count never changes a bit of any result (exact sums; independent rows)."""
+    return int(_load().oracle_set_threads(int(n)))
 
 
 # ---------------------------------------------------------------- primitives
@@ -169,9 +177,9 @@ def lanczos(n, rp, col, m, d, g, q) -> LanczosResult:
     col = np.ascontiguousarray(col, dtype=np.int32)
     m, d, g = _f64(m), _f64(d), _f64(g)
     v = np.zeros(n)
-    om = np.zeros(128)
-    rh = np.zeros(128)
-    sv = np.zeros(128)
+    om = np.zeros(int(q) + 1)
+    rh = np.zeros(int(q) + 1)
+    sv = np.zeros(int(q) + 1)
     th = D()
     k = ctypes.c_int()
     rc = _load().oracle_lanczos(n, rp.ctypes.data, col.ctypes.data, m.ctypes.data, d.ctypes.data, g.ctypes.data,
@@ -192,7 +200,7 @@ class Oracle:
 
     def __init__(self, L, R: int, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
                  scale: bool = True, qfix: int = 0, logcap: int = 0, vhist: int = 0, trace_le: bool = False,
-                 ineq: bool = False, box: tuple | None = None):
+                 ineq: bool = False, box: tuple | None = None, div_norm: bool = False):
         self.L = L
         self.n = L.n
         self.R = int(R)
@@ -206,7 +214,7 @@ class Oracle:
         self._h = _load().oracle_create(self.n, self._rp.ctypes.data, self._col.ctypes.data, self._val.ctypes.data,
                                         self.R, self.alpha_orig, float(beta0), int(seed), 1 if scale else 0,
                                         int(qfix), self.logcap, self.vhist_cap,
-                                        (1 if trace_le else 0) | (2 if ineq else 0))
+                                        (1 if trace_le else 0) | (2 if ineq else 0) | (4 if div_norm else 0))
         self.trace_le = bool(trace_le)
         self.ineq = bool(ineq) or box is not None
         if box is not None:  # K = {lo <= u <= hi}, original units

@@ -7,7 +7,10 @@
  * and this file shares no code with the CUDA path; the only common source is
  * the seeded input stream scg_inputs/include/scg_rng.h (random inputs only).
  *
- * Plain, slow, fp64, single-threaded.  Every function follows the paper
+ * Plain, slow, fp64.  OpenMP only splits independent row loops and the exact sums
+ * (CAC-2 sums are exact integers, so any split gives the same bits; the thread count
+ * never changes a result -- tests/test_oracle_pins.py checks 1 vs all threads).
+ * Every function follows the paper
  * (arXiv 1912.02949, /root/reference/PAPER.md, cited as P:<line>) step by step,
  * in the paper's order and notation, with the readings and the Canonical
  * Arithmetic Contract (CAC) written down in DESIGN.md section 3.  The CAC
@@ -31,6 +34,7 @@
  * math.fsum, loop invariants, brute-force cuts).
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -131,21 +135,46 @@ static double xs_round(xsum_t *a) {
   return neg ? -res : res;
 }
 
-/* CAC-2 dot product. */
+/* Add the exact value of b into a (integers: exact; both carried first so no digit overflows). */
+static void xs_merge(xsum_t *a, xsum_t *b) {
+  xs_carry(a);
+  xs_carry(b);
+  for (int i = 0; i < XS_LIMBS; ++i) a->d[i] += b->d[i];
+  a->err |= b->err;
+  a->adds = 0;
+}
+
+/* CAC-2 dot product: the exact sum of the rounded products fl(a_r b_r), rounded once.
+ * b == NULL: the exact sum of a.  Threads sum disjoint row ranges exactly and the partial
+ * integers are added exactly, so the result does not depend on the thread count. */
 static double o_dot(const double *a, const double *b, int64_t n, int *err) {
   xsum_t s;
   xs_init(&s);
-  for (int64_t r = 0; r < n; ++r) xs_add(&s, a[r] * b[r]);
+#pragma omp parallel if (n > 65536)
+  {
+    xsum_t part;
+    xs_init(&part);
+#pragma omp for schedule(static)
+    for (int64_t r = 0; r < n; ++r) xs_add(&part, b ? a[r] * b[r] : a[r]);
+#pragma omp critical
+    xs_merge(&s, &part);
+  }
   if (s.err && err) *err = 1;
   return xs_round(&s);
 }
 
 double oracle_xsum(const double *p, int64_t n, int *err) {
-  xsum_t s;
-  xs_init(&s);
-  for (int64_t r = 0; r < n; ++r) xs_add(&s, p[r]);
-  if (err) *err = s.err;
-  return xs_round(&s);
+  int e = 0;
+  double r = o_dot(p, NULL, n, &e);
+  if (err) *err = e;
+  return r;
+}
+
+/* Threads of the OpenMP loops (n <= 0: all cores); returns the count in effect. */
+int oracle_set_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+  else omp_set_num_threads(omp_get_num_procs());
+  return omp_get_max_threads();
 }
 
 double oracle_dot(const double *a, const double *b, int64_t n) { return o_dot(a, b, n, NULL); }
@@ -167,6 +196,7 @@ typedef struct {
  * off = 16, 8, 4, 2, 1 and l < off; the row is fl(fl(d_r x_r) + L[0]). */
 #define O_LONG_ROW 32
 static void o_apply(const o_off *A, const double *d, const double *x, double *y) {
+#pragma omp parallel for schedule(static, 4096) if (A->n > 65536)
   for (int64_t r = 0; r < A->n; ++r) {
     const int64_t a = A->rp[r], b = A->rp[r + 1];
     if (b - a <= O_LONG_ROW) {
@@ -224,7 +254,9 @@ static double o_pow2_of(double a) { /* 2^floor(log2 a) for normal a > 0 (exact) 
 int oracle_tridiag_mineig(const double *om, const double *rho, int k, double *theta, double *s) {
   if (k <= 0) return -1;
   if (k == 1) { *theta = om[0]; s[0] = 1.0; return 0; }
-  double rho2[128];
+  double *rho2 = (double *)malloc(sizeof(double) * (size_t)k * 8);
+  double *u0 = rho2 + k, *u1 = u0 + k, *u2 = u1 + k, *mul = u2 + k, *x = mul + k;
+  int *swp = (int *)malloc(sizeof(int) * (size_t)k);
   double lo = 0.0, hi = 0.0, NT = 0.0;
   for (int j = 0; j < k - 1; ++j) rho2[j] = rho[j] * rho[j];
   for (int j = 0; j < k; ++j) {
@@ -236,7 +268,12 @@ int oracle_tridiag_mineig(const double *om, const double *rho, int k, double *th
     if (j == 0 || b > hi) hi = b;
   }
   NT = fabs(lo) > fabs(hi) ? fabs(lo) : fabs(hi);
-  if (NT == 0.0) { *theta = 0.0; for (int j = 0; j < k; ++j) s[j] = j == 0 ? 1.0 : 0.0; return 0; }
+  if (NT == 0.0) {
+    *theta = 0.0;
+    for (int j = 0; j < k; ++j) s[j] = j == 0 ? 1.0 : 0.0;
+    free(rho2); free(swp);
+    return 0;
+  }
   double pad = NT * 0x1p-20;
   lo = lo - pad;
   hi = hi + pad;
@@ -258,8 +295,6 @@ int oracle_tridiag_mineig(const double *om, const double *rho, int k, double *th
   *theta = th;
   /* inverse iteration: Gaussian elimination with partial pivoting of T - theta I
    * (rows swapped when the sub-diagonal entry is larger), U has three diagonals. */
-  double u0[128], u1[128], u2[128], mul[128], x[128];
-  int swp[128];
   double tiny = NT * 0x1p-60;
   double c0 = om[0] - th, c1 = k > 1 ? rho[0] : 0.0, c2 = 0.0;
   for (int i = 0; i < k - 1; ++i) {
@@ -299,32 +334,46 @@ int oracle_tridiag_mineig(const double *om, const double *rho, int k, double *th
   int jm = 0;
   for (int j = 1; j < k; ++j) if (fabs(s[j]) > fabs(s[jm])) jm = j;
   if (s[jm] < 0.0) for (int j = 0; j < k; ++j) s[j] = -s[j];
+  free(rho2); free(swp);
   return 0;
 }
 
 /* ------------------------------------------------------------------------- */
 /* Alg. 2 ApproxMinEvec, two passes.
  * g: the randn start vector of line 1; q: the iteration bound (callers pass
- * min{q_t, n-1}, line 3).  Outputs theta (xi of line 12 = Ritz value), v (line
- * 13, explicitly normalized: reading A6), k, omega[k], rho[k-1]. */
+ * min{q_t, n-1}, line 3; there is no other cap).  Outputs theta (xi of line 12 = Ritz
+ * value), v (line 13, explicitly normalized: reading A6), k, omega[k], rho[k-1].
+ * div_norm = 0: a normalization "v / rho" is evaluated as v * fl(1/rho) (reading R26, the
+ * contract the GPU path shares); div_norm = 1: as the printed division v / rho per entry
+ * (tests pin R26 against this literal form). */
 typedef struct {
   double theta;
   int k;
   int err;
-  double omega[128];
-  double rho[128];
-  double svec[128];
+  double *omega, *rho, *svec; /* q entries each */
 } o_lanczos_res;
 
+static void o_res_alloc(o_lanczos_res *res, int q) {
+  memset(res, 0, sizeof(*res));
+  res->omega = (double *)calloc((size_t)q + 1, sizeof(double));
+  res->rho = (double *)calloc((size_t)q + 1, sizeof(double));
+  res->svec = (double *)calloc((size_t)q + 1, sizeof(double));
+}
+static void o_res_free(o_lanczos_res *res) { free(res->omega); free(res->rho); free(res->svec); }
+
+/* v[r] / rho for the chosen normalization form */
+#define O_NORM(v, rho, rrho, div_norm) ((div_norm) ? (v) / (rho) : (v) * (rrho))
+
 static void o_lanczos(const o_off *A, const double *d, const double *g, int q, double *v,
-                      double *w1, double *w2, double *w3, double *a, o_lanczos_res *res) {
+                      double *w1, double *w2, double *w3, double *a, o_lanczos_res *res, int div_norm) {
   int64_t n = A->n;
   int err = 0;
   double *vprev = w1, *vcur = w2, *vnext = w3;
   /* lines 1-2: v1 = randn / ||randn|| */
   double nu0 = sqrt(o_dot(g, g, n, &err));
-  double rnu0 = 1.0 / nu0; /* v / rho is evaluated as v * fl(1/rho) (reading R26) */
-  for (int64_t r = 0; r < n; ++r) vcur[r] = g[r] * rnu0;
+  double rnu0 = 1.0 / nu0;
+#pragma omp parallel for schedule(static) if (n > 65536)
+  for (int64_t r = 0; r < n; ++r) vcur[r] = O_NORM(g[r], nu0, rnu0, div_norm);
   int k = q;
   for (int i = 1; i <= q; ++i) {
     o_apply(A, d, vcur, a);                            /* M v_i */
@@ -332,6 +381,7 @@ static void o_lanczos(const o_off *A, const double *d, const double *g, int q, d
     if (i == q) { k = q; break; }                       /* reading A2: last step needs no v_{i+1} */
     double om = res->omega[i - 1];
     double rp = i >= 2 ? res->rho[i - 2] : 0.0;
+#pragma omp parallel for schedule(static) if (n > 65536)
     for (int64_t r = 0; r < n; ++r) {                   /* line 6: three-term recurrence */
       double w = fma(-om, vcur[r], a[r]);
       if (i >= 2) w = fma(-rp, vprev[r], w);
@@ -341,7 +391,8 @@ static void o_lanczos(const o_off *A, const double *d, const double *g, int q, d
     res->rho[i - 1] = rho;
     if (rho <= 0x1p-45 * (fabs(om) + rp)) { k = i; break; } /* line 8 (reading A3) */
     double rrho = 1.0 / rho;
-    for (int64_t r = 0; r < n; ++r) vnext[r] = vnext[r] * rrho; /* line 9 */
+#pragma omp parallel for schedule(static) if (n > 65536)
+    for (int64_t r = 0; r < n; ++r) vnext[r] = O_NORM(vnext[r], rho, rrho, div_norm); /* line 9 */
     double *t = vprev; vprev = vcur; vcur = vnext; vnext = t;
   }
   res->k = k;
@@ -349,23 +400,31 @@ static void o_lanczos(const o_off *A, const double *d, const double *g, int q, d
   oracle_tridiag_mineig(res->omega, res->rho, k, &res->theta, res->svec);
   /* line 13, regenerating v_2..v_k (second pass) */
   vprev = w1; vcur = w2; vnext = w3;
-  for (int64_t r = 0; r < n; ++r) vcur[r] = g[r] * rnu0;
-  for (int64_t r = 0; r < n; ++r) v[r] = res->svec[0] * vcur[r];
+#pragma omp parallel for schedule(static) if (n > 65536)
+  for (int64_t r = 0; r < n; ++r) {
+    vcur[r] = O_NORM(g[r], nu0, rnu0, div_norm);
+    v[r] = res->svec[0] * vcur[r];
+  }
   for (int i = 1; i < k; ++i) {
     o_apply(A, d, vcur, a);
     double om = res->omega[i - 1];
     double rp = i >= 2 ? res->rho[i - 2] : 0.0;
-    double rrho = 1.0 / res->rho[i - 1];
+    double rho = res->rho[i - 1];
+    double rrho = 1.0 / rho;
+    double si = res->svec[i];
+#pragma omp parallel for schedule(static) if (n > 65536)
     for (int64_t r = 0; r < n; ++r) {
       double w = fma(-om, vcur[r], a[r]);
       if (i >= 2) w = fma(-rp, vprev[r], w);
-      vnext[r] = w * rrho;
+      vnext[r] = O_NORM(w, rho, rrho, div_norm);
+      v[r] = fma(si, vnext[r], v[r]);
     }
-    for (int64_t r = 0; r < n; ++r) v[r] = fma(res->svec[i], vnext[r], v[r]);
     double *t = vprev; vprev = vcur; vcur = vnext; vnext = t;
   }
-  double rnx = 1.0 / sqrt(o_dot(v, v, n, &err));
-  for (int64_t r = 0; r < n; ++r) v[r] = v[r] * rnx;
+  double nx = sqrt(o_dot(v, v, n, &err));
+  double rnx = 1.0 / nx;
+#pragma omp parallel for schedule(static) if (n > 65536)
+  for (int64_t r = 0; r < n; ++r) v[r] = O_NORM(v[r], nx, rnx, div_norm);
   res->err = err;
 }
 
@@ -373,18 +432,20 @@ static void o_lanczos(const o_off *A, const double *d, const double *g, int q, d
 int oracle_lanczos(int64_t n, const int64_t *rp, const int32_t *col, const double *m, const double *d,
                    const double *g, int q, double *v, double *theta, int *k, double *omega, double *rho,
                    double *svec) {
-  if (q < 1 || q > 127) return -1;
+  if (q < 1) return -1;
   o_off A = {n, rp, col, m};
   double *buf = (double *)malloc(sizeof(double) * (size_t)n * 4);
   o_lanczos_res res;
-  memset(&res, 0, sizeof(res));
-  o_lanczos(&A, d, g, q, v, buf, buf + n, buf + 2 * n, buf + 3 * n, &res);
+  o_res_alloc(&res, q);
+  o_lanczos(&A, d, g, q, v, buf, buf + n, buf + 2 * n, buf + 3 * n, &res, 0);
   free(buf);
   *theta = res.theta;
   *k = res.k;
   for (int j = 0; j < res.k; ++j) { omega[j] = res.omega[j]; svec[j] = res.svec[j]; }
   for (int j = 0; j + 1 < res.k; ++j) rho[j] = res.rho[j];
-  return res.err ? -2 : 0;
+  int rc = res.err ? -2 : 0;
+  o_res_free(&res);
+  return rc;
 }
 
 /* ------------------------------------------------------------------------- */
@@ -395,7 +456,6 @@ int oracle_qt(int64_t t, int64_t n) {
   int64_t q = (int64_t)ceil(x);
   if (q < 2) q = 2;
   if (q > n - 1) q = n - 1;
-  if (q > 127) q = 127;
   return (int)q;
 }
 
@@ -422,6 +482,7 @@ typedef struct {
   int trace_le; /* tr X <= alpha: H = alpha v v* if xi < 0, else 0 */
   int ineq;     /* general template with a box K = {lo <= u <= hi} */
   double lo, hi; /* scaled units; bit 1 of the mode (SCG_INEQ): lo = -inf, hi = b */
+  int div_norm; /* bit 2 of the mode: normalizations as printed divisions (R26 pin, see o_lanczos) */
   uint64_t seed;
   int qfix; /* test-only: fixed Lanczos bound (may be n); 0 = schedule */
   int64_t t; /* iterations done */
@@ -449,6 +510,7 @@ void *oracle_create(int64_t n, const int64_t *rp_L, const int32_t *col_L, const 
   o->n = n; o->R = R; o->beta0 = beta0; o->seed = seed; o->scale = scale; o->qfix = qfix;
   o->trace_le = trace_le & 1;      /* bit 0: trace-bounded set */
   o->ineq = (trace_le >> 1) & 1;    /* bit 1: inequality constraints A X <= b */
+  o->div_norm = (trace_le >> 2) & 1; /* bit 2: literal division v / rho (test-only, reading R26) */
   o->alpha_orig = alpha;
   /* ||C||_F = ||L||_F over all stored entries (CAC-2), scaling P:1805-1814 (reading A13) */
   int err = 0;
@@ -498,6 +560,7 @@ void *oracle_create(int64_t n, const int64_t *rp_L, const int32_t *col_L, const 
   o->Omega = (double *)malloc(sizeof(double) * (size_t)n * R);
   /* NystromSketch.Init (Alg. 3 line 2): Omega column-major, reading A8 */
   for (int32_t kk = 0; kk < R; ++kk)
+#pragma omp parallel for schedule(static) if (n > 65536)
     for (int64_t i = 0; i < n; ++i) o->Omega[(int64_t)kk * n + i] = scg_omega(seed, i, kk);
   o->logcap = logcap;
   o->log = (double *)calloc((size_t)(logcap > 0 ? logcap : 1) * O_LOGW, sizeof(double));
@@ -558,14 +621,15 @@ int oracle_step(void *h, int64_t T) {
     /* line 6: D = C + A*(y + beta (z - b)) ; diagonal of D (primitive 2).
      * General template, K = {u <= b}: b is replaced by the slack
      * w_t = proj_K(z_t + y_t / beta_t) = min(max(z_t + y_t / beta_t, lo), hi), elementwise (R32). */
+#pragma omp parallel for schedule(static) if (n > 65536)
     for (int64_t r = 0; r < n; ++r) {
       const double wr = o->ineq ? fmin(fmax(o->z[r] + o->y[r] / beta, o->lo), o->hi) : o->bval;
       o->d[r] = fma(beta, o->z[r] - wr, o->y[r]) + o->cdiag[r];
+      o->g[r] = scg_lanczos_start(o->seed, t, r);
     }
-    for (int64_t r = 0; r < n; ++r) o->g[r] = scg_lanczos_start(o->seed, t, r);
     o_lanczos_res res;
-    memset(&res, 0, sizeof(res));
-    o_lanczos(&A, o->d, o->g, q, o->v, o->w1, o->w2, o->w3, o->a, &res);
+    o_res_alloc(&res, q);
+    o_lanczos(&A, o->d, o->g, q, o->v, o->w1, o->w2, o->w3, o->a, &res, o->div_norm);
     o->err |= res.err;
     /* monitors: xi = v* D v (eqn 5.1), c = v* C v (p update) */
     int err = 0;
@@ -578,6 +642,7 @@ int oracle_step(void *h, int64_t T) {
      * (xi is the Rayleigh quotient approximating lambda_min) */
     const int hoff = o->trace_le && !(xi < 0.0);
     /* line 7: z <- (1 - eta) z + eta A(H)  (primitive 3) */
+#pragma omp parallel for schedule(static) if (n > 65536)
     for (int64_t r = 0; r < n; ++r) {
       double h = o->alpha * (o->v[r] * o->v[r]);
       o->z[r] = hoff ? one_m_eta * o->z[r] : fma(eta, h, one_m_eta * o->z[r]);
@@ -586,18 +651,21 @@ int oracle_step(void *h, int64_t T) {
      * b is replaced by wbar_t = proj_K(z_{t+1} + y_t / beta_{t+1}) and the step rule keeps the
      * form gamma ||z - wbar||^2 <= beta_t eta_t^2 alpha^2 ||A||^2 (reading R32). */
     const double beta1 = o->beta0 * sqrt((double)(t + 2));
+#pragma omp parallel for schedule(static) if (n > 65536)
     for (int64_t r = 0; r < n; ++r) {
       const double wb = o->ineq ? fmin(fmax(o->z[r] + o->y[r] / beta1, o->lo), o->hi) : o->bval;
       o->a[r] = o->z[r] - wb;
     }
     double nz = o_dot(o->a, o->a, n, &err);
     double gamma = oracle_gamma(t, o->alpha, o->beta0, nz);
+#pragma omp parallel for schedule(static) if (n > 65536)
     for (int64_t r = 0; r < n; ++r) o->y[r] = fma(gamma, o->a[r], o->y[r]);
     /* line 9: NystromSketch.RankOneUpdate(sqrt(alpha) v, eta): S <- (1-eta) S + eta alpha v (v* Omega) */
     for (int kk = 0; kk < R; ++kk) {
       double gk = o_dot(o->v, o->Omega + (int64_t)kk * n, n, &err);
       double c = hoff ? 0.0 : (eta * o->alpha) * gk;
       double *Sk = o->S + (int64_t)kk * n;
+#pragma omp parallel for schedule(static) if (n > 65536)
       for (int64_t r = 0; r < n; ++r) Sk[r] = fma(c, o->v[r], one_m_eta * Sk[r]);
     }
     /* tau, p */
@@ -622,6 +690,7 @@ int oracle_step(void *h, int64_t T) {
       if (o->ineq) L[10] = L[11] = NAN; /* the gap / bound formulas are for A X = b (reading R32) */
     }
     if (o->vhist && t - 1 < o->vhist_cap) memcpy(o->vhist + (t - 1) * n, o->v, sizeof(double) * (size_t)n);
+    o_res_free(&res);
     o->t = t;
   }
   return o->err ? -2 : 0;

@@ -103,7 +103,7 @@ EXPORTS = ["sketchycgal_maxcut_init", "sketchycgal_step", "sketchycgal_synchroni
            "sketchycgal_kernel_stats", "sketchycgal_reset_stats", "sketchycgal_nccl_unique_id",
            "sketchycgal_row_splits", "sketchycgal_halo_plan", "sketchycgal_run",
            "sketchycgal_selftest_division", "sketchycgal_last_error", "sketchycgal_destroy",
-           "sketchycgal_maxcut_alpha_doubling", "sketchycgal_set_box"]
+           "sketchycgal_maxcut_alpha_doubling", "sketchycgal_set_box", "sketchycgal_set_lanczos_q"]
 
 _lib = None
 
@@ -132,6 +132,8 @@ def open_library(path: str = LIB_PATH):
     lib.sketchycgal_reset_stats.argtypes = [P]
     lib.sketchycgal_run.restype = ctypes.c_int
     lib.sketchycgal_run.argtypes = [P, I64, D, I64, ctypes.POINTER(I64)]
+    lib.sketchycgal_set_lanczos_q.restype = ctypes.c_int
+    lib.sketchycgal_set_lanczos_q.argtypes = [P, I32]
     lib.sketchycgal_set_box.restype = ctypes.c_int
     lib.sketchycgal_set_box.argtypes = [P, D, D]
     lib.sketchycgal_maxcut_alpha_doubling.restype = ctypes.c_int
@@ -229,7 +231,7 @@ class SketchyCGAL:
                  stream=None, regenerate: bool = False, trace_le: bool = False, shards: int = 1, splits=None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None, ineq: bool = False,
                  box: tuple | None = None, pdl: bool = True, fused_pass1: bool = False, ws_spmv: bool = False,
-                 tma_b: bool = False, debug_log: bool = False):
+                 tma_b: bool = False, debug_log: bool = False, qfix: int = 0):
         self.lib = load()
         self.n = int(L.n)
         self.R = int(R)
@@ -271,6 +273,8 @@ class SketchyCGAL:
                                               flags, dptr, int(device), stream)
         if st != 0:
             raise ScgError(f"sketchycgal_maxcut_init: {STATUS.get(st, st)}")
+        if qfix:  # fixed Lanczos bound (Alg. 2 input q) instead of the q_t schedule
+            self._check(self.lib.sketchycgal_set_lanczos_q(self._h, int(qfix)), "sketchycgal_set_lanczos_q")
         if box is not None:  # K = {lo <= u <= hi}
             self._check(self.lib.sketchycgal_set_box(self._h, float(box[0]), float(box[1])), "sketchycgal_set_box")
 

@@ -20,7 +20,8 @@
 
 namespace scg {
 
-constexpr int kMaxQ = 128;   // Lanczos bound cap (max q_t in configs[0..4] is 94)
+constexpr int kMaxQ = 256;   // device arrays hold q <= kMaxQ - 1 = 255 Lanczos steps (q_t of configs[0..4]
+                             // is <= 94; a larger q_t is an SCG_EUNSUPPORTED error, never truncated)
 constexpr int kMaxR = 64;    // sketch rank cap (BASELINE: R <= 50)
 constexpr int kBlock = 256;
 constexpr int kBlockA = 256;  // threads per block of k_lanczos_a (the SpMV of pass 1)

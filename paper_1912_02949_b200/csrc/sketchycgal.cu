@@ -159,6 +159,7 @@ struct scg_ctx {
   // regenerate mode: slots 1, 2 = ring of w_i
   int wcap = 0;
   bool store = true;
+  int qfix = 0;  // > 0: fixed Lanczos bound instead of the q_t schedule (sketchycgal_set_lanczos_q)
   // deferred sketch updates (k_sketch_flush): iterations pending, their 1 - eta, last v slot
   int spend = 0, vlast = 0;
   double ome[kSketchB] = {0};
@@ -1134,22 +1135,25 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
       return bad(st);
   }
   tick("shards");
-  // Lanczos vector storage.  One rank: grown on demand.  Sharded: fixed at init (peers map it).
+  // Lanczos vector storage.  One rank: grown on demand.  Sharded: fixed at init (peers map it),
+  // sized for q_t up to t = 1000 (+16); a later q_t above it switches every rank to the two-pass
+  // form (bitwise the same iterates) in sketchycgal_step.
   c->store = (flags & SCG_REGENERATE) == 0;
   int cap = 3;
+  int64_t q1000 = (int64_t)std::ceil(std::sqrt(std::sqrt(1000.0)) * c->lnN);
+  q1000 = std::min<int64_t>(std::min<int64_t>(q1000, n - 1), kMaxQ - 1);
   if (world == 1 && c->store) {  // pre-size the store for q_t up to t = 1000 when it fits comfortably
-    int64_t q1000 = (int64_t)std::ceil(std::sqrt(std::sqrt(1000.0)) * c->lnN);
-    q1000 = std::min<int64_t>(std::min<int64_t>(q1000, n - 1), kMaxQ - 1);
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
     const size_t need = sizeof(double) * (size_t)c->npad * (size_t)(q1000 + 2);
     if (2 * need < fr) cap = (int)std::max<int64_t>(3, q1000 + 1);
   }
   if (world > 1 && c->store) {
+    const int64_t want = std::max<int64_t>(3, std::min<int64_t>(q1000 + 16, kMaxQ - 1));
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
-    const size_t need = sizeof(double) * (size_t)c->npad * (size_t)kMaxQ * nshard;
-    if (need + (size_t)(2ull << 30) < fr) cap = kMaxQ - 1;
+    const size_t need = sizeof(double) * (size_t)c->npad * (size_t)(want + 1) * nshard;
+    if (need + (size_t)(2ull << 30) < fr) cap = (int)want;
     else c->store = false;  // (multi-process: every rank must decide alike, checked after connect_peers)
   }
   c->wcap = cap;
@@ -1247,8 +1251,12 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     int64_t q = (int64_t)std::ceil(std::sqrt(std::sqrt((double)t)) * c->lnN);
     if (q < 2) q = 2;
     if (q > c->n - 1) q = c->n - 1;
-    if (q > kMaxQ - 1) q = kMaxQ - 1;
+    if (c->qfix > 0) q = c->qfix;  // sketchycgal_set_lanczos_q: fixed bound (Alg. 2 input q)
+    if (q > kMaxQ - 1)  // the device arrays hold kMaxQ - 1 Lanczos steps: never truncate silently
+      return fail(c, SCG_EUNSUPPORTED, "Lanczos bound q_t = " + std::to_string(q) + " exceeds the device bound " +
+                                           std::to_string(kMaxQ - 1) + " at t = " + std::to_string(t));
     A.q = (int)q;
+    if (!P1 && c->store && c->wcap < q) c->store = false;  // sharded store (peer-mapped) too small: two-pass
     if (P1 && c->store && c->wcap < q) {  // grow the Lanczos-vector store (slot 0 = g is kept)
       const int cap = (int)std::min<int64_t>(q + 16, kMaxQ - 1);
       size_t fr = 0, tot = 0;
@@ -1737,6 +1745,12 @@ scg_status sketchycgal_maxcut_alpha_doubling(scg_ctx **out, const scg_csr *L, in
     alpha = 2.0 * alpha;  // step 4
   }
   *out = prev;
+  return SCG_OK;
+}
+
+scg_status sketchycgal_set_lanczos_q(scg_ctx *c, int32_t q) {
+  if (!c || q < 0 || q > kMaxQ - 1 || q > c->n) return SCG_EINVAL;
+  c->qfix = q;
   return SCG_OK;
 }
 

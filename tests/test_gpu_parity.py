@@ -135,6 +135,27 @@ def test_launch_policy_forced_bitwise(gpu, cfg, T, pdl):
     _assert_trajectory(g, o, T)
 
 
+@pytest.mark.parametrize("cfg,T", [("c0", 200), ("c3", 1)])
+def test_tma_staged_recurrence_bitwise(gpu, cfg, T):
+    """The opt-in TMA-staged recurrence kernel (SCG_TMA_B) gives the same bitwise trajectory."""
+    L = si.laplacian(cfg)
+    c = si.CONFIGS[cfg]
+    g, o = _run_pair(gpu, L, c["R"], T, seed=c["seed"], tma_b=True)
+    _assert_trajectory(g, o, T)
+
+
+def test_sketch_rank_50(gpu):
+    """R = 50 (BASELINE allows R <= 50) on configs[0]: the g = v^T Omega column loop in chunks of 16,
+    the deferred sketch flush and the R x R reconstruction core at their largest."""
+    L = si.laplacian("c0")
+    T = 150
+    g, o = _run_pair(gpu, L, 50, T, seed=0)
+    _assert_trajectory(g, o, T)
+    U, lam, _ = g.reconstruct()
+    Uo, lam_o, _ = oracle.nystrom_reconstruct(o.S, o.Omega, o.tau)
+    np.testing.assert_allclose(lam, oracle.trace_correct(lam_o, o.alpha) * (L.n / o.alpha), rtol=1e-8)
+
+
 @pytest.mark.parametrize("cfg,T", [("c0", 300), ("c3", 1)])
 def test_warp_specialized_spmv_engine_bitwise(gpu, cfg, T):
     """The opt-in warp-specialized TMA k_lanczos_a (SCG_WS_SPMV: producer warp + mbarrier ring)
@@ -260,6 +281,17 @@ def test_sharded_config0_trajectory_and_cut(gpu, P):
     U1, lam1, _ = one.reconstruct()
     U, lam, _ = g.reconstruct()
     np.testing.assert_allclose(lam, lam1, rtol=1e-9)
+    # the sharded reconstruction against the oracle's (Alg. 3 with LAPACK), not only the 1-GPU path
+    Uo, lam_o, _ = oracle.nystrom_reconstruct(o.S, o.Omega, o.tau)
+    lam_tc = oracle.trace_correct(lam_o, o.alpha) * (L.n / o.alpha)
+    np.testing.assert_allclose(lam, lam_tc, rtol=1e-9)
+    assert abs(g.objective()[1] - oracle.objective_hat(L, Uo, lam_tc)) <= 1e-6 * oracle.objective_hat(L, Uo, lam_tc)
+    f_o = oracle.feasibility_hat(Uo, lam_tc)
+    assert abs(g.feasibility()[1] - f_o[0]) <= 1e-6 * f_o[0]
+    chi_o, w_o, _ = oracle.round_cut(L, Uo)
+    chi_g, w_g = g.round()
+    np.testing.assert_array_equal(chi_g, chi_o)
+    assert w_g == w_o
     np.testing.assert_allclose(g.objective(), one.objective(), rtol=1e-9)
     np.testing.assert_allclose(g.feasibility(), one.feasibility(), rtol=1e-9)
     chi, w = g.round()

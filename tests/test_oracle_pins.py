@@ -601,3 +601,149 @@ def test_box_constraint_set_closed_forms():
     i2.step(300)
     np.testing.assert_array_equal(i1.log, i2.log)
     np.testing.assert_array_equal(i1.y, i2.y)
+
+
+# ------------------------------------------------------------- one-shot metrics
+def test_objective_and_feasibility_hat_bipartite_cut_closed_form():
+    """X^ = chi chi^T for a cut chi of a bipartite graph with every edge crossing: tr(L X^) = chi^T L chi
+    = sum_E w (chi_i - chi_j)^2 = 4 sum w (eqn:comb-laplacian P:97-100) and diag X^ = 1, so both
+    infeasibility normalizations are 0 (BASELINE)."""
+    rng = np.random.default_rng(4)
+    a, b = 7, 9
+    edges = [(i, a + j) for i in range(a) for j in range(b) if rng.random() < 0.5]
+    i, j = zip(*edges)
+    w = rng.uniform(0.5, 2.0, size=len(edges))
+    L = si.laplacian_from_edges(a + b, i, j, w)
+    chi = np.array([1.0] * a + [-1.0] * b)
+    n = a + b
+    U = (chi / np.sqrt(n))[:, None]
+    Lam = np.array([float(n)])
+    assert abs(oracle.objective_hat(L, U, Lam) - 4.0 * w.sum()) <= 1e-12 * 4.0 * w.sum()
+    f1, f2 = oracle.feasibility_hat(U, Lam)
+    assert f1 <= 1e-14 and f2 <= 1e-14
+
+
+@pytest.mark.parametrize("a,b", [(3.0, 1.0), (0.5, 2.25), (4.0, 0.0)])
+def test_objective_and_feasibility_hat_rank2_closed_form(a, b):
+    """Hand-built rank-2 X^ on the 4-cycle C_4 (unit weights): u1 = 1/2 (1,1,1,1), u2 = 1/2 (1,-1,1,-1),
+    Lambda = (a, b).  u1^T L u1 = 0 (L 1 = 0), u2^T L u2 = sum over the 4 edges of (u_i - u_j)^2 = 4,
+    so tr(L X^) = 4 b; diag X^ = (a + b)/4 in every entry, so ||diag X^ - 1|| = 2 |(a + b)/4 - 1| and the
+    two normalizations divide it by ||1|| = 2 and 1 + ||1|| = 3."""
+    L = _edges_graph(4, [(0, 1), (1, 2), (2, 3), (3, 0)])
+    U = 0.5 * np.array([[1.0, 1.0], [1.0, -1.0], [1.0, 1.0], [1.0, -1.0]])
+    Lam = np.array([a, b])
+    assert abs(oracle.objective_hat(L, U, Lam) - 4.0 * b) <= 1e-14 * max(1.0, 4.0 * b)
+    r = 2.0 * abs((a + b) / 4.0 - 1.0)
+    f1, f2 = oracle.feasibility_hat(U, Lam)
+    assert abs(f1 - r / 2.0) <= 1e-15 and abs(f2 - r / 3.0) <= 1e-15
+
+
+@pytest.mark.parametrize("n", [4, 6, 9])
+def test_implicit_objective_and_infeasibility_star_closed_form(n):
+    """Star K_{1,n-1}: L has eigenvalues 0, 1 (n-2 times) and n, with the simple top eigenvector
+    (n-1, -1, ..., -1)/sqrt(n(n-1)).  At t = 1 (z = y = 0) D_1 = -L/||L||_F - beta_1 b I, whose minimum
+    eigenvector is that top vector; the full Krylov space (q = n; three distinct eigenvalues, so the
+    Krylov space is exhausted after 3 steps) gives it to rounding.  With eta_1 = 1 the implicit iterate is
+    X_2 = alpha v v^T, so in original units z = n (v o v) = (n-1, 1/(n-1), ..., 1/(n-1)):
+      ||z - 1|| / (1 + sqrt n) = sqrt((n-2)^2 + (n-1)(1/(n-1) - 1)^2) / (1 + sqrt n)
+      tr(L X_2) = n lambda_max(L) = n^2."""
+    L = _edges_graph(n, [(0, j) for j in range(1, n)])
+    o = oracle.Oracle(L, 2, seed=11, qfix=n, logcap=1)
+    o.step(1)
+    want = math.sqrt((n - 2) ** 2 + (n - 1) * (1.0 / (n - 1) - 1.0) ** 2) / (1.0 + math.sqrt(n))
+    assert abs(o.implicit_infeasibility() - want) <= 1e-12 * want
+    assert abs(o.implicit_objective() - n * n) <= 1e-12 * n * n
+
+
+def test_implicit_infeasibility_balanced_cycle_is_zero():
+    """Even cycle C_8: the top eigenvector of L is the alternating vector (eigenvalue 4, simple), so
+    v o v = 1/n exactly up to rounding at every t (z = b, y = 0 keep D_t = C - beta b I): the implicit
+    iterate is feasible, ||z - b|| = 0 to rounding for all t."""
+    L = _edges_graph(8, [(k, (k + 1) % 8) for k in range(8)])
+    o = oracle.Oracle(L, 2, seed=3, qfix=8, logcap=5)
+    o.step(5)
+    assert o.implicit_infeasibility() <= 1e-11
+    assert abs(o.implicit_objective() - 8 * 4.0) <= 1e-12 * 32.0
+
+
+# ------------------------------------------------------------- reading R26 (normalization by a reciprocal)
+def test_r26_reciprocal_normalization_within_noise_floor():
+    """Reading R26 evaluates Alg. 2 line 9's v / rho as v * fl(1/rho) (<= 1 ulp per entry from the
+    printed division).  Pin: the oracle with the literal division (div_norm) on configs[0] stays within
+    the noise floor any rounding-level change produces without reorthogonalization (SURVEY.md Appendix A:
+    two fp64 implementations differing in summation order agree to ~1e-12 in theta_t only for t <~ 20,
+    the objective to ~1e-4): theta_t within 1e-10 relative for t <= 20, the implicit objective after
+    T = 1000 within 1e-4, and the rounded cut weight within 0.5%."""
+    L = si.laplacian("c0")
+    T = 1000
+    a = oracle.solve(L, 10, T, seed=0)
+    o2 = oracle.Oracle(L, 10, seed=0, logcap=T, div_norm=True)
+    o2.step(T)
+    th, th2 = a["oracle"].log[:, 3], o2.log[:, 3]
+    assert np.max(np.abs(th[:20] - th2[:20]) / np.abs(th[:20])) <= 1e-10
+    assert not np.array_equal(th, th2)  # the two forms are different roundings
+    o_a, o_b = a["implicit_objective"], o2.implicit_objective()
+    assert abs(o_a - o_b) <= 1e-4 * abs(o_a)
+    U2, lam2, _ = oracle.nystrom_reconstruct(o2.S, o2.Omega, o2.tau)
+    _, w2, _ = oracle.round_cut(L, U2)
+    assert abs(w2 - a["cut_weight"]) <= 5e-3 * a["cut_weight"]
+
+
+# ------------------------------------------------------------- OpenMP (thread count is bitwise-neutral)
+def test_thread_count_does_not_change_bits():
+    """The exact sums (CAC-2) are integer sums, and the row loops are independent, so 1 thread and all
+    cores give identical bits (checked on a graph above the oracle's 65536-row parallel threshold)."""
+    L = si.generate("rgg", 1 << 17, seed=5)
+    runs = []
+    for th in (1, 0):
+        oracle.set_threads(th)
+        o = oracle.Oracle(L, 3, seed=5, logcap=2)
+        o.step(2)
+        runs.append((o.log.copy(), o.z, o.y, o.v, o.S))
+    oracle.set_threads(0)
+    for x, y in zip(*runs):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_qt_has_no_cap():
+    """q_t = min(n - 1, max(2, ceil(t^(1/4) ln n))) (reading A9) with no other bound: for
+    n = 2^25 and t = 10^6 it is ceil(31.62... * 17.33...) = 549 (the earlier oracle capped it at 127)."""
+    assert oracle.qt(10 ** 6, 1 << 25) == math.ceil(math.sqrt(math.sqrt(1e6)) * math.log(2.0 ** 25))
+    assert oracle.qt(10 ** 6, 1 << 25) > 127
+    assert oracle.qt(10 ** 6, 100) == 99
+
+
+def test_lanczos_beyond_127_steps_dense_rayleigh_ritz():
+    """Alg. 2 with q = 160 > 127 on a 400 x 400 matrix with a well separated bottom eigenvalue: theta is
+    lambda_min (dense eigh) to 1e-10 ||D|| and the vector's Rayleigh quotient matches."""
+    rng = np.random.default_rng(7)
+    n = 400
+    Q = np.linalg.qr(rng.standard_normal((n, n)))[0]
+    ev = np.concatenate([[-3.0], rng.uniform(0.0, 1.0, n - 1)])
+    M = (Q * ev) @ Q.T
+    M = 0.5 * (M + M.T)
+    rp, col, m, d = oracle.offdiag_of_dense(M)
+    g = si.normals(3, 1, 1, 0, n)
+    res = oracle.lanczos(n, rp, col, m, d, g, 160)
+    lmin = np.linalg.eigvalsh(M)[0]
+    assert res.k == 160 or res.k < 160  # no cap below q
+    assert abs(res.theta - lmin) <= 1e-10 * np.abs(ev).max()
+    assert abs(res.v @ M @ res.v - lmin) <= 1e-8
+
+
+# ------------------------------------------------------------- golden fixtures come from the oracle
+def test_golden_fixture_reproduces_from_oracle():
+    """tests/golden/*.json are written by tests/golden/make_golden.py from oracle/ only; the cheap case
+    is regenerated here and must match the stored fixture exactly (log, digests, S sample)."""
+    import json
+    import os
+    import sys
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    sys.path.insert(0, here)
+    import make_golden
+    fresh = make_golden.make("c1_q255")
+    with open(os.path.join(here, "c1_q255.json")) as f:
+        stored = json.load(f)
+    for k in ("log", "sha256", "S_rows", "S_sample", "S_absmax", "p", "tau", "R", "T", "qfix"):
+        assert fresh[k] == stored[k], k
+    assert max(int(float.fromhex(r[2])) for r in stored["log"]) > 127  # k beyond the old cap

@@ -1,0 +1,31 @@
+#!/bin/bash
+# Round-2 GPU call: build, smoke, GPU tests, bench (driver flags), ncu launch list and full captures.
+# usage: tools/gpu_r2.sh <tag> [what...]   what: smoke tests bench launches ncu:<regex> full
+TAG=${1:-r02}; shift
+[ $# -eq 0 ] && set -- smoke tests bench launches
+O=gpurun_out/$TAG; mkdir -p $O
+nvidia-smi > $O/nvsmi.txt 2>&1; nproc > $O/nproc.txt; lscpu | grep "Model name" >> $O/nproc.txt
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo "build exit $?" >> $O/build.log
+for w in "$@"; do
+  case $w in
+    smoke) python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log ;;
+    tests) timeout 1500 python -m pytest tests -m gpu -q -x --durations=25 > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log ;;
+    tests:*) timeout 1500 python -m pytest tests -m gpu -q -x --durations=25 -k "${w#tests:}" > $O/pytest_gpu_k.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu_k.log ;;
+    bench) timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err; echo "bench exit $?" >> $O/bench.err ;;
+    benchnocpu) timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 --no-cpu > $O/bench.json 2> $O/bench.err; echo "bench exit $?" >> $O/bench.err ;;
+    full) timeout 900 python bench.py --steps 997 --warmup 3 --no-cpu --no-e2e > $O/bench_full.json 2> $O/bench_full.err; echo "exit $?" >> $O/bench_full.err ;;
+    ref) timeout 900 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $O/ref.json 2> $O/ref.err; echo "ref exit $?" >> $O/ref.err ;;
+    launches)
+      CMD="python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e"
+      $CMD > $O/plain.log 2>&1 && \
+      ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $O/launches.csv $CMD > $O/ncu_launch.log 2>&1
+      echo "ncu launches exit $?" >> $O/plain.log ;;
+    ncu:*)  # ncu:<kernel regex>:<launches to skip>
+      SPEC=${w#ncu:}; KRE=${SPEC%%:*}; SKIP=${SPEC##*:}; [ "$SKIP" = "$SPEC" ] && SKIP=60
+      N=${KRE//[^a-zA-Z0-9_]/_}
+      CMD="python bench.py --steps 2 --warmup 5 --no-cpu --no-e2e --no-profile"
+      ncu --set full --clock-control none --import-source on -k regex:"$KRE" -s $SKIP -c 2 -o $O/prof_$N $CMD > $O/ncu_full_$N.log 2>&1
+      echo "ncu full exit $?" >> $O/ncu_full_$N.log ;;
+  esac
+done
+echo done > $O/DONE
