@@ -80,7 +80,8 @@ enum {
   SCG_FUSED_PASS1 = 1u << 10,   /* one GPU: all q steps of Lanczos pass 1 in one persistent cooperative kernel */
   SCG_WS_SPMV = 1u << 11,       /* uniform weights: warp-specialized TMA SpMV (producer warp + mbarrier ring) */
   SCG_TMA_B = 1u << 12,         /* TMA-staged recurrence kernel (bulk copies into shared memory) */
-  SCG_DEBUG_LOG = 1u << 13      /* host init stage timings and layout facts on stderr */
+  SCG_DEBUG_LOG = 1u << 13,     /* host init stage timings and layout facts on stderr */
+  SCG_NO_ELL = 1u << 14         /* keep the SELL-32 layout even when every row has <= 8 entries (ELL-W otherwise) */
 };
 
 /* This rank's rows [row_begin, row_end) of the symmetric weighted Laplacian

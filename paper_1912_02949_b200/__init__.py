@@ -33,6 +33,7 @@ SCG_FUSED_PASS1 = 1 << 10
 SCG_WS_SPMV = 1 << 11
 SCG_TMA_B = 1 << 12
 SCG_DEBUG_LOG = 1 << 13
+SCG_NO_ELL = 1 << 14
 
 STATUS = {0: "SCG_OK", -1: "SCG_EINVAL", -2: "SCG_ENOMEM", -3: "SCG_ECUDA", -4: "SCG_ENCCL", -5: "SCG_ECHOL",
           -6: "SCG_ESTATE", -7: "SCG_ERANGE", -8: "SCG_EUNSUPPORTED"}
@@ -223,7 +224,8 @@ class SketchyCGAL:
 
     Execution options (bitwise-neutral): ``pdl`` (programmatic dependent
     launches, default on), ``fused_pass1`` (persistent pass-1 kernel), ``ws_spmv``
-    (warp-specialized TMA SpMV), ``tma_b`` (TMA-staged recurrence kernel), ``debug_log``.
+    (warp-specialized TMA SpMV), ``tma_b`` (TMA-staged recurrence kernel), ``ell`` (ELL-W layout when
+    every row has <= 8 entries, default on), ``debug_log``.
     """
 
     def __init__(self, L, R: int, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
@@ -231,7 +233,7 @@ class SketchyCGAL:
                  stream=None, regenerate: bool = False, trace_le: bool = False, shards: int = 1, splits=None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None, ineq: bool = False,
                  box: tuple | None = None, pdl: bool = True, fused_pass1: bool = False, ws_spmv: bool = False,
-                 tma_b: bool = False, debug_log: bool = False, qfix: int = 0):
+                 tma_b: bool = False, debug_log: bool = False, qfix: int = 0, ell: bool = True):
         self.lib = load()
         self.n = int(L.n)
         self.R = int(R)
@@ -262,7 +264,7 @@ class SketchyCGAL:
                 (SCG_PROFILE if profile else 0) | (SCG_REGENERATE if regenerate else 0) | \
                 (SCG_TRACE_LE if trace_le else 0) | (SCG_INEQ if ineq else 0) | (0 if pdl else SCG_NO_PDL) | \
                 (SCG_FUSED_PASS1 if fused_pass1 else 0) | (SCG_WS_SPMV if ws_spmv else 0) | \
-                (SCG_TMA_B if tma_b else 0) | (SCG_DEBUG_LOG if debug_log else 0)
+                (SCG_TMA_B if tma_b else 0) | (SCG_DEBUG_LOG if debug_log else 0) | (0 if ell else SCG_NO_ELL)
         self._h = ctypes.c_void_p()
         dptr = None
         if dist is not None:

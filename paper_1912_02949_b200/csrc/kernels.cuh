@@ -171,7 +171,8 @@ __device__ __forceinline__ double div_rn(double a, double b, double rb) {
 // entries per round (coalesced) and the lanes run the strided partial chains of reading
 // R27; long rows are listed at init (longest first) and taken by the first warps of the
 // grid so they start early.
-constexpr int kMinBlocksUni = 3;  // min blocks per SM of the uniform-weight SpMV kernels (80-register cap)
+constexpr int kMinBlocksUni = 3;  // min blocks per SM of the uniform-weight SELL SpMV kernels (80-register cap)
+constexpr int kMinBlocksEll = 4;  // min blocks per SM of the ELL SpMV kernels (64-register cap)
 constexpr int kLongRow = 32;
 
 struct Rows {
@@ -188,7 +189,14 @@ struct Rows {
   int nslice;
   unsigned *work;       // non-null: dynamic slice distribution (chunks of kDynCh slices from this
                         // counter; zeroed again by the kernel's last block) -- skewed graphs
+  // ELL-W layout (graphs whose rows all have <= kEllMax entries: no long rows, no slice metadata):
+  // slice s = rows 32 s .. 32 s + 31, slot j of lane l at ecol[(32 s) W + 32 j + l]; rows shorter
+  // than W are padded with the dummy column n (gathered value +0, negative coefficient)
+  const int *ecol;      // column | 0x80000000 for a negative uniform value
+  const double *eval;   // per-slot values, or nullptr when all |C_rj| equal m0
+  int padc;             // the padding code
 };
+constexpr int kEllMax = 8;  // widest ELL layout (rows of at most 8 off-diagonal entries)
 constexpr int kDynCh = 8;
 
 constexpr int kWin = 1024;  // vector padding granularity (rows)
@@ -491,6 +499,111 @@ __device__ __forceinline__ void bulk_seg(void *sdst, const void *gbase, long lon
 }
 template <int ES>
 __device__ __forceinline__ int seg_shift(long long i0) { return (int)(((i0 * ES) & 15ll) / ES); }
+
+// ---------------------------------------------------------------- ELL-W engine
+// Every row has at most W off-diagonal entries (W a compile-time constant): slices of 32 rows
+// with exactly W slots each, so a slice's column block sits at a computed offset -- no slice
+// metadata, no dependent meta load, no width switch.  Each warp walks its block's slices with
+// a three-stage register pipeline: while slice i is computed, the gathers of slice i+1 (their
+// columns arrived during the previous step) and the columns and own entries of slice i+2 are in
+// flight.  Per row the arithmetic is spmv_rows' CAC-3 single chain (reading R27 needs no strided
+// chains here: every row has <= 32 entries), padding slots add fma(-m, +0, acc) == acc.
+template <int NC, bool UNI, int W, class Epi>
+__device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restrict__ X, double den,
+                                         const double *__restrict__ diag0, const double *__restrict__ diag1,
+                                         long long rb, int nl, Epi &epi) {
+  const int lane = threadIdx.x & 31;
+  const double rden = 1.0 / den;
+  const int nsl = (nl + 31) >> 5;
+  const int per = (nsl + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int s_end = min(nsl, ((int)blockIdx.x + 1) * per);
+  const int wstep = blockDim.x >> 5;
+  int sl = (int)blockIdx.x * per + (threadIdx.x >> 5);
+  const int *__restrict__ ec = RL.ecol + lane;
+  const double *__restrict__ ev = RL.eval + lane;
+  const int padc = RL.padc;
+  const double m0 = RL.m0;
+  auto cload = [&](int q, int (&c)[W], double (&v)[W]) {
+    if (q < s_end) {
+      const long long b = (long long)q * (32 * W);
+#pragma unroll
+      for (int u = 0; u < W; ++u) {
+        c[u] = __ldg(ec + b + 32 * u);
+        if (!UNI) v[u] = __ldg(ev + b + 32 * u);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < W; ++u) {
+        c[u] = padc;
+        if (!UNI) v[u] = -0.0;
+      }
+    }
+  };
+  auto gload = [&](const int (&c)[W], double (&g)[W]) {
+#pragma unroll
+    for (int u = 0; u < W; ++u) g[u] = __ldg(&X[c[u] & 0x7fffffff]);
+  };
+  auto oload = [&](int q, double &xo, double &dd0, double &dd1) {
+    const int p = q * 32 + lane;
+    xo = 0.0;
+    dd0 = 0.0;
+    dd1 = 0.0;
+    if (q < s_end && p < nl) {
+      xo = X[rb + p];
+      dd0 = diag0[p];
+      if (NC > 1) dd1 = diag1[p];
+    }
+  };
+  int c0[W], c1[W];
+  double v0[W], v1[W], g0[W];
+  double xo0, d00, d10, xo1, d01, d11;
+  cload(sl, c0, v0);
+  oload(sl, xo0, d00, d10);
+  gload(c0, g0);
+  cload(sl + wstep, c1, v1);
+  oload(sl + wstep, xo1, d01, d11);
+  for (; sl < s_end; sl += wstep) {
+    double g1[W];
+    gload(c1, g1);  // gathers of slice i+1
+    int c2[W];
+    double v2[W], xo2, d02, d12;
+    cload(sl + 2 * wstep, c2, v2);  // columns and own entries of slice i+2
+    oload(sl + 2 * wstep, xo2, d02, d12);
+    // compute slice i
+    const int p = sl * 32 + lane;
+    RowOut<NC> o;
+    o.r = p;
+    o.xr = xo0 * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
+    o.s[0] = d00 * o.xr;
+    if (NC > 1) o.s[NC - 1] = d10 * o.xr;
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      const double mm = UNI ? (c0[u] < 0 ? -m0 : m0) : v0[u];
+      const double x = g0[u] * rden;
+#pragma unroll
+      for (int t = 0; t < NC; ++t) o.s[t] = fma(mm, x, o.s[t]);
+    }
+    if (p < nl) epi(o);
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      c0[u] = c1[u];
+      c1[u] = c2[u];
+      g0[u] = g1[u];
+      if (!UNI) { v0[u] = v1[u]; v1[u] = v2[u]; }
+    }
+    xo0 = xo1; d00 = d01; d10 = d11;
+    xo1 = xo2; d01 = d02; d11 = d12;
+  }
+}
+
+// SpMV dispatch: ELL-W when the layout has one (W > 0), else SELL + long rows.
+template <int NC, bool UNI, int W, class Epi>
+__device__ __forceinline__ void spmv_any(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
+                                         const double *__restrict__ diag0, const double *__restrict__ diag1,
+                                         long long rb, int nl, Epi &epi) {
+  if constexpr (W > 0) spmv_ell<NC, UNI, W>(RL, X, den, diag0, diag1, rb, nl, epi);
+  else spmv_rows<NC, UNI>(C, RL, X, den, diag0, diag1, rb, nl, epi);
+}
 
 // ---------------------------------------------------------------- block reduction
 // Block-level exact accumulators (shared memory) for NS sums.
@@ -863,8 +976,8 @@ struct EpiA {
   }
 };
 
-template <bool UNI>
-__global__ void __launch_bounds__(kBlockA, UNI ? kMinBlocksUni : 2) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
+template <bool UNI, int W>  // W > 0: ELL-W layout (spmv_ell), 0: SELL + long rows
+__global__ void __launch_bounds__(kBlockA, W > 0 ? kMinBlocksEll : (UNI ? kMinBlocksUni : 2)) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ X, int nl, long long rb, int i,
                                                          double *__restrict__ a, XSlot *slot, DevScalars *sc,
                                                          Net net) {
@@ -878,7 +991,7 @@ __global__ void __launch_bounds__(kBlockA, UNI ? kMinBlocksUni : 2) k_lanczos_a(
   epi.blk = xb.l[0];
   xwin_init(epi.acc[0]);
   epi.err = 0;
-  spmv_rows<1, UNI>(C, RL, X, den, d, nullptr, rb, nl, epi);
+  spmv_any<1, UNI, W>(C, RL, X, den, d, nullptr, rb, nl, epi);
   int err = epi.err;
   XWin (&acc)[1] = epi.acc;
   if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P, 0u) && threadIdx.x == 0) {
@@ -1574,8 +1687,8 @@ struct EpiC {
   }
 };
 
-template <bool UNI>
-__global__ void __launch_bounds__(kBlock, UNI ? kMinBlocksUni : 2) k_lanczos_c(Csr C, Rows RL, const double *__restrict__ d,
+template <bool UNI, int W>
+__global__ void __launch_bounds__(kBlock, W > 0 ? kMinBlocksEll : (UNI ? kMinBlocksUni : 2)) k_lanczos_c(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ Xj, const double *Xjm1,
                                                          double *Xjp1, double *__restrict__ x, int nl, long long rb,
                                                          int j, DevScalars *sc, XSlot *slot, Net net) {
@@ -1583,7 +1696,7 @@ __global__ void __launch_bounds__(kBlock, UNI ? kMinBlocksUni : 2) k_lanczos_c(C
   if (j >= sc->k) return;  // sc->k holds the effective k after k_tridiag
   EpiC epi{Xjm1, Xjp1, x, rb, &net, j, sc->om[j - 1], sc->rho[j - 1], j >= 2 ? sc->rho[j - 2] : 1.0, sc->rho[j],
            sc->s[0], sc->s[j], 1.0 / sc->rho[j], 1.0 / (j >= 2 ? sc->rho[j - 2] : 1.0)};
-  spmv_rows<1, UNI>(C, RL, Xj, epi.den, d, nullptr, rb, nl, epi);
+  spmv_any<1, UNI, W>(C, RL, Xj, epi.den, d, nullptr, rb, nl, epi);
   // P > 1: the next step gathers w_{j+1} -- a barrier collective (no sums)
   if (net.P > 1 && ticket_only(slot) && threadIdx.x == 0) {
     FinArgs f{};
@@ -1682,7 +1795,7 @@ struct EpiM {
   }
 };
 
-template <bool UNI>
+template <bool UNI, int W>
 __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const double *__restrict__ d,
                                                        const double *__restrict__ cdiag, const double *__restrict__ x,
                                                        double *__restrict__ v, int nl, long long rb, XSlot *slot,
@@ -1698,7 +1811,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
   xwin_init(epi.acc[1]);
   xwin_init(epi.acc[2]);
   epi.err = 0;
-  spmv_rows<2, UNI>(C, RL, x, nu, d, cdiag, rb, nl, epi);
+  spmv_any<2, UNI, W>(C, RL, x, nu, d, cdiag, rb, nl, epi);
   int err = epi.err;
   XWin (&acc)[3] = epi.acc;
   if (commit_and_ticket<3>(acc, xb, slot, err, sc, net.P, 0u) && threadIdx.x == 0) {

@@ -103,6 +103,10 @@ struct Shard {
   bool sell_uniform = false;
   int nslice = 0;
   unsigned *work = nullptr;  // dynamic slice counter of k_lanczos_a (graphs with long rows)
+  int *ell_col = nullptr;    // ELL-W layout (rows of <= kEllMax entries), W = ellw; 0: none
+  double *ell_val = nullptr;
+  int ellw = 0, padc = 0;
+  int grid_ell = 1, grid_ell_mon = 1, grid_ell_c = 1;
   bool dyn = false;
   // row relabeling (SELL engine): local row nu holds input row rb + origloc[nu]
   std::vector<int> origloc;
@@ -337,8 +341,22 @@ Rows rows_of(const Shard *s, bool dyn = false) {
   r.sval = s->sell_val;
   r.m0 = s->sell_m0;
   r.nslice = s->nslice;
+  r.ecol = s->ell_col;
+  r.eval = s->ell_val;
+  r.padc = s->padc;
   return r;
 }
+
+// Kernel instantiation for a shard's layout: uniform weights (values in the column's sign bit) or
+// not, and the ELL width (0: SELL + long rows).
+constexpr int kEllWidths[] = {2, 3, 4, 6, 8};
+#define SCG_PICK(K, U, W)                                          \
+  ((W) == 2   ? ((U) ? K<true, 2> : K<false, 2>)                   \
+   : (W) == 3 ? ((U) ? K<true, 3> : K<false, 3>)                   \
+   : (W) == 4 ? ((U) ? K<true, 4> : K<false, 4>)                   \
+   : (W) == 6 ? ((U) ? K<true, 6> : K<false, 6>)                   \
+   : (W) == 8 ? ((U) ? K<true, 8> : K<false, 8>)                   \
+              : ((U) ? K<true, 0> : K<false, 0>))
 
 Net net_of(const scg_ctx *c, const Shard *s, unsigned long long E) {
   Net n{};
@@ -385,7 +403,8 @@ void free_shard(Shard *s) {
   void *ptrs[] = {s->rp, s->col, s->val, s->wts, s->ldiag, s->cdiag, s->d, s->z, s->y, s->a, s->v, s->G,
                   s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
                   s->sc, s->slots, s->dlog, s->longrows, s->sell_col, s->sell_meta, s->sell_val,
-                  s->mask, s->mb, s->peerG, s->peerMB, s->orig, s->V, s->ckr, s->work, s->gflag};
+                  s->mask, s->mb, s->peerG, s->peerMB, s->orig, s->V, s->ckr, s->work, s->gflag, s->ell_col,
+                  s->ell_val};
   for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -613,7 +632,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
 
   // grid sizes from occupancy
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_a<true>, kBlock, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lanczos_a<true, 0>, kBlock, 0);
   s->grid_rows = grid_for(nl, std::max(1, occ) * c->nsm);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_primal<false>, kBlock, 0);
   s->grid_primal = grid_for(nl, std::max(1, occ) * c->nsm);
@@ -750,25 +769,77 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
       CK(cudaMemcpyAsync(s->sell_val, sval.data(), sizeof(double) * sval.size(), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
     s->sell_slots = (double)scol.size();
-    matbytes = s->sell_slots * (uni ? 4.0 : 12.0) + 8.0 * s->nslice;
+    s->padc = padc;
+    // ELL-W: every row has <= kEllMax entries (no long rows) and the padding
+    // to the widest row stays below 2x the entries -- configs[1], [3] and [4]; SCG_NO_ELL opts out
+    int maxlen = 0;
+#pragma omp parallel for schedule(static, 4096) reduction(max : maxlen)
+    for (int64_t r = 0; r < nl; ++r) maxlen = std::max(maxlen, h_rp[(size_t)r + 1] - h_rp[(size_t)r]);
+    int W = 0;
+    for (int w : kEllWidths)
+      if (W == 0 && w >= maxlen) W = w;
+    const int64_t nsl32 = (nl + 31) / 32;
+    if (!(c->flags & SCG_NO_ELL) && s->nlong == 0 && W > 0 && (double)W * (double)nl <= 2.0 * (double)cnt_off + 64.0) {
+      const size_t ne = (size_t)nsl32 * 32 * W;
+      hvec<int> ecol(ne);
+      hvec<double> eval;
+      if (!uni) eval.resize(ne);
+#pragma omp parallel for schedule(static, 1024)
+      for (int64_t q = 0; q < nsl32; ++q)
+        for (int j = 0; j < W; ++j)
+          for (int l = 0; l < 32; ++l) {
+            const int64_t r = q * 32 + l;
+            const size_t slot = (size_t)q * 32 * W + (size_t)j * 32 + l;
+            const int e = r < nl ? h_rp[(size_t)r] + j : -1;
+            if (e >= 0 && e < h_rp[(size_t)r + 1]) {
+              ecol[slot] = enc(e);
+              if (!uni) eval[slot] = valof(e);
+            } else {
+              ecol[slot] = padc;
+              if (!uni) eval[slot] = -0.0;
+            }
+          }
+      if (!alloc((void **)&s->ell_col, sizeof(int) * ne) || (!uni && !alloc((void **)&s->ell_val, sizeof(double) * ne)))
+        return fail(c, SCG_ENOMEM, "ELL layout");
+      CK(cudaMemcpyAsync(s->ell_col, ecol.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
+      if (!uni) CK(cudaMemcpyAsync(s->ell_val, eval.data(), sizeof(double) * ne, cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+      s->ellw = W;
+    }
+    // algorithmic matrix bytes: one column index (+ value unless uniform) per stored entry --
+    // independent of the layout's padding and metadata
+    matbytes = (double)cnt_off * (uni ? 4.0 : 12.0);
   }
   {  // grids of the SpMV kernels
     const bool U = s->sell_uniform;
     int oa = 1, om = 1;
     if (U) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<true>, kBlock, 0);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<true>, kBlock, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<true, 0>, kBlock, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<true, 0>, kBlock, 0);
     } else {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<false>, kBlock, 0);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<false>, kBlock, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<false, 0>, kBlock, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<false, 0>, kBlock, 0);
     }
     const int need = (int)std::max<int64_t>((s->nslice + 7) / 8, (s->nlong + 7) / 8);
     s->grid_spmv = std::max(1, std::min(need, std::max(1, oa) * c->nsm));
     const int needA = (int)std::max<int64_t>((s->nslice + kBlockA / 32 - 1) / (kBlockA / 32), 1);
     s->grid_a = std::max(1, std::min(needA, std::max(1, oa) * c->nsm));
     s->grid_mon = std::max(1, std::min(need, std::max(1, om) * c->nsm));
-    dbg_log(c, "[scg] shard %d: nl=%lld long=%d uni=%d occ_a=%d occ_m=%d grid_a=%d\n", s->rank, (long long)nl, s->nlong,
-            (int)U, oa, om, s->grid_a);
+    if (s->ellw) {
+      int oe = 1, oem = 1, oec = 1;
+      auto kA = SCG_PICK(k_lanczos_a, U, s->ellw);
+      auto kM = SCG_PICK(k_monitor, U, s->ellw);
+      auto kC = SCG_PICK(k_lanczos_c, U, s->ellw);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oe, kA, kBlockA, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oem, kM, kBlock, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oec, kC, kBlock, 0);
+      const int needE = (int)std::max<int64_t>(((nl + 31) / 32 + 7) / 8, 1);
+      s->grid_ell = std::max(1, std::min(needE, std::max(1, oe) * c->nsm));
+      s->grid_ell_mon = std::max(1, std::min(needE, std::max(1, oem) * c->nsm));
+      s->grid_ell_c = std::max(1, std::min(needE, std::max(1, oec) * c->nsm));
+    }
+    dbg_log(c, "[scg] shard %d: nl=%lld long=%d uni=%d ellw=%d occ_a=%d occ_m=%d grid_a=%d grid_ell=%d\n", s->rank,
+            (long long)nl, s->nlong, (int)U, s->ellw, oa, om, s->grid_a, s->grid_ell);
   }
   // dynamic slice distribution for skewed graphs (long rows present): warps that carry hub
   // rows take fewer slices.  Off for graphs without long rows (static ranges keep L1 locality).
@@ -1292,13 +1363,13 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       for (Shard *s : c->sh) {
         Csr C{s->rp, s->col, s->val};
         Rows TT = rows_of(s, s->dyn);
-        auto kA = s->sell_uniform ? k_lanczos_a<true> : k_lanczos_a<false>;
+        auto kA = SCG_PICK(k_lanczos_a, s->sell_uniform, s->ellw);
         if (s->ws)
           launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], k_lanczos_a_ws<true>, dim3(s->grid_ws), dim3(kWsThreads),
                       sizeof(WsSmem), C, TT, (const double *)s->d, (const double *)slot(s, i), (int)s->nl,
                       (long long)s->rb, i, s->a, s->slots + SLOT_OM, s->sc, net_of(c, s, E));
         else
-          launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->grid_a), dim3(kBlockA), 0, C, TT,
+          launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->ellw ? s->grid_ell : s->grid_a), dim3(kBlockA), 0, C, TT,
                       (const double *)s->d, (const double *)slot(s, i), (int)s->nl, (long long)s->rb, i, s->a,
                       s->slots + SLOT_OM, s->sc, net_of(c, s, E));
       }
@@ -1336,9 +1407,9 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
         for (Shard *s : c->sh) {
           Csr C{s->rp, s->col, s->val};
           Rows TT = rows_of(s);
-          auto kC = s->sell_uniform ? k_lanczos_c<true> : k_lanczos_c<false>;
+          auto kC = SCG_PICK(k_lanczos_c, s->sell_uniform, s->ellw);
           const double *Xjm1 = (j == 1) ? nullptr : slot(s, j - 1);
-          launch_smem(c, KC_LANCZOS_C, s->kb[KC_LANCZOS_C], kC, dim3(s->grid_spmv), dim3(kBlock), 0, C, TT,
+          launch_smem(c, KC_LANCZOS_C, s->kb[KC_LANCZOS_C], kC, dim3(s->ellw ? s->grid_ell_c : s->grid_spmv), dim3(kBlock), 0, C, TT,
                  (const double *)s->d, (const double *)slot(s, j), Xjm1, slot(s, j + 1), c->xg(s), (int)s->nl,
                  (long long)s->rb, j, s->sc, s->slots + SLOT_BAR, net_of(c, s, E));
         }
@@ -1359,8 +1430,8 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     for (Shard *s : c->sh) {
       Csr C{s->rp, s->col, s->val};
       Rows TT = rows_of(s, s->dyn);
-      auto kM = s->sell_uniform ? k_monitor<true> : k_monitor<false>;
-      launch_smem(c, KC_MONITOR, s->kb[KC_MONITOR], kM, dim3(s->grid_mon), dim3(kBlock), 0, C, TT, (const double *)s->d,
+      auto kM = SCG_PICK(k_monitor, s->sell_uniform, s->ellw);
+      launch_smem(c, KC_MONITOR, s->kb[KC_MONITOR], kM, dim3(s->ellw ? s->grid_ell_mon : s->grid_mon), dim3(kBlock), 0, C, TT, (const double *)s->d,
              (const double *)s->cdiag, (const double *)c->xg(s), c->vslot(s, js), (int)s->nl, (long long)s->rb,
              s->slots + SLOT_MON, s->sc, net_of(c, s, E));
     }

@@ -135,6 +135,17 @@ def test_launch_policy_forced_bitwise(gpu, cfg, T, pdl):
     _assert_trajectory(g, o, T)
 
 
+@pytest.mark.parametrize("cfg,T", [("c1", 300), ("c3", 2), ("c4", 1)])
+def test_sell_layout_where_ell_applies_bitwise(gpu, cfg, T):
+    """Graphs whose rows all have <= 8 entries run the ELL-W SpMV by default; the SELL-32 layout
+    (SCG_NO_ELL) gives the same bitwise trajectory on them."""
+    L = si.laplacian(cfg)
+    c = si.CONFIGS[cfg]
+    R = 2 if cfg == "c4" else c["R"]
+    g, o = _run_pair(gpu, L, R, T, seed=c["seed"], ell=False)
+    _assert_trajectory(g, o, T)
+
+
 @pytest.mark.parametrize("cfg,T", [("c0", 200), ("c3", 1)])
 def test_tma_staged_recurrence_bitwise(gpu, cfg, T):
     """The opt-in TMA-staged recurrence kernel (SCG_TMA_B) gives the same bitwise trajectory."""
