@@ -34,6 +34,7 @@ struct DevScalars {
   double gk[kMaxR];        // g = v^T Omega
   double theta, nu_x, xi, c, vv, nz, gamma, p, tau;
   double my[4];            // sums over the state (y_t, z_t) of the NEXT iteration: y, y.z, z.z, z (k_dual_sketch)
+  double g2n[2];           // ||g||^2 of the start vector drawn ahead on the side stream, by parity of its t
   int k, brk, err, pad;
 };
 
@@ -140,7 +141,7 @@ __device__ __forceinline__ void gstore(const Net &net, double *dst, int r, doubl
   }
 }
 
-enum FinKind { FK_FROB = 0, FK_RHO0, FK_OM, FK_RHO, FK_NUX, FK_MON, FK_NZ, FK_BAR, FK_RHO0M };
+enum FinKind { FK_FROB = 0, FK_RHO0, FK_OM, FK_RHO, FK_NUX, FK_MON, FK_NZ, FK_BAR, FK_RHO0M, FK_GEN, FK_RHO0S };
 
 struct FinArgs {
   int i;                 // Lanczos step (FK_OM, FK_RHO, FK_BAR)
@@ -541,7 +542,7 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
   };
   auto gload = [&](const int (&c)[W], double (&g)[W]) {
 #pragma unroll
-    for (int u = 0; u < W; ++u) g[u] = __ldg(&X[c[u] & 0x7fffffff]);
+    for (int u = 0; u < W; ++u) g[u] = __ldg(X + ((unsigned)c[u] & 0x7fffffffu));  // one IMAD.WIDE.U32 per address
   };
   auto oload = [&](int q, double &xo, double &dd0, double &dd1) {
     const int p = q * 32 + lane;
@@ -578,10 +579,17 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
     if (NC > 1) o.s[NC - 1] = d10 * o.xr;
 #pragma unroll
     for (int u = 0; u < W; ++u) {
-      const double mm = UNI ? (c0[u] < 0 ? -m0 : m0) : v0[u];
-      const double x = g0[u] * rden;
+      double x = g0[u] * rden;
+      if (UNI) {
+        // fma(-m0, x, acc) == fma(m0, -x, acc) exactly: the coefficient's sign (bit 31 of the column
+        // code) is moved onto x with one XOR of its high word
+        x = __hiloint2double(__double2hiint(x) ^ (c0[u] & (int)0x80000000), __double2loint(x));
 #pragma unroll
-      for (int t = 0; t < NC; ++t) o.s[t] = fma(mm, x, o.s[t]);
+        for (int t = 0; t < NC; ++t) o.s[t] = fma(m0, x, o.s[t]);
+      } else {
+#pragma unroll
+        for (int t = 0; t < NC; ++t) o.s[t] = fma(v0[u], x, o.s[t]);
+      }
     }
     if (p < nl) epi(o);
 #pragma unroll
@@ -720,6 +728,13 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
       sc->k = 0;
       if (kind == FK_RHO0M)
         for (int j = 0; j < 4; ++j) sc->my[j] = xacc_round(L[1 + j]);
+      break;
+    case FK_GEN: sc->g2n[f.i & 1] = xacc_round(L[0]); break;  // start vector of iteration f.i, drawn ahead
+    case FK_RHO0S:  // k_dual_sketch without the draw: the next start vector's norm comes from FK_GEN
+      sc->rho[0] = sqrt(sc->g2n[f.i & 1]);
+      sc->brk = 0;
+      sc->k = 0;
+      for (int j = 0; j < 4; ++j) sc->my[j] = xacc_round(L[j]);
       break;
     case FK_OM: sc->om[f.i - 1] = xacc_round(L[0]); break;
     case FK_RHO: fin_rho(sc, f.i, xacc_round(L[0])); break;
@@ -943,9 +958,11 @@ __global__ void k_init_d(const double *__restrict__ z, const double *__restrict_
 }
 
 // Lanczos start vector g = randn (Alg. 2 line 1) for iteration t and ||g||^2 (exact).
+// kind FK_RHO0: the start vector of the iteration about to run (init); FK_GEN: drawn one iteration
+// ahead on the side stream, its norm parked in sc->g2n[t & 1].
 __global__ void __launch_bounds__(kBlock) k_gen_start(double *__restrict__ g, int nl, long long rb, uint64_t seed,
                                                       long long t, XSlot *slot, DevScalars *sc, Net net,
-                                                      const int *__restrict__ orig) {
+                                                      const int *__restrict__ orig, int kind) {
   pdl_entry();
   __shared__ XBlk<1> xb;
   xblk_init<1>(xb);
@@ -957,8 +974,11 @@ __global__ void __launch_bounds__(kBlock) k_gen_start(double *__restrict__ g, in
     gstore(net, g + rb + r, r, v);
     xwin_add_nn(acc[0], v * v, err, xb.l[0]);
   }
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0)
-    emit<1>(slot, sc, net, FK_RHO0, FinArgs{}, nullptr);
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P) && threadIdx.x == 0) {
+    FinArgs f{};
+    f.i = (int)(t & 1);
+    emit<1>(slot, sc, net, kind, f, nullptr);
+  }
 }
 
 // ---------------------------------------------------------------- Lanczos pass 1
@@ -1329,15 +1349,16 @@ __device__ __forceinline__ void st_release_gpu(unsigned long long *p, unsigned l
 
 template <bool UNI>
 __global__ void __launch_bounds__(kBlockA, UNI ? kMinBlocksUni : 2)
-    k_lanczos_pass1(Csr C, Rows RL, const double *__restrict__ d, double *G, long long npad, int store, int q,
+    k_lanczos_pass1(Csr C, Rows RL, const double *__restrict__ d, double *G, double *W1, long long npad, int store, int q,
                     int nl, double *a, XSlot *slot_om, XSlot *slot_rho, DevScalars *sc, Net net,
                     unsigned long long *gflag, unsigned long long ebase) {
   pdl_entry();
   __shared__ XBlk<1> xb;
   __shared__ int s_go;
-  auto vslot = [&](int j) -> double * {  // buffer of w_j (the host's slot(s, j))
+  auto vslot = [&](int j) -> double * {  // buffer of w_j (the host's slot(s, j)); w_1 = W1
+    if (j == 1) return W1;
     if (store) return G + (long long)j * npad;
-    return j == 1 ? G + npad : G + (long long)(2 + (j & 1)) * npad;
+    return G + (long long)(2 + (j & 1)) * npad;
   };
   unsigned long long ph = ebase;
   // close a phase: the last block finalizes (fin) and opens the barrier, the others wait
@@ -1709,7 +1730,8 @@ __global__ void __launch_bounds__(kBlock, W > 0 ? kMinBlocksEll : (UNI ? kMinBlo
 // Lanczos vectors w_j kept by pass 1 (slot j-1 of Wst, leading dimension ldw)
 // replace the pass-2 regeneration: x = s_1 v_1 + sum_j fma(s_j, v_j, .), v_j = w_j / rho_{j-1},
 // bitwise equal to the two-pass result; then ||x||^2 (exact).
-__global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict__ Wst, long long ldw,
+__global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict__ W1, const double *__restrict__ Wst,
+                                                       long long ldw,
                                                        double *__restrict__ x, int nl, long long rb, XSlot *slot,
                                                        DevScalars *sc, Net net) {
   pdl_entry();
@@ -1727,8 +1749,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_combine(const double *__restrict_
   unsigned peer = 0u;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
     const unsigned mk = gmask(net, r);  // issued with the row's loads
-    const double *w = Wst + rb + r;
-    double xr = s_s[0] * (__ldg(w) * s_rr[0]);
+    const double *w = Wst + rb + r;  // w_{j+1} at slot j (j >= 1); w_1 = the start vector in W1
+    double xr = s_s[0] * (__ldg(W1 + rb + r) * s_rr[0]);
     int j = 1;
     for (; j + 4 <= k; j += 4) {
       double wv[4];
@@ -1907,11 +1929,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
   }
 }
 
-// y <- y + gamma (z - b) (Alg. 4 line 9); d for t+1; next start vector g_{t+1} and
-// ||g_{t+1}||^2 (exact).  The sketch update of Alg. 4 line 10 is deferred (k_sketch_flush):
+// y <- y + gamma (z - b) (Alg. 4 line 9); d for t+1; GEN: also the next start vector g_{t+1} and
+// ||g_{t+1}||^2 (exact) -- otherwise g_{t+1} was drawn ahead on the side stream (k_gen_start, FK_GEN)
+// and only its norm is taken over.  The sketch update of Alg. 4 line 10 is deferred (k_sketch_flush):
 // this kernel records its coefficients ck = fl(eta alpha) g_k in the ring slot js.
-template <bool BOX>  // box constraint set (A.ineq): compiled out of the equality instantiation
-__global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restrict__ z, double *__restrict__ y,
+template <bool BOX, bool GEN>  // BOX: box constraint set (A.ineq), compiled out of the equality instantiation
+__global__ void __launch_bounds__(kBlock, GEN ? 2 : 4) k_dual_sketch(const double *__restrict__ z, double *__restrict__ y,
                                                         double *__restrict__ d, const double *__restrict__ cdiag,
                                                         double *__restrict__ ckr, int js,
                                                         double *__restrict__ g, int nl, long long rb, int R,
@@ -1921,13 +1944,14 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
   const double gam = sc->gamma;
   if (blockIdx.x == 0 && (int)threadIdx.x < R)  // H = 0 (trace-bounded, xi_t >= 0): no rank-one term
     ckr[js * kMaxR + threadIdx.x] = (A.trace_le && !(sc->xi < 0.0)) ? 0.0 : (A.eta * A.alpha) * sc->gk[threadIdx.x];
-  // exact sums: ||g_{t+1}||^2, and over the next iteration's state (y_{t+1}, z_{t+1}):
+  // exact sums: [GEN: ||g_{t+1}||^2,] and over the next iteration's state (y_{t+1}, z_{t+1}):
   // sum y, y.z, z.z, sum z (surrogate gap / stopping rule, finalize FK_NZ)
-  __shared__ XBlk<5> xb;
-  xblk_init<5>(xb);
-  XWin acc[5];
+  constexpr int NS = GEN ? 5 : 4, o = GEN ? 1 : 0;
+  __shared__ XBlk<NS> xb;
+  xblk_init<NS>(xb);
+  XWin acc[NS];
 #pragma unroll
-  for (int q = 0; q < 5; ++q) xwin_init(acc[q]);
+  for (int q = 0; q < NS; ++q) xwin_init(acc[q]);
   int err = 0;
   unsigned peer = 0u;
   const int stride = gridDim.x * blockDim.x;
@@ -1938,7 +1962,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int r = r0 + u * stride;
-      if (r < nl) { zr[u] = z[r]; yv[u] = y[r]; cd[u] = cdiag[r]; og[u] = orig[r]; mk[u] = gmask(net, r); }
+      if (r < nl) {
+        zr[u] = z[r];
+        yv[u] = y[r];
+        cd[u] = cdiag[r];
+        if (GEN) { og[u] = orig[r]; mk[u] = gmask(net, r); }
+      }
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -1950,19 +1979,24 @@ __global__ void __launch_bounds__(kBlock, 2) k_dual_sketch(const double *__restr
         y[r] = yr;
         const double e1 = BOX ? zr[u] - fmin(fmax(zr[u] + yr / A.beta_next, A.lo), A.hi) : e;
         d[r] = fma(A.beta_next, e1, yr) + cd[u];
-        const double gv = scg_lanczos_start(seed, A.t + 1, rb + og[u]);
-        gstore_m(net, g + rb + r, mk[u], gv);
-        peer |= mk[u];
-        xwin_add_nn(acc[0], gv * gv, err, xb.l[0]);
-        xwin_add(acc[1], yr, err, xb.l[1]);
-        xwin_add(acc[2], yr * zr[u], err, xb.l[2]);
-        xwin_add_nn(acc[3], zr[u] * zr[u], err, xb.l[3]);
-        xwin_add_nn(acc[4], zr[u], err, xb.l[4]);  // z >= 0 (convex combination of alpha v o v)
+        if (GEN) {
+          const double gv = scg_lanczos_start(seed, A.t + 1, rb + og[u]);
+          gstore_m(net, g + rb + r, mk[u], gv);
+          peer |= mk[u];
+          xwin_add_nn(acc[0], gv * gv, err, xb.l[0]);
+        }
+        xwin_add(acc[o + 0], yr, err, xb.l[o + 0]);
+        xwin_add(acc[o + 1], yr * zr[u], err, xb.l[o + 1]);
+        xwin_add_nn(acc[o + 2], zr[u] * zr[u], err, xb.l[o + 2]);
+        xwin_add_nn(acc[o + 3], zr[u], err, xb.l[o + 3]);  // z >= 0 (convex combination of alpha v o v)
       }
     }
   }
-  if (commit_and_ticket<5>(acc, xb, slot, err, sc, net.P, peer) && threadIdx.x == 0)
-    emit<5>(slot, sc, net, FK_RHO0M, FinArgs{}, nullptr);
+  if (commit_and_ticket<NS>(acc, xb, slot, err, sc, net.P, peer) && threadIdx.x == 0) {
+    FinArgs f{};
+    f.i = (int)((A.t + 1) & 1);
+    emit<NS>(slot, sc, net, GEN ? FK_RHO0M : FK_RHO0S, f, nullptr);
+  }
 }
 
 // Deferred sketch updates (Alg. 4 line 10, eqn:sketch-update PAPER.md:1162-1169): S is

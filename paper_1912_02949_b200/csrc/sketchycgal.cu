@@ -62,19 +62,19 @@ using hvec = std::vector<T, noinit_alloc<T>>;
 
 enum KClass {
   KC_LANCZOS_A = 0, KC_LANCZOS_B, KC_TRIDIAG, KC_LANCZOS_C, KC_NORM_X, KC_COMBINE, KC_MONITOR, KC_PRIMAL,
-  KC_DUAL_SKETCH, KC_SKETCH, KC_PULL, KC_OTHER, KC_PASS1, KC_COUNT
+  KC_DUAL_SKETCH, KC_SKETCH, KC_PULL, KC_OTHER, KC_PASS1, KC_GEN, KC_COUNT
 };
 const char *kKClassName[KC_COUNT] = {"lanczos_a_spmv_dot", "lanczos_b_axpy_norm", "tridiag_mineig",
                                      "lanczos_c_spmv_regen", "norm_x", "combine_stored", "monitor_spmv",
                                      "primal_z_gpart", "dual_next_g", "sketch_flush", "pull_collective", "other",
-                                     "lanczos_pass1_fused"};
+                                     "lanczos_pass1_fused", "gen_start_side"};
 
 struct EvPair {
   cudaEvent_t a, b;
   int cls;
 };
 
-enum { SLOT_NU0 = 0, SLOT_OM, SLOT_RHO, SLOT_XX, SLOT_MON, SLOT_NZ, SLOT_INIT, SLOT_BAR, SLOT_COUNT };
+enum { SLOT_NU0 = 0, SLOT_OM, SLOT_RHO, SLOT_XX, SLOT_MON, SLOT_NZ, SLOT_INIT, SLOT_BAR, SLOT_GEN, SLOT_COUNT };
 
 }  // namespace
 
@@ -88,6 +88,7 @@ struct Shard {
   double *d = nullptr, *z = nullptr, *y = nullptr, *a = nullptr, *v = nullptr;
   double *V = nullptr, *ckr = nullptr;  // deferred sketch updates: ring of kSketchB eigenvectors + coefficients
   double *G = nullptr;  // gathered region: [x | W slot 0 (= g) | W slot 1 | ...], each npad long
+  double *gB = nullptr; // side-stream draws: start vector of even iterations (odd ones use W slot 0)
   double *S = nullptr, *Om = nullptr, *gpart = nullptr;
   double *U = nullptr, *tmp1 = nullptr, *tmp2 = nullptr, *dmat = nullptr, *partial = nullptr, *dlam = nullptr;
   double *dscalar = nullptr;
@@ -106,7 +107,7 @@ struct Shard {
   int *ell_col = nullptr;    // ELL-W layout (rows of <= kEllMax entries), W = ellw; 0: none
   double *ell_val = nullptr;
   int ellw = 0, padc = 0;
-  int grid_ell = 1, grid_ell_mon = 1, grid_ell_c = 1;
+  int grid_ell = 1, grid_ell_mon = 1, grid_ell_c = 1, grid_dual_s = 1;
   bool dyn = false;
   // row relabeling (SELL engine): local row nu holds input row rb + origloc[nu]
   std::vector<int> origloc;
@@ -132,6 +133,11 @@ struct Shard {
 struct scg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // one GPU: the next iteration's start vector is drawn on this lower-priority stream while the
+  // current iteration's Lanczos passes run (evA: its buffer is free; evB: drawn) -- DESIGN.md section 5
+  cudaStream_t side = nullptr;
+  cudaEvent_t evA = nullptr, evB = nullptr;
+  bool side_rng = false;
   bool own_stream = false;
   int nsm = 148;
   int64_t n = 0, npad = 0;
@@ -189,6 +195,8 @@ struct scg_ctx {
     return s;
   }
   double *xg(const Shard *s) const { return s->G; }
+  // buffer of the start vector w_1 of iteration t
+  double *gslot(const Shard *s, int64_t t) const { return (side_rng && !(t & 1)) ? s->gB : s->G + npad; }
   double *wslot(const Shard *s, int j) const { return s->G + (long long)(1 + j) * npad; }
 };
 
@@ -226,6 +234,7 @@ int grid_for(int64_t rows, int maxgrid) {
 void ev_flush(scg_ctx *c) {
   if (c->pending.empty()) return;
   cudaStreamSynchronize(c->stream);
+  if (c->side) cudaStreamSynchronize(c->side);
   for (auto &p : c->pending) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, p.a, p.b);
@@ -248,7 +257,15 @@ cudaEvent_t ev_get(scg_ctx *c) {
 }
 
 template <typename Kern, typename... Args>
+void launch_on(scg_ctx *c, cudaStream_t stream, bool pdl, int cls, double bytes, Kern kern, dim3 grid, dim3 block,
+               size_t smem, Args... args);
+template <typename Kern, typename... Args>
 void launch_smem(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 block, size_t smem, Args... args) {
+  launch_on(c, c->stream, c->pdl, cls, bytes, kern, grid, block, smem, args...);
+}
+template <typename Kern, typename... Args>
+void launch_on(scg_ctx *c, cudaStream_t stream, bool pdl, int cls, double bytes, Kern kern, dim3 grid, dim3 block,
+               size_t smem, Args... args) {
   // SCG_PROFILE: CUDA events around every prof_every-th launch of each kernel class (events
   // between kernels serialize programmatic launches; timing all of them costs ~5% on c3)
   const bool prof = (c->flags & SCG_PROFILE) != 0 && c->kl[cls] % c->prof_every == 0;
@@ -259,14 +276,14 @@ void launch_smem(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 b
     p.a = ev_get(c);
     p.b = ev_get(c);
     p.cls = cls;
-    cudaEventRecord(p.a, c->stream);
+    cudaEventRecord(p.a, stream);
   }
-  if (c->pdl) {  // programmatic dependent launch (kernels.cuh pdl_entry)
+  if (pdl) {  // programmatic dependent launch (kernels.cuh pdl_entry)
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
-    cfg.stream = c->stream;
+    cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -274,10 +291,10 @@ void launch_smem(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 b
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, kern, args...);
   } else {
-    kern<<<grid, block, smem, c->stream>>>(args...);
+    kern<<<grid, block, smem, stream>>>(args...);
   }
   if (prof) {
-    cudaEventRecord(p.b, c->stream);
+    cudaEventRecord(p.b, stream);
     c->pending.push_back(p);
   }
   c->kl[cls]++;
@@ -404,7 +421,7 @@ void free_shard(Shard *s) {
                   s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
                   s->sc, s->slots, s->dlog, s->longrows, s->sell_col, s->sell_meta, s->sell_val,
                   s->mask, s->mb, s->peerG, s->peerMB, s->orig, s->V, s->ckr, s->work, s->gflag, s->ell_col,
-                  s->ell_val};
+                  s->ell_val, s->gB};
   for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -640,8 +657,10 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   s->grid_b = grid_for(nl, std::max(1, occ) * c->nsm);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_combine, kBlock, 0);
   s->grid_comb = grid_for(nl, std::max(1, occ) * c->nsm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dual_sketch<false>, kBlock, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dual_sketch<false, true>, kBlock, 0);
   s->grid_dual = grid_for(nl, std::max(1, occ) * c->nsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dual_sketch<false, false>, kBlock, 0);
+  s->grid_dual_s = grid_for(nl, std::max(1, occ) * c->nsm);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_norm_x, kBlock, 0);
   s->grid_norm = grid_for(nl, std::max(1, occ) * c->nsm);
   cudaFuncSetAttribute((const void *)k_lanczos_b_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BSmem));
@@ -1076,6 +1095,12 @@ void sketchycgal_destroy(scg_ctx *c) {
   if (c->dred) cudaFree(c->dred);
   for (auto &p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto e : c->evpool) cudaEventDestroy(e);
+  if (c->side) {
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+  }
+  if (c->evA) cudaEventDestroy(c->evA);
+  if (c->evB) cudaEventDestroy(c->evB);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1169,7 +1194,9 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
   if (cuda_stream) c->stream = (cudaStream_t)cuda_stream;
   else {
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bad(SCG_ECUDA);
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);  // (lo = least urgent, hi = most urgent)
+    if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi) != cudaSuccess) return bad(SCG_ECUDA);
     c->own_stream = true;
   }
   scg_status st;
@@ -1271,10 +1298,25 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
     launch(c, KC_OTHER, 0.0, k_init_d, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z, (const double *)s->y,
            (const double *)s->cdiag, s->d, (int)s->nl, c->b, beta1, c->box ? 1 : 0, c->klo, c->khi);
   }
+  // one GPU: draw each next start vector on a lower-priority side stream during the Lanczos passes
+  // (SCG_FUSED_RNG keeps the draw inside k_dual_sketch, as sharded runs always do)
+  c->side_rng = world == 1 && !(flags & SCG_FUSED_RNG);
+  if (c->side_rng) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    Shard *s = c->sh[0];
+    if (cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->evA, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->evB, cudaEventDisableTiming) != cudaSuccess ||
+        cudaMalloc(&s->gB, sizeof(double) * (size_t)c->npad) != cudaSuccess ||
+        cudaMemsetAsync(s->gB, 0, sizeof(double) * (size_t)c->npad, c->stream) != cudaSuccess)
+      return bad(fail(c, SCG_ECUDA, "side stream"));
+  }
   const unsigned long long E1 = ++c->epoch;
   for (Shard *s : c->sh)
-    launch(c, KC_OTHER, 0.0, k_gen_start, dim3(s->grid_rows), dim3(kBlock), c->wslot(s, 0), (int)s->nl,
-           (long long)s->rb, seed, (long long)1, s->slots + SLOT_NU0, s->sc, net_of(c, s, E1), (const int *)s->orig);
+    launch(c, KC_OTHER, 0.0, k_gen_start, dim3(s->grid_rows), dim3(kBlock), c->gslot(s, 1), (int)s->nl,
+           (long long)s->rb, seed, (long long)1, s->slots + SLOT_NU0, s->sc, net_of(c, s, E1), (const int *)s->orig,
+           (int)FK_RHO0);
   pull_all(c, FK_RHO0, 1, E1, FinArgs{});
   if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) return bad(SCG_ECUDA);
   tick("layout+omega");
@@ -1342,9 +1384,19 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       }
     }
     auto slot = [&](const Shard *s, int j) -> double * {  // buffer holding w_j (j >= 1; w_1 = g)
+      if (j == 1) return c->gslot(s, t);
       if (c->store) return c->wslot(s, j - 1);
-      return j == 1 ? c->wslot(s, 0) : c->wslot(s, 1 + (j & 1));
+      return c->wslot(s, 1 + (j & 1));
     };
+    if (c->side_rng) {  // draw g_{t+1} into the buffer iteration t-1 used, once its readers are done
+      Shard *s = c->sh[0];
+      cudaEventRecord(c->evA, c->stream);
+      cudaStreamWaitEvent(c->side, c->evA, 0);
+      launch_on(c, c->side, false, KC_GEN, 8.0 * (double)s->nl, k_gen_start, dim3(grid_for(s->nl, 64 * c->nsm)),
+                dim3(kBlock), 0, c->gslot(s, t + 1), (int)s->nl, (long long)s->rb, c->seed, (long long)(t + 1),
+                s->slots + SLOT_GEN, s->sc, net_of(c, s, 0), (const int *)s->orig, (int)FK_GEN);
+      cudaEventRecord(c->evB, c->side);
+    }
     // ---- Lanczos pass 1 (Alg. 2 lines 1-9)
     if (c->fused && c->world == 1) {  // all q steps in one persistent launch
       Shard *s = c->sh[0];
@@ -1355,7 +1407,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       const unsigned long long eb = c->gphase;
       c->gphase += 2ull * (unsigned long long)q;
       launch_coop(c, KC_PASS1, q * s->kb[KC_LANCZOS_A] + (q - 1) * s->kb[KC_LANCZOS_B], kP, dim3(s->grid_a),
-                  dim3(kBlockA), C, TT, (const double *)s->d, s->G, (long long)c->npad, c->store ? 1 : 0, q,
+                  dim3(kBlockA), C, TT, (const double *)s->d, s->G, slot(s, 1), (long long)c->npad, c->store ? 1 : 0, q,
                   (int)s->nl, s->a, s->slots + SLOT_OM, s->slots + SLOT_RHO, s->sc, net_of(c, s, E), s->gflag, eb);
     } else
     for (int i = 1; i <= q; ++i) {
@@ -1398,7 +1450,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       const unsigned long long E = ++c->epoch;
       for (Shard *s : c->sh)
         launch(c, KC_COMBINE, 8.0 * (double)s->nl * (double)q + 8.0 * (double)s->nl, k_combine, dim3(s->grid_comb),
-               dim3(kBlock), (const double *)c->wslot(s, 0), (long long)c->npad, c->xg(s), (int)s->nl,
+               dim3(kBlock), (const double *)slot(s, 1), (const double *)c->wslot(s, 0), (long long)c->npad, c->xg(s), (int)s->nl,
                (long long)s->rb, s->slots + SLOT_XX, s->sc, net_of(c, s, E));
       pull_all(c, FK_NUX, 1, E, FinArgs{});
     } else {  // ---- pass 2 (line 13): regenerate v_2..v_k
@@ -1420,7 +1472,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       const unsigned long long E = ++c->epoch;
       for (Shard *s : c->sh)
         launch(c, KC_NORM_X, s->kb[KC_NORM_X], k_norm_x, dim3(s->grid_norm), dim3(kBlock),
-               (const double *)c->wslot(s, 0), c->xg(s), (int)s->nl, (long long)s->rb, s->slots + SLOT_XX, s->sc,
+               (const double *)slot(s, 1), c->xg(s), (int)s->nl, (long long)s->rb, s->slots + SLOT_XX, s->sc,
                net_of(c, s, E));
       pull_all(c, FK_NUX, 1, E, FinArgs{});
     }
@@ -1447,11 +1499,16 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       pull_all(c, FK_NZ, 1, E, f);
     }
     E = ++c->epoch;
-    for (Shard *s : c->sh)
-      launch(c, KC_DUAL_SKETCH, s->kb[KC_DUAL_SKETCH], c->box ? k_dual_sketch<true> : k_dual_sketch<false>, dim3(s->grid_dual), dim3(kBlock),
+    if (c->side_rng) cudaStreamWaitEvent(c->stream, c->evB, 0);  // g_{t+1} and its norm are drawn
+    for (Shard *s : c->sh) {
+      auto kD = c->side_rng ? (c->box ? k_dual_sketch<true, false> : k_dual_sketch<false, false>)
+                            : (c->box ? k_dual_sketch<true, true> : k_dual_sketch<false, true>);
+      launch(c, KC_DUAL_SKETCH, c->side_rng ? 40.0 * (double)s->nl : s->kb[KC_DUAL_SKETCH], kD,
+             dim3(c->side_rng ? s->grid_dual_s : s->grid_dual), dim3(kBlock),
              (const double *)s->z, s->y, s->d, (const double *)s->cdiag, s->ckr, js, c->wslot(s, 0),
              (int)s->nl, (long long)s->rb, c->R, A, c->seed, s->slots + SLOT_NU0, s->sc, net_of(c, s, E),
              (const int *)s->orig);
+    }
     pull_all(c, FK_RHO0M, 5, E, FinArgs{});
     c->ome[js] = A.one_m_eta;
     c->vlast = js;
