@@ -201,8 +201,11 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     L = si.laplacian(args.config)
     c = si.CONFIGS[args.config]
-    stream = torch.cuda.Stream()
+    # the library's stream at the highest priority: the next Lanczos start vector is drawn on a
+    # lower-priority side stream in the gaps
+    stream = torch.cuda.Stream(priority=-100)
     W, K = args.warmup, args.steps
+    opts = parse_opts(args.opts)
     dkw = {}
     if world > 1:
         # one process per GPU: rows sharded over the ranks; torch.distributed only
@@ -222,7 +225,7 @@ def run_ours(args, rank, world, local_rank):
 
     with torch.cuda.stream(stream):
         solver = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], profile=not args.no_profile, device=local_rank,
-                                 stream=ctypes_stream(stream), **dkw)
+                                 stream=ctypes_stream(stream), **dkw, **opts)
         solver.step(W)
         solver.synchronize()
         solver.reset_stats()
@@ -311,6 +314,15 @@ def gpu_window_rate(scg, L, c, tw, dev):
     return tw / (e0.elapsed_time(e1) / 1e3)
 
 
+def parse_opts(spec):
+    """--opts key=0|1,... -> SketchyCGAL execution options (bitwise-neutral, for A/B runs)."""
+    out = {}
+    for kv in filter(None, (spec or "").split(",")):
+        k, v = kv.split("=")
+        out[k.strip()] = bool(int(v))
+    return out
+
+
 def ctypes_stream(stream):
     import ctypes
     return ctypes.c_void_p(stream.cuda_stream)
@@ -372,6 +384,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="no per-kernel events (no roofline line)")
+    ap.add_argument("--opts", default="", help="execution options, e.g. side_rng=0,ell=1 (A/B runs)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:  # not under torchrun: relaunch one process per GPU
         import random

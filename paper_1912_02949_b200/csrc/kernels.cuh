@@ -173,7 +173,8 @@ __device__ __forceinline__ double div_rn(double a, double b, double rb) {
 // R27; long rows are listed at init (longest first) and taken by the first warps of the
 // grid so they start early.
 constexpr int kMinBlocksUni = 3;  // min blocks per SM of the uniform-weight SELL SpMV kernels (80-register cap)
-constexpr int kMinBlocksEll = 4;  // min blocks per SM of the ELL SpMV kernels (64-register cap)
+// min blocks per SM of the ELL SpMV kernels: 64-register cap up to W = 4, wider rows need more stage registers
+constexpr int ell_min_blocks(int W, bool uni) { return W <= 4 ? 4 : (uni ? 3 : 2); }
 constexpr int kLongRow = 32;
 
 struct Rows {
@@ -504,11 +505,22 @@ __device__ __forceinline__ int seg_shift(long long i0) { return (int)(((i0 * ES)
 // ---------------------------------------------------------------- ELL-W engine
 // Every row has at most W off-diagonal entries (W a compile-time constant): slices of 32 rows
 // with exactly W slots each, so a slice's column block sits at a computed offset -- no slice
-// metadata, no dependent meta load, no width switch.  Each warp walks its block's slices with
-// a three-stage register pipeline: while slice i is computed, the gathers of slice i+1 (their
-// columns arrived during the previous step) and the columns and own entries of slice i+2 are in
-// flight.  Per row the arithmetic is spmv_rows' CAC-3 single chain (reading R27 needs no strided
-// chains here: every row has <= 32 entries), padding slots add fma(-m, +0, acc) == acc.
+// metadata, no dependent meta load, no width switch.  Each warp walks its block's slices with a
+// register pipeline: while slice i is computed, the gathers of slice i+1, the own entries (x_r,
+// d_r) of slice i+2 and the columns of slice i+3 are in flight -- the column stream gets two
+// steps of slack before its gathers are issued (one step left the DRAM latency exposed: ncu put
+// half of the stall samples on the first use of the columns).  Once a slice's gathers are issued
+// its columns are dead; only their sign bits (uniform weights) travel on, packed in one word.
+// Per row the arithmetic is the CAC-3 single chain (every row has <= 32 entries, reading R27);
+// padding slots add fma(-m, +0, acc) == acc.
+__device__ __forceinline__ const double *gaddr(const double *X, int c) {
+  // X + (c & 0x7fffffff) as one 32x32->64 multiply-add (the compiler otherwise builds the 64-bit
+  // offset with six integer instructions)
+  const double *p;
+  asm("mad.wide.u32 %0, %1, 8, %2;" : "=l"(p) : "r"((unsigned)c & 0x7fffffffu), "l"(X));
+  return p;
+}
+
 template <int NC, bool UNI, int W, class Epi>
 __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restrict__ X, double den,
                                          const double *__restrict__ diag0, const double *__restrict__ diag1,
@@ -524,25 +536,31 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
   const double *__restrict__ ev = RL.eval + lane;
   const int padc = RL.padc;
   const double m0 = RL.m0;
-  auto cload = [&](int q, int (&c)[W], double (&v)[W]) {
+  auto cload = [&](int q, int (&c)[W]) {
     if (q < s_end) {
-      const long long b = (long long)q * (32 * W);
+      const int *cp = ec + (long long)q * (32 * W);
 #pragma unroll
-      for (int u = 0; u < W; ++u) {
-        c[u] = __ldg(ec + b + 32 * u);
-        if (!UNI) v[u] = __ldg(ev + b + 32 * u);
-      }
+      for (int u = 0; u < W; ++u) c[u] = __ldg(cp + 32 * u);
     } else {
 #pragma unroll
-      for (int u = 0; u < W; ++u) {
-        c[u] = padc;
-        if (!UNI) v[u] = -0.0;
-      }
+      for (int u = 0; u < W; ++u) c[u] = padc;
     }
   };
-  auto gload = [&](const int (&c)[W], double (&g)[W]) {
+  // gathers of slice q from its columns; values (non-uniform weights) travel with the gathers;
+  // returns the packed sign bits of the uniform coefficients (bit u = slot u negative)
+  auto gload = [&](int q, const int (&c)[W], double (&g)[W], double (&v)[W]) -> unsigned {
+    unsigned sg = 0u;
 #pragma unroll
-    for (int u = 0; u < W; ++u) g[u] = __ldg(X + ((unsigned)c[u] & 0x7fffffffu));  // one IMAD.WIDE.U32 per address
+    for (int u = 0; u < W; ++u) {
+      g[u] = __ldg(gaddr(X, c[u]));
+      if (UNI) sg |= ((unsigned)c[u] >> 31) << u;
+    }
+    if (!UNI) {
+      const double *vp = ev + (long long)q * (32 * W);
+#pragma unroll
+      for (int u = 0; u < W; ++u) v[u] = q < s_end ? __ldg(vp + 32 * u) : -0.0;
+    }
+    return sg;
   };
   auto oload = [&](int q, double &xo, double &dd0, double &dd1) {
     const int p = q * 32 + lane;
@@ -555,21 +573,26 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
       if (NC > 1) dd1 = diag1[p];
     }
   };
-  int c0[W], c1[W];
-  double v0[W], v1[W], g0[W];
+  int cb[W], cc[W];
+  double g0[W], v0[W];
   double xo0, d00, d10, xo1, d01, d11;
-  cload(sl, c0, v0);
-  oload(sl, xo0, d00, d10);
-  gload(c0, g0);
-  cload(sl + wstep, c1, v1);
+  unsigned s0;
+  {
+    int ca[W];
+    cload(sl, ca);
+    oload(sl, xo0, d00, d10);
+    s0 = gload(sl, ca, g0, v0);
+  }
+  cload(sl + wstep, cb);
   oload(sl + wstep, xo1, d01, d11);
+  cload(sl + 2 * wstep, cc);
   for (; sl < s_end; sl += wstep) {
-    double g1[W];
-    gload(c1, g1);  // gathers of slice i+1
-    int c2[W];
-    double v2[W], xo2, d02, d12;
-    cload(sl + 2 * wstep, c2, v2);  // columns and own entries of slice i+2
-    oload(sl + 2 * wstep, xo2, d02, d12);
+    double g1[W], v1[W];
+    const unsigned s1 = gload(sl + wstep, cb, g1, v1);  // gathers of slice i+1
+    int cd[W];
+    cload(sl + 3 * wstep, cd);                         // columns of slice i+3
+    double xo2, d02, d12;
+    oload(sl + 2 * wstep, xo2, d02, d12);              // own entries of slice i+2
     // compute slice i
     const int p = sl * 32 + lane;
     RowOut<NC> o;
@@ -581,9 +604,9 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
     for (int u = 0; u < W; ++u) {
       double x = g0[u] * rden;
       if (UNI) {
-        // fma(-m0, x, acc) == fma(m0, -x, acc) exactly: the coefficient's sign (bit 31 of the column
-        // code) is moved onto x with one XOR of its high word
-        x = __hiloint2double(__double2hiint(x) ^ (c0[u] & (int)0x80000000), __double2loint(x));
+        // fma(-m0, x, acc) == fma(m0, -x, acc) exactly: the coefficient's sign is moved onto x
+        // with one XOR of its high word
+        x = __hiloint2double(__double2hiint(x) ^ (int)(((s0 >> u) & 1u) << 31), __double2loint(x));
 #pragma unroll
         for (int t = 0; t < NC; ++t) o.s[t] = fma(m0, x, o.s[t]);
       } else {
@@ -594,11 +617,12 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
     if (p < nl) epi(o);
 #pragma unroll
     for (int u = 0; u < W; ++u) {
-      c0[u] = c1[u];
-      c1[u] = c2[u];
+      cb[u] = cc[u];
+      cc[u] = cd[u];
       g0[u] = g1[u];
-      if (!UNI) { v0[u] = v1[u]; v1[u] = v2[u]; }
+      if (!UNI) v0[u] = v1[u];
     }
+    s0 = s1;
     xo0 = xo1; d00 = d01; d10 = d11;
     xo1 = xo2; d01 = d02; d11 = d12;
   }
@@ -997,7 +1021,7 @@ struct EpiA {
 };
 
 template <bool UNI, int W>  // W > 0: ELL-W layout (spmv_ell), 0: SELL + long rows
-__global__ void __launch_bounds__(kBlockA, W > 0 ? kMinBlocksEll : (UNI ? kMinBlocksUni : 2)) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
+__global__ void __launch_bounds__(kBlockA, W > 0 ? ell_min_blocks(W, UNI) : (UNI ? kMinBlocksUni : 2)) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ X, int nl, long long rb, int i,
                                                          double *__restrict__ a, XSlot *slot, DevScalars *sc,
                                                          Net net) {
@@ -1709,7 +1733,7 @@ struct EpiC {
 };
 
 template <bool UNI, int W>
-__global__ void __launch_bounds__(kBlock, W > 0 ? kMinBlocksEll : (UNI ? kMinBlocksUni : 2)) k_lanczos_c(Csr C, Rows RL, const double *__restrict__ d,
+__global__ void __launch_bounds__(kBlock, W > 0 ? ell_min_blocks(W, UNI) : (UNI ? kMinBlocksUni : 2)) k_lanczos_c(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ Xj, const double *Xjm1,
                                                          double *Xjp1, double *__restrict__ x, int nl, long long rb,
                                                          int j, DevScalars *sc, XSlot *slot, Net net) {

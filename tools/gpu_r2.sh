@@ -12,6 +12,9 @@ for w in "$@"; do
     tests) timeout 1500 python -m pytest tests -m gpu -q -x --durations=25 > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log ;;
     tests:*) timeout 1500 python -m pytest tests -m gpu -q -x --durations=25 -k "${w#tests:}" > $O/pytest_gpu_k.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu_k.log ;;
     bench) timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err; echo "bench exit $?" >> $O/bench.err ;;
+    ab:*)  # ab:<opts> -- bench with execution options (no cpu / e2e legs)
+      OPTS=${w#ab:}; N=${OPTS//[^a-zA-Z0-9_]/_}
+      timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 --no-cpu --no-e2e --opts "$OPTS" > $O/ab_$N.json 2> $O/ab_$N.err; echo "exit $?" >> $O/ab_$N.err ;;
     benchnocpu) timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 --no-cpu > $O/bench.json 2> $O/bench.err; echo "bench exit $?" >> $O/bench.err ;;
     full) timeout 900 python bench.py --steps 997 --warmup 3 --no-cpu --no-e2e > $O/bench_full.json 2> $O/bench_full.err; echo "exit $?" >> $O/bench_full.err ;;
     ref) timeout 900 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $O/ref.json 2> $O/ref.err; echo "ref exit $?" >> $O/ref.err ;;
