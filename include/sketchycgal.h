@@ -54,7 +54,8 @@ typedef enum {
   SCG_ECHOL = -5,    /* Nystrom reconstruction: Cholesky failed after 40 shift doublings */
   SCG_ESTATE = -6,   /* call on a failed context, or out of order (e.g. objective before reconstruct) */
   SCG_ERANGE = -7,   /* a summand of an exact sum was non-finite or >= 2^100 (DESIGN.md CAC-2) */
-  SCG_EUNSUPPORTED = -8
+  SCG_EUNSUPPORTED = -8,
+  SCG_ECOMM = -9     /* a host transport callback (scg_host_comm) failed */
 } scg_status;
 
 /* init flags */
@@ -111,21 +112,42 @@ typedef struct {
  * global sums (CAC-2) combine through per-rank device mailboxes, so the iterates
  * are bitwise identical for every world size.  world <= 8.
  *
- *   emulate = 0: one process per GPU (NCCL transport for setup: CUDA IPC handle
- *     exchange and the one-shot reconstruction reductions).  Every rank passes its
- *     own rows in scg_csr (row_begin = row_splits[rank], row_end = row_splits[rank+1]),
- *     the same row_splits (required when world > 1), and the same 128-byte NCCL
- *     unique id, created on rank 0 (sketchycgal_nccl_unique_id) and broadcast by the
- *     caller, e.g. through torch.distributed.
+ *   emulate = 0: one process per rank (setup transport for the CUDA IPC handle exchange,
+ *     the row-label exchange and the one-shot reconstruction reductions: NCCL, or the
+ *     caller's scg_host_comm).  Every rank passes its own rows in scg_csr
+ *     (row_begin = row_splits[rank], row_end = row_splits[rank+1]), the same row_splits
+ *     (required when world > 1), and either host_comm or the same 128-byte NCCL unique
+ *     id, created on rank 0 (sketchycgal_nccl_unique_id) and broadcast by the caller,
+ *     e.g. through torch.distributed.
  *   emulate = 1: all `world` shards live in this one context on one device (peers are
  *     the other shards' buffers, no NCCL).  scg_csr holds ALL rows; row_splits may be
  *     NULL (balanced split, sketchycgal_row_splits).  Every per-row output of the
  *     context then covers all n rows.  This runs the sharded kernels on one GPU. */
+/* Host-side transport for the setup and one-shot exchanges of a multi-process run (emulate = 0),
+ * supplied by the caller (e.g. torch.distributed), instead of NCCL.  Every function is called
+ * collectively by all ranks in the same order and returns 0 on success.
+ *   allgather:     out (world * bytes, host) receives every rank's `in` (bytes, host) in rank order
+ *   allreduce_sum: in-place sum of count doubles (host) over the ranks
+ *   barrier:       returns once every rank has called it
+ *   sync_collectives = 1: before each device-side collective (the mailbox pull of an exact sum or a
+ *     halo barrier) the caller's stream is synchronized and the ranks meet in `barrier`, and the pull
+ *     then only checks the peers' flags (an absent flag is an error, never a wait).  No kernel ever
+ *     waits for another rank's kernel: ranks may share a GPU (tests), at the cost of one host round
+ *     trip per collective.  0: the pulls wait on the device (one process per GPU). */
+typedef struct {
+  void *ctx;
+  int32_t (*allgather)(void *ctx, const void *in, void *out, int64_t bytes);
+  int32_t (*allreduce_sum)(void *ctx, double *buf, int64_t count);
+  int32_t (*barrier)(void *ctx);
+  int32_t sync_collectives;
+} scg_host_comm;
+
 typedef struct {
   int32_t rank, world;
-  const void *nccl_unique_id;   /* host, 128 bytes (emulate = 0) */
+  const void *nccl_unique_id;   /* host, 128 bytes (emulate = 0 without host_comm) */
   const int64_t *row_splits;    /* host, world + 1 ascending offsets, [0] = 0, [world] = n; may be NULL if emulate */
   int32_t emulate;
+  const scg_host_comm *host_comm; /* emulate = 0: setup transport; NULL = NCCL (nccl_unique_id required) */
 } scg_dist;
 
 /* One record per iteration t (Alg. 4), original units where noted. */

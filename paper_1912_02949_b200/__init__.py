@@ -37,7 +37,7 @@ SCG_NO_ELL = 1 << 14
 SCG_FUSED_RNG = 1 << 15
 
 STATUS = {0: "SCG_OK", -1: "SCG_EINVAL", -2: "SCG_ENOMEM", -3: "SCG_ECUDA", -4: "SCG_ENCCL", -5: "SCG_ECHOL",
-          -6: "SCG_ESTATE", -7: "SCG_ERANGE", -8: "SCG_EUNSUPPORTED"}
+          -6: "SCG_ESTATE", -7: "SCG_ERANGE", -8: "SCG_EUNSUPPORTED", -9: "SCG_ECOMM"}
 
 
 def _nccl_paths():
@@ -94,9 +94,65 @@ class Csr(ctypes.Structure):
                 ("has_diagonal", ctypes.c_int32)]
 
 
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int64)
+BARRIER_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p)
+
+
+class HostCommStruct(ctypes.Structure):
+    _fields_ = [("ctx", ctypes.c_void_p), ("allgather", ALLGATHER_FN), ("allreduce_sum", ALLREDUCE_FN),
+                ("barrier", BARRIER_FN), ("sync_collectives", ctypes.c_int32)]
+
+
 class Dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
-                ("row_splits", ctypes.c_void_p), ("emulate", ctypes.c_int32)]
+                ("row_splits", ctypes.c_void_p), ("emulate", ctypes.c_int32),
+                ("host_comm", ctypes.POINTER(HostCommStruct))]
+
+
+class TorchHostComm:
+    """scg_host_comm over torch.distributed (any backend with CPU tensors, e.g. gloo): the setup and
+    one-shot exchanges of a multi-process run without NCCL.  ``sync_collectives=True`` makes every
+    device collective meet on the host first (ranks may then share one GPU: no kernel ever waits for
+    another rank's kernel) -- include/sketchycgal.h."""
+
+    def __init__(self, group=None, sync_collectives: bool = True):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.world = dist.get_world_size(group)
+
+        def allgather(ctx, src, dst, nbytes):
+            try:
+                import torch
+                t = torch.frombuffer(bytearray(ctypes.string_at(src, nbytes)), dtype=torch.uint8)
+                out = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(self.world)]
+                dist.all_gather(out, t, group=self.group)
+                buf = b"".join(o.numpy().tobytes() for o in out)
+                ctypes.memmove(dst, buf, len(buf))
+                return 0
+            except Exception:
+                return -1
+
+        def allreduce_sum(ctx, buf, count):
+            try:
+                import torch
+                a = np.ctypeslib.as_array(buf, shape=(count,))
+                t = torch.from_numpy(a.copy())
+                dist.all_reduce(t, group=self.group)
+                a[:] = t.numpy()
+                return 0
+            except Exception:
+                return -1
+
+        def barrier(ctx):
+            try:
+                dist.barrier(group=self.group)
+                return 0
+            except Exception:
+                return -1
+
+        self._fns = (ALLGATHER_FN(allgather), ALLREDUCE_FN(allreduce_sum), BARRIER_FN(barrier))
+        self.struct = HostCommStruct(None, *self._fns, 1 if sync_collectives else 0)
 
 
 EXPORTS = ["sketchycgal_maxcut_init", "sketchycgal_step", "sketchycgal_synchronize", "sketchycgal_reconstruct",
@@ -235,7 +291,7 @@ class SketchyCGAL:
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None, ineq: bool = False,
                  box: tuple | None = None, pdl: bool = True, fused_pass1: bool = False, ws_spmv: bool = False,
                  tma_b: bool = False, debug_log: bool = False, qfix: int = 0, ell: bool = True,
-                 side_rng: bool = True):
+                 side_rng: bool = True, host_comm: "TorchHostComm | None" = None):
         self.lib = load()
         self.n = int(L.n)
         self.R = int(R)
@@ -246,8 +302,10 @@ class SketchyCGAL:
             sp = row_splits(L.row_ptr, P) if splits is None else _c64(splits, np.int64)
             self._splits = sp
             self._uid = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+            self._host_comm = host_comm  # keeps the callbacks alive for the context's lifetime
             dist = Dist(0 if shards > 1 else int(rank), int(P), ctypes.addressof(self._uid) if self._uid else None,
-                        sp.ctypes.data, 1 if shards > 1 else 0)
+                        sp.ctypes.data, 1 if shards > 1 else 0,
+                        ctypes.pointer(host_comm.struct) if (host_comm is not None and shards <= 1) else None)
         if world > 1 and shards <= 1:
             self.row_begin, self.row_end = int(self._splits[rank]), int(self._splits[rank + 1])
         else:

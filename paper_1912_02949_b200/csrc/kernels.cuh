@@ -106,6 +106,7 @@ struct Net {
   Mailbox *const *peerMB;     // [P] every rank's mailbox
   Mailbox *mb;                // own mailbox
   int P, me;
+  int nowait;                 // the host synchronized the ranks before this pull: check the flags once
   unsigned long long E;       // epoch of the collective this launch takes part in
 };
 
@@ -885,7 +886,7 @@ __global__ void k_pull(int kind, int ns, Net net, DevScalars *sc, FinArgs f) {
   if (lane < net.P) {
     const long long t0 = clock64();
     while (ld_acquire_sys(&m->flag[e][lane]) != net.E) {
-      if (clock64() - t0 > (1ll << 34)) {
+      if (net.nowait || clock64() - t0 > (1ll << 34)) {  // (nowait: every producer has completed)
         ok = 0;
         break;
       }

@@ -161,6 +161,8 @@ struct scg_ctx {
 #ifdef SCG_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
+  bool hcomm = false;     // multi-process setup transport: the caller's host callbacks (else NCCL)
+  scg_host_comm hc{};
   double *dred = nullptr;  // device scratch for host all-reduces (mode 2)
   int64_t t = 0;
   int64_t launches = 0;
@@ -384,6 +386,7 @@ Net net_of(const scg_ctx *c, const Shard *s, unsigned long long E) {
   n.mb = s->mb;
   n.P = c->world;
   n.me = s->rank;
+  n.nowait = c->hcomm && c->hc.sync_collectives ? 1 : 0;
   n.E = E;
   return n;
 }
@@ -392,6 +395,12 @@ Net net_of(const scg_ctx *c, const Shard *s, unsigned long long E) {
 // for all ranks' contributions to epoch E and finalizes.
 void pull_all(scg_ctx *c, int kind, int ns, unsigned long long E, const FinArgs &f0) {
   if (c->world <= 1) return;
+  if (c->hcomm && c->hc.sync_collectives) {  // ranks sharing a GPU: meet on the host, the pull only checks
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess || c->hc.barrier(c->hc.ctx) != 0) {
+      c->failed = 1;
+      c->err_msg = "host barrier before a collective failed";
+    }
+  }
   for (Shard *s : c->sh) {
     FinArgs f = f0;
     if (kind == FK_NZ) f.log = s->dlog;
@@ -403,6 +412,10 @@ void pull_all(scg_ctx *c, int kind, int ns, unsigned long long E, const FinArgs 
 // Sum a small host vector over the ranks of a multi-process job (identity otherwise).
 scg_status host_allreduce(scg_ctx *c, std::vector<double> &v) {
   if (c->mode != 2 || c->world <= 1 || v.empty()) return SCG_OK;
+  if (c->hcomm) {
+    if (c->hc.allreduce_sum(c->hc.ctx, v.data(), (int64_t)v.size()) != 0) return fail(c, SCG_ECOMM, "host allreduce");
+    return SCG_OK;
+  }
 #ifdef SCG_WITH_NCCL
   const size_t bytes = sizeof(double) * v.size();
   if (v.size() > (size_t)kMaxR * kMaxR * 4) return fail(c, SCG_EINVAL, "host_allreduce: vector too long");
@@ -471,6 +484,19 @@ scg_status build_gmap(scg_ctx *c) {
     for (Shard *s : c->sh)
 #pragma omp parallel for schedule(static, 65536)
       for (int64_t nu = 0; nu < s->nl; ++nu) c->gmap[(size_t)(s->rb + s->origloc[(size_t)nu])] = (int)(s->rb + nu);
+    return SCG_OK;
+  }
+  if (c->hcomm) {  // every rank's origloc (padded to the largest shard) through the host allgather
+    int64_t mx = 0;
+    for (int q = 0; q < c->world; ++q) mx = std::max<int64_t>(mx, c->splits[(size_t)q + 1] - c->splits[(size_t)q]);
+    std::vector<int> mine((size_t)mx, 0), all((size_t)mx * c->world);
+    std::copy(c->sh[0]->origloc.begin(), c->sh[0]->origloc.end(), mine.begin());
+    if (c->hc.allgather(c->hc.ctx, mine.data(), all.data(), (int64_t)sizeof(int) * mx) != 0)
+      return fail(c, SCG_ECOMM, "host allgather (row labels)");
+    for (int q = 0; q < c->world; ++q) {
+      const int64_t a = c->splits[(size_t)q], b = c->splits[(size_t)q + 1];
+      for (int64_t nu = 0; nu < b - a; ++nu) c->gmap[(size_t)(a + all[(size_t)(q * mx + nu)])] = (int)(a + nu);
+    }
     return SCG_OK;
   }
 #ifdef SCG_WITH_NCCL
@@ -925,21 +951,28 @@ scg_status connect_peers(scg_ctx *c, const void *uid) {
   if (c->mode == 1 || P == 1) {
     for (Shard *s : c->sh) { hG[s->rank] = s->G; hM[s->rank] = s->mb; }
   } else {
-#ifdef SCG_WITH_NCCL
     Shard *s = c->sh[0];
     (void)uid;  // the communicator was created at the start of init
     cudaIpcMemHandle_t hh[2];
     CK(cudaIpcGetMemHandle(&hh[0], s->G));
     CK(cudaIpcGetMemHandle(&hh[1], s->mb));
-    char *dbuf = nullptr;
     const size_t per = sizeof(hh);
-    CK(cudaMalloc(&dbuf, per * P));
-    CK(cudaMemcpyAsync(dbuf + per * c->rank, hh, per, cudaMemcpyHostToDevice, c->stream));
-    NK(ncclAllGather(dbuf + per * c->rank, dbuf, per, ncclChar, c->comm, c->stream));
     std::vector<cudaIpcMemHandle_t> all((size_t)2 * P);
-    CK(cudaMemcpyAsync(all.data(), dbuf, per * P, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    cudaFree(dbuf);
+    if (c->hcomm) {
+      if (c->hc.allgather(c->hc.ctx, hh, all.data(), (int64_t)per) != 0) return fail(c, SCG_ECOMM, "host allgather (IPC)");
+    } else {
+#ifdef SCG_WITH_NCCL
+      char *dbuf = nullptr;
+      CK(cudaMalloc(&dbuf, per * P));
+      CK(cudaMemcpyAsync(dbuf + per * c->rank, hh, per, cudaMemcpyHostToDevice, c->stream));
+      NK(ncclAllGather(dbuf + per * c->rank, dbuf, per, ncclChar, c->comm, c->stream));
+      CK(cudaMemcpyAsync(all.data(), dbuf, per * P, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      cudaFree(dbuf);
+#else
+      return fail(c, SCG_EUNSUPPORTED, "multi-process sharding needs the NCCL build or a host transport");
+#endif
+    }
     for (int q = 0; q < P; ++q) {
       if (q == c->rank) { hG[q] = s->G; hM[q] = s->mb; continue; }
       void *pg = nullptr, *pm = nullptr;
@@ -950,22 +983,22 @@ scg_status connect_peers(scg_ctx *c, const void *uid) {
       hG[q] = (double *)pg;
       hM[q] = (Mailbox *)pm;
     }
-#else
-    (void)uid;
-    return fail(c, SCG_EUNSUPPORTED, "multi-process sharding needs the NCCL build");
-#endif
   }
   for (Shard *s : c->sh) {
     CK(cudaMemcpyAsync(s->peerG, hG.data(), sizeof(double *) * P, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(s->peerMB, hM.data(), sizeof(Mailbox *) * P, cudaMemcpyHostToDevice, c->stream));
   }
   CK(cudaStreamSynchronize(c->stream));
-#ifdef SCG_WITH_NCCL
   if (c->mode == 2 && P > 1) {  // every rank's tables are in place before anyone stores to a peer
-    NK(ncclAllReduce(c->dred, c->dred, 1, ncclDouble, ncclSum, c->comm, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-  }
+    if (c->hcomm) {
+      if (c->hc.barrier(c->hc.ctx) != 0) return fail(c, SCG_ECOMM, "host barrier");
+    } else {
+#ifdef SCG_WITH_NCCL
+      NK(ncclAllReduce(c->dred, c->dred, 1, ncclDouble, ncclSum, c->comm, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
 #endif
+    }
+  }
   return SCG_OK;
 }
 
@@ -1163,7 +1196,13 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
     emulate = dist->emulate;
     rank = dist->rank;
     if (world > kMaxRanks || world > n || rank < 0 || rank >= world) return bad(SCG_EINVAL);
-    if (!emulate && (!dist->row_splits || !dist->nccl_unique_id)) return bad(SCG_EINVAL);
+    if (!emulate && (!dist->row_splits || (!dist->nccl_unique_id && !dist->host_comm))) return bad(SCG_EINVAL);
+    if (!emulate && dist->host_comm) {
+      const scg_host_comm *h = dist->host_comm;
+      if (!h->allgather || !h->allreduce_sum || !h->barrier) return bad(SCG_EINVAL);
+      c->hcomm = true;
+      c->hc = *h;
+    }
   }
   c->world = world;
   c->mode = world == 1 ? 0 : (emulate ? 1 : 2);
@@ -1202,14 +1241,14 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   scg_status st;
   const int nshard = c->mode == 1 ? world : 1;
 #ifdef SCG_WITH_NCCL
-  if (c->mode == 2) {
+  if (c->mode == 2 && !c->hcomm) {
     ncclUniqueId id;
     std::memcpy(&id, dist->nccl_unique_id, sizeof(id));
     if (ncclCommInitRank(&c->comm, world, id, c->rank) != ncclSuccess) return bad(SCG_ENCCL);
     if (cudaMalloc(&c->dred, sizeof(double) * kMaxR * kMaxR * 4) != cudaSuccess) return bad(SCG_ENOMEM);
   }
 #else
-  if (c->mode == 2) return bad(SCG_EUNSUPPORTED);
+  if (c->mode == 2 && !c->hcomm) return bad(SCG_EUNSUPPORTED);
 #endif
   // row relabeling within sorting windows (SELL engine), then the global id map
   for (int p = 0; p < nshard; ++p) {
@@ -1258,13 +1297,11 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   for (Shard *s : c->sh)
     if ((st = alloc_G(c, s, cap))) return bad(st);
   if ((st = connect_peers(c, dist ? dist->nccl_unique_id : nullptr))) return bad(st);
-#ifdef SCG_WITH_NCCL
   if (c->mode == 2) {  // agree on the storage mode (all ranks store, or none)
     std::vector<double> v{c->store ? 0.0 : 1.0};
     if ((st = host_allreduce(c, v))) return bad(st);
     if (v[0] != 0.0) c->store = false;  // some rank cannot store: all ranks run the two-pass form
   }
-#endif
 
   // ||L||_F (exact sum over all stored entries of all ranks) and C = -L / ||L||_F
   const unsigned long long E0 = ++c->epoch;
@@ -1515,6 +1552,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     if (++c->spend == kSketchB) sketch_flush(c);
     c->t = t;
   }
+  if (c->failed) return SCG_ECOMM;  // a host barrier of the transport failed (pull_all)
   CK(cudaGetLastError());
   c->have_recon = false;
   return SCG_OK;

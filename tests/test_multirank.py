@@ -84,3 +84,39 @@ def test_halo_plan_consistent_across_ranks(cfg):
     result = mgr.dict()
     mp.spawn(_worker, args=(world, port, cfg, result), nprocs=world, join=True)
     assert all(result[r] == 1 for r in range(world))
+
+
+def _comm_worker(rank, world, port, result):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import ctypes
+        hc = scg.TorchHostComm()
+        st = hc.struct
+        ok = True
+        # allgather: every rank contributes 24 bytes, receives world x 24 in rank order
+        mine = bytes([rank * 10 + i for i in range(24)])
+        out = ctypes.create_string_buffer(24 * world)
+        ok &= st.allgather(None, mine, out, 24) == 0
+        ok &= out.raw == b"".join(bytes([p * 10 + i for i in range(24)]) for p in range(world))
+        # allreduce_sum in place over doubles
+        buf = (ctypes.c_double * 5)(*[rank + 0.25 * i for i in range(5)])
+        ok &= st.allreduce_sum(None, buf, 5) == 0
+        ok &= list(buf) == [sum(p + 0.25 * i for p in range(world)) for i in range(5)]
+        ok &= st.barrier(None) == 0
+        ok &= st.sync_collectives == 1
+        result[rank] = int(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_torch_host_comm_callbacks_gloo():
+    """The scg_host_comm transport the library calls for a multi-process run without NCCL
+    (include/sketchycgal.h): allgather in rank order, in-place double sum, barrier -- over gloo."""
+    world = 2
+    port = 31500 + (os.getpid() % 2000)
+    mgr = mp.Manager()
+    result = mgr.dict()
+    mp.spawn(_comm_worker, args=(world, port, result), nprocs=world, join=True)
+    assert all(result[r] == 1 for r in range(world))
