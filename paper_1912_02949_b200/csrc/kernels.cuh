@@ -175,7 +175,7 @@ __device__ __forceinline__ double div_rn(double a, double b, double rb) {
 // grid so they start early.
 constexpr int kMinBlocksUni = 3;  // min blocks per SM of the uniform-weight SELL SpMV kernels (80-register cap)
 // min blocks per SM of the ELL SpMV kernels: 64-register cap up to W = 4, wider rows need more stage registers
-constexpr int ell_min_blocks(int W, bool uni) { return W < 0 ? (W >= -4 ? 4 : 3) : (W <= 4 ? 4 : (uni ? 3 : 2)); }
+constexpr int ell_min_blocks(int W, bool uni) { return W <= 4 ? 4 : (uni ? 3 : 2); }
 constexpr int kLongRow = 32;
 
 struct Rows {
@@ -198,15 +198,7 @@ struct Rows {
   const int *ecol;      // column | 0x80000000 for a negative uniform value
   const double *eval;   // per-slot values, or nullptr when all |C_rj| equal m0
   int padc;             // the padding code
-  // ELL16-W (uniform weights): per row W 16-bit codes, contiguous per row (slice s, lane l at
-  // e16[(32 s + l) W]): bit 0 valid, bit 1 negative coefficient, bits 15..2 the signed column offset
-  // from the row (|offset| < 2^13); all-zero = padding.  Rows with a farther column are "special":
-  // slot 0 holds kE16Special and the row is done from the CSR arrays (list spec[0 .. nspec)).
-  const unsigned short *e16;
-  const int *spec;
-  int nspec;
 };
-constexpr unsigned short kE16Special = 2;
 constexpr int kEllMax = 8;  // widest ELL layout (rows of at most 8 off-diagonal entries)
 constexpr int kDynCh = 8;
 
@@ -637,163 +629,12 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
   }
 }
 
-// ---------------------------------------------------------------- ELL16-W engine (uniform weights)
-// spmv_ell with 16-bit column offsets (RL.e16): a row's W codes are one vector load (8 bytes for
-// W = 4, half the int32 column stream of ELL-W); the gather address is the own entry's address plus
-// the offset (one signed 32x32->64 multiply-add); padding slots are skipped by predication, so the
-// chain is the same CAC-3 fma sequence.  Special rows (a column offset >= 2^13, ~1 % of configs[3]'s
-// rows) are skipped here and done thread-per-row from the CSR arrays afterwards.
-template <int W>
-struct E16Vec;
-template <>
-struct E16Vec<2> {
-  using T = unsigned;
-};
-template <>
-struct E16Vec<4> {
-  using T = uint2;
-};
-template <>
-struct E16Vec<8> {
-  using T = uint4;
-};
-template <int W>
-__device__ __forceinline__ void e16_unpack(const typename E16Vec<W>::T &v, unsigned (&w)[(W + 1) / 2]) {
-  if constexpr (W == 2) w[0] = v;
-  else if constexpr (W == 4) { w[0] = v.x; w[1] = v.y; }
-  else { w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w; }
-}
-__device__ __forceinline__ unsigned e16_code(const unsigned *w, int u) {  // 16-bit code u (zero-extended)
-  return (u & 1) ? (w[u >> 1] >> 16) : (w[u >> 1] & 0xffffu);
-}
-__device__ __forceinline__ const double *gaddr_off(const double *base, unsigned code) {
-  // base + (signed bits 15..2 of the code)
-  const int off = ((int)(code << 16)) >> 18;
-  const double *p;
-  asm("mad.wide.s32 %0, %1, 8, %2;" : "=l"(p) : "r"(off), "l"(base));
-  return p;
-}
-
-template <int NC, int W, class Epi>
-__device__ __forceinline__ void spmv_ell16(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
-                                           const double *__restrict__ diag0, const double *__restrict__ diag1,
-                                           long long rb, int nl, Epi &epi) {
-  using VT = typename E16Vec<W>::T;
-  constexpr int NW = (W + 1) / 2;
-  const int lane = threadIdx.x & 31;
-  const double rden = 1.0 / den;
-  const int nsl = (nl + 31) >> 5;
-  const int per = (nsl + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int s_end = min(nsl, ((int)blockIdx.x + 1) * per);
-  const int wstep = blockDim.x >> 5;
-  int sl = (int)blockIdx.x * per + (threadIdx.x >> 5);
-  const VT *__restrict__ ec = reinterpret_cast<const VT *>(RL.e16) + lane;
-  const double m0 = RL.m0;
-  auto cload = [&](int q, unsigned (&w)[NW]) {
-    if (q < s_end) {
-      const VT v = __ldg(ec + (long long)q * 32);
-      e16_unpack<W>(v, w);
-    } else {
-#pragma unroll
-      for (int j = 0; j < NW; ++j) w[j] = 0u;
-    }
-  };
-  // gathers of slice q (its own row's address + each valid offset); returns the codes' valid/sign
-  // bits packed (bit 2u valid, bit 2u+1 negative) and whether the row is special
-  auto gload = [&](int q, const unsigned (&w)[NW], double (&g)[W]) -> unsigned {
-    const double *own = X + rb + ((long long)q * 32 + lane);
-    unsigned vs = 0u;
-#pragma unroll
-    for (int u = 0; u < W; ++u) {
-      const unsigned code = e16_code(w, u);
-      if (code & 1u) g[u] = __ldg(gaddr_off(own, code));
-      vs |= (code & 3u) << (2 * u);
-    }
-    return vs;
-  };
-  auto oload = [&](int q, double &xo, double &dd0, double &dd1) {
-    const int p = q * 32 + lane;
-    xo = 0.0;
-    dd0 = 0.0;
-    dd1 = 0.0;
-    if (q < s_end && p < nl) {
-      xo = X[rb + p];
-      dd0 = diag0[p];
-      if (NC > 1) dd1 = diag1[p];
-    }
-  };
-  unsigned cb[NW], cc[NW];
-  double g0[W];
-  double xo0, d00, d10, xo1, d01, d11;
-  unsigned s0;
-  {
-    unsigned ca[NW];
-    cload(sl, ca);
-    oload(sl, xo0, d00, d10);
-    s0 = gload(sl, ca, g0);
-  }
-  cload(sl + wstep, cb);
-  oload(sl + wstep, xo1, d01, d11);
-  cload(sl + 2 * wstep, cc);
-  for (; sl < s_end; sl += wstep) {
-    double g1[W];
-    const unsigned s1 = gload(sl + wstep, cb, g1);  // gathers of slice i+1
-    unsigned cd[NW];
-    cload(sl + 3 * wstep, cd);                      // codes of slice i+3
-    double xo2, d02, d12;
-    oload(sl + 2 * wstep, xo2, d02, d12);           // own entries of slice i+2
-    const int p = sl * 32 + lane;
-    RowOut<NC> o;
-    o.r = p;
-    o.xr = xo0 * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
-    o.s[0] = d00 * o.xr;
-    if (NC > 1) o.s[NC - 1] = d10 * o.xr;
-#pragma unroll
-    for (int u = 0; u < W; ++u)
-      if ((s0 >> (2 * u)) & 1u) {
-        double x = g0[u] * rden;
-        x = __hiloint2double(__double2hiint(x) ^ (int)(((s0 >> (2 * u + 1)) & 1u) << 31), __double2loint(x));
-#pragma unroll
-        for (int t = 0; t < NC; ++t) o.s[t] = fma(m0, x, o.s[t]);
-      }
-    if (p < nl && (s0 & 3u) != kE16Special) epi(o);
-#pragma unroll
-    for (int j = 0; j < NW; ++j) {
-      cb[j] = cc[j];
-      cc[j] = cd[j];
-    }
-#pragma unroll
-    for (int u = 0; u < W; ++u) g0[u] = g1[u];
-    s0 = s1;
-    xo0 = xo1; d00 = d01; d10 = d11;
-    xo1 = xo2; d01 = d02; d11 = d12;
-  }
-  // special rows: thread per row from the CSR (<= kEllMax entries: the single CAC-3 chain)
-  for (int k = (int)(blockIdx.x * blockDim.x + threadIdx.x); k < RL.nspec; k += (int)(gridDim.x * blockDim.x)) {
-    const int r = __ldg(&RL.spec[k]);
-    const int e0 = __ldg(&C.rp[r]), e1 = __ldg(&C.rp[r + 1]);
-    RowOut<NC> o;
-    o.r = r;
-    o.xr = X[rb + r] * rden;
-    o.s[0] = diag0[r] * o.xr;
-    if (NC > 1) o.s[NC - 1] = diag1[r] * o.xr;
-    for (int e = e0; e < e1; ++e) {
-      const double m = __ldg(&C.val[e]);
-      const double x = __ldg(&X[__ldg(&C.col[e])]) * rden;
-#pragma unroll
-      for (int t = 0; t < NC; ++t) o.s[t] = fma(m, x, o.s[t]);
-    }
-    epi(o);
-  }
-}
-
 // SpMV dispatch: ELL-W when the layout has one (W > 0), else SELL + long rows.
 template <int NC, bool UNI, int W, class Epi>
 __device__ __forceinline__ void spmv_any(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
                                          const double *__restrict__ diag0, const double *__restrict__ diag1,
                                          long long rb, int nl, Epi &epi) {
   if constexpr (W > 0) spmv_ell<NC, UNI, W>(RL, X, den, diag0, diag1, rb, nl, epi);
-  else if constexpr (W < 0) spmv_ell16<NC, -W>(C, RL, X, den, diag0, diag1, rb, nl, epi);
   else spmv_rows<NC, UNI>(C, RL, X, den, diag0, diag1, rb, nl, epi);
 }
 
@@ -1181,7 +1022,7 @@ struct EpiA {
 };
 
 template <bool UNI, int W>  // W > 0: ELL-W layout (spmv_ell), 0: SELL + long rows
-__global__ void __launch_bounds__(kBlockA, W != 0 ? ell_min_blocks(W, UNI) : (UNI ? kMinBlocksUni : 2)) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
+__global__ void __launch_bounds__(kBlockA, W > 0 ? ell_min_blocks(W, UNI) : (UNI ? kMinBlocksUni : 2)) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ X, int nl, long long rb, int i,
                                                          double *__restrict__ a, XSlot *slot, DevScalars *sc,
                                                          Net net) {
@@ -1893,7 +1734,7 @@ struct EpiC {
 };
 
 template <bool UNI, int W>
-__global__ void __launch_bounds__(kBlock, W != 0 ? ell_min_blocks(W, UNI) : (UNI ? kMinBlocksUni : 2)) k_lanczos_c(Csr C, Rows RL, const double *__restrict__ d,
+__global__ void __launch_bounds__(kBlock, W > 0 ? ell_min_blocks(W, UNI) : (UNI ? kMinBlocksUni : 2)) k_lanczos_c(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ Xj, const double *Xjm1,
                                                          double *Xjp1, double *__restrict__ x, int nl, long long rb,
                                                          int j, DevScalars *sc, XSlot *slot, Net net) {

@@ -106,10 +106,7 @@ struct Shard {
   unsigned *work = nullptr;  // dynamic slice counter of k_lanczos_a (graphs with long rows)
   int *ell_col = nullptr;    // ELL-W layout (rows of <= kEllMax entries), W = ellw; 0: none
   double *ell_val = nullptr;
-  int ellw = 0, padc = 0;      // ellw < 0: ELL16 layout of width -ellw (16-bit column offsets)
-  unsigned short *e16 = nullptr;
-  int *spec = nullptr;         // ELL16 special rows (a column offset >= 2^13), local ids
-  int nspec = 0;
+  int ellw = 0, padc = 0;
   int grid_ell = 1, grid_ell_mon = 1, grid_ell_c = 1, grid_dual_s = 1;
   bool dyn = false;
   // row relabeling (SELL engine): local row nu holds input row rb + origloc[nu]
@@ -366,9 +363,6 @@ Rows rows_of(const Shard *s, bool dyn = false) {
   r.ecol = s->ell_col;
   r.eval = s->ell_val;
   r.padc = s->padc;
-  r.e16 = s->e16;
-  r.spec = s->spec;
-  r.nspec = s->nspec;
   return r;
 }
 
@@ -376,10 +370,7 @@ Rows rows_of(const Shard *s, bool dyn = false) {
 // not, and the ELL width (0: SELL + long rows).
 constexpr int kEllWidths[] = {2, 3, 4, 6, 8};
 #define SCG_PICK(K, U, W)                                          \
-  ((W) == -2  ? K<true, -2>                                        \
-   : (W) == -4 ? K<true, -4>                                       \
-   : (W) == -8 ? K<true, -8>                                       \
-   : (W) == 2 ? ((U) ? K<true, 2> : K<false, 2>)                   \
+  ((W) == 2   ? ((U) ? K<true, 2> : K<false, 2>)                   \
    : (W) == 3 ? ((U) ? K<true, 3> : K<false, 3>)                   \
    : (W) == 4 ? ((U) ? K<true, 4> : K<false, 4>)                   \
    : (W) == 6 ? ((U) ? K<true, 6> : K<false, 6>)                   \
@@ -443,7 +434,7 @@ void free_shard(Shard *s) {
                   s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
                   s->sc, s->slots, s->dlog, s->longrows, s->sell_col, s->sell_meta, s->sell_val,
                   s->mask, s->mb, s->peerG, s->peerMB, s->orig, s->V, s->ckr, s->work, s->gflag, s->ell_col,
-                  s->ell_val, s->gB, s->e16, s->spec};
+                  s->ell_val, s->gB};
   for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -859,52 +850,6 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
       if (!uni) CK(cudaMemcpyAsync(s->ell_val, eval.data(), sizeof(double) * ne, cudaMemcpyHostToDevice, st));
       CK(cudaStreamSynchronize(st));
       s->ellw = W;
-      // ELL16 (uniform weights): 16-bit column offsets; rows with an offset beyond 2^13 - 1 are
-      // special (CSR path) -- used when they are at most 3 % of the rows (configs[1], [3])
-      int W16 = 0;
-      for (int w : {2, 4, 8})
-        if (W16 == 0 && w >= maxlen) W16 = w;
-      if (uni && W16 > 0 && !(c->flags & SCG_NO_ELL16)) {
-        const size_t n16 = (size_t)nsl32 * 32 * W16;
-        hvec<unsigned short> e16(n16);
-        std::vector<unsigned char> special((size_t)nl, 0);
-        const int64_t rbase = s->rb;
-#pragma omp parallel for schedule(static, 1024)
-        for (int64_t r = 0; r < nsl32 * 32; ++r) {
-          unsigned short *cp = e16.data() + (size_t)r * W16;
-          for (int j = 0; j < W16; ++j) cp[j] = 0;
-          if (r >= nl) continue;
-          bool sp = false;
-          for (int64_t e = h_rp[(size_t)r]; e < h_rp[(size_t)r + 1]; ++e) {
-            const int64_t off = (int64_t)h_col[(size_t)e] - (rbase + r);
-            if (off < -8191 || off > 8191) sp = true;
-          }
-          if (sp) {
-            special[(size_t)r] = 1;
-            cp[0] = kE16Special;
-            continue;
-          }
-          int j = 0;
-          for (int64_t e = h_rp[(size_t)r]; e < h_rp[(size_t)r + 1]; ++e, ++j) {
-            const int off = (int)((int64_t)h_col[(size_t)e] - (rbase + r));
-            cp[j] = (unsigned short)(((unsigned)off << 2) | (h_w[(size_t)e] < 0 ? 2u : 0u) | 1u);
-          }
-        }
-        std::vector<int> spl;
-        for (int64_t r = 0; r < nl; ++r)
-          if (special[(size_t)r]) spl.push_back((int)r);
-        if ((double)spl.size() <= 0.03 * (double)nl) {
-          if (!alloc((void **)&s->e16, sizeof(unsigned short) * n16) ||
-              !alloc((void **)&s->spec, sizeof(int) * std::max<size_t>(1, spl.size())))
-            return fail(c, SCG_ENOMEM, "ELL16 layout");
-          CK(cudaMemcpyAsync(s->e16, e16.data(), sizeof(unsigned short) * n16, cudaMemcpyHostToDevice, st));
-          if (!spl.empty())
-            CK(cudaMemcpyAsync(s->spec, spl.data(), sizeof(int) * spl.size(), cudaMemcpyHostToDevice, st));
-          CK(cudaStreamSynchronize(st));
-          s->nspec = (int)spl.size();
-          s->ellw = -W16;
-        }
-      }
     }
     // algorithmic matrix bytes: one column index (+ value unless uniform) per stored entry --
     // independent of the layout's padding and metadata

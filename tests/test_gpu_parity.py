@@ -135,33 +135,15 @@ def test_launch_policy_forced_bitwise(gpu, cfg, T, pdl):
     _assert_trajectory(g, o, T)
 
 
-@pytest.mark.parametrize("cfg,T,layout", [("c1", 300, "sell"), ("c3", 2, "sell"), ("c4", 1, "sell"),
-                                          ("c1", 300, "ell32"), ("c3", 2, "ell32")])
-def test_other_layouts_where_ell16_applies_bitwise(gpu, cfg, T, layout):
-    """Uniform-weight graphs whose rows all have <= 8 entries run the ELL16 SpMV by default (configs[1],
-    [3]; configs[4] has values: ELL-W); the SELL-32 layout (SCG_NO_ELL) and 32-bit ELL columns
-    (SCG_NO_ELL16) give the same bitwise trajectory on them."""
+@pytest.mark.parametrize("cfg,T", [("c1", 300), ("c3", 2), ("c4", 1)])
+def test_sell_layout_where_ell_applies_bitwise(gpu, cfg, T):
+    """Graphs whose rows all have <= 8 entries run the ELL-W SpMV by default; the SELL-32 layout
+    (SCG_NO_ELL) gives the same bitwise trajectory on them."""
     L = si.laplacian(cfg)
     c = si.CONFIGS[cfg]
     R = 2 if cfg == "c4" else c["R"]
-    g, o = _run_pair(gpu, L, R, T, seed=c["seed"], **({"ell": False} if layout == "sell" else {"ell16": False}))
+    g, o = _run_pair(gpu, L, R, T, seed=c["seed"], ell=False)
     _assert_trajectory(g, o, T)
-
-
-def test_ell16_special_rows_bitwise(gpu):
-    """ELL16 rows with a column offset beyond 2^13 - 1 go through the CSR path: a ring of 20000 vertices
-    with a few long chords (every row <= 8 entries) -- both kinds of rows in one launch."""
-    n = 20000
-    i = np.arange(n)
-    j = (i + 1) % n
-    rng = np.random.default_rng(5)
-    a = rng.integers(0, n, 150)
-    b = (a + rng.integers(9000, 11000, 150)) % n
-    keep = a != b
-    L = si.laplacian_from_edges(n, np.concatenate([i, a[keep]]), np.concatenate([j, b[keep]]),
-                                np.ones(n + int(keep.sum())), dedupe=True)
-    g, o = _run_pair(gpu, L, 6, 60, seed=4)
-    _assert_trajectory(g, o, 60)
 
 
 @pytest.mark.parametrize("cfg,T", [("c0", 200), ("c3", 1)])
