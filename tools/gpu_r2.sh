@@ -15,6 +15,14 @@ for w in "$@"; do
     ab:*)  # ab:<opts> -- bench with execution options (no cpu / e2e legs)
       OPTS=${w#ab:}; N=${OPTS//[^a-zA-Z0-9_]/_}
       timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 --no-cpu --no-e2e --opts "$OPTS" > $O/ab_$N.json 2> $O/ab_$N.err; echo "exit $?" >> $O/ab_$N.err ;;
+    abl:*)  # abl:<variant library file under paper_1912_02949_b200/lib/> -- bench with that build
+      LIBF=${w#abl:}; N=${LIBF//[^a-zA-Z0-9_]/_}
+      SCG_LIB=paper_1912_02949_b200/lib/$LIBF timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 --no-cpu --no-e2e > $O/abl_$N.json 2> $O/abl_$N.err; echo "exit $?" >> $O/abl_$N.err ;;
+    ncul:*)  # ncul:<variant library>:<kernel regex>:<skip>
+      SPEC=${w#ncul:}; LIBF=${SPEC%%:*}; REST=${SPEC#*:}; KRE=${REST%%:*}; SKIP=${REST##*:}
+      N=${LIBF//[^a-zA-Z0-9_]/_}_${KRE//[^a-zA-Z0-9_]/_}
+      SCG_LIB=paper_1912_02949_b200/lib/$LIBF ncu --set full --clock-control none --import-source on -k regex:"$KRE" -s $SKIP -c 2 -o $O/prof_$N python bench.py --steps 2 --warmup 5 --no-cpu --no-e2e --no-profile > $O/ncu_full_$N.log 2>&1
+      echo "ncu exit $?" >> $O/ncu_full_$N.log ;;
     benchnocpu) timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 --no-cpu > $O/bench.json 2> $O/bench.err; echo "bench exit $?" >> $O/bench.err ;;
     full) timeout 900 python bench.py --steps 997 --warmup 3 --no-cpu --no-e2e > $O/bench_full.json 2> $O/bench_full.err; echo "exit $?" >> $O/bench_full.err ;;
     ref) timeout 900 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $O/ref.json 2> $O/ref.err; echo "ref exit $?" >> $O/ref.err ;;
