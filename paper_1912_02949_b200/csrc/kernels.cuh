@@ -175,10 +175,9 @@ __device__ __forceinline__ double div_rn(double a, double b, double rb) {
 // grid so they start early.
 constexpr int kMinBlocksUni = 3;  // min blocks per SM of the uniform-weight SELL SpMV kernels (80-register cap)
 // min blocks per SM of the ELL SpMV kernels: 64-register cap up to W = 4, wider rows need more stage registers
-#ifndef SCG_ELL_GD
-#define SCG_ELL_GD 1  // ELL pipeline: gathers issued this many slices ahead (experiment: 2)
-#endif
-constexpr int ell_min_blocks(int W, bool uni) { return W <= 4 ? (SCG_ELL_GD == 2 ? 3 : 4) : (uni ? 3 : 2); }
+// (a deeper pipeline -- gathers two slices ahead, 78 registers, 3 blocks/SM -- measured 171 us against
+// 140 us on configs[3]: the fourth block per SM is worth more than the extra slack)
+constexpr int ell_min_blocks(int W, bool uni) { return W <= 4 ? 4 : (uni ? 3 : 2); }
 constexpr int kLongRow = 32;
 
 struct Rows {
@@ -577,64 +576,6 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
       if (NC > 1) dd1 = diag1[p];
     }
   };
-#if SCG_ELL_GD == 2
-  // gathers two slices ahead, columns four ahead
-  int cc[W], cd[W];
-  double g0[W], v0[W], g1[W], v1[W];
-  double xo0, d00, d10, xo1, d01, d11;
-  unsigned s0, s1;
-  {
-    int ca[W], cb[W];
-    cload(sl, ca);
-    oload(sl, xo0, d00, d10);
-    s0 = gload(sl, ca, g0, v0);
-    cload(sl + wstep, cb);
-    oload(sl + wstep, xo1, d01, d11);
-    s1 = gload(sl + wstep, cb, g1, v1);
-  }
-  cload(sl + 2 * wstep, cc);
-  cload(sl + 3 * wstep, cd);
-  for (; sl < s_end; sl += wstep) {
-    double g2[W], v2[W];
-    const unsigned s2 = gload(sl + 2 * wstep, cc, g2, v2);  // gathers of slice i+2
-    int ce[W];
-    cload(sl + 4 * wstep, ce);                             // columns of slice i+4
-    double xo2, d02, d12;
-    oload(sl + 2 * wstep, xo2, d02, d12);                  // own entries of slice i+2
-    const int p = sl * 32 + lane;
-    RowOut<NC> o;
-    o.r = p;
-    o.xr = xo0 * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
-    o.s[0] = d00 * o.xr;
-    if (NC > 1) o.s[NC - 1] = d10 * o.xr;
-#pragma unroll
-    for (int u = 0; u < W; ++u) {
-      double x = g0[u] * rden;
-      if (UNI) {
-        x = __hiloint2double(__double2hiint(x) ^ (int)(((s0 >> u) & 1u) << 31), __double2loint(x));
-#pragma unroll
-        for (int t = 0; t < NC; ++t) o.s[t] = fma(m0, x, o.s[t]);
-      } else {
-#pragma unroll
-        for (int t = 0; t < NC; ++t) o.s[t] = fma(v0[u], x, o.s[t]);
-      }
-    }
-    if (p < nl) epi(o);
-#pragma unroll
-    for (int u = 0; u < W; ++u) {
-      cc[u] = cd[u];
-      cd[u] = ce[u];
-      g0[u] = g1[u];
-      g1[u] = g2[u];
-      if (!UNI) { v0[u] = v1[u]; v1[u] = v2[u]; }
-    }
-    s0 = s1;
-    s1 = s2;
-    xo0 = xo1; d00 = d01; d10 = d11;
-    xo1 = xo2; d01 = d02; d11 = d12;
-  }
-}
-#else
   int cb[W], cc[W];
   double g0[W], v0[W];
   double xo0, d00, d10, xo1, d01, d11;
@@ -689,7 +630,6 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
     xo1 = xo2; d01 = d02; d11 = d12;
   }
 }
-#endif
 
 // SpMV dispatch: ELL-W when the layout has one (W > 0), else SELL + long rows.
 template <int NC, bool UNI, int W, class Epi>
