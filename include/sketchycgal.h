@@ -83,9 +83,11 @@ enum {
   SCG_TMA_B = 1u << 12,         /* TMA-staged recurrence kernel (bulk copies into shared memory) */
   SCG_DEBUG_LOG = 1u << 13,     /* host init stage timings and layout facts on stderr */
   SCG_NO_ELL = 1u << 14,        /* keep the SELL-32 layout even when every row has <= 8 entries (ELL-W otherwise) */
-  SCG_FUSED_RNG = 1u << 15      /* one GPU: draw the next Lanczos start vector inside the dual-update kernel instead of
+  SCG_FUSED_RNG = 1u << 15,     /* one GPU: draw the next Lanczos start vector inside the dual-update kernel instead of
                                    on a lower-priority side stream overlapped with the Lanczos passes (sharded runs
                                    always draw inside the dual kernel) */
+  SCG_NO_RESIDENT = 1u << 17    /* one GPU, n <= 65536: keep the multi-kernel iteration instead of one launch of one
+                                   thread-block cluster per iteration (k_resident) */
 };
 
 /* This rank's rows [row_begin, row_end) of the symmetric weighted Laplacian

@@ -13,6 +13,7 @@
 //   rows live at [rb, rb + nl).  Local vectors (a, z, y, v) are length nl.
 //   Omega, S: nl x R column-major, leading dimension nl.
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdint>
 
 #include "xsum.cuh"
@@ -816,7 +817,7 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
       rec.tau = sc->tau;
       rec.gap = A.ineq ? NAN : gapv;  // the gap / bound formulas are for A X = b (reading R32)
       rec.bound = A.ineq ? NAN : boundv;
-      f.log[A.t - 1] = rec;
+      if (f.log) f.log[A.t - 1] = rec;
       break;
     }
     default: break;
@@ -1601,10 +1602,16 @@ __device__ int sturm_count(const double *om, const double *rho2, int k, double x
 
 // One warp: multisection (32 Sturm counts per round, one per lane) for theta, then
 // inverse iteration (lane 0, partial pivoting) for s (Alg. 2 lines 11-12).
-__global__ void k_tridiag(DevScalars *sc, int q) {
-  pdl_entry();
-  __shared__ double om[kMaxQ], rho[kMaxQ], rho2[kMaxQ];
-  const int lane = threadIdx.x;
+struct TriScratch {  // shared-memory working arrays of one tridiagonal solve
+  double om[kMaxQ], rho[kMaxQ], rho2[kMaxQ], u0[kMaxQ], u1[kMaxQ], u2[kMaxQ], mul[kMaxQ], xv[kMaxQ], s[kMaxQ],
+      ru0[kMaxQ];
+  int swp[kMaxQ];
+};
+
+// CAC-5 on one full warp (lanes 0..31 of the calling warp); sc may live in shared memory.
+__device__ __noinline__ void tridiag_warp(DevScalars *sc, int q, TriScratch &T) {
+  double *om = T.om, *rho = T.rho, *rho2 = T.rho2;
+  const int lane = threadIdx.x & 31;
   const int k = sc->brk ? sc->k : q;
   for (int j = lane; j < k; j += 32) om[j] = sc->om[j];
   for (int j = lane; j < k - 1; j += 32) { rho[j] = sc->rho[j + 1]; rho2[j] = rho[j] * rho[j]; }
@@ -1657,8 +1664,8 @@ __global__ void k_tridiag(DevScalars *sc, int q) {
   sc->theta = th;
   // working arrays of the sequential part in shared memory (a local-memory stack would start
   // cold in L1 at every launch)
-  __shared__ double u0[kMaxQ], u1[kMaxQ], u2[kMaxQ], mul[kMaxQ], xv[kMaxQ], s[kMaxQ], ru0[kMaxQ];
-  __shared__ int swp[kMaxQ];
+  double *u0 = T.u0, *u1 = T.u1, *u2 = T.u2, *mul = T.mul, *xv = T.xv, *s = T.s, *ru0 = T.ru0;
+  int *swp = T.swp;
   const double tiny = NT * 0x1p-60;
   double c0 = om[0] - th, c1 = rho[0], c2 = 0.0;
   for (int i = 0; i < k - 1; ++i) {
@@ -1712,6 +1719,12 @@ __global__ void k_tridiag(DevScalars *sc, int q) {
   const double sg = s[jm] < 0.0 ? -1.0 : 1.0;
   for (int j = 0; j < k; ++j) sc->s[j] = sg < 0.0 ? -s[j] : s[j];
   sc->k = k;
+}
+
+__global__ void k_tridiag(DevScalars *sc, int q) {
+  pdl_entry();
+  __shared__ TriScratch T;
+  tridiag_warp(sc, q, T);
 }
 
 // ---------------------------------------------------------------- Lanczos pass 2
@@ -2220,6 +2233,261 @@ __global__ void k_selftest_div(long long n, uint64_t seed, unsigned long long *m
     bad += (__double_as_longlong(q) != __double_as_longlong(ref));
   }
   atomicAdd(mismatch, bad);
+}
+
+
+// ---------------------------------------------------------------- resident cluster kernel (small graphs)
+// One whole iteration of Alg. 4 (Lanczos pass 1, tridiagonal eigenpair, stored-vector combine,
+// monitor, primal, dual) in ONE launch of ONE thread-block cluster (up to 16 CTAs on 16 SMs), for
+// graphs that live in L2 (configs[0], [1]).  The multi-kernel path pays a launch and a grid-wide
+// exact-sum tail (block flush, global limb atomics, ticket, last-block finalize) per reduction -- two
+// per Lanczos step, about 60 launches per iteration; here a reduction is a block flush into shared
+// memory, one cluster barrier, and a read of the other CTAs' limbs through distributed shared memory.
+// Every CTA adds the limbs of all CTAs (exact integers: the same bits in every CTA) and finalizes
+// into its own shared-memory copy of the scalar state, so all CTAs proceed with identical scalars and
+// no second barrier is needed.  Vectors stay in global memory (L2); the cluster barrier (release /
+// acquire at cluster scope) orders one phase's stores before the next phase's gathers.  Per-row
+// arithmetic is that of the multi-kernel path's kernels: the same iterates, bit for bit.
+namespace cg = cooperative_groups;
+constexpr int kResThreads = 512;
+constexpr int kResMaxN = 1 << 16;  // rows up to which an iteration runs as one cluster launch
+
+struct ResShared {
+  DevScalars sc;                              // replicated scalar state (identical in every CTA)
+  long long xb[2][kMaxSums][kLimbs];          // this CTA's block partials, double-buffered by reduction
+  double gk[2][kMaxR];                        // this CTA's partials of g = v^T Omega
+  double red[kResThreads / 32][kMaxR];        // warp partials of g
+  double sv[kMaxQ], srr[kMaxQ];               // s_j and fl(1/rho_j) of the combine
+  TriScratch tri;
+  unsigned long long xbw[kMaxSums][kLimbs];   // (scratch of the limb reads)
+};
+
+// Cluster-wide exact reduction of NS sums (and, with R > 0, of the CTAs' g partials in CTA order),
+// then finalize(kind) in every CTA into its own copy of the scalars.  par: this reduction's buffer.
+template <int NS>
+__device__ __forceinline__ void res_reduce(XWin (&acc)[NS], int err, ResShared &sm, int &par, int kind,
+                                           const FinArgs &f, int R) {
+  cg::cluster_group cl = cg::this_cluster();
+#pragma unroll
+  for (int s = 0; s < NS; ++s) xwin_flush(acc[s], sm.xb[par][s]);
+  if (__syncthreads_or(err) && threadIdx.x == 0) sm.sc.err |= 1;
+  cl.sync();  // every CTA's partials are complete (and every store of the phase is visible)
+  const int ncta = (int)cl.num_blocks();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    long long part[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int idx = lane + 32 * h;
+      if (idx < NS * kLimbs)
+        for (int c = 0; c < ncta; ++c) part[h] += *cl.map_shared_rank(&sm.xb[par][0][0] + idx, c);
+    }
+    double gpart[2] = {0.0, 0.0};  // g_k summed over the CTAs in CTA order
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = lane + 32 * h;
+      if (k < R)
+        for (int c = 0; c < ncta; ++c) gpart[h] += *cl.map_shared_rank(&sm.gk[par][k], c);
+    }
+    long long L[kMaxSums][kLimbs];
+    double gk[kMaxR];
+    for (int idx = 0; idx < kMaxSums * kLimbs; ++idx) {
+      const long long v = __shfl_sync(0xffffffffu, part[idx >> 5], idx & 31);
+      if (lane == 0) L[idx / kLimbs][idx % kLimbs] = idx < NS * kLimbs ? v : 0ll;
+    }
+    for (int k = 0; k < kMaxR; ++k) {
+      const double v = __shfl_sync(0xffffffffu, gpart[k >> 5], k & 31);
+      if (lane == 0) gk[k] = v;
+    }
+    if (lane == 0) finalize(kind, &sm.sc, L, gk, f);
+  }
+  // the other buffer is free: its readers (the previous reduction) are past this barrier
+  for (int i = threadIdx.x; i < kMaxSums * kLimbs; i += blockDim.x) (&sm.xb[par ^ 1][0][0])[i] = 0;
+  par ^= 1;
+  __syncthreads();
+}
+
+struct ResArgs {
+  double *G;            // gathered region: [x | w_1 | w_2 | ...] (store mode), npad apart
+  long long npad;
+  double *a, *d, *z, *y;
+  const double *cdiag, *Om;
+  double *V;            // v ring (deferred sketch): slot js
+  long long ldv;
+  int js;
+  double *ckr;          // deferred sketch coefficients
+  DevScalars *sc;       // global scalar state (loaded at entry, stored back by CTA 0 at exit)
+  scg_iter_rec *log;
+  IterArgs A;
+  int R, nl;
+  uint64_t seed;
+  const int *orig;
+};
+
+template <bool UNI, int W>
+__global__ void __launch_bounds__(kResThreads, 1) k_resident(Csr C, Rows RL, ResArgs P) {
+  pdl_entry();
+  extern __shared__ __align__(16) unsigned char res_raw[];
+  ResShared &sm = *reinterpret_cast<ResShared *>(res_raw);
+  cg::cluster_group cl = cg::this_cluster();
+  const int tid = threadIdx.x;
+  const int gtid = (int)blockIdx.x * blockDim.x + tid, gstride = (int)gridDim.x * blockDim.x;
+  const IterArgs &A = P.A;
+  const int nl = P.nl, q = A.q;
+  const Net net{};  // one GPU: no peers (mask == nullptr)
+  for (int i = tid; i < (int)(sizeof(DevScalars) / sizeof(int)); i += blockDim.x)
+    reinterpret_cast<int *>(&sm.sc)[i] = __ldcg(reinterpret_cast<const int *>(P.sc) + i);
+  for (int i = tid; i < 2 * kMaxSums * kLimbs; i += blockDim.x) (&sm.xb[0][0][0])[i] = 0;
+  int par = 0;
+  cl.sync();
+  auto slot = [&](int j) -> double * { return P.G + (long long)j * P.npad; };  // w_j (j >= 1); x = slot(0)
+  // ---- Lanczos pass 1 (Alg. 2 lines 1-9): k_lanczos_a + k_lanczos_b per step
+  for (int i = 1; i <= q && !sm.sc.brk; ++i) {
+    {
+      EpiA epi;
+      epi.a = P.a;
+      epi.blk = sm.xb[par][0];
+      xwin_init(epi.acc[0]);
+      epi.err = 0;
+      spmv_any<1, UNI, W>(C, RL, slot(i), sm.sc.rho[i - 1], P.d, nullptr, 0, nl, epi);
+      FinArgs f{};
+      f.i = i;
+      res_reduce<1>(epi.acc, epi.err, sm, par, FK_OM, f, 0);
+    }
+    if (i == q) break;
+    {
+      const double om = sm.sc.om[i - 1], den = sm.sc.rho[i - 1];
+      const double denm = i >= 2 ? sm.sc.rho[i - 2] : 1.0;
+      const double rden = 1.0 / den, rdenm = 1.0 / denm;
+      const double *Xi = slot(i), *Xim1 = slot(i > 1 ? i - 1 : 1);
+      double *Xip1 = slot(i + 1);
+      XWin acc[1];
+      xwin_init(acc[0]);
+      int err = 0;
+      for (int r = gtid; r < nl; r += gstride) {
+        double w = fma(-om, Xi[r] * rden, P.a[r]);
+        if (i >= 2) w = fma(-den, Xim1[r] * rdenm, w);  // rho_{i-1} = rho[i-1] = den
+        Xip1[r] = w;
+        xwin_add_nn(acc[0], w * w, err, sm.xb[par][0]);
+      }
+      FinArgs f{};
+      f.i = i;
+      res_reduce<1>(acc, err, sm, par, FK_RHO, f, 0);
+    }
+  }
+  // ---- tridiagonal eigenpair (lines 11-12), replicated in every CTA
+  if (tid < 32) tridiag_warp(&sm.sc, q, sm.tri);
+  __syncthreads();
+  // ---- line 13 from the stored vectors (k_combine), ||x||^2
+  {
+    const int k = sm.sc.k;
+    for (int j = tid; j < k; j += blockDim.x) {
+      sm.sv[j] = sm.sc.s[j];
+      sm.srr[j] = 1.0 / sm.sc.rho[j];
+    }
+    __syncthreads();
+    XWin acc[1];
+    xwin_init(acc[0]);
+    int err = 0;
+    double *x = slot(0);
+    for (int r = gtid; r < nl; r += gstride) {
+      double xr = sm.sv[0] * (__ldcg(slot(1) + r) * sm.srr[0]);
+      for (int j = 1; j < k; ++j) xr = fma(sm.sv[j], __ldcg(slot(j + 1) + r) * sm.srr[j], xr);
+      x[r] = xr;
+      xwin_add_nn(acc[0], xr * xr, err, sm.xb[par][0]);
+    }
+    res_reduce<1>(acc, err, sm, par, FK_NUX, FinArgs{}, 0);
+  }
+  // ---- monitor: v = x / ||x||, xi, v^T C v, ||v||^2 (k_monitor)
+  double *v = P.V + (long long)P.js * P.ldv;
+  {
+    EpiM epi;
+    epi.v = v;
+    epi.blk = sm.xb[par];
+    xwin_init(epi.acc[0]);
+    xwin_init(epi.acc[1]);
+    xwin_init(epi.acc[2]);
+    epi.err = 0;
+    spmv_any<2, UNI, W>(C, RL, slot(0), sm.sc.nu_x, P.d, P.cdiag, 0, nl, epi);
+    res_reduce<3>(epi.acc, epi.err, sm, par, FK_MON, FinArgs{}, 0);
+  }
+  // ---- primal: z <- (1 - eta) z + eta alpha (v o v), ||z - b||^2, g = v^T Omega (k_primal)
+  {
+    const bool hoff = A.trace_le && !(sm.sc.xi < 0.0);
+    XWin acc[1];
+    xwin_init(acc[0]);
+    int err = 0;
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int kc = 0; kc < P.R; kc += 16) {
+      double gp[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) gp[u] = 0.0;
+      for (int r = gtid; r < nl; r += gstride) {
+        const double vr = v[r];
+        if (kc == 0) {
+          const double hv = A.alpha * (vr * vr);
+          const double zr = hoff ? A.one_m_eta * P.z[r] : fma(A.eta, hv, A.one_m_eta * P.z[r]);
+          P.z[r] = zr;
+          const double e = zr - A.b;
+          xwin_add_nn(acc[0], e * e, err, sm.xb[par][0]);
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (kc + u < P.R) gp[u] = fma(vr, __ldg(&P.Om[(long long)(kc + u) * nl + r]), gp[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        double t = gp[u];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+        if (lane == 0 && kc + u < P.R) sm.red[warp][kc + u] = t;
+      }
+    }
+    __syncthreads();
+    if (tid < P.R) {
+      double t = 0.0;
+      for (int w = 0; w < kResThreads / 32; ++w) t += sm.red[w][tid];
+      sm.gk[par][tid] = t;
+    }
+    FinArgs f{};
+    f.R = P.R;
+    f.A = A;
+    f.log = blockIdx.x == 0 ? P.log : nullptr;
+    res_reduce<1>(acc, err, sm, par, FK_NZ, f, P.R);
+  }
+  // ---- dual: y <- y + gamma (z - b), d for t+1, next start vector and ||g||^2, gap sums (k_dual_sketch)
+  {
+    const double gam = sm.sc.gamma;
+    if (blockIdx.x == 0 && tid < P.R)
+      P.ckr[P.js * kMaxR + tid] = (A.trace_le && !(sm.sc.xi < 0.0)) ? 0.0 : (A.eta * A.alpha) * sm.sc.gk[tid];
+    XWin acc[5];
+#pragma unroll
+    for (int s = 0; s < 5; ++s) xwin_init(acc[s]);
+    int err = 0;
+    double *g = slot(1);
+    for (int r = gtid; r < nl; r += gstride) {
+      const double zr = P.z[r], yv = P.y[r];
+      const double e = zr - A.b;
+      const double yr = fma(gam, e, yv);
+      P.y[r] = yr;
+      P.d[r] = fma(A.beta_next, e, yr) + P.cdiag[r];
+      const double gv = scg_lanczos_start(P.seed, A.t + 1, P.orig[r]);
+      g[r] = gv;
+      xwin_add_nn(acc[0], gv * gv, err, sm.xb[par][0]);
+      xwin_add(acc[1], yr, err, sm.xb[par][1]);
+      xwin_add(acc[2], yr * zr, err, sm.xb[par][2]);
+      xwin_add_nn(acc[3], zr * zr, err, sm.xb[par][3]);
+      xwin_add_nn(acc[4], zr, err, sm.xb[par][4]);
+    }
+    res_reduce<5>(acc, err, sm, par, FK_RHO0M, FinArgs{}, 0);
+  }
+  (void)net;
+  if (blockIdx.x == 0) {
+    for (int i = tid; i < (int)(sizeof(DevScalars) / sizeof(int)); i += blockDim.x)
+      reinterpret_cast<int *>(P.sc)[i] = reinterpret_cast<const int *>(&sm.sc)[i];
+  }
+  cl.sync();  // range errors seen by any CTA (its own summands) reach the global flag
+  if (blockIdx.x != 0 && tid == 0 && sm.sc.err) atomicOr(&P.sc->err, sm.sc.err);
 }
 
 }  // namespace scg

@@ -62,12 +62,12 @@ using hvec = std::vector<T, noinit_alloc<T>>;
 
 enum KClass {
   KC_LANCZOS_A = 0, KC_LANCZOS_B, KC_TRIDIAG, KC_LANCZOS_C, KC_NORM_X, KC_COMBINE, KC_MONITOR, KC_PRIMAL,
-  KC_DUAL_SKETCH, KC_SKETCH, KC_PULL, KC_OTHER, KC_PASS1, KC_GEN, KC_COUNT
+  KC_DUAL_SKETCH, KC_SKETCH, KC_PULL, KC_OTHER, KC_PASS1, KC_GEN, KC_RESIDENT, KC_COUNT
 };
 const char *kKClassName[KC_COUNT] = {"lanczos_a_spmv_dot", "lanczos_b_axpy_norm", "tridiag_mineig",
                                      "lanczos_c_spmv_regen", "norm_x", "combine_stored", "monitor_spmv",
                                      "primal_z_gpart", "dual_next_g", "sketch_flush", "pull_collective", "other",
-                                     "lanczos_pass1_fused", "gen_start_side"};
+                                     "lanczos_pass1_fused", "gen_start_side", "resident_iteration"};
 
 struct EvPair {
   cudaEvent_t a, b;
@@ -138,6 +138,8 @@ struct scg_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t evA = nullptr, evB = nullptr;
   bool side_rng = false;
+  // small graphs (L2-resident): each iteration is one launch of one thread-block cluster (k_resident)
+  int res_cl = 0;  // cluster size, 0: off
   bool own_stream = false;
   int nsm = 148;
   int64_t n = 0, npad = 0;
@@ -350,6 +352,49 @@ void launch_coop(scg_ctx *c, int cls, double bytes, Kern kern, dim3 grid, dim3 b
   c->launches++;
 }
 
+// One-cluster launch (k_resident): grid = one cluster of cl CTAs, with the programmatic-serialization
+// attribute when enabled; same profiling as launch_smem.
+template <typename Kern, typename... Args>
+void launch_cluster(scg_ctx *c, int cls, double bytes, Kern kern, int cl, dim3 block, size_t smem, Args... args) {
+  const bool prof = (c->flags & SCG_PROFILE) != 0 && c->kl[cls] % c->prof_every == 0;
+  if (prof) c->ks[cls]++;
+  EvPair p{};
+  if (prof) {
+    if (c->pending.size() >= 8192) ev_flush(c);
+    p.a = ev_get(c);
+    p.b = ev_get(c);
+    p.cls = cls;
+    cudaEventRecord(p.a, c->stream);
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cl);
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeClusterDimension;
+  attr[na].val.clusterDim.x = cl;
+  attr[na].val.clusterDim.y = 1;
+  attr[na].val.clusterDim.z = 1;
+  ++na;
+  if (c->pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+  if (prof) {
+    cudaEventRecord(p.b, c->stream);
+    c->pending.push_back(p);
+  }
+  c->kl[cls]++;
+  c->kbytes_sum[cls] += bytes;
+  c->launches++;
+}
+
 Rows rows_of(const Shard *s, bool dyn = false) {
   Rows r{};
   r.work = dyn ? s->work : nullptr;
@@ -369,6 +414,12 @@ Rows rows_of(const Shard *s, bool dyn = false) {
 // Kernel instantiation for a shard's layout: uniform weights (values in the column's sign bit) or
 // not, and the ELL width (0: SELL + long rows).
 constexpr int kEllWidths[] = {2, 3, 4, 6, 8};
+// the resident cluster kernel exists for SELL (0) and ELL-3 / ELL-4; other widths use its SELL form
+#define SCG_RES_W(W) (((W) == 3 || (W) == 4) ? (W) : 0)
+#define SCG_PICK_RES(U, W)                                                                          \
+  (SCG_RES_W(W) == 3 ? ((U) ? k_resident<true, 3> : k_resident<false, 3>)                           \
+   : SCG_RES_W(W) == 4 ? ((U) ? k_resident<true, 4> : k_resident<false, 4>)                         \
+                       : ((U) ? k_resident<true, 0> : k_resident<false, 0>))
 #define SCG_PICK(K, U, W)                                          \
   ((W) == 2   ? ((U) ? K<true, 2> : K<false, 2>)                   \
    : (W) == 3 ? ((U) ? K<true, 3> : K<false, 3>)                   \
@@ -1337,7 +1388,35 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   }
   // one GPU: draw each next start vector on a lower-priority side stream during the Lanczos passes
   // (SCG_FUSED_RNG keeps the draw inside k_dual_sketch, as sharded runs always do)
-  c->side_rng = world == 1 && !(flags & SCG_FUSED_RNG);
+  // small graphs on one GPU: one cluster launch per iteration (k_resident), largest cluster that fits
+  if (world == 1 && c->store && n <= kResMaxN && !(flags & SCG_NO_RESIDENT)) {
+    Shard *s = c->sh[0];
+    auto kR = SCG_PICK_RES(s->sell_uniform, s->ellw);
+    const int smem = (int)sizeof(ResShared);
+    cudaFuncSetAttribute((const void *)kR, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute((const void *)kR, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int cl : {16, 8}) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(cl);
+      cfg.blockDim = dim3(kResThreads);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at{};
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = cl;
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      cfg.attrs = &at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, (const void *)kR, &cfg) == cudaSuccess && ncl >= 1) {
+        c->res_cl = cl;
+        break;
+      }
+    }
+    cudaGetLastError();  // (a refused query leaves the multi-kernel path)
+    dbg_log(c, "[scg] resident cluster kernel: %d CTAs, %d B shared memory\n", c->res_cl, smem);
+  }
+  c->side_rng = world == 1 && !(flags & SCG_FUSED_RNG) && c->res_cl == 0;
   if (c->side_rng) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -1425,6 +1504,40 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       if (c->store) return c->wslot(s, j - 1);
       return c->wslot(s, 1 + (j & 1));
     };
+    if (c->res_cl && !c->box && c->store && !c->fused) {  // ---- the whole iteration in one cluster launch
+      Shard *s = c->sh[0];
+      const int js = c->spend;
+      ResArgs P{};
+      P.G = s->G;
+      P.npad = c->npad;
+      P.a = s->a;
+      P.d = s->d;
+      P.z = s->z;
+      P.y = s->y;
+      P.cdiag = s->cdiag;
+      P.Om = s->Om;
+      P.V = s->V;
+      P.ldv = s->nlpad;
+      P.js = js;
+      P.ckr = s->ckr;
+      P.sc = s->sc;
+      P.log = s->dlog;
+      P.A = A;
+      P.R = c->R;
+      P.nl = (int)s->nl;
+      P.seed = c->seed;
+      P.orig = s->orig;
+      const double nb = (double)s->nl;
+      launch_cluster(c, KC_RESIDENT, q * s->kb[KC_LANCZOS_A] + (q - 1) * s->kb[KC_LANCZOS_B] + 8.0 * nb * q +
+                                         s->kb[KC_MONITOR] + s->kb[KC_PRIMAL] + s->kb[KC_DUAL_SKETCH],
+                     SCG_PICK_RES(s->sell_uniform, s->ellw), c->res_cl, dim3(kResThreads), sizeof(ResShared),
+                     Csr{s->rp, s->col, s->val}, rows_of(s), P);
+      c->ome[js] = A.one_m_eta;
+      c->vlast = js;
+      if (++c->spend == kSketchB) sketch_flush(c);
+      c->t = t;
+      continue;
+    }
     if (c->side_rng) {  // draw g_{t+1} into the buffer iteration t-1 used, once its readers are done
       Shard *s = c->sh[0];
       cudaEventRecord(c->evA, c->stream);

@@ -41,11 +41,14 @@ def _assert_trajectory(g, o, T):
     np.testing.assert_allclose(g.state("S"), S_o, rtol=0, atol=1e-13 * np.abs(S_o).max())
 
 
-def test_config0_full_trajectory_and_cut(gpu):
-    """configs[0] (ER n=800, R=10, T=1000, seed 0): every iterate, the objective and the cut."""
+@pytest.mark.parametrize("resident", [True, False])
+def test_config0_full_trajectory_and_cut(gpu, resident):
+    """configs[0] (ER n=800, R=10, T=1000, seed 0): every iterate, the objective and the cut -- with
+    the resident cluster kernel (one launch per iteration, the default below 2^16 rows) and with the
+    multi-kernel iteration."""
     L = si.laplacian("c0")
     T = 1000
-    g, o = _run_pair(gpu, L, 10, T, seed=0)
+    g, o = _run_pair(gpu, L, 10, T, seed=0, resident=resident)
     _assert_trajectory(g, o, T)
     U, lam, err = g.reconstruct()
     Uo, lam_o, err_o = oracle.nystrom_reconstruct(o.S, o.Omega, o.tau)
@@ -67,11 +70,12 @@ def test_config0_full_trajectory_and_cut(gpu):
     assert w == w_o
 
 
-@pytest.mark.parametrize("regenerate", [False, True])
-def test_config1_trajectory_signed_weights(gpu, regenerate):
-    """configs[1] shape (torus, +-1 weights), first 300 iterations bitwise, both Lanczos modes."""
+@pytest.mark.parametrize("regenerate,resident", [(False, True), (False, False), (True, False)])
+def test_config1_trajectory_signed_weights(gpu, regenerate, resident):
+    """configs[1] shape (torus, +-1 weights), first 300 iterations bitwise, both Lanczos modes, with and
+    without the resident cluster kernel."""
     L = si.laplacian("c1")
-    g, o = _run_pair(gpu, L, 10, 300, seed=1, regenerate=regenerate)
+    g, o = _run_pair(gpu, L, 10, 300, seed=1, regenerate=regenerate, resident=resident)
     _assert_trajectory(g, o, 300)
 
 
@@ -88,19 +92,20 @@ def test_unscaled_variant(gpu):
     _assert_trajectory(g, o, 60)
 
 
-@pytest.mark.parametrize("regenerate", [False, True])
-def test_breakdown_complete_graph(gpu, regenerate):
+@pytest.mark.parametrize("regenerate,resident", [(False, True), (False, False), (True, False)])
+def test_breakdown_complete_graph(gpu, regenerate, resident):
     """K_8: D_1 has two eigenvalues -> invariant subspace after 2 steps (Alg. 2 line 8)."""
     n = 8
     i, j = np.triu_indices(n, 1)
     L = si.laplacian_from_edges(n, i, j, np.ones(len(i)))
-    g, o = _run_pair(gpu, L, 3, 25, seed=2, regenerate=regenerate)
+    g, o = _run_pair(gpu, L, 3, 25, seed=2, regenerate=regenerate, resident=resident)
     assert o.log[0, 2] == 2 and o.log[0, 1] == 3  # k = 2 < q_1 = ceil(ln 8) = 3
     _assert_trajectory(g, o, 25)
 
 
+@pytest.mark.parametrize("resident", [True, False])
 @pytest.mark.parametrize("n", [2, 3, 5, 33, 257, 1000])
-def test_small_and_ragged_sizes(gpu, n):
+def test_small_and_ragged_sizes(gpu, n, resident):
     rng = np.random.default_rng(n)
     i = np.arange(n - 1)
     j = i + 1  # a path keeps the graph connected
@@ -111,7 +116,7 @@ def test_small_and_ragged_sizes(gpu, n):
     w = rng.uniform(0.5, 1.5, size=len(i))
     L = si.laplacian_from_edges(n, i, j, w)
     R = min(4, n)
-    g, o = _run_pair(gpu, L, R, 40, seed=n)
+    g, o = _run_pair(gpu, L, R, 40, seed=n, resident=resident)
     _assert_trajectory(g, o, 40)
 
 
