@@ -23,6 +23,10 @@ for w in "$@"; do
       N=${LIBF//[^a-zA-Z0-9_]/_}_${KRE//[^a-zA-Z0-9_]/_}
       SCG_LIB=paper_1912_02949_b200/lib/$LIBF ncu --set full --clock-control none --import-source on -k regex:"$KRE" -s $SKIP -c 2 -o $O/prof_$N python bench.py --steps 2 --warmup 5 --no-cpu --no-e2e --no-profile > $O/ncu_full_$N.log 2>&1
       echo "ncu exit $?" >> $O/ncu_full_$N.log ;;
+    cfg:*)  # cfg:<config>:<steps>:<opts> -- bench another workload
+      SPEC=${w#cfg:}; CFG=${SPEC%%:*}; REST=${SPEC#*:}; STEPS=${REST%%:*}; OPTS=${REST#*:}; [ "$OPTS" = "$REST" ] && OPTS=""
+      N=${CFG}_${STEPS}_${OPTS//[^a-zA-Z0-9_]/_}
+      timeout 900 python bench.py --config $CFG --steps $STEPS --warmup 3 --no-cpu --no-e2e --opts "$OPTS" > $O/cfg_$N.json 2> $O/cfg_$N.err; echo "exit $?" >> $O/cfg_$N.err ;;
     benchnocpu) timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 --no-cpu > $O/bench.json 2> $O/bench.err; echo "bench exit $?" >> $O/bench.err ;;
     full) timeout 900 python bench.py --steps 997 --warmup 3 --no-cpu --no-e2e > $O/bench_full.json 2> $O/bench_full.err; echo "exit $?" >> $O/bench_full.err ;;
     ref) timeout 900 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $O/ref.json 2> $O/ref.err; echo "ref exit $?" >> $O/ref.err ;;
