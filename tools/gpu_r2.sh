@@ -27,6 +27,11 @@ for w in "$@"; do
       SPEC=${w#cfg:}; CFG=${SPEC%%:*}; REST=${SPEC#*:}; STEPS=${REST%%:*}; OPTS=${REST#*:}; [ "$OPTS" = "$REST" ] && OPTS=""
       N=${CFG}_${STEPS}_${OPTS//[^a-zA-Z0-9_]/_}
       timeout 900 python bench.py --config $CFG --steps $STEPS --warmup 3 --no-cpu --no-e2e --opts "$OPTS" > $O/cfg_$N.json 2> $O/cfg_$N.err; echo "exit $?" >> $O/cfg_$N.err ;;
+    ncuc:*)  # ncuc:<config>:<kernel regex>:<skip>
+      SPEC=${w#ncuc:}; CFG=${SPEC%%:*}; REST=${SPEC#*:}; KRE=${REST%%:*}; SKIP=${REST##*:}
+      N=${CFG}_${KRE//[^a-zA-Z0-9_]/_}
+      ncu --set full --clock-control none --import-source on -k regex:"$KRE" -s $SKIP -c 1 -o $O/prof_$N python bench.py --config $CFG --steps 2 --warmup 60 --no-cpu --no-e2e --no-profile > $O/ncu_full_$N.log 2>&1
+      echo "ncu exit $?" >> $O/ncu_full_$N.log ;;
     benchnocpu) timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 --no-cpu > $O/bench.json 2> $O/bench.err; echo "bench exit $?" >> $O/bench.err ;;
     full) timeout 900 python bench.py --steps 997 --warmup 3 --no-cpu --no-e2e > $O/bench_full.json 2> $O/bench_full.err; echo "exit $?" >> $O/bench_full.err ;;
     ref) timeout 900 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $O/ref.json 2> $O/ref.err; echo "ref exit $?" >> $O/ref.err ;;
