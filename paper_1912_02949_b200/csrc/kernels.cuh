@@ -1606,9 +1606,34 @@ struct TriScratch {  // shared-memory working arrays of one tridiagonal solve
   double om[kMaxQ], rho[kMaxQ], rho2[kMaxQ], u0[kMaxQ], u1[kMaxQ], u2[kMaxQ], mul[kMaxQ], xv[kMaxQ], s[kMaxQ],
       ru0[kMaxQ];
   int swp[kMaxQ];
+  unsigned char uok[kMaxQ];  // u0[i] inside the range where the shared-divisor division is exact
 };
 
-// CAC-5 on one full warp (lanes 0..31 of the calling warp); sc may live in shared memory.
+// Warp reductions that return, on every lane, exactly what a left-to-right scan over j = 0..k-1
+// returns: the first (lowest j) extreme value; v, j hold the lane's own scan result (j = -1: none).
+__device__ __forceinline__ void warp_first_min(double &v, int &j) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+    if (oj >= 0 && (j < 0 || ov < v || (ov == v && oj < j))) { v = ov; j = oj; }
+  }
+}
+__device__ __forceinline__ void warp_first_max(double &v, int &j) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+    if (oj >= 0 && (j < 0 || ov > v || (ov == v && oj < j))) { v = ov; j = oj; }
+  }
+}
+
+// CAC-5 on one full warp (lanes 0..31 of the calling warp); sc may live in shared memory.  The
+// arithmetic is the sequential algorithm's, operation for operation: the independent parts (the
+// Gershgorin bounds, the 32 Sturm counts of a multisection round, 1/u0, the initial vector, the
+// max-norm rescaling, the sign fix) are spread over the lanes -- exact min / max scans keep the
+// first extreme, like the sequential scan -- and the three dependent recurrences (the pivoted LU,
+// forward elimination and back substitution) run on lane 0 with their running values in registers.
 __device__ __noinline__ void tridiag_warp(DevScalars *sc, int q, TriScratch &T) {
   double *om = T.om, *rho = T.rho, *rho2 = T.rho2;
   const int lane = threadIdx.x & 31;
@@ -1620,23 +1645,23 @@ __device__ __noinline__ void tridiag_warp(DevScalars *sc, int q, TriScratch &T) 
     if (lane == 0) { sc->theta = om[0]; sc->s[0] = 1.0; sc->k = 1; }
     return;
   }
-  // Gershgorin interval (sequential on lane 0; min/max are exact anyway)
+  // Gershgorin interval: lo = min_j (om_j - r_j), hi = max_j (om_j + r_j), exact
   double lo = 0.0, hi = 0.0;
-  if (lane == 0) {
-    for (int j = 0; j < k; ++j) {
-      const double rl = j > 0 ? rho[j - 1] : 0.0;
-      const double rr = j < k - 1 ? rho[j] : 0.0;
-      const double rj = rl + rr;
-      const double a = om[j] - rj, b = om[j] + rj;
-      if (j == 0 || a < lo) lo = a;
-      if (j == 0 || b > hi) hi = b;
-    }
+  int jl = -1, jh = -1;
+  for (int j = lane; j < k; j += 32) {
+    const double rl = j > 0 ? rho[j - 1] : 0.0;
+    const double rr = j < k - 1 ? rho[j] : 0.0;
+    const double rj = rl + rr;
+    const double a = om[j] - rj, b = om[j] + rj;
+    if (jl < 0 || a < lo) { lo = a; jl = j; }
+    if (jh < 0 || b > hi) { hi = b; jh = j; }
   }
-  lo = __shfl_sync(0xffffffffu, lo, 0);
-  hi = __shfl_sync(0xffffffffu, hi, 0);
+  warp_first_min(lo, jl);
+  warp_first_max(hi, jh);
   const double NT = fabs(lo) > fabs(hi) ? fabs(lo) : fabs(hi);
   if (NT == 0.0) {
-    if (lane == 0) { sc->theta = 0.0; for (int j = 0; j < k; ++j) sc->s[j] = j == 0 ? 1.0 : 0.0; sc->k = k; }
+    for (int j = lane; j < k; j += 32) sc->s[j] = j == 0 ? 1.0 : 0.0;
+    if (lane == 0) { sc->theta = 0.0; sc->k = k; }
     return;
   }
   const double pad = NT * 0x1p-20;
@@ -1659,66 +1684,97 @@ __device__ __noinline__ void tridiag_warp(DevScalars *sc, int q, TriScratch &T) 
       lo = __shfl_sync(0xffffffffu, x, 31);
     }
   }
-  if (lane != 0) return;
   const double th = (lo + hi) * 0.5;
-  sc->theta = th;
-  // working arrays of the sequential part in shared memory (a local-memory stack would start
-  // cold in L1 at every launch)
   double *u0 = T.u0, *u1 = T.u1, *u2 = T.u2, *mul = T.mul, *xv = T.xv, *s = T.s, *ru0 = T.ru0;
   int *swp = T.swp;
   const double tiny = NT * 0x1p-60;
-  double c0 = om[0] - th, c1 = rho[0], c2 = 0.0;
-  for (int i = 0; i < k - 1; ++i) {
-    const double nb = rho[i], na = om[i + 1] - th, nc = (i + 1 < k - 1) ? rho[i + 1] : 0.0;
-    if (fabs(c0) >= fabs(nb)) {
-      const double m = c0 != 0.0 ? nb / c0 : 0.0;
-      u0[i] = c0; u1[i] = c1; u2[i] = c2; swp[i] = 0; mul[i] = m;
-      c0 = na - m * c1;
-      c1 = nc - m * c2;
-      c2 = 0.0;
-    } else {
-      const double m = c0 / nb;
-      u0[i] = nb; u1[i] = na; u2[i] = nc; swp[i] = 1; mul[i] = m;
-      const double t0 = c1 - m * na, t1 = c2 - m * nc;
-      c0 = t0;
-      c1 = t1;
-      c2 = 0.0;
-    }
-  }
-  u0[k - 1] = c0; u1[k - 1] = 0.0; u2[k - 1] = 0.0;
-  for (int i = 0; i < k; ++i)
-    if (fabs(u0[i]) < tiny) u0[i] = u0[i] < 0.0 ? -tiny : tiny;
-  // the three back substitutions divide by the same pivots: RN(1/u0) once, then the
-  // shared-divisor IEEE division div_rn (bitwise RN(t/u0) for normal-range operands,
-  // self-tested; hardware division outside that range)
-  for (int i = 0; i < k; ++i) ru0[i] = 1.0 / u0[i];
-  for (int j = 0; j < k; ++j) s[j] = (double)(j % 5 + 1) * 0.25;
-  for (int it = 0; it < 3; ++it) {
-    for (int j = 0; j < k; ++j) xv[j] = s[j];
+  if (lane == 0) {  // Gaussian elimination with partial pivoting of T - theta I (three upper diagonals)
+    sc->theta = th;
+    double c0 = om[0] - th, c1 = rho[0], c2 = 0.0;
+#pragma unroll 4
     for (int i = 0; i < k - 1; ++i) {
-      if (swp[i]) { const double t = xv[i]; xv[i] = xv[i + 1]; xv[i + 1] = t; }
-      xv[i + 1] = fma(-mul[i], xv[i], xv[i + 1]);
+      const double nb = rho[i], na = om[i + 1] - th, nc = (i + 1 < k - 1) ? rho[i + 1] : 0.0;
+      if (fabs(c0) >= fabs(nb)) {
+        const double m = c0 != 0.0 ? nb / c0 : 0.0;
+        u0[i] = c0; u1[i] = c1; u2[i] = c2; swp[i] = 0; mul[i] = m;
+        c0 = na - m * c1;
+        c1 = nc - m * c2;
+        c2 = 0.0;
+      } else {
+        const double m = c0 / nb;
+        u0[i] = nb; u1[i] = na; u2[i] = nc; swp[i] = 1; mul[i] = m;
+        const double t0 = c1 - m * na, t1 = c2 - m * nc;
+        c0 = t0;
+        c1 = t1;
+        c2 = 0.0;
+      }
     }
-    for (int i = k - 1; i >= 0; --i) {
-      double t = xv[i];
-      if (i + 1 < k) t = fma(-u1[i], xv[i + 1], t);
-      if (i + 2 < k) t = fma(-u2[i], xv[i + 2], t);
-      const double at = fabs(t), au = fabs(u0[i]);
-      xv[i] = (at > 0x1p-400 && at < 0x1p400 && au > 0x1p-400 && au < 0x1p400) ? div_rn(t, u0[i], ru0[i])
-                                                                            : t / u0[i];
+    u0[k - 1] = c0; u1[k - 1] = 0.0; u2[k - 1] = 0.0;
+  }
+  __syncwarp();
+  // pivot clamp; the three back substitutions divide by the same pivots: RN(1/u0) once, then the
+  // shared-divisor IEEE division div_rn (bitwise RN(t/u0) for normal-range operands, self-tested;
+  // hardware division outside that range)
+  for (int i = lane; i < k; i += 32) {
+    double u = u0[i];
+    if (fabs(u) < tiny) u = u < 0.0 ? -tiny : tiny;
+    u0[i] = u;
+    ru0[i] = 1.0 / u;
+    const double au = fabs(u);
+    T.uok[i] = au > 0x1p-400 && au < 0x1p400;
+  }
+  for (int j = lane; j < k; j += 32) s[j] = (double)(j % 5 + 1) * 0.25;
+  __syncwarp();
+  for (int it = 0; it < 3; ++it) {
+    for (int j = lane; j < k; j += 32) xv[j] = s[j];
+    __syncwarp();
+    if (lane == 0) {
+      // forward elimination: a = the running entry i, b = entry i+1
+      double a = xv[0];
+#pragma unroll 4
+      for (int i = 0; i < k - 1; ++i) {
+        double b = xv[i + 1];
+        if (swp[i]) { const double t = a; a = b; b = t; }
+        xv[i] = a;
+        a = fma(-mul[i], a, b);
+      }
+      xv[k - 1] = a;
+      // back substitution: x1, x2 = the new entries i+1, i+2
+      double x1 = 0.0, x2 = 0.0;
+#pragma unroll 4
+      for (int i = k - 1; i >= 0; --i) {
+        double t = xv[i];
+        if (i + 1 < k) t = fma(-u1[i], x1, t);
+        if (i + 2 < k) t = fma(-u2[i], x2, t);
+        const double at = fabs(t);
+        const double r = (at > 0x1p-400 && at < 0x1p400 && T.uok[i]) ? div_rn(t, u0[i], ru0[i]) : t / u0[i];
+        xv[i] = r;
+        x2 = x1;
+        x1 = r;
+      }
     }
+    __syncwarp();
     double mx = 0.0;
-    for (int j = 0; j < k; ++j) mx = fabs(xv[j]) > mx ? fabs(xv[j]) : mx;
+    for (int j = lane; j < k; j += 32) mx = fabs(xv[j]) > mx ? fabs(xv[j]) : mx;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double om2 = __shfl_xor_sync(0xffffffffu, mx, o);
+      mx = om2 > mx ? om2 : mx;
+    }
     const double p2 = __longlong_as_double(__double_as_longlong(mx) & 0x7ff0000000000000ll);
     const double sc2 = 1.0 / p2;
-    for (int j = 0; j < k; ++j) s[j] = xv[j] * sc2;
+    for (int j = lane; j < k; j += 32) s[j] = xv[j] * sc2;
+    __syncwarp();
   }
-  int jm = 0;
-  for (int j = 1; j < k; ++j)
-    if (fabs(s[j]) > fabs(s[jm])) jm = j;
-  const double sg = s[jm] < 0.0 ? -1.0 : 1.0;
-  for (int j = 0; j < k; ++j) sc->s[j] = sg < 0.0 ? -s[j] : s[j];
-  sc->k = k;
+  // sign: the largest |s_j| (first on ties) positive
+  double am = -1.0;
+  int jm = -1;
+  for (int j = lane; j < k; j += 32)
+    if (jm < 0 || fabs(s[j]) > am) { am = fabs(s[j]); jm = j; }
+  warp_first_max(am, jm);
+  const bool neg = s[jm] < 0.0;
+  for (int j = lane; j < k; j += 32) sc->s[j] = neg ? -s[j] : s[j];
+  if (lane == 0) sc->k = k;
 }
 
 __global__ void k_tridiag(DevScalars *sc, int q) {
@@ -2259,7 +2315,8 @@ struct ResShared {
   double red[kResThreads / 32][kMaxR];        // warp partials of g
   double sv[kMaxQ], srr[kMaxQ];               // s_j and fl(1/rho_j) of the combine
   TriScratch tri;
-  unsigned long long xbw[kMaxSums][kLimbs];   // (scratch of the limb reads)
+  long long Lsum[kMaxSums][kLimbs];           // the cluster totals of the current reduction
+  double gsum[kMaxR];
 };
 
 // Cluster-wide exact reduction of NS sums (and, with R > 0, of the CTAs' g partials in CTA order),
@@ -2274,32 +2331,22 @@ __device__ __forceinline__ void res_reduce(XWin (&acc)[NS], int err, ResShared &
   cl.sync();  // every CTA's partials are complete (and every store of the phase is visible)
   const int ncta = (int)cl.num_blocks();
   if (threadIdx.x < 32) {
+    // lanes add the CTAs' limbs (exact integers) and g partials (fp64, CTA order) straight into
+    // shared memory; lane 0 finalizes from there (no shuffles, no local-memory arrays)
     const int lane = threadIdx.x;
-    long long part[2] = {0, 0};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int idx = lane + 32 * h;
+    for (int idx = lane; idx < kMaxSums * kLimbs; idx += 32) {
+      long long t = 0;
       if (idx < NS * kLimbs)
-        for (int c = 0; c < ncta; ++c) part[h] += *cl.map_shared_rank(&sm.xb[par][0][0] + idx, c);
+        for (int c = 0; c < ncta; ++c) t += *cl.map_shared_rank(&sm.xb[par][0][0] + idx, c);
+      (&sm.Lsum[0][0])[idx] = t;
     }
-    double gpart[2] = {0.0, 0.0};  // g_k summed over the CTAs in CTA order
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k = lane + 32 * h;
-      if (k < R)
-        for (int c = 0; c < ncta; ++c) gpart[h] += *cl.map_shared_rank(&sm.gk[par][k], c);
+    for (int k = lane; k < R; k += 32) {
+      double t = 0.0;
+      for (int c = 0; c < ncta; ++c) t += *cl.map_shared_rank(&sm.gk[par][k], c);
+      sm.gsum[k] = t;
     }
-    long long L[kMaxSums][kLimbs];
-    double gk[kMaxR];
-    for (int idx = 0; idx < kMaxSums * kLimbs; ++idx) {
-      const long long v = __shfl_sync(0xffffffffu, part[idx >> 5], idx & 31);
-      if (lane == 0) L[idx / kLimbs][idx % kLimbs] = idx < NS * kLimbs ? v : 0ll;
-    }
-    for (int k = 0; k < kMaxR; ++k) {
-      const double v = __shfl_sync(0xffffffffu, gpart[k >> 5], k & 31);
-      if (lane == 0) gk[k] = v;
-    }
-    if (lane == 0) finalize(kind, &sm.sc, L, gk, f);
+    __syncwarp();
+    if (lane == 0) finalize(kind, &sm.sc, sm.Lsum, sm.gsum, f);
   }
   // the other buffer is free: its readers (the previous reduction) are past this barrier
   for (int i = threadIdx.x; i < kMaxSums * kLimbs; i += blockDim.x) (&sm.xb[par ^ 1][0][0])[i] = 0;
