@@ -525,33 +525,6 @@ __device__ __forceinline__ const double *gaddr(const double *X, int c) {
   return p;
 }
 
-#ifndef SCG_L2HINT
-#define SCG_L2HINT 0  // experiment: L2 eviction hints (streams evict-first, the SpMV output evict-last)
-#endif
-__device__ __forceinline__ unsigned long long l2_policy_first() {
-  unsigned long long p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ unsigned long long l2_policy_last() {
-  unsigned long long p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ int ld_first_i32(const int *p, unsigned long long pol) {
-  int v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double ld_first_f64(const double *p, unsigned long long pol) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void st_last_f64(double *p, double v, unsigned long long pol) {
-  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
-}
-
 template <int NC, bool UNI, int W, class Epi>
 __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restrict__ X, double den,
                                          const double *__restrict__ diag0, const double *__restrict__ diag1,
@@ -567,12 +540,11 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
   const double *__restrict__ ev = RL.eval + lane;
   const int padc = RL.padc;
   const double m0 = RL.m0;
-  const unsigned long long pfirst = SCG_L2HINT ? l2_policy_first() : 0ull;
   auto cload = [&](int q, int (&c)[W]) {
     if (q < s_end) {
       const int *cp = ec + (long long)q * (32 * W);
 #pragma unroll
-      for (int u = 0; u < W; ++u) c[u] = SCG_L2HINT ? ld_first_i32(cp + 32 * u, pfirst) : __ldg(cp + 32 * u);
+      for (int u = 0; u < W; ++u) c[u] = __ldg(cp + 32 * u);
     } else {
 #pragma unroll
       for (int u = 0; u < W; ++u) c[u] = padc;
@@ -601,7 +573,7 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
     dd1 = 0.0;
     if (q < s_end && p < nl) {
       xo = X[rb + p];
-      dd0 = SCG_L2HINT ? ld_first_f64(diag0 + p, pfirst) : diag0[p];
+      dd0 = diag0[p];
       if (NC > 1) dd1 = diag1[p];
     }
   };
@@ -1047,11 +1019,7 @@ struct EpiA {
   XWin acc[1];
   int err;
   __device__ __forceinline__ void operator()(const RowOut<1> &o) {
-#if SCG_L2HINT
-    st_last_f64(&a[o.r], o.s[0], l2_policy_last());  // read back by the recurrence kernel right after
-#else
     a[o.r] = o.s[0];
-#endif
     xwin_add(acc[0], o.xr * o.s[0], err, blk);
   }
 };
@@ -1625,9 +1593,13 @@ __device__ int sturm_count(const double *om, const double *rho2, int k, double x
     pprev = p;
     p = pn;
     s = sn;
+    // rescale by 2^-500 / 2^500 when the sequence leaves [2^-500, 2^500]: branch-free (every lane has
+    // its own x, a branch would diverge); a multiplication by 1.0 is exact, so the bits are those of
+    // the branching form
     const double ap = fabs(p), aq = fabs(pprev);
-    if (ap > 0x1p500) { p *= 0x1p-500; pprev *= 0x1p-500; }
-    else if (ap < 0x1p-500 && aq < 0x1p-500) { p *= 0x1p500; pprev *= 0x1p500; }
+    const double f = ap > 0x1p500 ? 0x1p-500 : ((ap < 0x1p-500 && aq < 0x1p-500) ? 0x1p500 : 1.0);
+    p *= f;
+    pprev *= f;
   }
   return cnt;
 }
@@ -1779,7 +1751,8 @@ __device__ __noinline__ void tridiag_warp(DevScalars *sc, int q, TriScratch &T) 
         if (i + 1 < k) t = fma(-u1[i], x1, t);
         if (i + 2 < k) t = fma(-u2[i], x2, t);
         const double at = fabs(t);
-        const double r = (at > 0x1p-400 && at < 0x1p400 && T.uok[i]) ? div_rn(t, u0[i], ru0[i]) : t / u0[i];
+        double r = div_rn(t, u0[i], ru0[i]);
+        if (!(at > 0x1p-400 && at < 0x1p400 && T.uok[i])) r = t / u0[i];  // (rare: outside the exact range)
         xv[i] = r;
         x2 = x1;
         x1 = r;

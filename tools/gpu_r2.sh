@@ -32,6 +32,10 @@ for w in "$@"; do
       N=${CFG}_${KRE//[^a-zA-Z0-9_]/_}
       ncu --set full --clock-control none --import-source on -k regex:"$KRE" -s $SKIP -c 1 -o $O/prof_$N python bench.py --config $CFG --steps 2 --warmup 60 --no-cpu --no-e2e --no-profile > $O/ncu_full_$N.log 2>&1
       echo "ncu exit $?" >> $O/ncu_full_$N.log ;;
+    cfgnp:*)  # cfgnp:<config>:<steps>:<opts> -- as cfg, without per-kernel events (launch-bound graphs)
+      SPEC=${w#cfgnp:}; CFG=${SPEC%%:*}; REST=${SPEC#*:}; STEPS=${REST%%:*}; OPTS=${REST#*:}; [ "$OPTS" = "$REST" ] && OPTS=""
+      N=${CFG}_${STEPS}_${OPTS//[^a-zA-Z0-9_]/_}
+      timeout 900 python bench.py --config $CFG --steps $STEPS --warmup 3 --no-cpu --no-e2e --no-profile --opts "$OPTS" > $O/cfgnp_$N.json 2> $O/cfgnp_$N.err; echo "exit $?" >> $O/cfgnp_$N.err ;;
     benchnocpu) timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 --no-cpu > $O/bench.json 2> $O/bench.err; echo "bench exit $?" >> $O/bench.err ;;
     full) timeout 900 python bench.py --steps 997 --warmup 3 --no-cpu --no-e2e > $O/bench_full.json 2> $O/bench_full.err; echo "exit $?" >> $O/bench_full.err ;;
     ref) timeout 900 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $O/ref.json 2> $O/ref.err; echo "ref exit $?" >> $O/ref.err ;;
