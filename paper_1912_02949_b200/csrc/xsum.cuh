@@ -157,42 +157,31 @@ __device__ __forceinline__ void xwin_add_nn(XWin &a, double p, int &err, long lo
 }
 
 // Flush a thread's window into the block accumulator (all 32 lanes of the warp call this).
+// The lanes' windows are placed at their absolute digit positions inside the warp's common span
+// [qlo, qhi + 4] (a register re-indexing, no arithmetic), then each digit of the span is summed with
+// one shuffle tree and lane 0 adds it to the block accumulator: one reduction round whatever the
+// mix of anchors (lanes whose first summands differ in magnitude).
 __device__ __forceinline__ void xwin_flush(const XWin &a, long long *blk) {
-  const int qa0 = __shfl_sync(0xffffffffu, a.qa, 0);
-  const bool same = __all_sync(0xffffffffu, a.qa == qa0 || a.qa < 0) && qa0 >= 0;
+  const bool has = a.qa >= 0;
+  int qlo = has ? a.qa : 1 << 20, qhi = has ? a.qa : -1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    qlo = min(qlo, __shfl_xor_sync(0xffffffffu, qlo, o));
+    qhi = max(qhi, __shfl_xor_sync(0xffffffffu, qhi, o));
+  }
+  if (qhi < 0) return;  // no lane has a summand
   const bool mine = (threadIdx.x & 31) == 0;
-  long long w[5] = {a.w0, a.w1, a.w2, a.w3, a.w4};
-  if (same) {
+  const long long w[5] = {a.w0, a.w1, a.w2, a.w3, a.w4};
+  const int sh = has ? a.qa - qlo : 0;  // this lane's offset inside the span
+#pragma unroll 2
+  for (int p = 0; p <= qhi - qlo + 4; ++p) {  // digit qlo + p (warp-uniform bound, <= kLimbs)
+    const int j = p - sh;  // this lane's window word at that digit
+    long long v = 0;
 #pragma unroll
-    for (int j = 0; j < 5; ++j) {
+    for (int u = 0; u < 5; ++u) v = (has && j == u) ? w[u] : v;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) w[j] += __shfl_down_sync(0xffffffffu, w[j], o);
-    }
-    if (mine)
-#pragma unroll
-      for (int j = 0; j < 5; ++j)
-        if (w[j]) atomicAdd(reinterpret_cast<unsigned long long *>(&blk[qa0 + j]), (unsigned long long)w[j]);
-  } else {
-    // Lanes anchored at different digit classes: reduce each anchor group with shuffles
-    // (a few rounds; one per distinct anchor) instead of 32 lanes spinning on the same
-    // shared limb (64-bit shared atomics are CAS loops on sm_100).
-    unsigned pending = __ballot_sync(0xffffffffu, a.qa >= 0);
-    while (pending) {
-      const int ql = __shfl_sync(0xffffffffu, a.qa, __ffs(pending) - 1);
-      const bool in = a.qa == ql;
-      pending &= ~__ballot_sync(0xffffffffu, in);
-      long long v[5];
-#pragma unroll
-      for (int j = 0; j < 5; ++j) {
-        v[j] = in ? w[j] : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_down_sync(0xffffffffu, v[j], o);
-      }
-      if (mine)
-#pragma unroll
-        for (int j = 0; j < 5; ++j)
-          if (v[j]) atomicAdd(reinterpret_cast<unsigned long long *>(&blk[ql + j]), (unsigned long long)v[j]);
-    }
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (mine && v) atomicAdd(reinterpret_cast<unsigned long long *>(&blk[qlo + p]), (unsigned long long)v);
   }
 }
 
