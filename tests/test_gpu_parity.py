@@ -460,22 +460,26 @@ def test_sharded_rejects_asymmetric_pattern(gpu):
     gpu.SketchyCGAL(bad, R=4, seed=1).close()
 
 
-def test_bench_launch_configuration_bitwise(gpu):
-    """The configuration bench.py times -- torch's stream passed in, SCG_PROFILE event sampling,
-    programmatic dependent launches -- gives the oracle's bits (configs[1] shape, 200 iterations)."""
+@pytest.mark.parametrize("resident", [False, True])
+def test_bench_launch_configuration_bitwise(gpu, resident):
+    """The configuration bench.py times -- torch's stream passed in (high priority), SCG_PROFILE event
+    sampling, programmatic dependent launches, the side-stream start vectors (multi-kernel) or the
+    resident cluster kernel -- gives the oracle's bits (configs[1] shape, 200 iterations)."""
     import ctypes
     import torch
     L = si.laplacian("c1")
-    stream = torch.cuda.Stream()
+    stream = torch.cuda.Stream(priority=-100)
     with torch.cuda.stream(stream):
-        g = gpu.SketchyCGAL(L, R=10, seed=1, profile=True, stream=ctypes.c_void_p(stream.cuda_stream))
+        g = gpu.SketchyCGAL(L, R=10, seed=1, profile=True, stream=ctypes.c_void_p(stream.cuda_stream),
+                            resident=resident)
         g.step(3)
         g.synchronize()
         g.reset_stats()
         g.step(197)
         g.synchronize()
         stats = {s["name"]: s for s in g.kernel_stats()}
-    assert stats["lanczos_a_spmv_dot"]["launches"] > 0 and stats["lanczos_a_spmv_dot"]["total_ms"] > 0
+    main = "resident_iteration" if resident else "lanczos_a_spmv_dot"
+    assert stats[main]["launches"] > 0 and stats[main]["total_ms"] > 0
     o = oracle.Oracle(L, 10, seed=1, logcap=200)
     o.step(200)
     _assert_trajectory(g, o, 200)
