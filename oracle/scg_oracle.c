@@ -24,7 +24,8 @@
  *          dot(a, b) = xsum(fl(a_r * b_r)).
  *   CAC-3  (D x)_r = d_r x_r + sum_{j in N(r), ascending} m_rj x_j, left to right,
  *          acc = fl(d_r * x_r); acc = fma(m_rj, x_j, acc); rows of more than 32
- *          entries: 32 strided partial chains combined by halving (reading R27).
+ *          entries: 32 (rows of more than 1024 entries: 256) strided partial chains
+ *          combined by halving (reading R27).
  *   CAC-4  Alg. 2 as printed, two-pass, with readings R1-R5; a
  *          normalization v / rho is evaluated as v * fl(1/rho) (reading R26).
  *   CAC-5  tridiagonal min eigenpair by Sturm multisection + inverse iteration.
@@ -190,11 +191,13 @@ typedef struct {
 } o_off;
 
 /* CAC-3 row of D x.  Rows with at most 32 off-diagonal entries: one chain from fl(d_r x_r).
- * Longer rows (reading R27, SURVEY.md section 8(c) CAC-2 with W = 32): partial chain l
- * (l = 0..31) runs over the entries k = l, l+32, l+64, ... of the row (ascending column
- * order) by fma from 0; the 32 partials combine by halving, L[l] = L[l] + L[l+off] for
- * off = 16, 8, 4, 2, 1 and l < off; the row is fl(fl(d_r x_r) + L[0]). */
+ * Longer rows (reading R27): W strided partial chains, W = 32 for
+ * rows of 33..1024 entries and W = 256 for rows of more than 1024 entries; partial chain l
+ * (l = 0..W-1) runs over the entries k = l, l+W, l+2W, ... of the row (ascending column order)
+ * by fma from 0; the W partials combine by halving, L[l] = L[l] + L[l+off] for
+ * off = W/2, ..., 2, 1 and l < off; the row is fl(fl(d_r x_r) + L[0]). */
 #define O_LONG_ROW 32
+#define O_HEAVY_ROW 1024
 static void o_apply(const o_off *A, const double *d, const double *x, double *y) {
 #pragma omp parallel for schedule(static, 4096) if (A->n > 65536)
   for (int64_t r = 0; r < A->n; ++r) {
@@ -204,13 +207,14 @@ static void o_apply(const o_off *A, const double *d, const double *x, double *y)
       for (int64_t k = a; k < b; ++k) acc = fma(A->m[k], x[A->col[k]], acc);
       y[r] = acc;
     } else {
-      double L[O_LONG_ROW];
-      for (int l = 0; l < O_LONG_ROW; ++l) L[l] = 0.0;
+      const int W = b - a > O_HEAVY_ROW ? 256 : 32;
+      double L[256];
+      for (int l = 0; l < W; ++l) L[l] = 0.0;
       for (int64_t k = a; k < b; ++k) {
-        const int l = (int)((k - a) % O_LONG_ROW);
+        const int l = (int)((k - a) % W);
         L[l] = fma(A->m[k], x[A->col[k]], L[l]);
       }
-      for (int off = O_LONG_ROW / 2; off >= 1; off /= 2)
+      for (int off = W / 2; off >= 1; off /= 2)
         for (int l = 0; l < off; ++l) L[l] = L[l] + L[l + off];
       y[r] = d[r] * x[r] + L[0];
     }

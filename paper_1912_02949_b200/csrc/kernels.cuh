@@ -180,10 +180,13 @@ constexpr int kMinBlocksUni = 3;  // min blocks per SM of the uniform-weight SEL
 // 140 us on configs[3]: the fourth block per SM is worth more than the extra slack)
 constexpr int ell_min_blocks(int W, bool uni) { return W <= 4 ? 4 : (uni ? 3 : 2); }
 constexpr int kLongRow = 32;
+constexpr int kHeavyRow = 1024;  // rows with more entries are "heavy": a block each (256 strided chains)
 
 struct Rows {
-  const int *longrows;  // local ids of long rows
+  const int *longrows;  // local ids of long rows (33..1024 entries), longest first
   int nlong;
+  const int *heavyrows; // local ids of heavy rows (> 1024 entries), longest first
+  int nheavy;
   // SELL-32-sigma layout of the short rows.  Rows are relabeled at init so that each
   // window of kSortWin rows is sorted by length (long rows first): slice s covers the 32
   // consecutive rows 32 s .. 32 s + 31; slot j of lane l is at meta[s].x + 32 j + l;
@@ -306,8 +309,62 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                : "memory");
 }
 
+// One heavy row (> kHeavyRow entries) by a block; result valid in thread 0.  CAC-3 for heavy rows
+// (reading R27, SURVEY CAC-2's W = 256 bin): thread l (l < 256) runs the partial chain over the row's
+// entries l, l+256, ... (ascending column order) by fma from 0; the partials combine by halving in
+// shared memory (L[l] = L[l] + L[l+off], off = 128..1) and the row is fl(fl(d_r x_r) + L[0]).  Every
+// thread of the block calls this (threads >= 256 only take part in the barriers).
+template <int NC>
+__device__ __forceinline__ void heavy_row_chain(const Csr &C, int r, const double *__restrict__ X, double den,
+                                                const double *__restrict__ diag0, const double *__restrict__ diag1,
+                                                long long rb, RowOut<NC> &o) {
+  __shared__ double hv[NC][256];
+  const int tid = threadIdx.x;
+  const int e0 = __ldg(&C.rp[r]), e1 = __ldg(&C.rp[r + 1]);
+  const double rden = 1.0 / den;
+  double part[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) part[c] = 0.0;
+  if (tid < 256) {
+    int e = e0 + tid;
+    // four entries of the thread's chain in flight at a time
+    for (; e + 3 * 256 < e1; e += 4 * 256) {
+      double m[4], x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        m[u] = __ldg(&C.val[e + u * 256]);
+        x[u] = __ldg(&X[__ldg(&C.col[e + u * 256])]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) part[c] = fma(m[u], x[u] * rden, part[c]);  // v = w * fl(1/rho) (R26)
+    }
+    for (; e < e1; e += 256) {
+      const double m = __ldg(&C.val[e]), x = __ldg(&X[__ldg(&C.col[e])]) * rden;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) part[c] = fma(m, x, part[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) hv[c][tid] = part[c];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int off = 128; off >= 1; off >>= 1) {
+    if (tid < off)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) hv[c][tid] = hv[c][tid] + hv[c][tid + off];
+    __syncthreads();
+  }
+  o.r = r;
+  o.xr = X[rb + r] * rden;
+  o.s[0] = diag0[r] * o.xr + hv[0][0];
+  if (NC > 1) o.s[NC - 1] = diag1[r] * o.xr + hv[NC - 1][0];
+  __syncthreads();  // hv is reused by the block's next heavy row
+}
+
 // Visit every row of this rank once: epi(RowOut) is called by the owning thread
-// (short rows) or by lane 0 of the owning warp (long rows).
+// (short rows), lane 0 of the owning warp (long rows) or thread 0 of the owning block (heavy rows).
 template <int NC, bool UNI, class Epi>
 __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
                                           const double *__restrict__ diag0, const double *__restrict__ diag1,
@@ -315,6 +372,11 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int h = blockIdx.x; h < RL.nheavy; h += gridDim.x) {  // block-uniform loop
+    RowOut<NC> o;
+    heavy_row_chain<NC>(C, RL.heavyrows[h], X, den, diag0, diag1, rb, o);
+    if (threadIdx.x == 0) epi(o);
+  }
   for (int w = gw; w < RL.nlong; w += nw) {
     RowOut<NC> o;
     long_row_chain<NC>(C, RL.longrows[w], X, den, diag0, diag1, rb, o);

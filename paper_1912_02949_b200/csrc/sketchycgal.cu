@@ -95,8 +95,10 @@ struct Shard {
   DevScalars *sc = nullptr;
   XSlot *slots = nullptr;
   scg_iter_rec *dlog = nullptr;
-  int *longrows = nullptr;
+  int *longrows = nullptr;  // rows of 33..1024 entries (warp per row), longest first
   int nlong = 0;
+  int *heavyrows = nullptr;  // rows of more than 1024 entries (block per row), longest first
+  int nheavy = 0;
   int *sell_col = nullptr;
   int2 *sell_meta = nullptr;
   double *sell_val = nullptr;
@@ -400,6 +402,8 @@ Rows rows_of(const Shard *s, bool dyn = false) {
   r.work = dyn ? s->work : nullptr;
   r.longrows = s->longrows;
   r.nlong = s->nlong;
+  r.heavyrows = s->heavyrows;
+  r.nheavy = s->nheavy;
   r.meta = s->sell_meta;
   r.scol = s->sell_col;
   r.sval = s->sell_val;
@@ -483,7 +487,7 @@ scg_status host_allreduce(scg_ctx *c, std::vector<double> &v) {
 void free_shard(Shard *s) {
   void *ptrs[] = {s->rp, s->col, s->val, s->wts, s->ldiag, s->cdiag, s->d, s->z, s->y, s->a, s->v, s->G,
                   s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
-                  s->sc, s->slots, s->dlog, s->longrows, s->sell_col, s->sell_meta, s->sell_val,
+                  s->sc, s->slots, s->dlog, s->longrows, s->heavyrows, s->sell_col, s->sell_meta, s->sell_val,
                   s->mask, s->mb, s->peerG, s->peerMB, s->orig, s->V, s->ckr, s->work, s->gflag, s->ell_col,
                   s->ell_val, s->gB};
   for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
@@ -701,7 +705,13 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   std::stable_sort(h_long.begin(), h_long.end(), [&](int x, int y) {
     return h_rp[(size_t)x + 1] - h_rp[(size_t)x] > h_rp[(size_t)y + 1] - h_rp[(size_t)y];
   });
+  // rows of more than kHeavyRow entries get a block each (256 strided chains, reading R27)
+  size_t nh = 0;  // (h_long is sorted longest first)
+  while (nh < h_long.size() && h_rp[(size_t)h_long[nh] + 1] - h_rp[(size_t)h_long[nh]] > kHeavyRow) ++nh;
+  std::vector<int> h_heavy(h_long.begin(), h_long.begin() + (long)nh);
+  h_long.erase(h_long.begin(), h_long.begin() + (long)nh);
   s->nlong = (int)h_long.size();
+  s->nheavy = (int)h_heavy.size();
 
   auto alloc = [&](void **p, size_t bytes) -> bool { return cudaMalloc(p, bytes ? bytes : 8) == cudaSuccess; };
   s->nlpad = (nl + 4 + kWin - 1) / kWin * kWin;  // >= 16 bytes of slack for the bulk copies
@@ -716,6 +726,7 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
             alloc((void **)&s->dscalar, sizeof(double) * 8) &&
             alloc((void **)&s->dlog, sizeof(scg_iter_rec) * c->log_cap) &&
             alloc((void **)&s->longrows, sizeof(int) * h_long.size()) &&
+            alloc((void **)&s->heavyrows, sizeof(int) * h_heavy.size()) &&
             alloc((void **)&s->mb, sizeof(Mailbox)) && alloc((void **)&s->peerG, sizeof(double *) * kMaxRanks) &&
             alloc((void **)&s->orig, sizeof(int) * (size_t)nl) && alloc((void **)&s->work, sizeof(unsigned)) &&
             alloc((void **)&s->peerMB, sizeof(Mailbox *) * kMaxRanks) &&
@@ -755,6 +766,8 @@ scg_status build_shard(scg_ctx *c, Shard *s, const int64_t *rp, const int32_t *c
   CK(cudaMemcpyAsync(s->ldiag, h_diag.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, st));
   if (!h_long.empty())
     CK(cudaMemcpyAsync(s->longrows, h_long.data(), sizeof(int) * h_long.size(), cudaMemcpyHostToDevice, st));
+  if (!h_heavy.empty())
+    CK(cudaMemcpyAsync(s->heavyrows, h_heavy.data(), sizeof(int) * h_heavy.size(), cudaMemcpyHostToDevice, st));
   if (c->world > 1) CK(cudaMemcpyAsync(s->mask, h_mask.data(), (size_t)nl, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(s->orig, s->origloc.data(), sizeof(int) * (size_t)nl, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(s->sc, 0, sizeof(DevScalars), st));
@@ -875,7 +888,7 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
     for (int w : kEllWidths)
       if (W == 0 && w >= maxlen) W = w;
     const int64_t nsl32 = (nl + 31) / 32;
-    if (!(c->flags & SCG_NO_ELL) && s->nlong == 0 && W > 0 && (double)W * (double)nl <= 2.0 * (double)cnt_off + 64.0) {
+    if (!(c->flags & SCG_NO_ELL) && s->nlong == 0 && s->nheavy == 0 && W > 0 && (double)W * (double)nl <= 2.0 * (double)cnt_off + 64.0) {
       const size_t ne = (size_t)nsl32 * 32 * W;
       hvec<int> ecol(ne);
       hvec<double> eval;
@@ -916,7 +929,7 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_lanczos_a<false, 0>, kBlock, 0);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_monitor<false, 0>, kBlock, 0);
     }
-    const int need = (int)std::max<int64_t>((s->nslice + 7) / 8, (s->nlong + 7) / 8);
+    const int need = (int)std::max<int64_t>(std::max<int64_t>((s->nslice + 7) / 8, (s->nlong + 7) / 8), s->nheavy);
     s->grid_spmv = std::max(1, std::min(need, std::max(1, oa) * c->nsm));
     const int needA = (int)std::max<int64_t>((s->nslice + kBlockA / 32 - 1) / (kBlockA / 32), 1);
     s->grid_a = std::max(1, std::min(needA, std::max(1, oa) * c->nsm));
@@ -939,7 +952,7 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
   }
   // dynamic slice distribution for skewed graphs (long rows present): warps that carry hub
   // rows take fewer slices.  Off for graphs without long rows (static ranges keep L1 locality).
-  s->dyn = s->nlong > 0;
+  s->dyn = s->nlong + s->nheavy > 0;
   // warp-specialized TMA k_lanczos_a (uniform weights, static slice ranges; SCG_WS_SPMV)
   s->ws = s->sell_uniform && !s->dyn && (c->flags & SCG_WS_SPMV);
   if (s->ws) {

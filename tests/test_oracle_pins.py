@@ -128,6 +128,43 @@ def test_apply_long_row_order_differs_from_single_chain():
     assert y[0] != acc
 
 
+def test_apply_heavy_rows_integer_exact_and_bounded():
+    # Rows of > 1024 entries take 256 strided partial chains (SURVEY CAC-2's W = 256 bin, reading
+    # R27): exact on small integers, within the summation rounding bound on real data, and a
+    # different rounding from the 32-chain order on cancelling data (so the bin boundary is pinned).
+    rng = np.random.default_rng(8)
+    n = 3000
+    hub = rng.integers(-5, 6, size=n - 1).astype(float)
+    hub[hub == 0] = 1.0
+    i = np.zeros(n - 1, dtype=np.int64)
+    j = np.arange(1, n)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    rp[1] = n - 1
+    rp[2:] = n - 1 + np.arange(1, n)
+    col = np.concatenate([j, np.zeros(n - 1, dtype=np.int64)]).astype(np.int32)
+    m = np.concatenate([hub, hub])
+    d = rng.integers(-9, 10, size=n).astype(float)
+    x = rng.integers(-7, 8, size=n).astype(float)
+    y = oracle.apply(n, rp, col, m, d, x)
+    assert y[0] == d[0] * x[0] + float(np.dot(hub, x[1:]))
+    hr = rng.standard_normal(n - 1) * np.exp(rng.uniform(-15, 15, n - 1))
+    xr = rng.standard_normal(n)
+    mr = np.concatenate([hr, hr])
+    y = oracle.apply(n, rp, col, mr, d, xr)
+    exact = Fraction(d[0]) * Fraction(xr[0]) + sum(Fraction(a) * Fraction(b) for a, b in zip(hr, xr[1:]))
+    bound = n * 2.0 ** -53 * (abs(d[0] * xr[0]) + float(np.sum(np.abs(hr * xr[1:])))) * 1.01
+    assert abs(float(Fraction(y[0]) - exact)) <= bound
+    L32 = [0.0] * 32  # the W = 32 order the row would take below the bin boundary
+    for k in range(n - 1):
+        L32[k % 32] = _fma(hr[k], xr[1 + k], L32[k % 32])
+    off = 16
+    while off >= 1:
+        for l in range(off):
+            L32[l] = L32[l] + L32[l + off]
+        off //= 2
+    assert y[0] != d[0] * xr[0] + L32[0]
+
+
 # ------------------------------------------------------------- Laplacian
 def test_laplacian_identities():
     L = si.laplacian("c0")
