@@ -25,7 +25,9 @@ c = si.CONFIGS[cfg]
 W, K = 3, int(os.environ.get("STEPS", "60"))
 res = {}
 for P in [int(a) for a in sys.argv[1:]] or [1, 2, 4]:
-    s = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], profile=True, shards=P)
+    # the start vector drawn inside k_dual_sketch at every P (the side-stream draw of one GPU overlaps
+    # other kernels, which a sum of per-kernel times cannot represent)
+    s = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], profile=True, shards=P, side_rng=False)
     s.step(W)
     s.synchronize()
     s.reset_stats()
