@@ -72,7 +72,8 @@ enum {
                                    uses the tracked trace tau instead of alpha (reading R29) */
   SCG_INEQ = 1u << 4,           /* general template with K = {u <= b}: diag X <= 1
                                    instead of diag X = 1; b is replaced by the slack w = min(z + y/beta, b) in D_t
-                                   and in the dual update (reading R32); the gap / bound records are NaN */
+                                   and in the dual update (reading R32); the gap / bound records are the
+                                   general-template ones (reading R33) */
   SCG_PROFILE = 1u << 8,        /* record CUDA events around every 16th launch of each kernel class (bench /
                                    kernel stats) */
   /* execution options: none changes a single bit of the results (every variant is checked bitwise
@@ -166,7 +167,8 @@ typedef struct {
   double gamma;       /* dual step gamma_t (eqn:sketchy-cgal-dual-step) */
   double tau;         /* trace tracker tau */
   double gap;         /* surrogate duality gap g_t(X_t) with lambda_min(D_t) ~ xi_t (eqn:cgal-gap,
-                         PAPER.md:1550-1555), scaled units, state before the update of iteration t */
+                         PAPER.md:1550-1555), scaled units, state before the update of iteration t;
+                         box sets K: b replaced by the slack w_t (reading R33) */
   double bound;       /* posterior suboptimality bound of X_t, = the stopping numerator
                          p_t + <y_t, b> + beta_t/2 <z_t - b, z_t + b> - alpha xi_t
                          (PAPER.md:1557-1562, 4044-4048), scaled units */
@@ -231,7 +233,8 @@ scg_status sketchycgal_maxcut_alpha_doubling(scg_ctx **out, const scg_csr *L, in
  * hi = 1 + delta; lo = -INFINITY, hi = 1 is SCG_INEQ).  Original units (the MaxCut b is 1).
  * Call after init and before the first step (recomputes D_1's diagonal); SCG_EINVAL
  * otherwise, for NaN bounds, lo > hi or hi = -inf.  Reading R32: slack
- * w = min(max(z + y / beta, lo), hi); the gap / bound records are NaN. */
+ * w = min(max(z + y / beta, lo), hi); the gap / bound records use w in place of b (reading R33):
+ * gap = p + <y,z> + beta <z-w,z> - alpha xi, bound = p + <y,w> + beta/2 <z-w,z+w> - alpha xi. */
 scg_status sketchycgal_set_box(scg_ctx *c, double lo, double hi);
 
 /* Fixed Lanczos bound: every later iteration runs Alg. 2 with q instead of the schedule

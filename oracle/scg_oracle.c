@@ -620,6 +620,26 @@ int oracle_step(void *h, int64_t T) {
     const double S_yz = o_dot(o->y, o->z, n, &gerr);
     const double S_zz = o_dot(o->z, o->z, n, &gerr);
     const double S_z = o_dot(o->z, o->ones, n, &gerr);
+    /* General template (A X in K): the same two quantities with the slack w_t = proj_K(z_t + y_t /
+     * beta_t) in place of b (reading R33): f_t(X) = <C, X> + min_{w in K} <y, A X - w> +
+     * beta/2 ||A X - w||^2 is convex with gradient D_t and f_t(X_star) <= p_star, so the derivation of
+     * P:3100-3140 gives
+     *   gap   = p_t + <y_t, z_t> + beta_t <z_t - w_t, z_t> - alpha xi_t
+     *   bound = p_t + <y_t, w_t> + beta_t/2 <z_t - w_t, z_t + w_t> - alpha xi_t
+     * (w_t = b gives the equality formulas above) */
+    double S_ez = 0.0, S_yw = 0.0, S_ezw = 0.0;
+    if (o->ineq) {
+      double *e = o->a, *w = o->cv, *zw = o->w1; /* free until the Lanczos call below */
+#pragma omp parallel for schedule(static) if (n > 65536)
+      for (int64_t r = 0; r < n; ++r) {
+        w[r] = fmin(fmax(o->z[r] + o->y[r] / beta, o->lo), o->hi);
+        e[r] = o->z[r] - w[r];
+        zw[r] = o->z[r] + w[r];
+      }
+      S_ez = o_dot(e, o->z, n, &gerr);
+      S_yw = o_dot(o->y, w, n, &gerr);
+      S_ezw = o_dot(e, zw, n, &gerr);
+    }
     const double p_t = o->p;
     o->err |= gerr;
     /* line 6: D = C + A*(y + beta (z - b)) ; diagonal of D (primitive 2).
@@ -688,10 +708,14 @@ int oracle_step(void *h, int64_t T) {
       L[5] = cval; L[6] = o->p; L[7] = sqrt(nz); L[8] = gamma; L[9] = o->tau;
       /* min over the set of <D, H>: alpha xi (tr X = alpha) or alpha min(xi, 0) (tr X <= alpha) */
       const double ax = o->alpha * ((o->trace_le && xi > 0.0) ? 0.0 : xi);
-      L[10] = ((p_t + S_yz) + beta * (S_zz - o->bval * S_z)) - ax;
       const double nbb = ((double)n * o->bval) * o->bval;
-      L[11] = ((p_t + o->bval * S_y) + (0.5 * beta) * (S_zz - nbb)) - ax;
-      if (o->ineq) L[10] = L[11] = NAN; /* the gap / bound formulas are for A X = b (reading R32) */
+      if (o->ineq) { /* general template (reading R33) */
+        L[10] = ((p_t + S_yz) + beta * S_ez) - ax;
+        L[11] = ((p_t + S_yw) + (0.5 * beta) * S_ezw) - ax;
+      } else {
+        L[10] = ((p_t + S_yz) + beta * (S_zz - o->bval * S_z)) - ax;
+        L[11] = ((p_t + o->bval * S_y) + (0.5 * beta) * (S_zz - nbb)) - ax;
+      }
     }
     if (o->vhist && t - 1 < o->vhist_cap) memcpy(o->vhist + (t - 1) * n, o->v, sizeof(double) * (size_t)n);
     o_res_free(&res);

@@ -143,7 +143,7 @@ __device__ __forceinline__ void gstore(const Net &net, double *dst, int r, doubl
   }
 }
 
-enum FinKind { FK_FROB = 0, FK_RHO0, FK_OM, FK_RHO, FK_NUX, FK_MON, FK_NZ, FK_BAR, FK_RHO0M, FK_GEN, FK_RHO0S };
+enum FinKind { FK_FROB = 0, FK_RHO0, FK_OM, FK_RHO, FK_NUX, FK_MON, FK_NZ, FK_BAR, FK_RHO0M, FK_GEN, FK_RHO0S, FK_MY4 };
 
 struct FinArgs {
   int i;                 // Lanczos step (FK_OM, FK_RHO, FK_BAR)
@@ -952,6 +952,9 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
         for (int j = 0; j < 4; ++j) sc->my[j] = xacc_round(L[1 + j]);
       break;
     case FK_GEN: sc->g2n[f.i & 1] = xacc_round(L[0]); break;  // start vector of iteration f.i, drawn ahead
+    case FK_MY4:  // gap / bound sums over the initial state (box sets, k_init_box)
+      for (int j = 0; j < 4; ++j) sc->my[j] = xacc_round(L[j]);
+      break;
     case FK_RHO0S:  // k_dual_sketch without the draw: the next start vector's norm comes from FK_GEN
       sc->rho[0] = sqrt(sc->g2n[f.i & 1]);
       sc->brk = 0;
@@ -979,14 +982,23 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
         const double beta = A.beta0 * A.sq;
         // min over the constraint set of <D_t, H>: alpha xi_t (tr X = alpha), alpha min(xi_t, 0) (tr X <= alpha)
         const double pt = sc->p, ax = A.alpha * ((A.trace_le && sc->xi > 0.0) ? 0.0 : sc->xi);
-        const double zmb_z = sc->my[2] - A.b * sc->my[3];
-        double g = pt + sc->my[1];
-        g = g + beta * zmb_z;
-        gapv = g - ax;
-        const double zpb = sc->my[2] - A.nbb;
-        double u = pt + A.b * sc->my[0];
-        u = u + (0.5 * beta) * zpb;
-        boundv = u - ax;
+        if (A.ineq) {  // general template (reading R33): my = (<y,z>, <z-w,z>, <y,w>, <z-w,z+w>)
+          double g = pt + sc->my[0];
+          g = g + beta * sc->my[1];
+          gapv = g - ax;
+          double u = pt + sc->my[2];
+          u = u + (0.5 * beta) * sc->my[3];
+          boundv = u - ax;
+        } else {       // my = (sum y, <y,z>, <z,z>, sum z)
+          const double zmb_z = sc->my[2] - A.b * sc->my[3];
+          double g = pt + sc->my[1];
+          g = g + beta * zmb_z;
+          gapv = g - ax;
+          const double zpb = sc->my[2] - A.nbb;
+          double u = pt + A.b * sc->my[0];
+          u = u + (0.5 * beta) * zpb;
+          boundv = u - ax;
+        }
       }
       sc->nz = nz;
       sc->gamma = gamma_rule(A, nz);
@@ -1009,8 +1021,8 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
       rec.znorm = sqrt(nz);
       rec.gamma = sc->gamma;
       rec.tau = sc->tau;
-      rec.gap = A.ineq ? NAN : gapv;  // the gap / bound formulas are for A X = b (reading R32)
-      rec.bound = A.ineq ? NAN : boundv;
+      rec.gap = gapv;
+      rec.bound = boundv;
       if (f.log) f.log[A.t - 1] = rec;
       break;
     }
@@ -1177,6 +1189,32 @@ __global__ void k_init_d(const double *__restrict__ z, const double *__restrict_
     const double w = ineq ? fmin(fmax(z[r] + y[r] / beta, lo), hi) : b;  // slack w_1 = proj_K(z + y / beta)
     d[r] = fma(beta, z[r] - w, y[r]) + cdiag[r];
   }
+}
+
+// Box sets (sketchycgal_set_box, before the first step): d for t = 1 with w_1 = proj_K(z_1 + y_1 / beta_1)
+// and the general-template gap / bound sums over the initial state (reading R33).
+__global__ void k_init_box(const double *__restrict__ z, const double *__restrict__ y, const double *__restrict__ cdiag,
+                           double *__restrict__ d, int nl, double beta, double lo, double hi, XSlot *slot,
+                           DevScalars *sc, Net net) {
+  pdl_entry();
+  __shared__ XBlk<4> xb;
+  xblk_init<4>(xb);
+  XWin acc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) xwin_init(acc[q]);
+  int err = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double zr = z[r], yr = y[r];
+    const double w = fmin(fmax(zr + yr / beta, lo), hi);  // slack w_1 = proj_K(z_1 + y_1 / beta_1)
+    const double e = zr - w;
+    d[r] = fma(beta, e, yr) + cdiag[r];
+    xwin_add(acc[0], yr * zr, err, xb.l[0]);
+    xwin_add(acc[1], e * zr, err, xb.l[1]);
+    xwin_add(acc[2], yr * w, err, xb.l[2]);
+    xwin_add(acc[3], e * (zr + w), err, xb.l[3]);
+  }
+  if (commit_and_ticket<4>(acc, xb, slot, err, sc, net.P, 0u) && threadIdx.x == 0)
+    emit<4>(slot, sc, net, FK_MY4, FinArgs{}, nullptr);
 }
 
 // Lanczos start vector g = randn (Alg. 2 line 1) for iteration t and ||g||^2 (exact).
@@ -2280,10 +2318,18 @@ __global__ void __launch_bounds__(kBlock, GEN ? 2 : 4) k_dual_sketch(const doubl
           peer |= mk[u];
           xwin_add_nn(acc[0], gv * gv, err, xb.l[0]);
         }
-        xwin_add(acc[o + 0], yr, err, xb.l[o + 0]);
-        xwin_add(acc[o + 1], yr * zr[u], err, xb.l[o + 1]);
-        xwin_add_nn(acc[o + 2], zr[u] * zr[u], err, xb.l[o + 2]);
-        xwin_add_nn(acc[o + 3], zr[u], err, xb.l[o + 3]);  // z >= 0 (convex combination of alpha v o v)
+        if (BOX) {  // general template (reading R33): <y,z>, <z-w,z>, <y,w>, <z-w,z+w> with w = w_{t+1}
+          const double wk = fmin(fmax(zr[u] + yr / A.beta_next, A.lo), A.hi);  // (the w of e1 above)
+          xwin_add(acc[o + 0], yr * zr[u], err, xb.l[o + 0]);
+          xwin_add(acc[o + 1], e1 * zr[u], err, xb.l[o + 1]);
+          xwin_add(acc[o + 2], yr * wk, err, xb.l[o + 2]);
+          xwin_add(acc[o + 3], e1 * (zr[u] + wk), err, xb.l[o + 3]);
+        } else {
+          xwin_add(acc[o + 0], yr, err, xb.l[o + 0]);
+          xwin_add(acc[o + 1], yr * zr[u], err, xb.l[o + 1]);
+          xwin_add_nn(acc[o + 2], zr[u] * zr[u], err, xb.l[o + 2]);
+          xwin_add_nn(acc[o + 3], zr[u], err, xb.l[o + 3]);  // z >= 0 (convex combination of alpha v o v)
+        }
       }
     }
   }

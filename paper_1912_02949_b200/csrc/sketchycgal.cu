@@ -2109,9 +2109,14 @@ scg_status sketchycgal_set_box(scg_ctx *c, double lo, double hi) {
   c->klo = scale ? lo / (double)c->n : lo;  // scaled units like b = 1/n
   c->khi = scale ? hi / (double)c->n : hi;
   const double beta1 = c->beta0 * std::sqrt(2.0);
-  for (Shard *s : c->sh)  // D_1's diagonal with the slack w_1 = proj_K(z_1 + y_1 / beta_1)
-    launch(c, KC_OTHER, 0.0, k_init_d, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z, (const double *)s->y,
-           (const double *)s->cdiag, s->d, (int)s->nl, c->b, beta1, 1, c->klo, c->khi);
+  // D_1's diagonal with the slack w_1 = proj_K(z_1 + y_1 / beta_1), and the general-template gap /
+  // bound sums over the initial state (reading R33)
+  const unsigned long long E = ++c->epoch;
+  for (Shard *s : c->sh)
+    launch(c, KC_OTHER, 0.0, k_init_box, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z, (const double *)s->y,
+           (const double *)s->cdiag, s->d, (int)s->nl, beta1, c->klo, c->khi, s->slots + SLOT_INIT, s->sc,
+           net_of(c, s, E));
+  pull_all(c, FK_MY4, 4, E, FinArgs{});
   return sketchycgal_synchronize(c);
 }
 

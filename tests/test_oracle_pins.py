@@ -596,14 +596,16 @@ def test_inequality_template_closed_forms():
     diag X <= 1.  On C5 the optimum still has diag X = 1 (L is psd), so the closed-form SDP value
     is recovered; with tr X <= n/2 as well, the equality problem is infeasible while the
     inequality one has the vertex-transitive optimum (1/2) X*, value SDP/2, and a feasible
-    iterate (z <= b).  The gap / bound records (equality-only formulas) are NaN."""
+    iterate (z <= b).  The gap / bound records are the general-template ones (reading R33): finite,
+    and the gap shrinks toward 0."""
     n = 5
     L = _edges_graph(n, [(k, (k + 1) % n) for k in range(n)])
     sdp = 2 * n * (1 + math.cos(math.pi / n))
     o = oracle.Oracle(L, 3, seed=5, logcap=3000, ineq=True)
     o.step(3000)
     assert abs(o.implicit_objective() - sdp) <= 3e-3 * sdp
-    assert np.all(np.isnan(o.log[:, 10:12]))
+    assert np.all(np.isfinite(o.log[:, 10:12]))
+    assert abs(o.log[-1, 10]) < 0.05 * abs(o.log[4, 10])
     h = oracle.Oracle(L, 3, seed=5, logcap=3000, ineq=True, trace_le=True, alpha=n / 2)
     h.step(3000)
     assert abs(h.implicit_objective() - sdp / 2) <= 3e-3 * sdp
@@ -614,8 +616,8 @@ def test_inequality_template_closed_forms():
 def test_box_constraint_set_closed_forms():
     """Box K = {lo <= u <= hi} (the l_inf ball |u - 1| <= delta of P:3915-3918): on C5 with
     diag X in [1 - delta, 1 + delta] and tr X <= 1.05 n (1 + delta) the optimum is (1 + delta) X*,
-    value (1 + delta) SDP.  Special cases: lo = hi = 1 is the equality problem (every record but
-    the NaN gap / bound bitwise), lo = -inf, hi = 1 is SCG_INEQ (bitwise)."""
+    value (1 + delta) SDP.  Special cases: lo = hi = 1 is the equality problem (every iterate bitwise,
+    the general-template gap / bound equal to rounding), lo = -inf, hi = 1 is SCG_INEQ (bitwise)."""
     n = 5
     L = _edges_graph(n, [(k, (k + 1) % n) for k in range(n)])
     sdp = 2 * n * (1 + math.cos(math.pi / n))
@@ -631,7 +633,8 @@ def test_box_constraint_set_closed_forms():
     b.step(300)
     np.testing.assert_array_equal(b.log[:, :10], e.log[:, :10])
     np.testing.assert_array_equal(b.z, e.z)
-    assert np.all(np.isnan(b.log[:, 10:12]))
+    # the general-template gap / bound (reading R33) with w = b are the equality ones, up to rounding
+    np.testing.assert_allclose(b.log[:, 10:12], e.log[:, 10:12], rtol=1e-11, atol=1e-14)
     i1 = oracle.Oracle(L, 3, seed=5, logcap=300, box=(-np.inf, 1.0))
     i1.step(300)
     i2 = oracle.Oracle(L, 3, seed=5, logcap=300, ineq=True)
@@ -784,3 +787,36 @@ def test_golden_fixture_reproduces_from_oracle():
     for k in ("log", "sha256", "S_rows", "S_sample", "S_absmax", "p", "tau", "R", "T", "qfix"):
         assert fresh[k] == stored[k], k
     assert max(int(float.fromhex(r[2])) for r in stored["log"]) > 127  # k beyond the old cap
+
+
+def test_general_template_bound_dominates_suboptimality():
+    """General template (reading R33): f_t(X) = <C,X> + min_{w in K} <y, AX - w> + beta/2 ||AX - w||^2
+    is convex with gradient D_t = C + A*(y + beta (AX - w_t)), w_t = proj_K(AX + y/beta), and
+    f_t(X_star) <= p_star, so the derivation of P:3100-3140 gives the bound
+    p_t + <y_t, w_t> + beta_t/2 <z_t - w_t, z_t + w_t> - alpha min(lambda_min(D_t), 0) >= p_t - p_star
+    (trace-bounded set).  Pin on C5 with the box diag X in [1 - delta, 1 + delta], whose optimum is
+    (1 + delta) SDP (closed form, test_box_constraint_set_closed_forms); the logged bound (xi_t) is
+    <= the exact one, and gap - bound = <y, z - w> + beta/2 ||z - w||^2."""
+    n = 5
+    L = _edges_graph(n, [(k, (k + 1) % n) for k in range(n)])
+    sdp = 2 * n * (1 + math.cos(math.pi / n))
+    d = 0.2
+    alpha = 1.05 * n * (1 + d)
+    o = oracle.Oracle(L, 3, seed=5, logcap=700, box=(1 - d, 1 + d), trace_le=True, alpha=alpha)
+    Ld = L.dense()
+    for t in (5, 50, 600):
+        o.step(t - o.t)
+        y, z, p, a_s = o.y.copy(), o.z.copy(), o.p, o.alpha
+        lo, hi = (1 - d) / n, (1 + d) / n
+        p_star = -(1 + d) * sdp / (n * o.nrmL)
+        beta = math.sqrt(t + 2)
+        w = np.minimum(np.maximum(z + y / beta, lo), hi)
+        D = -Ld / o.nrmL + np.diag(y + beta * (z - w))
+        lam = float(np.linalg.eigvalsh(D)[0])
+        bound_exact = p + float(np.dot(y, w)) + 0.5 * beta * float(np.dot(z - w, z + w)) - a_s * min(lam, 0.0)
+        assert p - p_star <= bound_exact + 1e-12, (t, p - p_star, bound_exact)
+        o.step(1)
+        rec = o.log[t]
+        assert rec[11] <= bound_exact + 1e-12
+        ident = float(np.dot(y, z - w)) + 0.5 * beta * float(np.dot(z - w, z - w))
+        assert abs((rec[10] - rec[11]) - ident) <= 1e-12 * max(1.0, abs(rec[10]))
