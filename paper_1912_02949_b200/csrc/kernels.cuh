@@ -178,7 +178,7 @@ constexpr int kMinBlocksUni = 3;  // min blocks per SM of the uniform-weight SEL
 // min blocks per SM of the ELL SpMV kernels: 64-register cap up to W = 4, wider rows need more stage registers
 // (a deeper pipeline -- gathers two slices ahead, 78 registers, 3 blocks/SM -- measured 171 us against
 // 140 us on configs[3]: the fourth block per SM is worth more than the extra slack)
-constexpr int ell_min_blocks(int W, bool uni) { return W > 100 ? 2 : (W <= 4 ? 4 : (uni ? 3 : 2)); }
+constexpr int ell_min_blocks(int W, bool uni) { return W <= 4 ? 4 : (uni ? 3 : 2); }
 constexpr int kLongRow = 32;
 constexpr int kHeavyRow = 1024;  // rows with more entries are "heavy": a block each (256 strided chains)
 
@@ -204,10 +204,6 @@ struct Rows {
   const int *ecol;      // column | 0x80000000 for a negative uniform value
   const double *eval;   // per-slot values, or nullptr when all |C_rj| equal m0
   int padc;             // the padding code
-  // ELL2-W (one GPU): the same slots in 64-row slices, lane l owning rows 2l and 2l+1 -- slot j of
-  // slice s at e2col[(64 s) W + 64 j + 2 l + (0 | 1)]
-  const int *e2col;
-  const double *e2val;
 };
 constexpr int kEllMax = 8;  // widest ELL layout (rows of at most 8 off-diagonal entries)
 constexpr int kDynCh = 8;
@@ -698,140 +694,12 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
   }
 }
 
-// ---------------------------------------------------------------- ELL2-W engine (two rows per lane)
-// spmv_ell with 64-row slices, lane l owning rows 2l and 2l+1 (one GPU: the row base is 0, so the
-// own entries are 16-byte aligned): a slot's two column codes are one 8-byte load, the own entries,
-// the diagonal and the outputs 16-byte accesses, and the per-slice overhead (addresses, predicates,
-// loop control, pipeline moves) is shared by 64 rows.  Same stages as spmv_ell: gathers of slice
-// i+1, own entries of slice i+2 and columns of slice i+3 in flight while slice i is computed.  The
-// rows are visited in the same chains (per row, CAC-3), so the bits are those of spmv_ell.
-template <int NC, bool UNI, int W, class Epi>
-__device__ __forceinline__ void spmv_ell2(const Rows &RL, const double *__restrict__ X, double den,
-                                          const double *__restrict__ diag0, const double *__restrict__ diag1,
-                                          int nl, Epi &epi) {
-  const int lane = threadIdx.x & 31;
-  const double rden = 1.0 / den;
-  const int nsl = (nl + 63) >> 6;
-  const int per = (nsl + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int s_end = min(nsl, ((int)blockIdx.x + 1) * per);
-  const int wstep = blockDim.x >> 5;
-  int sl = (int)blockIdx.x * per + (threadIdx.x >> 5);
-  const int2 *__restrict__ ec = reinterpret_cast<const int2 *>(RL.e2col) + lane;
-  const double2 *__restrict__ ev = reinterpret_cast<const double2 *>(RL.e2val) + lane;
-  const int padc = RL.padc;
-  const double m0 = RL.m0;
-  auto cload = [&](int q, int2 (&c)[W]) {
-    if (q < s_end) {
-      const int2 *cp = ec + (long long)q * (32 * W);
-#pragma unroll
-      for (int u = 0; u < W; ++u) c[u] = __ldg(cp + 32 * u);
-    } else {
-#pragma unroll
-      for (int u = 0; u < W; ++u) c[u] = make_int2(padc, padc);
-    }
-  };
-  auto gload = [&](int q, const int2 (&c)[W], double (&g)[2 * W], double (&v)[2 * W]) -> unsigned {
-    unsigned sg = 0u;
-#pragma unroll
-    for (int u = 0; u < W; ++u) {
-      g[2 * u] = __ldg(gaddr(X, c[u].x));
-      g[2 * u + 1] = __ldg(gaddr(X, c[u].y));
-      if (UNI) sg |= (((unsigned)c[u].x >> 31) << (2 * u)) | (((unsigned)c[u].y >> 31) << (2 * u + 1));
-    }
-    if (!UNI) {
-      const double2 *vp = ev + (long long)q * (32 * W);
-#pragma unroll
-      for (int u = 0; u < W; ++u) {
-        const double2 t = q < s_end ? __ldg(vp + 32 * u) : make_double2(-0.0, -0.0);
-        v[2 * u] = t.x;
-        v[2 * u + 1] = t.y;
-      }
-    }
-    return sg;
-  };
-  auto oload = [&](int q, double2 &xo, double2 &dd0, double2 &dd1) {
-    const int p = q * 64 + 2 * lane;
-    xo = make_double2(0.0, 0.0);
-    dd0 = xo;
-    dd1 = xo;
-    if (q < s_end && p < nl) {
-      if (p + 1 < nl) {
-        xo = *reinterpret_cast<const double2 *>(X + p);
-        dd0 = *reinterpret_cast<const double2 *>(diag0 + p);
-        if (NC > 1) dd1 = *reinterpret_cast<const double2 *>(diag1 + p);
-      } else {
-        xo.x = X[p];
-        dd0.x = diag0[p];
-        if (NC > 1) dd1.x = diag1[p];
-      }
-    }
-  };
-  int2 cb[W], cc[W];
-  double g0[2 * W], v0[2 * W];
-  double2 xo0, d00, d10, xo1, d01, d11;
-  unsigned s0;
-  {
-    int2 ca[W];
-    cload(sl, ca);
-    oload(sl, xo0, d00, d10);
-    s0 = gload(sl, ca, g0, v0);
-  }
-  cload(sl + wstep, cb);
-  oload(sl + wstep, xo1, d01, d11);
-  cload(sl + 2 * wstep, cc);
-  for (; sl < s_end; sl += wstep) {
-    double g1[2 * W], v1[2 * W];
-    const unsigned s1 = gload(sl + wstep, cb, g1, v1);  // gathers of slice i+1
-    int2 cd[W];
-    cload(sl + 3 * wstep, cd);                         // columns of slice i+3
-    double2 xo2, d02, d12;
-    oload(sl + 2 * wstep, xo2, d02, d12);              // own entries of slice i+2
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {  // rows 2 lane + h of slice i
-      const int p = sl * 64 + 2 * lane + h;
-      RowOut<NC> o;
-      o.r = p;
-      o.xr = (h ? xo0.y : xo0.x) * rden;  // v = w * fl(1/rho) (Alg. 2 line 9, reading R26)
-      o.s[0] = (h ? d00.y : d00.x) * o.xr;
-      if (NC > 1) o.s[NC - 1] = (h ? d10.y : d10.x) * o.xr;
-#pragma unroll
-      for (int u = 0; u < W; ++u) {
-        const int k = 2 * u + h;
-        double x = g0[k] * rden;
-        if (UNI) {
-          x = __hiloint2double(__double2hiint(x) ^ (int)(((s0 >> k) & 1u) << 31), __double2loint(x));
-#pragma unroll
-          for (int t = 0; t < NC; ++t) o.s[t] = fma(m0, x, o.s[t]);
-        } else {
-#pragma unroll
-          for (int t = 0; t < NC; ++t) o.s[t] = fma(v0[k], x, o.s[t]);
-        }
-      }
-      if (p < nl) epi(o);
-    }
-#pragma unroll
-    for (int u = 0; u < W; ++u) {
-      cb[u] = cc[u];
-      cc[u] = cd[u];
-    }
-#pragma unroll
-    for (int k = 0; k < 2 * W; ++k) {
-      g0[k] = g1[k];
-      if (!UNI) v0[k] = v1[k];
-    }
-    s0 = s1;
-    xo0 = xo1; d00 = d01; d10 = d11;
-    xo1 = xo2; d01 = d02; d11 = d12;
-  }
-}
-
 // SpMV dispatch: ELL-W when the layout has one (W > 0), else SELL + long rows.
 template <int NC, bool UNI, int W, class Epi>
 __device__ __forceinline__ void spmv_any(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
                                          const double *__restrict__ diag0, const double *__restrict__ diag1,
                                          long long rb, int nl, Epi &epi) {
-  if constexpr (W > 100) spmv_ell2<NC, UNI, W - 100>(RL, X, den, diag0, diag1, nl, epi);  // (rb == 0)
-  else if constexpr (W > 0) spmv_ell<NC, UNI, W>(RL, X, den, diag0, diag1, rb, nl, epi);
+  if constexpr (W > 0) spmv_ell<NC, UNI, W>(RL, X, den, diag0, diag1, rb, nl, epi);
   else spmv_rows<NC, UNI>(C, RL, X, den, diag0, diag1, rb, nl, epi);
 }
 

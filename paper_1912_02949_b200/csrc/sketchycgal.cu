@@ -109,10 +109,6 @@ struct Shard {
   int *ell_col = nullptr;    // ELL-W layout (rows of <= kEllMax entries), W = ellw; 0: none
   double *ell_val = nullptr;
   int ellw = 0, padc = 0;
-  int *ell2_col = nullptr;   // ELL2 (two rows per lane, one GPU) copy of the ELL layout for k_lanczos_a
-  double *ell2_val = nullptr;
-  bool ell2 = false;
-  int grid_ell2 = 1;
   int grid_ell = 1, grid_ell_mon = 1, grid_ell_c = 1, grid_dual_s = 1;
   bool dyn = false;
   // row relabeling (SELL engine): local row nu holds input row rb + origloc[nu]
@@ -401,11 +397,6 @@ void launch_cluster(scg_ctx *c, int cls, double bytes, Kern kern, int cl, dim3 b
   c->launches++;
 }
 
-// k_lanczos_a for a shard: ELL2 (two rows per lane) when built, else the shard's layout
-using KernA = void (*)(Csr, Rows, const double *, const double *, int, long long, int, double *, XSlot *, DevScalars *,
-                       Net);
-KernA pick_a(const Shard *s);
-
 Rows rows_of(const Shard *s, bool dyn = false) {
   Rows r{};
   r.work = dyn ? s->work : nullptr;
@@ -421,8 +412,6 @@ Rows rows_of(const Shard *s, bool dyn = false) {
   r.ecol = s->ell_col;
   r.eval = s->ell_val;
   r.padc = s->padc;
-  r.e2col = s->ell2_col;
-  r.e2val = s->ell2_val;
   return r;
 }
 
@@ -442,15 +431,6 @@ constexpr int kEllWidths[] = {2, 3, 4, 6, 8};
    : (W) == 6 ? ((U) ? K<true, 6> : K<false, 6>)                   \
    : (W) == 8 ? ((U) ? K<true, 8> : K<false, 8>)                   \
               : ((U) ? K<true, 0> : K<false, 0>))
-
-KernA pick_a(const Shard *s) {
-  if (s->ell2) {
-    if (s->ellw == 3) return s->sell_uniform ? k_lanczos_a<true, 103> : k_lanczos_a<false, 103>;
-    return s->sell_uniform ? k_lanczos_a<true, 104> : k_lanczos_a<false, 104>;
-  }
-  return SCG_PICK(k_lanczos_a, s->sell_uniform, s->ellw);
-}
-
 
 Net net_of(const scg_ctx *c, const Shard *s, unsigned long long E) {
   Net n{};
@@ -509,7 +489,7 @@ void free_shard(Shard *s) {
                   s->S, s->Om, s->gpart, s->U, s->tmp1, s->tmp2, s->dmat, s->partial, s->dlam, s->dscalar,
                   s->sc, s->slots, s->dlog, s->longrows, s->heavyrows, s->sell_col, s->sell_meta, s->sell_val,
                   s->mask, s->mb, s->peerG, s->peerMB, s->orig, s->V, s->ckr, s->work, s->gflag, s->ell_col,
-                  s->ell_val, s->gB, s->ell2_col, s->ell2_val};
+                  s->ell_val, s->gB};
   for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -934,35 +914,6 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
       if (!uni) CK(cudaMemcpyAsync(s->ell_val, eval.data(), sizeof(double) * ne, cudaMemcpyHostToDevice, st));
       CK(cudaStreamSynchronize(st));
       s->ellw = W;
-      // ELL2 copy for k_lanczos_a (one GPU, W <= 4): 64-row slices, lane l owns rows 2l, 2l+1
-      if (c->world == 1 && W <= 4 && W >= 3 && !(c->flags & SCG_NO_ELL2)) {
-        const int64_t nsl64 = (nl + 63) / 64;
-        const size_t n2 = (size_t)nsl64 * 64 * W;
-        hvec<int> e2(n2);
-        hvec<double> v2;
-        if (!uni) v2.resize(n2);
-#pragma omp parallel for schedule(static, 256)
-        for (int64_t q = 0; q < nsl64; ++q)
-          for (int j = 0; j < W; ++j)
-            for (int l = 0; l < 64; ++l) {
-              const int64_t r = q * 64 + l;
-              const size_t slot = (size_t)q * 64 * W + (size_t)j * 64 + l;
-              const int e = r < nl ? h_rp[(size_t)r] + j : -1;
-              if (e >= 0 && e < h_rp[(size_t)r + 1]) {
-                e2[slot] = enc(e);
-                if (!uni) v2[slot] = valof(e);
-              } else {
-                e2[slot] = padc;
-                if (!uni) v2[slot] = -0.0;
-              }
-            }
-        if (!alloc((void **)&s->ell2_col, sizeof(int) * n2) || (!uni && !alloc((void **)&s->ell2_val, sizeof(double) * n2)))
-          return fail(c, SCG_ENOMEM, "ELL2 layout");
-        CK(cudaMemcpyAsync(s->ell2_col, e2.data(), sizeof(int) * n2, cudaMemcpyHostToDevice, st));
-        if (!uni) CK(cudaMemcpyAsync(s->ell2_val, v2.data(), sizeof(double) * n2, cudaMemcpyHostToDevice, st));
-        CK(cudaStreamSynchronize(st));
-        s->ell2 = true;
-      }
     }
     // algorithmic matrix bytes: one column index (+ value unless uniform) per stored entry --
     // independent of the layout's padding and metadata
@@ -995,12 +946,6 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
       s->grid_ell = std::max(1, std::min(needE, std::max(1, oe) * c->nsm));
       s->grid_ell_mon = std::max(1, std::min(needE, std::max(1, oem) * c->nsm));
       s->grid_ell_c = std::max(1, std::min(needE, std::max(1, oec) * c->nsm));
-      if (s->ell2) {
-        int o2 = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pick_a(s), kBlockA, 0);
-        const int need2 = (int)std::max<int64_t>(((nl + 63) / 64 + 7) / 8, 1);
-        s->grid_ell2 = std::max(1, std::min(need2, std::max(1, o2) * c->nsm));
-      }
     }
     dbg_log(c, "[scg] shard %d: nl=%lld long=%d uni=%d ellw=%d occ_a=%d occ_m=%d grid_a=%d grid_ell=%d\n", s->rank,
             (long long)nl, s->nlong, (int)U, s->ellw, oa, om, s->grid_a, s->grid_ell);
@@ -1633,14 +1578,13 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       for (Shard *s : c->sh) {
         Csr C{s->rp, s->col, s->val};
         Rows TT = rows_of(s, s->dyn);
-        auto kA = pick_a(s);
+        auto kA = SCG_PICK(k_lanczos_a, s->sell_uniform, s->ellw);
         if (s->ws)
           launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], k_lanczos_a_ws<true>, dim3(s->grid_ws), dim3(kWsThreads),
                       sizeof(WsSmem), C, TT, (const double *)s->d, (const double *)slot(s, i), (int)s->nl,
                       (long long)s->rb, i, s->a, s->slots + SLOT_OM, s->sc, net_of(c, s, E));
         else
-          launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA,
-                      dim3(s->ell2 ? s->grid_ell2 : (s->ellw ? s->grid_ell : s->grid_a)), dim3(kBlockA), 0, C, TT,
+          launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->ellw ? s->grid_ell : s->grid_a), dim3(kBlockA), 0, C, TT,
                       (const double *)s->d, (const double *)slot(s, i), (int)s->nl, (long long)s->rb, i, s->a,
                       s->slots + SLOT_OM, s->sc, net_of(c, s, E));
       }

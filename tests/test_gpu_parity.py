@@ -140,23 +140,21 @@ def test_launch_policy_forced_bitwise(gpu, cfg, T, pdl):
     _assert_trajectory(g, o, T)
 
 
-@pytest.mark.parametrize("cfg,T,layout", [("c1", 300, "sell"), ("c3", 2, "sell"), ("c4", 1, "sell"),
-                                          ("c1", 300, "ell1"), ("c3", 2, "ell1"), ("c4", 1, "ell1")])
-def test_other_layouts_where_ell_applies_bitwise(gpu, cfg, T, layout):
-    """Graphs whose rows all have <= 8 entries run the ELL-W SpMV by default (two rows per lane in the
-    pass-1 kernel on one GPU); the SELL-32 layout (SCG_NO_ELL) and one row per lane (SCG_NO_ELL2) give
-    the same bitwise trajectory on them (configs[1] through the multi-kernel iteration)."""
+@pytest.mark.parametrize("cfg,T", [("c1", 300), ("c3", 2), ("c4", 1)])
+def test_sell_layout_where_ell_applies_bitwise(gpu, cfg, T):
+    """Graphs whose rows all have <= 8 entries run the ELL-W SpMV by default; the SELL-32 layout
+    (SCG_NO_ELL) gives the same bitwise trajectory on them."""
     L = si.laplacian(cfg)
     c = si.CONFIGS[cfg]
     R = 2 if cfg == "c4" else c["R"]
-    opts = {"ell": False} if layout == "sell" else {"ell2": False}
-    g, o = _run_pair(gpu, L, R, T, seed=c["seed"], resident=False, **opts)
+    g, o = _run_pair(gpu, L, R, T, seed=c["seed"], ell=False)
     _assert_trajectory(g, o, T)
 
 
-@pytest.mark.parametrize("n", [8000, 8001, 8063])
-def test_ell2_ragged_tail_bitwise(gpu, n):
-    """Two rows per lane with row counts that are not a multiple of 64 (the last lane's pair split)."""
+@pytest.mark.parametrize("n", [8000, 8001, 8031])
+def test_ell_ragged_tail_bitwise(gpu, n):
+    """ELL-W with a row count that is not a multiple of the 32-row slice (signed weights, a ring plus
+    chords: every row <= 4 entries), multi-kernel iteration."""
     i = np.arange(n)
     L = si.laplacian_from_edges(n, np.concatenate([i, i]), np.concatenate([(i + 1) % n, (i + 97) % n]),
                                 np.concatenate([np.ones(n), -np.ones(n)]), dedupe=True)
