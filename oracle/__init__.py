@@ -76,6 +76,8 @@ def _load():
         lib.oracle_step.argtypes = [P, I64]
         lib.oracle_set_box.restype = ctypes.c_int
         lib.oracle_set_box.argtypes = [P, ctypes.c_double, ctypes.c_double]
+        lib.oracle_set_ball.restype = ctypes.c_int
+        lib.oracle_set_ball.argtypes = [P, ctypes.c_double]
         lib.oracle_t_done.restype = I64
         lib.oracle_t_done.argtypes = [P]
         lib.oracle_scalar.restype = D
@@ -200,7 +202,7 @@ class Oracle:
 
     def __init__(self, L, R: int, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
                  scale: bool = True, qfix: int = 0, logcap: int = 0, vhist: int = 0, trace_le: bool = False,
-                 ineq: bool = False, box: tuple | None = None, div_norm: bool = False):
+                 ineq: bool = False, box: tuple | None = None, div_norm: bool = False, ball: float | None = None):
         self.L = L
         self.n = L.n
         self.R = int(R)
@@ -216,10 +218,13 @@ class Oracle:
                                         int(qfix), self.logcap, self.vhist_cap,
                                         (1 if trace_le else 0) | (2 if ineq else 0) | (4 if div_norm else 0))
         self.trace_le = bool(trace_le)
-        self.ineq = bool(ineq) or box is not None
+        self.ineq = bool(ineq) or box is not None or ball is not None
         if box is not None:  # K = {lo <= u <= hi}, original units
             if _load().oracle_set_box(self._h, float(box[0]), float(box[1])) != 0:
                 raise ValueError("oracle_set_box: after the first step or lo > hi")
+        if ball is not None:  # K = {||u - 1||_2 <= ball}, original units
+            if _load().oracle_set_ball(self._h, float(ball)) != 0:
+                raise ValueError("oracle_set_ball: after the first step or delta < 0")
         self.beta0 = float(beta0)
 
     def __del__(self):

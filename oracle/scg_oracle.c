@@ -487,6 +487,9 @@ typedef struct {
   int ineq;     /* general template with a box K = {lo <= u <= hi} */
   double lo, hi; /* scaled units; bit 1 of the mode (SCG_INEQ): lo = -inf, hi = b */
   int div_norm; /* bit 2 of the mode: normalizations as printed divisions (R26 pin, see o_lanczos) */
+  int ball;      /* K = {u : ||u - b||_2 <= delta} (norm constraint; reading R34) */
+  double delta;  /* scaled units */
+  double *pw, *pe; /* projection work arrays */
   uint64_t seed;
   int qfix; /* test-only: fixed Lanczos bound (may be n); 0 = schedule */
   int64_t t; /* iterations done */
@@ -560,6 +563,8 @@ void *oracle_create(int64_t n, const int64_t *rp_L, const int32_t *col_L, const 
   o->w3 = (double *)calloc((size_t)n, sizeof(double));
   o->a = (double *)calloc((size_t)n, sizeof(double));
   o->cv = (double *)calloc((size_t)n, sizeof(double));
+  o->pw = (double *)calloc((size_t)n, sizeof(double));
+  o->pe = (double *)calloc((size_t)n, sizeof(double));
   o->S = (double *)calloc((size_t)n * R, sizeof(double));
   o->Omega = (double *)malloc(sizeof(double) * (size_t)n * R);
   /* NystromSketch.Init (Alg. 3 line 2): Omega column-major, reading A8 */
@@ -580,8 +585,43 @@ void oracle_destroy(void *h) {
   free(o->rp); free(o->col); free(o->m); free(o->cdiag);
   free(o->z); free(o->y); free(o->d); free(o->v); free(o->g);
   free(o->w1); free(o->w2); free(o->w3); free(o->a); free(o->cv);
-  free(o->S); free(o->Omega); free(o->log); free(o->vhist); free(o->ones);
+  free(o->S); free(o->Omega); free(o->log); free(o->vhist); free(o->ones); free(o->pw); free(o->pe);
   free(o);
+}
+
+/* Projection onto K of the points p_r = fl(z_r + fl(y_r / beta)), into w.
+ *   box K = {lo <= u <= hi}: w_r = min(max(p_r, lo), hi) (reading R32);
+ *   l2 ball K = {||u - b|| <= delta}: e_r = fl(p_r - b), N = sqrt(xsum(e^2)) (exact sum, CAC-2);
+ *     N <= delta: w = p (already in K); else w_r = fl(b + fl(s e_r)), s = fl(delta / N) (reading R34). */
+static void o_proj(oracle_t *o, const double *z, const double *y, double beta, double *w, int *err) {
+  const int64_t n = o->n;
+#pragma omp parallel for schedule(static) if (n > 65536)
+  for (int64_t r = 0; r < n; ++r) w[r] = z[r] + y[r] / beta;
+  if (!o->ball) {
+#pragma omp parallel for schedule(static) if (n > 65536)
+    for (int64_t r = 0; r < n; ++r) w[r] = fmin(fmax(w[r], o->lo), o->hi);
+    return;
+  }
+  double *e = o->pe;
+#pragma omp parallel for schedule(static) if (n > 65536)
+  for (int64_t r = 0; r < n; ++r) e[r] = w[r] - o->bval;
+  const double N = sqrt(o_dot(e, e, n, err));
+  if (N > o->delta) {
+    const double s = o->delta / N;
+#pragma omp parallel for schedule(static) if (n > 65536)
+    for (int64_t r = 0; r < n; ++r) w[r] = o->bval + s * e[r];
+  }
+}
+
+/* l2 ball K = {||u - 1|| <= delta} in original units (norm constraint); before the first
+ * step.  (Scaled units: delta / n, like b = 1/n.) */
+int oracle_set_ball(void *h, double delta) {
+  oracle_t *o = (oracle_t *)h;
+  if (o->t != 0 || !(delta >= 0.0)) return -1;
+  o->ineq = 1;
+  o->ball = 1;
+  o->delta = o->scale ? delta / (double)o->n : delta;
+  return 0;
 }
 
 /* Box K = {lo <= u <= hi} in original units; before the first step. */
@@ -628,16 +668,17 @@ int oracle_step(void *h, int64_t T) {
      *   bound = p_t + <y_t, w_t> + beta_t/2 <z_t - w_t, z_t + w_t> - alpha xi_t
      * (w_t = b gives the equality formulas above) */
     double S_ez = 0.0, S_yw = 0.0, S_ezw = 0.0;
+    double *wt = o->cv; /* w_t = proj_K(z_t + y_t / beta_t) (general template); free until the monitor */
     if (o->ineq) {
-      double *e = o->a, *w = o->cv, *zw = o->w1; /* free until the Lanczos call below */
+      double *e = o->a, *zw = o->w1; /* free until the Lanczos call below */
+      o_proj(o, o->z, o->y, beta, wt, &gerr);
 #pragma omp parallel for schedule(static) if (n > 65536)
       for (int64_t r = 0; r < n; ++r) {
-        w[r] = fmin(fmax(o->z[r] + o->y[r] / beta, o->lo), o->hi);
-        e[r] = o->z[r] - w[r];
-        zw[r] = o->z[r] + w[r];
+        e[r] = o->z[r] - wt[r];
+        zw[r] = o->z[r] + wt[r];
       }
       S_ez = o_dot(e, o->z, n, &gerr);
-      S_yw = o_dot(o->y, w, n, &gerr);
+      S_yw = o_dot(o->y, wt, n, &gerr);
       S_ezw = o_dot(e, zw, n, &gerr);
     }
     const double p_t = o->p;
@@ -647,7 +688,7 @@ int oracle_step(void *h, int64_t T) {
      * w_t = proj_K(z_t + y_t / beta_t) = min(max(z_t + y_t / beta_t, lo), hi), elementwise (R32). */
 #pragma omp parallel for schedule(static) if (n > 65536)
     for (int64_t r = 0; r < n; ++r) {
-      const double wr = o->ineq ? fmin(fmax(o->z[r] + o->y[r] / beta, o->lo), o->hi) : o->bval;
+      const double wr = o->ineq ? wt[r] : o->bval;
       o->d[r] = fma(beta, o->z[r] - wr, o->y[r]) + o->cdiag[r];
       o->g[r] = scg_lanczos_start(o->seed, t, r);
     }
@@ -675,9 +716,10 @@ int oracle_step(void *h, int64_t T) {
      * b is replaced by wbar_t = proj_K(z_{t+1} + y_t / beta_{t+1}) and the step rule keeps the
      * form gamma ||z - wbar||^2 <= beta_t eta_t^2 alpha^2 ||A||^2 (reading R32). */
     const double beta1 = o->beta0 * sqrt((double)(t + 2));
+    if (o->ineq) o_proj(o, o->z, o->y, beta1, o->pw, &err);
 #pragma omp parallel for schedule(static) if (n > 65536)
     for (int64_t r = 0; r < n; ++r) {
-      const double wb = o->ineq ? fmin(fmax(o->z[r] + o->y[r] / beta1, o->lo), o->hi) : o->bval;
+      const double wb = o->ineq ? o->pw[r] : o->bval;
       o->a[r] = o->z[r] - wb;
     }
     double nz = o_dot(o->a, o->a, n, &err);

@@ -820,3 +820,46 @@ def test_general_template_bound_dominates_suboptimality():
         assert rec[11] <= bound_exact + 1e-12
         ident = float(np.dot(y, z - w)) + 0.5 * beta * float(np.dot(z - w, z - w))
         assert abs((rec[10] - rec[11]) - ident) <= 1e-12 * max(1.0, abs(rec[10]))
+
+
+def test_l2_ball_constraint_set_closed_forms():
+    """Norm constraint K = {u : ||u - 1||_2 <= delta} (projection reading R34).  On C5
+    (vertex-transitive) the optimum of max tr(LX) with ||diag X - 1|| <= delta (and tr X <= alpha, large
+    enough) has a uniform diagonal 1 + delta / sqrt(n), so its value is (1 + delta / sqrt n) SDP.
+    delta = 0 is the equality problem: every iterate bitwise (the projection is then exactly b), the
+    general-template gap / bound equal to rounding; the bound dominates the suboptimality (exact
+    lambda_min) as for the box."""
+    n = 5
+    L = _edges_graph(n, [(k, (k + 1) % n) for k in range(n)])
+    sdp = 2 * n * (1 + math.cos(math.pi / n))
+    for d in (0.2, 0.6):
+        c = 1 + d / math.sqrt(n)
+        o = oracle.Oracle(L, 3, seed=5, logcap=3000, ball=d, trace_le=True, alpha=1.05 * n * c)
+        o.step(3000)
+        assert abs(o.implicit_objective() - c * sdp) <= 3e-3 * sdp
+        z = o.z * (o.alpha_orig / o.alpha)
+        assert abs(np.linalg.norm(z - 1.0) - d) <= 5e-3
+    e = oracle.Oracle(L, 3, seed=5, logcap=300)
+    e.step(300)
+    b = oracle.Oracle(L, 3, seed=5, logcap=300, ball=0.0)
+    b.step(300)
+    np.testing.assert_array_equal(b.log[:, :10], e.log[:, :10])
+    np.testing.assert_array_equal(b.z, e.z)
+    np.testing.assert_allclose(b.log[:, 10:12], e.log[:, 10:12], rtol=1e-11, atol=1e-14)
+    d = 0.4
+    c = 1 + d / math.sqrt(n)
+    alpha = 1.05 * n * c
+    o = oracle.Oracle(L, 3, seed=5, logcap=700, ball=d, trace_le=True, alpha=alpha)
+    Ld = L.dense()
+    for t in (5, 50, 600):
+        o.step(t - o.t)
+        y, z, p = o.y.copy(), o.z.copy(), o.p
+        beta = math.sqrt(t + 2)
+        pt = z + y / beta
+        ev = pt - 1.0 / n
+        N = float(np.linalg.norm(ev))
+        w = pt if N <= d / n else 1.0 / n + (d / n / N) * ev
+        D = -Ld / o.nrmL + np.diag(y + beta * (z - w))
+        lam = float(np.linalg.eigvalsh(D)[0])
+        bound_exact = p + float(np.dot(y, w)) + 0.5 * beta * float(np.dot(z - w, z + w)) - o.alpha * min(lam, 0.0)
+        assert p - (-c * sdp / (n * o.nrmL)) <= bound_exact + 1e-12
