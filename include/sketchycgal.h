@@ -236,6 +236,17 @@ scg_status sketchycgal_maxcut_alpha_doubling(scg_ctx **out, const scg_csr *L, in
  * gap = p + <y,z> + beta <z-w,z> - alpha xi, bound = p + <y,w> + beta/2 <z-w,z+w> - alpha xi. */
 scg_status sketchycgal_set_box(scg_ctx *c, double lo, double hi);
 
+/* Convex inclusion A X in K for the l2 ball K = {u : ||u - b||_2 <= delta} (the norm constraint
+ * ||A X - b|| <= delta of PAPER.md:3915-3918, general template P:3909-3941).  delta in original
+ * units (the MaxCut b is 1; delta >= 0, finite).  Call after init and before the first step
+ * (recomputes D_1's diagonal with the slack w_1); SCG_EINVAL otherwise.  Reading R34: the slack
+ * w = proj_K(p), p = z + y / beta, is p when ||p - b|| <= delta, else b + s (p - b) with
+ * s = delta / ||p - b||, the norm an exact sum over all ranks (each projection is one more
+ * reduction per use: wbar_t before the dual step, w_{t+1} after it).  The gap / bound records use
+ * w as in sketchycgal_set_box (reading R33).  Runs the multi-kernel path (no resident cluster
+ * kernel) and draws the next Lanczos start vector inside the dual step. */
+scg_status sketchycgal_set_ball(scg_ctx *c, double delta);
+
 /* Fixed Lanczos bound: every later iteration runs Alg. 2 with q instead of the schedule
  * q_t = min(n - 1, max(2, ceil(t^(1/4) ln n))) (ApproxMinEvec takes q as an input, PAPER.md:1068-1086;
  * Fact 4.1, gives the q for a target accuracy).  q = 0 restores the schedule.

@@ -36,6 +36,8 @@ struct DevScalars {
   double theta, nu_x, xi, c, vv, nz, gamma, p, tau;
   double my[4];            // sums over the state (y_t, z_t) of the NEXT iteration: y, y.z, z.z, z (k_dual_sketch)
   double g2n[2];           // ||g||^2 of the start vector drawn ahead on the side stream, by parity of its t
+  double bs[2];            // l2 ball projections: scale fl(delta / N) of [0] wbar_t, [1] w_{t+1} (reading R34)
+  int bin[2];              //   and whether the point is already inside the ball (the projection is then the point)
   int k, brk, err, pad;
 };
 
@@ -70,8 +72,9 @@ struct IterArgs {
   long long t;
   int q;
   int trace_le;  // SCG_TRACE_LE: H = 0 when xi_t >= 0
-  int ineq;      // box K = {lo <= u <= hi} (SCG_INEQ: lo = -inf, hi = b): slack w = min(max(z + y/beta, lo), hi)
-  double lo, hi; //   (reading R32)
+  int ineq;      // general template A X in K (box or ball): gap / bound with the slack (reading R33)
+  double lo, hi; // box K = {lo <= u <= hi} (SCG_INEQ: lo = -inf, hi = b): w = min(max(z + y/beta, lo), hi) (R32)
+  double delta;  // l2 ball K = {||u - b|| <= delta} (sketchycgal_set_ball, reading R34)
   double eta, one_m_eta, alpha, b, beta0, sq, beta_next, nbb;  // nbb = fl(fl(n b) b) = ||b||^2
 };
 
@@ -143,7 +146,8 @@ __device__ __forceinline__ void gstore(const Net &net, double *dst, int r, doubl
   }
 }
 
-enum FinKind { FK_FROB = 0, FK_RHO0, FK_OM, FK_RHO, FK_NUX, FK_MON, FK_NZ, FK_BAR, FK_RHO0M, FK_GEN, FK_RHO0S, FK_MY4 };
+enum FinKind { FK_FROB = 0, FK_RHO0, FK_OM, FK_RHO, FK_NUX, FK_MON, FK_NZ, FK_BAR, FK_RHO0M, FK_GEN, FK_RHO0S, FK_MY4,
+               FK_GK, FK_BALLS };
 
 struct FinArgs {
   int i;                 // Lanczos step (FK_OM, FK_RHO, FK_BAR)
@@ -820,9 +824,19 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
         for (int j = 0; j < 4; ++j) sc->my[j] = xacc_round(L[1 + j]);
       break;
     case FK_GEN: sc->g2n[f.i & 1] = xacc_round(L[0]); break;  // start vector of iteration f.i, drawn ahead
-    case FK_MY4:  // gap / bound sums over the initial state (box sets, k_init_box)
+    case FK_MY4:  // gap / bound sums over the state (box sets k_init_box, l2 ball k_ball_d)
       for (int j = 0; j < 4; ++j) sc->my[j] = xacc_round(L[j]);
       break;
+    case FK_GK:  // g = v^T Omega (l2 ball: the dual step needs another pass first)
+      for (int k = 0; k < f.R; ++k) sc->gk[k] = gk[k];
+      break;
+    case FK_BALLS: {  // N = ||p - b|| of the points to project onto the l2 ball (reading R34)
+      const double N = sqrt(xacc_round(L[0]));
+      const int j = f.i;
+      sc->bin[j] = !(N > f.A.delta);
+      sc->bs[j] = sc->bin[j] ? 1.0 : f.A.delta / N;
+      break;
+    }
     case FK_RHO0S:  // k_dual_sketch without the draw: the next start vector's norm comes from FK_GEN
       sc->rho[0] = sqrt(sc->g2n[f.i & 1]);
       sc->brk = 0;
@@ -935,7 +949,7 @@ __device__ __forceinline__ void emit(XSlot *slot, DevScalars *sc, const Net &net
     return;
   }
   const int e = (int)(net.E & 3ull);
-  const int nf = kind == FK_NZ ? f.R : 0;
+  const int nf = (kind == FK_NZ || kind == FK_GK) ? f.R : 0;
   for (int q = 0; q < net.P; ++q) {
     Mailbox *m = net.peerMB[q];
     for (int s = 0; s < NS; ++s)
@@ -983,7 +997,7 @@ __global__ void k_pull(int kind, int ns, Net net, DevScalars *sc, FinArgs f) {
       for (int p = 0; p < net.P; ++p) part[h] += __ldcv(&m->limbs[e][p][idx / kLimbs][idx % kLimbs]);
   }
   double gpart[2] = {0.0, 0.0};  // g_k = sum over ranks in rank order, k = lane, lane + 32
-  if (kind == FK_NZ)
+  if (kind == FK_NZ || kind == FK_GK)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int k = lane + 32 * h;
@@ -2046,7 +2060,17 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
 // ---------------------------------------------------------------- primal / dual / sketch
 // z <- (1-eta) z + eta alpha (v o v) (Alg. 4 line 8, primitive 3), ||z - b||^2 (exact),
 // per-block partials of g = v^T Omega (fp64, fixed tree; off the feedback path).
-template <bool BOX>  // box constraint set (A.ineq): compiled out of the equality instantiation
+// The projection onto the constraint set K of the point p = fl(z + fl(y / beta)): KS = 1 box
+// (min / max, reading R32), KS = 2 l2 ball with the scale s and the inside flag of the exact-sum
+// norm pass (k_ball_sum, reading R34).
+template <int KS>
+__device__ __forceinline__ double proj_k(double zr, double yr, double beta, const IterArgs &A, double s, int inside) {
+  const double p = zr + yr / beta;
+  if (KS == 1) return fmin(fmax(p, A.lo), A.hi);
+  return inside ? p : A.b + s * (p - A.b);
+}
+
+template <int KS>  // constraint set: 0 A X = b, 1 box (A.ineq), 2 l2 ball (nz in k_ball_nz)
 __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__ v, double *__restrict__ z,
                                                    const double *__restrict__ y,
                                                    const double *__restrict__ Om, int nl, int R, IterArgs A,
@@ -2088,8 +2112,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
             const double zr = hoff ? A.one_m_eta * zv[h] : fma(A.eta, hv, A.one_m_eta * zv[h]);
             z[r] = zr;
             // z_{t+1} - b, or z_{t+1} - wbar_t, wbar_t = proj_K(z_{t+1} + y_t / beta_{t+1})
-            const double e = zr - (BOX ? fmin(fmax(zr + y[r] / A.beta_next, A.lo), A.hi) : A.b);
-            xwin_add_nn(acc[0], e * e, err, xb.l[0]);
+            if (KS < 2) {
+              const double e = zr - (KS == 1 ? proj_k<1>(zr, y[r], A.beta_next, A, 0.0, 0) : A.b);
+              xwin_add_nn(acc[0], e * e, err, xb.l[0]);
+            }
           }
 #pragma unroll
           for (int u = 0; u < 16; ++u) gp[u] = fma(vr[h], om[h][u], gp[u]);
@@ -2125,7 +2151,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
       f.R = R;
       f.A = A;
       f.log = log;
-      emit<1>(slot, sc, net, FK_NZ, f, gsum);
+      emit<1>(slot, sc, net, KS == 2 ? FK_GK : FK_NZ, f, gsum);
     }
   }
 }
@@ -2134,7 +2160,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
 // ||g_{t+1}||^2 (exact) -- otherwise g_{t+1} was drawn ahead on the side stream (k_gen_start, FK_GEN)
 // and only its norm is taken over.  The sketch update of Alg. 4 line 10 is deferred (k_sketch_flush):
 // this kernel records its coefficients ck = fl(eta alpha) g_k in the ring slot js.
-template <bool BOX, bool GEN>  // BOX: box constraint set (A.ineq), compiled out of the equality instantiation
+template <int KS, bool GEN>  // constraint set: 0 A X = b, 1 box, 2 l2 ball (d and the gap sums in k_ball_d)
 __global__ void __launch_bounds__(kBlock, GEN ? 2 : 4) k_dual_sketch(const double *__restrict__ z, double *__restrict__ y,
                                                         double *__restrict__ d, const double *__restrict__ cdiag,
                                                         double *__restrict__ ckr, int js,
@@ -2143,11 +2169,13 @@ __global__ void __launch_bounds__(kBlock, GEN ? 2 : 4) k_dual_sketch(const doubl
                                                         Net net, const int *__restrict__ orig) {
   pdl_entry();
   const double gam = sc->gamma;
+  const double bs0 = KS == 2 ? sc->bs[0] : 0.0;  // l2 ball: projection of wbar_t (k_ball_sum j = 0)
+  const int bin0 = KS == 2 ? sc->bin[0] : 0;
   if (blockIdx.x == 0 && (int)threadIdx.x < R)  // H = 0 (trace-bounded, xi_t >= 0): no rank-one term
     ckr[js * kMaxR + threadIdx.x] = (A.trace_le && !(sc->xi < 0.0)) ? 0.0 : (A.eta * A.alpha) * sc->gk[threadIdx.x];
   // exact sums: [GEN: ||g_{t+1}||^2,] and over the next iteration's state (y_{t+1}, z_{t+1}):
   // sum y, y.z, z.z, sum z (surrogate gap / stopping rule, finalize FK_NZ)
-  constexpr int NS = GEN ? 5 : 4, o = GEN ? 1 : 0;
+  constexpr int NS = (GEN ? 1 : 0) + (KS == 2 ? 0 : 4), o = GEN ? 1 : 0;
   __shared__ XBlk<NS> xb;
   xblk_init<NS>(xb);
   XWin acc[NS];
@@ -2175,19 +2203,21 @@ __global__ void __launch_bounds__(kBlock, GEN ? 2 : 4) k_dual_sketch(const doubl
       const int r = r0 + u * stride;
       if (r < nl) {
         // dual update with wbar_t (b when A X = b) and the next diagonal with w_{t+1}
-        const double e = zr[u] - (BOX ? fmin(fmax(zr[u] + yv[u] / A.beta_next, A.lo), A.hi) : A.b);
+        const double e = zr[u] - (KS ? proj_k<KS>(zr[u], yv[u], A.beta_next, A, bs0, bin0) : A.b);
         const double yr = fma(gam, e, yv[u]);
         y[r] = yr;
-        const double e1 = BOX ? zr[u] - fmin(fmax(zr[u] + yr / A.beta_next, A.lo), A.hi) : e;
-        d[r] = fma(A.beta_next, e1, yr) + cd[u];
+        const double e1 = KS == 1 ? zr[u] - proj_k<1>(zr[u], yr, A.beta_next, A, 0.0, 0) : e;
+        if (KS < 2) d[r] = fma(A.beta_next, e1, yr) + cd[u];
         if (GEN) {
           const double gv = scg_lanczos_start(seed, A.t + 1, rb + og[u]);
           gstore_m(net, g + rb + r, mk[u], gv);
           peer |= mk[u];
           xwin_add_nn(acc[0], gv * gv, err, xb.l[0]);
         }
-        if (BOX) {  // general template (reading R33): <y,z>, <z-w,z>, <y,w>, <z-w,z+w> with w = w_{t+1}
-          const double wk = fmin(fmax(zr[u] + yr / A.beta_next, A.lo), A.hi);  // (the w of e1 above)
+        if (KS == 2) {
+          // l2 ball: d and the gap sums follow the norm pass over the new points (k_ball_d)
+        } else if (KS == 1) {  // general template (reading R33): <y,z>, <z-w,z>, <y,w>, <z-w,z+w>, w = w_{t+1}
+          const double wk = proj_k<1>(zr[u], yr, A.beta_next, A, 0.0, 0);  // (the w of e1 above)
           xwin_add(acc[o + 0], yr * zr[u], err, xb.l[o + 0]);
           xwin_add(acc[o + 1], e1 * zr[u], err, xb.l[o + 1]);
           xwin_add(acc[o + 2], yr * wk, err, xb.l[o + 2]);
@@ -2204,8 +2234,85 @@ __global__ void __launch_bounds__(kBlock, GEN ? 2 : 4) k_dual_sketch(const doubl
   if (commit_and_ticket<NS>(acc, xb, slot, err, sc, net.P, peer) && threadIdx.x == 0) {
     FinArgs f{};
     f.i = (int)((A.t + 1) & 1);
-    emit<NS>(slot, sc, net, GEN ? FK_RHO0M : FK_RHO0S, f, nullptr);
+    emit<NS>(slot, sc, net, KS == 2 ? FK_RHO0 : (GEN ? FK_RHO0M : FK_RHO0S), f, nullptr);
   }
+}
+
+// l2 ball (reading R34): N^2 = ||p - b||^2 (exact) of the points p = fl(z + fl(y / beta)), finalized into
+// the scale / inside flag of projection j (0: wbar_t of the dual step, 1: w_{t+1} of D_{t+1}).
+__global__ void __launch_bounds__(kBlock) k_ball_sum(const double *__restrict__ z, const double *__restrict__ y,
+                                                     double beta, int nl, IterArgs A, int j, XSlot *slot,
+                                                     DevScalars *sc, Net net) {
+  pdl_entry();
+  __shared__ XBlk<1> xb;
+  xblk_init<1>(xb);
+  XWin acc[1];
+  xwin_init(acc[0]);
+  int err = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double e = (z[r] + y[r] / beta) - A.b;
+    xwin_add_nn(acc[0], e * e, err, xb.l[0]);
+  }
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P, 0u) && threadIdx.x == 0) {
+    FinArgs f{};
+    f.i = j;
+    f.A = A;
+    emit<1>(slot, sc, net, FK_BALLS, f, nullptr);
+  }
+}
+
+// l2 ball: ||z_{t+1} - wbar_t||^2 (exact) -> the dual step, objective tracker and record (FK_NZ; g was
+// finalized by k_primal's FK_GK, so no g payload here).
+__global__ void __launch_bounds__(kBlock) k_ball_nz(const double *__restrict__ z, const double *__restrict__ y, int nl,
+                                                    IterArgs A, XSlot *slot, DevScalars *sc, scg_iter_rec *log,
+                                                    Net net) {
+  pdl_entry();
+  const double s = sc->bs[0];
+  const int inside = sc->bin[0];
+  __shared__ XBlk<1> xb;
+  xblk_init<1>(xb);
+  XWin acc[1];
+  xwin_init(acc[0]);
+  int err = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double e = z[r] - proj_k<2>(z[r], y[r], A.beta_next, A, s, inside);
+    xwin_add_nn(acc[0], e * e, err, xb.l[0]);
+  }
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P, 0u) && threadIdx.x == 0) {
+    FinArgs f{};
+    f.R = 0;  // g already in sc->gk
+    f.A = A;
+    f.log = log;
+    emit<1>(slot, sc, net, FK_NZ, f, sc->gk);
+  }
+}
+
+// l2 ball: d for D_{t+1} with w_{t+1} = proj_K(z_{t+1} + y_{t+1} / beta_{t+1}) and the general-template
+// gap / bound sums over the state (y_{t+1}, z_{t+1}, w_{t+1}) (reading R33); also the t = 1 setup.
+__global__ void __launch_bounds__(kBlock) k_ball_d(const double *__restrict__ z, const double *__restrict__ y,
+                                                   const double *__restrict__ cdiag, double *__restrict__ d, int nl,
+                                                   double beta, IterArgs A, XSlot *slot, DevScalars *sc, Net net) {
+  pdl_entry();
+  const double s = sc->bs[1];
+  const int inside = sc->bin[1];
+  __shared__ XBlk<4> xb;
+  xblk_init<4>(xb);
+  XWin acc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) xwin_init(acc[q]);
+  int err = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double zr = z[r], yr = y[r];
+    const double w = proj_k<2>(zr, yr, beta, A, s, inside);
+    const double e = zr - w;
+    d[r] = fma(beta, e, yr) + cdiag[r];
+    xwin_add(acc[0], yr * zr, err, xb.l[0]);
+    xwin_add(acc[1], e * zr, err, xb.l[1]);
+    xwin_add(acc[2], yr * w, err, xb.l[2]);
+    xwin_add(acc[3], e * (zr + w), err, xb.l[3]);
+  }
+  if (commit_and_ticket<4>(acc, xb, slot, err, sc, net.P, 0u) && threadIdx.x == 0)
+    emit<4>(slot, sc, net, FK_MY4, FinArgs{}, nullptr);
 }
 
 // Deferred sketch updates (Alg. 4 line 10, eqn:sketch-update PAPER.md:1162-1169): S is

@@ -74,7 +74,7 @@ struct EvPair {
   int cls;
 };
 
-enum { SLOT_NU0 = 0, SLOT_OM, SLOT_RHO, SLOT_XX, SLOT_MON, SLOT_NZ, SLOT_INIT, SLOT_BAR, SLOT_GEN, SLOT_COUNT };
+enum { SLOT_NU0 = 0, SLOT_OM, SLOT_RHO, SLOT_XX, SLOT_MON, SLOT_NZ, SLOT_INIT, SLOT_BAR, SLOT_GEN, SLOT_BALL, SLOT_COUNT };
 
 }  // namespace
 
@@ -153,6 +153,8 @@ struct scg_ctx {
   int world = 1, mode = 0;  // mode 0: single, 1: emulated shards, 2: one rank of a multi-process job
   bool box = false;           // constraint set K = {klo <= u <= khi} (scaled units): SCG_INEQ or sketchycgal_set_box
   double klo = 0.0, khi = 0.0;
+  bool ball = false;          // K = {||u - b|| <= delta} (sketchycgal_set_ball; box is then set too: general template)
+  double delta = 0.0;         //   scaled units
   bool fused = false;        // one GPU: Lanczos pass 1 as one persistent kernel (SCG_FUSED_PASS1)
   unsigned long long gphase = 0;  // grid-barrier phases issued so far (fused pass 1)
   bool pdl = true;          // programmatic dependent launches (SCG_NO_PDL disables)
@@ -1455,6 +1457,29 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   return SCG_OK;
 }
 
+// l2 ball (reading R34): N = ||z + y / beta - b|| over all ranks -> scale / inside flag of projection j.
+static void ball_norm(scg_ctx *c, double beta, const IterArgs &A, int j) {
+  const unsigned long long E = ++c->epoch;
+  for (Shard *s : c->sh)
+    launch(c, KC_OTHER, 0.0, k_ball_sum, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z, (const double *)s->y,
+           beta, (int)s->nl, A, j, s->slots + SLOT_BALL, s->sc, net_of(c, s, E));
+  FinArgs f{};
+  f.i = j;
+  f.A = A;
+  pull_all(c, FK_BALLS, 1, E, f);
+}
+
+// l2 ball: w = proj_K(z + y / beta) of the current state, d = beta (z - w) + y + cdiag, and the
+// general-template gap / bound sums <y,z>, <z-w,z>, <y,w>, <z-w,z+w> (reading R33).
+static void ball_state(scg_ctx *c, double beta, const IterArgs &A) {
+  ball_norm(c, beta, A, 1);
+  const unsigned long long E = ++c->epoch;
+  for (Shard *s : c->sh)
+    launch(c, KC_OTHER, 0.0, k_ball_d, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z, (const double *)s->y,
+           (const double *)s->cdiag, s->d, (int)s->nl, beta, A, s->slots + SLOT_BALL, s->sc, net_of(c, s, E));
+  pull_all(c, FK_MY4, 4, E, FinArgs{});
+}
+
 scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
   if (!c) return SCG_EINVAL;
   if (c->failed) return SCG_ESTATE;
@@ -1490,6 +1515,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     A.ineq = c->box ? 1 : 0;
     A.lo = c->klo;
     A.hi = c->khi;
+    A.delta = c->delta;
     int64_t q = (int64_t)std::ceil(std::sqrt(std::sqrt((double)t)) * c->lnN);
     if (q < 2) q = 2;
     if (q > c->n - 1) q = c->n - 1;
@@ -1652,27 +1678,45 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     }
     pull_all(c, FK_MON, 3, E, FinArgs{});
     E = ++c->epoch;
+    const int ks = c->ball ? 2 : (c->box ? 1 : 0);  // constraint set: A X = b, box, l2 ball
     for (Shard *s : c->sh)
-      launch(c, KC_PRIMAL, s->kb[KC_PRIMAL], c->box ? k_primal<true> : k_primal<false>, dim3(s->grid_primal), dim3(kBlock), (const double *)c->vslot(s, js), s->z,
+      launch(c, KC_PRIMAL, s->kb[KC_PRIMAL], ks == 2 ? k_primal<2> : (ks ? k_primal<1> : k_primal<0>),
+             dim3(s->grid_primal), dim3(kBlock), (const double *)c->vslot(s, js), s->z,
              (const double *)s->y, (const double *)s->Om, (int)s->nl, c->R, A, s->gpart, s->slots + SLOT_NZ, s->sc, s->dlog, net_of(c, s, E));
     {
       FinArgs f{};
       f.R = c->R;
+      f.A = A;
+      pull_all(c, ks == 2 ? FK_GK : FK_NZ, 1, E, f);
+    }
+    if (ks == 2) {  // l2 ball (reading R34): wbar_t needs ||z_{t+1} + y_t / beta_{t+1} - b|| first
+      ball_norm(c, A.beta_next, A, 0);
+      E = ++c->epoch;
+      for (Shard *s : c->sh)
+        launch(c, KC_OTHER, 0.0, k_ball_nz, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z,
+               (const double *)s->y, (int)s->nl, A, s->slots + SLOT_BALL, s->sc, s->dlog, net_of(c, s, E));
+      FinArgs f{};
+      f.R = 0;  // g finalized by FK_GK
       f.A = A;
       pull_all(c, FK_NZ, 1, E, f);
     }
     E = ++c->epoch;
     if (c->side_rng) cudaStreamWaitEvent(c->stream, c->evB, 0);  // g_{t+1} and its norm are drawn
     for (Shard *s : c->sh) {
-      auto kD = c->side_rng ? (c->box ? k_dual_sketch<true, false> : k_dual_sketch<false, false>)
-                            : (c->box ? k_dual_sketch<true, true> : k_dual_sketch<false, true>);
+      auto kD = c->side_rng ? (ks == 1 ? k_dual_sketch<1, false> : k_dual_sketch<0, false>)
+                            : (ks == 2 ? k_dual_sketch<2, true> : (ks ? k_dual_sketch<1, true> : k_dual_sketch<0, true>));
       launch(c, KC_DUAL_SKETCH, c->side_rng ? 40.0 * (double)s->nl : s->kb[KC_DUAL_SKETCH], kD,
              dim3(c->side_rng ? s->grid_dual_s : s->grid_dual), dim3(kBlock),
              (const double *)s->z, s->y, s->d, (const double *)s->cdiag, s->ckr, js, c->wslot(s, 0),
              (int)s->nl, (long long)s->rb, c->R, A, c->seed, s->slots + SLOT_NU0, s->sc, net_of(c, s, E),
              (const int *)s->orig);
     }
-    pull_all(c, FK_RHO0M, 5, E, FinArgs{});
+    if (ks == 2) {
+      pull_all(c, FK_RHO0, 1, E, FinArgs{});
+      ball_state(c, A.beta_next, A);  // w_{t+1}, D_{t+1}'s diagonal and the gap / bound sums
+    } else {
+      pull_all(c, FK_RHO0M, 5, E, FinArgs{});
+    }
     c->ome[js] = A.one_m_eta;
     c->vlast = js;
     if (++c->spend == kSketchB) sketch_flush(c);
@@ -2061,6 +2105,23 @@ scg_status sketchycgal_set_box(scg_ctx *c, double lo, double hi) {
            (const double *)s->cdiag, s->d, (int)s->nl, beta1, c->klo, c->khi, s->slots + SLOT_INIT, s->sc,
            net_of(c, s, E));
   pull_all(c, FK_MY4, 4, E, FinArgs{});
+  return sketchycgal_synchronize(c);
+}
+
+scg_status sketchycgal_set_ball(scg_ctx *c, double delta) {
+  if (!c || c->t != 0 || !(delta >= 0.0) || !std::isfinite(delta)) return SCG_EINVAL;
+  const bool scale = (c->flags & SCG_SCALE) != 0;
+  c->box = true;  // general template (gap / bound with the slack, reading R33)
+  c->ball = true;
+  c->delta = scale ? delta / (double)c->n : delta;  // scaled units like b = 1/n
+  if (c->side_rng) {  // the ball's dual step keeps the draw of g_{t+1} in k_dual_sketch
+    cudaStreamSynchronize(c->side);
+    c->side_rng = false;
+  }
+  IterArgs A{};
+  A.b = c->b;
+  A.delta = c->delta;
+  ball_state(c, c->beta0 * std::sqrt(2.0), A);  // D_1 with w_1 = proj_K(z_1 + y_1 / beta_1)
   return sketchycgal_synchronize(c);
 }
 
