@@ -78,6 +78,10 @@ def _load():
         lib.oracle_set_box.argtypes = [P, ctypes.c_double, ctypes.c_double]
         lib.oracle_set_ball.restype = ctypes.c_int
         lib.oracle_set_ball.argtypes = [P, ctypes.c_double]
+        lib.oracle_set_l1_ball.restype = ctypes.c_int
+        lib.oracle_proj.restype = ctypes.c_int
+        lib.oracle_proj.argtypes = [P, P, P, ctypes.c_double, P]
+        lib.oracle_set_l1_ball.argtypes = [P, ctypes.c_double]
         lib.oracle_t_done.restype = I64
         lib.oracle_t_done.argtypes = [P]
         lib.oracle_scalar.restype = D
@@ -202,7 +206,8 @@ class Oracle:
 
     def __init__(self, L, R: int, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
                  scale: bool = True, qfix: int = 0, logcap: int = 0, vhist: int = 0, trace_le: bool = False,
-                 ineq: bool = False, box: tuple | None = None, div_norm: bool = False, ball: float | None = None):
+                 ineq: bool = False, box: tuple | None = None, div_norm: bool = False, ball: float | None = None,
+                 l1_ball: float | None = None):
         self.L = L
         self.n = L.n
         self.R = int(R)
@@ -218,13 +223,16 @@ class Oracle:
                                         int(qfix), self.logcap, self.vhist_cap,
                                         (1 if trace_le else 0) | (2 if ineq else 0) | (4 if div_norm else 0))
         self.trace_le = bool(trace_le)
-        self.ineq = bool(ineq) or box is not None or ball is not None
+        self.ineq = bool(ineq) or box is not None or ball is not None or l1_ball is not None
         if box is not None:  # K = {lo <= u <= hi}, original units
             if _load().oracle_set_box(self._h, float(box[0]), float(box[1])) != 0:
                 raise ValueError("oracle_set_box: after the first step or lo > hi")
         if ball is not None:  # K = {||u - 1||_2 <= ball}, original units
             if _load().oracle_set_ball(self._h, float(ball)) != 0:
                 raise ValueError("oracle_set_ball: after the first step or delta < 0")
+        if l1_ball is not None:  # K = {||u - 1||_1 <= l1_ball}, original units
+            if _load().oracle_set_l1_ball(self._h, float(l1_ball)) != 0:
+                raise ValueError("oracle_set_l1_ball: after the first step or delta < 0")
         self.beta0 = float(beta0)
 
     def __del__(self):
@@ -300,6 +308,15 @@ class Oracle:
         return _load().oracle_scalar(self._h, 4)
 
     # ---- original-units monitors ("evaluated with respect to the original data")
+    def project(self, z, y=None, beta: float = 1.0) -> np.ndarray:
+        """proj_K(z + y / beta) onto the constraint set in effect, scaled units."""
+        z = _f64(z)
+        y = np.zeros_like(z) if y is None else _f64(y)
+        w = np.empty_like(z)
+        if _load().oracle_proj(self._h, z.ctypes.data, y.ctypes.data, float(beta), w.ctypes.data) != 0:
+            raise ValueError("oracle_proj: no constraint set, or a range error in its exact sums")
+        return w
+
     def implicit_objective(self) -> float:
         """tr(L X_t) of the implicit iterate from the tracked p_t = <C~, X~_t>."""
         if self.scale:

@@ -487,7 +487,7 @@ typedef struct {
   int ineq;     /* general template with a box K = {lo <= u <= hi} */
   double lo, hi; /* scaled units; bit 1 of the mode (SCG_INEQ): lo = -inf, hi = b */
   int div_norm; /* bit 2 of the mode: normalizations as printed divisions (R26 pin, see o_lanczos) */
-  int ball;      /* K = {u : ||u - b||_2 <= delta} (norm constraint; reading R34) */
+  int ball;      /* K = {u : ||u - b|| <= delta} (norm constraint): 1 l2 (R34), 2 l1 (R35) */
   double delta;  /* scaled units */
   double *pw, *pe; /* projection work arrays */
   uint64_t seed;
@@ -589,6 +589,66 @@ void oracle_destroy(void *h) {
   free(o);
 }
 
+/* The exact value S - c a - delta, rounded once (its sign is exact): S an exact sum, c a an exact
+ * product by the error-free transformation hi = fl(c a), lo = fma(c, a, -hi) (CAC-2 summands). */
+static double o_l1_g(const xsum_t *S, double c, double a, double delta) {
+  xsum_t g = *S;
+  const double hi = c * a, lo = fma(c, a, -hi);
+  xs_add(&g, -hi);
+  xs_add(&g, -lo);
+  xs_add(&g, -delta);
+  return xs_round(&g);
+}
+
+static int o_desc(const void *x, const void *y) {
+  const double a = *(const double *)x, b = *(const double *)y;
+  return a < b ? 1 : (a > b ? -1 : 0);
+}
+
+/* Euclidean projection onto the l1 ball {||u - b||_1 <= delta} (reading R35), in place on
+ * the points w = p:  e_r = fl(p_r - b), a_r = |e_r|.
+ *   sum_r a_r - delta <= 0 (exact): w = p (already in K).  Else delta = 0: w = b.
+ *   Else soft thresholding w_r = fl(b + sign(e_r) max(fl(a_r - theta), 0)) with the threshold of the
+ *   sorted a_(1) >= a_(2) >= ... : rho = max{j : S_j - j a_(j) - delta < 0} (S_j = a_(1) + ... + a_(j),
+ *   decided exactly; S_j - j a_(j) grows with j), theta = fl(fl(S_rho - delta) / rho) (S_rho - delta
+ *   summed exactly, rounded once). */
+static void o_proj_l1(oracle_t *o, double *w, int *err) {
+  const int64_t n = o->n;
+  double *e = o->pe;
+  double *a = (double *)malloc(sizeof(double) * (size_t)n);
+  for (int64_t r = 0; r < n; ++r) {
+    e[r] = w[r] - o->bval;
+    a[r] = fabs(e[r]);
+  }
+  xsum_t S;
+  xs_init(&S);
+  for (int64_t r = 0; r < n; ++r) xs_add(&S, a[r]);
+  if (S.err && err) *err = 1;
+  if (o_l1_g(&S, 0.0, 0.0, o->delta) <= 0.0) { /* inside: w = p */
+    free(a);
+    return;
+  }
+  if (o->delta == 0.0) {
+    for (int64_t r = 0; r < n; ++r) w[r] = o->bval;
+    free(a);
+    return;
+  }
+  qsort(a, (size_t)n, sizeof(double), o_desc);
+  xs_init(&S);
+  xsum_t Srho;
+  int64_t rho = 0;
+  for (int64_t j = 1; j <= n; ++j) {
+    xs_add(&S, a[j - 1]);
+    if (!(o_l1_g(&S, (double)j, a[j - 1], o->delta) < 0.0)) break;
+    rho = j;
+    Srho = S;
+  }
+  /* rho >= 1: S_1 - a_(1) - delta = -delta < 0 */
+  const double theta = o_l1_g(&Srho, 0.0, 0.0, o->delta) / (double)rho;
+  for (int64_t r = 0; r < n; ++r) w[r] = o->bval + copysign(fmax(fabs(e[r]) - theta, 0.0), e[r]);
+  free(a);
+}
+
 /* Projection onto K of the points p_r = fl(z_r + fl(y_r / beta)), into w.
  *   box K = {lo <= u <= hi}: w_r = min(max(p_r, lo), hi) (reading R32);
  *   l2 ball K = {||u - b|| <= delta}: e_r = fl(p_r - b), N = sqrt(xsum(e^2)) (exact sum, CAC-2);
@@ -600,6 +660,10 @@ static void o_proj(oracle_t *o, const double *z, const double *y, double beta, d
   if (!o->ball) {
 #pragma omp parallel for schedule(static) if (n > 65536)
     for (int64_t r = 0; r < n; ++r) w[r] = fmin(fmax(w[r], o->lo), o->hi);
+    return;
+  }
+  if (o->ball == 2) {
+    o_proj_l1(o, w, err);
     return;
   }
   double *e = o->pe;
@@ -620,6 +684,26 @@ int oracle_set_ball(void *h, double delta) {
   if (o->t != 0 || !(delta >= 0.0)) return -1;
   o->ineq = 1;
   o->ball = 1;
+  o->delta = o->scale ? delta / (double)o->n : delta;
+  return 0;
+}
+
+/* proj_K(z + y / beta) of the constraint set in effect, scaled units (test access to o_proj). */
+int oracle_proj(void *h, const double *z, const double *y, double beta, double *w) {
+  oracle_t *o = (oracle_t *)h;
+  int err = 0;
+  if (!o->ineq) return -1;
+  o_proj(o, z, y, beta, w, &err);
+  return err ? -2 : 0;
+}
+
+/* l1 ball K = {||u - 1||_1 <= delta} in original units (reading R35); before the first
+ * step.  (Scaled units: delta / n.) */
+int oracle_set_l1_ball(void *h, double delta) {
+  oracle_t *o = (oracle_t *)h;
+  if (o->t != 0 || !(delta >= 0.0)) return -1;
+  o->ineq = 1;
+  o->ball = 2;
   o->delta = o->scale ? delta / (double)o->n : delta;
   return 0;
 }

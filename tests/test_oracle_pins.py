@@ -863,3 +863,94 @@ def test_l2_ball_constraint_set_closed_forms():
         lam = float(np.linalg.eigvalsh(D)[0])
         bound_exact = p + float(np.dot(y, w)) + 0.5 * beta * float(np.dot(z - w, z + w)) - o.alpha * min(lam, 0.0)
         assert p - (-c * sdp / (n * o.nrmL)) <= bound_exact + 1e-12
+
+
+def _soft_threshold_bisect(e, delta):
+    """Euclidean projection of e onto {||u||_1 <= delta} by bisection on the threshold theta of
+    F(theta) = sum max(|e| - theta, 0) = delta (an algorithm independent of the oracle's sort)."""
+    a = np.abs(e)
+    if a.sum() <= delta:
+        return e.copy()
+    lo, hi = 0.0, float(a.max())
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if np.maximum(a - mid, 0).sum() > delta:
+            lo = mid
+        else:
+            hi = mid
+    return np.sign(e) * np.maximum(a - 0.5 * (lo + hi), 0)
+
+
+def test_l1_ball_projection_pins():
+    """l1-ball projection (reading R35) against values fixed by the definition: ties
+    ([4,4,4,2] - 1 with delta 1: the top three share theta = 8/3), a uniform |e| (theta = |e| -
+    delta / n), a point already inside (returned unchanged, bitwise), delta = 0 (b, bitwise), and
+    random vectors against an independent bisection on the threshold (1e-12): the projection lies on
+    the sphere ||w - b||_1 = delta and keeps the signs of e."""
+    n = 6
+    L = _edges_graph(n, [(k, (k + 1) % n) for k in range(n)])
+    o = oracle.Oracle(L, 2, scale=False, l1_ball=1.0)
+    w = o.project(np.array([4.0, 4.0, 4.0, 2.0, 1.0, 1.0]))
+    np.testing.assert_allclose(w, [4 / 3, 4 / 3, 4 / 3, 1, 1, 1], rtol=1e-15)
+    w = o.project(np.full(n, 1.5))  # |e| = 0.5, n |e| = 3 > 1: theta = 0.5 - 1/6
+    np.testing.assert_allclose(w, np.full(n, 1 + 1 / 6), rtol=1e-15)
+    w = o.project(np.full(n, 0.5))
+    np.testing.assert_allclose(w, np.full(n, 1 - 1 / 6), rtol=1e-15)
+    p = np.array([1.2, 1.0, 0.9, 1.0, 1.1, 0.95])  # ||p - 1||_1 = 0.45 <= 1
+    np.testing.assert_array_equal(o.project(p), p)
+    z = oracle.Oracle(L, 2, scale=False, l1_ball=0.0)
+    np.testing.assert_array_equal(z.project(np.array([4.0, -1, 3, 2, 1, 0])), np.ones(n))
+    rng = np.random.default_rng(7)
+    n = 300
+    L = _edges_graph(n, [(k, (k + 1) % n) for k in range(n)])
+    for delta in (0.3, 5.0, 40.0):
+        o = oracle.Oracle(L, 2, scale=False, l1_ball=delta)
+        for _ in range(5):
+            e = rng.standard_normal(n) * rng.choice([0.1, 1.0], n)
+            e[rng.integers(0, n, 20)] = 0.25  # ties
+            w = o.project(1.0 + e)
+            want = 1.0 + _soft_threshold_bisect(e, delta)
+            np.testing.assert_allclose(w, want, rtol=0, atol=1e-12)
+            if np.abs(e).sum() > delta:
+                assert abs(np.abs(w - 1.0).sum() - delta) <= 1e-12 * n
+                assert np.all(np.sign(w - 1.0) * np.sign(e) >= 0)
+
+
+def test_l1_ball_constraint_set_closed_forms():
+    """Norm constraint K = {u : ||u - 1||_1 <= delta} (projection reading R35).  On C5
+    (vertex-transitive; the ball is permutation invariant and the optimal value concave in the
+    diagonal) the optimum of max tr(LX) with ||diag X - 1||_1 <= delta has the uniform diagonal
+    1 + delta / n: value (1 + delta / n) SDP.  delta = 0 is the equality problem: every iterate bitwise,
+    the general-template gap / bound equal to rounding; the bound dominates the suboptimality (exact
+    lambda_min)."""
+    n = 5
+    L = _edges_graph(n, [(k, (k + 1) % n) for k in range(n)])
+    sdp = 2 * n * (1 + math.cos(math.pi / n))
+    for d in (0.3, 1.0):
+        c = 1 + d / n
+        o = oracle.Oracle(L, 3, seed=5, logcap=3000, l1_ball=d, trace_le=True, alpha=1.05 * n * c)
+        o.step(3000)
+        assert abs(o.implicit_objective() - c * sdp) <= 3e-3 * sdp
+        z = o.z * (o.alpha_orig / o.alpha)
+        assert abs(np.abs(z - 1.0).sum() - d) <= 1e-2
+    e = oracle.Oracle(L, 3, seed=5, logcap=300)
+    e.step(300)
+    b = oracle.Oracle(L, 3, seed=5, logcap=300, l1_ball=0.0)
+    b.step(300)
+    np.testing.assert_array_equal(b.log[:, :10], e.log[:, :10])
+    np.testing.assert_array_equal(b.z, e.z)
+    np.testing.assert_allclose(b.log[:, 10:12], e.log[:, 10:12], rtol=1e-11, atol=1e-14)
+    d = 0.5
+    c = 1 + d / n
+    o = oracle.Oracle(L, 3, seed=5, logcap=700, l1_ball=d, trace_le=True, alpha=1.05 * n * c)
+    Ld = L.dense()
+    for t in (5, 50, 600):
+        o.step(t - o.t)
+        y, z, p = o.y.copy(), o.z.copy(), o.p
+        beta = math.sqrt(t + 2)
+        w = 1.0 / n + _soft_threshold_bisect(z + y / beta - 1.0 / n, d / n)
+        D = -Ld / o.nrmL + np.diag(y + beta * (z - w))
+        lam = float(np.linalg.eigvalsh(D)[0])
+        bound_exact = p + float(np.dot(y, w)) + 0.5 * beta * float(np.dot(z - w, z + w)) - o.alpha * min(lam, 0.0)
+        assert p - (-c * sdp / (n * o.nrmL)) <= bound_exact + 1e-12
+        np.testing.assert_allclose(o.project(z, y, beta), w, rtol=0, atol=1e-15)
