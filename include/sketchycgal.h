@@ -247,6 +247,16 @@ scg_status sketchycgal_set_box(scg_ctx *c, double lo, double hi);
  * kernel) and draws the next Lanczos start vector inside the dual step. */
 scg_status sketchycgal_set_ball(scg_ctx *c, double delta);
 
+/* Convex inclusion A X in K for the l1 ball K = {u : ||u - b||_1 <= delta} (the norm constraint of
+ * PAPER.md:3915-3918 with the l1 norm).  delta in original units, >= 0 and finite; call after init
+ * and before the first step (SCG_EINVAL otherwise).  Reading R35: the slack w = proj_K(p) is p when
+ * ||p - b||_1 <= delta, b when delta = 0, else the soft threshold w_r = b + sign(e_r) max(|e_r| -
+ * theta, 0), e = p - b, theta = (S - delta) / c over the active set {|e_r| >= v*} (c entries, exact
+ * sum S) whose least entry v* satisfies S(v) - c(v) v - delta < 0 -- found without a sort by a 63-step
+ * bisection on the bit pattern of v, each step an exact-sum pass over all ranks.  Same execution
+ * path and gap / bound records as sketchycgal_set_ball. */
+scg_status sketchycgal_set_ball_l1(scg_ctx *c, double delta);
+
 /* Fixed Lanczos bound: every later iteration runs Alg. 2 with q instead of the schedule
  * q_t = min(n - 1, max(2, ceil(t^(1/4) ln n))) (ApproxMinEvec takes q as an input, PAPER.md:1068-1086;
  * Fact 4.1, gives the q for a target accuracy).  q = 0 restores the schedule.

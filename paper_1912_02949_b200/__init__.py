@@ -162,7 +162,7 @@ EXPORTS = ["sketchycgal_maxcut_init", "sketchycgal_step", "sketchycgal_synchroni
            "sketchycgal_kernel_stats", "sketchycgal_reset_stats", "sketchycgal_nccl_unique_id",
            "sketchycgal_row_splits", "sketchycgal_halo_plan", "sketchycgal_run",
            "sketchycgal_selftest_division", "sketchycgal_last_error", "sketchycgal_destroy",
-           "sketchycgal_maxcut_alpha_doubling", "sketchycgal_set_box", "sketchycgal_set_ball",
+           "sketchycgal_maxcut_alpha_doubling", "sketchycgal_set_box", "sketchycgal_set_ball", "sketchycgal_set_ball_l1",
            "sketchycgal_set_lanczos_q"]
 
 _lib = None
@@ -198,6 +198,8 @@ def open_library(path: str = LIB_PATH):
     lib.sketchycgal_set_box.argtypes = [P, D, D]
     lib.sketchycgal_set_ball.restype = ctypes.c_int
     lib.sketchycgal_set_ball.argtypes = [P, D]
+    lib.sketchycgal_set_ball_l1.restype = ctypes.c_int
+    lib.sketchycgal_set_ball_l1.argtypes = [P, D]
     lib.sketchycgal_maxcut_alpha_doubling.restype = ctypes.c_int
     lib.sketchycgal_maxcut_alpha_doubling.argtypes = [ctypes.POINTER(P), ctypes.POINTER(Csr), I32, D, D,
                                                       ctypes.c_uint64, ctypes.c_uint32, I32, P, I64, D, I32, P, P,
@@ -293,7 +295,8 @@ class SketchyCGAL:
                  scale: bool = True, trace_correct: bool = True, profile: bool = False, device: int = 0,
                  stream=None, regenerate: bool = False, trace_le: bool = False, shards: int = 1, splits=None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None, ineq: bool = False,
-                 box: tuple | None = None, ball: float | None = None, pdl: bool = True, fused_pass1: bool = False, ws_spmv: bool = False,
+                 box: tuple | None = None, ball: float | None = None,
+                 l1_ball: float | None = None, pdl: bool = True, fused_pass1: bool = False, ws_spmv: bool = False,
                  tma_b: bool = False, debug_log: bool = False, qfix: int = 0, ell: bool = True,
                  side_rng: bool = True, host_comm: "TorchHostComm | None" = None, resident: bool = True):
         self.lib = load()
@@ -346,6 +349,8 @@ class SketchyCGAL:
             self._check(self.lib.sketchycgal_set_box(self._h, float(box[0]), float(box[1])), "sketchycgal_set_box")
         if ball is not None:  # K = {||u - 1|| <= delta} (reading R34)
             self._check(self.lib.sketchycgal_set_ball(self._h, float(ball)), "sketchycgal_set_ball")
+        if l1_ball is not None:  # K = {||u - 1||_1 <= delta} (reading R35)
+            self._check(self.lib.sketchycgal_set_ball_l1(self._h, float(l1_ball)), "sketchycgal_set_ball_l1")
 
     @classmethod
     def alpha_doubling(cls, L, R: int, alpha0: float, T: int, rtol: float = 1e-2, max_rounds: int = 8,

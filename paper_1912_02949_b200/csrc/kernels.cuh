@@ -36,8 +36,11 @@ struct DevScalars {
   double theta, nu_x, xi, c, vv, nz, gamma, p, tau;
   double my[4];            // sums over the state (y_t, z_t) of the NEXT iteration: y, y.z, z.z, z (k_dual_sketch)
   double g2n[2];           // ||g||^2 of the start vector drawn ahead on the side stream, by parity of its t
-  double bs[2];            // l2 ball projections: scale fl(delta / N) of [0] wbar_t, [1] w_{t+1} (reading R34)
+  double bs[2];            // ball projections [0] wbar_t, [1] w_{t+1}: l2 scale fl(delta / N) (reading R34),
+                           //   l1 threshold theta (reading R35)
   int bin[2];              //   and whether the point is already inside the ball (the projection is then the point)
+  unsigned long long bk[2];  // l1 threshold search: keys (bit patterns) lo, hi of the bracket (reading R35)
+  int bdone, bpad;
   int k, brk, err, pad;
 };
 
@@ -147,7 +150,7 @@ __device__ __forceinline__ void gstore(const Net &net, double *dst, int r, doubl
 }
 
 enum FinKind { FK_FROB = 0, FK_RHO0, FK_OM, FK_RHO, FK_NUX, FK_MON, FK_NZ, FK_BAR, FK_RHO0M, FK_GEN, FK_RHO0S, FK_MY4,
-               FK_GK, FK_BALLS };
+               FK_GK, FK_BALLS, FK_L1S, FK_L1B };
 
 struct FinArgs {
   int i;                 // Lanczos step (FK_OM, FK_RHO, FK_BAR)
@@ -835,6 +838,45 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
       const int j = f.i;
       sc->bin[j] = !(N > f.A.delta);
       sc->bs[j] = sc->bin[j] ? 1.0 : f.A.delta / N;
+      break;
+    }
+    case FK_L1S: {  // l1 ball: ||p - b||_1 - delta <= 0 (exact sign): p is inside (reading R35)
+      XAcc g;
+      for (int i = 0; i < kLimbs; ++i) g.d[i] = L[0][i];
+      int e = 0;
+      xacc_add(g, -f.A.delta, e);
+      const int j = f.i;
+      sc->bin[j] = !(xacc_round(g.d) > 0.0);
+      sc->bdone = sc->bin[j];
+      if (!sc->bin[j] && f.A.delta == 0.0) {  // K = {b}: theta = inf gives w = b
+        sc->bs[j] = INFINITY;
+        sc->bdone = 1;
+      }
+      sc->bk[0] = 0ull;                    // G(0) > 0
+      sc->bk[1] = 0x7fefffffffffffffull;   // G(DBL_MAX) = -delta < 0
+      break;
+    }
+    case FK_L1B: {  // one bisection step on the key of v: G(v) = S(v) - c(v) v - delta < 0 ?
+      if (sc->bdone) break;
+      const unsigned long long lo = sc->bk[0], hi = sc->bk[1], mid = lo + ((hi - lo) >> 1);
+      const double v = __longlong_as_double((long long)mid);
+      const double c = xacc_round(L[1]);
+      XAcc g;
+      for (int i = 0; i < kLimbs; ++i) g.d[i] = L[0][i];
+      XAcc sd = g;
+      int e = 0;
+      const double ph = c * v, pl = fma(c, v, -ph);  // exact product c v
+      xacc_add(g, -ph, e);
+      xacc_add(g, -pl, e);
+      xacc_add(g, -f.A.delta, e);
+      xacc_add(sd, -f.A.delta, e);
+      if (xacc_round(g.d) < 0.0) {
+        sc->bk[1] = mid;
+        sc->bs[f.i] = xacc_round(sd.d) / c;  // theta = fl(fl(S - delta) / c) of the new bracket top
+      } else {
+        sc->bk[0] = mid;
+      }
+      if (sc->bk[1] - sc->bk[0] <= 1ull) sc->bdone = 1;
       break;
     }
     case FK_RHO0S:  // k_dual_sketch without the draw: the next start vector's norm comes from FK_GEN
@@ -2062,15 +2104,19 @@ __global__ void __launch_bounds__(kBlock, 2) k_monitor(Csr C, Rows RL, const dou
 // per-block partials of g = v^T Omega (fp64, fixed tree; off the feedback path).
 // The projection onto the constraint set K of the point p = fl(z + fl(y / beta)): KS = 1 box
 // (min / max, reading R32), KS = 2 l2 ball with the scale s and the inside flag of the exact-sum
-// norm pass (k_ball_sum, reading R34).
+// norm pass (k_ball_sum, reading R34), KS = 3 l1 ball with the threshold s of the exact bisection
+// (k_l1_pass, reading R35).
 template <int KS>
 __device__ __forceinline__ double proj_k(double zr, double yr, double beta, const IterArgs &A, double s, int inside) {
   const double p = zr + yr / beta;
   if (KS == 1) return fmin(fmax(p, A.lo), A.hi);
-  return inside ? p : A.b + s * (p - A.b);
+  if (inside) return p;
+  const double e = p - A.b;
+  if (KS == 3) return A.b + copysign(fmax(fabs(e) - s, 0.0), e);  // l1: soft threshold s = theta (R35)
+  return A.b + s * e;
 }
 
-template <int KS>  // constraint set: 0 A X = b, 1 box (A.ineq), 2 l2 ball (nz in k_ball_nz)
+template <int KS>  // constraint set: 0 A X = b, 1 box (A.ineq), 2/3 l2/l1 ball (nz in k_ball_nz)
 __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__ v, double *__restrict__ z,
                                                    const double *__restrict__ y,
                                                    const double *__restrict__ Om, int nl, int R, IterArgs A,
@@ -2151,7 +2197,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
       f.R = R;
       f.A = A;
       f.log = log;
-      emit<1>(slot, sc, net, KS == 2 ? FK_GK : FK_NZ, f, gsum);
+      emit<1>(slot, sc, net, KS >= 2 ? FK_GK : FK_NZ, f, gsum);
     }
   }
 }
@@ -2160,7 +2206,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
 // ||g_{t+1}||^2 (exact) -- otherwise g_{t+1} was drawn ahead on the side stream (k_gen_start, FK_GEN)
 // and only its norm is taken over.  The sketch update of Alg. 4 line 10 is deferred (k_sketch_flush):
 // this kernel records its coefficients ck = fl(eta alpha) g_k in the ring slot js.
-template <int KS, bool GEN>  // constraint set: 0 A X = b, 1 box, 2 l2 ball (d and the gap sums in k_ball_d)
+template <int KS, bool GEN>  // constraint set: 0 A X = b, 1 box, 2/3 l2/l1 ball (d and gap sums in k_ball_d)
 __global__ void __launch_bounds__(kBlock, GEN ? 2 : 4) k_dual_sketch(const double *__restrict__ z, double *__restrict__ y,
                                                         double *__restrict__ d, const double *__restrict__ cdiag,
                                                         double *__restrict__ ckr, int js,
@@ -2169,13 +2215,13 @@ __global__ void __launch_bounds__(kBlock, GEN ? 2 : 4) k_dual_sketch(const doubl
                                                         Net net, const int *__restrict__ orig) {
   pdl_entry();
   const double gam = sc->gamma;
-  const double bs0 = KS == 2 ? sc->bs[0] : 0.0;  // l2 ball: projection of wbar_t (k_ball_sum j = 0)
-  const int bin0 = KS == 2 ? sc->bin[0] : 0;
+  const double bs0 = KS >= 2 ? sc->bs[0] : 0.0;  // balls: projection of wbar_t (j = 0)
+  const int bin0 = KS >= 2 ? sc->bin[0] : 0;
   if (blockIdx.x == 0 && (int)threadIdx.x < R)  // H = 0 (trace-bounded, xi_t >= 0): no rank-one term
     ckr[js * kMaxR + threadIdx.x] = (A.trace_le && !(sc->xi < 0.0)) ? 0.0 : (A.eta * A.alpha) * sc->gk[threadIdx.x];
   // exact sums: [GEN: ||g_{t+1}||^2,] and over the next iteration's state (y_{t+1}, z_{t+1}):
   // sum y, y.z, z.z, sum z (surrogate gap / stopping rule, finalize FK_NZ)
-  constexpr int NS = (GEN ? 1 : 0) + (KS == 2 ? 0 : 4), o = GEN ? 1 : 0;
+  constexpr int NS = (GEN ? 1 : 0) + (KS >= 2 ? 0 : 4), o = GEN ? 1 : 0;
   __shared__ XBlk<NS> xb;
   xblk_init<NS>(xb);
   XWin acc[NS];
@@ -2214,8 +2260,8 @@ __global__ void __launch_bounds__(kBlock, GEN ? 2 : 4) k_dual_sketch(const doubl
           peer |= mk[u];
           xwin_add_nn(acc[0], gv * gv, err, xb.l[0]);
         }
-        if (KS == 2) {
-          // l2 ball: d and the gap sums follow the norm pass over the new points (k_ball_d)
+        if (KS >= 2) {
+          // balls: d and the gap sums follow the projection passes over the new points (k_ball_d)
         } else if (KS == 1) {  // general template (reading R33): <y,z>, <z-w,z>, <y,w>, <z-w,z+w>, w = w_{t+1}
           const double wk = proj_k<1>(zr[u], yr, A.beta_next, A, 0.0, 0);  // (the w of e1 above)
           xwin_add(acc[o + 0], yr * zr[u], err, xb.l[o + 0]);
@@ -2234,7 +2280,7 @@ __global__ void __launch_bounds__(kBlock, GEN ? 2 : 4) k_dual_sketch(const doubl
   if (commit_and_ticket<NS>(acc, xb, slot, err, sc, net.P, peer) && threadIdx.x == 0) {
     FinArgs f{};
     f.i = (int)((A.t + 1) & 1);
-    emit<NS>(slot, sc, net, KS == 2 ? FK_RHO0 : (GEN ? FK_RHO0M : FK_RHO0S), f, nullptr);
+    emit<NS>(slot, sc, net, KS >= 2 ? FK_RHO0 : (GEN ? FK_RHO0M : FK_RHO0S), f, nullptr);
   }
 }
 
@@ -2261,8 +2307,42 @@ __global__ void __launch_bounds__(kBlock) k_ball_sum(const double *__restrict__ 
   }
 }
 
+// l1 ball (reading R35): one pass of the exact threshold search for projection j of the points
+// p = fl(z + fl(y / beta)), a = |fl(p - b)|.  Pass -1: sum a (inside test, FK_L1S).  Pass >= 0: with v
+// the value of the bracket's middle key, sum a and count over a >= v (FK_L1B: G(v) < 0 moves the top).
+// 63 passes close the bracket [0, DBL_MAX] to the least key with G < 0: the active set a >= v* is the
+// sorted top-rho set of the oracle (G decreasing in v).
+__global__ void __launch_bounds__(kBlock) k_l1_pass(const double *__restrict__ z, const double *__restrict__ y,
+                                                    double beta, int nl, IterArgs A, int j, int pass, XSlot *slot,
+                                                    DevScalars *sc, Net net) {
+  pdl_entry();
+  __shared__ XBlk<2> xb;
+  xblk_init<2>(xb);
+  XWin acc[2];
+  xwin_init(acc[0]);
+  xwin_init(acc[1]);
+  int err = 0;
+  const bool run = pass < 0 || !sc->bdone;
+  const unsigned long long mid = sc->bk[0] + ((sc->bk[1] - sc->bk[0]) >> 1);
+  if (run)
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+      const double a = fabs((z[r] + y[r] / beta) - A.b);
+      if (pass < 0 || (unsigned long long)__double_as_longlong(a) >= mid) {
+        xwin_add_nn(acc[0], a, err, xb.l[0]);
+        xwin_add_nn(acc[1], 1.0, err, xb.l[1]);
+      }
+    }
+  if (commit_and_ticket<2>(acc, xb, slot, err, sc, net.P, 0u) && threadIdx.x == 0) {
+    FinArgs f{};
+    f.i = j;
+    f.A = A;
+    emit<2>(slot, sc, net, pass < 0 ? FK_L1S : FK_L1B, f, nullptr);
+  }
+}
+
 // l2 ball: ||z_{t+1} - wbar_t||^2 (exact) -> the dual step, objective tracker and record (FK_NZ; g was
 // finalized by k_primal's FK_GK, so no g payload here).
+template <int KS>
 __global__ void __launch_bounds__(kBlock) k_ball_nz(const double *__restrict__ z, const double *__restrict__ y, int nl,
                                                     IterArgs A, XSlot *slot, DevScalars *sc, scg_iter_rec *log,
                                                     Net net) {
@@ -2275,7 +2355,7 @@ __global__ void __launch_bounds__(kBlock) k_ball_nz(const double *__restrict__ z
   xwin_init(acc[0]);
   int err = 0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
-    const double e = z[r] - proj_k<2>(z[r], y[r], A.beta_next, A, s, inside);
+    const double e = z[r] - proj_k<KS>(z[r], y[r], A.beta_next, A, s, inside);
     xwin_add_nn(acc[0], e * e, err, xb.l[0]);
   }
   if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P, 0u) && threadIdx.x == 0) {
@@ -2289,6 +2369,7 @@ __global__ void __launch_bounds__(kBlock) k_ball_nz(const double *__restrict__ z
 
 // l2 ball: d for D_{t+1} with w_{t+1} = proj_K(z_{t+1} + y_{t+1} / beta_{t+1}) and the general-template
 // gap / bound sums over the state (y_{t+1}, z_{t+1}, w_{t+1}) (reading R33); also the t = 1 setup.
+template <int KS>
 __global__ void __launch_bounds__(kBlock) k_ball_d(const double *__restrict__ z, const double *__restrict__ y,
                                                    const double *__restrict__ cdiag, double *__restrict__ d, int nl,
                                                    double beta, IterArgs A, XSlot *slot, DevScalars *sc, Net net) {
@@ -2303,7 +2384,7 @@ __global__ void __launch_bounds__(kBlock) k_ball_d(const double *__restrict__ z,
   int err = 0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
     const double zr = z[r], yr = y[r];
-    const double w = proj_k<2>(zr, yr, beta, A, s, inside);
+    const double w = proj_k<KS>(zr, yr, beta, A, s, inside);
     const double e = zr - w;
     d[r] = fma(beta, e, yr) + cdiag[r];
     xwin_add(acc[0], yr * zr, err, xb.l[0]);

@@ -153,7 +153,7 @@ struct scg_ctx {
   int world = 1, mode = 0;  // mode 0: single, 1: emulated shards, 2: one rank of a multi-process job
   bool box = false;           // constraint set K = {klo <= u <= khi} (scaled units): SCG_INEQ or sketchycgal_set_box
   double klo = 0.0, khi = 0.0;
-  bool ball = false;          // K = {||u - b|| <= delta} (sketchycgal_set_ball; box is then set too: general template)
+  int ball = 0;               // K = {||u - b|| <= delta}: 2 l2, 1 l1 (sketchycgal_set_ball[_l1]; box is set too)
   double delta = 0.0;         //   scaled units
   bool fused = false;        // one GPU: Lanczos pass 1 as one persistent kernel (SCG_FUSED_PASS1)
   unsigned long long gphase = 0;  // grid-barrier phases issued so far (fused pass 1)
@@ -1457,8 +1457,22 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
   return SCG_OK;
 }
 
-// l2 ball (reading R34): N = ||z + y / beta - b|| over all ranks -> scale / inside flag of projection j.
+// Ball projection j of the points z + y / beta over all ranks: l2 (reading R34) N = ||p - b|| -> scale and
+// inside flag; l1 (reading R35) the inside test and the 63-step exact bisection for the threshold.
 static void ball_norm(scg_ctx *c, double beta, const IterArgs &A, int j) {
+  if (c->ball == 1) {
+    for (int pass = -1; pass < 63; ++pass) {
+      const unsigned long long E = ++c->epoch;
+      for (Shard *s : c->sh)
+        launch(c, KC_OTHER, 0.0, k_l1_pass, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z,
+               (const double *)s->y, beta, (int)s->nl, A, j, pass, s->slots + SLOT_BALL, s->sc, net_of(c, s, E));
+      FinArgs f{};
+      f.i = j;
+      f.A = A;
+      pull_all(c, pass < 0 ? FK_L1S : FK_L1B, 2, E, f);
+    }
+    return;
+  }
   const unsigned long long E = ++c->epoch;
   for (Shard *s : c->sh)
     launch(c, KC_OTHER, 0.0, k_ball_sum, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z, (const double *)s->y,
@@ -1475,7 +1489,7 @@ static void ball_state(scg_ctx *c, double beta, const IterArgs &A) {
   ball_norm(c, beta, A, 1);
   const unsigned long long E = ++c->epoch;
   for (Shard *s : c->sh)
-    launch(c, KC_OTHER, 0.0, k_ball_d, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z, (const double *)s->y,
+    launch(c, KC_OTHER, 0.0, c->ball == 1 ? k_ball_d<3> : k_ball_d<2>, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z, (const double *)s->y,
            (const double *)s->cdiag, s->d, (int)s->nl, beta, A, s->slots + SLOT_BALL, s->sc, net_of(c, s, E));
   pull_all(c, FK_MY4, 4, E, FinArgs{});
 }
@@ -1678,22 +1692,22 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     }
     pull_all(c, FK_MON, 3, E, FinArgs{});
     E = ++c->epoch;
-    const int ks = c->ball ? 2 : (c->box ? 1 : 0);  // constraint set: A X = b, box, l2 ball
+    const int ks = c->ball == 2 ? 2 : c->ball == 1 ? 3 : (c->box ? 1 : 0);  // A X = b, box, l2, l1 ball
     for (Shard *s : c->sh)
-      launch(c, KC_PRIMAL, s->kb[KC_PRIMAL], ks == 2 ? k_primal<2> : (ks ? k_primal<1> : k_primal<0>),
+      launch(c, KC_PRIMAL, s->kb[KC_PRIMAL], ks >= 2 ? k_primal<2> : (ks ? k_primal<1> : k_primal<0>),
              dim3(s->grid_primal), dim3(kBlock), (const double *)c->vslot(s, js), s->z,
              (const double *)s->y, (const double *)s->Om, (int)s->nl, c->R, A, s->gpart, s->slots + SLOT_NZ, s->sc, s->dlog, net_of(c, s, E));
     {
       FinArgs f{};
       f.R = c->R;
       f.A = A;
-      pull_all(c, ks == 2 ? FK_GK : FK_NZ, 1, E, f);
+      pull_all(c, ks >= 2 ? FK_GK : FK_NZ, 1, E, f);
     }
-    if (ks == 2) {  // l2 ball (reading R34): wbar_t needs ||z_{t+1} + y_t / beta_{t+1} - b|| first
+    if (ks >= 2) {  // balls (readings R34, R35): wbar_t needs the projection pass over z_{t+1} + y_t / beta_{t+1}
       ball_norm(c, A.beta_next, A, 0);
       E = ++c->epoch;
       for (Shard *s : c->sh)
-        launch(c, KC_OTHER, 0.0, k_ball_nz, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z,
+        launch(c, KC_OTHER, 0.0, ks == 3 ? k_ball_nz<3> : k_ball_nz<2>, dim3(s->grid_rows), dim3(kBlock), (const double *)s->z,
                (const double *)s->y, (int)s->nl, A, s->slots + SLOT_BALL, s->sc, s->dlog, net_of(c, s, E));
       FinArgs f{};
       f.R = 0;  // g finalized by FK_GK
@@ -1704,14 +1718,15 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     if (c->side_rng) cudaStreamWaitEvent(c->stream, c->evB, 0);  // g_{t+1} and its norm are drawn
     for (Shard *s : c->sh) {
       auto kD = c->side_rng ? (ks == 1 ? k_dual_sketch<1, false> : k_dual_sketch<0, false>)
-                            : (ks == 2 ? k_dual_sketch<2, true> : (ks ? k_dual_sketch<1, true> : k_dual_sketch<0, true>));
+                            : (ks == 3 ? k_dual_sketch<3, true> : ks == 2 ? k_dual_sketch<2, true>
+                                         : (ks ? k_dual_sketch<1, true> : k_dual_sketch<0, true>));
       launch(c, KC_DUAL_SKETCH, c->side_rng ? 40.0 * (double)s->nl : s->kb[KC_DUAL_SKETCH], kD,
              dim3(c->side_rng ? s->grid_dual_s : s->grid_dual), dim3(kBlock),
              (const double *)s->z, s->y, s->d, (const double *)s->cdiag, s->ckr, js, c->wslot(s, 0),
              (int)s->nl, (long long)s->rb, c->R, A, c->seed, s->slots + SLOT_NU0, s->sc, net_of(c, s, E),
              (const int *)s->orig);
     }
-    if (ks == 2) {
+    if (ks >= 2) {
       pull_all(c, FK_RHO0, 1, E, FinArgs{});
       ball_state(c, A.beta_next, A);  // w_{t+1}, D_{t+1}'s diagonal and the gap / bound sums
     } else {
@@ -2108,11 +2123,11 @@ scg_status sketchycgal_set_box(scg_ctx *c, double lo, double hi) {
   return sketchycgal_synchronize(c);
 }
 
-scg_status sketchycgal_set_ball(scg_ctx *c, double delta) {
+static scg_status set_ball(scg_ctx *c, double delta, int kind) {
   if (!c || c->t != 0 || !(delta >= 0.0) || !std::isfinite(delta)) return SCG_EINVAL;
   const bool scale = (c->flags & SCG_SCALE) != 0;
   c->box = true;  // general template (gap / bound with the slack, reading R33)
-  c->ball = true;
+  c->ball = kind;
   c->delta = scale ? delta / (double)c->n : delta;  // scaled units like b = 1/n
   if (c->side_rng) {  // the ball's dual step keeps the draw of g_{t+1} in k_dual_sketch
     cudaStreamSynchronize(c->side);
@@ -2124,6 +2139,10 @@ scg_status sketchycgal_set_ball(scg_ctx *c, double delta) {
   ball_state(c, c->beta0 * std::sqrt(2.0), A);  // D_1 with w_1 = proj_K(z_1 + y_1 / beta_1)
   return sketchycgal_synchronize(c);
 }
+
+scg_status sketchycgal_set_ball(scg_ctx *c, double delta) { return set_ball(c, delta, 2); }
+
+scg_status sketchycgal_set_ball_l1(scg_ctx *c, double delta) { return set_ball(c, delta, 1); }
 
 scg_status sketchycgal_objective(scg_ctx *c, double out[2]) {
   if (!c || !out) return SCG_EINVAL;

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared():
     src = open(os.path.join(ROOT, "include", "sketchycgal.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(sketchycgal_[a-zA-Z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(sketchycgal_\w+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():

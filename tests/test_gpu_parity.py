@@ -562,29 +562,35 @@ def test_box_constraint_set_bitwise(gpu, graph, box, shards):
     assert h.lib.sketchycgal_set_box(h._h, float("nan"), 1.0) != 0
 
 
+@pytest.mark.parametrize("norm", ["l2", "l1"])
 @pytest.mark.parametrize("graph,delta,shards", [("c0", 3.0, 1), ("c0", 3.0, 3), ("c0", 200.0, 1), ("c5", 0.4, 1),
                                                 ("c5", 0.0, 2)])
-def test_l2_ball_constraint_set_bitwise(gpu, graph, delta, shards):
-    """l2 ball K = {||u - 1|| <= delta} through sketchycgal_set_ball (reading R34): the
-    projection scale is an exact-sum norm over all shards, so every iterate is bitwise equal to the
-    oracle's -- with the projection active (small delta), mostly inactive (delta = 200 on c0), and
-    delta = 0 (the projection is then exactly b).  The setter refuses negative / NaN delta and calls
+def test_ball_constraint_sets_bitwise(gpu, graph, delta, shards, norm):
+    """l2 / l1 balls K = {||u - 1|| <= delta} through sketchycgal_set_ball / _set_ball_l1 (P:3915-3918,
+    readings R34, R35): the l2 scale is an exact-sum norm over all shards and the l1 threshold comes
+    from an exact bisection over all shards, so every iterate is bitwise equal to the oracle's (which
+    sorts) -- with the projection active (small delta), mostly inactive (delta = 200 on c0), and
+    delta = 0 (the projection is then exactly b).  The setters refuse negative / NaN delta and calls
     after the first step."""
     if graph == "c5":
         n = 5
         i = np.arange(n)
         L = si.laplacian_from_edges(n, i, (i + 1) % n, np.ones(n))
-        R, seed, T = 3, 5, 400
+        R, seed, T = 3, 5, 400 if norm == "l2" else 150
     else:
         L = si.laplacian(graph)
-        R, seed, T = 10, 0, 200
-    alpha = 1.05 * L.n * (1 + delta / np.sqrt(L.n))
-    g = gpu.SketchyCGAL(L, R=R, seed=seed, alpha=alpha, trace_le=True, ball=delta, shards=shards)
+        R, seed, T = 10, 0, 200 if norm == "l2" else 60
+    r = np.sqrt(L.n) if norm == "l2" else L.n
+    alpha = 1.05 * L.n * (1 + delta / r)
+    kw = {"ball": delta} if norm == "l2" else {"l1_ball": delta}
+    g = gpu.SketchyCGAL(L, R=R, seed=seed, alpha=alpha, trace_le=True, shards=shards, **kw)
     g.step(T)
-    o = oracle.Oracle(L, R, seed=seed, alpha=alpha, logcap=T, trace_le=True, ball=delta)
+    o = oracle.Oracle(L, R, seed=seed, alpha=alpha, logcap=T, trace_le=True, **kw)
     o.step(T)
     _assert_trajectory(g, o, T)
-    assert g.lib.sketchycgal_set_ball(g._h, 1.0) != 0  # after the first step
+    setter = g.lib.sketchycgal_set_ball if norm == "l2" else g.lib.sketchycgal_set_ball_l1
+    assert setter(g._h, 1.0) != 0  # after the first step
     h = gpu.SketchyCGAL(L, R=R, seed=seed)
-    assert h.lib.sketchycgal_set_ball(h._h, -1.0) != 0
-    assert h.lib.sketchycgal_set_ball(h._h, float("nan")) != 0
+    setter = h.lib.sketchycgal_set_ball if norm == "l2" else h.lib.sketchycgal_set_ball_l1
+    assert setter(h._h, -1.0) != 0
+    assert setter(h._h, float("nan")) != 0
