@@ -185,7 +185,11 @@ constexpr int kMinBlocksUni = 3;  // min blocks per SM of the uniform-weight SEL
 // min blocks per SM of the ELL SpMV kernels: 64-register cap up to W = 4, wider rows need more stage registers
 // (a deeper pipeline -- gathers two slices ahead, 78 registers, 3 blocks/SM -- measured 171 us against
 // 140 us on configs[3]: the fourth block per SM is worth more than the extra slack)
-constexpr int ell_min_blocks(int W, bool uni) { return W <= 4 ? 4 : (uni ? 3 : 2); }
+constexpr int ell_min_blocks(int W, bool uni) { return (W & 15) <= 4 ? 4 : (uni ? 3 : 2); }
+// ELL width code: W & 15 = slots per row; kEllNeg set = every coefficient is -m0 (uniform weights,
+// every stored off-diagonal of C~ negative -- the unit-weight MaxCut Laplacian): the layout then
+// carries no sign bits and the SpMV no sign handling
+constexpr int kEllNeg = 32;
 constexpr int kLongRow = 32;
 constexpr int kHeavyRow = 1024;  // rows with more entries are "heavy": a block each (256 strided chains)
 
@@ -206,9 +210,10 @@ struct Rows {
   unsigned *work;       // non-null: dynamic slice distribution (chunks of kDynCh slices from this
                         // counter; zeroed again by the kernel's last block) -- skewed graphs
   // ELL-W layout (graphs whose rows all have <= kEllMax entries: no long rows, no slice metadata):
-  // slice s = rows 32 s .. 32 s + 31, slot j of lane l at ecol[(32 s) W + 32 j + l]; rows shorter
+  // slice s = rows 32 s .. 32 s + 31, slot j of lane l at ecol[(32 s) W + 32 j + l] (W = 2, 4:
+  // at ecol[(32 s) W + W l + j], one vector load per lane); rows shorter
   // than W are padded with the dummy column n (gathered value +0, negative coefficient)
-  const int *ecol;      // column | 0x80000000 for a negative uniform value
+  const int *ecol;      // column | 0x80000000 for a negative uniform value (no sign bits: kEllNeg)
   const double *eval;   // per-slot values, or nullptr when all |C_rj| equal m0
   int padc;             // the padding code
 };
@@ -586,18 +591,24 @@ __device__ __forceinline__ int seg_shift(long long i0) { return (int)(((i0 * ES)
 // its columns are dead; only their sign bits (uniform weights) travel on, packed in one word.
 // Per row the arithmetic is the CAC-3 single chain (every row has <= 32 entries, reading R27);
 // padding slots add fma(-m, +0, acc) == acc.
+template <bool MASK>
 __device__ __forceinline__ const double *gaddr(const double *X, int c) {
-  // X + (c & 0x7fffffff) as one 32x32->64 multiply-add (the compiler otherwise builds the 64-bit
-  // offset with six integer instructions)
+  // X + c (sign bit masked off) as one 32x32->64 multiply-add (a shift pair in SASS; the compiler
+  // otherwise builds the 64-bit offset with six integer instructions)
   const double *p;
-  asm("mad.wide.u32 %0, %1, 8, %2;" : "=l"(p) : "r"((unsigned)c & 0x7fffffffu), "l"(X));
+  asm("mad.wide.u32 %0, %1, 8, %2;" : "=l"(p) : "r"(MASK ? (unsigned)c & 0x7fffffffu : (unsigned)c), "l"(X));
   return p;
 }
 
-template <int NC, bool UNI, int W, class Epi>
+template <int NC, bool UNI, int WC, class Epi>
 __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restrict__ X, double den,
                                          const double *__restrict__ diag0, const double *__restrict__ diag1,
                                          long long rb, int nl, Epi &epi) {
+  constexpr int W = WC & 15;
+  constexpr bool NEG = UNI && (WC & kEllNeg) != 0;  // every coefficient -m0, no sign bits
+  constexpr bool SGN = UNI && !NEG;                 // uniform magnitude, sign in bit 31 of the column
+  // W = 2, 4: lane-major slots (lane l's W columns / values contiguous: one vector load each)
+  constexpr bool VEC = W == 2 || W == 4;
   const int lane = threadIdx.x & 31;
   const double rden = 1.0 / den;
   const int nsl = (nl + 31) >> 5;
@@ -605,15 +616,23 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
   const int s_end = min(nsl, ((int)blockIdx.x + 1) * per);
   const int wstep = blockDim.x >> 5;
   int sl = (int)blockIdx.x * per + (threadIdx.x >> 5);
-  const int *__restrict__ ec = RL.ecol + lane;
-  const double *__restrict__ ev = RL.eval + lane;
-  const int padc = RL.padc;
-  const double m0 = RL.m0;
+  const int *__restrict__ ec = RL.ecol + (VEC ? W * lane : lane);
+  const double *__restrict__ ev = RL.eval + (VEC ? W * lane : lane);
+  const int padc = NEG ? (int)((unsigned)RL.padc & 0x7fffffffu) : RL.padc;
+  const double m0 = NEG ? -RL.m0 : RL.m0;
   auto cload = [&](int q, int (&c)[W]) {
     if (q < s_end) {
       const int *cp = ec + (long long)q * (32 * W);
+      if constexpr (W == 4) {
+        const int4 v = __ldg(reinterpret_cast<const int4 *>(cp));
+        c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w;
+      } else if constexpr (W == 2) {
+        const int2 v = __ldg(reinterpret_cast<const int2 *>(cp));
+        c[0] = v.x; c[1] = v.y;
+      } else {
 #pragma unroll
-      for (int u = 0; u < W; ++u) c[u] = __ldg(cp + 32 * u);
+        for (int u = 0; u < W; ++u) c[u] = __ldg(cp + 32 * u);
+      }
     } else {
 #pragma unroll
       for (int u = 0; u < W; ++u) c[u] = padc;
@@ -625,13 +644,23 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
     unsigned sg = 0u;
 #pragma unroll
     for (int u = 0; u < W; ++u) {
-      g[u] = __ldg(gaddr(X, c[u]));
-      if (UNI) sg |= ((unsigned)c[u] >> 31) << u;
+      g[u] = __ldg(gaddr<SGN>(X, c[u]));
+      if (SGN) sg |= ((unsigned)c[u] >> 31) << u;
     }
     if (!UNI) {
       const double *vp = ev + (long long)q * (32 * W);
+      if constexpr (VEC) {
 #pragma unroll
-      for (int u = 0; u < W; ++u) v[u] = q < s_end ? __ldg(vp + 32 * u) : -0.0;
+        for (int u = 0; u < W; u += 2) {
+          double2 t = make_double2(-0.0, -0.0);
+          if (q < s_end) t = __ldg(reinterpret_cast<const double2 *>(vp + u));
+          v[u] = t.x;
+          v[u + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < W; ++u) v[u] = q < s_end ? __ldg(vp + 32 * u) : -0.0;
+      }
     }
     return sg;
   };
@@ -659,6 +688,9 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
   cload(sl + wstep, cb);
   oload(sl + wstep, xo1, d01, d11);
   cload(sl + 2 * wstep, cc);
+  // not unrolled: unrolling by 2 / 3 / 6 kept most register moves and measured 7-19 % slower on
+  // configs[3] (gpurun_out/r3a)
+#pragma unroll 1
   for (; sl < s_end; sl += wstep) {
     double g1[W], v1[W];
     const unsigned s1 = gload(sl + wstep, cb, g1, v1);  // gathers of slice i+1
@@ -678,8 +710,8 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
       double x = g0[u] * rden;
       if (UNI) {
         // fma(-m0, x, acc) == fma(m0, -x, acc) exactly: the coefficient's sign is moved onto x
-        // with one XOR of its high word
-        x = __hiloint2double(__double2hiint(x) ^ (int)(((s0 >> u) & 1u) << 31), __double2loint(x));
+        // with one XOR of its high word (NEG: m0 carries the common sign)
+        if (SGN) x = __hiloint2double(__double2hiint(x) ^ (int)(((s0 >> u) & 1u) << 31), __double2loint(x));
 #pragma unroll
         for (int t = 0; t < NC; ++t) o.s[t] = fma(m0, x, o.s[t]);
       } else {
@@ -706,7 +738,7 @@ template <int NC, bool UNI, int W, class Epi>
 __device__ __forceinline__ void spmv_any(const Csr &C, const Rows &RL, const double *__restrict__ X, double den,
                                          const double *__restrict__ diag0, const double *__restrict__ diag1,
                                          long long rb, int nl, Epi &epi) {
-  if constexpr (W > 0) spmv_ell<NC, UNI, W>(RL, X, den, diag0, diag1, rb, nl, epi);
+  if constexpr (W > 0) spmv_ell<NC, UNI, W>(RL, X, den, diag0, diag1, rb, nl, epi);  // W: width code
   else spmv_rows<NC, UNI>(C, RL, X, den, diag0, diag1, rb, nl, epi);
 }
 

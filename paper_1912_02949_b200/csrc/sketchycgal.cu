@@ -421,13 +421,18 @@ Rows rows_of(const Shard *s, bool dyn = false) {
 // not, and the ELL width (0: SELL + long rows).
 constexpr int kEllWidths[] = {2, 3, 4, 6, 8};
 // the resident cluster kernel exists for SELL (0) and ELL-3 / ELL-4; other widths use its SELL form
-#define SCG_RES_W(W) (((W) == 3 || (W) == 4) ? (W) : 0)
+#define SCG_RES_W(W) (((W) == 3 || (W) == 4 || (W) == (3 | kEllNeg) || (W) == (4 | kEllNeg)) ? (W) : 0)
 #define SCG_PICK_RES(U, W)                                                                          \
   (SCG_RES_W(W) == 3 ? ((U) ? k_resident<true, 3> : k_resident<false, 3>)                           \
    : SCG_RES_W(W) == 4 ? ((U) ? k_resident<true, 4> : k_resident<false, 4>)                         \
+   : SCG_RES_W(W) == (3 | kEllNeg) ? k_resident<true, 3 | kEllNeg>                                  \
+   : SCG_RES_W(W) == (4 | kEllNeg) ? k_resident<true, 4 | kEllNeg>                                  \
                        : ((U) ? k_resident<true, 0> : k_resident<false, 0>))
+// W: ELL width code (kernels.cuh kEllNeg); the sign-free codes exist for uniform weights only
 #define SCG_PICK(K, U, W)                                          \
-  ((W) == 2   ? ((U) ? K<true, 2> : K<false, 2>)                   \
+  ((W) == (3 | kEllNeg) ? K<true, 3 | kEllNeg>                      \
+   : (W) == (4 | kEllNeg) ? K<true, 4 | kEllNeg>                    \
+   : (W) == 2   ? ((U) ? K<true, 2> : K<false, 2>)                 \
    : (W) == 3 ? ((U) ? K<true, 3> : K<false, 3>)                   \
    : (W) == 4 ? ((U) ? K<true, 4> : K<false, 4>)                   \
    : (W) == 6 ? ((U) ? K<true, 6> : K<false, 6>)                   \
@@ -900,7 +905,8 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
         for (int j = 0; j < W; ++j)
           for (int l = 0; l < 32; ++l) {
             const int64_t r = q * 32 + l;
-            const size_t slot = (size_t)q * 32 * W + (size_t)j * 32 + l;
+            // W = 2, 4: lane-major (lane l's slots contiguous, one vector load in spmv_ell)
+            const size_t slot = (size_t)q * 32 * W + ((W == 2 || W == 4) ? (size_t)l * W + j : (size_t)j * 32 + l);
             const int e = r < nl ? h_rp[(size_t)r] + j : -1;
             if (e >= 0 && e < h_rp[(size_t)r + 1]) {
               ecol[slot] = enc(e);
@@ -910,12 +916,23 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
               if (!uni) eval[slot] = -0.0;
             }
           }
+      // every slot's coefficient negative (uniform unit-weight Laplacians, padding included): drop the
+      // sign bits, the kernels take -m0 as the one coefficient (kEllNeg)
+      int allneg = uni && (W == 3 || W == 4) ? 1 : 0;
+      if (allneg) {
+#pragma omp parallel for schedule(static, 65536) reduction(& : allneg)
+        for (size_t k = 0; k < ne; ++k) allneg &= (int)((unsigned)ecol[k] >> 31);
+      }
+      if (allneg) {
+#pragma omp parallel for schedule(static, 65536)
+        for (size_t k = 0; k < ne; ++k) ecol[k] = (int)((unsigned)ecol[k] & 0x7fffffffu);
+      }
       if (!alloc((void **)&s->ell_col, sizeof(int) * ne) || (!uni && !alloc((void **)&s->ell_val, sizeof(double) * ne)))
         return fail(c, SCG_ENOMEM, "ELL layout");
       CK(cudaMemcpyAsync(s->ell_col, ecol.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
       if (!uni) CK(cudaMemcpyAsync(s->ell_val, eval.data(), sizeof(double) * ne, cudaMemcpyHostToDevice, st));
       CK(cudaStreamSynchronize(st));
-      s->ellw = W;
+      s->ellw = allneg ? (W | kEllNeg) : W;
     }
     // algorithmic matrix bytes: one column index (+ value unless uniform) per stored entry --
     // independent of the layout's padding and metadata

@@ -107,7 +107,32 @@ __device__ __forceinline__ bool xs_split(double p, int &q, long long &s0, long l
 
 // The window covers the digit classes qa, qa+1, qa+2, centred on the class of
 // the thread's first summand (magnitudes straddling a class boundary stay fast).
+// Normal summands (the fast path): the signed 54-bit mantissa M (two's complement) shifted by r
+// is split as d0 + d1 2^32 + d2 2^64 with d0, d1 unsigned and d2 signed -- no per-digit negation.
 __device__ __forceinline__ void xwin_add(XWin &a, double p, int &err, long long *blk) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(p);
+  const int e = (int)((b >> 52) & 0x7ffull);
+  if ((unsigned)(e - (1075 + kLsbExp)) < (unsigned)(1123 - (1075 + kLsbExp))) {  // no Q truncation, in range
+    const unsigned long long m = (b & 0x000fffffffffffffull) | 0x0010000000000000ull;
+    const long long ms = (long long)b < 0 ? -(long long)m : (long long)m;
+    const int s = e - (1075 + kLsbExp);
+    const int q = s >> 5, r = s & 31;
+    const unsigned lo = (unsigned)ms, hi = (unsigned)((unsigned long long)ms >> 32);
+    const long long d0 = (long long)(lo << r);
+    const long long d1 = (long long)__funnelshift_l(lo, hi, r);
+    const long long d2 = (long long)(int)__funnelshift_l(hi, (unsigned)((int)hi >> 31), r);
+    if (a.qa < 0) a.qa = q < 1 ? 0 : (q > 6 ? 5 : q - 1);
+    const int d = q - a.qa;
+    if (d == 0) { a.w0 += d0; a.w1 += d1; a.w2 += d2; }
+    else if (d == 1) { a.w1 += d0; a.w2 += d1; a.w3 += d2; }
+    else if (d == 2) { a.w2 += d0; a.w3 += d1; a.w4 += d2; }
+    else {
+      atomicAdd(reinterpret_cast<unsigned long long *>(&blk[q]), (unsigned long long)d0);
+      atomicAdd(reinterpret_cast<unsigned long long *>(&blk[q + 1]), (unsigned long long)d1);
+      atomicAdd(reinterpret_cast<unsigned long long *>(&blk[q + 2]), (unsigned long long)d2);
+    }
+    return;
+  }
   int q;
   long long s0, s1, s2;
   if (!xs_split(p, q, s0, s1, s2, err)) return;
