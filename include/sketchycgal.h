@@ -331,6 +331,14 @@ scg_status sketchycgal_nccl_unique_id(void *out128);
  * hardware IEEE division on n pseudo-random operand pairs; *mismatches = count. */
 scg_status sketchycgal_selftest_division(int32_t device, int64_t n, uint64_t seed, int64_t *mismatches);
 
+/* Exact-sum self-test (CAC-2): the n host values are copied to the device and
+ * summed by a grid x block launch of the kernels' per-thread exact accumulators (fast fp64 bins,
+ * spills, slow path, block and grid commits); *sum = xsum(values) rounded once, *range_error = 1 if
+ * a value was non-finite or >= 2^100 in magnitude.  block a multiple of 32 in [32, 1024], grid >= 1.
+ * Test access only (no context). */
+scg_status sketchycgal_selftest_xsum(int32_t device, const double *values, int64_t n, int32_t grid, int32_t block,
+                                     double *sum, int32_t *range_error);
+
 const char *sketchycgal_last_error(const scg_ctx *c);
 void sketchycgal_destroy(scg_ctx *c);
 

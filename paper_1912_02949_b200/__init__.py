@@ -161,7 +161,7 @@ EXPORTS = ["sketchycgal_maxcut_init", "sketchycgal_step", "sketchycgal_synchroni
            "sketchycgal_get_state", "sketchycgal_apply_D", "sketchycgal_iterations", "sketchycgal_launch_count",
            "sketchycgal_kernel_stats", "sketchycgal_reset_stats", "sketchycgal_nccl_unique_id",
            "sketchycgal_row_splits", "sketchycgal_halo_plan", "sketchycgal_run",
-           "sketchycgal_selftest_division", "sketchycgal_last_error", "sketchycgal_destroy",
+           "sketchycgal_selftest_division", "sketchycgal_selftest_xsum", "sketchycgal_last_error", "sketchycgal_destroy",
            "sketchycgal_maxcut_alpha_doubling", "sketchycgal_set_box", "sketchycgal_set_ball", "sketchycgal_set_ball_l1",
            "sketchycgal_set_lanczos_q"]
 
@@ -210,6 +210,8 @@ def open_library(path: str = LIB_PATH):
     lib.sketchycgal_halo_plan.argtypes = [P, P, I64, I64, P, I32, P]
     lib.sketchycgal_selftest_division.restype = ctypes.c_int
     lib.sketchycgal_selftest_division.argtypes = [I32, I64, ctypes.c_uint64, ctypes.POINTER(I64)]
+    lib.sketchycgal_selftest_xsum.restype = ctypes.c_int
+    lib.sketchycgal_selftest_xsum.argtypes = [I32, P, I64, I32, I32, ctypes.POINTER(D), ctypes.POINTER(I32)]
     lib.sketchycgal_last_error.restype = ctypes.c_char_p
     lib.sketchycgal_last_error.argtypes = [P]
     lib.sketchycgal_destroy.restype = None
@@ -270,6 +272,17 @@ def selftest_division(n: int = 1 << 26, seed: int = 1, device: int = 0) -> int:
     if st != 0:
         raise ScgError(f"selftest: {STATUS.get(st, st)}")
     return int(out.value)
+
+
+def selftest_xsum(values, grid: int = 64, block: int = 256, device: int = 0):
+    """(xsum(values) rounded once, range error flag) from the device's per-thread exact accumulators."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    out, rerr = ctypes.c_double(0.0), ctypes.c_int32(0)
+    st = load().sketchycgal_selftest_xsum(int(device), v.ctypes.data, int(v.size), int(grid), int(block),
+                                          ctypes.byref(out), ctypes.byref(rerr))
+    if st != 0:
+        raise ScgError(f"selftest_xsum: {STATUS.get(st, st)}")
+    return float(out.value), int(rerr.value)
 
 
 def _c64(a, dt):

@@ -186,10 +186,10 @@ constexpr int kMinBlocksUni = 3;  // min blocks per SM of the uniform-weight SEL
 // (a deeper pipeline -- gathers two slices ahead, 78 registers, 3 blocks/SM -- measured 171 us against
 // 140 us on configs[3]: the fourth block per SM is worth more than the extra slack)
 constexpr int ell_min_blocks(int W, bool uni) { return (W & 15) <= 4 ? 4 : (uni ? 3 : 2); }
-// ELL width code: W & 15 = slots per row; kEllNeg set = every coefficient is -m0 (uniform weights,
-// every stored off-diagonal of C~ negative -- the unit-weight MaxCut Laplacian): the layout then
-// carries no sign bits and the SpMV no sign handling
-constexpr int kEllNeg = 32;
+// ELL width code: W & 15 = slots per row; kEllPos set = every coefficient is +m0 (uniform positive
+// weights -- C~ = -L / ||L|| has the positive off-diagonals w / ||L|| -- padding included): the layout
+// then carries no sign bits and the SpMV no sign handling
+constexpr int kEllPos = 32;
 constexpr int kLongRow = 32;
 constexpr int kHeavyRow = 1024;  // rows with more entries are "heavy": a block each (256 strided chains)
 
@@ -212,8 +212,9 @@ struct Rows {
   // ELL-W layout (graphs whose rows all have <= kEllMax entries: no long rows, no slice metadata):
   // slice s = rows 32 s .. 32 s + 31, slot j of lane l at ecol[(32 s) W + 32 j + l] (W = 2, 4:
   // at ecol[(32 s) W + W l + j], one vector load per lane); rows shorter
-  // than W are padded with the dummy column n (gathered value +0, negative coefficient)
-  const int *ecol;      // column | 0x80000000 for a negative uniform value (no sign bits: kEllNeg)
+  // than W are padded with the dummy column n (gathered value -0, coefficient +m0 or value +0: the
+  // product is -0 and fma(., ., acc) == acc for every acc, -0 included)
+  const int *ecol;      // column | 0x80000000 for a negative uniform value (no sign bits: kEllPos)
   const double *eval;   // per-slot values, or nullptr when all |C_rj| equal m0
   int padc;             // the padding code
 };
@@ -429,7 +430,7 @@ __device__ __forceinline__ void spmv_rows(const Csr &C, const Rows &RL, const do
       for (int u = 0; u < 4; ++u) vv[u] = w > u ? __ldg(vp + 32 * u) : 0.0;
     }
   };
-  // padding slots hold the dummy column n (gathered value +0, negative coefficient): no test
+  // padding slots hold the dummy column n (gathered value -0, positive coefficient): no test
   auto gload = [&](int2 m, const int (&cv)[4], double (&gv)[4]) {
     switch (m.y & 0xff) {
       case 0: break;
@@ -600,28 +601,28 @@ __device__ __forceinline__ const double *gaddr(const double *X, int c) {
   return p;
 }
 
-template <int NC, bool UNI, int WC, class Epi>
-__device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restrict__ X, double den,
-                                         const double *__restrict__ diag0, const double *__restrict__ diag1,
-                                         long long rb, int nl, Epi &epi) {
-  constexpr int W = WC & 15;
-  constexpr bool NEG = UNI && (WC & kEllNeg) != 0;  // every coefficient -m0, no sign bits
-  constexpr bool SGN = UNI && !NEG;                 // uniform magnitude, sign in bit 31 of the column
-  // W = 2, 4: lane-major slots (lane l's W columns / values contiguous: one vector load each)
+// One warp-pipelined pass of the fixed-width engine over the slice positions [q0, q1) of this block:
+// slice q has its W slots at ec0 + q 32 W (lane-major for W = 2, 4, else slot-major) and its rows at
+// 32 q + lane.  (Tried and reverted on configs[3], where ELL-4 pads 40 % of the slots: slices
+// grouped in equal-width classes, each class through its own fixed-width run -- 30 % fewer column
+// bytes but the gathers lost their locality: DRAM read 566 -> 698 MB, 126 -> 174 us, gpurun_out/r3j;
+// a per-slice width inside one run: more instructions than bytes saved, 126 -> 145 us, r3i; 16-bit
+// column codes relative to the row with escaped far rows: DRAM read 566 -> 428 MB but a longer
+// decode -> address -> gather chain, 126 -> 157 us, r3m.)
+template <int NC, bool UNI, bool POS, int W, class Epi>
+__device__ __forceinline__ void ell_run(const double *__restrict__ X, double rden, const double *__restrict__ diag0,
+                                        const double *__restrict__ diag1, long long rb, int nl,
+                                        const int *__restrict__ ec0, const double *__restrict__ ev0, int q0,
+                                        int q1, int padc, double m0, Epi &epi) {
+  constexpr bool SGN = UNI && !POS;  // uniform magnitude, sign in bit 31 of the column
   constexpr bool VEC = W == 2 || W == 4;
   const int lane = threadIdx.x & 31;
-  const double rden = 1.0 / den;
-  const int nsl = (nl + 31) >> 5;
-  const int per = (nsl + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int s_end = min(nsl, ((int)blockIdx.x + 1) * per);
   const int wstep = blockDim.x >> 5;
-  int sl = (int)blockIdx.x * per + (threadIdx.x >> 5);
-  const int *__restrict__ ec = RL.ecol + (VEC ? W * lane : lane);
-  const double *__restrict__ ev = RL.eval + (VEC ? W * lane : lane);
-  const int padc = NEG ? (int)((unsigned)RL.padc & 0x7fffffffu) : RL.padc;
-  const double m0 = NEG ? -RL.m0 : RL.m0;
+  int sl = q0 + (int)(threadIdx.x >> 5);
+  const int *__restrict__ ec = ec0 + (VEC ? W * lane : lane);
+  const double *__restrict__ ev = ev0 + (VEC ? W * lane : lane);
   auto cload = [&](int q, int (&c)[W]) {
-    if (q < s_end) {
+    if (q < q1) {
       const int *cp = ec + (long long)q * (32 * W);
       if constexpr (W == 4) {
         const int4 v = __ldg(reinterpret_cast<const int4 *>(cp));
@@ -652,14 +653,14 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
       if constexpr (VEC) {
 #pragma unroll
         for (int u = 0; u < W; u += 2) {
-          double2 t = make_double2(-0.0, -0.0);
-          if (q < s_end) t = __ldg(reinterpret_cast<const double2 *>(vp + u));
+          double2 t = make_double2(0.0, 0.0);
+          if (q < q1) t = __ldg(reinterpret_cast<const double2 *>(vp + u));
           v[u] = t.x;
           v[u + 1] = t.y;
         }
       } else {
 #pragma unroll
-        for (int u = 0; u < W; ++u) v[u] = q < s_end ? __ldg(vp + 32 * u) : -0.0;
+        for (int u = 0; u < W; ++u) v[u] = q < q1 ? __ldg(vp + 32 * u) : 0.0;
       }
     }
     return sg;
@@ -669,7 +670,7 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
     xo = 0.0;
     dd0 = 0.0;
     dd1 = 0.0;
-    if (q < s_end && p < nl) {
+    if (q < q1 && p < nl) {
       xo = X[rb + p];
       dd0 = diag0[p];
       if (NC > 1) dd1 = diag1[p];
@@ -691,7 +692,7 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
   // not unrolled: unrolling by 2 / 3 / 6 kept most register moves and measured 7-19 % slower on
   // configs[3] (gpurun_out/r3a)
 #pragma unroll 1
-  for (; sl < s_end; sl += wstep) {
+  for (; sl < q1; sl += wstep) {
     double g1[W], v1[W];
     const unsigned s1 = gload(sl + wstep, cb, g1, v1);  // gathers of slice i+1
     int cd[W];
@@ -710,7 +711,7 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
       double x = g0[u] * rden;
       if (UNI) {
         // fma(-m0, x, acc) == fma(m0, -x, acc) exactly: the coefficient's sign is moved onto x
-        // with one XOR of its high word (NEG: m0 carries the common sign)
+        // with one XOR of its high word (POS: no negative coefficient)
         if (SGN) x = __hiloint2double(__double2hiint(x) ^ (int)(((s0 >> u) & 1u) << 31), __double2loint(x));
 #pragma unroll
         for (int t = 0; t < NC; ++t) o.s[t] = fma(m0, x, o.s[t]);
@@ -731,6 +732,20 @@ __device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restric
     xo0 = xo1; d00 = d01; d10 = d11;
     xo1 = xo2; d01 = d02; d11 = d12;
   }
+}
+
+// ELL SpMV (width code W): the block's share of the slices in row order through the fixed-width engine.
+template <int NC, bool UNI, int WC, class Epi>
+__device__ __forceinline__ void spmv_ell(const Rows &RL, const double *__restrict__ X, double den,
+                                         const double *__restrict__ diag0, const double *__restrict__ diag1,
+                                         long long rb, int nl, Epi &epi) {
+  constexpr int W = WC & 15;
+  constexpr bool POS = UNI && (WC & kEllPos) != 0;  // every coefficient +m0, no sign bits
+  const int G = (int)gridDim.x, b = (int)blockIdx.x;
+  const int nsl = (nl + 31) >> 5;
+  const int per = (nsl + G - 1) / G;
+  ell_run<NC, UNI, POS, W>(X, 1.0 / den, diag0, diag1, rb, nl, RL.ecol, RL.eval, b * per, min(nsl, (b + 1) * per),
+                           RL.padc, RL.m0, epi);
 }
 
 // SpMV dispatch: ELL-W when the layout has one (W > 0), else SELL + long rows.
@@ -2602,6 +2617,24 @@ __global__ void k_unperm(double *__restrict__ out, const double *__restrict__ in
 
 // Self-test: div_rn against the hardware IEEE division on pseudo-random operands
 // (mantissas drawn uniformly, including the extremes 1 and 2 - ulp), exponents in +-60.
+// Exact-sum self-test (sketchycgal_selftest_xsum): the n values through the kernels' per-thread
+// accumulators (xwin_add, spills, flush, block and grid commits) and the final rounding.
+__global__ void k_selftest_xsum(const double *__restrict__ v, long long n, XSlot *slot, DevScalars *sc,
+                                double *out) {
+  __shared__ XBlk<1> xb;
+  xblk_init<1>(xb);
+  XWin acc[1];
+  xwin_init(acc[0]);
+  int err = 0;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    xwin_add(acc[0], v[k], err, xb.l[0]);
+  if (commit_and_ticket<1>(acc, xb, slot, err, sc, 1, 0u) && threadIdx.x == 0) {
+    long long L[kLimbs];
+    for (int i = 0; i < kLimbs; ++i) L[i] = __ldcg(&slot->limbs[0][i]);
+    *out = xacc_round(L);
+  }
+}
+
 __global__ void k_selftest_div(long long n, uint64_t seed, unsigned long long *mismatch) {
   pdl_entry();
   unsigned long long bad = 0;

@@ -421,17 +421,17 @@ Rows rows_of(const Shard *s, bool dyn = false) {
 // not, and the ELL width (0: SELL + long rows).
 constexpr int kEllWidths[] = {2, 3, 4, 6, 8};
 // the resident cluster kernel exists for SELL (0) and ELL-3 / ELL-4; other widths use its SELL form
-#define SCG_RES_W(W) (((W) == 3 || (W) == 4 || (W) == (3 | kEllNeg) || (W) == (4 | kEllNeg)) ? (W) : 0)
+#define SCG_RES_W(W) (((W) == 3 || (W) == 4 || (W) == (3 | kEllPos) || (W) == (4 | kEllPos)) ? (W) : 0)
 #define SCG_PICK_RES(U, W)                                                                          \
   (SCG_RES_W(W) == 3 ? ((U) ? k_resident<true, 3> : k_resident<false, 3>)                           \
    : SCG_RES_W(W) == 4 ? ((U) ? k_resident<true, 4> : k_resident<false, 4>)                         \
-   : SCG_RES_W(W) == (3 | kEllNeg) ? k_resident<true, 3 | kEllNeg>                                  \
-   : SCG_RES_W(W) == (4 | kEllNeg) ? k_resident<true, 4 | kEllNeg>                                  \
+   : SCG_RES_W(W) == (3 | kEllPos) ? k_resident<true, 3 | kEllPos>                                  \
+   : SCG_RES_W(W) == (4 | kEllPos) ? k_resident<true, 4 | kEllPos>                                  \
                        : ((U) ? k_resident<true, 0> : k_resident<false, 0>))
-// W: ELL width code (kernels.cuh kEllNeg); the sign-free codes exist for uniform weights only
+// W: ELL width code (kernels.cuh kEllPos); the sign-free codes exist for uniform weights only
 #define SCG_PICK(K, U, W)                                          \
-  ((W) == (3 | kEllNeg) ? K<true, 3 | kEllNeg>                      \
-   : (W) == (4 | kEllNeg) ? K<true, 4 | kEllNeg>                    \
+  ((W) == (3 | kEllPos) ? K<true, 3 | kEllPos>                      \
+   : (W) == (4 | kEllPos) ? K<true, 4 | kEllPos>                    \
    : (W) == 2   ? ((U) ? K<true, 2> : K<false, 2>)                 \
    : (W) == 3 ? ((U) ? K<true, 3> : K<false, 3>)                   \
    : (W) == 4 ? ((U) ? K<true, 4> : K<false, 4>)                   \
@@ -849,10 +849,10 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
       if (slots >= (size_t)INT32_MAX) return fail(c, SCG_EINVAL, "SELL layout too large");
     }
     // padding slots (rows shorter than their slice, long-row lanes) point at the dummy column n,
-    // whose gathered value is +0 in every gathered vector (zeroed slack), with a negative
-    // coefficient: fma(-m, +0, acc) == acc exactly for every acc (also +-0), so the kernel needs
-    // no per-slot padding test.
-    const int padc = uni ? (int)((unsigned)c->n | 0x80000000u) : (int)c->n;
+    // whose gathered value is -0 in every gathered vector (set_pad_zero), with a positive
+    // coefficient (+m0, or the value +0): the product is -0 and fma(., ., acc) == acc exactly for
+    // every acc (also +-0), so the kernels need no per-slot padding test.
+    const int padc = (int)c->n;
     scol.resize(slots);
     if (!uni) sval.resize(slots);
     // pass 2 (parallel): fill every slot, padding included
@@ -870,7 +870,7 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
             if (!uni) sval[slot] = valof(e);
           } else {
             scol[slot] = padc;
-            if (!uni) sval[slot] = -0.0;
+            if (!uni) sval[slot] = 0.0;
           }
         }
     }
@@ -901,38 +901,37 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
       hvec<double> eval;
       if (!uni) eval.resize(ne);
 #pragma omp parallel for schedule(static, 1024)
-      for (int64_t q = 0; q < nsl32; ++q)
-        for (int j = 0; j < W; ++j)
+      for (int64_t q = 0; q < nsl32; ++q) {
+        const int w = W;
+        const size_t base = (size_t)q * 32 * W;
+        for (int j = 0; j < w; ++j)
           for (int l = 0; l < 32; ++l) {
             const int64_t r = q * 32 + l;
-            // W = 2, 4: lane-major (lane l's slots contiguous, one vector load in spmv_ell)
-            const size_t slot = (size_t)q * 32 * W + ((W == 2 || W == 4) ? (size_t)l * W + j : (size_t)j * 32 + l);
+            // widths 2, 4: lane-major (lane l's slots contiguous, one vector load); else slot-major
+            const size_t slot = base + ((w == 2 || w == 4) ? (size_t)l * w + j : (size_t)j * 32 + l);
             const int e = r < nl ? h_rp[(size_t)r] + j : -1;
             if (e >= 0 && e < h_rp[(size_t)r + 1]) {
               ecol[slot] = enc(e);
               if (!uni) eval[slot] = valof(e);
             } else {
               ecol[slot] = padc;
-              if (!uni) eval[slot] = -0.0;
+              if (!uni) eval[slot] = 0.0;
             }
           }
-      // every slot's coefficient negative (uniform unit-weight Laplacians, padding included): drop the
-      // sign bits, the kernels take -m0 as the one coefficient (kEllNeg)
-      int allneg = uni && (W == 3 || W == 4) ? 1 : 0;
-      if (allneg) {
-#pragma omp parallel for schedule(static, 65536) reduction(& : allneg)
-        for (size_t k = 0; k < ne; ++k) allneg &= (int)((unsigned)ecol[k] >> 31);
       }
-      if (allneg) {
-#pragma omp parallel for schedule(static, 65536)
-        for (size_t k = 0; k < ne; ++k) ecol[k] = (int)((unsigned)ecol[k] & 0x7fffffffu);
+      // every slot's coefficient +m0 (uniform positive weights -- unit-weight MaxCut graphs --, padding
+      // included): the kernels skip the sign handling (kEllPos)
+      int allpos = uni && (W == 3 || W == 4) ? 1 : 0;
+      if (allpos) {
+#pragma omp parallel for schedule(static, 65536) reduction(& : allpos)
+        for (size_t k = 0; k < ne; ++k) allpos &= (int)(1u - ((unsigned)ecol[k] >> 31));
       }
       if (!alloc((void **)&s->ell_col, sizeof(int) * ne) || (!uni && !alloc((void **)&s->ell_val, sizeof(double) * ne)))
         return fail(c, SCG_ENOMEM, "ELL layout");
       CK(cudaMemcpyAsync(s->ell_col, ecol.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
       if (!uni) CK(cudaMemcpyAsync(s->ell_val, eval.data(), sizeof(double) * ne, cudaMemcpyHostToDevice, st));
       CK(cudaStreamSynchronize(st));
-      s->ellw = allneg ? (W | kEllNeg) : W;
+      s->ellw = allpos ? (W | kEllPos) : W;
     }
     // algorithmic matrix bytes: one column index (+ value unless uniform) per stored entry --
     // independent of the layout's padding and metadata
@@ -1002,6 +1001,16 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
   return SCG_OK;
 }
 
+// X[n] = -0 in `count` gathered vectors `pitch` doubles apart (the SpMV padding's dummy column: its
+// product with the padding coefficient +m0 / value +0 is -0, an exact no-op in every fma chain).
+cudaError_t set_pad_zero(scg_ctx *c, double *p, size_t pitch, size_t count) {
+  const std::vector<double> nz(count, -0.0);
+  cudaError_t e = cudaMemcpy2DAsync(p, sizeof(double) * pitch, nz.data(), sizeof(double), sizeof(double), count,
+                                    cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  return e;
+}
+
 // Allocate the gathered region with `cap` W slots (+ the x slot).  Slots are always
 // written before they are read; only the x slot and W slot 0 are zeroed.
 scg_status alloc_G(scg_ctx *c, Shard *s, int cap) {
@@ -1009,9 +1018,10 @@ scg_status alloc_G(scg_ctx *c, Shard *s, int cap) {
   double *G = nullptr;
   CK(cudaMalloc(&G, bytes));
   CK(cudaMemsetAsync(G, 0, sizeof(double) * (size_t)c->npad * 2, c->stream));
-  // slack [n, npad) of every slot reads as +0 (the SELL padding's dummy column n)
+  // slack [n, npad) of every slot reads as +0, except the padding's dummy column n: -0
   CK(cudaMemset2DAsync(G + c->n, sizeof(double) * (size_t)c->npad, 0, sizeof(double) * (size_t)(c->npad - c->n),
                        (size_t)(1 + cap), c->stream));
+  CK(set_pad_zero(c, G + c->n, (size_t)c->npad, (size_t)(1 + cap)));
   if (s->G) {  // keep W slot 0 (the start vector g of the next iteration)
     CK(cudaMemcpyAsync(G + c->npad, s->G + c->npad, sizeof(double) * c->npad, cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1153,6 +1163,37 @@ scg_status sketchycgal_selftest_division(int32_t device, int64_t n, uint64_t see
   if (e != cudaSuccess) return SCG_ECUDA;
   *mismatches = (int64_t)h;
   return SCG_OK;
+}
+
+scg_status sketchycgal_selftest_xsum(int32_t device, const double *values, int64_t n, int32_t grid, int32_t block,
+                                     double *sum, int32_t *range_error) {
+  if (!sum || !range_error || n < 0 || (n > 0 && !values) || grid < 1 || block < 32 || block > 1024 || (block & 31))
+    return SCG_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return SCG_ECUDA;
+  double *dv = nullptr, *dout = nullptr;
+  XSlot *slot = nullptr;
+  DevScalars *sc = nullptr;
+  scg_status st = SCG_OK;
+  if (cudaMalloc(&dv, sizeof(double) * (size_t)std::max<int64_t>(n, 1)) != cudaSuccess ||
+      cudaMalloc(&dout, sizeof(double)) != cudaSuccess || cudaMalloc(&slot, sizeof(XSlot)) != cudaSuccess ||
+      cudaMalloc(&sc, sizeof(DevScalars)) != cudaSuccess)
+    st = SCG_ENOMEM;
+  if (!st && ((n > 0 && cudaMemcpy(dv, values, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice) != cudaSuccess) ||
+              cudaMemset(slot, 0, sizeof(XSlot)) != cudaSuccess || cudaMemset(sc, 0, sizeof(DevScalars)) != cudaSuccess))
+    st = SCG_ECUDA;
+  if (!st) {
+    k_selftest_xsum<<<grid, block>>>(dv, (long long)n, slot, sc, dout);
+    int e = 0;
+    if (cudaMemcpy(sum, dout, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(&e, &sc->err, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+      st = SCG_ECUDA;
+    *range_error = e & 1;
+  }
+  cudaFree(dv);
+  cudaFree(dout);
+  cudaFree(slot);
+  cudaFree(sc);
+  return st;
 }
 
 int64_t sketchycgal_iterations(const scg_ctx *c) { return c ? c->t : -1; }
@@ -1457,7 +1498,8 @@ scg_status sketchycgal_maxcut_init(scg_ctx **out, const scg_csr *L, int32_t R, d
         cudaEventCreateWithFlags(&c->evA, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->evB, cudaEventDisableTiming) != cudaSuccess ||
         cudaMalloc(&s->gB, sizeof(double) * (size_t)c->npad) != cudaSuccess ||
-        cudaMemsetAsync(s->gB, 0, sizeof(double) * (size_t)c->npad, c->stream) != cudaSuccess)
+        cudaMemsetAsync(s->gB, 0, sizeof(double) * (size_t)c->npad, c->stream) != cudaSuccess ||
+        set_pad_zero(c, s->gB + n, (size_t)c->npad, 1) != cudaSuccess)
       return bad(fail(c, SCG_ECUDA, "side stream"));
   }
   const unsigned long long E1 = ++c->epoch;
@@ -1874,6 +1916,7 @@ scg_status sketchycgal_apply_D(scg_ctx *c, const double *xh, double *yh) {
   double *dx = nullptr, *dy = nullptr;
   CK(cudaMalloc(&dx, sizeof(double) * c->npad));
   CK(cudaMemset(dx, 0, sizeof(double) * c->npad));
+  CK(set_pad_zero(c, dx + c->n, (size_t)c->npad, 1));
   {  // x in input order -> device labels
     std::vector<double> xr((size_t)c->n);
     for (int64_t g = 0; g < c->n; ++g) xr[(size_t)c->gmap[(size_t)g]] = xh[g];

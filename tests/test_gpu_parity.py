@@ -162,6 +162,40 @@ def test_ell_ragged_tail_bitwise(gpu, n):
     _assert_trajectory(g, o, 30)
 
 
+@pytest.mark.parametrize("weights", ["unit", "signed", "valued"])
+@pytest.mark.parametrize("resident", [False, True])
+def test_ell_mixed_row_lengths_bitwise(gpu, weights, resident):
+    """ELL-3 against the oracle on rows of 1-3 entries (most rows padded), a ragged last slice, unit
+    weights (the sign-free positive layout), signed unit weights and general weights: the padding's
+    -0 products leave every chain unchanged; with the resident cluster kernel (the ELL engine for
+    W <= 4 as well)."""
+    n = 8001
+    i = np.arange(n)
+    ch = i[i % 3 == 0]
+    u, v = np.concatenate([i[i % 7 != 0], ch]), np.concatenate([(i[i % 7 != 0] + 1) % n, (ch + 97) % n])
+    rng = np.random.default_rng(11)
+    w = {"unit": np.ones(len(u)), "signed": np.where(rng.random(len(u)) < 0.5, -1.0, 1.0),
+         "valued": rng.uniform(0.5, 1.5, len(u))}[weights]
+    L = si.laplacian_from_edges(n, u, v, w, dedupe=True)
+    lens = np.diff(np.asarray(L.row_ptr)) - 1
+    assert lens.max() <= 4 and lens.min() <= 2
+    g, o = _run_pair(gpu, L, 4, 30, seed=6, resident=resident)
+    _assert_trajectory(g, o, 30)
+
+
+def test_ell_far_columns_bitwise(gpu):
+    """Unit-weight ELL (the sign-free positive layout) with columns n/2 rows away on every fifth vertex
+    and short chords elsewhere, n = 100001 (ragged last slice), against the oracle."""
+    n = 100001
+    i = np.arange(n)
+    far, near = i[i % 5 == 0], i[i % 5 == 2]
+    u = np.concatenate([i, far, near])
+    v = np.concatenate([(i + 1) % n, (far + n // 2) % n, (near + 300) % n])
+    L = si.laplacian_from_edges(n, u, v, np.ones(len(u)), dedupe=True)
+    g, o = _run_pair(gpu, L, 4, 12, seed=8)
+    _assert_trajectory(g, o, 12)
+
+
 @pytest.mark.parametrize("cfg,T", [("c0", 200), ("c3", 1)])
 def test_tma_staged_recurrence_bitwise(gpu, cfg, T):
     """The opt-in TMA-staged recurrence kernel (SCG_TMA_B) gives the same bitwise trajectory."""
@@ -281,6 +315,36 @@ def test_config4_first_iteration_bitwise(gpu):
     L = si.laplacian("c4")
     g, o = _run_pair(gpu, L, 2, 1, seed=4)
     _assert_trajectory(g, o, 1)
+
+
+def _xsum_cases():
+    rng = np.random.default_rng(5)
+    n = 200000
+    wide = rng.standard_normal(n) * np.exp2(rng.integers(-300, 95, n).astype(float))
+    cancel = np.concatenate([wide, -wide[::-1], [1e-300, 3.0]])
+    mixed = rng.standard_normal(n) * np.exp2(rng.integers(-40, 40, n).astype(float))
+    mixed[rng.integers(0, n, 500)] = 0.0
+    mixed[rng.integers(0, n, 500)] = 5e-324  # subnormals (Q truncation at 2^-200)
+    near = np.exp2(rng.uniform(90, 99.9, 1000)) * rng.choice([-1.0, 1.0], 1000)
+    same = np.full(300000, 0.1)  # thousands of deposits per thread: the bins spill
+    return {"wide": wide, "cancel": cancel, "mixed": mixed, "near_2^100": near, "same": same,
+            "tiny": rng.standard_normal(n) * 1e-250, "empty": np.zeros(0)}
+
+
+@pytest.mark.parametrize("case", ["wide", "cancel", "mixed", "near_2^100", "same", "tiny", "empty"])
+@pytest.mark.parametrize("grid,block", [(296, 256), (1, 32), (3, 64)])
+def test_exact_sum_accumulators(gpu, case, grid, block):
+    """The kernels' per-thread exact accumulators (fp64 bins with spills, slow path, block and grid
+    commits; CAC-2) against the oracle's independent integer exact sum, bitwise: magnitudes over 400
+    binades, exact cancellation, zeros and subnormals (Q truncation), values near the 2^100 range
+    limit, and 10^4 deposits per thread (grid 1 x 32)."""
+    v = _xsum_cases()[case]
+    s, rerr = gpu.selftest_xsum(v, grid=grid, block=block)
+    want = oracle.xsum(v)
+    assert rerr == 0
+    assert float.hex(s) == float.hex(want), (s, want)
+    bad = np.concatenate([v, [2.0 ** 100]])
+    assert gpu.selftest_xsum(bad, grid=grid, block=block)[1] == 1
 
 
 def test_shared_divisor_division_is_ieee(gpu):

@@ -48,8 +48,13 @@ for w in "$@"; do
       SPEC=${w#ncu:}; KRE=${SPEC%%:*}; SKIP=${SPEC##*:}; [ "$SKIP" = "$SPEC" ] && SKIP=60
       N=${KRE//[^a-zA-Z0-9_]/_}
       CMD="python bench.py --steps 2 --warmup 5 --no-cpu --no-e2e --no-profile"
-      ncu --set full --clock-control none --import-source on -k regex:"$KRE" -s $SKIP -c 2 -o $O/prof_$N $CMD > $O/ncu_full_$N.log 2>&1
-      echo "ncu full exit $?" >> $O/ncu_full_$N.log ;;
+      ncu --set full --clock-control none --import-source on -k regex:"$KRE" -s $SKIP -c 1 -o $O/prof_$N $CMD > $O/ncu_full_$N.log 2>&1
+      echo "ncu full exit $?" >> $O/ncu_full_$N.log
+      # text pages for reading here (the merge back is capped at 64 MiB: keep the report compressed)
+      ncu -i $O/prof_$N.ncu-rep --page raw --csv > $O/prof_${N}_raw.csv 2>/dev/null
+      ncu -i $O/prof_$N.ncu-rep --page details --csv > $O/prof_${N}_details.csv 2>/dev/null
+      ncu -i $O/prof_$N.ncu-rep --page source --csv > $O/prof_${N}_source.csv 2>/dev/null
+      gzip -f $O/prof_$N.ncu-rep ;;
   esac
 done
 echo done > $O/DONE
