@@ -40,6 +40,7 @@ struct DevScalars {
                            //   l1 threshold theta (reading R35)
   int bin[2];              //   and whether the point is already inside the ball (the projection is then the point)
   unsigned long long bk[2];  // l1 threshold search: keys (bit patterns) lo, hi of the bracket (reading R35)
+  double mz[2];            // A X = b: sum z_{t+1}, z_{t+1}.z_{t+1} from k_primal (FK_NZZ), taken into my by the dual
   int bdone, bpad;
   int k, brk, err, pad;
 };
@@ -150,6 +151,7 @@ __device__ __forceinline__ void gstore(const Net &net, double *dst, int r, doubl
 }
 
 enum FinKind { FK_FROB = 0, FK_RHO0, FK_OM, FK_RHO, FK_NUX, FK_MON, FK_NZ, FK_BAR, FK_RHO0M, FK_GEN, FK_RHO0S, FK_MY4,
+               FK_NZZ, FK_RHO0Y, FK_RHO0SY,
                FK_GK, FK_BALLS, FK_L1S, FK_L1B };
 
 struct FinArgs {
@@ -926,6 +928,18 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
       if (sc->bk[1] - sc->bk[0] <= 1ull) sc->bdone = 1;
       break;
     }
+    case FK_RHO0Y:   // A X = b: [||g||^2,] sum y, y.z from k_dual_sketch; z.z, sum z from k_primal (FK_NZZ)
+    case FK_RHO0SY: {
+      const int o = kind == FK_RHO0Y ? 1 : 0;
+      sc->rho[0] = o ? sqrt(xacc_round(L[0])) : sqrt(sc->g2n[f.i & 1]);
+      sc->brk = 0;
+      sc->k = 0;
+      sc->my[0] = xacc_round(L[o]);
+      sc->my[1] = xacc_round(L[o + 1]);
+      sc->my[2] = sc->mz[1];
+      sc->my[3] = sc->mz[0];
+      break;
+    }
     case FK_RHO0S:  // k_dual_sketch without the draw: the next start vector's norm comes from FK_GEN
       sc->rho[0] = sqrt(sc->g2n[f.i & 1]);
       sc->brk = 0;
@@ -940,7 +954,8 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
       sc->c = xacc_round(L[1]);
       sc->vv = xacc_round(L[2]);
       break;
-    case FK_NZ: {
+    case FK_NZ:
+    case FK_NZZ: {
       for (int k = 0; k < f.R; ++k) sc->gk[k] = gk[k];
       const IterArgs &A = f.A;
       const double nz = xacc_round(L[0]);
@@ -972,6 +987,10 @@ __device__ __noinline__ void finalize(int kind, DevScalars *sc, const long long 
         }
       }
       sc->nz = nz;
+      if (kind == FK_NZZ) {  // sums over z_{t+1} for the next gap (my is read above, before this)
+        sc->mz[0] = xacc_round(L[1]);
+        sc->mz[1] = xacc_round(L[2]);
+      }
       sc->gamma = gamma_rule(A, nz);
       const double ea2 = A.eta * A.alpha;
       if (A.trace_le && !(sc->xi < 0.0)) {  // H = 0: X <- (1 - eta) X
@@ -1038,7 +1057,7 @@ __device__ __forceinline__ void emit(XSlot *slot, DevScalars *sc, const Net &net
     return;
   }
   const int e = (int)(net.E & 3ull);
-  const int nf = (kind == FK_NZ || kind == FK_GK) ? f.R : 0;
+  const int nf = (kind == FK_NZ || kind == FK_NZZ || kind == FK_GK) ? f.R : 0;
   for (int q = 0; q < net.P; ++q) {
     Mailbox *m = net.peerMB[q];
     for (int s = 0; s < NS; ++s)
@@ -1086,7 +1105,7 @@ __global__ void k_pull(int kind, int ns, Net net, DevScalars *sc, FinArgs f) {
       for (int p = 0; p < net.P; ++p) part[h] += __ldcv(&m->limbs[e][p][idx / kLimbs][idx % kLimbs]);
   }
   double gpart[2] = {0.0, 0.0};  // g_k = sum over ranks in rank order, k = lane, lane + 32
-  if (kind == FK_NZ || kind == FK_GK)
+  if (kind == FK_NZ || kind == FK_NZZ || kind == FK_GK)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int k = lane + 32 * h;
@@ -2172,10 +2191,14 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
   pdl_entry();
   const bool hoff = A.trace_le && !(sc->xi < 0.0);
   __shared__ double red[kBlock / 32][kMaxR];
-  __shared__ XBlk<1> xb;
-  xblk_init<1>(xb);
-  XWin acc[1];
-  xwin_init(acc[0]);
+  // exact sums: ||z_{t+1} - b||^2 (or - wbar_t); A X = b: also sum z_{t+1}, z_{t+1}.z_{t+1} (the next
+  // iteration's gap / bound, FK_NZZ; summed here, where z_{t+1} is formed, instead of in the dual step)
+  constexpr int NS = KS == 0 ? 3 : 1;
+  __shared__ XBlk<NS> xb;
+  xblk_init<NS>(xb);
+  XWin acc[NS];
+#pragma unroll
+  for (int q = 0; q < NS; ++q) xwin_init(acc[q]);
   int err = 0;
   // thread-per-row; per-thread partial g_k for 16 columns at a time
   constexpr int kPR = 1;
@@ -2209,6 +2232,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
               const double e = zr - (KS == 1 ? proj_k<1>(zr, y[r], A.beta_next, A, 0.0, 0) : A.b);
               xwin_add_nn(acc[0], e * e, err, xb.l[0]);
             }
+            if (KS == 0) {
+              xwin_add_nn(acc[NS - 2], zr, err, xb.l[NS - 2]);  // z >= 0 (convex combination of alpha v o v)
+              xwin_add_nn(acc[NS - 1], zr * zr, err, xb.l[NS - 1]);
+            }
           }
 #pragma unroll
           for (int u = 0; u < 16; ++u) gp[u] = fma(vr[h], om[h][u], gp[u]);
@@ -2230,7 +2257,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
     gpart[(long long)blockIdx.x * R + threadIdx.x] = t;
   }
   __syncthreads();
-  if (commit_and_ticket<1>(acc, xb, slot, err, sc, net.P, 0u)) {
+  if (commit_and_ticket<NS>(acc, xb, slot, err, sc, net.P, 0u)) {
     __shared__ double gsum[kMaxR];
     // sum block partials in a fixed order: thread k sums column k over blocks
     if (threadIdx.x < R) {
@@ -2244,7 +2271,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_primal(const double *__restrict__
       f.R = R;
       f.A = A;
       f.log = log;
-      emit<1>(slot, sc, net, KS >= 2 ? FK_GK : FK_NZ, f, gsum);
+      emit<NS>(slot, sc, net, KS >= 2 ? FK_GK : (KS == 0 ? FK_NZZ : FK_NZ), f, gsum);
     }
   }
 }
@@ -2266,9 +2293,10 @@ __global__ void __launch_bounds__(kBlock, GEN ? 2 : 4) k_dual_sketch(const doubl
   const int bin0 = KS >= 2 ? sc->bin[0] : 0;
   if (blockIdx.x == 0 && (int)threadIdx.x < R)  // H = 0 (trace-bounded, xi_t >= 0): no rank-one term
     ckr[js * kMaxR + threadIdx.x] = (A.trace_le && !(sc->xi < 0.0)) ? 0.0 : (A.eta * A.alpha) * sc->gk[threadIdx.x];
-  // exact sums: [GEN: ||g_{t+1}||^2,] and over the next iteration's state (y_{t+1}, z_{t+1}):
-  // sum y, y.z, z.z, sum z (surrogate gap / stopping rule, finalize FK_NZ)
-  constexpr int NS = (GEN ? 1 : 0) + (KS >= 2 ? 0 : 4), o = GEN ? 1 : 0;
+  // exact sums: [GEN: ||g_{t+1}||^2,] and over the next iteration's state (y_{t+1}, z_{t+1}) for the
+  // surrogate gap / stopping rule (finalize FK_NZ): A X = b sum y, y.z (z.z, sum z: k_primal); box
+  // the four general-template dots
+  constexpr int NS = (GEN ? 1 : 0) + (KS >= 2 ? 0 : (KS == 1 ? 4 : 2)), o = GEN ? 1 : 0;
   __shared__ XBlk<NS> xb;
   xblk_init<NS>(xb);
   XWin acc[NS];
@@ -2315,11 +2343,9 @@ __global__ void __launch_bounds__(kBlock, GEN ? 2 : 4) k_dual_sketch(const doubl
           xwin_add(acc[o + 1], e1 * zr[u], err, xb.l[o + 1]);
           xwin_add(acc[o + 2], yr * wk, err, xb.l[o + 2]);
           xwin_add(acc[o + 3], e1 * (zr[u] + wk), err, xb.l[o + 3]);
-        } else {
+        } else {  // sum y, y.z (sum z and z.z come from k_primal)
           xwin_add(acc[o + 0], yr, err, xb.l[o + 0]);
           xwin_add(acc[o + 1], yr * zr[u], err, xb.l[o + 1]);
-          xwin_add_nn(acc[o + 2], zr[u] * zr[u], err, xb.l[o + 2]);
-          xwin_add_nn(acc[o + 3], zr[u], err, xb.l[o + 3]);  // z >= 0 (convex combination of alpha v o v)
         }
       }
     }
@@ -2327,7 +2353,8 @@ __global__ void __launch_bounds__(kBlock, GEN ? 2 : 4) k_dual_sketch(const doubl
   if (commit_and_ticket<NS>(acc, xb, slot, err, sc, net.P, peer) && threadIdx.x == 0) {
     FinArgs f{};
     f.i = (int)((A.t + 1) & 1);
-    emit<NS>(slot, sc, net, KS >= 2 ? FK_RHO0 : (GEN ? FK_RHO0M : FK_RHO0S), f, nullptr);
+    emit<NS>(slot, sc, net,
+             KS >= 2 ? FK_RHO0 : (KS == 1 ? (GEN ? FK_RHO0M : FK_RHO0S) : (GEN ? FK_RHO0Y : FK_RHO0SY)), f, nullptr);
   }
 }
 

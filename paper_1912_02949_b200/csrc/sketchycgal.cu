@@ -465,7 +465,7 @@ void pull_all(scg_ctx *c, int kind, int ns, unsigned long long E, const FinArgs 
   }
   for (Shard *s : c->sh) {
     FinArgs f = f0;
-    if (kind == FK_NZ) f.log = s->dlog;
+    if (kind == FK_NZ || kind == FK_NZZ) f.log = s->dlog;
     if (kind == FK_FROB) f.out = s->dscalar;
     launch(c, KC_PULL, 0.0, k_pull, dim3(1), dim3(32), kind, ns, net_of(c, s, E), s->sc, f);
   }
@@ -1760,7 +1760,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       FinArgs f{};
       f.R = c->R;
       f.A = A;
-      pull_all(c, ks >= 2 ? FK_GK : FK_NZ, 1, E, f);
+      pull_all(c, ks >= 2 ? FK_GK : (ks == 0 ? FK_NZZ : FK_NZ), ks == 0 ? 3 : 1, E, f);
     }
     if (ks >= 2) {  // balls (readings R34, R35): wbar_t needs the projection pass over z_{t+1} + y_t / beta_{t+1}
       ball_norm(c, A.beta_next, A, 0);
@@ -1789,7 +1789,8 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       pull_all(c, FK_RHO0, 1, E, FinArgs{});
       ball_state(c, A.beta_next, A);  // w_{t+1}, D_{t+1}'s diagonal and the gap / bound sums
     } else {
-      pull_all(c, FK_RHO0M, 5, E, FinArgs{});
+      if (ks == 0) pull_all(c, FK_RHO0Y, 3, E, FinArgs{});
+      else pull_all(c, FK_RHO0M, 5, E, FinArgs{});
     }
     c->ome[js] = A.one_m_eta;
     c->vlast = js;
