@@ -157,3 +157,58 @@ def philox(counter, key) -> np.ndarray:
     out = np.zeros(4, dtype=np.uint32)
     _load().scg_philox(*[int(x) for x in counter], *[int(x) for x in key], out.ctypes.data)
     return out
+
+
+# ---------------------------------------------------------------------------
+# Synthetic abstract phase retrieval instances.
+SCG_STREAM_PHASE = 3  # include/scg_rng.h: sub 0 = unit phase, 1 = magnitude, 2 = signal
+PHASE_L = 12  # d = 12 n coded-diffraction measurements
+
+
+@dataclass
+class PhaseInstance:
+    """psi: (L, n) complex modulating waveforms; chi: (n,) the signal chi_natural;
+    b: (L, n) real phaseless measurements, b[j, l] = |(W_n diag(psi_j)^* chi)_l|^2 (reading R36)."""
+    n: int
+    psi: np.ndarray
+    chi: np.ndarray
+    b: np.ndarray
+
+
+def phase_psi(n: int, seed: int, L: int = PHASE_L) -> np.ndarray:
+    """Coded diffraction waveforms (P:4298-4300): each entry is a uniform draw from {1, i, -1, -i}
+    times an independent draw from {sqrt(2)/2, sqrt(3)} with probabilities 0.8 / 0.2."""
+    cnt = L * n
+    u_unit = uniforms(seed, SCG_STREAM_PHASE, 0, 0, cnt)
+    u_mag = uniforms(seed, SCG_STREAM_PHASE, 1, 0, cnt)
+    k = np.minimum((u_unit * 4.0).astype(np.int64), 3)
+    unit = np.array([1.0 + 0.0j, 0.0 + 1.0j, -1.0 + 0.0j, 0.0 - 1.0j])[k]
+    mag = np.where(u_mag < 0.8, np.sqrt(2.0) / 2.0, np.sqrt(3.0))
+    return (unit * mag).reshape(L, n)
+
+
+def phase_signal(n: int, seed: int) -> np.ndarray:
+    """chi_natural from the complex standard normal distribution: real and imaginary
+    parts independent N(0, 1/2), so E|chi_i|^2 = 1 (reading R36)."""
+    g = normals(seed, SCG_STREAM_PHASE, 2, 0, 2 * n)
+    return (g[0::2] + 1j * g[1::2]) * np.sqrt(0.5)
+
+
+def phase_instance(n: int, seed: int = 0, L: int = PHASE_L) -> PhaseInstance:
+    """One synthetic instance: psi, chi_natural and the d = L n measurements b.
+    The measurement of the data recipe uses numpy's FFT (W_n(l, k) = exp(-2 pi i l k / n))."""
+    psi = phase_psi(n, seed, L)
+    chi = phase_signal(n, seed)
+    b = np.abs(np.fft.fft(np.conj(psi) * chi[None, :], axis=1)) ** 2
+    return PhaseInstance(n, psi, chi, b)
+
+
+# Workloads of the phase retrieval experiment (P:2027-2038): n in {10^2, ..., 10^6}, d = 12 n,
+# R = 5, alpha = 3 n.
+PHASE_CONFIGS = {
+    "p2": dict(n=100, seed=0, R=5),
+    "p3": dict(n=1000, seed=1, R=5),
+    "p4": dict(n=10000, seed=2, R=5),
+    "p5": dict(n=100000, seed=3, R=5),
+    "p6": dict(n=1000000, seed=4, R=5),
+}

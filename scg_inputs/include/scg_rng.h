@@ -49,6 +49,7 @@
 #define SCG_STREAM_OMEGA 0u
 #define SCG_STREAM_LANCZOS 1u
 #define SCG_STREAM_GRAPH 2u
+#define SCG_STREAM_PHASE 3u /* phase retrieval instance: sub 0 unit phase, 1 magnitude, 2 signal */
 
 typedef struct {
   uint32_t w[4];
