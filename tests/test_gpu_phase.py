@@ -1,0 +1,123 @@
+"""GPU parity of the phase retrieval path (csrc/phase.cu through include/scg_phase.h) against the
+CPU oracle (oracle/phase.py) on the same seeded instances.
+
+Tolerances: the FFT is a different summation order than numpy's pocketfft,
+so the comparisons are within floating-point bounds rather than bitwise -- operator entries within
+1e-12 relative to the operator scale (an FFT of length n has error ~ eps log2 n), the Ritz values
+within 1e-8 relative for the first iterations (BASELINE's per-iteration eigenvalue bound), the
+state within 1e-6 after the window, and the recovered signal within the paper's 1e-2 accuracy."""
+import numpy as np
+import pytest
+
+import scg_inputs as si
+from oracle import phase as ph
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pr(gpu):
+    from paper_1912_02949_b200 import phase as prm
+    prm.load()
+    return prm
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+# sizes: the paper's n = 10^2..10^6 plus ragged {2,3,5}-smooth shapes (odd radices, n1 != n2)
+@pytest.mark.parametrize("n", [100, 360, 1000, 2 * 3 * 5 * 7 - 30, 4500, 10000, 100000, 1000000])
+def test_operator_parity(pr, n):
+    I = si.phase_instance(n, seed=11)
+    ctx = pr.PhaseRetrieval(I.psi, I.b, R=5, seed=11)
+    kappa, bt = ph.scaling(I.psi, I.b, 3.0 * n)
+    np.testing.assert_allclose(ctx.state("kappa"), kappa, rtol=1e-12)
+    np.testing.assert_allclose(ctx.state("bt"), bt, rtol=1e-11, atol=1e-14 * np.abs(bt).max())
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    assert _rel(ctx.measure(x), ph.A_rank1(I.psi, kappa, x)) < 1e-12
+    w = rng.standard_normal((12, n))
+    assert _rel(ctx.apply_D(w, x), ph.apply_D(I.psi, kappa, w, x)) < 1e-12
+    # the signal itself: A~(chi chi^*) / alpha = b~
+    assert _rel(ctx.measure(I.chi) / (3.0 * n), bt) < 1e-12
+    ctx.close()
+
+
+def _run_both(n, seed, T, R=5):
+    from paper_1912_02949_b200 import phase as prm
+    I = si.phase_instance(n, seed=seed)
+    g = prm.PhaseRetrieval(I.psi, I.b, R=R, seed=seed)
+    g.step(T)
+    o = ph.PhaseOracle(I.psi, I.b, R=R, seed=seed)
+    o.step(T)
+    return I, g, o
+
+
+@pytest.mark.parametrize("n,seed,T", [(100, 0, 60), (1000, 1, 40), (4500, 5, 25)])
+def test_trajectory_parity(pr, n, seed, T):
+    I, g, o = _run_both(n, seed, T)
+    gl, ol = g.iter_log(), o.logarr
+    assert gl.shape == ol.shape
+    np.testing.assert_array_equal(gl[:, 1], ol[:, 1])               # q_t
+    np.testing.assert_array_equal(gl[:, 2], ol[:, 2])               # k_t
+    win = min(T, 20)
+    scale = np.abs(ol[:win, 3]).max()
+    assert np.max(np.abs(gl[:win, 3] - ol[:win, 3])) <= 1e-8 * scale   # theta_t
+    assert np.max(np.abs(gl[:win, 4] - ol[:win, 4])) <= 1e-8 * scale   # xi_t
+    np.testing.assert_array_equal(gl[:, 4] < 0, ol[:, 4] < 0)        # LMO branch
+    for col in (6, 7, 9):                                            # p, ||z - b||, tau
+        assert _rel(gl[:, col], ol[:, col]) < 1e-6
+    assert _rel(g.state("z"), o.z) < 1e-6
+    assert _rel(g.state("y"), o.y) < 1e-6
+    assert _rel(g.state("S"), o.S) < 1e-6
+    np.testing.assert_allclose(g.state("Omega"), o.Omega, rtol=0, atol=0)   # the same seeded draws
+    # v up to a global phase (sign): |<v_gpu, v_oracle>| = 1
+    v = g.state("v")
+    assert abs(abs(np.vdot(v, o.v)) - 1.0) < 1e-6
+
+
+def test_reconstruction_parity_on_gpu_sketch(pr):
+    """Alg. 3 on the GPU against the oracle's Nystrom applied to the GPU's own S and Omega."""
+    n = 1000
+    I = si.phase_instance(n, seed=3)
+    g = pr.PhaseRetrieval(I.psi, I.b, R=5, seed=3)
+    g.step(80)
+    U, lam = g.reconstruct()
+    Uo, lamo = ph.nystrom_reconstruct_c(g.state("S"), g.state("Omega"))
+    np.testing.assert_allclose(lam, lamo, rtol=1e-9, atol=1e-12 * lamo[0])
+    assert np.allclose(U.conj().T @ U, np.eye(5), atol=1e-10)
+    for k in range(2):          # the well separated leading columns, up to a phase
+        assert abs(abs(np.vdot(U[:, k], Uo[:, k])) - 1.0) < 1e-8
+    chi = g.signal()
+    np.testing.assert_allclose(chi, np.sqrt(3.0 * n * lam[0]) * U[:, 0], rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("n,T", [(100, 1000), (1000, 1500)])
+def test_recovers_signal_like_the_paper(pr, n, T):
+    """relative error below 1e-2; the oracle's and the GPU's signals agree."""
+    I, g, o = _run_both(n, 0, T)
+    g.reconstruct()
+    chi_g, chi_o = g.signal(), o.signal()
+    eg, eo = ph.relative_error(chi_g, I.chi), ph.relative_error(chi_o, I.chi)
+    assert eg < 1e-2 and eo < 1e-2, (eg, eo)
+    assert ph.relative_error(chi_g, chi_o) < 1e-3
+    gl = g.iter_log()
+    assert abs(gl[-1, 9] - o.tau) < 1e-6 * o.tau
+
+
+def test_full_size_first_iteration_p6(pr):
+    """n = 10^6 (the paper's largest), the bench configuration: the first iteration's
+    Ritz value, monitor and z against the oracle."""
+    n = 1000000
+    I = si.phase_instance(n, seed=4)
+    g = pr.PhaseRetrieval(I.psi, I.b, R=5, seed=4)
+    g.step(1)
+    o = ph.PhaseOracle(I.psi, I.b, R=5, seed=4)
+    o.step(1)
+    gl, ol = g.iter_log(), o.logarr
+    assert gl[0, 1] == ol[0, 1] and gl[0, 2] == ol[0, 2]
+    assert abs(gl[0, 3] - ol[0, 3]) <= 1e-8 * abs(ol[0, 3])
+    assert abs(gl[0, 4] - ol[0, 4]) <= 1e-8 * abs(ol[0, 4])
+    assert _rel(g.state("z"), o.z) < 1e-6
+    assert _rel(g.state("y"), o.y) < 1e-6
