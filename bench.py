@@ -375,6 +375,141 @@ def run_e2e(scg, si, L, c, K, W, dev, dkw, world):
                     "split, SELL layout and Omega draw; per-rank bytes"}
 
 
+PHASE_METRIC = "SketchyCGAL phase retrieval iterations/s and FFT matvec HBM GB/s (fraction of peak), 1 B200"
+
+
+def _phase_config(cfg, t0, t1, world=1):
+    import scg_inputs as si
+    c = si.PHASE_CONFIGS[cfg]
+    n = c["n"]
+    q = [min(n - 1, max(2, int(np.ceil(np.sqrt(np.sqrt(float(t))) * np.log(float(n)))))) for t in (t0, t1)]
+    return {"workload": f"{cfg}: abstract phase retrieval SDP (P:2027-2038), n={n}, d=12n coded-diffraction "
+                        f"measurements, R={c['R']}, alpha=3n, seed {c['seed']}", "n": n, "d": 12 * n, "R": c["R"],
+            "t_window": [int(t0), int(t1)], "q_t_window": q, "parallelism": f"replica{world}",
+            "l2": "no flush: per-iteration working set (12n complex FFT intermediates, 192 MB at n=10^6) > 126 MB L2"}
+
+
+def run_phase_reference(args, rank):
+    """--impl reference for the phase retrieval configs: the numpy oracle (oracle/phase.py) on the host."""
+    import scg_inputs as si
+    from oracle import phase as ph
+    if rank != 0:
+        return
+    c = si.PHASE_CONFIGS[args.config]
+    I = si.phase_instance(c["n"], seed=c["seed"])
+    o = ph.PhaseOracle(I.psi, I.b, R=c["R"], seed=c["seed"])
+    iters = max(1, min(args.steps, args.ref_iters))
+    t0 = time.perf_counter()
+    o.step(iters)
+    dt = time.perf_counter() - t0
+    v = iters / dt
+    cb = {"value": v, "unit": "iterations/s", "cores": os.cpu_count(), "kind": "oracle",
+          "sample": f"numpy oracle (pocketfft, complex128) on {args.config} iterations t=1..{iters}, {dt:.1f} s",
+          "host": host_info()}
+    print(json.dumps({"impl": "reference", "metric": PHASE_METRIC, "value": v, "unit": "iterations/s", "n_gpus": 1,
+                      "steps": iters, "warmup": 0, "ms_per_step": 1e3 / v, "higher_is_better": True,
+                      "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+                      "config": _phase_config(args.config, 1, iters), "cpu_baseline": cb,
+                      "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def run_phase(args, rank, local_rank, world=1):
+    """SketchyCGAL on the synthetic phase retrieval SDP (csrc/phase.cu).  One GPU per
+    problem ("replicas only"): with --gpus N every rank solves its own instance."""
+    import torch
+    import scg_inputs as si
+    from paper_1912_02949_b200 import phase as prm
+    torch.cuda.set_device(local_rank)
+    c = si.PHASE_CONFIGS[args.config]
+    n, R = c["n"], c["R"]
+    W, K = args.warmup, args.steps
+    if world > 1:  # replicas: every rank solves its own instance (seed + rank); max-over-ranks time
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    I = si.phase_instance(n, seed=c["seed"] + rank)
+    g = prm.PhaseRetrieval(I.psi, I.b, R=R, seed=c["seed"] + rank, profile=not args.no_profile, device=local_rank)
+    g.step(W)
+    g.reset_stats()
+    st = torch.cuda.ExternalStream(g.stream_ptr())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        e0.record(st)
+        g.step(K)
+        e1.record(st)
+        e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    stats = [s for s in g.kernel_stats() if s["launches"] > 0]
+    lg = g.iter_log()[W:W + K]
+    g.close()
+    peak, peak_kind = _peaks()
+
+    def gbs(s):
+        return s["bytes_per_launch"] * s["launches"] / (s["total_ms"] / 1e3) / 1e9 if s["total_ms"] > 0 else 0.0
+
+    kernels = {s["name"]: {"launches": s["launches"], "avg_us": 1e3 * s["total_ms"] / s["launches"],
+                           "share": s["total_ms"] / ms if ms > 0 else None, "gbs": round(gbs(s), 1)} for s in stats}
+    top = max(stats, key=lambda s: s["total_ms"]) if stats else None
+    mv = [s for s in stats if s["name"] in ("k_pr_f1", "k_pr_b", "k_pr_c")]
+    mv_bytes = sum(s["bytes_per_launch"] * s["launches"] for s in mv)
+    mv_sec = sum(s["total_ms"] for s in mv) / 1e3
+    matvecs = float(np.sum(lg[:, 2] + 1))
+    # end to end through the C ABI with host buffers: init (psi, b H2D), W + K iterations, reconstruction,
+    # the signal estimate (D2H)
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g2 = prm.PhaseRetrieval(I.psi, I.b, R=R, seed=c["seed"], device=local_rank)
+        g2.step(W + K)
+        lg2 = g2.iter_log()
+        U, lam = g2.reconstruct()
+        chi = g2.signal()
+        t1 = time.perf_counter()
+        g2.close()
+        h2d = I.psi.nbytes + I.b.nbytes
+        d2h = lg2.nbytes + U.nbytes + lam.nbytes + chi.nbytes
+        e2e = {"value": (W + K) / (t1 - t0), "unit": "iterations/s", "h2d_bytes_per_step": h2d / (W + K),
+               "d2h_bytes_per_step": d2h / (W + K), "seconds": t1 - t0,
+               "note": "pageable numpy psi (L x n complex) and b copied inside init; t=1..W+K; reconstruction "
+                       "and signal estimate read back"}
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import phase as ph
+        o = ph.PhaseOracle(I.psi, I.b, R=R, seed=c["seed"])
+        t0 = time.perf_counter()
+        o.step(1)
+        dt = time.perf_counter() - t0
+        cb = {"value": 1.0 / dt, "unit": "iterations/s", "cores": os.cpu_count(), "kind": "oracle",
+              "sample": f"numpy oracle (pocketfft, complex128) on {args.config} iteration t=1 (q_t="
+                        f"{int(o.logarr[0, 1])}), {dt:.1f} s", "host": host_info()}
+    line = {"metric": PHASE_METRIC, "value": world * K / (ms / 1e3), "unit": "iterations/s", "n_gpus": world,
+            "steps": K,
+            "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128", "data": "synthetic", "config": _phase_config(args.config, W + 1, W + K, world),
+            "roofline": None if top is None else {
+                "bound": "hbm", "kernel": top["name"], "achieved": round(gbs(top), 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": gbs(top) / peak, "traffic": None,
+                "algorithmic_bytes_per_launch": top["bytes_per_launch"]},
+            "fft_matvec": {"kernels": [s["name"] for s in mv], "achieved": round(mv_bytes / mv_sec / 1e9, 1) if mv_sec else None,
+                           "peak": peak, "unit": "GB/s", "frac": (mv_bytes / mv_sec / 1e9) / peak if mv_sec else None,
+                           "matvecs_per_s": matvecs / (ms / 1e3)},
+            "kernels": kernels, "cpu_baseline": cb, "clocks": clk.summary(), "e2e": e2e,
+            "gpu_launches": int(sum(s["launches"] for s in stats))}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -396,7 +531,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
+    if args.config.startswith("p"):  # phase retrieval workloads
+        if args.impl == "reference":
+            run_phase_reference(args, rank)
+        else:
+            run_phase(args, rank, local_rank, world)
+    elif args.impl == "reference":
         run_reference(args, rank, world)
     else:
         run_ours(args, rank, world, local_rank)

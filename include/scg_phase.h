@@ -66,11 +66,16 @@ typedef struct {
  *   flags  SCG_PR_PROFILE (1 << 8): per-kernel CUDA-event timing (scg_pr_kernel_stats);
  *          SCG_PR_TM2 (1 << 9): two transforms per FFT block instead of four (execution option);
  *          SCG_PR_GENERIC (1 << 10): runtime radix plans even where a compile-time plan exists
- *          (execution option; the results agree within the FFT's rounding).
+ *          (execution option; the results agree within the FFT's rounding);
+ *          SCG_PR_NOPF_F1 / _B / _C (1 << 11 / 12 / 13): load the next tile after (instead of before)
+ *          the current tile's transform in k_pr_f1 / k_pr_b / k_pr_c (execution options, same bits).
  * Errors: SCG_EINVAL, SCG_EUNSUPPORTED, SCG_ENOMEM, SCG_ECUDA. */
 #define SCG_PR_PROFILE (1u << 8)
 #define SCG_PR_TM2 (1u << 9)
 #define SCG_PR_GENERIC (1u << 10)
+#define SCG_PR_NOPF_F1 (1u << 11)
+#define SCG_PR_NOPF_B (1u << 12)
+#define SCG_PR_NOPF_C (1u << 13)
 int scg_pr_init(int64_t n, int32_t L, const double *psi, const double *b, int32_t R, double alpha,
                 double beta0, uint64_t seed, uint32_t flags, scg_pr_ctx **out);
 

@@ -392,12 +392,14 @@ __device__ __forceinline__ void load_tables(double2 *twsm, const double2 *__rest
 }
 
 // Forward step A: per (m1 tile, j): x = conj(psi_j) o (s u), length-n2 FFT over m2 -> Y[j][k2][m1].
-template <int NC, int TMC>
+// Persistent: each block walks tiles (j, m1 tile) with the next tile's inputs loaded into registers
+// while the current one is transformed.
+template <int NC, int TMC, bool PF>
 __global__ void __launch_bounds__(512) k_pr_f1(const double2 *__restrict__ u, const double *__restrict__ scale_p,
                                                int step, const PrScal *__restrict__ sc,
                                                const uint8_t *__restrict__ codes, const double2 *__restrict__ book,
                                                double2 *__restrict__ Y, Plan P, const double2 *__restrict__ tw,
-                                               int n1, int n2, int TMr) {
+                                               int n1, int n2, int TMr, int L) {
   if (skip_step(sc, step)) return;
   const Sub<NC, TMC> F(P, TMr);
   extern __shared__ double2 sm[];
@@ -406,35 +408,53 @@ __global__ void __launch_bounds__(512) k_pr_f1(const double2 *__restrict__ u, co
   load_tables(twsm, tw, F.N(), cb, book);
   __syncthreads();
   const int64_t n = (int64_t)n1 * F.N();
-  const int j = blockIdx.y, m1_0 = blockIdx.x * F.TM;
+  const int tiles_per_j = n1 / F.TM, ntiles = tiles_per_j * L;
   const double s = scale_p ? *scale_p : 1.0;
-  const uint8_t *cj = codes + (size_t)j * n;
-  double2 x[8];
-  if (F.jb < F.NR0()) {
+  const bool ld = F.jb < F.NR0();
+  double2 un[8];
+  uint8_t cn[8];
+  auto fetch = [&](int tile) {
+    const int j = tile / tiles_per_j, m1_0 = (tile - j * tiles_per_j) * F.TM;
+    const uint8_t *cj = codes + (size_t)j * n;
 #pragma unroll
     for (int r = 0; r < 8; ++r)
       if (r < F.R0()) {
         const int64_t m = m1_0 + F.t + (int64_t)n1 * F.in_pos(r);
-        x[r] = cmulc(cscale(__ldg(u + m), s), cb[cj[m]]);
+        un[r] = __ldg(u + m);
+        cn[r] = __ldg(cj + m);
       }
-  }
-  F.template run<false>(x, sm, twsm);
-  if (F.jb < F.NRL()) {
-    double2 *Yj = Y + (size_t)j * n + m1_0 + F.t;
+  };
+  int tile = blockIdx.x;
+  if (ld && tile < ntiles) fetch(tile);
+  for (; tile < ntiles; tile += gridDim.x) {
+    double2 x[8];
+    if (ld) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (r < F.RL()) Yj[(size_t)F.out_pos(r) * n1] = x[r];
+      for (int r = 0; r < 8; ++r)
+        if (r < F.R0()) x[r] = cmulc(cscale(un[r], s), cb[cn[r]]);
+      if (PF && tile + (int)gridDim.x < ntiles) fetch(tile + gridDim.x);
+    }
+    F.template run<false>(x, sm, twsm);
+    if (!PF && ld && tile + (int)gridDim.x < ntiles) fetch(tile + gridDim.x);
+    if (F.jb < F.NRL()) {
+      const int j = tile / tiles_per_j, m1_0 = (tile - j * tiles_per_j) * F.TM;
+      double2 *Yj = Y + (size_t)j * n + m1_0 + F.t;
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r < F.RL()) Yj[(size_t)F.out_pos(r) * n1] = x[r];
+    }
   }
 }
 
 // Middle step: per (k2 tile, j): twiddle, length-n1 FFT over m1, [h = |.|^2], times w, inverse FFT,
-// twiddle back, in place.  mode 0: matvec, 1: matvec + h (monitor), 2: h only (measure).
-template <int NC, int TMC>
+// twiddle back, in place.  mode 0: matvec, 1: matvec + h (monitor), 2: h only (measure).  Persistent with
+// the next tile's row loaded during the current tile's transforms.
+template <int NC, int TMC, bool PF>
 __global__ void __launch_bounds__(512) k_pr_b(double2 *__restrict__ Y, const double *__restrict__ wk,
                                               double *__restrict__ h, int mode, int step,
                                               const PrScal *__restrict__ sc, Plan P, const double2 *__restrict__ tw,
                                               const double2 *__restrict__ twlo, const double2 *__restrict__ twhi,
-                                              int n1, int n2, int TMr) {
+                                              int n1, int n2, int TMr, int L) {
   if (skip_step(sc, step)) return;
   const Sub<NC, TMC> F(P, TMr);
   extern __shared__ double2 sm[];
@@ -443,63 +463,83 @@ __global__ void __launch_bounds__(512) k_pr_b(double2 *__restrict__ Y, const dou
   __syncthreads();
   const int n1c = F.N();
   const int64_t n = (int64_t)n1c * n2;
-  const int j = blockIdx.y, k2 = blockIdx.x * F.TM + F.t;
-  double2 *row = Y + (size_t)j * n + (size_t)k2 * n1c;
-  double2 x[8];
-  if (F.jb < F.NR0()) {
-    // w_n^{m1 k2} for m1 = jb + r NR0: base w_n^{jb k2} times powers of w_n^{NR0 k2}
-    const double2 w0 = twn(twlo, twhi, (long long)F.jb * k2);
-    const double2 w1 = twn(twlo, twhi, (long long)F.NR0() * k2);
-    double2 w = w0;
+  const int tiles_per_j = n2 / F.TM, ntiles = tiles_per_j * L;
+  const bool ld = F.jb < F.NR0();
+  double2 yn[8];
+  auto fetch = [&](int tile) {
+    const int j = tile / tiles_per_j, k2 = (tile - j * tiles_per_j) * F.TM + F.t;
+    const double2 *row = Y + (size_t)j * n + (size_t)k2 * n1c;
 #pragma unroll
     for (int r = 0; r < 8; ++r)
-      if (r < F.R0()) {
-        x[r] = cmul(row[F.in_pos(r)], w);
-        w = cmul(w, w1);
-      }
-  }
-  F.template run<false>(x, sm, twsm);
-  const size_t base = (size_t)j * n + (size_t)k2 * n1c;
-  if (F.jb < F.NRL()) {
+      if (r < F.R0()) yn[r] = row[F.in_pos(r)];
+  };
+  int tile = blockIdx.x;
+  if (ld && tile < ntiles) fetch(tile);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int j = tile / tiles_per_j, k2 = (tile - j * tiles_per_j) * F.TM + F.t;
+    const size_t base = (size_t)j * n + (size_t)k2 * n1c;
+    double2 x[8];
+    double wv[8];
+    if (mode <= 1 && F.jb < F.NRL()) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (r < F.RL()) {
-        const int k1 = F.out_pos(r);
-        if (mode >= 1) h[base + k1] = x[r].x * x[r].x + x[r].y * x[r].y;
-        if (mode <= 1) x[r] = cscale(x[r], __ldg(wk + base + k1));
-      }
-  }
-  if (mode == 2) return;
-  // re-enter shared memory for the inverse transform over k1
-  __syncthreads();
-  if (F.jb < F.NRL()) {
+      for (int r = 0; r < 8; ++r)
+        if (r < F.RL()) wv[r] = __ldg(wk + base + F.out_pos(r));
+    }
+    if (ld) {
+      // w_n^{m1 k2} for m1 = jb + r NR0: base w_n^{jb k2} times powers of w_n^{NR0 k2}
+      const double2 w1 = twn(twlo, twhi, (long long)F.NR0() * k2);
+      double2 w = twn(twlo, twhi, (long long)F.jb * k2);
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (r < F.RL()) sm[F.out_pos(r) * F.TM + F.t] = x[r];
-  }
-  __syncthreads();
-  if (F.jb < F.NR0()) {
+      for (int r = 0; r < 8; ++r)
+        if (r < F.R0()) {
+          x[r] = cmul(yn[r], w);
+          w = cmul(w, w1);
+        }
+      if (PF && tile + (int)gridDim.x < ntiles) fetch(tile + gridDim.x);
+    }
+    F.template run<false>(x, sm, twsm);
+    if (F.jb < F.NRL()) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (r < F.R0()) x[r] = sm[F.in_pos(r) * F.TM + F.t];
-  }
-  __syncthreads();
-  F.template run<true>(x, sm, twsm);
-  if (F.jb < F.NRL()) {
+      for (int r = 0; r < 8; ++r)
+        if (r < F.RL()) {
+          if (mode >= 1) h[base + F.out_pos(r)] = x[r].x * x[r].x + x[r].y * x[r].y;
+          if (mode <= 1) x[r] = cscale(x[r], wv[r]);
+        }
+    }
+    if (mode == 2) continue;
+    // re-enter shared memory for the inverse transform over k1
+    if (F.jb < F.NRL()) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (r < F.RL()) {
-        const int m1 = F.out_pos(r);
-        row[m1] = cmulc(x[r], twn(twlo, twhi, (long long)m1 * k2));
-      }
+      for (int r = 0; r < 8; ++r)
+        if (r < F.RL()) sm[F.out_pos(r) * F.TM + F.t] = x[r];
+    }
+    __syncthreads();
+    if (ld) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r < F.R0()) x[r] = sm[F.in_pos(r) * F.TM + F.t];
+    }
+    __syncthreads();
+    if (!PF && ld && tile + (int)gridDim.x < ntiles) fetch(tile + gridDim.x);
+    F.template run<true>(x, sm, twsm);
+    if (F.jb < F.NRL()) {
+      double2 *row = Y + base;
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r < F.RL()) {
+          const int m1 = F.out_pos(r);
+          row[m1] = cmulc(x[r], twn(twlo, twhi, (long long)m1 * k2));
+        }
+    }
   }
 }
 
 // Inverse step A' + demodulation + sum over j + C~ x + Lanczos dot:
 //   a = s u / sqrt(n) + sum_j psi_j o (inverse length-n2 FFT over k2 of Y[j][.][m1]).
 // mode 0: write a, omega[step-1] = Re((s u)^* a);  mode 1 (monitor): xi = Re(v^* a), a not written;
-// mode 2 (apply_D hook): write a only.
-template <int NC, int TMC>
+// mode 2 (apply_D hook): write a only.  The sum over j accumulates in shared memory (each position is
+// owned by one thread); Y of modulation j + 1 is loaded while j is transformed.
+template <int NC, int TMC, bool PF>
 __global__ void __launch_bounds__(512) k_pr_c(const double2 *__restrict__ Y, const double2 *__restrict__ u,
                                               const double *__restrict__ scale_p, double2 *__restrict__ a,
                                               const uint8_t *__restrict__ codes, const double2 *__restrict__ book,
@@ -511,41 +551,57 @@ __global__ void __launch_bounds__(512) k_pr_c(const double2 *__restrict__ Y, con
   __shared__ double red[32];
   double2 *twsm = sm + (size_t)F.TM * F.N();
   double2 *cb = twsm + F.N();
+  double2 *acc = cb + 256;
   load_tables(twsm, tw, F.N(), cb, book);
   const int64_t n = (int64_t)n1 * F.N();
-  const int m1_0 = blockIdx.x * F.TM;
-  double2 acc[8];
-#pragma unroll
-  for (int r = 0; r < 8; ++r) acc[r] = make_double2(0.0, 0.0);
-  double2 x[8];
-  for (int j = 0; j < L; ++j) {
-    const double2 *Yj = Y + (size_t)j * n + m1_0 + F.t;
-    if (F.jb < F.NR0()) {
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-        if (r < F.R0()) x[r] = Yj[(size_t)F.in_pos(r) * n1];
-    }
-    __syncthreads();  // previous j's last-stage shared-memory reads are done (and the tables are in)
-    F.template run<true>(x, sm, twsm);
-    if (F.jb < F.NRL()) {
-      const uint8_t *cj = codes + (size_t)j * n + m1_0 + F.t;
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-        if (r < F.RL()) acc[r] = cadd(acc[r], cmul(cb[cj[(int64_t)n1 * F.out_pos(r)]], x[r]));
-    }
-  }
   const double s = scale_p ? *scale_p : 1.0;
+  const bool ld = F.jb < F.NR0(), st = F.jb < F.NRL();
   double v[1] = {0.0};
-  if (F.jb < F.NRL()) {
+  for (int tile = blockIdx.x; tile < n1 / F.TM; tile += gridDim.x) {
+    const int m1_0 = tile * F.TM;
+    double2 yn[8];
+    auto fetch = [&](int j) {
+      const double2 *Yj = Y + (size_t)j * n + m1_0 + F.t;
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (r < F.RL()) {
-        const int64_t m = m1_0 + F.t + (int64_t)n1 * F.out_pos(r);
-        const double2 uv = cscale(__ldg(u + m), s);
-        const double2 am = cadd(cscale(uv, rsn), acc[r]);
-        if (mode != 1) a[m] = am;
-        v[0] += uv.x * am.x + uv.y * am.y;
+      for (int r = 0; r < 8; ++r)
+        if (r < F.R0()) yn[r] = Yj[(size_t)F.in_pos(r) * n1];
+    };
+    if (ld) fetch(0);
+    if (st) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r < F.RL()) acc[F.out_pos(r) * F.TM + F.t] = make_double2(0.0, 0.0);
+    }
+    for (int j = 0; j < L; ++j) {
+      double2 x[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) x[r] = yn[r];
+      if (PF && ld && j + 1 < L) fetch(j + 1);
+      __syncthreads();  // the tables are in (first pass); previous shared-memory reads are done
+      F.template run<true>(x, sm, twsm);
+      if (!PF && ld && j + 1 < L) fetch(j + 1);
+      if (st) {
+        const uint8_t *cj = codes + (size_t)j * n + m1_0 + F.t;
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          if (r < F.RL()) {
+            const int pos = F.out_pos(r);
+            acc[pos * F.TM + F.t] = cadd(acc[pos * F.TM + F.t], cmul(cb[__ldg(cj + (int64_t)n1 * pos)], x[r]));
+          }
       }
+    }
+    if (st) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r < F.RL()) {
+          const int pos = F.out_pos(r);
+          const int64_t m = m1_0 + F.t + (int64_t)n1 * pos;
+          const double2 uv = cscale(__ldg(u + m), s);
+          const double2 am = cadd(cscale(uv, rsn), acc[pos * F.TM + F.t]);
+          if (mode != 1) a[m] = am;
+          v[0] += uv.x * am.x + uv.y * am.y;
+        }
+    }
   }
   if (mode == 2) return;
   if (grid_sum<1>(v, partials, &sc->ticket[1], red) && threadIdx.x == 0) {
@@ -557,22 +613,24 @@ __global__ void __launch_bounds__(512) k_pr_c(const double2 *__restrict__ Y, con
 // Kernel variants: compile-time plans for the sub-lengths of the paper's n = 10^4..10^6
 // (100, 250, 400, 1000) with TM = 2 or 4 transforms per block; any other length runs the runtime plan.
 typedef void (*F1Fn)(const double2 *, const double *, int, const PrScal *, const uint8_t *, const double2 *, double2 *,
-                     Plan, const double2 *, int, int, int);
+                     Plan, const double2 *, int, int, int, int);
 typedef void (*BFn)(double2 *, const double *, double *, int, int, const PrScal *, Plan, const double2 *,
-                    const double2 *, const double2 *, int, int, int);
+                    const double2 *, const double2 *, int, int, int, int);
 typedef void (*CFn)(const double2 *, const double2 *, const double *, double2 *, const uint8_t *, const double2 *, Plan,
                     const double2 *, int, int, int, int, double, int, int, PrScal *, double *);
 struct Variant {
   int N, TM;
-  F1Fn f1;
-  BFn b;
-  CFn c;
+  F1Fn f1, f1n;  // with / without the register prefetch of the next tile
+  BFn b, bn;
+  CFn c, cn;
 };
-#define SCG_PR_VARIANT(N, TM) {N, TM, k_pr_f1<N, TM>, k_pr_b<N, TM>, k_pr_c<N, TM>}
+#define SCG_PR_VARIANT(N, TM)                                                                      \
+  {N, TM, k_pr_f1<N, TM, true>, k_pr_f1<N, TM, false>, k_pr_b<N, TM, true>, k_pr_b<N, TM, false>, \
+   k_pr_c<N, TM, true>, k_pr_c<N, TM, false>}
 const Variant kVariants[] = {SCG_PR_VARIANT(100, 4), SCG_PR_VARIANT(250, 4), SCG_PR_VARIANT(400, 4),
                              SCG_PR_VARIANT(1000, 2), SCG_PR_VARIANT(100, 2), SCG_PR_VARIANT(250, 2),
                              SCG_PR_VARIANT(400, 2)};
-const Variant kGeneric = {0, 0, k_pr_f1<0, 0>, k_pr_b<0, 0>, k_pr_c<0, 0>};
+const Variant kGeneric = SCG_PR_VARIANT(0, 0);
 const Variant *find_variant(int N, int TM) {
   for (const Variant &v : kVariants)
     if (v.N == N && v.TM == TM) return &v;
@@ -1071,9 +1129,13 @@ static const char *kKsNames[KS_COUNT] = {"k_pr_start", "k_pr_f1", "k_pr_b", "k_p
 struct scg_pr_ctx {
   int64_t n;
   int L, R, n1, n2, tm1, tm2, nthr1, nthr2;
-  size_t smem1, smem2;
+  size_t smem1, smem2, smemc;
+  int gf1, gb, gc;  // persistent grids of the FFT kernels
   Plan P1, P2;  // P1: length n1 (k_pr_b), P2: length n2 (k_pr_f1 / k_pr_c)
   const Variant *v1, *v2;  // v1: k_pr_f1 / k_pr_c (length n2, tm1), v2: k_pr_b (length n1, tm2)
+  F1Fn kf1;
+  BFn kb;
+  CFn kc;
   double alpha, beta0, opnorm, rsn;
   uint64_t seed;
   uint32_t flags;
@@ -1164,18 +1226,17 @@ static void set_bytes(scg_pr_ctx *c) {
 
 static int launch_matvec(scg_pr_ctx *c, const double2 *x, const double *scale_p, double2 *out, int step,
                          int mode /* 0 lanczos, 1 monitor, 2 hook */) {
-  dim3 g1(c->n1 / c->tm1, c->L), g2(c->n2 / c->tm2, c->L);
   prof_begin(c, mode == 1 ? KS_F1M : KS_F1);
-  c->v1->f1<<<g1, c->nthr1, c->smem1, c->st>>>(x, scale_p, step, c->sc, c->codes, c->book, c->Y, c->P2, c->tw2, c->n1,
-                                              c->n2, c->tm1);
+  c->kf1<<<c->gf1, c->nthr1, c->smem1, c->st>>>(x, scale_p, step, c->sc, c->codes, c->book, c->Y, c->P2, c->tw2,
+                                                   c->n1, c->n2, c->tm1, c->L);
   prof_end(c);
   prof_begin(c, mode == 1 ? KS_BM : KS_B);
-  c->v2->b<<<g2, c->nthr2, c->smem2, c->st>>>(c->Y, c->wk, c->h, mode == 1 ? 1 : 0, step, c->sc, c->P1, c->tw1, c->twlo,
-                                             c->twhi, c->n1, c->n2, c->tm2);
+  c->kb<<<c->gb, c->nthr2, c->smem2, c->st>>>(c->Y, c->wk, c->h, mode == 1 ? 1 : 0, step, c->sc, c->P1, c->tw1,
+                                                 c->twlo, c->twhi, c->n1, c->n2, c->tm2, c->L);
   prof_end(c);
   prof_begin(c, mode == 1 ? KS_CM : KS_C);
-  c->v1->c<<<c->n1 / c->tm1, c->nthr1, c->smem1, c->st>>>(c->Y, x, scale_p, out, c->codes, c->book, c->P2, c->tw2, c->n1,
-                                                         c->n2, c->tm1, c->L, c->rsn, mode, step, c->sc, c->partials);
+  c->kc<<<c->gc, c->nthr1, c->smemc, c->st>>>(c->Y, x, scale_p, out, c->codes, c->book, c->P2, c->tw2, c->n1,
+                                                 c->n2, c->tm1, c->L, c->rsn, mode, step, c->sc, c->partials);
   prof_end(c);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -1277,10 +1338,14 @@ int scg_pr_init(int64_t n, int32_t L, const double *psi, const double *b, int32_
   c->v2 = find_variant(n1, c->tm2);
   if (!c->v1 || (flags & SCG_PR_GENERIC)) c->v1 = &kGeneric;
   if (!c->v2 || (flags & SCG_PR_GENERIC)) c->v2 = &kGeneric;
+  c->kf1 = (flags & SCG_PR_NOPF_F1) ? c->v1->f1n : c->v1->f1;
+  c->kb = (flags & SCG_PR_NOPF_B) ? c->v2->bn : c->v2->b;
+  c->kc = (flags & SCG_PR_NOPF_C) ? c->v1->cn : c->v1->c;
   c->nthr1 = c->tm1 * (n2 / plan_rmin(P2));
   c->nthr2 = c->tm2 * (n1 / plan_rmin(P1));
   c->smem1 = sizeof(double2) * ((size_t)c->tm1 * n2 + n2 + 256);
   c->smem2 = sizeof(double2) * ((size_t)c->tm2 * n1 + n1);
+  c->smemc = c->smem1 + sizeof(double2) * (size_t)c->tm1 * n2;
   const int rc = pr_init_device(c, codes, book, b);
   if (rc != SCG_OK) {
     scg_pr_destroy(c);
@@ -1300,9 +1365,20 @@ static int pr_init_device(scg_pr_ctx *c, const std::vector<uint8_t> &codes, cons
   const uint64_t seed = c->seed;
   const uint32_t flags = c->flags;
   PR_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
-  PR_CUDA(cudaFuncSetAttribute(c->v1->f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
-  PR_CUDA(cudaFuncSetAttribute(c->v1->c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
-  PR_CUDA(cudaFuncSetAttribute(c->v2->b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem2));
+  PR_CUDA(cudaFuncSetAttribute(c->kf1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
+  PR_CUDA(cudaFuncSetAttribute(c->kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smemc));
+  PR_CUDA(cudaFuncSetAttribute(c->kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem2));
+  {  // persistent grids: resident blocks per SM x SMs, capped at the tile counts
+    int dev = 0, sms = 148, o1 = 1, o2 = 1, o3 = 1;
+    PR_CUDA(cudaGetDevice(&dev));
+    PR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, c->kf1, c->nthr1, c->smem1));
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, c->kb, c->nthr2, c->smem2));
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, c->kc, c->nthr1, c->smemc));
+    c->gf1 = (int)std::min<int64_t>((int64_t)std::max(o1, 1) * sms, (int64_t)(n1 / c->tm1) * L);
+    c->gb = (int)std::min<int64_t>((int64_t)std::max(o2, 1) * sms, (int64_t)(n2 / c->tm2) * L);
+    c->gc = (int)std::min<int64_t>((int64_t)std::max(o3, 1) * sms, (int64_t)(n1 / c->tm1));
+  }
   const size_t dn = (size_t)L * n;
   PR_CUDA(cudaMalloc(&c->codes, dn));
   PR_CUDA(cudaMalloc(&c->book, sizeof(double2) * 256));
@@ -1516,37 +1592,41 @@ int scg_pr_reconstruct(scg_pr_ctx *c, double *Uout, double *Lam) {
   herm_eig(G, R, w, E);
   const double nrm = std::sqrt(std::max(w[R - 1], 0.0));
   std::vector<double2> Mh((size_t)R * R);
-  if (nrm == 0.0) return SCG_ESTATE;
-  double nu = std::sqrt((double)n) * matlab_eps(nrm);  // Alg. 3 line 1
-  bool ok = false;
-  for (int attempt = 0; attempt < 40; ++attempt) {
-    // B = Omega^* (S + nu Omega)  (line 2-3)
-    std::vector<double2> I((size_t)R * R, make_double2(0.0, 0.0));
-    for (int i = 0; i < R; ++i) I[(size_t)i * R + i] = make_double2(1.0, 0.0);
-    double2 *dM = c->Mx;
-    PR_CUDA(cudaMemcpyAsync(dM, I.data(), sizeof(double2) * R * R, cudaMemcpyHostToDevice, c->st));
-    k_pr_rmul<<<grid_for(n, 256), 256, 0, c->st>>>(c->S, c->Om, nu, dM, n, R, c->tmpA);  // S_nu
-    rc = gram(c, c->Om, c->tmpA, G);
-    if (rc) return rc;
-    std::vector<cplx> B((size_t)R * R);
-    for (int i = 0; i < R; ++i)
-      for (int j = 0; j < R; ++j) B[(size_t)i * R + j] = 0.5 * (G[(size_t)i * R + j] + std::conj(G[(size_t)j * R + i]));
-    if (chol_upper(B, R, C)) {
-      ok = true;
-      break;
-    }
-    nu *= 2.0;
-  }
-  if (!ok) return SCG_ECHOL;
-  // Y = S_nu C^{-1} (line 4), then CholQR: Q = Y R1^{-1}, and the SVD of the R x R factor
-  std::vector<cplx> Ci = inv_upper(C, R);
+  // S = 0 (no iteration took H = v v^*): X^ = 0 -- Lam = 0 with an orthonormal basis of range(Omega)
+  const bool zero = nrm == 0.0;
+  double nu = zero ? 0.0 : std::sqrt((double)n) * matlab_eps(nrm);  // Alg. 3 line 1
   double2 *dM = c->Mx;
   auto upload = [&](const std::vector<cplx> &M) {
     for (int i = 0; i < R * R; ++i) Mh[i] = make_double2(M[i].real(), M[i].imag());
     return cudaMemcpyAsync(dM, Mh.data(), sizeof(double2) * R * R, cudaMemcpyHostToDevice, c->st);
   };
-  PR_CUDA(upload(Ci));
-  k_pr_rmul<<<grid_for(n, 256), 256, 0, c->st>>>(c->tmpA, nullptr, 0.0, dM, n, R, c->tmpB);  // Y
+  if (zero) {
+    PR_CUDA(cudaMemcpyAsync(c->tmpB, c->Om, sizeof(double2) * (size_t)R * n, cudaMemcpyDeviceToDevice, c->st));
+  } else {
+    bool ok = false;
+    for (int attempt = 0; attempt < 40; ++attempt) {
+      // B = Omega^* (S + nu Omega)  (line 2-3)
+      std::vector<double2> I((size_t)R * R, make_double2(0.0, 0.0));
+      for (int i = 0; i < R; ++i) I[(size_t)i * R + i] = make_double2(1.0, 0.0);
+      PR_CUDA(cudaMemcpyAsync(dM, I.data(), sizeof(double2) * R * R, cudaMemcpyHostToDevice, c->st));
+      k_pr_rmul<<<grid_for(n, 256), 256, 0, c->st>>>(c->S, c->Om, nu, dM, n, R, c->tmpA);  // S_nu
+      rc = gram(c, c->Om, c->tmpA, G);
+      if (rc) return rc;
+      std::vector<cplx> B((size_t)R * R);
+      for (int i = 0; i < R; ++i)
+        for (int j = 0; j < R; ++j) B[(size_t)i * R + j] = 0.5 * (G[(size_t)i * R + j] + std::conj(G[(size_t)j * R + i]));
+      if (chol_upper(B, R, C)) {
+        ok = true;
+        break;
+      }
+      nu *= 2.0;
+    }
+    if (!ok) return SCG_ECHOL;
+    // Y = S_nu C^{-1} (line 4), then CholQR: Q = Y R1^{-1}, and the SVD of the R x R factor
+    std::vector<cplx> Ci = inv_upper(C, R);
+    PR_CUDA(upload(Ci));
+    k_pr_rmul<<<grid_for(n, 256), 256, 0, c->st>>>(c->tmpA, nullptr, 0.0, dM, n, R, c->tmpB);  // Y
+  }
   // two CholQR rounds: Y = Q Rt
   std::vector<cplx> Rt((size_t)R * R, cplx(0.0, 0.0));
   for (int i = 0; i < R; ++i) Rt[(size_t)i * R + i] = 1.0;
@@ -1575,7 +1655,7 @@ int scg_pr_reconstruct(scg_pr_ctx *c, double *Uout, double *Lam) {
   c->lam.assign(R, 0.0);
   for (int col = 0; col < R; ++col) {
     const int s = R - 1 - col;
-    c->lam[col] = std::max(w[s] - nu, 0.0);
+    c->lam[col] = zero ? 0.0 : std::max(w[s] - nu, 0.0);
     for (int r = 0; r < R; ++r) Wd[(size_t)r * R + col] = E[(size_t)r * R + s];
   }
   PR_CUDA(upload(Wd));
@@ -1627,11 +1707,10 @@ int scg_pr_measure(scg_pr_ctx *c, const double *x, double *hout) {
   PR_CUDA(cudaStreamSynchronize(c->st));
   double2 *xd = c->a;
   PR_CUDA(cudaMemcpyAsync(xd, x, sizeof(double2) * n, cudaMemcpyHostToDevice, c->st));
-  dim3 g1(c->n1 / c->tm1, c->L), g2(c->n2 / c->tm2, c->L);
-  c->v1->f1<<<g1, c->nthr1, c->smem1, c->st>>>(xd, nullptr, 0, c->sc, c->codes, c->book, c->Y, c->P2, c->tw2, c->n1,
-                                              c->n2, c->tm1);
-  c->v2->b<<<g2, c->nthr2, c->smem2, c->st>>>(c->Y, c->wk, c->h, 2, 0, c->sc, c->P1, c->tw1, c->twlo, c->twhi, c->n1,
-                                             c->n2, c->tm2);
+  c->kf1<<<c->gf1, c->nthr1, c->smem1, c->st>>>(xd, nullptr, 0, c->sc, c->codes, c->book, c->Y, c->P2, c->tw2,
+                                                   c->n1, c->n2, c->tm1, c->L);
+  c->kb<<<c->gb, c->nthr2, c->smem2, c->st>>>(c->Y, c->wk, c->h, 2, 0, c->sc, c->P1, c->tw1, c->twlo, c->twhi,
+                                                 c->n1, c->n2, c->tm2, c->L);
   double *tmp = reinterpret_cast<double *>(c->Y);
   k_pr_perm<<<grid_for(dn, 256), 256, 0, c->st>>>(c->h, tmp, c->n1, c->n2, c->L, c->kappa, 1.0, 0);
   PR_CUDA(cudaGetLastError());

@@ -101,7 +101,7 @@ class PhaseRetrieval:
     """SketchyCGAL on the phase retrieval SDP (scg_pr_init ... scg_pr_destroy), one GPU."""
 
     def __init__(self, psi, b, R: int = 5, alpha: float | None = None, beta0: float = 1.0, seed: int = 0,
-                 profile: bool = False, device: int = 0):
+                 profile: bool = False, device: int = 0, flags: int = 0):
         import torch  # device selection only
         torch.cuda.set_device(device)
         self.lib = load()
@@ -112,7 +112,7 @@ class PhaseRetrieval:
         self.alpha = 3.0 * self.n if alpha is None else float(alpha)
         h = ctypes.c_void_p()
         st = self.lib.scg_pr_init(self.n, self.L, psi.ctypes.data, b.ctypes.data, self.R, self.alpha, float(beta0),
-                                  int(seed), SCG_PR_PROFILE if profile else 0, ctypes.byref(h))
+                                  int(seed), (SCG_PR_PROFILE if profile else 0) | int(flags), ctypes.byref(h))
         self._check(st, "scg_pr_init")
         self._h = h
 

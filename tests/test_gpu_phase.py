@@ -121,3 +121,21 @@ def test_full_size_first_iteration_p6(pr):
     assert abs(gl[0, 4] - ol[0, 4]) <= 1e-8 * abs(ol[0, 4])
     assert _rel(g.state("z"), o.z) < 1e-6
     assert _rel(g.state("y"), o.y) < 1e-6
+
+
+def test_reconstruct_before_any_rank_one_update(pr):
+    """While xi_t >= 0 the trace-bounded LMO returns H = 0 and S stays 0: the
+    reconstruction is X^ = 0 (Lam = 0, U an orthonormal basis), like the oracle's."""
+    n = 100
+    I = si.phase_instance(n, seed=0)
+    g = pr.PhaseRetrieval(I.psi, I.b, R=5, seed=0)
+    o = ph.PhaseOracle(I.psi, I.b, R=5, seed=0)
+    g.step(3)
+    o.step(3)
+    assert np.all(o.logarr[:, 4] >= 0) and np.all(g.iter_log()[:, 4] >= 0)
+    assert not np.any(g.state("S"))
+    U, lam = g.reconstruct()
+    Uo, lamo = o.reconstruct()
+    assert np.all(lam == 0) and np.all(lamo == 0)
+    assert np.allclose(U.conj().T @ U, np.eye(5), atol=1e-12)
+    assert not np.any(g.signal())

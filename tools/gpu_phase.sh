@@ -6,8 +6,8 @@ O=gpurun_out/$TAG; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo "build exit $?" >> $O/build.log
 for w in "$@"; do
   case $w in
-    quick:*) S=${w#quick:}; N=${S%%:*}; T=${S#*:}
-      timeout 600 python tools/phase_quick.py $N $T > $O/quick_${N}_${T}.log 2>&1 ;;
+    quick:*) S=${w#quick:}; N=${S%%:*}; R1=${S#*:}; T=${R1%%:*}; FL=${R1#*:}; [ "$FL" = "$R1" ] && FL=0
+      timeout 600 python tools/phase_quick.py $N $T $FL > $O/quick_${N}_${T}_${FL}.log 2>&1 ;;
     tests) timeout 1500 python -m pytest tests/test_gpu_phase.py -q -x --durations=20 > $O/pytest_phase.log 2>&1; echo "pytest exit $?" >> $O/pytest_phase.log ;;
     ncu:*) S=${w#ncu:}; KRE=${S%%:*}; R1=${S#*:}; N=${R1%%:*}; R2=${R1#*:}; T=${R2%%:*}; SKIP=${R2#*:}
       NM=${KRE//[^a-zA-Z0-9_]/_}_$N
