@@ -286,6 +286,9 @@ struct Sub {
   __device__ __forceinline__ int NR0() const { return N() / R0(); }
   __device__ __forceinline__ int NRL() const { return N() / RL(); }
   __device__ __forceinline__ int in_pos(int r) const { return jb + r * NR0(); }
+  __device__ __forceinline__ int out_stride() const {
+    if constexpr (CT) { constexpr CPlan c = make_cplan(NC); return c.Ns[c.ns - 1]; } else { return P.Ns[P.ns - 1]; }
+  }
   __device__ __forceinline__ int out_pos(int r) const {
     if constexpr (CT) {
       constexpr CPlan c = make_cplan(NC);
@@ -524,11 +527,14 @@ __global__ void __launch_bounds__(512) k_pr_b(double2 *__restrict__ Y, const dou
     F.template run<true>(x, sm, twsm);
     if (F.jb < F.NRL()) {
       double2 *row = Y + base;
+      // w_n^{-m1 k2} for m1 = out_pos(0) + r Ns_last: base times powers
+      const double2 v1 = twn(twlo, twhi, (long long)F.out_stride() * k2);
+      double2 v = twn(twlo, twhi, (long long)F.out_pos(0) * k2);
 #pragma unroll
       for (int r = 0; r < 8; ++r)
         if (r < F.RL()) {
-          const int m1 = F.out_pos(r);
-          row[m1] = cmulc(x[r], twn(twlo, twhi, (long long)m1 * k2));
+          row[F.out_pos(r)] = cmulc(x[r], v);
+          v = cmul(v, v1);
         }
     }
   }
