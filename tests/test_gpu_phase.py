@@ -139,3 +139,60 @@ def test_reconstruct_before_any_rank_one_update(pr):
     assert np.all(lam == 0) and np.all(lamo == 0)
     assert np.allclose(U.conj().T @ U, np.eye(5), atol=1e-12)
     assert not np.any(g.signal())
+
+
+@pytest.mark.parametrize("flags", [1 << 10, (1 << 11) | (1 << 12) | (1 << 13), 1 << 9])
+def test_execution_options_agree(pr, flags):
+    """SCG_PR_GENERIC (runtime radix plans), SCG_PR_NOPF_* (no next-tile prefetch) and SCG_PR_TM2 give
+    the same operator and iterates within the FFT's rounding as the default kernels (n = 10^4: the
+    compile-time 100 x 100 plan)."""
+    n = 10000
+    I = si.phase_instance(n, seed=6)
+    a = pr.PhaseRetrieval(I.psi, I.b, R=5, seed=6)
+    b = pr.PhaseRetrieval(I.psi, I.b, R=5, seed=6, flags=flags)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    w = rng.standard_normal((12, n))
+    assert _rel(b.apply_D(w, x), a.apply_D(w, x)) < 1e-13
+    assert _rel(b.measure(x), a.measure(x)) < 1e-13
+    a.step(15)
+    b.step(15)
+    la, lb = a.iter_log(), b.iter_log()
+    np.testing.assert_array_equal(la[:, 1:3], lb[:, 1:3])
+    assert np.max(np.abs(la[:, 3] - lb[:, 3])) <= 1e-9 * np.abs(la[:, 3]).max()
+    assert _rel(b.state("z"), a.state("z")) < 1e-8
+
+
+@pytest.mark.parametrize("L,R", [(1, 1), (3, 2), (32, 16)])
+def test_other_modulation_counts_and_ranks(pr, L, R):
+    """The boundary's limits: L = 1..32 modulations, R = 1..16 (include/scg_phase.h), vs the oracle."""
+    n = 360  # 18 x 20: runtime plans with radix 3
+    psi = si.phase_psi(n, seed=9, L=L)
+    chi = si.phase_signal(n, seed=9)
+    b = np.abs(np.fft.fft(np.conj(psi) * chi[None, :], axis=1)) ** 2
+    g = pr.PhaseRetrieval(psi, b, R=R, seed=9)
+    o = ph.PhaseOracle(psi, b, R=R, seed=9)
+    kappa, _ = ph.scaling(psi, b, 3.0 * n)
+    np.testing.assert_allclose(g.state("kappa"), kappa, rtol=1e-12)
+    g.step(20)
+    o.step(20)
+    gl, ol = g.iter_log(), o.logarr
+    np.testing.assert_array_equal(gl[:, 1:3], ol[:, 1:3])
+    assert np.max(np.abs(gl[:, 3] - ol[:, 3])) <= 1e-8 * np.abs(ol[:, 3]).max()
+    assert _rel(g.state("z"), o.z) < 1e-6
+    assert _rel(g.state("S"), o.S) < 1e-6 or not np.any(o.S)
+
+
+def test_q_cap_on_tiny_n(pr):
+    """n = 6 (2 x 3): from t ~ 64 on, q_t = min(n - 1, ...) caps the Lanczos steps (P:1451 with
+    Alg. 2's min{q, n - 1}); GPU and oracle agree on q_t, k_t and theta_t."""
+    n = 6
+    I = si.phase_instance(n, seed=2)
+    g = pr.PhaseRetrieval(I.psi, I.b, R=3, seed=2)
+    o = ph.PhaseOracle(I.psi, I.b, R=3, seed=2)
+    g.step(120)
+    o.step(120)
+    gl, ol = g.iter_log(), o.logarr
+    np.testing.assert_array_equal(gl[:, 1:3], ol[:, 1:3])
+    assert gl[:, 1].max() == n - 1 and np.sum(gl[:, 1] == n - 1) > 20
+    assert np.max(np.abs(gl[:, 3] - ol[:, 3])) <= 1e-8 * np.abs(ol[:, 3]).max()
