@@ -91,15 +91,16 @@ class ClockSampler:
 def _ncu_traffic(kernel_name: str, cfg: str):
     """dram bytes per launch of the dominant kernel from the committed ncu --set full summary of the SAME
     workload (profiles/ncu_full_summary.json "workload" must equal --config), else None."""
-    path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
-    try:
-        with open(path) as f:
-            js = json.load(f)
-        ent = js.get("kernels", {}).get(kernel_name)
-        if ent and js.get("workload") == cfg:
-            return float(ent["dram_bytes"])
-    except Exception:
-        pass
+    for path in (os.path.join(ROOT, "profiles", f"ncu_full_summary_{cfg}.json"),
+                 os.path.join(ROOT, "profiles", "ncu_full_summary.json")):
+        try:
+            with open(path) as f:
+                js = json.load(f)
+            ent = js.get("kernels", {}).get(kernel_name)
+            if ent and js.get("workload") == cfg:
+                return float(ent["dram_bytes"])
+        except Exception:
+            pass
     return None
 
 
@@ -496,7 +497,8 @@ def run_phase(args, rank, local_rank, world=1):
             "dtype": "c128", "data": "synthetic", "config": _phase_config(args.config, W + 1, W + K, world),
             "roofline": None if top is None else {
                 "bound": "hbm", "kernel": top["name"], "achieved": round(gbs(top), 1), "peak": peak,
-                "peak_kind": peak_kind, "unit": "GB/s", "frac": gbs(top) / peak, "traffic": None,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": gbs(top) / peak,
+                "traffic": _ncu_traffic(top["name"], args.config),
                 "algorithmic_bytes_per_launch": top["bytes_per_launch"]},
             "fft_matvec": {"kernels": [s["name"] for s in mv], "achieved": round(mv_bytes / mv_sec / 1e9, 1) if mv_sec else None,
                            "peak": peak, "unit": "GB/s", "frac": (mv_bytes / mv_sec / 1e9) / peak if mv_sec else None,

@@ -40,7 +40,7 @@ rd = sum(nbytes(d, "dram__bytes_read.sum") for d in launches) / len(launches)
 wr = sum(nbytes(d, "dram__bytes_write.sum") for d in launches) / len(launches)
 tu = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(units.get("gpu__time_duration.sum", "usecond"), 1.0)
 dur = sum(num(d, "gpu__time_duration.sum") for d in launches) / len(launches) * tu
-path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+path = os.path.join(ROOT, "profiles", "ncu_full_summary.json" if workload == "c3" else f"ncu_full_summary_{workload}.json")
 try:
     js = json.load(open(path))
 except Exception:
