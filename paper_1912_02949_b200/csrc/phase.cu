@@ -229,6 +229,21 @@ __device__ __forceinline__ void fft_stages(double2 (&x)[8], double2 *sm, const P
   }
 }
 
+// Shared-memory swizzle of the compile-time plans (element e = i * TM + t): chosen by a bank-conflict
+// simulation of every stage's 128-bit accesses (8 lanes per wavefront): the radix-8 first stage stores
+// with a stride of 8 TM elements.  (1000, 2): XOR of the 8-element group index into the low bits (no
+// padding, conflict-free); TM = 4: two pad elements per 8 (conflict-free for 100 and 400).
+template <int N, int TM>
+__host__ __device__ constexpr int swz(int e) {
+  if constexpr (N == 1000 && TM == 2) return (e & ~7) | ((e ^ (e >> 3)) & 7);
+  else if constexpr (TM == 4) return e + ((e >> 3) << 1);
+  else return e;
+}
+// transform buffer (double2 elements) of TM transforms of length N, room for the padded swizzle
+__host__ __device__ constexpr size_t fft_buf(int TM, int N) {
+  return (size_t)TM * N + (((size_t)TM * N) >> 3) * 2 + 8;
+}
+
 // ---- compile-time plan (the hot lengths): every index is a constant expression.
 template <int N, int S, bool INV, int TM>
 __device__ __forceinline__ void ct_stage(double2 (&x)[8], double2 *sm, const double2 *tw, int t, int jb) {
@@ -238,7 +253,7 @@ __device__ __forceinline__ void ct_stage(double2 (&x)[8], double2 *sm, const dou
   if constexpr (S > 0) {
     if (act) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) x[r] = sm[(jb + r * NR) * TM + t];
+      for (int r = 0; r < R; ++r) x[r] = sm[swz<N, TM>((jb + r * NR) * TM + t)];
     }
     __syncthreads();
   }
@@ -258,7 +273,7 @@ __device__ __forceinline__ void ct_stage(double2 (&x)[8], double2 *sm, const dou
     if (act) {
       const int k = jb % Ns, idxD = (jb / Ns) * Ns * R + k;
 #pragma unroll
-      for (int r = 0; r < R; ++r) sm[(idxD + r * Ns) * TM + t] = x[r];
+      for (int r = 0; r < R; ++r) sm[swz<N, TM>((idxD + r * Ns) * TM + t)] = x[r];
     }
     __syncthreads();
     ct_stage<N, S + 1, INV, TM>(x, sm, tw, t, jb);
@@ -286,6 +301,12 @@ struct Sub {
   __device__ __forceinline__ int NR0() const { return N() / R0(); }
   __device__ __forceinline__ int NRL() const { return N() / RL(); }
   __device__ __forceinline__ int in_pos(int r) const { return jb + r * NR0(); }
+  // shared-memory slot of element i of this thread's transform
+  __device__ __forceinline__ int slot(int i) const {
+    if constexpr (CT) return swz<NC, TMC>(i * TMC + t);
+    else return i * TM + t;
+  }
+  __device__ __forceinline__ size_t buf() const { return fft_buf(TM, N()); }
   __device__ __forceinline__ int out_stride() const {
     if constexpr (CT) { constexpr CPlan c = make_cplan(NC); return c.Ns[c.ns - 1]; } else { return P.Ns[P.ns - 1]; }
   }
@@ -406,7 +427,7 @@ __global__ void __launch_bounds__(512) k_pr_f1(const double2 *__restrict__ u, co
   if (skip_step(sc, step)) return;
   const Sub<NC, TMC> F(P, TMr);
   extern __shared__ double2 sm[];
-  double2 *twsm = sm + (size_t)F.TM * F.N();
+  double2 *twsm = sm + F.buf();
   double2 *cb = twsm + F.N();
   load_tables(twsm, tw, F.N(), cb, book);
   __syncthreads();
@@ -461,7 +482,7 @@ __global__ void __launch_bounds__(512) k_pr_b(double2 *__restrict__ Y, const dou
   if (skip_step(sc, step)) return;
   const Sub<NC, TMC> F(P, TMr);
   extern __shared__ double2 sm[];
-  double2 *twsm = sm + (size_t)F.TM * F.N();
+  double2 *twsm = sm + F.buf();
   load_tables(twsm, tw, F.N(), nullptr, nullptr);
   __syncthreads();
   const int n1c = F.N();
@@ -514,13 +535,13 @@ __global__ void __launch_bounds__(512) k_pr_b(double2 *__restrict__ Y, const dou
     if (F.jb < F.NRL()) {
 #pragma unroll
       for (int r = 0; r < 8; ++r)
-        if (r < F.RL()) sm[F.out_pos(r) * F.TM + F.t] = x[r];
+        if (r < F.RL()) sm[F.slot(F.out_pos(r))] = x[r];
     }
     __syncthreads();
     if (ld) {
 #pragma unroll
       for (int r = 0; r < 8; ++r)
-        if (r < F.R0()) x[r] = sm[F.in_pos(r) * F.TM + F.t];
+        if (r < F.R0()) x[r] = sm[F.slot(F.in_pos(r))];
     }
     __syncthreads();
     if (!PF && ld && tile + (int)gridDim.x < ntiles) fetch(tile + gridDim.x);
@@ -555,7 +576,7 @@ __global__ void __launch_bounds__(512) k_pr_c(const double2 *__restrict__ Y, con
   const Sub<NC, TMC> F(P, TMr);
   extern __shared__ double2 sm[];
   __shared__ double red[32];
-  double2 *twsm = sm + (size_t)F.TM * F.N();
+  double2 *twsm = sm + F.buf();
   double2 *cb = twsm + F.N();
   double2 *acc = cb + 256;
   load_tables(twsm, tw, F.N(), cb, book);
@@ -1349,8 +1370,8 @@ int scg_pr_init(int64_t n, int32_t L, const double *psi, const double *b, int32_
   c->kc = (flags & SCG_PR_NOPF_C) ? c->v1->cn : c->v1->c;
   c->nthr1 = c->tm1 * (n2 / plan_rmin(P2));
   c->nthr2 = c->tm2 * (n1 / plan_rmin(P1));
-  c->smem1 = sizeof(double2) * ((size_t)c->tm1 * n2 + n2 + 256);
-  c->smem2 = sizeof(double2) * ((size_t)c->tm2 * n1 + n1);
+  c->smem1 = sizeof(double2) * (fft_buf(c->tm1, n2) + n2 + 256);
+  c->smem2 = sizeof(double2) * (fft_buf(c->tm2, n1) + n1);
   c->smemc = c->smem1 + sizeof(double2) * (size_t)c->tm1 * n2;
   const int rc = pr_init_device(c, codes, book, b);
   if (rc != SCG_OK) {
