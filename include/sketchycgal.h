@@ -87,8 +87,11 @@ enum {
   SCG_FUSED_RNG = 1u << 15,     /* one GPU: draw the next Lanczos start vector inside the dual-update kernel instead of
                                    on a lower-priority side stream overlapped with the Lanczos passes (sharded runs
                                    always draw inside the dual kernel) */
-  SCG_NO_RESIDENT = 1u << 17    /* one GPU, n <= 65536: keep the multi-kernel iteration instead of one launch of one
+  SCG_NO_RESIDENT = 1u << 17,   /* one GPU, n <= 65536: keep the multi-kernel iteration instead of one launch of one
                                    thread-block cluster per iteration (k_resident) */
+  SCG_SERIAL_RNG = 1u << 18     /* one GPU: draw the next start vector with the full-grid kernel on the main stream
+                                   (serial, no overlap with the Lanczos kernels) instead of the low-priority side
+                                   stream; bitwise-neutral execution option */
 };
 
 /* This rank's rows [row_begin, row_end) of the symmetric weighted Laplacian

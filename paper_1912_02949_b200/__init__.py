@@ -36,6 +36,7 @@ SCG_DEBUG_LOG = 1 << 13
 SCG_NO_ELL = 1 << 14
 SCG_FUSED_RNG = 1 << 15
 SCG_NO_RESIDENT = 1 << 17
+SCG_SERIAL_RNG = 1 << 18
 
 STATUS = {0: "SCG_OK", -1: "SCG_EINVAL", -2: "SCG_ENOMEM", -3: "SCG_ECUDA", -4: "SCG_ENCCL", -5: "SCG_ECHOL",
           -6: "SCG_ESTATE", -7: "SCG_ERANGE", -8: "SCG_EUNSUPPORTED", -9: "SCG_ECOMM"}
@@ -311,7 +312,8 @@ class SketchyCGAL:
                  box: tuple | None = None, ball: float | None = None,
                  l1_ball: float | None = None, pdl: bool = True, fused_pass1: bool = False, ws_spmv: bool = False,
                  tma_b: bool = False, debug_log: bool = False, qfix: int = 0, ell: bool = True,
-                 side_rng: bool = True, host_comm: "TorchHostComm | None" = None, resident: bool = True):
+                 side_rng: bool = True, host_comm: "TorchHostComm | None" = None, resident: bool = True,
+                 serial_rng: bool = False):
         self.lib = load()
         self.n = int(L.n)
         self.R = int(R)
@@ -345,7 +347,8 @@ class SketchyCGAL:
                 (SCG_TRACE_LE if trace_le else 0) | (SCG_INEQ if ineq else 0) | (0 if pdl else SCG_NO_PDL) | \
                 (SCG_FUSED_PASS1 if fused_pass1 else 0) | (SCG_WS_SPMV if ws_spmv else 0) | \
                 (SCG_TMA_B if tma_b else 0) | (SCG_DEBUG_LOG if debug_log else 0) | (0 if ell else SCG_NO_ELL) | \
-                (0 if side_rng else SCG_FUSED_RNG) | (0 if resident else SCG_NO_RESIDENT)
+                (0 if side_rng else SCG_FUSED_RNG) | (0 if resident else SCG_NO_RESIDENT) | \
+                (SCG_SERIAL_RNG if serial_rng else 0)
         self._h = ctypes.c_void_p()
         dptr = None
         if dist is not None:

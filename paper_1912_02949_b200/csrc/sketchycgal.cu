@@ -1652,12 +1652,16 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
     }
     if (c->side_rng) {  // draw g_{t+1} into the buffer iteration t-1 used, once its readers are done
       Shard *s = c->sh[0];
-      cudaEventRecord(c->evA, c->stream);
-      cudaStreamWaitEvent(c->side, c->evA, 0);
-      launch_on(c, c->side, false, KC_GEN, 8.0 * (double)s->nl, k_gen_start, dim3(grid_for(s->nl, 64 * c->nsm)),
+      // SCG_SERIAL_RNG: the same draw on the main stream, between iterations (no overlap with pass 1)
+      const bool ser = (c->flags & SCG_SERIAL_RNG) != 0;
+      if (!ser) {
+        cudaEventRecord(c->evA, c->stream);
+        cudaStreamWaitEvent(c->side, c->evA, 0);
+      }
+      launch_on(c, ser ? c->stream : c->side, false, KC_GEN, 8.0 * (double)s->nl, k_gen_start, dim3(grid_for(s->nl, 64 * c->nsm)),
                 dim3(kBlock), 0, c->gslot(s, t + 1), (int)s->nl, (long long)s->rb, c->seed, (long long)(t + 1),
                 s->slots + SLOT_GEN, s->sc, net_of(c, s, 0), (const int *)s->orig, (int)FK_GEN);
-      cudaEventRecord(c->evB, c->side);
+      if (!ser) cudaEventRecord(c->evB, c->side);
     }
     // ---- Lanczos pass 1 (Alg. 2 lines 1-9)
     if (c->fused && c->world == 1) {  // all q steps in one persistent launch
@@ -1774,7 +1778,7 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
       pull_all(c, FK_NZ, 1, E, f);
     }
     E = ++c->epoch;
-    if (c->side_rng) cudaStreamWaitEvent(c->stream, c->evB, 0);  // g_{t+1} and its norm are drawn
+    if (c->side_rng && !(c->flags & SCG_SERIAL_RNG)) cudaStreamWaitEvent(c->stream, c->evB, 0);  // g_{t+1} drawn
     for (Shard *s : c->sh) {
       auto kD = c->side_rng ? (ks == 1 ? k_dual_sketch<1, false> : k_dual_sketch<0, false>)
                             : (ks == 3 ? k_dual_sketch<3, true> : ks == 2 ? k_dual_sketch<2, true>

@@ -535,8 +535,8 @@ def test_sharded_rejects_asymmetric_pattern(gpu):
     gpu.SketchyCGAL(bad, R=4, seed=1).close()
 
 
-@pytest.mark.parametrize("resident", [False, True])
-def test_bench_launch_configuration_bitwise(gpu, resident):
+@pytest.mark.parametrize("resident,serial", [(False, False), (True, False), (False, True)])
+def test_bench_launch_configuration_bitwise(gpu, resident, serial):
     """The configuration bench.py times -- torch's stream passed in (high priority), SCG_PROFILE event
     sampling, programmatic dependent launches, the side-stream start vectors (multi-kernel) or the
     resident cluster kernel -- gives the oracle's bits (configs[1] shape, 200 iterations)."""
@@ -546,7 +546,7 @@ def test_bench_launch_configuration_bitwise(gpu, resident):
     stream = torch.cuda.Stream(priority=-100)
     with torch.cuda.stream(stream):
         g = gpu.SketchyCGAL(L, R=10, seed=1, profile=True, stream=ctypes.c_void_p(stream.cuda_stream),
-                            resident=resident)
+                            resident=resident, serial_rng=serial)
         g.step(3)
         g.synchronize()
         g.reset_stats()
