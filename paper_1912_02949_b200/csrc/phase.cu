@@ -39,6 +39,7 @@ constexpr int kRMax = 16;
 constexpr int kLMax = 32;
 constexpr int kMaxStages = 12;
 constexpr int kSubMax = 4096;
+constexpr int kXR = 10;  // largest radix (10: compile-time plans of powers of ten)
 
 typedef std::complex<double> cplx;
 
@@ -116,7 +117,7 @@ __device__ __forceinline__ void dft5(double2 &x0, double2 &x1, double2 &x2, doub
   x3 = csub(a2, b2);
 }
 template <bool INV>
-__device__ __forceinline__ void dft8(double2 (&x)[8]) {
+__device__ __forceinline__ void dft8(double2 (&x)[kXR]) {
   const double r = 0.70710678118654752440;
   dft4<INV>(x[0], x[2], x[4], x[6]);
   dft4<INV>(x[1], x[3], x[5], x[7]);
@@ -137,13 +138,41 @@ __device__ __forceinline__ void dft8(double2 (&x)[8]) {
   x[7] = csub(e3, o3);
 }
 
+// DFT10 = 5 DFT2 (n = n2 + 5 n1), twiddles w10^{n2} on the odd half, 2 DFT5 (outputs k = k1 + 2 k2)
+template <bool INV>
+__device__ __forceinline__ void dft10(double2 (&x)[kXR]) {
+  const double c1 = 0.80901699437494742410, s1 = 0.58778525229247312917;  // w10 = e^{-2 pi i / 10}
+  const double c2 = 0.30901699437494742410, s2 = 0.95105651629515357212;  // w10^2
+  double2 u0[5], u1[5];
+#pragma unroll
+  for (int m = 0; m < 5; ++m) {
+    u0[m] = cadd(x[m], x[m + 5]);
+    u1[m] = csub(x[m], x[m + 5]);
+  }
+  // w10^{m} (forward: cos - i sin), m = 1..4: w^3 = -conj(w^2), w^4 = -conj(w^1)
+  const double2 w1 = make_double2(c1, INV ? s1 : -s1), w2 = make_double2(c2, INV ? s2 : -s2);
+  const double2 w3 = make_double2(-c2, INV ? s2 : -s2), w4 = make_double2(-c1, INV ? s1 : -s1);
+  u1[1] = cmul(u1[1], w1);
+  u1[2] = cmul(u1[2], w2);
+  u1[3] = cmul(u1[3], w3);
+  u1[4] = cmul(u1[4], w4);
+  dft5<INV>(u0[0], u0[1], u0[2], u0[3], u0[4]);
+  dft5<INV>(u1[0], u1[1], u1[2], u1[3], u1[4]);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    x[2 * k] = u0[k];
+    x[2 * k + 1] = u1[k];
+  }
+}
+
 template <int R, bool INV>
-__device__ __forceinline__ void dft(double2 (&x)[8]) {
+__device__ __forceinline__ void dft(double2 (&x)[kXR]) {
   if constexpr (R == 2) dft2<INV>(x[0], x[1]);
   if constexpr (R == 3) dft3<INV>(x[0], x[1], x[2]);
   if constexpr (R == 4) dft4<INV>(x[0], x[1], x[2], x[3]);
   if constexpr (R == 5) dft5<INV>(x[0], x[1], x[2], x[3], x[4]);
   if constexpr (R == 8) dft8<INV>(x);
+  if constexpr (R == 10) dft10<INV>(x);
 }
 
 // Radix plan of a sub-transform length N (host and device, constexpr): the power-of-two part in
@@ -153,9 +182,24 @@ struct CPlan {
   int R[kMaxStages];
   int Ns[kMaxStages];
 };
-__host__ __device__ constexpr CPlan make_cplan(int N) {
+__host__ __device__ constexpr CPlan make_cplan(int N, bool allow10 = false) {
   CPlan c{0, 8, {0}, {0}};
   if (N < 2 || N > kSubMax) return c;
+  if (allow10 && N == 1000) {  // radix-10 stages: 3 instead of 4 (measured faster at 1000, slower at 100)
+    int m = N, k = 0;
+    while (m % 10 == 0) { m /= 10; ++k; }
+    if (m == 1) {
+      c.ns = k;
+      c.rmin = 10;
+      int acc = 1;
+      for (int s = 0; s < k; ++s) {
+        c.R[s] = 10;
+        c.Ns[s] = acc;
+        acc *= 10;
+      }
+      return c;
+    }
+  }
   int m = N, a = 0;
   while (m % 2 == 0) { m /= 2; ++a; }
   int R[kMaxStages] = {0};
@@ -183,7 +227,7 @@ __host__ __device__ constexpr CPlan make_cplan(int N) {
 // ---- runtime plan (any supported length): one Stockham stage for a compile-time radix.
 // sm layout: element i of transform t at sm[i * TM + t]; tw = w_N^e table (shared memory).
 template <int R, bool INV>
-__device__ __forceinline__ void stage_body(double2 (&x)[8], double2 *sm, int s, const Plan &P, const double2 *tw,
+__device__ __forceinline__ void stage_body(double2 (&x)[kXR], double2 *sm, int s, const Plan &P, const double2 *tw,
                                            int TM, int t, int jb) {
   const int N = P.N, Ns = P.Ns[s], NR = N / R;
   const bool act = jb < NR;
@@ -216,7 +260,7 @@ __device__ __forceinline__ void stage_body(double2 (&x)[8], double2 *sm, int s, 
 }
 
 template <bool INV>
-__device__ __forceinline__ void fft_stages(double2 (&x)[8], double2 *sm, const Plan &P, const double2 *tw, int TM,
+__device__ __forceinline__ void fft_stages(double2 (&x)[kXR], double2 *sm, const Plan &P, const double2 *tw, int TM,
                                            int t, int jb) {
   for (int s = 0; s < P.ns; ++s) {
     switch (P.R[s]) {
@@ -232,10 +276,12 @@ __device__ __forceinline__ void fft_stages(double2 (&x)[8], double2 *sm, const P
 // Shared-memory swizzle of the compile-time plans (element e = i * TM + t): chosen by a bank-conflict
 // simulation of every stage's 128-bit accesses (8 lanes per wavefront): the radix-8 first stage stores
 // with a stride of 8 TM elements.  (1000, 2): XOR of the 8-element group index into the low bits (no
-// padding, conflict-free); TM = 4: two pad elements per 8 (conflict-free for 100 and 400).
+// padding, conflict-free); TM = 4: two pad elements per 8 (conflict-free for 400).  Radix-10 plans
+// (1000): XOR swizzles (5 % / 20 % excess wavefronts left for TM = 4 / 2).
 template <int N, int TM>
 __host__ __device__ constexpr int swz(int e) {
-  if constexpr (N == 1000 && TM == 2) return (e & ~7) | ((e ^ (e >> 3)) & 7);
+  if constexpr (N == 1000 && TM == 4) return (e & ~7) | ((e ^ (e >> 3)) & 7);  // radix 10
+  else if constexpr (N == 1000 && TM == 2) return (e & ~7) | ((e ^ (e >> 5)) & 7);
   else if constexpr (TM == 4) return e + ((e >> 3) << 1);
   else return e;
 }
@@ -246,8 +292,8 @@ __host__ __device__ constexpr size_t fft_buf(int TM, int N) {
 
 // ---- compile-time plan (the hot lengths): every index is a constant expression.
 template <int N, int S, bool INV, int TM>
-__device__ __forceinline__ void ct_stage(double2 (&x)[8], double2 *sm, const double2 *tw, int t, int jb) {
-  constexpr CPlan c = make_cplan(N);
+__device__ __forceinline__ void ct_stage(double2 (&x)[kXR], double2 *sm, const double2 *tw, int t, int jb) {
+  constexpr CPlan c = make_cplan(N, true);
   constexpr int R = c.R[S], Ns = c.Ns[S], NR = N / R;
   const bool act = jb < NR;
   if constexpr (S > 0) {
@@ -293,10 +339,10 @@ struct Sub {
   }
   __device__ __forceinline__ int N() const { return CT ? NC : P.N; }
   __device__ __forceinline__ int R0() const {
-    if constexpr (CT) { constexpr CPlan c = make_cplan(NC); return c.R[0]; } else { return P.R[0]; }
+    if constexpr (CT) { constexpr CPlan c = make_cplan(NC, true); return c.R[0]; } else { return P.R[0]; }
   }
   __device__ __forceinline__ int RL() const {
-    if constexpr (CT) { constexpr CPlan c = make_cplan(NC); return c.R[c.ns - 1]; } else { return P.R[P.ns - 1]; }
+    if constexpr (CT) { constexpr CPlan c = make_cplan(NC, true); return c.R[c.ns - 1]; } else { return P.R[P.ns - 1]; }
   }
   __device__ __forceinline__ int NR0() const { return N() / R0(); }
   __device__ __forceinline__ int NRL() const { return N() / RL(); }
@@ -308,11 +354,11 @@ struct Sub {
   }
   __device__ __forceinline__ size_t buf() const { return fft_buf(TM, N()); }
   __device__ __forceinline__ int out_stride() const {
-    if constexpr (CT) { constexpr CPlan c = make_cplan(NC); return c.Ns[c.ns - 1]; } else { return P.Ns[P.ns - 1]; }
+    if constexpr (CT) { constexpr CPlan c = make_cplan(NC, true); return c.Ns[c.ns - 1]; } else { return P.Ns[P.ns - 1]; }
   }
   __device__ __forceinline__ int out_pos(int r) const {
     if constexpr (CT) {
-      constexpr CPlan c = make_cplan(NC);
+      constexpr CPlan c = make_cplan(NC, true);
       constexpr int R = c.R[c.ns - 1], Ns = c.Ns[c.ns - 1];
       return (jb / Ns) * Ns * R + (jb % Ns) + r * Ns;
     } else {
@@ -321,7 +367,7 @@ struct Sub {
     }
   }
   template <bool INV>
-  __device__ __forceinline__ void run(double2 (&x)[8], double2 *sm, const double2 *tw) const {
+  __device__ __forceinline__ void run(double2 (&x)[kXR], double2 *sm, const double2 *tw) const {
     if constexpr (CT) ct_stage<NC, 0, INV, TMC>(x, sm, tw, t, jb);
     else fft_stages<INV>(x, sm, P, tw, TM, t, jb);
   }
@@ -435,13 +481,13 @@ __global__ void __launch_bounds__(512) k_pr_f1(const double2 *__restrict__ u, co
   const int tiles_per_j = n1 / F.TM, ntiles = tiles_per_j * L;
   const double s = scale_p ? *scale_p : 1.0;
   const bool ld = F.jb < F.NR0();
-  double2 un[8];
-  uint8_t cn[8];
+  double2 un[kXR];
+  uint8_t cn[kXR];
   auto fetch = [&](int tile) {
     const int j = tile / tiles_per_j, m1_0 = (tile - j * tiles_per_j) * F.TM;
     const uint8_t *cj = codes + (size_t)j * n;
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
+    for (int r = 0; r < kXR; ++r)
       if (r < F.R0()) {
         const int64_t m = m1_0 + F.t + (int64_t)n1 * F.in_pos(r);
         un[r] = __ldg(u + m);
@@ -451,10 +497,10 @@ __global__ void __launch_bounds__(512) k_pr_f1(const double2 *__restrict__ u, co
   int tile = blockIdx.x;
   if (ld && tile < ntiles) fetch(tile);
   for (; tile < ntiles; tile += gridDim.x) {
-    double2 x[8];
+    double2 x[kXR];
     if (ld) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < kXR; ++r)
         if (r < F.R0()) x[r] = cmulc(cscale(un[r], s), cb[cn[r]]);
       if (PF && tile + (int)gridDim.x < ntiles) fetch(tile + gridDim.x);
     }
@@ -464,7 +510,7 @@ __global__ void __launch_bounds__(512) k_pr_f1(const double2 *__restrict__ u, co
       const int j = tile / tiles_per_j, m1_0 = (tile - j * tiles_per_j) * F.TM;
       double2 *Yj = Y + (size_t)j * n + m1_0 + F.t;
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < kXR; ++r)
         if (r < F.RL()) Yj[(size_t)F.out_pos(r) * n1] = x[r];
     }
   }
@@ -489,12 +535,12 @@ __global__ void __launch_bounds__(512) k_pr_b(double2 *__restrict__ Y, const dou
   const int64_t n = (int64_t)n1c * n2;
   const int tiles_per_j = n2 / F.TM, ntiles = tiles_per_j * L;
   const bool ld = F.jb < F.NR0();
-  double2 yn[8];
+  double2 yn[kXR];
   auto fetch = [&](int tile) {
     const int j = tile / tiles_per_j, k2 = (tile - j * tiles_per_j) * F.TM + F.t;
     const double2 *row = Y + (size_t)j * n + (size_t)k2 * n1c;
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
+    for (int r = 0; r < kXR; ++r)
       if (r < F.R0()) yn[r] = row[F.in_pos(r)];
   };
   int tile = blockIdx.x;
@@ -502,11 +548,11 @@ __global__ void __launch_bounds__(512) k_pr_b(double2 *__restrict__ Y, const dou
   for (; tile < ntiles; tile += gridDim.x) {
     const int j = tile / tiles_per_j, k2 = (tile - j * tiles_per_j) * F.TM + F.t;
     const size_t base = (size_t)j * n + (size_t)k2 * n1c;
-    double2 x[8];
-    double wv[8];
+    double2 x[kXR];
+    double wv[kXR];
     if (mode <= 1 && F.jb < F.NRL()) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < kXR; ++r)
         if (r < F.RL()) wv[r] = __ldg(wk + base + F.out_pos(r));
     }
     if (ld) {
@@ -514,7 +560,7 @@ __global__ void __launch_bounds__(512) k_pr_b(double2 *__restrict__ Y, const dou
       const double2 w1 = twn(twlo, twhi, (long long)F.NR0() * k2);
       double2 w = twn(twlo, twhi, (long long)F.jb * k2);
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < kXR; ++r)
         if (r < F.R0()) {
           x[r] = cmul(yn[r], w);
           w = cmul(w, w1);
@@ -524,7 +570,7 @@ __global__ void __launch_bounds__(512) k_pr_b(double2 *__restrict__ Y, const dou
     F.template run<false>(x, sm, twsm);
     if (F.jb < F.NRL()) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < kXR; ++r)
         if (r < F.RL()) {
           if (mode >= 1) h[base + F.out_pos(r)] = x[r].x * x[r].x + x[r].y * x[r].y;
           if (mode <= 1) x[r] = cscale(x[r], wv[r]);
@@ -534,13 +580,13 @@ __global__ void __launch_bounds__(512) k_pr_b(double2 *__restrict__ Y, const dou
     // re-enter shared memory for the inverse transform over k1
     if (F.jb < F.NRL()) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < kXR; ++r)
         if (r < F.RL()) sm[F.slot(F.out_pos(r))] = x[r];
     }
     __syncthreads();
     if (ld) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < kXR; ++r)
         if (r < F.R0()) x[r] = sm[F.slot(F.in_pos(r))];
     }
     __syncthreads();
@@ -552,7 +598,7 @@ __global__ void __launch_bounds__(512) k_pr_b(double2 *__restrict__ Y, const dou
       const double2 v1 = twn(twlo, twhi, (long long)F.out_stride() * k2);
       double2 v = twn(twlo, twhi, (long long)F.out_pos(0) * k2);
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < kXR; ++r)
         if (r < F.RL()) {
           row[F.out_pos(r)] = cmulc(x[r], v);
           v = cmul(v, v1);
@@ -586,23 +632,23 @@ __global__ void __launch_bounds__(512) k_pr_c(const double2 *__restrict__ Y, con
   double v[1] = {0.0};
   for (int tile = blockIdx.x; tile < n1 / F.TM; tile += gridDim.x) {
     const int m1_0 = tile * F.TM;
-    double2 yn[8];
+    double2 yn[kXR];
     auto fetch = [&](int j) {
       const double2 *Yj = Y + (size_t)j * n + m1_0 + F.t;
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < kXR; ++r)
         if (r < F.R0()) yn[r] = Yj[(size_t)F.in_pos(r) * n1];
     };
     if (ld) fetch(0);
     if (st) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < kXR; ++r)
         if (r < F.RL()) acc[F.out_pos(r) * F.TM + F.t] = make_double2(0.0, 0.0);
     }
     for (int j = 0; j < L; ++j) {
-      double2 x[8];
+      double2 x[kXR];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) x[r] = yn[r];
+      for (int r = 0; r < kXR; ++r) x[r] = yn[r];
       if (PF && ld && j + 1 < L) fetch(j + 1);
       __syncthreads();  // the tables are in (first pass); previous shared-memory reads are done
       F.template run<true>(x, sm, twsm);
@@ -610,7 +656,7 @@ __global__ void __launch_bounds__(512) k_pr_c(const double2 *__restrict__ Y, con
       if (st) {
         const uint8_t *cj = codes + (size_t)j * n + m1_0 + F.t;
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
+        for (int r = 0; r < kXR; ++r)
           if (r < F.RL()) {
             const int pos = F.out_pos(r);
             acc[pos * F.TM + F.t] = cadd(acc[pos * F.TM + F.t], cmul(cb[__ldg(cj + (int64_t)n1 * pos)], x[r]));
@@ -619,7 +665,7 @@ __global__ void __launch_bounds__(512) k_pr_c(const double2 *__restrict__ Y, con
     }
     if (st) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < kXR; ++r)
         if (r < F.RL()) {
           const int pos = F.out_pos(r);
           const int64_t m = m1_0 + F.t + (int64_t)n1 * pos;
@@ -654,9 +700,9 @@ struct Variant {
 #define SCG_PR_VARIANT(N, TM)                                                                      \
   {N, TM, k_pr_f1<N, TM, true>, k_pr_f1<N, TM, false>, k_pr_b<N, TM, true>, k_pr_b<N, TM, false>, \
    k_pr_c<N, TM, true>, k_pr_c<N, TM, false>}
-const Variant kVariants[] = {SCG_PR_VARIANT(100, 4), SCG_PR_VARIANT(250, 4), SCG_PR_VARIANT(400, 4),
-                             SCG_PR_VARIANT(1000, 2), SCG_PR_VARIANT(100, 2), SCG_PR_VARIANT(250, 2),
-                             SCG_PR_VARIANT(400, 2)};
+const Variant kVariants[] = {SCG_PR_VARIANT(100, 4),  SCG_PR_VARIANT(250, 4), SCG_PR_VARIANT(400, 4),
+                             SCG_PR_VARIANT(1000, 4), SCG_PR_VARIANT(1000, 2), SCG_PR_VARIANT(100, 2),
+                             SCG_PR_VARIANT(250, 2),  SCG_PR_VARIANT(400, 2)};
 const Variant kGeneric = SCG_PR_VARIANT(0, 0);
 const Variant *find_variant(int N, int TM) {
   for (const Variant &v : kVariants)
@@ -1032,10 +1078,13 @@ bool factor_plan(int N, Plan *P) {
 int plan_rmin(const Plan &P) { return make_cplan(P.N).rmin; }
 // Transforms per block: a compile-time variant with TM = 4 (then 2) when it divides the other dimension and
 // fits 512 threads; else the runtime plan with the largest TM | other, TM * N / rmin <= 512, TM * N * 16 B <= 64 KB.
-int choose_tm(const Plan &P, int other, bool force2) {
+// prefer2: try two transforms per block first (k_pr_b at length 1000: 214 vs 249 us with four).
+int choose_tm(const Plan &P, int other, bool force2, bool generic, bool prefer2) {
   const int per = P.N / plan_rmin(P);
-  for (int tm : {4, 2})
-    if (!(force2 && tm == 4) && other % tm == 0 && tm * per <= 512 && find_variant(P.N, tm)) return tm;
+  const int per_ct = P.N / make_cplan(P.N, true).rmin;  // compile-time plans may use radix 10
+  for (int tm : {prefer2 ? 2 : 4, prefer2 ? 4 : 2})
+    if (!generic && !(force2 && tm == 4) && other % tm == 0 && tm * per_ct <= 512 && find_variant(P.N, tm))
+      return tm;
   int best = 1;
   for (int tm = 1; tm <= 64 && tm <= other; ++tm) {
     if (other % tm) continue;
@@ -1359,8 +1408,8 @@ int scg_pr_init(int64_t n, int32_t L, const double *psi, const double *b, int32_
   c->seed = seed;
   c->flags = flags;
   c->rsn = 1.0 / std::sqrt((double)n);
-  c->tm1 = choose_tm(P2, n1, flags & SCG_PR_TM2);
-  c->tm2 = choose_tm(P1, n2, flags & SCG_PR_TM2);
+  c->tm1 = choose_tm(P2, n1, flags & SCG_PR_TM2, flags & SCG_PR_GENERIC, false);
+  c->tm2 = choose_tm(P1, n2, flags & SCG_PR_TM2, flags & SCG_PR_GENERIC, n1 == 1000);
   c->v1 = find_variant(n2, c->tm1);
   c->v2 = find_variant(n1, c->tm2);
   if (!c->v1 || (flags & SCG_PR_GENERIC)) c->v1 = &kGeneric;
@@ -1368,8 +1417,8 @@ int scg_pr_init(int64_t n, int32_t L, const double *psi, const double *b, int32_
   c->kf1 = (flags & SCG_PR_NOPF_F1) ? c->v1->f1n : c->v1->f1;
   c->kb = (flags & SCG_PR_NOPF_B) ? c->v2->bn : c->v2->b;
   c->kc = (flags & SCG_PR_NOPF_C) ? c->v1->cn : c->v1->c;
-  c->nthr1 = c->tm1 * (n2 / plan_rmin(P2));
-  c->nthr2 = c->tm2 * (n1 / plan_rmin(P1));
+  c->nthr1 = c->tm1 * (n2 / (c->v1 != &kGeneric ? make_cplan(n2, true).rmin : plan_rmin(P2)));
+  c->nthr2 = c->tm2 * (n1 / (c->v2 != &kGeneric ? make_cplan(n1, true).rmin : plan_rmin(P1)));
   c->smem1 = sizeof(double2) * (fft_buf(c->tm1, n2) + n2 + 256);
   c->smem2 = sizeof(double2) * (fft_buf(c->tm2, n1) + n1);
   c->smemc = c->smem1 + sizeof(double2) * (size_t)c->tm1 * n2;
