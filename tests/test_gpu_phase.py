@@ -196,3 +196,24 @@ def test_q_cap_on_tiny_n(pr):
     np.testing.assert_array_equal(gl[:, 1:3], ol[:, 1:3])
     assert gl[:, 1].max() == n - 1 and np.sum(gl[:, 1] == n - 1) > 20
     assert np.max(np.abs(gl[:, 3] - ol[:, 3])) <= 1e-8 * np.abs(ol[:, 3]).max()
+
+
+def test_zero_signal_and_degenerate_inputs(pr):
+    """chi_nat = 0 gives b = 0: D_1 = I / sqrt(n) has xi > 0, the LMO returns H = 0 at every t and X
+    stays 0 (GPU and oracle); a modulation that is identically zero is rejected (||A_i||_F = 0 leaves
+    the row scaling of P:1811-1812 undefined)."""
+    n = 100
+    psi = si.phase_psi(n, seed=3)
+    b = np.zeros((12, n))
+    g = pr.PhaseRetrieval(psi, b, R=5, seed=3)
+    o = ph.PhaseOracle(psi, b, R=5, seed=3)
+    g.step(10)
+    o.step(10)
+    assert np.all(g.iter_log()[:, 4] > 0) and np.all(o.logarr[:, 4] > 0)
+    assert not np.any(g.state("z")) and not np.any(g.state("S"))
+    g.reconstruct()
+    assert not np.any(g.signal())
+    bad = psi.copy()
+    bad[4] = 0.0
+    with pytest.raises(pr.PhaseError):
+        pr.PhaseRetrieval(bad, b, R=5, seed=3)
