@@ -1114,14 +1114,18 @@ __global__ void k_pull(int kind, int ns, Net net, DevScalars *sc, FinArgs f) {
     }
   long long L[kMaxSums][kLimbs];
   double gk[kMaxR];
-  for (int idx = 0; idx < kMaxSums * kLimbs; ++idx) {
+  // only the ns sums and the R entries of g this kind carries cross the warp (uniform trip counts)
+  for (int idx = 0; idx < ns * kLimbs; ++idx) {
     const long long v = __shfl_sync(0xffffffffu, part[idx >> 5], idx & 31);
-    if (lane == 0) L[idx / kLimbs][idx % kLimbs] = idx < ns * kLimbs ? v : 0ll;
+    if (lane == 0) L[idx / kLimbs][idx % kLimbs] = v;
   }
-  for (int k = 0; k < kMaxR && k < 64; ++k) {
-    const double v = __shfl_sync(0xffffffffu, gpart[k >> 5], k & 31);
-    if (lane == 0) gk[k] = v;
-  }
+  if (lane == 0)
+    for (int idx = ns * kLimbs; idx < kMaxSums * kLimbs; ++idx) L[idx / kLimbs][idx % kLimbs] = 0ll;
+  if (kind == FK_NZ || kind == FK_NZZ || kind == FK_GK)
+    for (int k = 0; k < f.R && k < 64; ++k) {
+      const double v = __shfl_sync(0xffffffffu, gpart[k >> 5], k & 31);
+      if (lane == 0) gk[k] = v;
+    }
   if (lane == 0) finalize(kind, sc, L, gk, f);
 }
 
