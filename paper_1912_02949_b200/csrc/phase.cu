@@ -353,6 +353,17 @@ struct Sub {
     else return i * TM + t;
   }
   __device__ __forceinline__ size_t buf() const { return fft_buf(TM, N()); }
+  // the last stage leaves element out_pos(r) = jb + r N / R_last in x[r], which is exactly the first
+  // stage's input in_pos(r) = jb + r N / R_0 when R_0 = R_last (radix-10 plans): a forward transform can
+  // feed an inverse one from registers
+  __host__ __device__ static constexpr bool sym() {
+    if constexpr (CT) {
+      constexpr CPlan c = make_cplan(NC, true);
+      return c.R[0] == c.R[c.ns - 1] && c.Ns[c.ns - 1] == NC / c.R[0];
+    } else {
+      return false;
+    }
+  }
   __device__ __forceinline__ int out_stride() const {
     if constexpr (CT) { constexpr CPlan c = make_cplan(NC, true); return c.Ns[c.ns - 1]; } else { return P.Ns[P.ns - 1]; }
   }
@@ -577,19 +588,22 @@ __global__ void __launch_bounds__(512) k_pr_b(double2 *__restrict__ Y, const dou
         }
     }
     if (mode == 2) continue;
-    // re-enter shared memory for the inverse transform over k1
-    if (F.jb < F.NRL()) {
+    // re-enter shared memory for the inverse transform over k1 (not needed when the plan is symmetric:
+    // the forward's last-stage reads are complete at its barrier, the inverse's stage 0 starts from x)
+    if constexpr (!Sub<NC, TMC>::sym()) {
+      if (F.jb < F.NRL()) {
 #pragma unroll
-      for (int r = 0; r < kXR; ++r)
-        if (r < F.RL()) sm[F.slot(F.out_pos(r))] = x[r];
-    }
-    __syncthreads();
-    if (ld) {
+        for (int r = 0; r < kXR; ++r)
+          if (r < F.RL()) sm[F.slot(F.out_pos(r))] = x[r];
+      }
+      __syncthreads();
+      if (ld) {
 #pragma unroll
-      for (int r = 0; r < kXR; ++r)
-        if (r < F.R0()) x[r] = sm[F.slot(F.in_pos(r))];
+        for (int r = 0; r < kXR; ++r)
+          if (r < F.R0()) x[r] = sm[F.slot(F.in_pos(r))];
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (!PF && ld && tile + (int)gridDim.x < ntiles) fetch(tile + gridDim.x);
     F.template run<true>(x, sm, twsm);
     if (F.jb < F.NRL()) {
