@@ -2646,6 +2646,47 @@ __global__ void k_unperm(double *__restrict__ out, const double *__restrict__ in
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) out[orig[r]] = in[r];
 }
 
+// Sign rounding of one reconstructed column: chi[orig[r]] = sgn(u[r]) * flip (sgn(0) = +1),
+// in input order.
+__global__ void k_round_signs(const double *__restrict__ u, const int *__restrict__ orig, int nl, int flip,
+                              int8_t *__restrict__ chi) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x)
+    chi[orig[r]] = (int8_t)((u[r] >= 0.0 ? 1 : -1) * flip);
+}
+
+// One-shot metric (implicit infeasibility, not on the feedback path): per-block partial sums of
+// ((z_r - b) unit)^2 in a fixed order; k_sum_partials adds the partials in block order (one block).
+__global__ void __launch_bounds__(kBlock) k_sqdist(const double *__restrict__ z, int nl, double b, double unit,
+                                                   double *__restrict__ part) {
+  __shared__ double red[kBlock / 32];
+  double s = 0.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double e = (z[r] - b) * unit;
+    s += e * e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kBlock / 32; ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+__global__ void __launch_bounds__(kBlock) k_sum_partials(const double *__restrict__ part, int np, double *out) {
+  __shared__ double red[kBlock];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)blockDim.x; ++i) t += red[i];
+    *out = t;
+  }
+}
+
 // Self-test: div_rn against the hardware IEEE division on pseudo-random operands
 // (mantissas drawn uniformly, including the extremes 1 and 2 - ulp), exponents in +-60.
 // Exact-sum self-test (sketchycgal_selftest_xsum): the n values through the kernels' per-thread

@@ -170,6 +170,9 @@ struct scg_ctx {
   bool hcomm = false;     // multi-process setup transport: the caller's host callbacks (else NCCL)
   scg_host_comm hc{};
   double *dred = nullptr;  // device scratch for host all-reduces (mode 2)
+  double *dmet = nullptr;  // device scratch of the one-shot metrics (feasibility)
+  int8_t *dchi = nullptr;  // device scratch of the rounded cut
+  int64_t dchi_cap = 0;
   int64_t t = 0;
   int64_t launches = 0;
   int64_t log_cap = 0;
@@ -1250,6 +1253,8 @@ void sketchycgal_destroy(scg_ctx *c) {
   if (c->comm) ncclCommDestroy(c->comm);
 #endif
   if (c->dred) cudaFree(c->dred);
+  if (c->dmet) cudaFree(c->dmet);
+  if (c->dchi) cudaFree(c->dchi);
   for (auto &p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto e : c->evpool) cudaEventDestroy(e);
   if (c->side) {
@@ -2236,13 +2241,16 @@ scg_status sketchycgal_feasibility(scg_ctx *c, double out[3]) {
   // implicit: || n z~ - 1 || / (1 + sqrt n) in original units (scaled: z_orig = z * alpha_orig)
   const double unit = c->alpha_orig / c->alpha;
   std::vector<double> ssum{0.0};
-  for (Shard *s : c->sh) {
-    std::vector<double> z((size_t)s->nl);
-    CK(cudaMemcpy(z.data(), s->z, sizeof(double) * s->nl, cudaMemcpyDeviceToHost));
-    for (int64_t r = 0; r < s->nl; ++r) {
-      const double e = (z[(size_t)r] - c->b) * unit;
-      ssum[0] += e * e;
-    }
+  for (Shard *s : c->sh) {  // device reduction (k_sqdist + k_sum_partials), one double back per shard
+    if (!c->dmet && cudaMalloc(&c->dmet, sizeof(double) * (4096 + 1)) != cudaSuccess)
+      return fail(c, SCG_ENOMEM, "feasibility scratch");
+    const int g = std::min(4096, std::max(1, (int)((s->nl + kBlock - 1) / kBlock)));
+    k_sqdist<<<g, kBlock, 0, c->stream>>>(s->z, (int)s->nl, c->b, unit, c->dmet + 1);
+    k_sum_partials<<<1, kBlock, 0, c->stream>>>(c->dmet + 1, g, c->dmet);
+    double part = 0.0;
+    CK(cudaMemcpyAsync(&part, c->dmet, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    ssum[0] += part;
   }
   if ((st = host_allreduce(c, ssum))) return st;
   const double nb = std::sqrt((double)c->n);
@@ -2276,11 +2284,17 @@ scg_status sketchycgal_round(scg_ctx *c, int8_t *chi, double *cut_weight) {
   if ((st = host_allreduce(c, u0))) return st;
   const int flip = u0[0] >= 0.0 ? 1 : -1;
   int64_t off = 0;
-  for (Shard *s : c->sh) {
-    std::vector<double> u((size_t)s->nl);
-    CK(cudaMemcpy(u.data(), s->U + (size_t)best * s->nl, sizeof(double) * s->nl, cudaMemcpyDeviceToHost));
-    for (int64_t nu = 0; nu < s->nl; ++nu)
-      chi[off + s->origloc[(size_t)nu]] = (int8_t)((u[(size_t)nu] >= 0.0 ? 1 : -1) * flip);
+  for (Shard *s : c->sh) {  // signs on the device in input order (k_round_signs), n bytes back
+    if (c->dchi_cap < s->nl) {
+      if (c->dchi) cudaFree(c->dchi);
+      c->dchi = nullptr;
+      if (cudaMalloc(&c->dchi, (size_t)s->nl) != cudaSuccess) return fail(c, SCG_ENOMEM, "round scratch");
+      c->dchi_cap = s->nl;
+    }
+    k_round_signs<<<grid_for(s->nl, 8 * c->nsm), kBlock, 0, c->stream>>>(s->U + (size_t)best * s->nl, s->orig,
+                                                                          (int)s->nl, flip, c->dchi);
+    CK(cudaMemcpyAsync(chi + off, c->dchi, (size_t)s->nl, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
     off += s->nl;
   }
   *cut_weight = w[best];
