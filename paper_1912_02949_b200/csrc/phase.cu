@@ -25,7 +25,6 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
-#include <map>
 #include <vector>
 
 #include "../../include/scg_phase.h"
@@ -1384,26 +1383,28 @@ int scg_pr_init(int64_t n, int32_t L, const double *psi, const double *b, int32_
     }
   }
   if (!n1) return SCG_EUNSUPPORTED;
-  // codebook of psi values
-  std::map<std::pair<uint64_t, uint64_t>, int> idx;
+  // codebook of psi values: open addressing on the bit patterns (1024 slots for at most 256 values)
   std::vector<double2> book(256, make_double2(0.0, 0.0));
   std::vector<uint8_t> codes((size_t)L * n);
-  for (int64_t i = 0; i < (int64_t)L * n; ++i) {
-    uint64_t re, im;
-    memcpy(&re, psi + 2 * i, 8);
-    memcpy(&im, psi + 2 * i + 1, 8);
-    auto key = std::make_pair(re, im);
-    auto it = idx.find(key);
-    int code;
-    if (it == idx.end()) {
-      code = (int)idx.size();
-      if (code >= 256) return SCG_EUNSUPPORTED;
-      idx[key] = code;
-      book[code] = make_double2(psi[2 * i], psi[2 * i + 1]);
-    } else {
-      code = it->second;
+  {
+    std::vector<uint64_t> kre(1024), kim(1024);
+    std::vector<int> kc(1024, -1);
+    int ncode = 0;
+    for (int64_t i = 0; i < (int64_t)L * n; ++i) {
+      uint64_t re, im;
+      memcpy(&re, psi + 2 * i, 8);
+      memcpy(&im, psi + 2 * i + 1, 8);
+      int slot = (int)(((re * 0x9E3779B97F4A7C15ull) ^ (im * 0xC2B2AE3D27D4EB4Full)) >> 54);
+      while (kc[slot] >= 0 && (kre[slot] != re || kim[slot] != im)) slot = (slot + 1) & 1023;
+      if (kc[slot] < 0) {
+        if (ncode >= 256) return SCG_EUNSUPPORTED;
+        kre[slot] = re;
+        kim[slot] = im;
+        kc[slot] = ncode;
+        book[ncode++] = make_double2(psi[2 * i], psi[2 * i + 1]);
+      }
+      codes[(size_t)i] = (uint8_t)kc[slot];
     }
-    codes[(size_t)i] = (uint8_t)code;
   }
   scg_pr_ctx *c = static_cast<scg_pr_ctx *>(::operator new(sizeof(scg_pr_ctx)));
   memset((void *)c, 0, sizeof(*c));
