@@ -1783,8 +1783,9 @@ int scg_pr_apply_D(scg_pr_ctx *c, const double *w, const double *x, double *yout
   double *tmp = reinterpret_cast<double *>(c->Y);
   PR_CUDA(cudaMemcpyAsync(tmp, w, sizeof(double) * dn, cudaMemcpyHostToDevice, c->st));
   k_pr_perm<<<grid_for(dn, 256), 256, 0, c->st>>>(tmp, c->wk, c->n1, c->n2, c->L, c->kappa, 1.0, 1);
-  PR_CUDA(cudaMemcpyAsync(c->v, x, sizeof(double2) * n, cudaMemcpyHostToDevice, c->st));
-  int rc = launch_matvec(c, c->v, nullptr, c->a, 0, 2);
+  // x in a scratch buffer (tmpB: n complex at least; the reconstruction's U stays in tmpA), not in v
+  PR_CUDA(cudaMemcpyAsync(c->tmpB, x, sizeof(double2) * n, cudaMemcpyHostToDevice, c->st));
+  int rc = launch_matvec(c, c->tmpB, nullptr, c->a, 0, 2);
   if (rc) return rc;
   PR_CUDA(cudaMemcpyAsync(yout, c->a, sizeof(double2) * n, cudaMemcpyDeviceToHost, c->st));
   PR_CUDA(cudaMemcpyAsync(c->wk, saved, sizeof(double) * dn, cudaMemcpyDeviceToDevice, c->st));

@@ -217,3 +217,23 @@ def test_zero_signal_and_degenerate_inputs(pr):
     bad[4] = 0.0
     with pytest.raises(pr.PhaseError):
         pr.PhaseRetrieval(bad, b, R=5, seed=3)
+
+
+def test_hooks_leave_the_iteration_state_alone(pr):
+    """apply_D / measure run on scratch buffers: the iterates, the eigenvector and the next iterations are
+    those of a context without hook calls."""
+    n = 1000
+    I = si.phase_instance(n, seed=8)
+    a = pr.PhaseRetrieval(I.psi, I.b, R=5, seed=8)
+    b = pr.PhaseRetrieval(I.psi, I.b, R=5, seed=8)
+    a.step(5)
+    b.step(5)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    b.apply_D(rng.standard_normal((12, n)), x)
+    b.measure(x)
+    np.testing.assert_array_equal(a.state("v"), b.state("v"))
+    a.step(5)
+    b.step(5)
+    np.testing.assert_array_equal(a.iter_log(), b.iter_log())
+    np.testing.assert_array_equal(a.state("z"), b.state("z"))
