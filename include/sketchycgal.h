@@ -89,9 +89,12 @@ enum {
                                    always draw inside the dual kernel) */
   SCG_NO_RESIDENT = 1u << 17,   /* one GPU, n <= 65536: keep the multi-kernel iteration instead of one launch of one
                                    thread-block cluster per iteration (k_resident) */
-  SCG_SERIAL_RNG = 1u << 18     /* one GPU: draw the next start vector with the full-grid kernel on the main stream
+  SCG_SERIAL_RNG = 1u << 18,    /* one GPU: draw the next start vector with the full-grid kernel on the main stream
                                    (serial, no overlap with the Lanczos kernels) instead of the low-priority side
                                    stream; bitwise-neutral execution option */
+  SCG_INLINE_PULL = 1u << 19    /* P > 1 (not with host-callback transports): pull each Lanczos step's omega / rho
+                                   collective in the prologue of the kernel that consumes it instead of by a k_pull
+                                   launch; bitwise-neutral execution option */
 };
 
 /* This rank's rows [row_begin, row_end) of the symmetric weighted Laplacian

@@ -37,6 +37,7 @@ SCG_NO_ELL = 1 << 14
 SCG_FUSED_RNG = 1 << 15
 SCG_NO_RESIDENT = 1 << 17
 SCG_SERIAL_RNG = 1 << 18
+SCG_INLINE_PULL = 1 << 19
 
 STATUS = {0: "SCG_OK", -1: "SCG_EINVAL", -2: "SCG_ENOMEM", -3: "SCG_ECUDA", -4: "SCG_ENCCL", -5: "SCG_ECHOL",
           -6: "SCG_ESTATE", -7: "SCG_ERANGE", -8: "SCG_EUNSUPPORTED", -9: "SCG_ECOMM"}
@@ -313,7 +314,7 @@ class SketchyCGAL:
                  l1_ball: float | None = None, pdl: bool = True, fused_pass1: bool = False, ws_spmv: bool = False,
                  tma_b: bool = False, debug_log: bool = False, qfix: int = 0, ell: bool = True,
                  side_rng: bool = True, host_comm: "TorchHostComm | None" = None, resident: bool = True,
-                 serial_rng: bool = False):
+                 serial_rng: bool = False, inline_pull: bool = False):
         self.lib = load()
         self.n = int(L.n)
         self.R = int(R)
@@ -348,7 +349,7 @@ class SketchyCGAL:
                 (SCG_FUSED_PASS1 if fused_pass1 else 0) | (SCG_WS_SPMV if ws_spmv else 0) | \
                 (SCG_TMA_B if tma_b else 0) | (SCG_DEBUG_LOG if debug_log else 0) | (0 if ell else SCG_NO_ELL) | \
                 (0 if side_rng else SCG_FUSED_RNG) | (0 if resident else SCG_NO_RESIDENT) | \
-                (SCG_SERIAL_RNG if serial_rng else 0)
+                (SCG_SERIAL_RNG if serial_rng else 0) | (SCG_INLINE_PULL if inline_pull else 0)
         self._h = ctypes.c_void_p()
         dptr = None
         if dist is not None:

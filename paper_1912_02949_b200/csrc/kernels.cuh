@@ -1129,6 +1129,39 @@ __global__ void k_pull(int kind, int ns, Net net, DevScalars *sc, FinArgs f) {
   if (lane == 0) finalize(kind, sc, L, gk, f);
 }
 
+// Consumer-side pull (SCG_INLINE_PULL, P > 1), warp 0 of a block: wait for every rank's flag of
+// collective E, add the P limb sets of its first sum (exact integers, any order), round in lane 0 (*out).
+// The same flags, limbs and rounding as k_pull; returns 0 (sc->err |= 2) when a flag is lost.
+__device__ __forceinline__ int pull_one(const Net &net, unsigned long long E, DevScalars *sc, double *out) {
+  const int lane = threadIdx.x & 31;
+  const int e = (int)(E & 3ull);
+  Mailbox *m = net.mb;
+  int ok = 1;
+  if (lane < net.P) {
+    const long long t0 = clock64();
+    while (ld_acquire_sys(&m->flag[e][lane]) != E) {
+      if (net.nowait || clock64() - t0 > (1ll << 34)) {
+        ok = 0;
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+  if (!__all_sync(0xffffffffu, ok)) {
+    if (lane == 0) atomicOr(&sc->err, 2);
+    return 0;
+  }
+  __syncwarp();
+  long long part = 0;
+  if (lane < kLimbs)
+    for (int p = 0; p < net.P; ++p) part += __ldcv(&m->limbs[e][p][0][lane]);
+  long long L[kLimbs];
+#pragma unroll
+  for (int i = 0; i < kLimbs; ++i) L[i] = __shfl_sync(0xffffffffu, part, i);
+  if (lane == 0) *out = xacc_round(L);
+  return 1;
+}
+
 // ---------------------------------------------------------------- init kernels
 // ||L||_F^2 over all stored entries: off-diagonal weights (each stored once per
 // direction) and the diagonal (scaling).
@@ -1254,10 +1287,32 @@ template <bool UNI, int W>  // W > 0: ELL-W layout (spmv_ell), 0: SELL + long ro
 __global__ void __launch_bounds__(kBlockA, W > 0 ? ell_min_blocks(W, UNI) : (UNI ? kMinBlocksUni : 2)) k_lanczos_a(Csr C, Rows RL, const double *__restrict__ d,
                                                          const double *__restrict__ X, int nl, long long rb, int i,
                                                          double *__restrict__ a, XSlot *slot, DevScalars *sc,
-                                                         Net net) {
+                                                         Net net, unsigned long long pE) {
   pdl_entry();
   if (sc->brk) return;
-  const double den = sc->rho[i - 1];
+  double den;
+  if (pE) {  // SCG_INLINE_PULL: rho_{i-1} of collective pE (k_lanczos_b of step i - 1), fin_rho's arithmetic
+    __shared__ double s_den;
+    __shared__ int s_go;
+    if (threadIdx.x < 32) {
+      double r2 = 0.0;
+      const int ok = pull_one(net, pE, sc, &r2);
+      if (threadIdx.x == 0) {
+        const int j = i - 1;
+        const double rho = sqrt(r2);
+        const double rp = j >= 2 ? sc->rho[j - 1] : 0.0;
+        const bool brk = rho <= 0x1p-45 * (fabs(sc->om[j - 1]) + rp);  // fin_rho's test (Alg. 2 line 8)
+        if (ok && blockIdx.x == 0) fin_rho(sc, j, r2);  // the device scalars for later kernels
+        s_den = rho;
+        s_go = ok && !brk;
+      }
+    }
+    __syncthreads();
+    if (!s_go) return;
+    den = s_den;
+  } else {
+    den = sc->rho[i - 1];
+  }
   __shared__ XBlk<1> xb;
   xblk_init<1>(xb);
   EpiA epi;
@@ -1499,10 +1554,29 @@ constexpr int kMinBlocksB = 4;
 constexpr int kBU = 2;  // row pairs in flight per thread
 __global__ void __launch_bounds__(kBlock, kMinBlocksB) k_lanczos_b(const double *__restrict__ a, const double *Xi,
                                                       const double *Xim1, double *Xip1, int nl, long long rb,
-                                                      int i, XSlot *slot, DevScalars *sc, Net net) {
+                                                      int i, XSlot *slot, DevScalars *sc, Net net,
+                                                      unsigned long long pE) {
   pdl_entry();
   if (sc->brk) return;
-  const double om = sc->om[i - 1];
+  double om;
+  if (pE) {  // SCG_INLINE_PULL: omega_i of collective pE (k_lanczos_a of this step)
+    __shared__ double s_om;
+    __shared__ int s_go;
+    if (threadIdx.x < 32) {
+      double v = 0.0;
+      const int ok = pull_one(net, pE, sc, &v);
+      if (threadIdx.x == 0) {
+        if (ok && blockIdx.x == 0) sc->om[i - 1] = v;  // FK_OM's finalize, for the tridiagonal solve
+        s_om = v;
+        s_go = ok;
+      }
+    }
+    __syncthreads();
+    if (!s_go) return;
+    om = s_om;
+  } else {
+    om = sc->om[i - 1];
+  }
   const double den = sc->rho[i - 1];
   const double denm = i >= 2 ? sc->rho[i - 2] : 1.0;
   const double rden = 1.0 / den, rdenm = 1.0 / denm;

@@ -1681,8 +1681,16 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
                   dim3(kBlockA), C, TT, (const double *)s->d, s->G, slot(s, 1), (long long)c->npad, c->store ? 1 : 0, q,
                   (int)s->nl, s->a, s->slots + SLOT_OM, s->slots + SLOT_RHO, s->sc, net_of(c, s, E), s->gflag, eb);
     } else
+    {
+    // SCG_INLINE_PULL (P > 1): the per-step collectives are pulled in the prologue of the kernel that
+    // consumes them (omega_i in k_lanczos_b, rho_{i-1} in k_lanczos_a) instead of by k_pull launches;
+    // the last omega still goes through k_pull for the tridiagonal solve
+    bool inl = c->world > 1 && (c->flags & SCG_INLINE_PULL) && !c->btma && !c->hcomm;
+    for (Shard *s : c->sh) inl = inl && !s->ws;
+    unsigned long long Erho = 0;
     for (int i = 1; i <= q; ++i) {
       unsigned long long E = ++c->epoch;
+      const unsigned long long pa = (inl && i >= 2) ? Erho : 0ull;
       for (Shard *s : c->sh) {
         Csr C{s->rp, s->col, s->val};
         Rows TT = rows_of(s, s->dyn);
@@ -1694,12 +1702,13 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
         else
           launch_smem(c, KC_LANCZOS_A, s->kb[KC_LANCZOS_A], kA, dim3(s->ellw ? s->grid_ell : s->grid_a), dim3(kBlockA), 0, C, TT,
                       (const double *)s->d, (const double *)slot(s, i), (int)s->nl, (long long)s->rb, i, s->a,
-                      s->slots + SLOT_OM, s->sc, net_of(c, s, E));
+                      s->slots + SLOT_OM, s->sc, net_of(c, s, E), pa);
       }
       FinArgs f{};
       f.i = i;
-      pull_all(c, FK_OM, 1, E, f);
+      if (!inl || i == q) pull_all(c, FK_OM, 1, E, f);
       if (i < q) {
+        const unsigned long long Eom = E;
         E = ++c->epoch;
         for (Shard *s : c->sh) {
           const double *Xim1 = (i == 1) ? nullptr : slot(s, i - 1);
@@ -1710,10 +1719,12 @@ scg_status sketchycgal_step(scg_ctx *c, int64_t T) {
           else
             launch(c, KC_LANCZOS_B, s->kb[KC_LANCZOS_B], k_lanczos_b, dim3(s->grid_b), dim3(kBlock),
                    (const double *)s->a, (const double *)slot(s, i), Xim1, slot(s, i + 1), (int)s->nl, (long long)s->rb,
-                   i, s->slots + SLOT_RHO, s->sc, net_of(c, s, E));
+                   i, s->slots + SLOT_RHO, s->sc, net_of(c, s, E), inl ? Eom : 0ull);
         }
-        pull_all(c, FK_RHO, 1, E, f);
+        if (inl) Erho = E;
+        else pull_all(c, FK_RHO, 1, E, f);
       }
+    }
     }
     // ---- tridiagonal eigenpair (lines 11-12), replicated on every rank
     for (Shard *s : c->sh) launch(c, KC_TRIDIAG, 0.0, k_tridiag, dim3(1), dim3(32), s->sc, (int)q);

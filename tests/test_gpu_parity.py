@@ -658,3 +658,26 @@ def test_ball_constraint_sets_bitwise(gpu, graph, delta, shards, norm):
     setter = h.lib.sketchycgal_set_ball if norm == "l2" else h.lib.sketchycgal_set_ball_l1
     assert setter(h._h, -1.0) != 0
     assert setter(h._h, float("nan")) != 0
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_sharded_inline_pulls_bitwise(gpu, P):
+    """SCG_INLINE_PULL: each Lanczos step's omega / rho collective pulled in the prologue of the kernel
+    that consumes it (no k_pull launches inside pass 1) -- the oracle's bits (c0, 200 iterations), and
+    the Lanczos breakdown of K_8 (k = 2 < q) sharded the same way."""
+    L = si.laplacian("c0")
+    T = 200
+    g = gpu.SketchyCGAL(L, R=10, seed=0, shards=P, inline_pull=True)
+    g.step(T)
+    o = oracle.Oracle(L, 10, seed=0, logcap=T)
+    o.step(T)
+    _assert_trajectory(g, o, T)
+    n = 8
+    i, j = np.triu_indices(n, 1)
+    K8 = si.laplacian_from_edges(n, i, j, np.ones(len(i)))
+    g8 = gpu.SketchyCGAL(K8, R=3, seed=2, shards=min(P, 4), inline_pull=True)
+    g8.step(25)
+    o8 = oracle.Oracle(K8, 3, seed=2, logcap=25)
+    o8.step(25)
+    assert o8.log[0, 2] == 2
+    _assert_trajectory(g8, o8, 25)

@@ -20,6 +20,7 @@ import paper_1912_02949_b200 as scg
 import scg_inputs as si
 
 NVLINK_US = 3.0  # assumed flag round trip per collective (publish + acquire over NVSwitch)
+INLINE = os.environ.get("INLINE", "0") == "1"  # SCG_INLINE_PULL
 cfg = os.environ.get("CFG", "c3")
 L = si.laplacian(cfg)
 c = si.CONFIGS[cfg]
@@ -30,7 +31,7 @@ for P in [int(a) for a in sys.argv[1:]] or [1, 2, 4]:
     # the P shards run in turn on one stream, so device time / P is one rank's device time
     st0 = torch.cuda.Stream()
     s = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], profile=False, shards=P, side_rng=False,
-                        stream=ctypes.c_void_p(st0.cuda_stream))
+                        stream=ctypes.c_void_p(st0.cuda_stream), inline_pull=INLINE)
     s.step(W)
     s.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -44,7 +45,7 @@ for P in [int(a) for a in sys.argv[1:]] or [1, 2, 4]:
     # (b) per-kernel events for the breakdown (the events add a fixed cost to every launch)
     # the start vector drawn inside k_dual_sketch at every P (the side-stream draw of one GPU overlaps
     # other kernels, which a sum of per-kernel times cannot represent)
-    s = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], profile=True, shards=P, side_rng=False)
+    s = scg.SketchyCGAL(L, R=c["R"], seed=c["seed"], profile=True, shards=P, side_rng=False, inline_pull=INLINE)
     s.step(W)
     s.synchronize()
     s.reset_stats()
@@ -57,6 +58,9 @@ for P in [int(a) for a in sys.argv[1:]] or [1, 2, 4]:
     for name, k in st.items():
         per_gpu_ms += k["total_ms"] / (P if name != "pull_collective" else P)
     pulls = st.get("pull_collective", {"launches": 0})["launches"] / max(P, 1)
+    if INLINE and P > 1:  # collectives pulled inside the Lanczos kernels still cross NVLink once each
+        pulls += (st.get("lanczos_a_spmv_dot", {"launches": 0})["launches"]
+                  + st.get("lanczos_b_axpy_norm", {"launches": 0})["launches"]) / max(P, 1)
     proj_ms = per_gpu_ms + pulls * NVLINK_US / 1e3
     res[P] = {"emulated_wall_s": round(wall, 3), "per_gpu_device_ms": round(per_gpu_ms, 2),
               "stream_device_ms_per_rank": round(dev_ms / P, 2),
@@ -72,6 +76,7 @@ for P, r in res.items():
     r["projected_strong_efficiency"] = round(r["projected_it_per_s"] / (base * P), 3)
     r["projected_stream_efficiency"] = round(bstream / (P * r["projected_stream_ms"]), 3)
 print(json.dumps({"config": cfg, "window": [W + 1, W + K], "nvlink_us_per_collective_assumed": NVLINK_US,
+                  "inline_pull": INLINE,
                   "model": "per-GPU device time of the emulated shards + assumed NVLink flag latency per collective; "
                            "projected_stream_*: the emulated stream's device time (no per-kernel events) / P, "
                            "projected_*: the sum of per-kernel event times / P",
