@@ -2705,13 +2705,13 @@ struct EpiY {
   __device__ __forceinline__ void operator()(const RowOut<1> &o) { y[o.r] = o.s[0]; }
 };
 
-template <bool UNI>
+template <bool UNI, int W>  // W > 0: ELL-W layout, 0: SELL + long rows (the engines of k_lanczos_a)
 __global__ void __launch_bounds__(kBlock) k_apply_d(Csr C, Rows RL, const double *__restrict__ d,
                                                     const double *__restrict__ X, int nl, long long rb,
                                                     double *__restrict__ y) {
   pdl_entry();
   EpiY epi{y};
-  spmv_rows<1, UNI>(C, RL, X, 1.0, d, nullptr, rb, nl, epi);
+  spmv_any<1, UNI, W>(C, RL, X, 1.0, d, nullptr, rb, nl, epi);
 }
 
 // out[orig[r]] = in[r]: device rows back to input order (outputs).

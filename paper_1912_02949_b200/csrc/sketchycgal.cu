@@ -819,9 +819,27 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
   auto valof = [&](int64_t e) { return scale ? h_w[(size_t)e] / c->nrmL : h_w[(size_t)e]; };
   double matbytes = 0.0;
   {
+    // ELL-W (DESIGN.md section 5): every row has <= kEllMax entries (no long rows) and the padding
+    // to the widest row stays below 2x the entries -- configs[1], [3] and [4]; SCG_NO_ELL opts out.
+    // The SELL layout is built only when a kernel needs it (no ELL, the fused / warp-specialized
+    // pass-1 options, which run the SELL engine, or a graph small enough for the resident kernel).
+    int maxlen = 0;
+#pragma omp parallel for schedule(static, 4096) reduction(max : maxlen)
+    for (int64_t r = 0; r < nl; ++r) maxlen = std::max(maxlen, h_rp[(size_t)r + 1] - h_rp[(size_t)r]);
+    int W = 0;
+    for (int w : kEllWidths)
+      if (W == 0 && w >= maxlen) W = w;
+    const bool ell_ok = !(c->flags & SCG_NO_ELL) && s->nlong == 0 && s->nheavy == 0 && W > 0 &&
+                        (double)W * (double)nl <= 2.0 * (double)cnt_off + 64.0;
+    // (small graphs keep it too: the resident cluster kernel has ELL engines for widths 3 and 4 only)
+    const bool need_sell = !ell_ok || (c->flags & (SCG_FUSED_PASS1 | SCG_WS_SPMV)) || c->n <= kResMaxN;
+    const int padc = (int)c->n;
+    s->padc = padc;
     // rows are already sorted by length within windows of kSortWin rows (relabel_perm), so a
     // slice is 32 consecutive rows; leading long rows (warp engine) are skipped lanes
     const int64_t nsl = (nl + 31) / 32;
+    s->nslice = (int)nsl;
+    if (need_sell) {
     hvec<int> scol;  // every slot is written by the fill pass (padding included)
     std::vector<int2> meta;
     hvec<double> sval;
@@ -855,7 +873,6 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
     // whose gathered value is -0 in every gathered vector (set_pad_zero), with a positive
     // coefficient (+m0, or the value +0): the product is -0 and fma(., ., acc) == acc exactly for
     // every acc (also +-0), so the kernels need no per-slot padding test.
-    const int padc = (int)c->n;
     scol.resize(slots);
     if (!uni) sval.resize(slots);
     // pass 2 (parallel): fill every slot, padding included
@@ -888,17 +905,9 @@ scg_status build_layout(scg_ctx *c, Shard *s) {
       CK(cudaMemcpyAsync(s->sell_val, sval.data(), sizeof(double) * sval.size(), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
     s->sell_slots = (double)scol.size();
-    s->padc = padc;
-    // ELL-W (DESIGN.md section 5): every row has <= kEllMax entries (no long rows) and the padding
-    // to the widest row stays below 2x the entries -- configs[1], [3] and [4]; SCG_NO_ELL opts out
-    int maxlen = 0;
-#pragma omp parallel for schedule(static, 4096) reduction(max : maxlen)
-    for (int64_t r = 0; r < nl; ++r) maxlen = std::max(maxlen, h_rp[(size_t)r + 1] - h_rp[(size_t)r]);
-    int W = 0;
-    for (int w : kEllWidths)
-      if (W == 0 && w >= maxlen) W = w;
+    }  // need_sell
     const int64_t nsl32 = (nl + 31) / 32;
-    if (!(c->flags & SCG_NO_ELL) && s->nlong == 0 && s->nheavy == 0 && W > 0 && (double)W * (double)nl <= 2.0 * (double)cnt_off + 64.0) {
+    if (ell_ok) {
       const size_t ne = (size_t)nsl32 * 32 * W;
       hvec<int> ecol(ne);
       hvec<double> eval;
@@ -1948,7 +1957,8 @@ scg_status sketchycgal_apply_D(scg_ctx *c, const double *xh, double *yh) {
     CK(cudaMalloc(&dy, sizeof(double) * std::max<int64_t>(1, s->nl)));
     Csr C{s->rp, s->col, s->val};
     Rows TT = rows_of(s);
-    launch_smem(c, KC_OTHER, 0.0, s->sell_uniform ? k_apply_d<true> : k_apply_d<false>, dim3(s->grid_spmv), dim3(kBlock), 0,
+    launch_smem(c, KC_OTHER, 0.0, SCG_PICK(k_apply_d, s->sell_uniform, s->ellw),
+                dim3(s->ellw ? s->grid_ell : s->grid_spmv), dim3(kBlock), 0,
            C, TT, (const double *)s->d, (const double *)dx, (int)s->nl, (long long)s->rb, dy);
     CK(cudaStreamSynchronize(c->stream));
     if ((st = fetch_rows(c, s, dy, yh, off))) return st;
