@@ -849,32 +849,37 @@ __global__ void k_pr_combine(const double2 *__restrict__ U, double2 *__restrict_
 }
 
 // v <- v / ||v||; vv = ||v||^2, c = v^* C~ v, g = v^* Omega (R complex).
+template <int RC>  // the sketch rank as a compile-time constant: 1 + 2 RC sums, no dead accumulators
 __global__ void k_pr_vnorm(double2 *__restrict__ v, const double2 *__restrict__ Om, int64_t n, int R, double rsn,
                            PrScal *sc, double *partials) {
-  __shared__ double red[32 * (1 + 2 * kRMax)];
+  constexpr int NV = 1 + 2 * RC;
+  __shared__ double red[32 * NV];
   const double inv = 1.0 / sc->vnrm;
-  double s[1 + 2 * kRMax];
+  double s[NV];
 #pragma unroll
-  for (int i = 0; i < 1 + 2 * kRMax; ++i) s[i] = 0.0;
+  for (int i = 0; i < NV; ++i) s[i] = 0.0;
   for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n; m += (int64_t)gridDim.x * blockDim.x) {
     const double2 x = cscale(v[m], inv);
     v[m] = x;
     s[0] += x.x * x.x + x.y * x.y;
 #pragma unroll
-    for (int kk = 0; kk < kRMax; ++kk) {
-      if (kk < R) {
-        const double2 o = __ldg(Om + (size_t)kk * n + m);
-        s[1 + 2 * kk] += x.x * o.x + x.y * o.y;  // conj(x) o
-        s[2 + 2 * kk] += x.x * o.y - x.y * o.x;
-      }
+    for (int kk = 0; kk < RC; ++kk) {
+      const double2 o = __ldg(Om + (size_t)kk * n + m);
+      s[1 + 2 * kk] += x.x * o.x + x.y * o.y;  // conj(x) o
+      s[2 + 2 * kk] += x.x * o.y - x.y * o.x;
     }
   }
-  if (grid_sum<1 + 2 * kRMax>(s, partials, &sc->ticket[4], red) && threadIdx.x == 0) {
+  if (grid_sum<NV>(s, partials, &sc->ticket[4], red) && threadIdx.x == 0) {
     sc->vv = s[0];
     sc->cval = s[0] * rsn;
-    for (int i = 0; i < 2 * kRMax; ++i) sc->g[i] = s[1 + i];
+    for (int i = 0; i < 2 * RC; ++i) sc->g[i] = s[1 + i];
   }
 }
+typedef void (*VnFn)(double2 *, const double2 *, int64_t, int, double, PrScal *, double *);
+const VnFn kVnorm[kRMax] = {k_pr_vnorm<1>,  k_pr_vnorm<2>,  k_pr_vnorm<3>,  k_pr_vnorm<4>,
+                            k_pr_vnorm<5>,  k_pr_vnorm<6>,  k_pr_vnorm<7>,  k_pr_vnorm<8>,
+                            k_pr_vnorm<9>,  k_pr_vnorm<10>, k_pr_vnorm<11>, k_pr_vnorm<12>,
+                            k_pr_vnorm<13>, k_pr_vnorm<14>, k_pr_vnorm<15>, k_pr_vnorm<16>};
 
 __device__ __forceinline__ double dual_gamma(int64_t t, double beta0, double nz) {
   if (nz == 0.0) return beta0;
@@ -1595,7 +1600,7 @@ int scg_pr_step(scg_pr_ctx *c, int64_t T) {
     k_pr_combine<<<gb, 256, 0, c->st>>>(c->U, c->v, n, c->sc, c->partials);
     prof_end(c);
     prof_begin(c, KS_VNORM);
-    k_pr_vnorm<<<gb, 256, 0, c->st>>>(c->v, c->Om, n, c->R, c->rsn, c->sc, c->partials);
+    kVnorm[c->R - 1]<<<gb, 256, 0, c->st>>>(c->v, c->Om, n, c->R, c->rsn, c->sc, c->partials);
     prof_end(c);
     rc = launch_matvec(c, c->v, nullptr, c->a, 0, 1);
     if (rc) return rc;
