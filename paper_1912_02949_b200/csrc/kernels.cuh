@@ -186,7 +186,9 @@ __device__ __forceinline__ double div_rn(double a, double b, double rb) {
 constexpr int kMinBlocksUni = 3;  // min blocks per SM of the uniform-weight SELL SpMV kernels (80-register cap)
 // min blocks per SM of the ELL SpMV kernels: 64-register cap up to W = 4, wider rows need more stage registers
 // (a deeper pipeline -- gathers two slices ahead, 78 registers, 3 blocks/SM -- measured 171 us against
-// 140 us on configs[3]: the fourth block per SM is worth more than the extra slack)
+// 140 us on configs[3]: the fourth block per SM is worth more than the extra slack; on configs[4]'s
+// valued ELL-3, 80 registers, 911 us either way: that launch moves 5.07 GB of DRAM reads for 2.01 GB
+// algorithmic, so it is bound by the random gathers' DRAM traffic, not by latency -- gpurun_out/ed)
 constexpr int ell_min_blocks(int W, bool uni) { return (W & 15) <= 4 ? 4 : (uni ? 3 : 2); }
 // ELL width code: W & 15 = slots per row; kEllPos set = every coefficient is +m0 (uniform positive
 // weights -- C~ = -L / ||L|| has the positive off-diagonals w / ||L|| -- padding included): the layout
