@@ -312,7 +312,11 @@ int64_t sketchycgal_iterations(const scg_ctx *c);
 /* Kernel launches issued since init / the last reset (counts only this library's kernels). */
 int64_t sketchycgal_launch_count(const scg_ctx *c);
 
-/* Kernel statistics (needs SCG_PROFILE): fills up to max entries, returns the count (<0 on error). */
+/* Kernel statistics (needs SCG_PROFILE): fills up to max entries, returns the count (<0 on error).
+ * One entry per kernel class, plus "lanczos_pass1_in_flow" (one GPU, multi-kernel path): every 8th
+ * iteration's whole Lanczos pass 1 (Alg. 2 lines 1-9) between ONE pair of events
+ * with none between its launches; launches = passes timed, total_ms their summed time,
+ * bytes_per_launch the mean algorithmic bytes of such a pass. */
 int32_t sketchycgal_kernel_stats(scg_ctx *c, scg_kstat *out, int32_t max);
 void sketchycgal_reset_stats(scg_ctx *c);
 

@@ -481,8 +481,8 @@ class SketchyCGAL:
         return chi, w.value
 
     def kernel_stats(self):
-        buf = (KStat * 16)()
-        n = self.lib.sketchycgal_kernel_stats(self._h, buf, 16)
+        buf = (KStat * 24)()
+        n = self.lib.sketchycgal_kernel_stats(self._h, buf, 24)
         return [dict(name=buf[i].name.decode(), launches=buf[i].launches, total_ms=buf[i].total_ms,
                      bytes_per_launch=buf[i].bytes_per_launch) for i in range(max(n, 0))]
 

@@ -555,6 +555,13 @@ def test_bench_launch_configuration_bitwise(gpu, resident, serial):
         stats = {s["name"]: s for s in g.kernel_stats()}
     main = "resident_iteration" if resident else "lanczos_a_spmv_dot"
     assert stats[main]["launches"] > 0 and stats[main]["total_ms"] > 0
+    flow = stats["lanczos_pass1_in_flow"]  # whole passes 1 between one pair of events (every 8th iteration)
+    if resident:
+        assert flow["launches"] == 0
+    else:  # t = 8, 16, ..., 200; a pass moves q k_lanczos_a + (q - 1) k_lanczos_b launches' bytes
+        assert flow["launches"] == 25 and flow["total_ms"] > 0
+        pair = stats["lanczos_a_spmv_dot"]["bytes_per_launch"] + stats["lanczos_b_axpy_norm"]["bytes_per_launch"]
+        assert flow["bytes_per_launch"] > 10 * pair
     o = oracle.Oracle(L, 10, seed=1, logcap=200)
     o.step(200)
     _assert_trajectory(g, o, 200)
